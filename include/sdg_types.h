@@ -1,0 +1,102 @@
+/*
+ * sdg_types.h — plain-C problem description shared by the B200 C-ABI
+ * (include/sdg_gpu.h) and the CPU oracle (oracle/sdg3d.h).
+ *
+ * This is the 3D generalisation of the reference's setup types:
+ *   - BandSpec / MeshSpec           /root/reference/proj/src/mesh.hpp:12-26
+ *   - GasModel                      /root/reference/proj/src/state.hpp:29-44
+ *   - CaseDef (+ exact solutions)   /root/reference/proj/src/cases.hpp:11-28,
+ *                                   /root/reference/proj/src/exact_solutions.hpp:9-42
+ *   - NodeKind                      /root/reference/proj/src/nodal_basis.hpp:11
+ *   - error classes                 /root/reference/proj/src/errors.hpp:9-21
+ *
+ * Geometry convention (the reference's 2D axes, extended by z):
+ *   bands (sliding blocks) are stacked along x, the sliding interfaces are
+ *   x-normal planes, a moving band translates rigidly along +y (the
+ *   interface-parallel index i_par = iy), z is the second tangential axis
+ *   (i_perp = iz).  BASELINE.json's configs are mapped by relabelling:
+ *   BASELINE z (split axis) -> x, BASELINE x (slide axis) -> y,
+ *   BASELINE y -> z.
+ *
+ * State layout (host and device, fp64):
+ *   U[e][i][j][k][v], i along x, j along y, k along z (k fastest),
+ *   v in {rho, rho*v1, rho*v2, rho*v3, rho*E}.
+ */
+#ifndef SDG_TYPES_H
+#define SDG_TYPES_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDG_MAX_BANDS 16
+#define SDG_NVARS 5
+#define SDG_NGRAD 12 /* (v1, v2, v3, T) x (d/dx, d/dy, d/dz): g[3*q + dir] */
+
+/* Status codes of every C entry point (0 = success). The C++ facade maps
+ * 1..3 to the reference's ConfigError / InvalidStateError / ProtocolError. */
+enum {
+  SDG_OK = 0,
+  SDG_ERR_CONFIG = 1,
+  SDG_ERR_INVALID_STATE = 2,
+  SDG_ERR_PROTOCOL = 3,
+  SDG_ERR_CUDA = 4,
+  SDG_ERR_NCCL = 5
+};
+
+enum { SDG_NODES_LGL = 0, SDG_NODES_GAUSS = 1 };
+
+enum {
+  SDG_CASE_FREESTREAM = 0,
+  SDG_CASE_DENSITY_WAVE = 1,
+  SDG_CASE_VORTEX = 2, /* isentropic vortex in the x-y plane, z-invariant */
+  SDG_CASE_TGV = 3     /* Taylor-Green vortex in BASELINE axes (see above) */
+};
+
+/* One band (block) of structured, axis-aligned hexahedra. */
+typedef struct {
+  int nx;            /* elements along x */
+  double width_frac; /* relative width, normalised over all bands */
+  double vg_y;       /* rigid translation speed along +y (0 = static) */
+} sdg_band_spec;
+
+typedef struct {
+  double x0, y0, z0;
+  double width, height, depth; /* extents along x, y, z */
+  int ny, nz;                  /* elements along y and z (all bands) */
+  int n_bands;
+  sdg_band_spec bands[SDG_MAX_BANDS];
+  int periodic_x, periodic_y, periodic_z;
+} sdg_mesh_spec;
+
+typedef struct {
+  double gamma, R, mu, Pr;
+} sdg_gas;
+
+typedef struct {
+  int kind;
+  /* freestream */
+  double fs_rho, fs_v[3], fs_p;
+  /* density wave: rho = 2 + alpha*sin(pi*(k.x - (k.a) t)), v = a, p = p0 */
+  double dw_alpha, dw_a[3], dw_k[3], dw_p0;
+  /* isentropic vortex (x-y plane) */
+  double vx_eps, vx_rc, vx_rho_inf, vx_v_inf, vx_theta, vx_ma_inf, vx_center[2];
+  /* Taylor-Green vortex: reference density, velocity, Mach number */
+  double tgv_rho0, tgv_v0, tgv_mach;
+} sdg_case;
+
+typedef struct {
+  int degree;
+  int node_kind;
+  sdg_gas gas;
+  sdg_case flow_case;
+} sdg_solver_config;
+
+/* One column of the paper's index array A, 7 ints:
+ * partner_rank, i_iface, i_par, i_perp, i_sub, i_face, ctx_tag. */
+#define SDG_TUPLE_INTS 7
+
+#ifdef __cplusplus
+}
+#endif
+#endif

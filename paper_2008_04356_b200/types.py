@@ -1,0 +1,144 @@
+"""ctypes mirrors of include/sdg_types.h plus builders for the problem description.
+
+The builders follow the reference's setup vocabulary (bands, ny/nz, band_vg,
+case kinds) — /root/reference/proj/src/config.cpp:132-212 maps the same keys
+into MeshSpec/CaseDef.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+SDG_MAX_BANDS = 16
+NVARS = 5
+NGRAD = 12
+TUPLE_INTS = 7
+
+OK, ERR_CONFIG, ERR_INVALID_STATE, ERR_PROTOCOL, ERR_CUDA, ERR_NCCL = range(6)
+NODES_LGL, NODES_GAUSS = 0, 1
+CASE_FREESTREAM, CASE_DENSITY_WAVE, CASE_VORTEX, CASE_TGV = range(4)
+
+
+class BandSpec(C.Structure):
+    _fields_ = [("nx", C.c_int), ("width_frac", C.c_double), ("vg_y", C.c_double)]
+
+
+class MeshSpec(C.Structure):
+    _fields_ = [
+        ("x0", C.c_double), ("y0", C.c_double), ("z0", C.c_double),
+        ("width", C.c_double), ("height", C.c_double), ("depth", C.c_double),
+        ("ny", C.c_int), ("nz", C.c_int),
+        ("n_bands", C.c_int),
+        ("bands", BandSpec * SDG_MAX_BANDS),
+        ("periodic_x", C.c_int), ("periodic_y", C.c_int), ("periodic_z", C.c_int),
+    ]
+
+
+class Gas(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("R", C.c_double), ("mu", C.c_double), ("Pr", C.c_double)]
+
+
+class Case(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int),
+        ("fs_rho", C.c_double), ("fs_v", C.c_double * 3), ("fs_p", C.c_double),
+        ("dw_alpha", C.c_double), ("dw_a", C.c_double * 3), ("dw_k", C.c_double * 3), ("dw_p0", C.c_double),
+        ("vx_eps", C.c_double), ("vx_rc", C.c_double), ("vx_rho_inf", C.c_double), ("vx_v_inf", C.c_double),
+        ("vx_theta", C.c_double), ("vx_ma_inf", C.c_double), ("vx_center", C.c_double * 2),
+        ("tgv_rho0", C.c_double), ("tgv_v0", C.c_double), ("tgv_mach", C.c_double),
+    ]
+
+
+class SolverConfig(C.Structure):
+    _fields_ = [("degree", C.c_int), ("node_kind", C.c_int), ("gas", Gas), ("flow_case", Case)]
+
+
+class SdgError(RuntimeError):
+    code = ERR_CONFIG
+
+
+class ConfigError(SdgError):
+    """Mirror of sdg::ConfigError (proj/src/errors.hpp:9-11)."""
+    code = ERR_CONFIG
+
+
+class InvalidStateError(SdgError):
+    """Mirror of sdg::InvalidStateError (proj/src/errors.hpp:14-16)."""
+    code = ERR_INVALID_STATE
+
+
+class ProtocolError(SdgError):
+    """Mirror of sdg::ProtocolError (proj/src/errors.hpp:19-21)."""
+    code = ERR_PROTOCOL
+
+
+class DeviceError(SdgError):
+    code = ERR_CUDA
+
+
+ERRORS = {ERR_CONFIG: ConfigError, ERR_INVALID_STATE: InvalidStateError, ERR_PROTOCOL: ProtocolError,
+          ERR_CUDA: DeviceError, ERR_NCCL: DeviceError}
+
+
+def raise_for(code: int, msg: str) -> None:
+    if code != OK:
+        raise ERRORS.get(code, SdgError)(msg)
+
+
+def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z0=0.0,
+              periodic=(True, True, True)) -> MeshSpec:
+    """bands: list of (nx, width_frac, vg_y) tuples, stacked along x."""
+    if not 1 <= len(bands) <= SDG_MAX_BANDS:
+        raise ConfigError("mesh needs 1..16 bands")
+    m = MeshSpec()
+    m.x0, m.y0, m.z0 = x0, y0, z0
+    m.width, m.height, m.depth = width, height, depth
+    m.ny, m.nz = ny, nz
+    m.n_bands = len(bands)
+    for i, b in enumerate(bands):
+        b = tuple(b)
+        nx, frac, vg = b[0], (b[1] if len(b) > 1 else 1.0), (b[2] if len(b) > 2 else 0.0)
+        m.bands[i].nx, m.bands[i].width_frac, m.bands[i].vg_y = int(nx), float(frac), float(vg)
+    m.periodic_x, m.periodic_y, m.periodic_z = (int(bool(p)) for p in periodic)
+    return m
+
+
+def freestream(rho=1.0, v=(1.0, 0.5, 0.0), p=1.0) -> Case:
+    c = Case()
+    c.kind = CASE_FREESTREAM
+    c.fs_rho, c.fs_p = rho, p
+    for i in range(3):
+        c.fs_v[i] = v[i]
+    return c
+
+
+def density_wave(alpha=0.1, a=(1.0, 1.0, 1.0), k=(1.0, 1.0, 1.0), p0=1.0) -> Case:
+    c = Case()
+    c.kind = CASE_DENSITY_WAVE
+    c.dw_alpha, c.dw_p0 = alpha, p0
+    for i in range(3):
+        c.dw_a[i], c.dw_k[i] = a[i], k[i]
+    return c
+
+
+def vortex(eps=1.0, rc=1.0, rho_inf=1.0, v_inf=1.0, theta=math.atan(0.5), ma_inf=0.3, center=(0.0, 0.0)) -> Case:
+    c = Case()
+    c.kind = CASE_VORTEX
+    c.vx_eps, c.vx_rc, c.vx_rho_inf, c.vx_v_inf, c.vx_theta, c.vx_ma_inf = eps, rc, rho_inf, v_inf, theta, ma_inf
+    c.vx_center[0], c.vx_center[1] = center
+    return c
+
+
+def tgv(rho0=1.0, v0=1.0, mach=0.1) -> Case:
+    c = Case()
+    c.kind = CASE_TGV
+    c.tgv_rho0, c.tgv_v0, c.tgv_mach = rho0, v0, mach
+    return c
+
+
+def solver_config(degree, node_kind=NODES_GAUSS, gamma=1.4, R=1.0, mu=0.0, Pr=0.72, case=None) -> SolverConfig:
+    s = SolverConfig()
+    s.degree, s.node_kind = degree, node_kind
+    s.gas.gamma, s.gas.R, s.gas.mu, s.gas.Pr = gamma, R, mu, Pr
+    s.flow_case = case if case is not None else freestream()
+    return s
