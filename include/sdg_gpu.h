@@ -1,0 +1,124 @@
+/*
+ * sdg_gpu.h — the C-ABI drop-in boundary of the B200 sliding-mesh DGSEM
+ * right-hand side.  Plain pointers and sizes only; every entry point returns
+ * an SDG_* status code (include/sdg_types.h) and leaves a message readable
+ * through sdg_last_error().
+ *
+ * Each entry point replaces one member of the reference's per-rank solver
+ * class `sdg::RankSolver` (/root/reference/proj/src/solver.hpp:64-98) or one
+ * of the setup calls its runner makes (/root/reference/proj/src/runner.cpp:33-55):
+ *
+ *   sdg_create                 Mesh(MeshSpec) mesh.hpp:79 + assign_ranks partition.hpp:26
+ *                              + build_local_domain face_topology.hpp:60 + NodeSet/
+ *                              build_basis_operators nodal_basis.hpp:26,59 +
+ *                              RankSolver::RankSolver solver.hpp:66-67
+ *   sdg_init_rank_maps         RankSolver::init_rank_maps            solver.hpp:70
+ *   sdg_set_initial_condition  RankSolver::set_initial_condition     solver.hpp:72
+ *   sdg_set_state/get_state    RankSolver::field() (mutable span)    solver.hpp:80-81
+ *   sdg_step                   RankSolver::step                      solver.hpp:75
+ *   sdg_compute_residual[_host] RankSolver::compute_residual         solver.hpp:85
+ *   sdg_compute_gradients_host RankSolver::compute_gradients + gradients() solver.hpp:89-90
+ *   sdg_suggest_dt             RankSolver::suggest_dt                solver.hpp:92
+ *   sdg_time                   RankSolver::time / step_index         solver.hpp:77-78
+ *   sdg_ctx_info               RankSolver::side_ctx                  solver.hpp:94
+ *   sdg_total_rebuilds         RankSolver::total_rebuilds            solver.hpp:95
+ *   sdg_get_pairing/mapping    RoleArrays::cols / InterfaceSideCtx::m solver.hpp:17,30 (read back
+ *                              from the device, where the pairing is recomputed every stage)
+ *   sdg_pairing_device         rebuild_index_arrays + build_schedule partition.hpp:100-115
+ *                              (run by the device pairing kernel on caller-given faces)
+ *
+ * The interface-displacement update (RankSolver::update_interfaces,
+ * solver.cpp:156-176) runs inside every stage: the host advances delta_base
+ * exactly as solver.cpp:922-926 and assembles the long-double mortar
+ * operators; the device recomputes displacement and pairing bit-exactly.
+ *
+ * Conventions: host pointers are borrowed for the call only; device buffers
+ * are owned by the context.  All work is enqueued on the context's stream;
+ * sdg_step / sdg_get_state / sdg_synchronize synchronise and report a deferred
+ * InvalidStateError (admissibility is checked on the device after every
+ * stage, solver.cpp:892-906).  Not thread-safe per context; one host thread
+ * per GPU.  Collective-style calls must be entered by all ranks in lock-step.
+ */
+#ifndef SDG_GPU_H
+#define SDG_GPU_H
+
+#include <stddef.h>
+
+#include "sdg_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sdg_ctx sdg_ctx;
+
+#define SDG_NCCL_ID_BYTES 128
+
+/* n_ranks/rank: one process (or host thread) per GPU.  nccl_id: the
+ * ncclUniqueId bytes shared by all ranks (NULL when n_ranks == 1). */
+int sdg_create(const sdg_mesh_spec* mesh, const sdg_solver_config* cfg, int n_ranks, int rank,
+               int device, const void* nccl_id, sdg_ctx** out);
+void sdg_destroy(sdg_ctx* ctx);
+const char* sdg_last_error(const sdg_ctx* ctx);
+const char* sdg_global_error(void);
+/* Fills SDG_NCCL_ID_BYTES bytes (rank 0 calls it and broadcasts). */
+int sdg_nccl_unique_id(void* out);
+
+int sdg_init_rank_maps(sdg_ctx* ctx);
+int sdg_set_initial_condition(sdg_ctx* ctx, double t0);
+
+int sdg_n1(const sdg_ctx* ctx);
+long sdg_n_local_elements(const sdg_ctx* ctx);
+long sdg_n_global_elements(const sdg_ctx* ctx);
+int sdg_local_element_ids(const sdg_ctx* ctx, long* gids);
+
+/* Local field, layout U[e][i][j][k][5] in local element order. */
+int sdg_set_state(sdg_ctx* ctx, const double* host_u);
+int sdg_get_state(sdg_ctx* ctx, double* host_u);
+int sdg_get_register(sdg_ctx* ctx, double* host_reg);
+/* Device pointer of the resident field (valid until sdg_destroy). */
+int sdg_state_device_ptr(sdg_ctx* ctx, double** d_u);
+
+int sdg_step(sdg_ctx* ctx, double dt);
+/* n steps enqueued without host synchronisation, then one synchronise. */
+int sdg_steps(sdg_ctx* ctx, double dt, int n_steps);
+/* Same, but returns without synchronising (timing / overlap). */
+int sdg_steps_async(sdg_ctx* ctx, double dt, int n_steps);
+int sdg_synchronize(sdg_ctx* ctx);
+
+int sdg_compute_residual(sdg_ctx* ctx, double t_stage, const double* d_u, double* d_dudt);
+int sdg_compute_residual_host(sdg_ctx* ctx, double t_stage, const double* h_u, double* h_dudt);
+/* BR1 gradients g[e][node][12], g[3*q + dir], q in (v1, v2, v3, T). */
+int sdg_compute_gradients_host(sdg_ctx* ctx, double t_stage, const double* h_u, double* h_grad);
+
+int sdg_suggest_dt(sdg_ctx* ctx, double cfl, double* dt);
+int sdg_time(const sdg_ctx* ctx, double* t, int* step_index);
+long sdg_total_rebuilds(const sdg_ctx* ctx);
+int sdg_n_contexts(const sdg_ctx* ctx);
+/* out5: iface, on_static, n_delta, conforming, n_faces_local (device-computed
+ * at the last stage); s_delta, sigma_side. */
+int sdg_ctx_info(sdg_ctx* ctx, int ctx_id, long* out5, double* s_delta, double* sigma_side);
+/* Sorted A columns of one role (0 static, 1 moving), SDG_TUPLE_INTS each. */
+int sdg_get_pairing(sdg_ctx* ctx, int role, int* ncols, int* cols);
+int sdg_get_mapping(sdg_ctx* ctx, int ctx_id, int* m);
+
+/* The device pairing kernel on an arbitrary face set (same contract as
+ * rebuild_index_arrays + build_schedule, partition.cpp:143-169). */
+int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,
+                       long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
+                       int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry);
+
+/* Instrumentation: the cudaStream_t the context enqueues on, the number of
+ * kernels this library launched, and per-kernel-class CUDA-event timing of
+ * the next sdg_steps_async call (ms, summed over launches). */
+void* sdg_stream(sdg_ctx* ctx);
+long sdg_kernel_launches(const sdg_ctx* ctx);
+int sdg_enable_kernel_timing(sdg_ctx* ctx, int on);
+/* names: comma-separated kernel classes; ms/launches per class. */
+int sdg_kernel_timing(sdg_ctx* ctx, char* names, int names_cap, double* ms, long* launches, int cap,
+                      int* n_classes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -16,6 +16,7 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <limits>
 #include <map>
 #include <sstream>
@@ -1184,8 +1185,10 @@ void orc_solver::send_gradients() {
 // interior_face_phase (solver.cpp:323-341): minus-side oriented, vg_n from the minus element.
 void orc_solver::interior_flux() {
   const int nif = static_cast<int>(interior.size());
+  // Exceptions may not leave an OpenMP region: keep the first, rethrow after.
+  std::exception_ptr first;
 #pragma omp parallel for schedule(static)
-  for (int fi = 0; fi < nif; ++fi) {
+  for (int fi = 0; fi < nif; ++fi) try {
     const InteriorFace& f = interior[fi];
     const int sm = 2 * f.dir + 1, sp = 2 * f.dir;
     const double* um = tr(f.em, sm);
@@ -1199,7 +1202,11 @@ void orc_solver::interior_flux() {
       face_flux(um + k * NV, up + k * NV, f.dir, vg_n, gm, gp, gas, om + k * NV);
       for (int v = 0; v < NV; ++v) op[k * NV + v] = om[k * NV + v];
     }
+  } catch (...) {
+#pragma omp critical
+    if (!first) first = std::current_exception();
   }
+  if (first) std::rethrow_exception(first);
 }
 
 // volume_kernel (solver.cpp:343-385): one accumulator per (node, var) over m

@@ -1,0 +1,272 @@
+"""ctypes binding of the C-ABI (include/sdg_gpu.h) and a Python mirror of the
+reference's per-rank solver interface (`sdg::RankSolver`,
+/root/reference/proj/src/solver.hpp:64-98), so tests read like the
+reference's own (proj/tests/test_solver.cpp).
+
+There is no CPU fallback: loading fails loudly when the CUDA library is
+missing, and every call goes to the device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import types as T
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsdg_gpu.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_lp = C.POINTER(C.c_long)
+_vp = C.c_void_p
+
+_lib = None
+
+
+def build() -> None:
+    """Compiles csrc/ for sm_100a into libsdg_gpu.so (nvcc cross-compiles without a GPU)."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "csrc")], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        L.sdg_create.argtypes = [C.POINTER(T.MeshSpec), C.POINTER(T.SolverConfig), C.c_int, C.c_int, C.c_int,
+                                 C.c_void_p, C.POINTER(_vp)]
+        L.sdg_destroy.argtypes = [_vp]
+        L.sdg_last_error.argtypes = [_vp]
+        L.sdg_last_error.restype = C.c_char_p
+        L.sdg_global_error.restype = C.c_char_p
+        L.sdg_nccl_unique_id.argtypes = [C.c_void_p]
+        L.sdg_init_rank_maps.argtypes = [_vp]
+        L.sdg_set_initial_condition.argtypes = [_vp, C.c_double]
+        L.sdg_n1.argtypes = [_vp]
+        L.sdg_n_local_elements.argtypes = [_vp]
+        L.sdg_n_local_elements.restype = C.c_long
+        L.sdg_n_global_elements.argtypes = [_vp]
+        L.sdg_n_global_elements.restype = C.c_long
+        L.sdg_local_element_ids.argtypes = [_vp, _lp]
+        L.sdg_set_state.argtypes = [_vp, _dp]
+        L.sdg_get_state.argtypes = [_vp, _dp]
+        L.sdg_get_register.argtypes = [_vp, _dp]
+        L.sdg_state_device_ptr.argtypes = [_vp, C.POINTER(_dp)]
+        L.sdg_step.argtypes = [_vp, C.c_double]
+        L.sdg_steps.argtypes = [_vp, C.c_double, C.c_int]
+        L.sdg_steps_async.argtypes = [_vp, C.c_double, C.c_int]
+        L.sdg_synchronize.argtypes = [_vp]
+        L.sdg_compute_residual.argtypes = [_vp, C.c_double, C.c_void_p, C.c_void_p]
+        L.sdg_compute_residual_host.argtypes = [_vp, C.c_double, _dp, _dp]
+        L.sdg_compute_gradients_host.argtypes = [_vp, C.c_double, _dp, _dp]
+        L.sdg_suggest_dt.argtypes = [_vp, C.c_double, _dp]
+        L.sdg_time.argtypes = [_vp, _dp, _ip]
+        L.sdg_total_rebuilds.argtypes = [_vp]
+        L.sdg_total_rebuilds.restype = C.c_long
+        L.sdg_n_contexts.argtypes = [_vp]
+        L.sdg_ctx_info.argtypes = [_vp, C.c_int, _lp, _dp, _dp]
+        L.sdg_get_pairing.argtypes = [_vp, C.c_int, _ip, _ip]
+        L.sdg_get_mapping.argtypes = [_vp, C.c_int, _ip]
+        L.sdg_pairing_device.argtypes = [C.c_int, _lp, C.c_long, C.c_long, _ip, C.c_long, C.c_int, C.c_int,
+                                         C.c_int, _ip, _ip, _ip, _lp, _ip, _ip, _ip]
+        L.sdg_stream.argtypes = [_vp]
+        L.sdg_stream.restype = C.c_void_p
+        L.sdg_kernel_launches.argtypes = [_vp]
+        L.sdg_kernel_launches.restype = C.c_long
+        L.sdg_enable_kernel_timing.argtypes = [_vp, C.c_int]
+        L.sdg_kernel_timing.argtypes = [_vp, C.c_char_p, C.c_int, _dp, _lp, C.c_int, _ip]
+        _lib = L
+    return _lib
+
+
+EXPORTED = [
+    "sdg_create", "sdg_destroy", "sdg_last_error", "sdg_global_error", "sdg_nccl_unique_id", "sdg_init_rank_maps",
+    "sdg_set_initial_condition", "sdg_n1", "sdg_n_local_elements", "sdg_n_global_elements",
+    "sdg_local_element_ids", "sdg_set_state", "sdg_get_state", "sdg_get_register", "sdg_state_device_ptr",
+    "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
+    "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
+    "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
+    "sdg_pairing_device", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
+]
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    T.raise_for(lib().sdg_nccl_unique_id(buf), lib().sdg_global_error().decode())
+    return buf.raw
+
+
+class RankSolver:
+    """One rank's share of the mesh on one GPU (mirror of sdg::RankSolver)."""
+
+    def __init__(self, mesh: T.MeshSpec, cfg: T.SolverConfig, n_ranks: int = 1, rank: int = 0, device: int = 0,
+                 nccl_id: bytes | None = None, init_rank_maps: bool = True):
+        self.lib = lib()
+        h = _vp()
+        idp = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        code = self.lib.sdg_create(C.byref(mesh), C.byref(cfg), n_ranks, rank, device, idp, C.byref(h))
+        T.raise_for(code, self.lib.sdg_global_error().decode())
+        self.h = h
+        self.n1 = self.lib.sdg_n1(h)
+        self.n_elements = self.lib.sdg_n_local_elements(h)
+        self.size = self.n_elements * self.n1 ** 3 * T.NVARS
+        if init_rank_maps:
+            self.init_rank_maps()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sdg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, code):
+        T.raise_for(code, self.lib.sdg_last_error(self.h).decode())
+
+    # --- reference interface -------------------------------------------------
+    def init_rank_maps(self):
+        self._check(self.lib.sdg_init_rank_maps(self.h))
+
+    def set_initial_condition(self, t0: float = 0.0):
+        self._check(self.lib.sdg_set_initial_condition(self.h, t0))
+
+    def field(self) -> np.ndarray:
+        u = np.empty(self.size)
+        self._check(self.lib.sdg_get_state(self.h, _d(u)))
+        return u
+
+    def register(self) -> np.ndarray:
+        r = np.empty(self.size)
+        self._check(self.lib.sdg_get_register(self.h, _d(r)))
+        return r
+
+    def set_state(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.size != self.size:
+            raise T.ConfigError("state size mismatch")
+        self._check(self.lib.sdg_set_state(self.h, _d(u)))
+
+    def step(self, dt: float, n: int = 1):
+        self._check(self.lib.sdg_steps(self.h, dt, n))
+
+    def steps_async(self, dt: float, n: int):
+        self._check(self.lib.sdg_steps_async(self.h, dt, n))
+
+    def synchronize(self):
+        self._check(self.lib.sdg_synchronize(self.h))
+
+    def compute_residual(self, t_stage: float, u=None) -> np.ndarray:
+        u = self.field() if u is None else np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros(self.size)
+        self._check(self.lib.sdg_compute_residual_host(self.h, t_stage, _d(u), _d(out)))
+        return out
+
+    def compute_residual_device(self, t_stage: float, d_u: int, d_dudt: int):
+        self._check(self.lib.sdg_compute_residual(self.h, t_stage, C.c_void_p(d_u), C.c_void_p(d_dudt)))
+
+    def compute_gradients(self, t_stage: float, u=None) -> np.ndarray:
+        u = self.field() if u is None else np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros(self.n_elements * self.n1 ** 3 * T.NGRAD)
+        self._check(self.lib.sdg_compute_gradients_host(self.h, t_stage, _d(u), _d(out)))
+        return out
+
+    def suggest_dt(self, cfl: float) -> float:
+        dt = C.c_double()
+        self._check(self.lib.sdg_suggest_dt(self.h, cfl, C.byref(dt)))
+        return dt.value
+
+    def time(self) -> float:
+        t = C.c_double()
+        self.lib.sdg_time(self.h, C.byref(t), None)
+        return t.value
+
+    def step_index(self) -> int:
+        s = C.c_int()
+        self.lib.sdg_time(self.h, None, C.byref(s))
+        return s.value
+
+    def total_rebuilds(self) -> int:
+        return self.lib.sdg_total_rebuilds(self.h)
+
+    def n_contexts(self) -> int:
+        return self.lib.sdg_n_contexts(self.h)
+
+    def ctx_info(self, ctx: int) -> dict:
+        o = (C.c_long * 5)()
+        sd, sg = C.c_double(), C.c_double()
+        self._check(self.lib.sdg_ctx_info(self.h, ctx, o, C.byref(sd), C.byref(sg)))
+        return dict(iface=o[0], on_static=bool(o[1]), n_delta=o[2], conforming=bool(o[3]), n_faces=o[4],
+                    s_delta=sd.value, sigma_side=sg.value)
+
+    def pairing(self, role: int) -> np.ndarray:
+        nc = C.c_int()
+        self._check(self.lib.sdg_get_pairing(self.h, role, C.byref(nc), None))
+        cols = np.zeros((max(nc.value, 1), T.TUPLE_INTS), dtype=np.int32)
+        self._check(self.lib.sdg_get_pairing(self.h, role, C.byref(nc), cols.ctypes.data_as(_ip)))
+        return cols[: nc.value]
+
+    def mapping(self, ctx: int) -> np.ndarray:
+        nf = self.ctx_info(ctx)["n_faces"]
+        m = np.zeros((2, nf), dtype=np.int32)
+        self._check(self.lib.sdg_get_mapping(self.h, ctx, m.ctypes.data_as(_ip)))
+        return m
+
+    def local_element_ids(self) -> np.ndarray:
+        g = np.zeros(self.n_elements, dtype=np.int64)
+        self.lib.sdg_local_element_ids(self.h, g.ctypes.data_as(_lp))
+        return g
+
+    # --- instrumentation -------------------------------------------------------
+    def stream(self) -> int:
+        return self.lib.sdg_stream(self.h) or 0
+
+    def state_device_ptr(self) -> int:
+        p = _dp()
+        self.lib.sdg_state_device_ptr(self.h, C.byref(p))
+        return C.cast(p, C.c_void_p).value
+
+    def kernel_launches(self) -> int:
+        return self.lib.sdg_kernel_launches(self.h)
+
+    def enable_kernel_timing(self, on: bool = True):
+        self.lib.sdg_enable_kernel_timing(self.h, int(on))
+
+    def kernel_timing(self) -> dict:
+        names = C.create_string_buffer(512)
+        ms = np.zeros(16)
+        cnt = np.zeros(16, dtype=np.int64)
+        n = C.c_int()
+        self._check(self.lib.sdg_kernel_timing(self.h, names, 512, _d(ms), cnt.ctypes.data_as(_lp), 16, C.byref(n)))
+        keys = names.value.decode().split(",")
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys[: n.value])}
+
+
+def pairing_device(faces, n_par, n_perp, ranks, n_delta, on_static, conforming, self_rank):
+    """Device pairing kernel on a caller-given face set (rebuild_index_arrays contract)."""
+    faces = np.ascontiguousarray(faces, dtype=np.int64).reshape(-1, 3)
+    ranks = np.ascontiguousarray(ranks, dtype=np.int32).reshape(-1)
+    nl = faces.shape[0]
+    cols = np.zeros((2 * nl + 1, T.TUPLE_INTS), dtype=np.int32)
+    w = (faces[:, 0].max() - faces[:, 0].min() + 1) if nl else 1
+    m = np.zeros(2 * w, dtype=np.int32)
+    ncols, nsched = C.c_int(), C.c_int()
+    face_lo = C.c_long()
+    sched = np.zeros(3 * (2 * nl + 1), dtype=np.int32)
+    self_e = np.zeros(3, dtype=np.int32)
+    code = lib().sdg_pairing_device(nl, faces.ctypes.data_as(_lp), n_par, n_perp, ranks.ctypes.data_as(_ip), n_delta,
+                                    int(on_static), int(conforming), self_rank, C.byref(ncols),
+                                    cols.ctypes.data_as(_ip), m.ctypes.data_as(_ip), C.byref(face_lo),
+                                    C.byref(nsched), sched.ctypes.data_as(_ip), self_e.ctypes.data_as(_ip))
+    T.raise_for(code, lib().sdg_global_error().decode())
+    return dict(cols=cols[: ncols.value], m=m.reshape(2, -1), face_lo=face_lo.value,
+                sched=sched[: 3 * nsched.value].reshape(-1, 3), self_entry=self_e)

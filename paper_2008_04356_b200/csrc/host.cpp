@@ -1,0 +1,518 @@
+// Host setup for the B200 path (see host.hpp).
+#include "host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <tuple>
+
+namespace sdg {
+
+// ---------------------------------------------------------------- mesh
+MeshGeom::MeshGeom(const sdg_mesh_spec& s) : spec(s) {
+  if (s.n_bands < 1 || s.n_bands > SDG_MAX_BANDS) throw ConfigError("mesh needs 1..16 bands");
+  if (s.ny < 1 || s.nz < 1) throw ConfigError("mesh needs ny >= 1 and nz >= 1");
+  if (!(s.width > 0.0) || !(s.height > 0.0) || !(s.depth > 0.0))
+    throw ConfigError("mesh extents must be positive");
+  double frac_sum = 0.0;
+  for (int b = 0; b < s.n_bands; ++b) {
+    if (s.bands[b].nx < 1) throw ConfigError("band element count nx must be >= 1");
+    if (!(s.bands[b].width_frac > 0.0)) throw ConfigError("band width fraction must be positive");
+    frac_sum += s.bands[b].width_frac;
+  }
+  const int nb = s.n_bands;
+  double x = s.x0, acc = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    BandGeom g{};
+    g.x_lo = x;
+    acc += s.bands[b].width_frac;
+    g.x_hi = (b == nb - 1) ? s.x0 + s.width : s.x0 + s.width * acc / frac_sum;
+    x = g.x_hi;
+    g.nx = s.bands[b].nx;
+    g.hx = (g.x_hi - g.x_lo) / g.nx;
+    g.hy = s.height / s.ny;
+    g.hz = s.depth / s.nz;
+    g.vg = s.bands[b].vg_y;
+    g.off = n_elements;
+    g.n_elements = static_cast<long>(g.nx) * s.ny * s.nz;
+    n_elements += g.n_elements;
+    if (g.vg < 0.0) throw ConfigError("moving bands must translate toward +y");
+    if (g.vg != 0.0 && !s.periodic_y)
+      throw ConfigError("a moving band requires periodicity along the movement direction");
+    bands.push_back(g);
+  }
+  const int n_pairs = s.periodic_x ? nb : nb - 1;
+  for (int p = 0; p < n_pairs; ++p) {
+    const int l = p, r = (p + 1) % nb;
+    if (nb == 1) continue;
+    if (bands[l].vg == bands[r].vg) continue;
+    if (bands[l].vg != 0.0 && bands[r].vg != 0.0)
+      throw ConfigError("sliding interface requires one static side");
+    IfaceGeom f{};
+    f.left = l;
+    f.right = r;
+    f.static_is_left = bands[l].vg == 0.0;
+    f.l_par = bands[l].hy;
+    f.n_faces = s.ny;
+    f.n_perp = s.nz;
+    f.vg_rel = f.static_is_left ? bands[r].vg : bands[l].vg;
+    ifaces.push_back(f);
+  }
+  if (ifaces.size() * 2 > static_cast<size_t>(kMaxCtx)) throw ConfigError("at most 4 sliding interfaces");
+}
+
+void MeshGeom::locate(long g, int& b, int& ix, int& iy, int& iz) const {
+  b = 0;
+  while (b + 1 < static_cast<int>(bands.size()) && g >= bands[b + 1].off) ++b;
+  long loc = g - bands[b].off;
+  iz = static_cast<int>(loc % spec.nz);
+  loc /= spec.nz;
+  iy = static_cast<int>(loc % spec.ny);
+  ix = static_cast<int>(loc / spec.ny);
+}
+
+// ---------------------------------------------------------------- partition
+int Partition::owner(int band, long local) const {
+  for (const auto& blk : band_blocks[band])
+    if (local >= blk.start && local < blk.start + blk.count) return blk.rank;
+  throw ProtocolError("ownership lookup outside any block");
+}
+
+Partition assign_ranks(const MeshGeom& mesh, int n_ranks) {
+  const int nb = static_cast<int>(mesh.bands.size());
+  if (n_ranks < 1) throw ConfigError("rank count must be positive");
+  Partition p;
+  p.n_ranks = n_ranks;
+  p.band_blocks.resize(nb);
+  if (n_ranks == 1) {
+    for (int b = 0; b < nb; ++b) p.band_blocks[b].push_back({0, 0, mesh.bands[b].n_elements});
+    return p;
+  }
+  if (n_ranks < nb) {
+    if (n_ranks != 2) throw ConfigError("rank count below band count is only supported for 2 ranks");
+    bool st = false, mv = false;
+    for (const auto& b : mesh.bands) (b.vg != 0.0 ? mv : st) = true;
+    if (!st || !mv) throw ConfigError("2 ranks over more bands requires both static and moving bands");
+    for (int b = 0; b < nb; ++b) p.band_blocks[b].push_back({mesh.bands[b].vg != 0.0 ? 1 : 0, 0, mesh.bands[b].n_elements});
+    return p;
+  }
+  const double total = static_cast<double>(mesh.n_elements);
+  std::vector<int> per(nb, 1);
+  int assigned = nb;
+  std::vector<std::pair<double, int>> rem;
+  for (int b = 0; b < nb; ++b) {
+    const double share = static_cast<double>(mesh.bands[b].n_elements) / total * n_ranks;
+    const int extra = std::max(0, static_cast<int>(std::floor(share)) - 1);
+    per[b] += extra;
+    assigned += extra;
+    rem.emplace_back(share - std::floor(share), b);
+  }
+  std::sort(rem.begin(), rem.end(), [](const auto& a, const auto& c) {
+    return a.first != c.first ? a.first > c.first : a.second < c.second;
+  });
+  for (int i = 0; assigned < n_ranks; ++i, ++assigned) per[rem[i % nb].second]++;
+  int next = 0;
+  for (int b = 0; b < nb; ++b) {
+    const long ne = mesh.bands[b].n_elements;
+    const long r = std::min<long>(per[b], ne);
+    long start = 0;
+    for (long k = 0; k < r; ++k) {
+      const long count = ne / r + (k < ne % r ? 1 : 0);
+      p.band_blocks[b].push_back({next++, start, count});
+      start += count;
+    }
+    next += static_cast<int>(std::max<long>(0, per[b] - r));
+  }
+  return p;
+}
+
+// ---------------------------------------------------------------- topology
+namespace {
+struct Nbr {
+  int kind;  // 0 conforming, 1 sliding, 2 dirichlet
+  int band, ix, iy, iz, side, iface;
+};
+
+// Neighbour across `side` (3D form of face_topology.cpp:14-46 + 64-121).
+Nbr neighbour(const MeshGeom& m, int b, int ix, int iy, int iz, int side) {
+  const auto& s = m.spec;
+  const int dir = side / 2;
+  const bool plus = side & 1;
+  const int opp = side ^ 1;
+  if (dir == 1) {
+    if (plus && iy + 1 == s.ny && !s.periodic_y) return {2, 0, 0, 0, 0, 0, -1};
+    if (!plus && iy == 0 && !s.periodic_y) return {2, 0, 0, 0, 0, 0, -1};
+    return {0, b, ix, plus ? (iy + 1) % s.ny : (iy - 1 + s.ny) % s.ny, iz, opp, -1};
+  }
+  if (dir == 2) {
+    if (plus && iz + 1 == s.nz && !s.periodic_z) return {2, 0, 0, 0, 0, 0, -1};
+    if (!plus && iz == 0 && !s.periodic_z) return {2, 0, 0, 0, 0, 0, -1};
+    return {0, b, ix, iy, plus ? (iz + 1) % s.nz : (iz - 1 + s.nz) % s.nz, opp, -1};
+  }
+  const int nb = static_cast<int>(m.bands.size());
+  const int nx = m.bands[b].nx;
+  if (plus && ix + 1 < nx) return {0, b, ix + 1, iy, iz, opp, -1};
+  if (!plus && ix > 0) return {0, b, ix - 1, iy, iz, opp, -1};
+  int other = plus ? b + 1 : b - 1;
+  if (other < 0 || other >= nb) {
+    if (!s.periodic_x) return {2, 0, 0, 0, 0, 0, -1};
+    other = (other + nb) % nb;
+  }
+  if (nb == 1) return {0, b, plus ? 0 : nx - 1, iy, iz, opp, -1};
+  const int left = plus ? b : other, right = plus ? other : b;
+  for (size_t i = 0; i < m.ifaces.size(); ++i)
+    if (m.ifaces[i].left == left && m.ifaces[i].right == right)
+      return {1, other, 0, iy, iz, opp, static_cast<int>(i)};
+  return {0, other, plus ? 0 : m.bands[other].nx - 1, iy, iz, opp, -1};
+}
+}  // namespace
+
+LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int rank) {
+  LocalTopology t;
+  t.rank = rank;
+  const int nb = static_cast<int>(mesh.bands.size());
+  std::map<long, int> local_of;
+  for (int b = 0; b < nb; ++b)
+    for (const auto& blk : part.band_blocks[b]) {
+      if (blk.rank != rank) continue;
+      for (long e = blk.start; e < blk.start + blk.count; ++e) {
+        const long g = mesh.bands[b].off + e;
+        local_of[g] = static_cast<int>(t.gids.size());
+        t.gids.push_back(g);
+      }
+    }
+  const int ne = static_cast<int>(t.gids.size());
+  t.coords.resize(4 * ne);
+  t.side_type.assign(6 * ne, kConforming);
+  t.side_idx.assign(6 * ne, -1);
+  struct Remote {
+    int partner;
+    long key;
+    int slot;
+  };
+  std::vector<Remote> remote;
+  for (int e = 0; e < ne; ++e) {
+    int b, ix, iy, iz;
+    mesh.locate(t.gids[e], b, ix, iy, iz);
+    t.coords[4 * e] = b;
+    t.coords[4 * e + 1] = ix;
+    t.coords[4 * e + 2] = iy;
+    t.coords[4 * e + 3] = iz;
+    for (int s = 0; s < 6; ++s) {
+      const Nbr n = neighbour(mesh, b, ix, iy, iz, s);
+      const int slot = 6 * e + s;
+      if (n.kind == 2) {
+        t.side_type[slot] = kDirichlet;
+        t.side_idx[slot] = static_cast<int>(t.dirichlet.size());
+        t.dirichlet.push_back({e, s});
+      } else if (n.kind == 1) {
+        t.side_type[slot] = kSliding;
+        t.side_idx[slot] = static_cast<int>(t.sliding.size());
+        t.sliding.push_back({n.iface, e, s, iy, iz});
+      } else {
+        const long ng = mesh.gid(n.band, n.ix, n.iy, n.iz);
+        const int owner = part.owner(n.band, ng - mesh.bands[n.band].off);
+        t.side_type[slot] = kConforming;
+        if (owner == rank) {
+          t.side_idx[slot] = 6 * local_of.at(ng) + n.side;
+        } else {
+          // Key of the face: minus element's global id and direction.
+          const long minus = (s & 1) ? t.gids[e] : ng;
+          remote.push_back({owner, minus * 3 + s / 2, slot});
+        }
+      }
+    }
+  }
+  std::sort(remote.begin(), remote.end(), [](const Remote& a, const Remote& c) {
+    return std::tie(a.partner, a.key) < std::tie(c.partner, c.key);
+  });
+  for (const auto& r : remote) {
+    if (t.peers.empty() || t.peers.back().partner != r.partner) t.peers.push_back({r.partner, {}, {}});
+    const int h = t.n_halo++;
+    t.side_idx[r.slot] = 6 * ne + h;
+    t.peers.back().send_slots.push_back(r.slot);
+    t.peers.back().recv_slots.push_back(6 * ne + h);
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------- basis
+namespace {
+void legendre_pd(int n, double x, double& p, double& dp) {
+  if (n == 0) {
+    p = 1.0;
+    dp = 0.0;
+    return;
+  }
+  double p0 = 1.0, p1 = x, d0 = 0.0, d1 = 1.0;
+  for (int k = 1; k < n; ++k) {
+    const double p2 = ((2.0 * k + 1.0) * x * p1 - k * p0) / (k + 1.0);
+    const double d2 = d0 + (2.0 * k + 1.0) * p1;
+    p0 = p1;
+    p1 = p2;
+    d0 = d1;
+    d1 = d2;
+  }
+  p = p1;
+  dp = d1;
+}
+}  // namespace
+
+Basis::Basis(int deg, int knd) : degree(deg), kind(knd), n(deg + 1) {
+  if (deg < 1 || deg > kMaxN1 - 1)
+    throw ConfigError("polynomial degree " + std::to_string(deg) + " outside the device range [1,7]");
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  const double pi = 3.14159265358979323846;
+  for (int j = 0; j <= (n - 1) / 2; ++j) {
+    if (kind == SDG_NODES_LGL) {
+      if (j == 0) {
+        x[0] = -1.0;
+        x[n - 1] = 1.0;
+        continue;
+      }
+      double r = -std::cos(pi * j / deg);
+      for (int it = 0; it < 50; ++it) {
+        double p, dp;
+        legendre_pd(deg, r, p, dp);
+        const double step = dp / ((2.0 * r * dp - deg * (deg + 1.0) * p) / (1.0 - r * r));
+        r -= step;
+        if (std::abs(step) < 1e-15) break;
+      }
+      x[j] = r;
+      x[deg - j] = -r;
+    } else {
+      double r = -std::cos(pi * (2.0 * j + 1.0) / (2.0 * n));
+      for (int it = 0; it < 50; ++it) {
+        double p, dp;
+        legendre_pd(n, r, p, dp);
+        const double step = p / dp;
+        r -= step;
+        if (std::abs(step) < 1e-15) break;
+      }
+      x[j] = r;
+      x[deg - j] = -r;
+    }
+  }
+  if (n % 2 == 1) x[deg / 2] = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double p, dp;
+    if (kind == SDG_NODES_LGL) {
+      legendre_pd(deg, x[j], p, dp);
+      w[j] = 2.0 / (deg * (deg + 1.0) * p * p);
+    } else {
+      legendre_pd(n, x[j], p, dp);
+      w[j] = 2.0 / ((1.0 - x[j] * x[j]) * dp * dp);
+    }
+  }
+  bary.assign(n, 1.0);
+  for (int j = 0; j < n; ++j) {
+    for (int k = 0; k < n; ++k)
+      if (k != j) bary[j] *= x[j] - x[k];
+    bary[j] = 1.0 / bary[j];
+  }
+  D.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double diag = 0.0;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      D[i * n + j] = (bary[j] / bary[i]) / (x[i] - x[j]);
+      diag -= D[i * n + j];
+    }
+    D[i * n + i] = diag;
+  }
+  fl.assign(n, 0.0);
+  fr.assign(n, 0.0);
+  lagrange(-1.0, fl.data());
+  lagrange(1.0, fr.data());
+}
+
+void Basis::lagrange(double xx, double* out) const {
+  for (int k = 0; k < n; ++k)
+    if (xx == x[k]) {
+      for (int j = 0; j < n; ++j) out[j] = j == k ? 1.0 : 0.0;
+      return;
+    }
+  double den = 0.0;
+  for (int k = 0; k < n; ++k) den += (out[k] = bary[k] / (xx - x[k]));
+  for (int k = 0; k < n; ++k) out[k] /= den;
+}
+
+// ---------------------------------------------------------------- mortar operators
+namespace {
+using ld = long double;
+
+struct LdLagrange {
+  std::vector<ld> x, b;
+  explicit LdLagrange(const std::vector<double>& nodes) : x(nodes.begin(), nodes.end()), b(nodes.size(), 1.0L) {
+    const int n = static_cast<int>(x.size());
+    for (int j = 0; j < n; ++j) {
+      for (int k = 0; k < n; ++k)
+        if (k != j) b[j] *= x[j] - x[k];
+      b[j] = 1.0L / b[j];
+    }
+  }
+  void eval(ld xx, ld* out) const {
+    const int n = static_cast<int>(x.size());
+    for (int k = 0; k < n; ++k)
+      if (xx == x[k]) {
+        for (int j = 0; j < n; ++j) out[j] = j == k ? 1.0L : 0.0L;
+        return;
+      }
+    ld den = 0.0L;
+    for (int k = 0; k < n; ++k) den += (out[k] = b[k] / (xx - x[k]));
+    for (int k = 0; k < n; ++k) out[k] /= den;
+  }
+};
+
+// In-place Cholesky of SPD a (n x n), then solve a X = rhs (n x n) column by column.
+void chol_solve(std::vector<ld> a, std::vector<ld>& rhs, int n) {
+  for (int j = 0; j < n; ++j) {
+    ld d = a[j * n + j];
+    for (int k = 0; k < j; ++k) d -= a[j * n + k] * a[j * n + k];
+    if (d <= 0.0L) throw ConfigError("mortar mass matrix not positive definite");
+    a[j * n + j] = std::sqrt(d);
+    for (int i = j + 1; i < n; ++i) {
+      ld s = a[i * n + j];
+      for (int k = 0; k < j; ++k) s -= a[i * n + k] * a[j * n + k];
+      a[i * n + j] = s / a[j * n + j];
+    }
+  }
+  for (int c = 0; c < n; ++c) {
+    for (int i = 0; i < n; ++i) {
+      ld s = rhs[i * n + c];
+      for (int k = 0; k < i; ++k) s -= a[i * n + k] * rhs[k * n + c];
+      rhs[i * n + c] = s / a[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      ld s = rhs[i * n + c];
+      for (int k = i + 1; k < n; ++k) s -= a[k * n + i] * rhs[k * n + c];
+      rhs[i * n + c] = s / a[i * n + i];
+    }
+  }
+}
+}  // namespace
+
+void build_mortar_ops(const Basis& bs, double sigma, double* fwd, double* bwd) {
+  if (!(sigma >= -1.0 && sigma < 1.0)) throw ConfigError("mortar position sigma must lie in [-1, 1)");
+  const int n = bs.n;
+  const Basis gauss(bs.degree, SDG_NODES_GAUSS);
+  const LdLagrange lag(bs.x);
+  std::vector<ld> mass(n * n, 0.0L), la(n), lb(n);
+  for (int q = 0; q < n; ++q) {
+    lag.eval(gauss.x[q], la.data());
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) mass[i * n + j] += static_cast<ld>(gauss.w[q]) * la[i] * la[j];
+  }
+  const ld frac[2] = {0.5L * (1.0L + sigma), 0.5L * (1.0L - sigma)};
+  for (int h = 0; h < 2; ++h) {
+    std::vector<ld> s(n * n, 0.0L);
+    for (int q = 0; q < n; ++q) {
+      const ld z = gauss.x[q];
+      const ld xi = h == 0 ? -1.0L + frac[0] * (z + 1.0L) : static_cast<ld>(sigma) + frac[1] * (z + 1.0L);
+      lag.eval(xi, la.data());
+      lag.eval(z, lb.data());
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) s[i * n + j] += static_cast<ld>(gauss.w[q]) * la[i] * lb[j];
+    }
+    std::vector<ld> f(n * n), bk(n * n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        f[i * n + j] = s[j * n + i];
+        bk[i * n + j] = frac[h] * s[i * n + j];
+      }
+    chol_solve(mass, f, n);
+    chol_solve(mass, bk, n);
+    for (int i = 0; i < n * n; ++i) {
+      fwd[h * n * n + i] = static_cast<double>(f[i]);
+      bwd[h * n * n + i] = static_cast<double>(bk[i]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kinematics
+Displacement displacement(double delta, double l_par, long n_faces) {
+  const double period = l_par * static_cast<double>(n_faces);
+  double d = std::fmod(delta, period);
+  if (d < 0.0) d += period;
+  const double ratio = d / l_par;
+  Displacement st;
+  st.delta = d;
+  st.n_delta = static_cast<long>(std::floor(ratio));
+  st.s_delta = ratio - static_cast<double>(st.n_delta);
+  if (st.n_delta >= n_faces) st = Displacement{};
+  return st;
+}
+
+long moving_index(long i_par, long n_delta, int i_sub, long n_faces) {
+  const long r = (i_par - n_delta + i_sub - 1) % n_faces;
+  return r < 0 ? r + n_faces : r;
+}
+long static_index(long i_moving, long n_delta, int i_sub, long n_faces) {
+  const long r = (i_moving + n_delta - i_sub + 1) % n_faces;
+  return r < 0 ? r + n_faces : r;
+}
+
+}  // namespace sdg
+
+namespace sdg {
+void eval_case_host(const sdg_case& cs, const sdg_gas& g, const double* x, double t, double* u) {
+  const double pi = 3.14159265358979323846;
+  const double gm1 = g.gamma - 1.0;
+  double rho, v0, v1, v2, p;
+  switch (cs.kind) {
+    case SDG_CASE_DENSITY_WAVE: {
+      const double* k = cs.dw_k;
+      const double* a = cs.dw_a;
+      const double ph = pi * (k[0] * x[0] + k[1] * x[1] + k[2] * x[2] - (k[0] * a[0] + k[1] * a[1] + k[2] * a[2]) * t);
+      rho = 2.0 + cs.dw_alpha * std::sin(ph);
+      v0 = a[0];
+      v1 = a[1];
+      v2 = a[2];
+      p = cs.dw_p0;
+      break;
+    }
+    case SDG_CASE_VORTEX: {
+      const double ui = cs.vx_v_inf * std::cos(cs.vx_theta), vi = cs.vx_v_inf * std::sin(cs.vx_theta);
+      const double xb = x[0] - cs.vx_center[0] - ui * t, yb = x[1] - cs.vx_center[1] - vi * t;
+      const double r2 = (xb * xb + yb * yb) / (cs.vx_rc * cs.vx_rc);
+      const double s = cs.vx_eps * std::exp(0.5 * (1.0 - r2));
+      v0 = ui - cs.vx_v_inf * s * yb / cs.vx_rc;
+      v1 = vi + cs.vx_v_inf * s * xb / cs.vx_rc;
+      v2 = 0.0;
+      const double tr =
+          1.0 - 0.5 * gm1 * cs.vx_eps * cs.vx_eps * cs.vx_ma_inf * cs.vx_ma_inf * std::exp(1.0 - r2);
+      rho = cs.vx_rho_inf * std::pow(tr, 1.0 / gm1);
+      const double pinf = cs.vx_rho_inf * cs.vx_v_inf * cs.vx_v_inf / (g.gamma * cs.vx_ma_inf * cs.vx_ma_inf);
+      p = pinf * std::pow(tr, g.gamma / gm1);
+      break;
+    }
+    case SDG_CASE_TGV: {
+      const double X = x[1], Y = x[2], Z = x[0];
+      const double V0 = cs.tgv_v0, r0 = cs.tgv_rho0;
+      rho = r0;
+      v0 = 0.0;
+      v1 = V0 * std::sin(X) * std::cos(Y) * std::cos(Z);
+      v2 = -V0 * std::cos(X) * std::sin(Y) * std::cos(Z);
+      const double p0 = r0 * V0 * V0 / (g.gamma * cs.tgv_mach * cs.tgv_mach);
+      p = p0 + r0 * V0 * V0 / 16.0 * (std::cos(2.0 * X) + std::cos(2.0 * Y)) * (std::cos(2.0 * Z) + 2.0);
+      break;
+    }
+    case SDG_CASE_FREESTREAM:
+      rho = cs.fs_rho;
+      v0 = cs.fs_v[0];
+      v1 = cs.fs_v[1];
+      v2 = cs.fs_v[2];
+      p = cs.fs_p;
+      break;
+    default:
+      throw ConfigError("unknown case kind");
+  }
+  if (!(rho > 0.0) || !(p > 0.0)) throw InvalidStateError("primitive state requires rho > 0 and p > 0");
+  u[0] = rho;
+  u[1] = rho * v0;
+  u[2] = rho * v1;
+  u[3] = rho * v2;
+  u[4] = p / gm1 + 0.5 * rho * (v0 * v0 + v1 * v1 + v2 * v2);
+}
+}  // namespace sdg

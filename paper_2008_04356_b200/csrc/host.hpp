@@ -1,0 +1,140 @@
+// Host-side setup of the B200 path: mesh geometry, rank partition, local face
+// tables in the flat form the kernels consume, nodal basis, long-double mortar
+// operator assembly and the scalar displacement chain.  Everything here is
+// per-run or per-stage scalar work; the per-node work lives in kernels.cu.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sdg_types.h"
+
+namespace sdg {
+
+// Error classes of the boundary (reference: proj/src/errors.hpp:9-21).
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidStateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ProtocolError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {
+  int code;
+  DeviceError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+constexpr int kMaxN1 = 8;       // N <= 7 on the device path
+constexpr int kMaxCtx = 8;      // interface sides per rank (4 interfaces)
+constexpr int kMaxPartners = 32;
+
+enum SideType : int8_t { kConforming = 0, kSliding = 1, kDirichlet = 2 };
+
+struct BandGeom {
+  double x_lo, x_hi, hx, hy, hz, vg;
+  int nx;
+  long off;  // first global element id
+  long n_elements;
+};
+
+struct IfaceGeom {
+  int left, right;
+  bool static_is_left;
+  double l_par;
+  long n_faces, n_perp;
+  double vg_rel;
+  int static_band() const { return static_is_left ? left : right; }
+  int moving_band() const { return static_is_left ? right : left; }
+};
+
+// Structured multi-band hexahedral mesh (3D form of proj/src/mesh.cpp:27-92).
+struct MeshGeom {
+  sdg_mesh_spec spec;
+  std::vector<BandGeom> bands;
+  std::vector<IfaceGeom> ifaces;
+  long n_elements = 0;
+
+  explicit MeshGeom(const sdg_mesh_spec& s);
+  long gid(int b, int ix, int iy, int iz) const {
+    return bands[b].off + (static_cast<long>(ix) * spec.ny + iy) * spec.nz + iz;
+  }
+  void locate(long g, int& b, int& ix, int& iy, int& iz) const;
+};
+
+// Contiguous blocks of each band per rank (proj/src/partition.cpp:17-83):
+// largest-remainder rank counts per band, no rank on both sides of a sliding
+// interface, 2 ranks over >2 bands -> static / moving split.
+struct Partition {
+  int n_ranks = 1;
+  struct Block {
+    int rank;
+    long start, count;  // band-local element range
+  };
+  std::vector<std::vector<Block>> band_blocks;
+  int owner(int band, long local) const;
+};
+Partition assign_ranks(const MeshGeom& mesh, int n_ranks);
+
+struct SlidingFaceRec {
+  int iface;
+  int elem;  // local element
+  int side;  // 0 (x-) or 1 (x+)
+  long i_par, i_perp;
+};
+
+// Flat per-rank topology consumed by the kernels.
+struct LocalTopology {
+  int rank = 0;
+  std::vector<long> gids;            // local element -> global id
+  std::vector<int> coords;           // 4 per element: band, ix, iy, iz
+  std::vector<int8_t> side_type;     // 6 per element
+  std::vector<int> side_idx;         // conforming: neighbour trace slot; sliding: sliding index; dirichlet: index
+  std::vector<std::array<int, 2>> dirichlet;  // (elem, side)
+  std::vector<SlidingFaceRec> sliding;        // compact sliding index -> record
+  int n_halo = 0;                             // halo trace slots after the 6*E local ones
+  struct PeerFaces {
+    int partner;
+    std::vector<int> send_slots;  // local trace slots (e*6+side), in global key order
+    std::vector<int> recv_slots;  // halo slots, same order
+  };
+  std::vector<PeerFaces> peers;   // ascending partner
+};
+LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int rank);
+
+// Nodal basis (proj/src/nodal_basis.cpp:89-182, same published algorithm).
+struct Basis {
+  int degree = 0, kind = SDG_NODES_GAUSS, n = 0;
+  std::vector<double> x, w, bary, D, fl, fr;
+  Basis() = default;
+  Basis(int degree, int kind);
+  void lagrange(double xx, double* out) const;
+};
+
+// Face<->mortar L2 projections for hanging node sigma (proj/src/mortar.cpp:79-134),
+// long double assembly.  fwd/bwd [2][n*n] row-major (Lower, Upper).
+void build_mortar_ops(const Basis& b, double sigma, double* fwd, double* bwd);
+
+struct Displacement {
+  double delta = 0.0;
+  long n_delta = 0;
+  double s_delta = 0.0;
+  bool conforming() const { return s_delta == 0.0; }
+};
+Displacement displacement(double delta, double l_par, long n_faces);  // proj/src/mesh.cpp:9-25
+
+// Pairing restatement on the host, used only to size the per-partner NCCL
+// blocks (the device computes A/m itself): counts of mortars per partner.
+long moving_index(long i_par, long n_delta, int i_sub, long n_faces);
+long static_index(long i_moving, long n_delta, int i_sub, long n_faces);
+
+}  // namespace sdg
+
+namespace sdg {
+// Exact case state at x, t (exact_solutions.cpp:7-35, cases.hpp:18-25), host side.
+void eval_case_host(const sdg_case& cs, const sdg_gas& gas, const double* x, double t, double* u);
+}  // namespace sdg

@@ -1,0 +1,1172 @@
+// sm_100a kernels of the sliding-mesh DGSEM right-hand side (fp64).
+//
+// Dataflow per RK stage (viscous):
+//   k_gradient  (element): U + neighbour traces -> BR1 lift* -> volume gradient ->
+//                          viscous normal flux Fv.n on every conforming side
+//                          (the 12-component gradient trace only on sliding /
+//                          Dirichlet sides, which need it unprojected)
+//   mortar kernels         face -> mortar transfer, two-sided mortar flux,
+//                          L2 back projection (only sliding faces)
+//   k_update    (element): U + neighbour traces + Fv.n -> Roe + viscous face flux,
+//                          recomputed gradient, volume flux + weak divergence,
+//                          surface lift, low-storage RK update, admissibility,
+//                          and the face traces of the NEW state for the next stage.
+// Each conforming face flux is evaluated by both of its elements with the
+// same instruction sequence on the same operands (minus side first), so both
+// sides see identical bits — the orientation rule of solver.cpp:323-341.
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace sdg {
+namespace {
+
+template <int N1>
+struct Dim {
+  static constexpr int N2 = N1 * N1;
+  static constexpr int N3 = N2 * N1;
+  // elements per CTA: keep CTAs at 200-512 threads
+  static constexpr int EPB = N1 == 2 ? 32 : N1 == 3 ? 8 : N1 == 4 ? 4 : N1 <= 6 ? 2 : 1;
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int TAB = ((N1 * N1 + 6 * N1) + 1) & ~1;  // shared operator table (doubles)
+};
+
+__device__ __forceinline__ double sel3(int d, double a, double b, double c) { return d == 0 ? a : (d == 1 ? b : c); }
+
+// ----------------------------------------------------------------------------
+// Canonical quantities that two kernels must reproduce bit-identically are
+// written with explicit rounding intrinsics (no contraction freedom).
+// ----------------------------------------------------------------------------
+
+// Face trace of one variable along the face normal (solver.cpp:208-232).
+template <int N1>
+__device__ __forceinline__ double prolong1(const double* __restrict__ s, const double* __restrict__ ell, int dir,
+                                           int a, int b) {
+  constexpr int N2 = N1 * N1;
+  const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
+  const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[base + m * stride], acc);
+  return acc;
+}
+
+// (v1, v2, v3, T) of a conserved state (state.hpp:47-84).
+__device__ __forceinline__ void prim4(const double* u, const GasD& g, double* q) {
+  const double ir = __drcp_rn(u[0]);
+  q[0] = __dmul_rn(u[1], ir);
+  q[1] = __dmul_rn(u[2], ir);
+  q[2] = __dmul_rn(u[3], ir);
+  const double m2 = __fma_rn(u[3], u[3], __fma_rn(u[2], u[2], __dmul_rn(u[1], u[1])));
+  const double p = __dmul_rn(g.gm1, __fma_rn(-__dmul_rn(0.5, m2), ir, u[4]));
+  q[3] = __dmul_rn(p, __dmul_rn(ir, g.inv_R));
+}
+
+__device__ __forceinline__ double pressure(const double* u, double ir, const GasD& g) {
+  const double m2 = u[1] * u[1] + u[2] * u[2] + u[3] * u[3];
+  return g.gm1 * (u[4] - 0.5 * m2 * ir);
+}
+
+__device__ __forceinline__ double entropy_fix(double lam, double lam_l, double lam_r) {
+  const double delta = fmax(0.0, fmax(lam - lam_l, lam_r - lam));
+  const double a = fabs(lam);
+  return a < 2.0 * delta ? lam * lam / (4.0 * delta) + delta : a;
+}
+
+// Roe flux, Harten-Hyman fix on acoustic waves, eigenvalues shifted by the
+// normal grid speed; axis normal e_dir (flux.cpp:68-133, 3D: second shear wave).
+// Returns false when the Roe-averaged c^2 is not positive.
+__device__ __forceinline__ bool roe_flux(const double* ul, const double* ur, int dir, double vg, const GasD& g,
+                                         double* f) {
+  const double rl = ul[0], rr = ur[0];
+  const double irl = __drcp_rn(rl), irr = __drcp_rn(rr);
+  const double mnl = sel3(dir, ul[1], ul[2], ul[3]), mal = sel3(dir, ul[2], ul[3], ul[1]),
+               mbl = sel3(dir, ul[3], ul[1], ul[2]);
+  const double mnr = sel3(dir, ur[1], ur[2], ur[3]), mar = sel3(dir, ur[2], ur[3], ur[1]),
+               mbr = sel3(dir, ur[3], ur[1], ur[2]);
+  const double unl = mnl * irl, ual = mal * irl, ubl = mbl * irl;
+  const double unr = mnr * irr, uar = mar * irr, ubr = mbr * irr;
+  const double pl = g.gm1 * (ul[4] - 0.5 * (mnl * unl + mal * ual + mbl * ubl));
+  const double pr = g.gm1 * (ur[4] - 0.5 * (mnr * unr + mar * uar + mbr * ubr));
+  const double hl = (ul[4] + pl) * irl, hr = (ur[4] + pr) * irr;
+  const double cl = sqrt(g.gamma * pl * irl), cr = sqrt(g.gamma * pr * irr);
+
+  const double sl = sqrt(rl), sr = sqrt(rr);
+  const double inv = __drcp_rn(sl + sr);
+  const double un = (sl * unl + sr * unr) * inv;
+  const double ua = (sl * ual + sr * uar) * inv;
+  const double ub = (sl * ubl + sr * ubr) * inv;
+  const double h = (sl * hl + sr * hr) * inv;
+  const double q2 = un * un + ua * ua + ub * ub;
+  const double c2 = g.gm1 * (h - 0.5 * q2);
+  if (!(c2 > 0.0)) return false;
+  const double c = sqrt(c2);
+  const double ic2 = __drcp_rn(c2);
+  const double rho = sl * sr;
+
+  const double dp = pr - pl, dun = unr - unl, dua = uar - ual, dub = ubr - ubl, drho = rr - rl;
+  const double a1 = (dp - rho * c * dun) * 0.5 * ic2;
+  const double a2 = drho - dp * ic2;
+  const double a3 = rho * dua;
+  const double a3b = rho * dub;
+  const double a4 = (dp + rho * c * dun) * 0.5 * ic2;
+
+  const double l1 = entropy_fix(un - c - vg, unl - cl - vg, unr - cr - vg);
+  const double l2 = fabs(un - vg);
+  const double l4 = entropy_fix(un + c - vg, unl + cl - vg, unr + cr - vg);
+  const double w1 = l1 * a1, w2 = l2 * a2, w4 = l4 * a4;
+  const double d0 = w1 + w2 + w4;
+  const double dn = w1 * (un - c) + w2 * un + w4 * (un + c);
+  const double da = d0 * ua + l2 * a3;
+  const double db = d0 * ub + l2 * a3b;
+  const double dE = w1 * (h - un * c) + w2 * 0.5 * q2 + l2 * a3 * ua + l2 * a3b * ub + w4 * (h + un * c);
+
+  // Physical normal fluxes minus vg_n U (flux.cpp:44-54).
+  const double f0 = 0.5 * ((rl * unl - vg * rl) + (rr * unr - vg * rr) - d0);
+  const double fn = 0.5 * ((mnl * unl + pl - vg * mnl) + (mnr * unr + pr - vg * mnr) - dn);
+  const double fa = 0.5 * ((mal * unl - vg * mal) + (mar * unr - vg * mar) - da);
+  const double fb = 0.5 * ((mbl * unl - vg * mbl) + (mbr * unr - vg * mbr) - db);
+  const double fE = 0.5 * (((ul[4] + pl) * unl - vg * ul[4]) + ((ur[4] + pr) * unr - vg * ur[4]) - dE);
+  f[0] = f0;
+  f[1] = sel3(dir, fn, fb, fa);
+  f[2] = sel3(dir, fa, fn, fb);
+  f[3] = sel3(dir, fb, fa, fn);
+  f[4] = fE;
+  return true;
+}
+
+// Viscous flux along direction dir, components 1..4 (flux.cpp:23-42).
+__device__ __forceinline__ void fv_dir(const double* u, const double* gr, int dir, const GasD& g, double* o) {
+  const double ir = __drcp_rn(u[0]);
+  const double v0 = u[1] * ir, v1 = u[2] * ir, v2 = u[3] * ir;
+  const double div = gr[0] + gr[4] + gr[8];
+  const double t00 = 2.0 * g.mu * gr[0] + g.lam * div;
+  const double t11 = 2.0 * g.mu * gr[4] + g.lam * div;
+  const double t22 = 2.0 * g.mu * gr[8] + g.lam * div;
+  const double t01 = g.mu * (gr[1] + gr[3]);
+  const double t02 = g.mu * (gr[2] + gr[6]);
+  const double t12 = g.mu * (gr[5] + gr[7]);
+  const double r0 = sel3(dir, t00, t01, t02), r1 = sel3(dir, t01, t11, t12), r2 = sel3(dir, t02, t12, t22);
+  const double dT = sel3(dir, gr[9], gr[10], gr[11]);
+  o[0] = r0;
+  o[1] = r1;
+  o[2] = r2;
+  o[3] = r0 * v0 + r1 * v1 + r2 * v2 + g.kcond * dT;
+}
+
+// face_numerical_flux with both viscous normal fluxes given (solver.cpp:308-321).
+__device__ __forceinline__ bool face_flux_fv(const double* um, const double* up, int dir, double vg,
+                                             const double* fvm, const double* fvp, const GasD& g, double* f) {
+  const bool ok = roe_flux(um, up, dir, vg, g, f);
+  if (fvm != nullptr) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) f[1 + v] -= 0.5 * (fvm[v] + fvp[v]);
+  }
+  return ok;
+}
+
+// Exact solutions (exact_solutions.cpp:7-35; TGV in BASELINE axes).
+__device__ void eval_case(const sdg_case& cs, const double* x, double t, const GasD& g, double* u) {
+  const double pi = 3.14159265358979323846;
+  double rho, v0, v1, v2, p;
+  switch (cs.kind) {
+    case SDG_CASE_DENSITY_WAVE: {
+      const double* k = cs.dw_k;
+      const double* a = cs.dw_a;
+      const double ph = pi * (k[0] * x[0] + k[1] * x[1] + k[2] * x[2] - (k[0] * a[0] + k[1] * a[1] + k[2] * a[2]) * t);
+      rho = 2.0 + cs.dw_alpha * sin(ph);
+      v0 = a[0];
+      v1 = a[1];
+      v2 = a[2];
+      p = cs.dw_p0;
+      break;
+    }
+    case SDG_CASE_VORTEX: {
+      const double ui = cs.vx_v_inf * cos(cs.vx_theta), vi = cs.vx_v_inf * sin(cs.vx_theta);
+      const double xb = x[0] - cs.vx_center[0] - ui * t, yb = x[1] - cs.vx_center[1] - vi * t;
+      const double r2 = (xb * xb + yb * yb) / (cs.vx_rc * cs.vx_rc);
+      const double s = cs.vx_eps * exp(0.5 * (1.0 - r2));
+      v0 = ui - cs.vx_v_inf * s * yb / cs.vx_rc;
+      v1 = vi + cs.vx_v_inf * s * xb / cs.vx_rc;
+      v2 = 0.0;
+      const double tr = 1.0 - 0.5 * g.gm1 * cs.vx_eps * cs.vx_eps * cs.vx_ma_inf * cs.vx_ma_inf * exp(1.0 - r2);
+      rho = cs.vx_rho_inf * pow(tr, 1.0 / g.gm1);
+      const double pinf = cs.vx_rho_inf * cs.vx_v_inf * cs.vx_v_inf / (g.gamma * cs.vx_ma_inf * cs.vx_ma_inf);
+      p = pinf * pow(tr, g.gamma / g.gm1);
+      break;
+    }
+    case SDG_CASE_TGV: {
+      const double X = x[1], Y = x[2], Z = x[0];
+      const double V0 = cs.tgv_v0, r0 = cs.tgv_rho0;
+      rho = r0;
+      v0 = 0.0;
+      v1 = V0 * sin(X) * cos(Y) * cos(Z);
+      v2 = -V0 * cos(X) * sin(Y) * cos(Z);
+      const double p0 = r0 * V0 * V0 / (g.gamma * cs.tgv_mach * cs.tgv_mach);
+      p = p0 + r0 * V0 * V0 / 16.0 * (cos(2.0 * X) + cos(2.0 * Y)) * (cos(2.0 * Z) + 2.0);
+      break;
+    }
+    default:
+      rho = cs.fs_rho;
+      v0 = cs.fs_v[0];
+      v1 = cs.fs_v[1];
+      v2 = cs.fs_v[2];
+      p = cs.fs_p;
+  }
+  u[0] = rho;
+  u[1] = rho * v0;
+  u[2] = rho * v1;
+  u[3] = rho * v2;
+  u[4] = p / g.gm1 + 0.5 * rho * (v0 * v0 + v1 * v1 + v2 * v2);
+}
+
+// Physical position of face node (a, b) of `side` at time t (mesh.cpp:118-122).
+template <int N1>
+__device__ __forceinline__ void face_position(const ElemConsts& C, const int* crd, int side, int a, int b, double t,
+                                              double* x) {
+  const BandD& B = C.bands[crd[0]];
+  const int dir = side >> 1;
+  const double pm = (side & 1) ? 1.0 : -1.0;
+  const double xi = dir == 0 ? pm : C.x[a];
+  const double eta = dir == 1 ? pm : (dir == 0 ? C.x[a] : C.x[b]);
+  const double zeta = dir == 2 ? pm : C.x[b];
+  x[0] = (B.x_lo + crd[1] * B.hx) + 0.5 * (xi + 1.0) * B.hx;
+  x[1] = (C.y0 + crd[2] * B.hy) + 0.5 * (eta + 1.0) * B.hy + B.vg * t;
+  x[2] = (C.z0 + crd[3] * B.hz) + 0.5 * (zeta + 1.0) * B.hz;
+}
+
+template <int N1>
+__device__ __forceinline__ void load_tables(const ElemConsts& C, double* tab) {
+  // tab: dhat[N1*N1] | fl | fr | liftw0 | liftw1 | inv_w | (unused)
+  for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) tab[q] = C.dhat[(q / N1) * kMaxN1 + q % N1];
+  for (int q = threadIdx.x; q < N1; q += blockDim.x) {
+    tab[N1 * N1 + q] = C.fl[q];
+    tab[N1 * N1 + N1 + q] = C.fr[q];
+    tab[N1 * N1 + 2 * N1 + q] = C.liftw[0][q];
+    tab[N1 * N1 + 3 * N1 + q] = C.liftw[1][q];
+    tab[N1 * N1 + 4 * N1 + q] = C.inv_w[q];
+  }
+}
+
+// Flat, coalesced load of EPB consecutive elements into SoA shared memory su[v][node].
+template <int N1>
+__device__ __forceinline__ void load_state(const double* __restrict__ U, int e0, int E, double* smem_elems,
+                                           int per_elem) {
+  constexpr int N3 = Dim<N1>::N3, EPB = Dim<N1>::EPB;
+  const int n_el = min(EPB, E - e0);
+  const double* src = U + static_cast<size_t>(e0) * 5 * N3;
+  for (int f = threadIdx.x; f < n_el * 5 * N3; f += blockDim.x) {
+    const int le = f / (5 * N3), r = f - le * 5 * N3;
+    smem_elems[le * per_elem + (r % 5) * N3 + r / 5] = __ldg(src + f);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Face traces of U (first stage of a step / residual entry).
+// ----------------------------------------------------------------------------
+template <int N1>
+__global__ void __launch_bounds__(Dim<N1>::THREADS) k_prolong(const __grid_constant__ ElemConsts C, FieldPtrs P) {
+  constexpr int N2 = Dim<N1>::N2, N3 = Dim<N1>::N3, EPB = Dim<N1>::EPB, TAB = Dim<N1>::TAB;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  double* elems = smem + TAB;
+  constexpr int PER = 5 * N3;
+  load_tables<N1>(C, tab);
+  const int e0 = blockIdx.x * EPB;
+  load_state<N1>(P.U, e0, P.E, elems, PER);
+  __syncthreads();
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  if (e >= P.E) return;
+  const double* su = elems + le * PER;
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double* dst = P.trace + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Shared face phase: BR1 surface values lift*[s][c][f] on all six sides
+// (run_lifting, solver.cpp:606-723), and optionally the own traces.
+// ----------------------------------------------------------------------------
+template <int N1>
+__device__ __forceinline__ void face_lift_phase(const ElemConsts& C, const FieldPtrs& P, const double* tab,
+                                                const double* su, int e, double t_stage, double* sLift,
+                                                double* sTr) {
+  constexpr int N2 = Dim<N1>::N2, N3 = Dim<N1>::N3;
+  const int t = threadIdx.x % N3;
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double own[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+    if (sTr != nullptr) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sTr[(s * N2 + f) * 5 + v] = own[v];
+    }
+    const int slot = e * 6 + s;
+    const int typ = P.side_type[slot], idx = P.side_idx[slot];
+    double lift[4];
+    if (typ == kConforming) {
+      const double* nb = P.trace + static_cast<size_t>(idx) * N2 * 5 + f * 5;
+      double other[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) other[v] = nb[v];
+      double qa[4], qb[4];
+      prim4(own, C.gas, qa);
+      prim4(other, C.gas, qb);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+    } else if (typ == kSliding) {
+      const double* sl = P.slide_lift + (static_cast<size_t>(idx) * N2 + f) * 4;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) lift[c] = sl[c];
+    } else {
+      double x[3], ext[5];
+      face_position<N1>(C, P.coords + 4 * e, s, a, b, t_stage, x);
+      eval_case(C.flow_case, x, t_stage, C.gas, ext);
+      prim4(ext, C.gas, lift);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+  }
+}
+
+// Volume BR1 gradient of (v1, v2, v3, T) at one node (assemble_gradients, solver.cpp:729-768).
+template <int N1>
+__device__ __forceinline__ void node_gradient(const double* tab, const double* sq, const double* sLift,
+                                              const BandD& B, int i, int j, int k, double* g) {
+  constexpr int N2 = Dim<N1>::N2, N3 = Dim<N1>::N3;
+  const double* dh = tab;
+  const double* fl = tab + N1 * N1;
+  const double* fr = fl + N1;
+  const double* iw = fl + 4 * N1;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* q = sq + c * N3;
+    double vx = 0.0, vy = 0.0, vz = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      vx += dh[i * N1 + m] * q[(m * N1 + j) * N1 + k];
+      vy += dh[j * N1 + m] * q[(i * N1 + m) * N1 + k];
+      vz += dh[k * N1 + m] * q[(i * N1 + j) * N1 + m];
+    }
+    const double sx = (sLift[(1 * 4 + c) * N2 + j * N1 + k] * fr[i] - sLift[(0 * 4 + c) * N2 + j * N1 + k] * fl[i]) * iw[i];
+    const double sy = (sLift[(3 * 4 + c) * N2 + i * N1 + k] * fr[j] - sLift[(2 * 4 + c) * N2 + i * N1 + k] * fl[j]) * iw[j];
+    const double sz = (sLift[(5 * 4 + c) * N2 + i * N1 + j] * fr[k] - sLift[(4 * 4 + c) * N2 + i * N1 + j] * fl[k]) * iw[k];
+    g[3 * c + 0] = B.cdir[0] * (sx - vx);
+    g[3 * c + 1] = B.cdir[1] * (sy - vy);
+    g[3 * c + 2] = B.cdir[2] * (sz - vz);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// k_gradient: lift* -> gradient -> Fv.n (conforming sides) / gradient traces
+// (sliding and Dirichlet sides).  Also serves compute_gradients (grad_out).
+// ----------------------------------------------------------------------------
+template <int N1>
+__global__ void __launch_bounds__(Dim<N1>::THREADS) k_gradient(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                               StageArgs A) {
+  constexpr int N2 = Dim<N1>::N2, N3 = Dim<N1>::N3, EPB = Dim<N1>::EPB, TAB = Dim<N1>::TAB;
+  constexpr int PER = 5 * N3 + 4 * N3 + 12 * N3 + 30 * N2 + 24 * N2;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  load_tables<N1>(C, tab);
+  const int e0 = blockIdx.x * EPB;
+  load_state<N1>(P.U, e0, P.E, smem + TAB, PER);
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = e < P.E;
+  double* su = smem + TAB + le * PER;
+  double* sq = su + 5 * N3;
+  double* sG = sq + 4 * N3;
+  double* sTr = sG + 12 * N3;
+  double* sLift = sTr + 30 * N2;
+  __syncthreads();
+  if (active) {
+    double u[5], q[4];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
+    prim4(u, C.gas, q);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sq[c * N3 + t] = q[c];
+    face_lift_phase<N1>(C, P, tab, su, e, A.t_stage, sLift, sTr);
+  }
+  __syncthreads();
+  if (active) {
+    const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+    double g[12];
+    node_gradient<N1>(tab, sq, sLift, C.bands[P.coords[4 * e]], i, j, k, g);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
+    if (P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = g[c];
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double gt[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+    const int slot = e * 6 + s;
+    const int typ = P.side_type[slot], idx = P.side_idx[slot];
+    if (typ == kConforming) {
+      double fv[4];
+      fv_dir(sTr + (s * N2 + f) * 5, gt, s >> 1, C.gas, fv);
+      double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dst[c] = fv[c];
+    } else {
+      double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+    }
+  }
+}
+
+__device__ __forceinline__ void record_error(ErrRec* err, int flag, int step, int stage, long long elem,
+                                             long long node, const double* vals) {
+  if (atomicCAS(&err->flag, 0, flag) == 0) {
+    err->step = step;
+    err->stage = stage;
+    err->elem = elem;
+    err->node = node;
+    for (int v = 0; v < 5; ++v) err->vals[v] = vals ? vals[v] : 0.0;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// k_update: the whole rest of the stage for one element (see file header).
+// ----------------------------------------------------------------------------
+template <int N1, bool VISC>
+__global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                             StageArgs A) {
+  constexpr int N2 = Dim<N1>::N2, N3 = Dim<N1>::N3, EPB = Dim<N1>::EPB, TAB = Dim<N1>::TAB;
+  constexpr int PER = 5 * N3 + 5 * N3 + 24 * N2 + 30 * N2;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  load_tables<N1>(C, tab);
+  const int e0 = blockIdx.x * EPB;
+  load_state<N1>(P.U, e0, P.E, smem + TAB, PER);
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = e < P.E;
+  double* su = smem + TAB + le * PER;
+  double* sF = su + 5 * N3;
+  double* sLift = sF + 5 * N3;
+  double* sFlux = sLift + 24 * N2;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  __syncthreads();
+
+  // Phase 1: numerical flux on all six sides -> sFlux[s][v][f]; lift* -> sLift.
+  if (active) {
+    if (VISC) {
+      double u[5], q[4];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
+      prim4(u, C.gas, q);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
+    }
+    for (int it = t; it < 6 * N2; it += N3) {
+      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1, dir = s >> 1;
+      const double* ell = tab + N1 * N1 + (s & 1) * N1;
+      double own[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b);
+      const int slot = e * 6 + s;
+      const int typ = P.side_type[slot], idx = P.side_idx[slot];
+      double flux[5], lift[4];
+      bool ok = true;
+      if (typ == kConforming) {
+        const double* nb = P.trace + static_cast<size_t>(idx) * N2 * 5 + f * 5;
+        double other[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) other[v] = nb[v];
+        const double vg = dir == 1 ? B.vg : 0.0;
+        const double* um = (s & 1) ? own : other;
+        const double* up = (s & 1) ? other : own;
+        if (VISC) {
+          double qa[4], qb[4];
+          prim4(own, C.gas, qa);
+          prim4(other, C.gas, qb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+          double fa[4], fb[4];
+          const double* pa = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
+          const double* pb = P.fvn + (static_cast<size_t>(idx) * N2 + f) * 4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            fa[c] = pa[c];
+            fb[c] = pb[c];
+          }
+          ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+        } else {
+          ok = roe_flux(um, up, dir, vg, C.gas, flux);
+        }
+      } else if (typ == kSliding) {
+        const double* sf = P.slide_flux + (static_cast<size_t>(idx) * N2 + f) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) flux[v] = sf[v];
+        if (VISC) {
+          const double* sl = P.slide_lift + (static_cast<size_t>(idx) * N2 + f) * 4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = sl[c];
+        }
+      } else {
+        double x[3], ext[5];
+        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        const double vg = dir == 1 ? B.vg : 0.0;
+        const double* um = (s & 1) ? own : ext;
+        const double* up = (s & 1) ? ext : own;
+        if (VISC) {
+          prim4(ext, C.gas, lift);
+          const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+          double gg[12];
+#pragma unroll
+          for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+          double fm[4], fp[4];
+          fv_dir(um, gg, dir, C.gas, fm);
+          fv_dir(up, gg, dir, C.gas, fp);
+          ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+        } else {
+          ok = roe_flux(um, up, dir, vg, C.gas, flux);
+        }
+      }
+      if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = flux[v];
+      if (VISC) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // Phase 2: pointwise volume flux (ALE convective minus viscous), flux.cpp:7-42.
+  double F[3][5];
+  double u[5];
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
+    const double ir = __drcp_rn(u[0]);
+    const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+    const double p = pressure(u, ir, C.gas);
+    const double vgv[3] = {0.0, B.vg, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      F[d][0] = u[0] * vv[d];
+      F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0);
+      F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0);
+      F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0);
+      F[d][4] = (u[4] + p) * vv[d];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) F[d][v] -= vgv[d] * u[v];
+    }
+    if (VISC) {
+      double g[12];
+      node_gradient<N1>(tab, sF, sLift, B, i, j, k, g);
+      const double div = g[0] + g[4] + g[8];
+      const double mu = C.gas.mu, lam = C.gas.lam;
+      const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
+                                {mu * (g[1] + g[3]), 2.0 * mu * g[4] + lam * div, mu * (g[5] + g[7])},
+                                {mu * (g[2] + g[6]), mu * (g[5] + g[7]), 2.0 * mu * g[8] + lam * div}};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        F[d][1] -= tau[d][0];
+        F[d][2] -= tau[d][1];
+        F[d][3] -= tau[d][2];
+        F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+      }
+    }
+  }
+
+  // Phase 3: weak divergence sum_m D-hat(i,m) F(m) per direction (volume_kernel, solver.cpp:372-383).
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double* dh = tab;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sF[v * N3 + t] = F[d][v] * B.sj[d];
+    }
+    __syncthreads();
+    if (active) {
+      const int ia = d == 0 ? i : (d == 1 ? j : k);
+      const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double c = dh[ia * N1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF[v * N3 + base + m * stride];
+      }
+    }
+  }
+
+  // Phase 4: surface lift (apply_all_faces, solver.cpp:547-582), sides X-,X+,Y-,Y+,Z-,Z+.
+  double du[5];
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
+    const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int dir = s >> 1;
+      const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+      const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+      const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
+      if (c != 0.0) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) sF[v * N3 + t] = du[v];
+  }
+  __syncthreads();
+
+  // Phase 5: flat coalesced RK update (solver.cpp:912-917) or residual store.
+  const int n_el = min(EPB, P.E - e0);
+  const size_t gbase = static_cast<size_t>(e0) * 5 * N3;
+  constexpr int PERB = 5 * N3 + 5 * N3 + 24 * N2 + 30 * N2;
+  double* elems = smem + TAB;
+  if (A.mode == 1) {
+    for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
+      const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+      P.out[gbase + fI] = elems[l * PERB + 5 * N3 + (r % 5) * N3 + r / 5];
+    }
+    return;
+  }
+  for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
+    const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+    double* us = elems + l * PERB + (r % 5) * N3 + r / 5;
+    const double d = us[5 * N3];
+    const double rg = A.rk_a * P.reg[gbase + fI] + A.dt * d;
+    const double un = *us + A.rk_b * rg;
+    P.reg[gbase + fI] = rg;
+    P.U[gbase + fI] = un;
+    *us = un;
+  }
+  __syncthreads();
+  if (!active) return;
+  // Admissibility (check_admissible, solver.cpp:892-906).
+  {
+    double w[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) w[v] = su[v * N3 + t];
+    const double p = pressure(w, __drcp_rn(w[0]), C.gas);
+    bool ok = w[0] > 0.0 && p > 0.0;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
+    if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+  }
+  // Face traces of the new state for the next stage.
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double* dst = P.trace + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// CFL time step (suggest_dt, solver.cpp:929-947): min over elements via an
+// order-preserving atomicMin on the bits of positive doubles.
+// ----------------------------------------------------------------------------
+template <int N1>
+__global__ void __launch_bounds__(Dim<N1>::THREADS) k_suggest_dt(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                                 double cfl, int degree, unsigned long long* out) {
+  constexpr int N3 = Dim<N1>::N3, EPB = Dim<N1>::EPB;
+  __shared__ double red[Dim<N1>::THREADS];
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = blockIdx.x * EPB + le;
+  double lm = 0.0;
+  if (e < P.E) {
+    const double* u = P.U + (static_cast<size_t>(e) * N3 + t) * 5;
+    const BandD& B = C.bands[P.coords[4 * e]];
+    const double ir = 1.0 / u[0];
+    const double a = u[1] * ir, b = u[2] * ir - B.vg, c = u[3] * ir;
+    const double p = pressure(u, ir, C.gas);
+    lm = sqrt(a * a + b * b + c * c) + sqrt(C.gas.gamma * p * ir);
+  }
+  red[threadIdx.x] = lm;
+  __syncthreads();
+  if (t == 0 && e < P.E) {
+    double m = 0.0;
+    for (int q = 0; q < N3; ++q) m = fmax(m, red[le * N3 + q]);
+    const BandD& B = C.bands[P.coords[4 * e]];
+    const double h = fmin(B.hx, fmin(B.hy, B.hz));
+    const double dt = cfl * h / (m * (2.0 * degree + 1.0));
+    atomicMin(out, static_cast<unsigned long long>(__double_as_longlong(dt)));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Device pairing (paper §4.4 / Appendix A; partition.cpp:85-169; solver.cpp:156-206):
+// per interface side the displacement (bit-exact scalar chain of mesh.cpp:9-25),
+// the mortar tuples, their nested sort by (partner, iface, i_par, i_perp, i_sub)
+// and the inverse map m.  The 5-key order restricted to one partner equals the
+// order of the dense key d = base[iface] + (i_par*n_perp + i_perp)*2 + i_sub, so
+// the sort is a per-partner counting pass over the dense key range.
+// One CTA per role.
+// ----------------------------------------------------------------------------
+constexpr int kPairThreads = 256;
+constexpr int kPairPartners = 16;
+
+__device__ __forceinline__ long long pmod(long long a, long long n) {
+  const long long r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+__global__ void __launch_bounds__(kPairThreads) k_pairing(const __grid_constant__ PairingArgs A, PairingPtrs P) {
+  const int role = blockIdx.x;
+  const int tid = threadIdx.x;
+  __shared__ long long s_nd[kMaxCtx];
+  __shared__ int s_conf[kMaxCtx];
+  __shared__ int S[kPairPartners][kPairThreads + 1];
+  __shared__ int tot[kPairPartners], off[kPairPartners];
+  __shared__ int s_bad;
+  if (tid == 0) s_bad = 0;
+  if (tid < A.n_ctx) {
+    const CtxD& c = A.ctx[tid];
+    const double delta = __dadd_rn(A.delta_base[tid], __dmul_rn(c.vg_rel, __dsub_rn(A.t_stage, A.time)));
+    const double period = __dmul_rn(c.l_par, static_cast<double>(c.n_par));
+    double d = fmod(delta, period);
+    if (d < 0.0) d = __dadd_rn(d, period);
+    const double ratio = __ddiv_rn(d, c.l_par);
+    long long nd = static_cast<long long>(floor(ratio));
+    double sd = __dsub_rn(ratio, static_cast<double>(nd));
+    if (nd >= c.n_par) {
+      nd = 0;
+      sd = 0.0;
+    }
+    s_nd[tid] = nd;
+    s_conf[tid] = sd == 0.0;
+    if (role == 0) {
+      P.ctx_state[2 * tid] = static_cast<int>(nd);
+      P.ctx_state[2 * tid + 1] = sd == 0.0;
+      P.ctx_sdelta[tid] = sd;
+    }
+  }
+  int* pres = P.pres[role];
+  int* payload = P.payload[role];
+  for (long long d = tid; d < A.dense_size; d += kPairThreads) pres[d] = -1;
+  for (int r = 0; r < A.role_nctx[role]; ++r) {
+    const CtxD& c = A.ctx[A.role_ctx[role][r]];
+    for (int q = tid; q < 2 * c.n_faces; q += kPairThreads) P.m[2 * c.face_off + q] = -1;
+  }
+  __syncthreads();
+  // Tuples (append_mortar_tuples).
+  for (int r = 0; r < A.role_nctx[role]; ++r) {
+    const int ci = A.role_ctx[role][r];
+    const CtxD& c = A.ctx[ci];
+    const long long nd = s_nd[ci];
+    const int conf = s_conf[ci];
+    for (int q = tid; q < 2 * c.n_faces; q += kPairThreads) {
+      const int f = q >> 1, sub = q & 1;
+      if (conf && sub == 0) continue;
+      const long long fpar = P.ctx_face_par[c.face_off + f], fperp = P.ctx_face_perp[c.face_off + f];
+      long long ipar;
+      int partner;
+      if (c.on_static) {
+        ipar = fpar;
+        partner = P.partner_map[c.map_off + fperp * c.n_par + pmod(fpar - nd + sub - 1, c.n_par)];
+      } else {
+        ipar = pmod(fpar + nd - sub + 1, c.n_par);
+        partner = P.partner_map[c.map_off + fperp * c.n_par + ipar];
+      }
+      if (partner < 0 || partner >= kPairPartners) {
+        s_bad = 1;
+        continue;
+      }
+      const long long d = A.iface_base[c.iface] + (ipar * c.n_perp + fperp) * 2 + sub;
+      pres[d] = partner;
+      payload[d] = (ci << 24) | f;
+    }
+  }
+  __syncthreads();
+  // Pass 1: per-thread segment counts per partner.
+  const long long D = A.dense_size;
+  const long long L = (D + kPairThreads - 1) / kPairThreads;
+  const long long lo = tid * L, hi = min(D, lo + L);
+  int cnt[kPairPartners];
+#pragma unroll
+  for (int p = 0; p < kPairPartners; ++p) cnt[p] = 0;
+  for (long long d = lo; d < hi; ++d) {
+    const int p = pres[d];
+#pragma unroll
+    for (int q = 0; q < kPairPartners; ++q) cnt[q] += (p == q);
+  }
+#pragma unroll
+  for (int p = 0; p < kPairPartners; ++p) S[p][tid] = cnt[p];
+  __syncthreads();
+  // Exclusive scans over threads, one warp per two partners.
+  {
+    const int w = tid >> 5, lane = tid & 31;
+    constexpr int PER = kPairThreads / 32;
+    for (int p = w; p < kPairPartners; p += kPairThreads / 32) {
+      int loc[PER], sum = 0;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        loc[r] = sum;
+        sum += S[p][lane * PER + r];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - sum;
+#pragma unroll
+      for (int r = 0; r < PER; ++r) S[p][lane * PER + r] = excl + loc[r];
+      if (lane == 31) tot[p] = incl;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int p = 0; p < kPairPartners; ++p) {
+      off[p] = acc;
+      acc += tot[p];
+    }
+    P.n_mortars[role] = acc;
+    if (s_bad || (A.expect_mortars[role] >= 0 && A.expect_mortars[role] != acc)) {
+      if (atomicCAS(&P.err->flag, 0, 3) == 0) {
+        P.err->elem = role;
+        P.err->node = acc;
+      }
+    }
+  }
+  __syncthreads();
+  // Pass 2: positions, A columns and m (sort_index_array + build_mapping).
+  int run[kPairPartners];
+#pragma unroll
+  for (int p = 0; p < kPairPartners; ++p) run[p] = 0;
+  for (long long d = lo; d < hi; ++d) {
+    const int p = pres[d];
+    if (p < 0) continue;
+    int pos = 0;
+#pragma unroll
+    for (int q = 0; q < kPairPartners; ++q)
+      if (p == q) pos = off[q] + S[q][tid] + run[q]++;
+    int ifc = 0;
+    for (int x = 1; x < A.n_ifaces; ++x)
+      if (d >= A.iface_base[x]) ifc = x;
+    long long rest = d - A.iface_base[ifc];
+    const int sub = static_cast<int>(rest & 1);
+    rest >>= 1;
+    const long long np = A.iface_nperp[ifc];
+    const int iperp = static_cast<int>(rest % np), ipar = static_cast<int>(rest / np);
+    const int pl = payload[d];
+    const int ci = pl >> 24, f = pl & 0xffffff;
+    int* col = P.cols[role] + 7 * pos;
+    col[0] = p;
+    col[1] = ifc;
+    col[2] = ipar;
+    col[3] = iperp;
+    col[4] = sub;
+    col[5] = f;
+    col[6] = ci;
+    const CtxD& c = A.ctx[ci];
+    P.m[2 * c.face_off + sub * c.n_faces + f] = pos;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Mortar kernels (fill_mortar_solution / send_gradient_phase / run_lifting /
+// mortar_flux_phase / mortar_apply_phase; solver.cpp:234-252, 657-714, 806-831,
+// 442-526).  The 1D operators act along the sliding axis j for every k line.
+// ----------------------------------------------------------------------------
+template <int N1>
+__device__ __forceinline__ void load_ops(const MortarOps& ops, int n_ctx, double* s_ops) {
+  for (int q = threadIdx.x; q < n_ctx * 2 * N1 * N1; q += blockDim.x) {
+    const int c = q / (2 * N1 * N1), r = q % (2 * N1 * N1), h = r / (N1 * N1), x = r % (N1 * N1);
+    s_ops[q] = ops.op[c][h][x];
+  }
+}
+
+template <int N1, int NC>
+__global__ void k_mortar_fill(const __grid_constant__ MortarOps ops, int n_ctx, MortarPtrs P, const double* src,
+                              double* dst0, double* dst1) {
+  constexpr int N2 = N1 * N1;
+  __shared__ double s_ops[kMaxCtx * 2 * N1 * N1];
+  load_ops<N1>(ops, n_ctx, s_ops);
+  __syncthreads();
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= P.S * 2 * N2) return;
+  const int ks = item / (2 * N2), sub = (item / N2) & 1, node = item % N2, jm = node / N1, kk = node % N1;
+  const int ci = P.slide_ctx[ks], f = P.slide_f[ks];
+  const int conf = P.ctx_state[2 * ci + 1];
+  if (conf && sub == 0) return;
+  const int role = P.ctx_role[ci];
+  const int mi = P.m[2 * P.ctx_face_off[ci] + sub * P.ctx_nf[ci] + f];
+  const double* s = NC == 5 ? src + (static_cast<size_t>(P.slide_elem[ks]) * 6 + P.slide_side[ks]) * N2 * NC
+                            : src + static_cast<size_t>(ks) * N2 * NC;
+  double* d = (role == 0 ? dst0 : dst1) + (static_cast<size_t>(mi) * N2 + node) * NC;
+  if (conf) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] = s[node * NC + c];
+    return;
+  }
+  const int half = role == 0 ? sub : 1 - sub;
+  const double* op = s_ops + (ci * 2 + half) * N2 + jm * N1;
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < N1; ++jj) {
+    const double w = op[jj];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] += w * s[(jj * N1 + kk) * NC + c];
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) d[c] = acc[c];
+}
+
+template <int N1>
+__global__ void k_mortar_lift(GasD g, MortarPtrs P, int max_mortars) {
+  constexpr int N2 = N1 * N1;
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= max_mortars * N2 || item / N2 >= P.n_mortars[0]) return;
+  const size_t q = static_cast<size_t>(item);
+  double a[4], b[4];
+  prim4(P.u_mine[0] + q * 5, g, a);
+  prim4(P.u_theirs + q * 5, g, b);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) P.lift[0][q * 4 + c] = __dmul_rn(0.5, __dadd_rn(a[c], b[c]));
+}
+
+template <int N1, int NC>
+__global__ void k_mortar_backproject(const __grid_constant__ MortarOps ops, int n_ctx, MortarPtrs P,
+                                     const double* src0, const double* src1, double* dst) {
+  constexpr int N2 = N1 * N1;
+  __shared__ double s_ops[kMaxCtx * 2 * N1 * N1];
+  load_ops<N1>(ops, n_ctx, s_ops);
+  __syncthreads();
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= P.S * N2) return;
+  const int ks = item / N2, node = item % N2, jj = node / N1, kk = node % N1;
+  const int ci = P.slide_ctx[ks], f = P.slide_f[ks];
+  const int conf = P.ctx_state[2 * ci + 1];
+  const int role = P.ctx_role[ci];
+  const double* src = role == 0 ? src0 : src1;
+  const int* mrow = P.m + 2 * P.ctx_face_off[ci];
+  const int nf = P.ctx_nf[ci];
+  double* d = dst + (static_cast<size_t>(ks) * N2 + node) * NC;
+  if (conf) {
+    const double* s = src + (static_cast<size_t>(mrow[nf + f]) * N2 + node) * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] = s[c];
+    return;
+  }
+  double out[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) out[c] = 0.0;
+#pragma unroll
+  for (int sub = 0; sub < 2; ++sub) {
+    const int half = role == 0 ? sub : 1 - sub;
+    const double* op = s_ops + (ci * 2 + half) * N2 + jj * N1;
+    const double* s = src + static_cast<size_t>(mrow[sub * nf + f]) * N2 * NC;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int jm = 0; jm < N1; ++jm) {
+      const double w = op[jm];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] += w * s[(jm * N1 + kk) * NC + c];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[c] += acc[c];
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) d[c] = out[c];
+}
+
+template <int N1, bool VISC>
+__global__ void k_mortar_flux(GasD g, MortarPtrs P, int max_mortars, ErrRec* err) {
+  constexpr int N2 = N1 * N1;
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= max_mortars * N2) return;
+  const int mc = item / N2;
+  if (mc >= P.n_mortars[0]) return;
+  const int ci = P.cols_static[7 * mc + 6];
+  const bool static_left = P.ctx_static_left[ci] != 0;
+  const size_t q = static_cast<size_t>(item);
+  const double* mine = P.u_mine[0] + q * 5;
+  const double* theirs = P.u_theirs + q * 5;
+  double f[5];
+  bool ok;
+  if (VISC) {
+    double fm[4], ft[4];
+    fv_dir(mine, P.g_mine[0] + q * 12, 0, g, fm);
+    fv_dir(theirs, P.g_theirs + q * 12, 0, g, ft);
+    ok = static_left ? face_flux_fv(mine, theirs, 0, 0.0, fm, ft, g, f)
+                     : face_flux_fv(theirs, mine, 0, 0.0, ft, fm, g, f);
+  } else {
+    ok = static_left ? roe_flux(mine, theirs, 0, 0.0, g, f) : roe_flux(theirs, mine, 0, 0.0, g, f);
+  }
+  if (!ok) record_error(err, 2, -1, -1, -1, mc, mine);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) P.flux[0][q * 5 + v] = f[v];
+}
+
+template <int N1>
+int smem_gradient() {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  return (Dim<N1>::TAB + Dim<N1>::EPB * (21 * N3 + 54 * N2)) * 8;
+}
+template <int N1>
+int smem_update() {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  return (Dim<N1>::TAB + Dim<N1>::EPB * (10 * N3 + 54 * N2)) * 8;
+}
+template <int N1>
+int smem_prolong() {
+  return (Dim<N1>::TAB + Dim<N1>::EPB * 5 * Dim<N1>::N3) * 8;
+}
+
+inline void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw DeviceError(SDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class K>
+void set_smem(K kernel, int bytes) {
+  static_assert(sizeof(K) > 0, "");
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <int N1>
+void prolong_t(const ElemConsts& c, const FieldPtrs& p, cudaStream_t st) {
+  const int blocks = (p.E + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
+  const int sm = smem_prolong<N1>();
+  set_smem(k_prolong<N1>, sm);
+  k_prolong<N1><<<blocks, Dim<N1>::THREADS, sm, st>>>(c, p);
+  check_launch("k_prolong");
+}
+template <int N1>
+void gradient_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  const int blocks = (p.E + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
+  const int sm = smem_gradient<N1>();
+  set_smem(k_gradient<N1>, sm);
+  k_gradient<N1><<<blocks, Dim<N1>::THREADS, sm, st>>>(c, p, a);
+  check_launch("k_gradient");
+}
+template <int N1>
+void update_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  const int blocks = (p.E + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
+  const int sm = smem_update<N1>();
+  if (c.gas.viscous) {
+    set_smem(k_update<N1, true>, sm);
+    k_update<N1, true><<<blocks, Dim<N1>::THREADS, sm, st>>>(c, p, a);
+  } else {
+    set_smem(k_update<N1, false>, sm);
+    k_update<N1, false><<<blocks, Dim<N1>::THREADS, sm, st>>>(c, p, a);
+  }
+  check_launch("k_update");
+}
+
+template <int N1>
+void mortar_fill_t(int nc, const double* src, double* const dst[2], const MortarOps& ops, const MortarPtrs& p,
+                   cudaStream_t st) {
+  const int items = p.S * 2 * N1 * N1;
+  if (items == 0) return;
+  const int bs = 128, blocks = (items + bs - 1) / bs;
+  int n_ctx = kMaxCtx;
+  if (nc == 5) k_mortar_fill<N1, 5><<<blocks, bs, 0, st>>>(ops, n_ctx, p, src, dst[0], dst[1]);
+  else k_mortar_fill<N1, 12><<<blocks, bs, 0, st>>>(ops, n_ctx, p, src, dst[0], dst[1]);
+  check_launch("k_mortar_fill");
+}
+template <int N1>
+void mortar_back_t(int nc, const double* const src[2], double* dst, const MortarOps& ops, const MortarPtrs& p,
+                   cudaStream_t st) {
+  const int items = p.S * N1 * N1;
+  if (items == 0) return;
+  const int bs = 128, blocks = (items + bs - 1) / bs;
+  if (nc == 4) k_mortar_backproject<N1, 4><<<blocks, bs, 0, st>>>(ops, kMaxCtx, p, src[0], src[1], dst);
+  else k_mortar_backproject<N1, 5><<<blocks, bs, 0, st>>>(ops, kMaxCtx, p, src[0], src[1], dst);
+  check_launch("k_mortar_backproject");
+}
+
+#define SDG_DISPATCH(n1, CALL)                          \
+  switch (n1) {                                         \
+    case 2: { constexpr int NN = 2; CALL; break; }      \
+    case 3: { constexpr int NN = 3; CALL; break; }      \
+    case 4: { constexpr int NN = 4; CALL; break; }      \
+    case 5: { constexpr int NN = 5; CALL; break; }      \
+    case 6: { constexpr int NN = 6; CALL; break; }      \
+    case 7: { constexpr int NN = 7; CALL; break; }      \
+    case 8: { constexpr int NN = 8; CALL; break; }      \
+    default: throw ConfigError("unsupported N+1");      \
+  }
+
+}  // namespace
+
+void launch_prolong(int n1, const ElemConsts& c, const FieldPtrs& p, cudaStream_t st) {
+  if (p.E == 0) return;
+  SDG_DISPATCH(n1, (prolong_t<NN>(c, p, st)));
+}
+void launch_gradient(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (p.E == 0) return;
+  SDG_DISPATCH(n1, (gradient_t<NN>(c, p, a, st)));
+}
+void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (p.E == 0) return;
+  SDG_DISPATCH(n1, (update_t<NN>(c, p, a, st)));
+}
+void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
+  k_pairing<<<2, kPairThreads, 0, st>>>(a, p);
+  check_launch("k_pairing");
+}
+void launch_mortar_fill(int n1, int nc, const double* src, double* const dst[2], const MortarOps& ops,
+                        const MortarPtrs& p, cudaStream_t st) {
+  SDG_DISPATCH(n1, (mortar_fill_t<NN>(nc, src, dst, ops, p, st)));
+}
+void launch_mortar_lift(int n1, const GasD& g, const MortarPtrs& p, int max_mortars, cudaStream_t st) {
+  const int items = max_mortars * n1 * n1;
+  if (items == 0) return;
+  const int bs = 128, blocks = (items + bs - 1) / bs;
+  SDG_DISPATCH(n1, (k_mortar_lift<NN><<<blocks, bs, 0, st>>>(g, p, max_mortars)));
+  check_launch("k_mortar_lift");
+}
+void launch_mortar_backproject(int n1, int nc, const double* const src[2], double* dst, const MortarOps& ops,
+                               const MortarPtrs& p, cudaStream_t st) {
+  SDG_DISPATCH(n1, (mortar_back_t<NN>(nc, src, dst, ops, p, st)));
+}
+void launch_mortar_flux(int n1, const GasD& g, int viscous, const MortarPtrs& p, int max_mortars, ErrRec* err,
+                        cudaStream_t st) {
+  const int items = max_mortars * n1 * n1;
+  if (items == 0) return;
+  const int bs = 128, blocks = (items + bs - 1) / bs;
+  if (viscous) {
+    SDG_DISPATCH(n1, (k_mortar_flux<NN, true><<<blocks, bs, 0, st>>>(g, p, max_mortars, err)));
+  } else {
+    SDG_DISPATCH(n1, (k_mortar_flux<NN, false><<<blocks, bs, 0, st>>>(g, p, max_mortars, err)));
+  }
+  check_launch("k_mortar_flux");
+}
+void launch_suggest_dt(int n1, const ElemConsts& c, const FieldPtrs& p, double cfl, int degree,
+                       unsigned long long* out, cudaStream_t st) {
+  if (p.E == 0) return;
+  SDG_DISPATCH(n1, (k_suggest_dt<NN><<<(p.E + Dim<NN>::EPB - 1) / Dim<NN>::EPB, Dim<NN>::THREADS, 0, st>>>(
+                        c, p, cfl, degree, out)));
+  check_launch("k_suggest_dt");
+}
+
+}  // namespace sdg

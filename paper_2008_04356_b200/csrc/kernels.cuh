@@ -1,0 +1,157 @@
+// Device-side data structures and launch wrappers of the B200 path.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sdg_types.h"
+#include "host.hpp"
+
+namespace sdg {
+
+struct GasD {
+  double gamma, gm1, R, inv_R, mu, lam, kcond;
+  int viscous;
+};
+
+struct BandD {
+  double x_lo, hx, hy, hz, vg;
+  double inv_jac;
+  double cdir[3];  // sJ_d / J
+  double sj[3];    // sJ_d
+};
+
+// Per-run constants, passed by value (__grid_constant__) to every element kernel.
+struct ElemConsts {
+  double dhat[kMaxN1 * kMaxN1];  // D-hat(i,m) = w_m D(m,i) / w_i  (solver.cpp:38-41)
+  double fl[kMaxN1], fr[kMaxN1];  // l_j(-1), l_j(+1)
+  double liftw[2][kMaxN1];        // l_j(-+1) / w_j
+  double inv_w[kMaxN1];
+  double x[kMaxN1];
+  BandD bands[SDG_MAX_BANDS];
+  GasD gas;
+  double y0, z0;
+  sdg_case flow_case;
+};
+
+// Deferred admissibility / protocol error record (written by the first failing thread).
+struct ErrRec {
+  int flag;  // 0 none, 2 invalid state, 3 protocol
+  int step, stage, pad;
+  long long elem, node;
+  double vals[5];
+};
+
+// Pointers of the resident fields and face arrays.
+struct FieldPtrs {
+  double* U;
+  double* reg;
+  double* out;         // dudt (residual mode)
+  double* trace;       // (6E + H) slots x N2 x 5   face traces of U
+  double* fvn;         // (6E + H) slots x N2 x 4   viscous normal flux (mom x,y,z, energy)
+  const double* slide_lift;  // S x N2 x 4
+  const double* slide_flux;  // S x N2 x 5
+  double* slide_g;           // S x N2 x 12
+  double* dir_g;             // ND x N2 x 12
+  const int8_t* side_type;   // E x 6
+  const int* side_idx;       // E x 6
+  const int* coords;         // E x 4 (band, ix, iy, iz)
+  double* grad_out;          // optional E x N3 x 12
+  ErrRec* err;
+  int E;
+};
+
+struct StageArgs {
+  double t_stage, dt, rk_a, rk_b;
+  int mode;  // 0: RK update (+ trace output), 1: residual into out
+  int step, stage;
+};
+
+// ---- mortar side ----
+// Interface-side context as the device sees it.
+struct CtxD {
+  int iface, on_static, role, n_faces;  // n_faces = local faces of this side
+  int face_off;                         // offset into ctx_faces / slide ids
+  int map_off;                          // offset into the partner rank map
+  long long n_par, n_perp;
+  int static_is_left;
+  double l_par, vg_rel;
+};
+
+struct PairingArgs {
+  int n_ctx;
+  CtxD ctx[kMaxCtx];
+  int role_ctx[2][kMaxCtx];
+  int role_nctx[2];
+  long long iface_base[kMaxCtx];  // dense-key base per interface (same for both roles)
+  long long iface_nperp[kMaxCtx];
+  long long dense_size;
+  int n_ifaces;
+  int self_rank;
+  double delta_base[kMaxCtx];
+  double time, t_stage;
+  int expect_mortars[2];           // host-side count per role, checked on the device
+};
+
+struct PairingPtrs {
+  const int* ctx_face_par;   // per ctx face: i_par (static frame for static, moving index for moving)
+  const int* ctx_face_perp;
+  const int* ctx_face_slide; // compact sliding index of the ctx face
+  const int* partner_map;    // concatenated partner-side rank maps
+  int* pres[2];              // dense scratch per role
+  int* payload[2];
+  int* cols[2];              // SDG_TUPLE_INTS per column
+  int* m;                    // per ctx: 2 x n_faces (offset 2*face_off)
+  int* ctx_state;            // per ctx: n_delta, conforming
+  double* ctx_sdelta;
+  int* n_mortars;            // 2
+  ErrRec* err;
+};
+
+struct MortarOps {
+  double op[kMaxCtx][2][kMaxN1 * kMaxN1];
+};
+
+struct MortarPtrs {
+  const double* trace;
+  double* u_mine[2];
+  double* u_theirs;     // static role
+  double* lift[2];
+  double* g_mine[2];
+  double* g_theirs;     // static role
+  double* flux[2];
+  double* slide_lift;
+  double* slide_flux;
+  const double* slide_g;
+  const int* slide_elem;   // S: element
+  const int* slide_side;   // S: side
+  const int* slide_ctx;    // S: ctx id
+  const int* slide_f;      // S: face index within ctx
+  const int* m;            // per ctx 2 x n_faces at 2*face_off
+  const int* ctx_face_off; // n_ctx
+  const int* ctx_nf;       // n_ctx
+  const int* ctx_role;     // n_ctx (0 static, 1 moving)
+  const int* ctx_state;    // per ctx: n_delta, conforming
+  const int* n_mortars;    // 2
+  const int* cols_static;  // ctx of each static mortar: cols[7*c + 6]
+  const int* ctx_static_left;
+  int S;
+};
+
+// ---- launch wrappers (kernels.cu) ----
+void launch_prolong(int n1, const ElemConsts& c, const FieldPtrs& p, cudaStream_t st);
+void launch_gradient(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st);
+void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
+                        const MortarPtrs& p, cudaStream_t st);
+void launch_mortar_lift(int n1, const GasD& g, const MortarPtrs& p, int max_mortars, cudaStream_t st);
+void launch_mortar_backproject(int n1, int ncomp, const double* const src[2], double* dst, const MortarOps& ops,
+                               const MortarPtrs& p, cudaStream_t st);
+void launch_mortar_flux(int n1, const GasD& g, int viscous, const MortarPtrs& p, int max_mortars, ErrRec* err,
+                        cudaStream_t st);
+void launch_suggest_dt(int n1, const ElemConsts& c, const FieldPtrs& p, double cfl, int degree,
+                       unsigned long long* out, cudaStream_t st);
+
+}  // namespace sdg

@@ -1,0 +1,1280 @@
+// GpuRankSolver: the per-rank, per-GPU context behind the C-ABI.
+//
+// Mirrors the public surface of sdg::RankSolver (/root/reference/proj/src/solver.hpp:64-98):
+// construction from mesh / partition / basis / gas / case, the one init-time
+// rank-map exchange, initial condition, step, compute_residual,
+// compute_gradients, suggest_dt, side_ctx and total_rebuilds.  Fields live on
+// the device for the lifetime of the context; every stage is a fixed sequence
+// of kernel launches on one stream.
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/sdg_gpu.h"
+#include "kernels.cuh"
+
+namespace sdg {
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(SDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw DeviceError(SDG_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc(v.size());
+    if (!v.empty()) cuda_check(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+  }
+  void zero(cudaStream_t st) {
+    if (n) cuda_check(cudaMemsetAsync(p, 0, n * sizeof(T), st), "memset");
+  }
+};
+
+// Carpenter-Kennedy 5-stage 2N-storage RK4 (proj/src/lsrk.cpp:7-29).
+const double RK_A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                        -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+const double RK_B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                        1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                        2277821191437.0 / 14882151754819.0};
+const double RK_C[5] = {0.0, 1432997174477.0 / 9575080441755.0, 2526269341429.0 / 6820363962896.0,
+                        2006345519317.0 / 3224310063776.0, 2802321613138.0 / 2924317926251.0};
+
+// Interface-side context on the host (InterfaceSideCtx, solver.hpp:16-42).
+struct SideCtx {
+  int iface = 0;
+  bool on_static = true;
+  std::vector<int> slides;  // compact sliding indices, sorted by (i_par, i_perp)
+  std::vector<int> static_map, moving_map;  // rank maps (r, r~), n_perp x n_par
+  double delta_base = 0.0;
+  Displacement st;
+  double sigma_side = -1.0;
+  bool conforming = true;
+  long last_n = -1;
+  bool last_conf = true, topo_valid = false;
+  long rebuilds = 0;
+  double ops_sigma = 2.0;  // sigma the cached operators were built for
+  std::vector<double> fwd, bwd;
+  // per-partner mortar counts of this side (for the NCCL blocks)
+};
+
+const char* kKernelClasses[] = {"prolong", "pairing", "mortar", "gradient", "update", "copy", "halo"};
+enum KClass { KC_PROLONG, KC_PAIRING, KC_MORTAR, KC_GRADIENT, KC_UPDATE, KC_COPY, KC_HALO, KC_N };
+
+}  // namespace
+
+class GpuRankSolver {
+ public:
+  GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& cfg, int n_ranks, int rank, int device,
+                const void* nccl_id);
+  ~GpuRankSolver();
+
+  void init_rank_maps();
+  void set_initial_condition(double t0);
+  void set_state(const double* h);
+  void get_state(double* h);
+  void get_register(double* h);
+  void steps(double dt, int n, bool sync);
+  void synchronize();
+  void compute_residual(double t_stage, const double* d_u, double* d_dudt);
+  void compute_gradients(double t_stage, const double* d_u, double* d_grad);
+  double suggest_dt(double cfl);
+  long total_rebuilds() const {
+    long t = 0;
+    for (const auto& s : sides_) t += s.rebuilds;
+    return t;
+  }
+  void ctx_info(int c, long* out5, double* sd, double* sig);
+  void get_pairing(int role, int* ncols, int* cols);
+  void get_mapping(int c, int* m);
+
+  int n1() const { return n_; }
+  long n_local() const { return E_; }
+  long n_global() const { return mesh_.n_elements; }
+  const std::vector<long>& gids() const { return topo_.gids; }
+  int n_contexts() const { return static_cast<int>(sides_.size()); }
+  double time() const { return time_; }
+  int step_index() const { return step_index_; }
+  double* d_state() { return U_.p; }
+  cudaStream_t stream() const { return stream_; }
+  long launches() const { return launches_; }
+  void enable_timing(bool on) { timing_ = on; }
+  std::vector<std::pair<double, long>> timing_totals();
+
+  std::string err;
+
+ private:
+  void build_consts();
+  void build_sides();
+  void upload_topology();
+  void stage(double t_stage, int mode, double rk_a, double rk_b, double dt, double* out, const double* u_override);
+  void update_interfaces_host(double t_stage);
+  void run_pairing(double t_stage);
+  void mortar_exchange(double* const src[2], double* dst_static, int ncomp, bool moving_to_static);
+  void halo_exchange(double* arr, int ncomp);
+  FieldPtrs field_ptrs(double* U, double* out);
+  MortarPtrs mortar_ptrs();
+  void check_error();
+  void mark(int cls, bool begin);
+
+  MeshGeom mesh_;
+  Partition part_;
+  LocalTopology topo_;
+  Basis basis_;
+  sdg_solver_config cfg_;
+  ElemConsts consts_{};
+  int n_ = 0, n2_ = 0, n3_ = 0;
+  int E_ = 0, S_ = 0, ND_ = 0;
+  int rank_ = 0, n_ranks_ = 1, device_ = 0;
+  bool lifting_ = false;
+  cudaStream_t stream_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+
+  DevBuf<double> U_, reg_, dudt_, trace_, fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
+  DevBuf<int8_t> side_type_;
+  DevBuf<int> side_idx_, coords_;
+  DevBuf<ErrRec> err_;
+  ErrRec* err_host_ = nullptr;
+  DevBuf<unsigned long long> dt_min_;
+  DevBuf<double> send_buf_;
+  DevBuf<int> send_slots_;
+
+  // mortar / pairing
+  std::vector<SideCtx> sides_;
+  std::vector<int> role_ids_[2];
+  PairingArgs pargs_{};
+  DevBuf<int> face_par_, face_perp_, face_slide_, partner_map_, pres_[2], payload_[2], cols_[2], m_, ctx_state_,
+      n_mortars_;
+  DevBuf<double> ctx_sdelta_;
+  DevBuf<int> slide_elem_, slide_side_, slide_ctx_, slide_f_, ctx_face_off_, ctx_nf_, ctx_role_, ctx_static_left_;
+  DevBuf<double> u_mine_[2], u_theirs_, mlift_[2], g_mine_[2], g_theirs_, mflux_[2];
+  int max_mortars_[2] = {0, 0};
+  int expect_mortars_[2] = {0, 0};
+  MortarOps fwd_ops_{}, bwd_ops_{};
+  // per role: mortar blocks per partner (partner, offset, count) + self
+  std::vector<std::array<int, 3>> sched_[2];
+  std::array<int, 3> self_[2] = {{0, 0, 0}, {0, 0, 0}};
+
+  double time_ = 0.0;
+  int step_index_ = 0, stage_index_ = 0;
+  bool traces_valid_ = false;
+  long launches_ = 0;
+  bool timing_ = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events_;
+  cudaEvent_t pending_start_ = nullptr;
+  double class_ms_[KC_N] = {};
+  long class_n_[KC_N] = {};
+};
+
+GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& cfg, int n_ranks, int rank,
+                             int device, const void* nccl_id)
+    : mesh_(ms), part_(assign_ranks(mesh_, n_ranks)), topo_(build_topology(mesh_, part_, rank)),
+      basis_(cfg.degree, cfg.node_kind), cfg_(cfg), rank_(rank), n_ranks_(n_ranks), device_(device) {
+  const auto& g = cfg.gas;
+  if (!(g.gamma > 1.0) || !(g.R > 0.0) || !(g.mu >= 0.0) || !(g.Pr > 0.0))
+    throw ConfigError("gas model requires gamma > 1, R > 0, mu >= 0, Pr > 0");
+  if (rank < 0 || rank >= n_ranks) throw ConfigError("rank outside [0, n_ranks)");
+  n_ = basis_.n;
+  n2_ = n_ * n_;
+  n3_ = n2_ * n_;
+  E_ = static_cast<int>(topo_.gids.size());
+  S_ = static_cast<int>(topo_.sliding.size());
+  ND_ = static_cast<int>(topo_.dirichlet.size());
+  lifting_ = g.mu > 0.0;
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (n_ranks > 1) {
+    if (!nccl_id) throw ConfigError("multi-rank context needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    nccl_check(ncclCommInitRank(&comm_, n_ranks, id, rank), "ncclCommInitRank");
+  }
+  build_consts();
+  upload_topology();
+  build_sides();
+  cuda_check(cudaMallocHost(&err_host_, sizeof(ErrRec)), "cudaMallocHost");
+  cuda_check(cudaStreamSynchronize(stream_), "setup sync");
+}
+
+GpuRankSolver::~GpuRankSolver() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& ev : events_) {
+    cudaEventDestroy(ev.second.first);
+    cudaEventDestroy(ev.second.second);
+  }
+  if (comm_) ncclCommDestroy(comm_);
+  if (err_host_) cudaFreeHost(err_host_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void GpuRankSolver::build_consts() {
+  const int n = n_;
+  for (int i = 0; i < n; ++i) {
+    for (int m = 0; m < n; ++m) consts_.dhat[i * kMaxN1 + m] = basis_.w[m] * basis_.D[m * n + i] / basis_.w[i];
+    consts_.fl[i] = basis_.fl[i];
+    consts_.fr[i] = basis_.fr[i];
+    consts_.liftw[0][i] = basis_.fl[i] / basis_.w[i];
+    consts_.liftw[1][i] = basis_.fr[i] / basis_.w[i];
+    consts_.inv_w[i] = 1.0 / basis_.w[i];
+    consts_.x[i] = basis_.x[i];
+  }
+  for (size_t b = 0; b < mesh_.bands.size(); ++b) {
+    const BandGeom& bg = mesh_.bands[b];
+    BandD& d = consts_.bands[b];
+    d.x_lo = bg.x_lo;
+    d.hx = bg.hx;
+    d.hy = bg.hy;
+    d.hz = bg.hz;
+    d.vg = bg.vg;
+    const double jac = 0.125 * bg.hx * bg.hy * bg.hz;
+    d.inv_jac = 1.0 / jac;
+    d.sj[0] = 0.25 * bg.hy * bg.hz;
+    d.sj[1] = 0.25 * bg.hx * bg.hz;
+    d.sj[2] = 0.25 * bg.hx * bg.hy;
+    for (int q = 0; q < 3; ++q) d.cdir[q] = d.sj[q] / jac;
+  }
+  const auto& g = cfg_.gas;
+  consts_.gas = {g.gamma, g.gamma - 1.0, g.R, 1.0 / g.R, g.mu, -2.0 / 3.0 * g.mu,
+                 g.gamma * g.R * g.mu / ((g.gamma - 1.0) * g.Pr), g.mu > 0.0 ? 1 : 0};
+  consts_.y0 = mesh_.spec.y0;
+  consts_.z0 = mesh_.spec.z0;
+  consts_.flow_case = cfg_.flow_case;
+}
+
+void GpuRankSolver::upload_topology() {
+  const size_t slots = static_cast<size_t>(6) * E_ + topo_.n_halo;
+  U_.alloc(static_cast<size_t>(E_) * n3_ * 5);
+  reg_.alloc(U_.n);
+  dudt_.alloc(U_.n);
+  U_.zero(stream_);
+  reg_.zero(stream_);
+  trace_.alloc(slots * n2_ * 5);
+  fvn_.alloc(slots * n2_ * 4);
+  trace_.zero(stream_);
+  fvn_.zero(stream_);
+  slide_lift_.alloc(static_cast<size_t>(S_) * n2_ * 4);
+  slide_flux_.alloc(static_cast<size_t>(S_) * n2_ * 5);
+  slide_g_.alloc(static_cast<size_t>(S_) * n2_ * 12);
+  dir_g_.alloc(static_cast<size_t>(ND_) * n2_ * 12);
+  side_type_.upload(topo_.side_type, stream_);
+  side_idx_.upload(topo_.side_idx, stream_);
+  coords_.upload(topo_.coords, stream_);
+  err_.alloc(1);
+  err_.zero(stream_);
+  dt_min_.alloc(1);
+  // Halo send slots (concatenated over peers).
+  std::vector<int> send;
+  for (const auto& p : topo_.peers) send.insert(send.end(), p.send_slots.begin(), p.send_slots.end());
+  send_slots_.upload(send, stream_);
+  send_buf_.alloc(send.size() * n2_ * 5);
+}
+
+// Interface-side contexts (solver.cpp:73-90) and the device pairing tables.
+void GpuRankSolver::build_sides() {
+  const int ni = static_cast<int>(mesh_.ifaces.size());
+  for (int ic = 0; ic < ni; ++ic)
+    for (const bool left : {true, false}) {
+      SideCtx c;
+      c.iface = ic;
+      for (int k = 0; k < S_; ++k) {
+        const auto& r = topo_.sliding[k];
+        if (r.iface == ic && (r.side == 1) == left) c.slides.push_back(k);
+      }
+      if (c.slides.empty()) continue;
+      c.on_static = mesh_.ifaces[ic].static_is_left == left;
+      std::sort(c.slides.begin(), c.slides.end(), [&](int a, int b) {
+        const auto &ra = topo_.sliding[a], &rb = topo_.sliding[b];
+        return ra.i_par != rb.i_par ? ra.i_par < rb.i_par : ra.i_perp < rb.i_perp;
+      });
+      c.fwd.assign(2 * n2_, 0.0);
+      c.bwd.assign(2 * n2_, 0.0);
+      sides_.push_back(std::move(c));
+    }
+  if (sides_.size() > static_cast<size_t>(kMaxCtx)) throw ConfigError("too many interface sides");
+  // Per-sliding-face lookup tables.
+  std::vector<int> s_elem(S_), s_side(S_), s_ctx(S_, -1), s_f(S_, -1);
+  std::vector<int> off(sides_.size()), nf(sides_.size()), role(sides_.size()), sleft(sides_.size());
+  std::vector<int> fpar, fperp, fslide;
+  int o = 0;
+  for (size_t c = 0; c < sides_.size(); ++c) {
+    const auto& sc = sides_[c];
+    off[c] = o;
+    nf[c] = static_cast<int>(sc.slides.size());
+    role[c] = sc.on_static ? 0 : 1;
+    sleft[c] = mesh_.ifaces[sc.iface].static_is_left ? 1 : 0;
+    role_ids_[role[c]].push_back(static_cast<int>(c));
+    for (int f = 0; f < nf[c]; ++f) {
+      const int k = sc.slides[f];
+      s_ctx[k] = static_cast<int>(c);
+      s_f[k] = f;
+      fpar.push_back(static_cast<int>(topo_.sliding[k].i_par));
+      fperp.push_back(static_cast<int>(topo_.sliding[k].i_perp));
+      fslide.push_back(k);
+    }
+    o += nf[c];
+    max_mortars_[role[c]] += 2 * nf[c];
+  }
+  for (int k = 0; k < S_; ++k) {
+    s_elem[k] = topo_.sliding[k].elem;
+    s_side[k] = topo_.sliding[k].side;
+  }
+  slide_elem_.upload(s_elem, stream_);
+  slide_side_.upload(s_side, stream_);
+  slide_ctx_.upload(s_ctx, stream_);
+  slide_f_.upload(s_f, stream_);
+  ctx_face_off_.upload(off, stream_);
+  ctx_nf_.upload(nf, stream_);
+  ctx_role_.upload(role, stream_);
+  ctx_static_left_.upload(sleft, stream_);
+  face_par_.upload(fpar, stream_);
+  face_perp_.upload(fperp, stream_);
+  face_slide_.upload(fslide, stream_);
+  m_.alloc(2 * static_cast<size_t>(std::max(o, 1)));
+  ctx_state_.alloc(2 * kMaxCtx);
+  ctx_state_.zero(stream_);
+  ctx_sdelta_.alloc(kMaxCtx);
+  n_mortars_.alloc(2);
+  n_mortars_.zero(stream_);
+  // Dense key space of the pairing sort.
+  pargs_.n_ctx = static_cast<int>(sides_.size());
+  pargs_.n_ifaces = ni;
+  long long base = 0;
+  for (int ic = 0; ic < ni; ++ic) {
+    pargs_.iface_base[ic] = base;
+    pargs_.iface_nperp[ic] = mesh_.ifaces[ic].n_perp;
+    base += 2LL * mesh_.ifaces[ic].n_faces * mesh_.ifaces[ic].n_perp;
+  }
+  pargs_.dense_size = base;
+  pargs_.self_rank = rank_;
+  for (int r = 0; r < 2; ++r) {
+    pargs_.role_nctx[r] = static_cast<int>(role_ids_[r].size());
+    for (size_t q = 0; q < role_ids_[r].size(); ++q) pargs_.role_ctx[r][q] = role_ids_[r][q];
+    pres_[r].alloc(std::max<long long>(base, 1));
+    payload_[r].alloc(std::max<long long>(base, 1));
+    cols_[r].alloc(7 * static_cast<size_t>(std::max(max_mortars_[r], 1)));
+    const size_t nodes = static_cast<size_t>(std::max(max_mortars_[r], 1)) * n2_;
+    u_mine_[r].alloc(nodes * 5);
+    mlift_[r].alloc(nodes * 4);
+    g_mine_[r].alloc(nodes * 12);
+    mflux_[r].alloc(nodes * 5);
+  }
+  const size_t snodes = static_cast<size_t>(std::max(max_mortars_[0], 1)) * n2_;
+  u_theirs_.alloc(snodes * 5);
+  g_theirs_.alloc(snodes * 12);
+  for (size_t c = 0; c < sides_.size(); ++c) {
+    const auto& ifc = mesh_.ifaces[sides_[c].iface];
+    CtxD& d = pargs_.ctx[c];
+    d.iface = sides_[c].iface;
+    d.on_static = sides_[c].on_static ? 1 : 0;
+    d.role = role[c];
+    d.n_faces = nf[c];
+    d.face_off = off[c];
+    d.n_par = ifc.n_faces;
+    d.n_perp = ifc.n_perp;
+    d.static_is_left = ifc.static_is_left ? 1 : 0;
+    d.l_par = ifc.l_par;
+    d.vg_rel = ifc.vg_rel;
+  }
+}
+
+// The one init-time collective (init_rank_maps, solver.cpp:95-133): every rank
+// contributes (iface, side, i_par, i_perp) of its interface faces; the owner
+// maps r, r~ follow, and each side keeps the map of its partner side.
+void GpuRankSolver::init_rank_maps() {
+  std::vector<int> mine;
+  for (const auto& c : sides_)
+    for (int k : c.slides) {
+      mine.push_back(c.iface);
+      mine.push_back(c.on_static ? 0 : 1);
+      mine.push_back(static_cast<int>(topo_.sliding[k].i_par));
+      mine.push_back(static_cast<int>(topo_.sliding[k].i_perp));
+    }
+  std::vector<std::vector<int>> all(n_ranks_);
+  if (n_ranks_ == 1) {
+    all[0] = mine;
+  } else {
+    // All-gather of the sizes, then of the padded payloads.
+    DevBuf<int> d_cnt, d_all_cnt;
+    d_cnt.alloc(1);
+    d_all_cnt.alloc(n_ranks_);
+    const int cnt = static_cast<int>(mine.size());
+    cuda_check(cudaMemcpyAsync(d_cnt.p, &cnt, sizeof(int), cudaMemcpyHostToDevice, stream_), "h2d");
+    nccl_check(ncclAllGather(d_cnt.p, d_all_cnt.p, 1, ncclInt32, comm_, stream_), "allgather sizes");
+    std::vector<int> counts(n_ranks_);
+    cuda_check(cudaMemcpyAsync(counts.data(), d_all_cnt.p, n_ranks_ * sizeof(int), cudaMemcpyDeviceToHost, stream_),
+               "d2h");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    const int mx = std::max(1, *std::max_element(counts.begin(), counts.end()));
+    std::vector<int> padded(mx, 0);
+    std::copy(mine.begin(), mine.end(), padded.begin());
+    DevBuf<int> d_mine, d_all;
+    d_mine.upload(padded, stream_);
+    d_all.alloc(static_cast<size_t>(mx) * n_ranks_);
+    nccl_check(ncclAllGather(d_mine.p, d_all.p, mx, ncclInt32, comm_, stream_), "allgather maps");
+    std::vector<int> h(static_cast<size_t>(mx) * n_ranks_);
+    cuda_check(cudaMemcpyAsync(h.data(), d_all.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    for (int r = 0; r < n_ranks_; ++r) all[r].assign(h.begin() + r * mx, h.begin() + r * mx + counts[r]);
+  }
+  const int ni = static_cast<int>(mesh_.ifaces.size());
+  std::vector<std::vector<int>> smap(ni), mmap(ni);
+  for (int ic = 0; ic < ni; ++ic) {
+    const size_t sz = static_cast<size_t>(mesh_.ifaces[ic].n_faces * mesh_.ifaces[ic].n_perp);
+    smap[ic].assign(sz, -1);
+    mmap[ic].assign(sz, -1);
+  }
+  for (int r = 0; r < n_ranks_; ++r)
+    for (size_t q = 0; q + 3 < all[r].size(); q += 4) {
+      const int ic = all[r][q];
+      const bool is_static = all[r][q + 1] == 0;
+      const long np = mesh_.ifaces[ic].n_faces;
+      const size_t slot = static_cast<size_t>(all[r][q + 3]) * np + all[r][q + 2];
+      int& owner = (is_static ? smap[ic] : mmap[ic])[slot];
+      if (owner != -1) throw ProtocolError("interface face claimed by two ranks");
+      owner = r;
+    }
+  for (int ic = 0; ic < ni; ++ic)
+    for (const auto* mp : {&smap[ic], &mmap[ic]})
+      for (int r : *mp)
+        if (r < 0) throw ProtocolError("interface face without an owner");
+  std::vector<int> concat;
+  for (size_t c = 0; c < sides_.size(); ++c) {
+    auto& sc = sides_[c];
+    sc.static_map = smap[sc.iface];
+    sc.moving_map = mmap[sc.iface];
+    pargs_.ctx[c].map_off = static_cast<int>(concat.size());
+    const auto& partner = sc.on_static ? sc.moving_map : sc.static_map;
+    concat.insert(concat.end(), partner.begin(), partner.end());
+  }
+  if (concat.empty()) concat.push_back(0);
+  partner_map_.upload(concat, stream_);
+  cuda_check(cudaStreamSynchronize(stream_), "rank maps");
+}
+
+void GpuRankSolver::set_initial_condition(double t0) {
+  time_ = t0;
+  step_index_ = 0;
+  std::vector<double> h(static_cast<size_t>(E_) * n3_ * 5);
+  const int n = n_;
+  for (int e = 0; e < E_; ++e) {
+    const int b = topo_.coords[4 * e], ix = topo_.coords[4 * e + 1], iy = topo_.coords[4 * e + 2],
+              iz = topo_.coords[4 * e + 3];
+    const BandGeom& B = mesh_.bands[b];
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        for (int k = 0; k < n; ++k) {
+          double x[3];
+          x[0] = (B.x_lo + ix * B.hx) + 0.5 * (basis_.x[i] + 1.0) * B.hx;
+          x[1] = (mesh_.spec.y0 + iy * B.hy) + 0.5 * (basis_.x[j] + 1.0) * B.hy + B.vg * t0;
+          x[2] = (mesh_.spec.z0 + iz * B.hz) + 0.5 * (basis_.x[k] + 1.0) * B.hz;
+          eval_case_host(cfg_.flow_case, cfg_.gas, x, t0, h.data() + ((static_cast<size_t>(e) * n3_) + (i * n + j) * n + k) * 5);
+        }
+  }
+  cuda_check(cudaMemcpyAsync(U_.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, stream_), "h2d");
+  reg_.zero(stream_);
+  for (auto& c : sides_) {
+    c.delta_base = mesh_.ifaces[c.iface].vg_rel * t0;
+    c.topo_valid = false;
+  }
+  traces_valid_ = false;
+  cuda_check(cudaStreamSynchronize(stream_), "set_initial_condition");
+}
+
+void GpuRankSolver::set_state(const double* h) {
+  cuda_check(cudaMemcpyAsync(U_.p, h, U_.n * sizeof(double), cudaMemcpyHostToDevice, stream_), "set_state");
+  cuda_check(cudaStreamSynchronize(stream_), "set_state");
+  traces_valid_ = false;
+}
+void GpuRankSolver::get_state(double* h) {
+  cuda_check(cudaMemcpyAsync(h, U_.p, U_.n * sizeof(double), cudaMemcpyDeviceToHost, stream_), "get_state");
+  synchronize();
+}
+void GpuRankSolver::get_register(double* h) {
+  cuda_check(cudaMemcpyAsync(h, reg_.p, reg_.n * sizeof(double), cudaMemcpyDeviceToHost, stream_), "get_register");
+  synchronize();
+}
+
+FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
+  FieldPtrs p{};
+  p.U = U;
+  p.reg = reg_.p;
+  p.out = out;
+  p.trace = trace_.p;
+  p.fvn = fvn_.p;
+  p.slide_lift = slide_lift_.p;
+  p.slide_flux = slide_flux_.p;
+  p.slide_g = slide_g_.p;
+  p.dir_g = dir_g_.p;
+  p.side_type = side_type_.p;
+  p.side_idx = side_idx_.p;
+  p.coords = coords_.p;
+  p.grad_out = nullptr;
+  p.err = err_.p;
+  p.E = E_;
+  return p;
+}
+
+MortarPtrs GpuRankSolver::mortar_ptrs() {
+  MortarPtrs p{};
+  p.trace = trace_.p;
+  for (int r = 0; r < 2; ++r) {
+    p.u_mine[r] = u_mine_[r].p;
+    p.lift[r] = mlift_[r].p;
+    p.g_mine[r] = g_mine_[r].p;
+    p.flux[r] = mflux_[r].p;
+  }
+  p.u_theirs = u_theirs_.p;
+  p.g_theirs = g_theirs_.p;
+  p.slide_lift = slide_lift_.p;
+  p.slide_flux = slide_flux_.p;
+  p.slide_g = slide_g_.p;
+  p.slide_elem = slide_elem_.p;
+  p.slide_side = slide_side_.p;
+  p.slide_ctx = slide_ctx_.p;
+  p.slide_f = slide_f_.p;
+  p.m = m_.p;
+  p.ctx_face_off = ctx_face_off_.p;
+  p.ctx_nf = ctx_nf_.p;
+  p.ctx_role = ctx_role_.p;
+  p.ctx_state = ctx_state_.p;
+  p.n_mortars = n_mortars_.p;
+  p.cols_static = cols_[0].p;
+  p.ctx_static_left = ctx_static_left_.p;
+  p.S = S_;
+  return p;
+}
+
+void GpuRankSolver::mark(int cls, bool begin) {
+  if (!timing_) return;
+  if (begin) {
+    cudaEvent_t a;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, stream_);
+    pending_start_ = a;
+  } else {
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, stream_);
+    events_.push_back({cls, {pending_start_, b}});
+  }
+}
+
+std::vector<std::pair<double, long>> GpuRankSolver::timing_totals() {
+  cuda_check(cudaStreamSynchronize(stream_), "timing sync");
+  for (auto& ev : events_) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev.second.first, ev.second.second);
+    class_ms_[ev.first] += ms;
+    class_n_[ev.first] += 1;
+    cudaEventDestroy(ev.second.first);
+    cudaEventDestroy(ev.second.second);
+  }
+  events_.clear();
+  std::vector<std::pair<double, long>> out;
+  for (int c = 0; c < KC_N; ++c) out.push_back({class_ms_[c], class_n_[c]});
+  for (int c = 0; c < KC_N; ++c) {
+    class_ms_[c] = 0.0;
+    class_n_[c] = 0;
+  }
+  return out;
+}
+
+// update_interfaces (solver.cpp:156-176) on the host: displacement, sigma,
+// long-double operators, topology-change bookkeeping and the per-partner
+// mortar blocks used to size the NCCL messages.
+void GpuRankSolver::update_interfaces_host(double t_stage) {
+  bool changed[2] = {false, false};
+  for (size_t c = 0; c < sides_.size(); ++c) {
+    SideCtx& sc = sides_[c];
+    const IfaceGeom& f = mesh_.ifaces[sc.iface];
+    const double delta = sc.delta_base + f.vg_rel * (t_stage - time_);
+    sc.st = displacement(delta, f.l_par, f.n_faces);
+    sc.conforming = sc.st.conforming();
+    const double sigma = 2.0 * sc.st.s_delta - 1.0;
+    sc.sigma_side = sc.on_static ? sigma : -sigma;
+    if (!sc.conforming && sc.sigma_side != sc.ops_sigma) {
+      build_mortar_ops(basis_, sc.sigma_side, sc.fwd.data(), sc.bwd.data());
+      sc.ops_sigma = sc.sigma_side;
+    }
+    for (int h = 0; h < 2; ++h)
+      for (int q = 0; q < n2_; ++q) {
+        fwd_ops_.op[c][h][(q / n_) * n_ + q % n_] = sc.fwd[h * n2_ + q];
+        bwd_ops_.op[c][h][(q / n_) * n_ + q % n_] = sc.bwd[h * n2_ + q];
+      }
+    if (!sc.topo_valid || sc.st.n_delta != sc.last_n || sc.conforming != sc.last_conf) {
+      sc.topo_valid = true;
+      sc.last_n = sc.st.n_delta;
+      sc.last_conf = sc.conforming;
+      sc.rebuilds++;
+      changed[sc.on_static ? 0 : 1] = true;
+    }
+  }
+  // Per-partner block sizes (build_schedule, partition.cpp:154-169) on a topology change.
+  for (int r = 0; r < 2; ++r) {
+    if (!changed[r]) continue;
+    std::map<int, int> cnt;
+    int total = 0;
+    for (int c : role_ids_[r]) {
+      const SideCtx& sc = sides_[c];
+      const IfaceGeom& f = mesh_.ifaces[sc.iface];
+      const auto& pmap = sc.on_static ? sc.moving_map : sc.static_map;
+      for (int k : sc.slides) {
+        const long ip = topo_.sliding[k].i_par, iq = topo_.sliding[k].i_perp;
+        for (int sub = sc.conforming ? 1 : 0; sub < 2; ++sub) {
+          const long par = sc.on_static ? moving_index(ip, sc.st.n_delta, sub, f.n_faces)
+                                        : static_index(ip, sc.st.n_delta, sub, f.n_faces);
+          cnt[pmap[static_cast<size_t>(iq) * f.n_faces + par]]++;
+          total++;
+        }
+      }
+    }
+    expect_mortars_[r] = total;
+    sched_[r].clear();
+    self_[r] = {rank_, 0, 0};
+    int offp = 0;
+    for (const auto& kv : cnt) {
+      if (kv.first == rank_) self_[r] = {rank_, offp, kv.second};
+      else sched_[r].push_back({kv.first, offp, kv.second});
+      offp += kv.second;
+    }
+  }
+}
+
+void GpuRankSolver::run_pairing(double t_stage) {
+  PairingArgs a = pargs_;
+  for (size_t c = 0; c < sides_.size(); ++c) a.delta_base[c] = sides_[c].delta_base;
+  a.time = time_;
+  a.t_stage = t_stage;
+  a.expect_mortars[0] = expect_mortars_[0];
+  a.expect_mortars[1] = expect_mortars_[1];
+  PairingPtrs p{};
+  p.ctx_face_par = face_par_.p;
+  p.ctx_face_perp = face_perp_.p;
+  p.ctx_face_slide = face_slide_.p;
+  p.partner_map = partner_map_.p;
+  for (int r = 0; r < 2; ++r) {
+    p.pres[r] = pres_[r].p;
+    p.payload[r] = payload_[r].p;
+    p.cols[r] = cols_[r].p;
+  }
+  p.m = m_.p;
+  p.ctx_state = ctx_state_.p;
+  p.ctx_sdelta = ctx_sdelta_.p;
+  p.n_mortars = n_mortars_.p;
+  p.err = err_.p;
+  mark(KC_PAIRING, true);
+  launch_pairing(a, p, stream_);
+  mark(KC_PAIRING, false);
+  launches_++;
+}
+
+// Mortar block exchange between the two roles (send_solution_phase etc.):
+// moving_to_static: src[1] blocks -> dst (static "theirs"); otherwise src[0]
+// blocks -> dst (moving array).  Self blocks are device copies, remote
+// blocks grouped NCCL send/recv in ascending partner order.
+void GpuRankSolver::mortar_exchange(double* const src[2], double* dst, int nc, bool moving_to_static) {
+  const int from = moving_to_static ? 1 : 0, to = 1 - from;
+  const size_t node = static_cast<size_t>(n2_) * nc;
+  const auto& sf = self_[from];
+  const auto& st = self_[to];
+  if (sf[2] > 0) {
+    if (sf[2] != st[2]) throw ProtocolError("loopback mortar block size mismatch");
+    mark(KC_COPY, true);
+    cuda_check(cudaMemcpyAsync(dst + st[1] * node, src[from] + sf[1] * node, sf[2] * node * sizeof(double),
+                               cudaMemcpyDeviceToDevice, stream_),
+               "self mortar copy");
+    mark(KC_COPY, false);
+  }
+  if (n_ranks_ == 1) return;
+  if (sched_[from].empty() && sched_[to].empty()) return;
+  mark(KC_HALO, true);
+  nccl_check(ncclGroupStart(), "group start");
+  for (const auto& e : sched_[from])
+    nccl_check(ncclSend(src[from] + e[1] * node, e[2] * node, ncclFloat64, e[0], comm_, stream_), "send");
+  for (const auto& e : sched_[to])
+    nccl_check(ncclRecv(dst + e[1] * node, e[2] * node, ncclFloat64, e[0], comm_, stream_), "recv");
+  nccl_check(ncclGroupEnd(), "group end");
+  mark(KC_HALO, false);
+}
+
+// Conforming halo exchange of face data (traces or Fv.n): gather the local
+// slots facing each peer, then grouped NCCL send/recv straight into the halo
+// slots (contiguous per peer by construction).
+__global__ void k_gather_slots(const double* src, const int* slots, int n_slots, int per_slot, double* dst) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(n_slots) * per_slot) return;
+  const int s = static_cast<int>(i / per_slot), q = static_cast<int>(i % per_slot);
+  dst[i] = src[static_cast<size_t>(slots[s]) * per_slot + q];
+}
+
+void GpuRankSolver::halo_exchange(double* arr, int nc) {
+  if (n_ranks_ == 1 || topo_.peers.empty()) return;
+  const int per = n2_ * nc;
+  const int ns = static_cast<int>(send_slots_.n);
+  mark(KC_HALO, true);
+  k_gather_slots<<<(ns * per + 255) / 256, 256, 0, stream_>>>(arr, send_slots_.p, ns, per, send_buf_.p);
+  launches_++;
+  nccl_check(ncclGroupStart(), "group start");
+  size_t off = 0;
+  for (const auto& p : topo_.peers) {
+    const size_t cnt = p.send_slots.size() * per;
+    nccl_check(ncclSend(send_buf_.p + off, cnt, ncclFloat64, p.partner, comm_, stream_), "halo send");
+    nccl_check(ncclRecv(arr + static_cast<size_t>(p.recv_slots.front()) * per, p.recv_slots.size() * per,
+                        ncclFloat64, p.partner, comm_, stream_),
+               "halo recv");
+    off += cnt;
+  }
+  nccl_check(ncclGroupEnd(), "group end");
+  mark(KC_HALO, false);
+}
+
+// One right-hand-side evaluation (compute_residual, solver.cpp:846-870) with
+// the RK update fused into the last kernel when mode == 0.
+void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, double dt, double* out,
+                          const double* u_override) {
+  double* U = u_override ? const_cast<double*>(u_override) : U_.p;
+  update_interfaces_host(t_stage);
+  run_pairing(t_stage);
+  const FieldPtrs fp = field_ptrs(U, out);
+  if (!traces_valid_ || u_override) {
+    mark(KC_PROLONG, true);
+    launch_prolong(n_, consts_, fp, stream_);
+    mark(KC_PROLONG, false);
+    launches_++;
+  }
+  halo_exchange(trace_.p, 5);
+  const MortarPtrs mp = mortar_ptrs();
+  double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
+  mark(KC_MORTAR, true);
+  launch_mortar_fill(n_, 5, trace_.p, u_src, fwd_ops_, mp, stream_);
+  mark(KC_MORTAR, false);
+  launches_ += S_ > 0;
+  mortar_exchange(u_src, u_theirs_.p, 5, true);
+  StageArgs a{t_stage, dt, rk_a, rk_b, mode, step_index_, stage_index_};
+  if (lifting_) {
+    mark(KC_MORTAR, true);
+    launch_mortar_lift(n_, consts_.gas, mp, max_mortars_[0], stream_);
+    mark(KC_MORTAR, false);
+    launches_ += max_mortars_[0] > 0;
+    double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
+    mortar_exchange(l_src, mlift_[1].p, 4, false);
+    mark(KC_MORTAR, true);
+    launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
+    mark(KC_MORTAR, false);
+    launches_ += S_ > 0;
+    mark(KC_GRADIENT, true);
+    launch_gradient(n_, consts_, fp, a, stream_);
+    mark(KC_GRADIENT, false);
+    launches_++;
+    halo_exchange(fvn_.p, 4);
+    double* const g_src[2] = {g_mine_[0].p, g_mine_[1].p};
+    mark(KC_MORTAR, true);
+    launch_mortar_fill(n_, 12, slide_g_.p, g_src, fwd_ops_, mp, stream_);
+    mark(KC_MORTAR, false);
+    launches_ += S_ > 0;
+    mortar_exchange(g_src, g_theirs_.p, 12, true);
+  }
+  mark(KC_MORTAR, true);
+  launch_mortar_flux(n_, consts_.gas, lifting_ ? 1 : 0, mp, max_mortars_[0], err_.p, stream_);
+  mark(KC_MORTAR, false);
+  launches_ += max_mortars_[0] > 0;
+  double* const f_src[2] = {mflux_[0].p, mflux_[1].p};
+  mortar_exchange(f_src, mflux_[1].p, 5, false);
+  mark(KC_MORTAR, true);
+  launch_mortar_backproject(n_, 5, f_src, slide_flux_.p, bwd_ops_, mp, stream_);
+  mark(KC_MORTAR, false);
+  launches_ += S_ > 0;
+  mark(KC_UPDATE, true);
+  launch_update(n_, consts_, fp, a, stream_);
+  mark(KC_UPDATE, false);
+  launches_++;
+  traces_valid_ = (mode == 0 && !u_override);
+}
+
+void GpuRankSolver::check_error() {
+  cuda_check(cudaMemcpyAsync(err_host_, err_.p, sizeof(ErrRec), cudaMemcpyDeviceToHost, stream_), "err d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+  if (err_host_->flag == 0) return;
+  const ErrRec r = *err_host_;
+  err_.zero(stream_);
+  cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+  std::ostringstream os;
+  if (r.flag == 3) {
+    os << "device pairing disagrees with the host schedule (role " << r.elem << ", " << r.node << " mortars)";
+    throw ProtocolError(os.str());
+  }
+  if (r.node < 0) {
+    os << "roe_flux: nonpositive Roe enthalpy average in element gid=" << (r.elem >= 0 ? topo_.gids[r.elem] : -1)
+       << " at step " << r.step << " stage " << r.stage;
+  } else {
+    os << "inadmissible state in element gid=" << (r.elem >= 0 ? topo_.gids[r.elem] : -1) << " node " << r.node
+       << " at step " << r.step << " stage " << r.stage << ": [" << r.vals[0] << ", " << r.vals[1] << ", "
+       << r.vals[2] << ", " << r.vals[3] << ", " << r.vals[4] << "]";
+  }
+  throw InvalidStateError(os.str());
+}
+
+void GpuRankSolver::synchronize() { check_error(); }
+
+// step (solver.cpp:908-927), n times without host synchronisation.
+void GpuRankSolver::steps(double dt, int n, bool sync) {
+  for (int it = 0; it < n; ++it) {
+    for (int s = 0; s < 5; ++s) {
+      stage_index_ = s;
+      stage(time_ + RK_C[s] * dt, 0, RK_A[s], RK_B[s], dt, nullptr, nullptr);
+    }
+    time_ += dt;
+    step_index_++;
+    for (auto& c : sides_) {
+      const IfaceGeom& f = mesh_.ifaces[c.iface];
+      c.delta_base += f.vg_rel * dt;
+      const double period = f.l_par * static_cast<double>(f.n_faces);
+      while (c.delta_base >= period) c.delta_base -= period;
+    }
+  }
+  if (sync) check_error();
+}
+
+void GpuRankSolver::compute_residual(double t_stage, const double* d_u, double* d_dudt) {
+  stage(t_stage, 1, 0.0, 0.0, 0.0, d_dudt, d_u == U_.p ? nullptr : d_u);
+  traces_valid_ = false;
+  check_error();
+}
+
+void GpuRankSolver::compute_gradients(double t_stage, const double* d_u, double* d_grad) {
+  double* U = const_cast<double*>(d_u);
+  update_interfaces_host(t_stage);
+  run_pairing(t_stage);
+  FieldPtrs fp = field_ptrs(U, nullptr);
+  launch_prolong(n_, consts_, fp, stream_);
+  halo_exchange(trace_.p, 5);
+  const MortarPtrs mp = mortar_ptrs();
+  double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
+  launch_mortar_fill(n_, 5, trace_.p, u_src, fwd_ops_, mp, stream_);
+  mortar_exchange(u_src, u_theirs_.p, 5, true);
+  launch_mortar_lift(n_, consts_.gas, mp, max_mortars_[0], stream_);
+  double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
+  mortar_exchange(l_src, mlift_[1].p, 4, false);
+  launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
+  fp.grad_out = d_grad;
+  ElemConsts c = consts_;
+  c.gas.viscous = 1;
+  StageArgs a{t_stage, 0.0, 0.0, 0.0, 1, step_index_, stage_index_};
+  launch_gradient(n_, c, fp, a, stream_);
+  launches_ += 6;
+  traces_valid_ = false;
+  check_error();
+}
+
+double GpuRankSolver::suggest_dt(double cfl) {
+  const unsigned long long init = 0x7fefffffffffffffULL;  // DBL_MAX bits
+  cuda_check(cudaMemcpyAsync(dt_min_.p, &init, sizeof(init), cudaMemcpyHostToDevice, stream_), "h2d");
+  launch_suggest_dt(n_, consts_, field_ptrs(U_.p, nullptr), cfl, basis_.degree, dt_min_.p, stream_);
+  launches_++;
+  unsigned long long bits = 0;
+  cuda_check(cudaMemcpyAsync(&bits, dt_min_.p, sizeof(bits), cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  double dt;
+  std::memcpy(&dt, &bits, sizeof(dt));
+  if (n_ranks_ > 1) {
+    DevBuf<double> d;
+    d.alloc(1);
+    cuda_check(cudaMemcpyAsync(d.p, &dt, sizeof(dt), cudaMemcpyHostToDevice, stream_), "h2d");
+    nccl_check(ncclAllReduce(d.p, d.p, 1, ncclFloat64, ncclMin, comm_, stream_), "allreduce dt");
+    cuda_check(cudaMemcpyAsync(&dt, d.p, sizeof(dt), cudaMemcpyDeviceToHost, stream_), "d2h");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+  }
+  return dt;
+}
+
+void GpuRankSolver::ctx_info(int c, long* out5, double* sd, double* sig) {
+  if (c < 0 || c >= static_cast<int>(sides_.size())) throw ConfigError("no such interface side context");
+  int st[2 * kMaxCtx];
+  double sdv[kMaxCtx];
+  cuda_check(cudaMemcpyAsync(st, ctx_state_.p, sizeof(st), cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaMemcpyAsync(sdv, ctx_sdelta_.p, sizeof(sdv), cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  out5[0] = sides_[c].iface;
+  out5[1] = sides_[c].on_static ? 1 : 0;
+  out5[2] = st[2 * c];
+  out5[3] = st[2 * c + 1];
+  out5[4] = static_cast<long>(sides_[c].slides.size());
+  *sd = sdv[c];
+  const double sigma = 2.0 * sdv[c] - 1.0;
+  *sig = sides_[c].on_static ? sigma : -sigma;
+}
+
+void GpuRankSolver::get_pairing(int role, int* ncols, int* cols) {
+  if (role < 0 || role > 1) throw ConfigError("role must be 0 (static) or 1 (moving)");
+  int nm[2];
+  cuda_check(cudaMemcpyAsync(nm, n_mortars_.p, sizeof(nm), cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  *ncols = nm[role];
+  if (cols && nm[role] > 0) {
+    cuda_check(cudaMemcpyAsync(cols, cols_[role].p, sizeof(int) * 7 * nm[role], cudaMemcpyDeviceToHost, stream_),
+               "d2h");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+  }
+}
+
+void GpuRankSolver::get_mapping(int c, int* m) {
+  if (c < 0 || c >= static_cast<int>(sides_.size())) throw ConfigError("no such interface side context");
+  const int nf = static_cast<int>(sides_[c].slides.size());
+  const int off = pargs_.ctx[c].face_off;
+  cuda_check(cudaMemcpyAsync(m, m_.p + 2 * off, sizeof(int) * 2 * nf, cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+}
+
+// Stand-alone device pairing on caller-given faces (Appendix-A fixture).
+static void device_pairing(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,
+                           long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
+                           int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry) {
+  cudaStream_t st;
+  cuda_check(cudaStreamCreate(&st), "stream");
+  PairingArgs a{};
+  a.n_ctx = 1;
+  a.n_ifaces = 1;
+  a.iface_base[0] = 0;
+  a.iface_nperp[0] = n_perp;
+  a.dense_size = 2LL * n_par * n_perp;
+  a.self_rank = self_rank;
+  const int role = on_static ? 0 : 1;
+  a.role_nctx[role] = 1;
+  a.role_ctx[role][0] = 0;
+  a.role_nctx[1 - role] = 0;
+  CtxD& c = a.ctx[0];
+  c.iface = 0;
+  c.on_static = on_static;
+  c.role = role;
+  c.n_faces = n_local;
+  c.face_off = 0;
+  c.map_off = 0;
+  c.n_par = n_par;
+  c.n_perp = n_perp;
+  c.l_par = 1.0;
+  c.vg_rel = 0.0;
+  // Displacement chain reproduces (n_delta, conforming): delta = n_delta (+ 0.5 if hanging).
+  a.delta_base[0] = static_cast<double>(n_delta) + (conforming ? 0.0 : 0.5);
+  a.time = 0.0;
+  a.t_stage = 0.0;
+  a.expect_mortars[0] = a.expect_mortars[1] = -1;
+  std::vector<int> fpar(n_local), fperp(n_local), fsl(n_local);
+  for (int f = 0; f < n_local; ++f) {
+    fpar[f] = static_cast<int>(faces[3 * f + 1]);
+    fperp[f] = static_cast<int>(faces[3 * f + 2]);
+    fsl[f] = f;
+  }
+  DevBuf<int> d_par, d_perp, d_sl, d_map, d_pres, d_pay, d_cols, d_m, d_state, d_nm, d_dummy;
+  DevBuf<double> d_sd;
+  DevBuf<ErrRec> d_err;
+  d_par.upload(fpar, st);
+  d_perp.upload(fperp, st);
+  d_sl.upload(fsl, st);
+  d_map.upload(std::vector<int>(partner_ranks, partner_ranks + n_par * n_perp), st);
+  d_pres.alloc(a.dense_size);
+  d_pay.alloc(a.dense_size);
+  d_cols.alloc(7 * static_cast<size_t>(2 * n_local + 1));
+  d_dummy.alloc(7);
+  d_m.alloc(2 * static_cast<size_t>(n_local) + 1);
+  d_state.alloc(2 * kMaxCtx);
+  d_sd.alloc(kMaxCtx);
+  d_nm.alloc(2);
+  d_nm.zero(st);
+  d_err.alloc(1);
+  d_err.zero(st);
+  PairingPtrs p{};
+  p.ctx_face_par = d_par.p;
+  p.ctx_face_perp = d_perp.p;
+  p.ctx_face_slide = d_sl.p;
+  p.partner_map = d_map.p;
+  p.pres[0] = p.pres[1] = d_pres.p;
+  p.payload[0] = p.payload[1] = d_pay.p;
+  p.cols[role] = d_cols.p;
+  p.cols[1 - role] = d_dummy.p;
+  p.m = d_m.p;
+  p.ctx_state = d_state.p;
+  p.ctx_sdelta = d_sd.p;
+  p.n_mortars = d_nm.p;
+  p.err = d_err.p;
+  launch_pairing(a, p, st);
+  int nm[2];
+  ErrRec er;
+  cuda_check(cudaMemcpyAsync(nm, d_nm.p, sizeof(nm), cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaMemcpyAsync(&er, d_err.p, sizeof(er), cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  std::vector<int> hc(7 * static_cast<size_t>(std::max(nm[role], 1))), hm(2 * static_cast<size_t>(n_local) + 1);
+  cuda_check(cudaMemcpy(hc.data(), d_cols.p, sizeof(int) * 7 * nm[role], cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(hm.data(), d_m.p, sizeof(int) * 2 * n_local, cudaMemcpyDeviceToHost), "d2h");
+  cudaStreamDestroy(st);
+  if (er.flag != 0) throw ProtocolError("rank map lookup hit an unset entry");
+  // Caller face ids ride along passively (build_mapping, partition.cpp:124-141).
+  long lo = 0, hi = -1;
+  if (n_local > 0) {
+    lo = hi = faces[0];
+    for (int f = 0; f < n_local; ++f) {
+      lo = std::min(lo, faces[3 * f]);
+      hi = std::max(hi, faces[3 * f]);
+    }
+  }
+  *face_lo = lo;
+  const long w = hi - lo + 1;
+  for (long q = 0; q < 2 * w; ++q) m_rows[q] = -1;
+  *ncols = nm[role];
+  for (int i = 0; i < nm[role]; ++i) {
+    int* o = cols + 7 * i;
+    for (int q = 0; q < 7; ++q) o[q] = hc[7 * i + q];
+    const int f = o[5];
+    o[5] = static_cast<int>(faces[3 * f]);
+    o[6] = 0;
+    m_rows[o[4] * w + (faces[3 * f] - lo)] = i;
+  }
+  int ns = 0;
+  self_entry[0] = self_rank;
+  self_entry[1] = 0;
+  self_entry[2] = 0;
+  for (int i = 0; i < nm[role]; ++i) {
+    const int p = cols[7 * i];
+    if (p == self_rank) {
+      if (self_entry[2] == 0) self_entry[1] = i;
+      self_entry[2]++;
+      continue;
+    }
+    if (ns == 0 || sched[3 * (ns - 1)] != p) {
+      sched[3 * ns] = p;
+      sched[3 * ns + 1] = i;
+      sched[3 * ns + 2] = 0;
+      ns++;
+    }
+    sched[3 * (ns - 1) + 2]++;
+  }
+  *nsched = ns;
+}
+
+}  // namespace sdg
+
+// ============================================================================
+// C-ABI (include/sdg_gpu.h)
+// ============================================================================
+using sdg::GpuRankSolver;
+
+struct sdg_ctx {
+  GpuRankSolver* s;
+};
+
+namespace {
+thread_local std::string g_error;
+
+template <class F>
+int guarded(const sdg_ctx* c, F&& fn) {
+  std::string* sink = c && c->s ? &c->s->err : &g_error;
+  try {
+    fn();
+    return SDG_OK;
+  } catch (const sdg::ConfigError& e) {
+    *sink = e.what();
+    return SDG_ERR_CONFIG;
+  } catch (const sdg::InvalidStateError& e) {
+    *sink = e.what();
+    return SDG_ERR_INVALID_STATE;
+  } catch (const sdg::ProtocolError& e) {
+    *sink = e.what();
+    return SDG_ERR_PROTOCOL;
+  } catch (const sdg::DeviceError& e) {
+    *sink = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    *sink = e.what();
+    return SDG_ERR_CONFIG;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int sdg_create(const sdg_mesh_spec* mesh, const sdg_solver_config* cfg, int n_ranks, int rank, int device,
+               const void* nccl_id, sdg_ctx** out) {
+  return guarded(nullptr, [&] {
+    if (!mesh || !cfg || !out) throw sdg::ConfigError("null argument");
+    auto* c = new sdg_ctx{nullptr};
+    try {
+      c->s = new GpuRankSolver(*mesh, *cfg, n_ranks, rank, device, nccl_id);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+void sdg_destroy(sdg_ctx* c) {
+  if (!c) return;
+  delete c->s;
+  delete c;
+}
+const char* sdg_last_error(const sdg_ctx* c) { return c && c->s ? c->s->err.c_str() : g_error.c_str(); }
+const char* sdg_global_error(void) { return g_error.c_str(); }
+int sdg_nccl_unique_id(void* out) {
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    sdg::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+int sdg_init_rank_maps(sdg_ctx* c) {
+  return guarded(c, [&] { c->s->init_rank_maps(); });
+}
+int sdg_set_initial_condition(sdg_ctx* c, double t0) {
+  return guarded(c, [&] { c->s->set_initial_condition(t0); });
+}
+int sdg_n1(const sdg_ctx* c) { return c->s->n1(); }
+long sdg_n_local_elements(const sdg_ctx* c) { return c->s->n_local(); }
+long sdg_n_global_elements(const sdg_ctx* c) { return c->s->n_global(); }
+int sdg_local_element_ids(const sdg_ctx* c, long* gids) {
+  std::copy(c->s->gids().begin(), c->s->gids().end(), gids);
+  return SDG_OK;
+}
+int sdg_set_state(sdg_ctx* c, const double* h) {
+  return guarded(c, [&] { c->s->set_state(h); });
+}
+int sdg_get_state(sdg_ctx* c, double* h) {
+  return guarded(c, [&] { c->s->get_state(h); });
+}
+int sdg_get_register(sdg_ctx* c, double* h) {
+  return guarded(c, [&] { c->s->get_register(h); });
+}
+int sdg_state_device_ptr(sdg_ctx* c, double** d) {
+  *d = c->s->d_state();
+  return SDG_OK;
+}
+int sdg_step(sdg_ctx* c, double dt) {
+  return guarded(c, [&] { c->s->steps(dt, 1, true); });
+}
+int sdg_steps(sdg_ctx* c, double dt, int n) {
+  return guarded(c, [&] { c->s->steps(dt, n, true); });
+}
+int sdg_steps_async(sdg_ctx* c, double dt, int n) {
+  return guarded(c, [&] { c->s->steps(dt, n, false); });
+}
+int sdg_synchronize(sdg_ctx* c) {
+  return guarded(c, [&] { c->s->synchronize(); });
+}
+int sdg_compute_residual(sdg_ctx* c, double t, const double* d_u, double* d_dudt) {
+  return guarded(c, [&] { c->s->compute_residual(t, d_u, d_dudt); });
+}
+int sdg_compute_residual_host(sdg_ctx* c, double t, const double* h_u, double* h_dudt) {
+  return guarded(c, [&] {
+    const size_t n = static_cast<size_t>(c->s->n_local()) * c->s->n1() * c->s->n1() * c->s->n1() * 5;
+    double *du = nullptr, *dd = nullptr;
+    sdg::cuda_check(cudaMalloc(&du, n * sizeof(double)), "malloc");
+    sdg::cuda_check(cudaMalloc(&dd, n * sizeof(double)), "malloc");
+    try {
+      sdg::cuda_check(cudaMemcpy(du, h_u, n * sizeof(double), cudaMemcpyHostToDevice), "h2d");
+      c->s->compute_residual(t, du, dd);
+      sdg::cuda_check(cudaMemcpy(h_dudt, dd, n * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    } catch (...) {
+      cudaFree(du);
+      cudaFree(dd);
+      throw;
+    }
+    cudaFree(du);
+    cudaFree(dd);
+  });
+}
+int sdg_compute_gradients_host(sdg_ctx* c, double t, const double* h_u, double* h_grad) {
+  return guarded(c, [&] {
+    const size_t nodes = static_cast<size_t>(c->s->n_local()) * c->s->n1() * c->s->n1() * c->s->n1();
+    double *du = nullptr, *dg = nullptr;
+    sdg::cuda_check(cudaMalloc(&du, nodes * 5 * sizeof(double)), "malloc");
+    sdg::cuda_check(cudaMalloc(&dg, nodes * 12 * sizeof(double)), "malloc");
+    try {
+      sdg::cuda_check(cudaMemcpy(du, h_u, nodes * 5 * sizeof(double), cudaMemcpyHostToDevice), "h2d");
+      c->s->compute_gradients(t, du, dg);
+      sdg::cuda_check(cudaMemcpy(h_grad, dg, nodes * 12 * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    } catch (...) {
+      cudaFree(du);
+      cudaFree(dg);
+      throw;
+    }
+    cudaFree(du);
+    cudaFree(dg);
+  });
+}
+int sdg_suggest_dt(sdg_ctx* c, double cfl, double* dt) {
+  return guarded(c, [&] { *dt = c->s->suggest_dt(cfl); });
+}
+int sdg_time(const sdg_ctx* c, double* t, int* step) {
+  if (t) *t = c->s->time();
+  if (step) *step = c->s->step_index();
+  return SDG_OK;
+}
+long sdg_total_rebuilds(const sdg_ctx* c) { return c->s->total_rebuilds(); }
+int sdg_n_contexts(const sdg_ctx* c) { return c->s->n_contexts(); }
+int sdg_ctx_info(sdg_ctx* c, int id, long* out5, double* sd, double* sig) {
+  return guarded(c, [&] { c->s->ctx_info(id, out5, sd, sig); });
+}
+int sdg_get_pairing(sdg_ctx* c, int role, int* ncols, int* cols) {
+  return guarded(c, [&] { c->s->get_pairing(role, ncols, cols); });
+}
+int sdg_get_mapping(sdg_ctx* c, int id, int* m) {
+  return guarded(c, [&] { c->s->get_mapping(id, m); });
+}
+int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,
+                       long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
+                       int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry) {
+  return guarded(nullptr, [&] {
+    sdg::device_pairing(n_local, faces, n_par, n_perp, partner_ranks, n_delta, on_static, conforming, self_rank,
+                        ncols, cols, m_rows, face_lo, nsched, sched, self_entry);
+  });
+}
+void* sdg_stream(sdg_ctx* c) { return c->s->stream(); }
+long sdg_kernel_launches(const sdg_ctx* c) { return c->s->launches(); }
+int sdg_enable_kernel_timing(sdg_ctx* c, int on) {
+  c->s->enable_timing(on != 0);
+  return SDG_OK;
+}
+int sdg_kernel_timing(sdg_ctx* c, char* names, int names_cap, double* ms, long* launches, int cap, int* n_classes) {
+  return guarded(c, [&] {
+    const auto t = c->s->timing_totals();
+    std::string nm;
+    for (int k = 0; k < static_cast<int>(t.size()); ++k) {
+      if (k) nm += ",";
+      nm += sdg::kKernelClasses[k];
+      if (k < cap) {
+        ms[k] = t[k].first;
+        launches[k] = t[k].second;
+      }
+    }
+    *n_classes = static_cast<int>(t.size());
+    if (names && names_cap > 0) {
+      std::strncpy(names, nm.c_str(), names_cap - 1);
+      names[names_cap - 1] = 0;
+    }
+  });
+}
+
+}  // extern "C"

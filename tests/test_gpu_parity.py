@@ -1,0 +1,186 @@
+"""CUDA path vs the 3D CPU oracle, through the C-ABI.
+
+Tolerances (north star): fp64 state relative Linf <= 1e-12 after one stage /
+step, <= 1e-10 after 100 stages; residuals compared relative to their own
+scale at 1e-12 (absolute 1e-12 for free-stream noise); pairing bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel_linf
+from oracle import pyoracle as P
+from paper_2008_04356_b200 import types as T
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_solver(mesh, cfg):
+    from paper_2008_04356_b200.capi import RankSolver
+    return RankSolver(mesh, cfg)
+
+
+def three_band(ny=6, nz=2, vg=1.0, nx=2):
+    return T.mesh_spec([(nx, 1.0, 0.0), (nx, 1.0, vg), (nx, 1.0, 0.0)], ny=ny, nz=nz, depth=1.0)
+
+
+def box0(n_per=4):
+    # BASELINE config [0]: [0,2]^3 split at the interface, upper block sliding +0.5,
+    # Dirichlet across the split axis (x here), periodic along the slide and the third axis.
+    return T.mesh_spec([(n_per, 1.0, 0.0), (n_per, 1.0, 0.5)], ny=n_per, nz=n_per, periodic=(False, True, True))
+
+
+CASES = {
+    "dw3band_lgl_inv": (three_band(), dict(degree=3, node_kind=T.NODES_LGL, mu=0.0)),
+    "dw3band_gauss_visc": (three_band(), dict(degree=3, node_kind=T.NODES_GAUSS, mu=1e-3)),
+    "box0_gauss_visc": (box0(2), dict(degree=3, node_kind=T.NODES_GAUSS, mu=1e-3)),
+    "box0_lgl_visc_n5": (box0(2), dict(degree=5, node_kind=T.NODES_LGL, mu=1e-3)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("t", [0.0, 0.05, 0.37])
+def test_residual_matches_oracle(name, t):
+    mesh, kw = CASES[name]
+    cfg = T.solver_config(case=T.density_wave(), **kw)
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    u = o.field()
+    rg, ro = g.compute_residual(t, u), o.compute_residual(t, u)
+    assert rel_linf(rg, ro) <= 1e-12
+
+
+@pytest.mark.parametrize("degree", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("kind", [T.NODES_LGL, T.NODES_GAUSS])
+def test_all_degrees_one_step(degree, kind):
+    mesh = three_band(ny=3, nz=2)
+    cfg = T.solver_config(degree, kind, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.4)
+    assert abs(g.suggest_dt(0.4) - dt) <= 1e-14 * dt
+    g.step(dt)
+    o.step(dt)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+def test_hundred_stages_box0():
+    mesh = box0(2)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 20)
+    o.step(dt, 20)
+    assert rel_linf(g.field(), o.field()) <= 1e-10
+    assert g.total_rebuilds() == o.total_rebuilds()
+
+
+def test_pairing_bit_exact_every_stage():
+    mesh = three_band(ny=6, nz=3)
+    cfg = T.solver_config(2, T.NODES_GAUSS, mu=0.0, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    u = o.field()
+    for t in [0.0, 0.05, 1.0 / 3.0, 0.37, 0.99, 2.0, 5.0 + 1e-9]:
+        g.compute_residual(t, u)
+        o.compute_residual(t, u)
+        for role in (0, 1):
+            assert np.array_equal(g.pairing(role), o.pairing(role))
+        for c in range(o.n_contexts()):
+            ig, io = g.ctx_info(c), o.ctx_info(c)
+            assert (ig["n_delta"], ig["conforming"], ig["s_delta"]) == (io["n_delta"], io["conforming"], io["s_delta"])
+            assert np.array_equal(g.mapping(c), o.mapping(c))
+
+
+@pytest.mark.parametrize("kind", [T.NODES_LGL, T.NODES_GAUSS])
+@pytest.mark.parametrize("mu", [0.0, 1e-3])
+def test_freestream_preserved_across_sliding(kind, mu):
+    mesh = three_band(ny=6, nz=2)
+    cfg = T.solver_config(4, kind, mu=mu, case=T.freestream(v=(1.0, 0.5, 0.25)))
+    g = gpu_solver(mesh, cfg)
+    g.set_initial_condition(0.0)
+    for t in [0.0, 0.05, 1.0 / 3.0, 0.37, 0.99, 2.0, 5.0 + 1e-9]:
+        assert np.abs(g.compute_residual(t)).max() < 1e-12
+
+
+def test_conservation_sliding_density_wave():
+    mesh = three_band(ny=6, nz=2)
+    cfg = T.solver_config(3, T.NODES_LGL, mu=0.0, case=T.density_wave(a=(1.0, 1.0, 0.5)))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    before = o.mass_energy(g.field())
+    g.step(0.008, 10)
+    after = o.mass_energy(g.field())
+    assert np.all(np.abs(after - before) / np.abs(before) < 1e-12)
+
+
+def test_dirichlet_all_sides():
+    mesh = T.mesh_spec([(3, 1.0, 0.0)], ny=3, nz=3, periodic=(False, False, False))
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.1)
+    o.set_initial_condition(0.1)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 2)
+    o.step(dt, 2)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+def test_gradients_match_oracle():
+    mesh = three_band(ny=4, nz=2)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    u = o.field()
+    gg, go = g.compute_gradients(0.21, u), o.compute_gradients(0.21, u)
+    assert rel_linf(gg, go) <= 1e-12
+
+
+def test_tgv_three_blocks():
+    L = 2 * math.pi
+    mesh = T.mesh_spec([(2, 1.0, 0.0), (2, 1.0, 0.2), (2, 1.0, 0.0)], ny=3, nz=3, width=L, height=L, depth=L)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 2)
+    o.step(dt, 2)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+def test_positivity_violation_raises():
+    mesh = three_band(ny=3, nz=1)
+    cfg = T.solver_config(2, T.NODES_LGL, case=T.freestream())
+    g = gpu_solver(mesh, cfg)
+    g.set_initial_condition(0.0)
+    u = g.field()
+    u[0] = -1.0
+    g.set_state(u)
+    with pytest.raises(T.InvalidStateError):
+        g.step(1e-6)
+
+
+def test_appendix_a_device_pairing():
+    # Worked sorting example, proj/tests/test_partition.cpp:23-53 and :110-150 (Appendix A).
+    faces = [(5, 4, 1), (6, 4, 2), (7, 5, 1), (8, 3, 2), (9, 3, 1)]
+    ranks = np.full((3, 6), 9, dtype=np.int32)
+    for (ip, iq, r) in [(1, 1, 7), (2, 1, 7), (3, 1, 4), (4, 1, 4), (1, 2, 7), (2, 2, 4), (3, 2, 4), (4, 2, 4)]:
+        ranks[iq, ip] = r
+    from paper_2008_04356_b200.capi import pairing_device
+    out = pairing_device(faces, 6, 3, ranks, 1, True, False, 0)
+    cols = out["cols"]
+    assert list(cols[:, 0]) == [4, 4, 4, 4, 4, 4, 7, 7, 7, 7]
+    assert list(cols[:, 2]) == [3, 4, 4, 4, 5, 5, 3, 3, 3, 4]
+    assert list(cols[:, 3]) == [2, 1, 2, 2, 1, 1, 1, 1, 2, 1]
+    assert list(cols[:, 4]) == [1, 1, 0, 1, 0, 1, 0, 1, 0, 0]
+    assert list(cols[:, 5]) == [8, 5, 6, 6, 7, 7, 9, 9, 8, 5]
+    assert out["face_lo"] == 5
+    assert list(out["m"][0] + 1) == [10, 3, 5, 9, 7]
+    assert list(out["m"][1] + 1) == [2, 4, 6, 1, 8]
+    assert out["sched"].tolist() == [[4, 0, 6], [7, 6, 4]]
+    assert out["self_entry"][2] == 0
