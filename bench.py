@@ -1,0 +1,329 @@
+"""Benchmark of the B200 sliding-mesh DG right-hand side + RK step.
+
+Workload (BASELINE.json configs[4], the largest configuration the reference's
+algorithm covers on one GPU — configs[1]-[3] need non-matching / oblique /
+curved / rotating interfaces that neither the reference nor this round
+implements): Taylor-Green vortex in [0, 2pi]^3 at M=0.1,
+Re=1600, three blocks stacked along BASELINE z with two planar sliding
+interfaces at 2pi/3 and 4pi/3, middle block sliding at +0.2 along BASELINE x;
+64^3 elements per GPU, N=5 Gauss nodes, fp64, viscous.  One "step" = one
+5-stage low-storage RK step (5 right-hand sides + mortars + updates).
+
+metric: DOF-updates/s = E*(N+1)^3 * 5 * steps / time, whole job over all GPUs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "DOF-updates/s (1/PID) per GPU, DG RHS+sliding mortars, 1/2/4/8 B200"
+UNIT = "DOF-updates/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--degree", type=int, default=5)
+    p.add_argument("--elems", type=int, default=64, help="elements per direction per GPU (weak scaling)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def tgv_mesh(T, elems_x, elems_yz):
+    """Three blocks along x (= BASELINE z); interfaces at 2pi/3, 4pi/3."""
+    L = 2.0 * math.pi
+    base, rem = divmod(elems_x, 3)
+    n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
+    bands = [(n[0], 1.0, 0.0), (n[1], 1.0, 0.2), (n[2], 1.0, 0.0)]
+    return T.mesh_spec(bands, ny=elems_yz, nz=elems_yz, width=L, height=L, depth=L), bands
+
+
+def workload(args, world):
+    from paper_2008_04356_b200 import types as T
+    mesh, bands = tgv_mesh(T, args.elems * world, args.elems)
+    cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
+    n1 = args.degree + 1
+    E = sum(b[0] for b in bands) * args.elems * args.elems
+    conf = {
+        "workload": f"BASELINE configs[4]: TGV M=0.1 Re=1600, 3 blocks, 2 planar sliding interfaces (middle +0.2), "
+                    f"{args.elems}^3 elements/GPU, N={args.degree} Gauss, viscous",
+        "elements": E,
+        "elements_per_gpu": E // world,
+        "degree": args.degree,
+        "nodes": "gauss",
+        "dof": E * n1 ** 3,
+        "bands_nx": [b[0] for b in bands],
+        "l2_policy": "inputs larger than L2 (state %.0f MB, face traces %.0f MB per GPU)" % (
+            E // world * n1 ** 3 * 40 / 1e6, E // world * 6 * n1 ** 2 * 72 / 1e6),
+        "parallelism": f"dp{world} (element partition, NCCL halo + mortar exchange)",
+    }
+    return mesh, cfg, conf, E * n1 ** 3
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(args, conf, timeout_s=20.0):
+    """The 3D CPU oracle (restatement of the reference path, 'port') on a bounded
+    sample of the same workload: same case/degree, reduced mesh, all host threads."""
+    from oracle import pyoracle as P
+    from paper_2008_04356_b200 import types as T
+    threads = os.cpu_count() or 1
+    P.oracle_lib().orc_set_threads(threads)
+    e = 6
+    mesh, bands = tgv_mesh(T, e, e)
+    cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
+    o = P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    dt = 1e-3
+    o.step(dt, 1)  # warm-up
+    steps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < timeout_s or steps == 0:
+        o.step(dt, 1)
+        steps += 1
+    el = time.perf_counter() - t0
+    dof = o.n_elements * (args.degree + 1) ** 3
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": dof * 5 * steps / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same TGV case at "
+                      f"{e}^3 elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the CPU implementation of the path on the host cores.
+    The reference library itself is 2D-only, so the 3D restatement
+    of its algorithm (oracle/sdg3d.cpp, 'port') runs this arm."""
+    if rank != 0:
+        return
+    mesh, cfg, conf, dof = workload(args, 1)
+    base = cpu_baseline(args, conf, timeout_s=max(2.0, 3.0 * args.steps / max(args.steps + args.warmup, 1)))
+    line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (TGV initial field, analytic)",
+            "config": conf, "impl": "reference", "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def roofline_update(kt, conf, args, peaks):
+    """Dominant kernel (k_update): algorithmic bytes per launch / mean launch time."""
+    n1 = args.degree + 1
+    n2, n3 = n1 * n1, n1 ** 3
+    E = conf["elements_per_gpu"]
+    # U r/w + reg r/w (20 n3) + per face node: neighbour trace 5 + own/neighbour Fv.n 8 + new trace 5
+    bytes_update = 8 * E * (20 * n3 + 6 * n2 * 18)
+    bytes_grad = 8 * E * (5 * n3 + 6 * n2 * 9)
+    ms, cnt = kt.get("update", (0.0, 0))
+    gms, gcnt = kt.get("gradient", (0.0, 0))
+    if cnt == 0:
+        return None, {}
+    t = ms / cnt / 1e3
+    ach = bytes_update / t / 1e9
+    traffic = None
+    prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*update_traffic*.json")))
+    if prof:
+        try:
+            traffic = json.load(open(prof[-1])).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    peak = peaks.get("hbm_gbs", 6650.0)
+    rl = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+          "kernel": "k_update", "algorithmic_bytes_per_launch": bytes_update,
+          "mean_launch_ms": t * 1e3, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+    extra = {}
+    if gcnt:
+        gt = gms / gcnt / 1e3
+        extra["k_gradient"] = {"achieved_gbs": bytes_grad / gt / 1e9, "mean_launch_ms": gt * 1e3,
+                               "algorithmic_bytes_per_launch": bytes_grad}
+    total = sum(v[0] for v in kt.values())
+    extra["share_of_step"] = {k: (v[0] / total if total else None) for k, v in kt.items()}
+    extra["launches"] = {k: v[1] for k, v in kt.items()}
+    return rl, extra
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+
+    import torch
+    from paper_2008_04356_b200 import capi
+
+    torch.cuda.set_device(local)
+    nccl_id = None
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        obj = [capi.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    mesh, cfg, conf, dof = workload(args, world)
+    s = capi.RankSolver(mesh, cfg, n_ranks=world, rank=rank, device=local, nccl_id=nccl_id)
+    s.set_initial_condition(0.0)
+    dt = s.suggest_dt(0.5)
+    stream = torch.cuda.ExternalStream(s.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    s.steps_async(dt, args.warmup)
+    s.synchronize()
+    barrier()
+    l0 = s.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        s.steps_async(dt, args.steps)
+        ev1.record(stream)
+        s.synchronize()
+        barrier()
+    launches = s.kernel_launches() - l0
+    ms = ev0.elapsed_time(ev1)
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = dof * 5 * args.steps / (ms_max / 1e3)
+
+    # Per-kernel timing pass (CUDA events around every launch on the context's stream).
+    s.enable_kernel_timing(True)
+    s.kernel_timing()
+    s.steps_async(dt, 2)
+    s.synchronize()
+    kt = s.kernel_timing()
+    s.enable_kernel_timing(False)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    roof, extra = roofline_update(kt, conf, args, peaks)
+
+    # End-to-end through the C-ABI with pinned host buffers: H2D state, step, D2H state.
+    e2e = None
+    if not args.no_e2e:
+        nbytes = s.size * 8
+        h = torch.empty(s.size, dtype=torch.float64).pin_memory()
+        hp = h.data_ptr()
+        import ctypes
+        dp = ctypes.cast(ctypes.c_void_p(hp), ctypes.POINTER(ctypes.c_double))
+        s.lib.sdg_get_state(s.h, dp)
+        reps = max(2, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            s._check(s.lib.sdg_set_state(s.h, dp))
+            s._check(s.lib.sdg_step(s.h, dt))
+            s._check(s.lib.sdg_get_state(s.h, dp))
+        barrier()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": dof * 5 * reps / el, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "steps": reps, "path": "sdg_set_state(pinned host) + sdg_step + sdg_get_state(pinned host), wall clock"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (TGV initial field, analytic)", "config": conf,
+                "value_per_gpu": value / world, "dt": dt, "gpu_launches": launches,
+                "clocks": clk.summary(), "roofline": roof, "kernels": extra, "e2e": e2e}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args, conf)
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

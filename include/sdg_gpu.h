@@ -108,6 +108,13 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
                        long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
                        int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry);
 
+/* Host-only partition / message plan of one rank (no GPU needed): JSON with the
+ * local elements, the conforming halo peers and face keys in send order, and
+ * the per-partner mortar blocks of both roles at interface displacement
+ * `delta` (init_rank_maps + build_schedule, solver.cpp:95-133,
+ * partition.cpp:154-169).  *len receives the full length. */
+int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta, char* buf, long cap, long* len);
+
 /* Instrumentation: the cudaStream_t the context enqueues on, the number of
  * kernels this library launched, and per-kernel-class CUDA-event timing of
  * the next sdg_steps_async call (ms, summed over launches). */

@@ -15,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <sstream>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -1076,6 +1077,98 @@ static void device_pairing(int n_local, const long* faces, long n_par, long n_pe
   *nsched = ns;
 }
 
+
+// Host-only description of one rank's share of a multi-rank run (no CUDA
+// calls): local elements, conforming halo peers with their face keys in send
+// order, and the per-partner mortar blocks of both roles for a displacement
+// `delta` of every interface.  Used by the CPU multi-process tests to check
+// that every pair of ranks derives matching message blocks independently
+// (the stamp check of proj/tests/test_partition.cpp:184-227, for the halo too).
+static std::string plan_json(const sdg_mesh_spec& ms, int n_ranks, int rank, double delta) {
+  const MeshGeom mesh(ms);
+  const Partition part = assign_ranks(mesh, n_ranks);
+  const LocalTopology topo = build_topology(mesh, part, rank);
+  std::ostringstream os;
+  os << "{\"rank\":" << rank << ",\"elements\":[";
+  for (size_t i = 0; i < topo.gids.size(); ++i) os << (i ? "," : "") << topo.gids[i];
+  os << "],\"halo\":[";
+  const int ne = static_cast<int>(topo.gids.size());
+  for (size_t p = 0; p < topo.peers.size(); ++p) {
+    const auto& pf = topo.peers[p];
+    os << (p ? "," : "") << "{\"partner\":" << pf.partner << ",\"keys\":[";
+    for (size_t q = 0; q < pf.send_slots.size(); ++q) {
+      const int slot = pf.send_slots[q], e = slot / 6, side = slot % 6;
+      // the same face key the partner sorts by: minus element gid * 3 + dir
+      long minus = topo.gids[e];
+      if (!(side & 1)) {
+        int b = topo.coords[4 * e], ix = topo.coords[4 * e + 1], iy = topo.coords[4 * e + 2], iz = topo.coords[4 * e + 3];
+        const int dir = side / 2;
+        if (dir == 0) {
+          if (ix > 0) ix--;
+          else {
+            b = (b - 1 + static_cast<int>(mesh.bands.size())) % static_cast<int>(mesh.bands.size());
+            ix = mesh.bands[b].nx - 1;
+          }
+        } else if (dir == 1) {
+          iy = (iy - 1 + ms.ny) % ms.ny;
+        } else {
+          iz = (iz - 1 + ms.nz) % ms.nz;
+        }
+        minus = mesh.gid(b, ix, iy, iz);
+      }
+      os << (q ? "," : "") << minus * 3 + side / 2;
+    }
+    os << "],\"recv_first\":" << (pf.recv_slots.empty() ? -1 : pf.recv_slots.front() - 6 * ne) << "}";
+  }
+  os << "],\"mortars\":[";
+  // Owner maps of every interface side (what init_rank_maps gathers).
+  bool first_role = true;
+  for (int role = 0; role < 2; ++role) {
+    struct Key {
+      int partner, iface;
+      long par, perp;
+      int sub;
+    };
+    std::vector<Key> keys;
+    for (size_t ic = 0; ic < mesh.ifaces.size(); ++ic) {
+      const IfaceGeom& f = mesh.ifaces[ic];
+      const int my_band = role == 0 ? f.static_band() : f.moving_band();
+      const int other_band = role == 0 ? f.moving_band() : f.static_band();
+      const int my_ix = (my_band == f.left) ? mesh.bands[my_band].nx - 1 : 0;
+      const int other_ix = (other_band == f.left) ? mesh.bands[other_band].nx - 1 : 0;
+      const Displacement st = displacement(delta, f.l_par, f.n_faces);
+      for (long iy = 0; iy < ms.ny; ++iy)
+        for (long iz = 0; iz < ms.nz; ++iz) {
+          const long g = mesh.gid(my_band, my_ix, static_cast<int>(iy), static_cast<int>(iz));
+          if (part.owner(my_band, g - mesh.bands[my_band].off) != rank) continue;
+          for (int sub = st.conforming() ? 1 : 0; sub < 2; ++sub) {
+            const long par = role == 0 ? iy : static_index(iy, st.n_delta, sub, f.n_faces);
+            const long opar = role == 0 ? moving_index(iy, st.n_delta, sub, f.n_faces) : par;
+            const long og = mesh.gid(other_band, other_ix, static_cast<int>(opar), static_cast<int>(iz));
+            const int partner = part.owner(other_band, og - mesh.bands[other_band].off);
+            keys.push_back({partner, static_cast<int>(ic), par, iz, sub});
+          }
+        }
+    }
+    std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+      return std::tie(a.partner, a.iface, a.par, a.perp, a.sub) < std::tie(b.partner, b.iface, b.par, b.perp, b.sub);
+    });
+    for (size_t i = 0; i < keys.size();) {
+      size_t j = i;
+      while (j < keys.size() && keys[j].partner == keys[i].partner) ++j;
+      os << (first_role ? "" : ",") << "{\"role\":" << role << ",\"partner\":" << keys[i].partner << ",\"keys\":[";
+      first_role = false;
+      for (size_t q = i; q < j; ++q)
+        os << (q > i ? "," : "") << "[" << keys[q].iface << "," << keys[q].par << "," << keys[q].perp << ","
+           << keys[q].sub << "]";
+      os << "]}";
+      i = j;
+    }
+  }
+  os << "]}";
+  return os.str();
+}
+
 }  // namespace sdg
 
 // ============================================================================
@@ -1249,6 +1342,17 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
   return guarded(nullptr, [&] {
     sdg::device_pairing(n_local, faces, n_par, n_perp, partner_ranks, n_delta, on_static, conforming, self_rank,
                         ncols, cols, m_rows, face_lo, nsched, sched, self_entry);
+  });
+}
+int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta, char* buf, long cap,
+                  long* len) {
+  return guarded(nullptr, [&] {
+    const std::string j = sdg::plan_json(*mesh, n_ranks, rank, delta);
+    *len = static_cast<long>(j.size());
+    if (buf && cap > 0) {
+      std::strncpy(buf, j.c_str(), static_cast<size_t>(cap) - 1);
+      buf[cap - 1] = 0;
+    }
   });
 }
 void* sdg_stream(sdg_ctx* c) { return c->s->stream(); }
