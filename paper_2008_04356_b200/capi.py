@@ -74,6 +74,7 @@ def lib():
         L.sdg_get_mapping.argtypes = [_vp, C.c_int, _ip]
         L.sdg_pairing_device.argtypes = [C.c_int, _lp, C.c_long, C.c_long, _ip, C.c_long, C.c_int, C.c_int,
                                          C.c_int, _ip, _ip, _ip, _lp, _ip, _ip, _ip]
+        L.sdg_plan_json.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_double, C.c_char_p, C.c_long, _lp]
         L.sdg_stream.argtypes = [_vp]
         L.sdg_stream.restype = C.c_void_p
         L.sdg_kernel_launches.argtypes = [_vp]
@@ -91,7 +92,7 @@ EXPORTED = [
     "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
-    "sdg_pairing_device", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
+    "sdg_pairing_device", "sdg_plan_json", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
 
@@ -249,6 +250,18 @@ class RankSolver:
         self._check(self.lib.sdg_kernel_timing(self.h, names, 512, _d(ms), cnt.ctypes.data_as(_lp), 16, C.byref(n)))
         keys = names.value.decode().split(",")
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys[: n.value])}
+
+
+def plan(mesh: T.MeshSpec, n_ranks: int, rank: int, delta: float = 0.0) -> dict:
+    """Host-only partition / message plan of one rank (no GPU): see sdg_plan_json."""
+    import json
+    n = C.c_long()
+    T.raise_for(lib().sdg_plan_json(C.byref(mesh), n_ranks, rank, delta, None, 0, C.byref(n)),
+                lib().sdg_global_error().decode())
+    buf = C.create_string_buffer(n.value + 1)
+    T.raise_for(lib().sdg_plan_json(C.byref(mesh), n_ranks, rank, delta, buf, n.value + 1, C.byref(n)),
+                lib().sdg_global_error().decode())
+    return json.loads(buf.value.decode())
 
 
 def pairing_device(faces, n_par, n_perp, ranks, n_delta, on_static, conforming, self_rank):

@@ -1,0 +1,113 @@
+"""N>1 host logic on CPU with gloo, world_size 2..8 (no GPU): every rank builds
+its own partition / halo / mortar message plan (what the NCCL rounds of
+solver.cu exchange), the plans are all-gathered over gloo, and every pair of
+ranks must derive matching blocks independently — the stamp check of
+proj/tests/test_partition.cpp:184-227 extended to the conforming halo.
+Partition rules follow proj/src/partition.cpp:17-83 (no rank on both sides of
+a sliding interface)."""
+import math
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2008_04356_b200 import capi
+from paper_2008_04356_b200 import types as T
+
+
+def meshes():
+    L = 2 * math.pi
+    return {
+        "tgv3": T.mesh_spec([(3, 1.0, 0.0), (4, 1.0, 0.2), (3, 1.0, 0.0)], ny=4, nz=3, width=L, height=L, depth=L),
+        "box0": T.mesh_spec([(4, 1.0, 0.0), (4, 1.0, 0.5)], ny=4, nz=4, periodic=(False, True, True)),
+        "bands5": T.mesh_spec([(2, 1.0, 0.0), (3, 1.0, 1.0), (2, 2.0, 0.0), (2, 1.0, 0.0), (2, 1.0, 0.7)], ny=5, nz=2),
+    }
+
+
+def check_plans(plans, n_ranks, mesh):
+    by_rank = {p["rank"]: p for p in plans}
+    elems = [g for p in plans for g in p["elements"]]
+    assert len(elems) == len(set(elems))
+    total = sum(mesh.bands[b].nx for b in range(mesh.n_bands)) * mesh.ny * mesh.nz
+    assert sorted(elems) == list(range(total))
+    for a in range(n_ranks):
+        for h in by_rank[a]["halo"]:
+            b = h["partner"]
+            assert b != a
+            back = [x for x in by_rank[b]["halo"] if x["partner"] == a]
+            assert len(back) == 1 and back[0]["keys"] == h["keys"], (a, b)
+        for m in by_rank[a]["mortars"]:
+            b = m["partner"]
+            back = [x for x in by_rank[b]["mortars"] if x["partner"] == a and x["role"] == 1 - m["role"]]
+            if a == b:
+                back = [x for x in by_rank[a]["mortars"] if x["partner"] == a and x["role"] == 1 - m["role"]]
+            assert len(back) == 1 and back[0]["keys"] == m["keys"], (a, b, m["role"])
+    if n_ranks > 1:
+        for p in plans:
+            roles = {m["role"] for m in p["mortars"]}
+            selfs = [m for m in p["mortars"] if m["partner"] == p["rank"]]
+            assert not selfs, "a rank may not own both sides of a sliding interface"
+            assert len(roles) <= 2
+
+
+def _worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = []
+    for name, mesh in meshes().items():
+        for delta in (0.0, 0.37, 1.0, 2.9):
+            try:
+                mine = capi.plan(mesh, world, rank, delta)
+            except T.ConfigError:  # e.g. 3 ranks over 5 bands (partition.cpp:31-46): same on every rank
+                continue
+            allp = [None] * world
+            dist.all_gather_object(allp, mine)
+            check_plans(allp, world, mesh)
+            ok.append((name, delta))
+    dist.barrier()
+    dist.destroy_process_group()
+    results[rank] = len(ok)
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_plans_agree_across_gloo_ranks(world):
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    res = mgr.dict()
+    procs = [ctx.Process(target=_worker, args=(r, world, PORTS[world], res))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    assert len(res) == world and len(set(res.values())) == 1
+
+
+PORTS = {2: free_port(), 3: free_port()}
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 6, 8])
+def test_plans_agree_in_process(world):
+    for mesh in meshes().values():
+        for delta in (0.0, 0.37, 1.0):
+            try:
+                plans = [capi.plan(mesh, world, r, delta) for r in range(world)]
+            except T.ConfigError:
+                continue
+            check_plans(plans, world, mesh)
+
+
+def test_two_ranks_over_three_bands_split_static_moving():
+    mesh = meshes()["tgv3"]
+    p0, p1 = capi.plan(mesh, 2, 0), capi.plan(mesh, 2, 1)
+    assert len(p0["elements"]) == 2 * 3 * 4 * 3 and len(p1["elements"]) == 4 * 4 * 3
