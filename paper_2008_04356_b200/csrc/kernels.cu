@@ -14,6 +14,7 @@
 // Each conforming face flux is evaluated by both of its elements with the
 // same instruction sequence on the same operands (minus side first), so both
 // sides see identical bits — the orientation rule of solver.cpp:323-341.
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -734,12 +735,17 @@ __device__ __forceinline__ long long pmod(long long a, long long n) {
 
 __global__ void __launch_bounds__(kPairThreads) k_pairing(const __grid_constant__ PairingArgs A, PairingPtrs P) {
   const int role = blockIdx.x;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kPairThreads / 32;
   __shared__ long long s_nd[kMaxCtx];
   __shared__ int s_conf[kMaxCtx];
-  __shared__ int S[kPairPartners][kPairThreads + 1];
-  __shared__ int tot[kPairPartners], off[kPairPartners];
+  __shared__ int cnt[kPairPartners], base[kPairPartners], carry[kPairPartners];
+  __shared__ int wcnt[kPairPartners][NW];
   __shared__ int s_bad;
+  if (tid < kPairPartners) {
+    cnt[tid] = 0;
+    carry[tid] = 0;
+  }
   if (tid == 0) s_bad = 0;
   if (tid < A.n_ctx) {
     const CtxD& c = A.ctx[tid];
@@ -770,7 +776,7 @@ __global__ void __launch_bounds__(kPairThreads) k_pairing(const __grid_constant_
     for (int q = tid; q < 2 * c.n_faces; q += kPairThreads) P.m[2 * c.face_off + q] = -1;
   }
   __syncthreads();
-  // Tuples (append_mortar_tuples).
+  // Tuples (append_mortar_tuples): dense key, partner and passive payload.
   for (int r = 0; r < A.role_nctx[role]; ++r) {
     const int ci = A.role_ctx[role][r];
     const CtxD& c = A.ctx[ci];
@@ -796,53 +802,15 @@ __global__ void __launch_bounds__(kPairThreads) k_pairing(const __grid_constant_
       const long long d = A.iface_base[c.iface] + (ipar * c.n_perp + fperp) * 2 + sub;
       pres[d] = partner;
       payload[d] = (ci << 24) | f;
-    }
-  }
-  __syncthreads();
-  // Pass 1: per-thread segment counts per partner.
-  const long long D = A.dense_size;
-  const long long L = (D + kPairThreads - 1) / kPairThreads;
-  const long long lo = tid * L, hi = min(D, lo + L);
-  int cnt[kPairPartners];
-#pragma unroll
-  for (int p = 0; p < kPairPartners; ++p) cnt[p] = 0;
-  for (long long d = lo; d < hi; ++d) {
-    const int p = pres[d];
-#pragma unroll
-    for (int q = 0; q < kPairPartners; ++q) cnt[q] += (p == q);
-  }
-#pragma unroll
-  for (int p = 0; p < kPairPartners; ++p) S[p][tid] = cnt[p];
-  __syncthreads();
-  // Exclusive scans over threads, one warp per two partners.
-  {
-    const int w = tid >> 5, lane = tid & 31;
-    constexpr int PER = kPairThreads / 32;
-    for (int p = w; p < kPairPartners; p += kPairThreads / 32) {
-      int loc[PER], sum = 0;
-#pragma unroll
-      for (int r = 0; r < PER; ++r) {
-        loc[r] = sum;
-        sum += S[p][lane * PER + r];
-      }
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - sum;
-#pragma unroll
-      for (int r = 0; r < PER; ++r) S[p][lane * PER + r] = excl + loc[r];
-      if (lane == 31) tot[p] = incl;
+      atomicAdd(&cnt[partner], 1);
     }
   }
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
     for (int p = 0; p < kPairPartners; ++p) {
-      off[p] = acc;
-      acc += tot[p];
+      base[p] = acc;
+      acc += cnt[p];
     }
     P.n_mortars[role] = acc;
     if (s_bad || (A.expect_mortars[role] >= 0 && A.expect_mortars[role] != acc)) {
@@ -853,37 +821,53 @@ __global__ void __launch_bounds__(kPairThreads) k_pairing(const __grid_constant_
     }
   }
   __syncthreads();
-  // Pass 2: positions, A columns and m (sort_index_array + build_mapping).
-  int run[kPairPartners];
+  // Positions (sort_index_array + build_mapping): one coalesced pass over the dense
+  // key range in chunks of the block; per partner, rank = running carry + warp
+  // offset + lane prefix from ballots.
+  const unsigned lt = (1u << lane) - 1u;
+  for (long long c0 = 0; c0 < A.dense_size; c0 += kPairThreads) {
+    const long long d = c0 + tid;
+    const int p = d < A.dense_size ? pres[d] : -1;
+    int my_pref = 0;
 #pragma unroll
-  for (int p = 0; p < kPairPartners; ++p) run[p] = 0;
-  for (long long d = lo; d < hi; ++d) {
-    const int p = pres[d];
-    if (p < 0) continue;
-    int pos = 0;
-#pragma unroll
-    for (int q = 0; q < kPairPartners; ++q)
-      if (p == q) pos = off[q] + S[q][tid] + run[q]++;
-    int ifc = 0;
-    for (int x = 1; x < A.n_ifaces; ++x)
-      if (d >= A.iface_base[x]) ifc = x;
-    long long rest = d - A.iface_base[ifc];
-    const int sub = static_cast<int>(rest & 1);
-    rest >>= 1;
-    const long long np = A.iface_nperp[ifc];
-    const int iperp = static_cast<int>(rest % np), ipar = static_cast<int>(rest / np);
-    const int pl = payload[d];
-    const int ci = pl >> 24, f = pl & 0xffffff;
-    int* col = P.cols[role] + 7 * pos;
-    col[0] = p;
-    col[1] = ifc;
-    col[2] = ipar;
-    col[3] = iperp;
-    col[4] = sub;
-    col[5] = f;
-    col[6] = ci;
-    const CtxD& c = A.ctx[ci];
-    P.m[2 * c.face_off + sub * c.n_faces + f] = pos;
+    for (int q = 0; q < kPairPartners; ++q) {
+      const unsigned m = __ballot_sync(0xffffffffu, p == q);
+      if (p == q) my_pref = __popc(m & lt);
+      if (lane == 0) wcnt[q][warp] = __popc(m);
+    }
+    __syncthreads();
+    if (p >= 0) {
+      int off = base[p] + carry[p] + my_pref;
+      for (int w = 0; w < warp; ++w) off += wcnt[p][w];
+      const int pos = off;
+      int ifc = 0;
+      for (int x = 1; x < A.n_ifaces; ++x)
+        if (d >= A.iface_base[x]) ifc = x;
+      long long rest = d - A.iface_base[ifc];
+      const int sub = static_cast<int>(rest & 1);
+      rest >>= 1;
+      const long long np = A.iface_nperp[ifc];
+      const int iperp = static_cast<int>(rest % np), ipar = static_cast<int>(rest / np);
+      const int pl = payload[d];
+      const int ci = pl >> 24, f = pl & 0xffffff;
+      int* col = P.cols[role] + 7 * pos;
+      col[0] = p;
+      col[1] = ifc;
+      col[2] = ipar;
+      col[3] = iperp;
+      col[4] = sub;
+      col[5] = f;
+      col[6] = ci;
+      const CtxD& c = A.ctx[ci];
+      P.m[2 * c.face_off + sub * c.n_faces + f] = pos;
+    }
+    __syncthreads();
+    if (tid < kPairPartners) {
+      int tot = 0;
+      for (int w = 0; w < NW; ++w) tot += wcnt[tid][w];
+      carry[tid] += tot;
+    }
+    __syncthreads();
   }
 }
 
@@ -1046,6 +1030,618 @@ inline void check_launch(const char* what) {
   if (e != cudaSuccess) throw DeviceError(SDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// ============================================================================
+// Persistent, TMA-pipelined element kernels (even N+1: every per-element and
+// per-face-slot block is a multiple of 16 bytes, as cp.async.bulk requires).
+//
+// Each CTA owns a strided sequence of element tiles.  One thread issues, per
+// tile, cp.async.bulk copies of everything the tile reads from HBM — the
+// element state, the RK register, its own Fv.n slots and, per side, the
+// neighbour's trace + Fv.n slot (or the sliding face's back-projected flux +
+// lift*) — into one of two shared-memory stages, completing on an mbarrier,
+// while the CTA computes the previous tile from the other stage.  Outputs
+// (new state, register, face traces, Fv.n) are assembled in shared memory and
+// written back with cp.async.bulk stores.  The compute phases are those of
+// k_gradient / k_update above.
+// ============================================================================
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+constexpr int kCodeShift = 29;
+
+template <int N1>
+struct Tma {
+  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  static constexpr int EPB = N1 == 2 ? 8 : (N1 == 4 ? 2 : 1);
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);  // resident CTAs per SM (shared-memory bound)
+  static constexpr int TAB = Dim<N1>::TAB;
+  static constexpr int EL = 5 * N3;  // state doubles per element
+  static constexpr int TS = 5 * N2;  // trace slot
+  static constexpr int FS = 4 * N2;  // Fv.n slot
+  static constexpr int NB = TS + FS;
+  // update stage: U, reg, own Fv.n (6 slots), neighbour data (6 x NB)
+  static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
+  static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
+  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
+  // gradient stage: U, neighbour traces / lift (6 x TS)
+  static constexpr int G_STAGE = EPB * (EL + 6 * TS);
+  static constexpr int G_WORK = EPB * (6 * TS + 24 * N2 + 4 * N3 + 12 * N3 + 6 * FS);
+  static constexpr int G_SMEM = (TAB + 2 * G_STAGE + G_WORK) * 8 + 64;
+  static_assert(EL % 2 == 0 && TS % 2 == 0, "TMA path needs 16-byte blocks");
+};
+
+// Side codes of one tile (8 ints per element) into shared memory, asynchronously.
+template <int N1>
+__device__ __forceinline__ void prefetch_codes(const FieldPtrs& P, int tile, int* dst) {
+  using D = Tma<N1>;
+  const int e0 = tile * D::EPB;
+  const int n = min(D::EPB, P.E - e0);
+  for (int q = 0; q < n * 2; ++q) cp_async16(dst + 4 * q, P.side_code + 8 * e0 + 4 * q);
+  cp_async_commit();
+}
+
+// Update-kernel loads of one tile (issued by one thread).
+template <int N1, bool VISC>
+__device__ __forceinline__ void issue_update_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
+                                                   uint64_t* bar) {
+  using D = Tma<N1>;
+  const int e0 = tile * D::EPB;
+  const int n = min(D::EPB, P.E - e0);
+  uint32_t bytes = 2u * n * D::EL * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int typ = codes[8 * le + s] >> kCodeShift;
+      if (typ != kDirichlet) bytes += (D::TS + (VISC ? D::FS : 0)) * 8u;
+    }
+  mbar_arrive_expect_tx(bar, bytes);
+  double* sU = st;
+  double* sR = st + D::EPB * D::EL;
+  double* sFv = sR + D::EPB * D::EL;
+  double* sNb = sFv + D::EPB * 6 * D::FS;
+  bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
+  bulk_g2s(sR, P.reg + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
+  if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D::FS, n * 6u * D::FS * 8u, bar);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int code = codes[8 * le + s];
+      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+      double* nb = sNb + (le * 6 + s) * D::NB;
+      if (typ == kConforming) {
+        bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        if (VISC) bulk_g2s(nb + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+      } else if (typ == kSliding) {
+        bulk_g2s(nb, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        if (VISC) bulk_g2s(nb + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+      }
+    }
+}
+
+// Prolongation of one variable from an AoS [node][5] element block.
+template <int N1>
+__device__ __forceinline__ double prolong_aos(const double* __restrict__ s, int v, const double* __restrict__ ell,
+                                              int dir, int a, int b) {
+  constexpr int N2 = N1 * N1;
+  const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
+  const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[(base + m * stride) * 5 + v], acc);
+  return acc;
+}
+
+template <int N1, bool VISC>
+__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_update_tma(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                                 StageArgs A) {
+  using D = Tma<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* work = stage0 + 2 * D::U_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK);
+  __shared__ __align__(16) int codes[2][8 * EPB];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E + EPB - 1) / EPB;
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < tiles) {
+    prefetch_codes<N1>(P, tile, codes[0]);
+    cp_async_wait_all();
+    issue_update_loads<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
+    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
+  }
+  double* wF = work;                               // EPB x 5 N3 (q, then F_d, SoA)
+  double* wLift = work + EPB * 5 * N3;             // EPB x 24 N2, SoA [s][c][f]
+  double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    const int sidx = it & 1;
+    double* st = stage0 + sidx * D::U_STAGE;
+    const int next = tile + gridDim.x;
+    if (threadIdx.x == 0) bulk_wait_read0();  // stores of the previous tile have read stage sidx^1 and wTr
+    if (threadIdx.x == 0 && next < tiles) {
+      cp_async_wait_all();  // codes of `next`
+      fence_proxy_async();
+      issue_update_loads<N1, VISC>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::U_STAGE,
+                                   &bars[sidx ^ 1]);
+      if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
+    }
+    const int e0 = tile * EPB;
+    const int e = e0 + le;
+    const bool active = e < P.E;
+    double* sU = st + le * D::EL;
+    double* sR = st + EPB * D::EL + le * D::EL;
+    double* sFv = st + 2 * EPB * D::EL + le * 6 * D::FS;
+    double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
+    double* q = wF + le * 5 * N3;
+    double* lf = wLift + le * 24 * N2;
+    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+    mbar_wait(&bars[sidx], (it >> 1) & 1);
+
+    // Phase 1: face fluxes (in place over the neighbour data) and lift*.
+    if (active) {
+      if (VISC) {
+        double u[5], qq[4];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+        prim4(u, C.gas, qq);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+      }
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        double* nb = sNb + s * D::NB;
+        const int code = P.side_code[8 * e + s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kSliding) {
+          if (VISC) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = nb[D::TS + f * 4 + c];
+          }
+          continue;
+        }
+        double own[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
+        double flux[5], lift[4];
+        bool ok;
+        const double vg = dir == 1 ? B.vg : 0.0;
+        if (typ == kConforming) {
+          double other[5];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
+          const double* um = (s & 1) ? own : other;
+          const double* up = (s & 1) ? other : own;
+          if (VISC) {
+            double qa[4], qb[4];
+            prim4(own, C.gas, qa);
+            prim4(other, C.gas, qb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+            double fa[4], fb[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              fa[c] = sFv[s * D::FS + f * 4 + c];
+              fb[c] = nb[D::TS + f * 4 + c];
+            }
+            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        } else {
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          const double* um = (s & 1) ? own : ext;
+          const double* up = (s & 1) ? ext : own;
+          if (VISC) {
+            prim4(ext, C.gas, lift);
+            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+            double gg[12];
+#pragma unroll
+            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+            double fm[4], fp[4];
+            fv_dir(um, gg, dir, C.gas, fm);
+            fv_dir(up, gg, dir, C.gas, fp);
+            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        }
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
+        if (VISC) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
+        }
+      }
+    }
+    __syncthreads();
+
+    // Phase 2: volume flux at the node (gradient recomputed from q and lift*).
+    double F[3][5], u[5];
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      const double ir = __drcp_rn(u[0]);
+      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+      const double p = pressure(u, ir, C.gas);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double vgd = d == 1 ? B.vg : 0.0;
+        F[d][0] = u[0] * vv[d] - vgd * u[0];
+        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
+        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
+        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
+        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
+      }
+      if (VISC) {
+        double g[12];
+        node_gradient<N1>(tab, q, lf, B, i, j, k, g);
+        const double div = g[0] + g[4] + g[8];
+        const double mu = C.gas.mu, lam = C.gas.lam;
+        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
+                     t22 = 2.0 * mu * g[8] + lam * div;
+        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
+        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          F[d][1] -= tau[d][0];
+          F[d][2] -= tau[d][1];
+          F[d][3] -= tau[d][2];
+          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+        }
+      }
+    }
+
+    // Phase 3: weak divergence per direction through shared memory.
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      __syncthreads();
+      if (active) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) q[v * N3 + t] = F[d][v] * B.sj[d];
+      }
+      __syncthreads();
+      if (active) {
+        const int ia = d == 0 ? i : (d == 1 ? j : k);
+        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          const double c = tab[ia * N1 + m];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
+        }
+      }
+    }
+
+    // Phase 4 + 5: surface lift, RK update in place, admissibility.
+    if (active) {
+      double du[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
+      const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int dir = s >> 1;
+        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
+        if (c != 0.0) {
+          const double* fl = sNb + s * D::NB + f * 5;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
+        }
+      }
+      if (A.mode == 1) {
+        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = du[v];
+      } else {
+        double w[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
+          w[v] = u[v] + A.rk_b * rg;
+          sR[t * 5 + v] = rg;
+          sU[t * 5 + v] = w[v];
+        }
+        const double p = pressure(w, __drcp_rn(w[0]), C.gas);
+        bool ok = w[0] > 0.0 && p > 0.0;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+      }
+    }
+    if (A.mode == 1) {
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    // Phase 6: traces of the new state, then bulk stores of U, reg and traces.
+    if (active) {
+      double* tr = wTr + le * 6 * D::TS;
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int n = min(EPB, P.E - e0);
+      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
+      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
+      bulk_s2g(P.trace + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+// Gradient-kernel loads of one tile: U and, per side, the neighbour trace
+// (conforming) or the back-projected lift* (sliding).
+template <int N1>
+__device__ __forceinline__ void issue_gradient_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
+                                                     uint64_t* bar) {
+  using D = Tma<N1>;
+  const int e0 = tile * D::EPB;
+  const int n = min(D::EPB, P.E - e0);
+  uint32_t bytes = n * D::EL * 8u;
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int typ = codes[8 * le + s] >> kCodeShift;
+      if (typ == kConforming) bytes += D::TS * 8u;
+      else if (typ == kSliding) bytes += D::FS * 8u;
+    }
+  mbar_arrive_expect_tx(bar, bytes);
+  bulk_g2s(st, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
+  double* sNb = st + D::EPB * D::EL;
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int code = codes[8 * le + s];
+      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+      double* nb = sNb + (le * 6 + s) * D::TS;
+      if (typ == kConforming) bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+      else if (typ == kSliding) bulk_g2s(nb, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+    }
+}
+
+template <int N1>
+__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_gradient_tma(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                                   StageArgs A) {
+  using D = Tma<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* work = stage0 + 2 * D::G_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::G_WORK);
+  __shared__ __align__(16) int codes[2][8 * EPB];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E + EPB - 1) / EPB;
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < tiles) {
+    prefetch_codes<N1>(P, tile, codes[0]);
+    cp_async_wait_all();
+    issue_gradient_loads<N1>(P, tile, codes[0], stage0, &bars[0]);
+    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
+  }
+  double* wTr = work;                       // EPB x 6 TS (own traces, AoS)
+  double* wLift = wTr + EPB * 6 * D::TS;    // EPB x 24 N2 SoA
+  double* wQ = wLift + EPB * 24 * N2;       // EPB x 4 N3 SoA
+  double* wG = wQ + EPB * 4 * N3;           // EPB x 12 N3 SoA
+  double* wFv = wG + EPB * 12 * N3;         // EPB x 6 FS (global slot layout)
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    const int sidx = it & 1;
+    double* st = stage0 + sidx * D::G_STAGE;
+    const int next = tile + gridDim.x;
+    if (threadIdx.x == 0) bulk_wait_read0();  // the previous Fv.n store has read wFv
+    if (threadIdx.x == 0 && next < tiles) {
+      cp_async_wait_all();
+      fence_proxy_async();
+      issue_gradient_loads<N1>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::G_STAGE, &bars[sidx ^ 1]);
+      if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
+    }
+    const int e0 = tile * EPB;
+    const int e = e0 + le;
+    const bool active = e < P.E;
+    double* sU = st + le * D::EL;
+    double* sNb = st + EPB * D::EL + le * 6 * D::TS;
+    double* tr = wTr + le * 6 * D::TS;
+    double* lf = wLift + le * 24 * N2;
+    double* q = wQ + le * 4 * N3;
+    double* gS = wG + le * 12 * N3;
+    double* fvo = wFv + le * 6 * D::FS;
+    mbar_wait(&bars[sidx], (it >> 1) & 1);
+    if (active) {
+      double u[5], qq[4];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      prim4(u, C.gas, qq);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        double own[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = own[v];
+        const int code = P.side_code[8 * e + s];
+        const int typ = code >> kCodeShift;
+        const double* nb = sNb + s * D::TS;
+        double lift[4];
+        if (typ == kConforming) {
+          double other[5], qa[4], qb[4];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
+          prim4(own, C.gas, qa);
+          prim4(other, C.gas, qb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+        } else if (typ == kSliding) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = nb[f * 4 + c];
+        } else {
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          prim4(ext, C.gas, lift);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
+      }
+    }
+    __syncthreads();
+    if (active) {
+      double g[12];
+      node_gradient<N1>(tab, q, lf, C.bands[P.coords[4 * e]], i, j, k, g);
+#pragma unroll
+      for (int c = 0; c < 12; ++c) gS[c * N3 + t] = g[c];
+      if (P.grad_out != nullptr) {
+        double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) go[c] = g[c];
+      }
+    }
+    __syncthreads();
+    if (active) {
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        double gt[12];
+#pragma unroll
+        for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(gS + c * N3, ell, s >> 1, a, b);
+        const int code = P.side_code[8 * e + s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kConforming) {
+          double fv[4];
+          fv_dir(tr + s * D::TS + f * 5, gt, s >> 1, C.gas, fv);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
+        } else {
+          double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+          for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int n = min(EPB, P.E - e0);
+      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, n * 6u * D::FS * 8u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+template <int N1>
+bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = Tma<N1>;
+    const int tiles = (p.E + D::EPB - 1) / D::EPB;
+    auto kern = c.gas.viscous ? k_update_tma<N1, true> : k_update_tma<N1, false>;
+    static int occ_v = -1, occ_i = -1;
+    int& occ = c.gas.viscous ? occ_v : occ_i;
+    if (occ < 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, D::U_SMEM);
+      if (occ < 1) occ = 1;
+    }
+    const int grid = std::min(tiles, n_sm * occ);
+    kern<<<grid, D::THREADS, D::U_SMEM, st>>>(c, p, a);
+    check_launch("k_update_tma");
+    return true;
+  }
+}
+template <int N1>
+bool gradient_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = Tma<N1>;
+    const int tiles = (p.E + D::EPB - 1) / D::EPB;
+    static int occ = -1;
+    if (occ < 0) {
+      cudaFuncSetAttribute(k_gradient_tma<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gradient_tma<N1>, D::THREADS, D::G_SMEM);
+      if (occ < 1) occ = 1;
+    }
+    const int grid = std::min(tiles, n_sm * occ);
+    k_gradient_tma<N1><<<grid, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+    check_launch("k_gradient_tma");
+    return true;
+  }
+}
+
 template <class K>
 void set_smem(K kernel, int bytes) {
   static_assert(sizeof(K) > 0, "");
@@ -1129,6 +1725,20 @@ void launch_gradient(int n1, const ElemConsts& c, const FieldPtrs& p, const Stag
 void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if (p.E == 0) return;
   SDG_DISPATCH(n1, (update_t<NN>(c, p, a, st)));
+}
+bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
+                         cudaStream_t st) {
+  if (p.E == 0) return true;
+  bool ok = false;
+  SDG_DISPATCH(n1, (ok = gradient_tma_t<NN>(c, p, a, n_sm, st)));
+  return ok;
+}
+bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
+                       cudaStream_t st) {
+  if (p.E == 0) return true;
+  bool ok = false;
+  SDG_DISPATCH(n1, (ok = update_tma_t<NN>(c, p, a, n_sm, st)));
+  return ok;
 }
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
   k_pairing<<<2, kPairThreads, 0, st>>>(a, p);

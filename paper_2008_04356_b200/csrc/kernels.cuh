@@ -57,6 +57,7 @@ struct FieldPtrs {
   const int8_t* side_type;   // E x 6
   const int* side_idx;       // E x 6
   const int* coords;         // E x 4 (band, ix, iy, iz)
+  const int* side_code;      // E x 8: idx | type << 29 for the 6 sides (+2 pad), 32 B per element
   double* grad_out;          // optional E x N3 x 12
   ErrRec* err;
   int E;
@@ -143,6 +144,11 @@ struct MortarPtrs {
 void launch_prolong(int n1, const ElemConsts& c, const FieldPtrs& p, cudaStream_t st);
 void launch_gradient(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+// Persistent TMA-pipelined element kernels (even N+1); return false when not applicable.
+bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
+                         cudaStream_t st);
+bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
+                       cudaStream_t st);
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);

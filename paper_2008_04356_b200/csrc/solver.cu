@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -159,7 +160,9 @@ class GpuRankSolver {
 
   DevBuf<double> U_, reg_, dudt_, trace_, fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
   DevBuf<int8_t> side_type_;
-  DevBuf<int> side_idx_, coords_;
+  DevBuf<int> side_idx_, coords_, side_code_;
+  int n_sm_ = 148;
+  bool use_tma_ = true;
   DevBuf<ErrRec> err_;
   ErrRec* err_host_ = nullptr;
   DevBuf<unsigned long long> dt_min_;
@@ -210,6 +213,8 @@ GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& c
   lifting_ = g.mu > 0.0;
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device), "device attribute");
+  if (const char* env = std::getenv("SDG_NO_TMA")) use_tma_ = env[0] == '0';
   if (n_ranks > 1) {
     if (!nccl_id) throw ConfigError("multi-rank context needs an NCCL unique id");
     ncclUniqueId id;
@@ -285,6 +290,16 @@ void GpuRankSolver::upload_topology() {
   dir_g_.alloc(static_cast<size_t>(ND_) * n2_ * 12);
   side_type_.upload(topo_.side_type, stream_);
   side_idx_.upload(topo_.side_idx, stream_);
+  {
+    std::vector<int> code(static_cast<size_t>(E_) * 8, 0);
+    for (int e = 0; e < E_; ++e)
+      for (int q = 0; q < 6; ++q) {
+        const int idx = topo_.side_idx[6 * e + q];
+        if (idx < 0 || idx >= (1 << 29)) throw ConfigError("face index exceeds the side-code range");
+        code[8 * e + q] = idx | (static_cast<int>(topo_.side_type[6 * e + q]) << 29);
+      }
+    side_code_.upload(code, stream_);
+  }
   coords_.upload(topo_.coords, stream_);
   err_.alloc(1);
   err_.zero(stream_);
@@ -535,6 +550,7 @@ FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
   p.side_type = side_type_.p;
   p.side_idx = side_idx_.p;
   p.coords = coords_.p;
+  p.side_code = side_code_.p;
   p.grad_out = nullptr;
   p.err = err_.p;
   p.E = E_;
@@ -790,7 +806,7 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     mark(KC_MORTAR, false);
     launches_ += S_ > 0;
     mark(KC_GRADIENT, true);
-    launch_gradient(n_, consts_, fp, a, stream_);
+    if (!(use_tma_ && launch_gradient_tma(n_, consts_, fp, a, n_sm_, stream_))) launch_gradient(n_, consts_, fp, a, stream_);
     mark(KC_GRADIENT, false);
     launches_++;
     halo_exchange(fvn_.p, 4);
@@ -812,7 +828,7 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   mark(KC_MORTAR, false);
   launches_ += S_ > 0;
   mark(KC_UPDATE, true);
-  launch_update(n_, consts_, fp, a, stream_);
+  if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm_, stream_))) launch_update(n_, consts_, fp, a, stream_);
   mark(KC_UPDATE, false);
   launches_++;
   traces_valid_ = (mode == 0 && !u_override);
