@@ -16,6 +16,7 @@
 // sides see identical bits — the orientation rule of solver.cpp:323-341.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_suggest_dt(const __grid_co
 // the sort is a per-partner counting pass over the dense key range.
 // One CTA per role.
 // ----------------------------------------------------------------------------
-constexpr int kPairThreads = 256;
+constexpr int kPairThreads = 1024;
 constexpr int kPairPartners = 16;
 
 __device__ __forceinline__ long long pmod(long long a, long long n) {
@@ -828,13 +829,11 @@ __global__ void __launch_bounds__(kPairThreads) k_pairing(const __grid_constant_
   for (long long c0 = 0; c0 < A.dense_size; c0 += kPairThreads) {
     const long long d = c0 + tid;
     const int p = d < A.dense_size ? pres[d] : -1;
-    int my_pref = 0;
-#pragma unroll
-    for (int q = 0; q < kPairPartners; ++q) {
-      const unsigned m = __ballot_sync(0xffffffffu, p == q);
-      if (p == q) my_pref = __popc(m & lt);
-      if (lane == 0) wcnt[q][warp] = __popc(m);
-    }
+    if (lane < kPairPartners) wcnt[lane][warp] = 0;
+    __syncwarp();
+    const unsigned peers = __match_any_sync(0xffffffffu, p);
+    const int my_pref = __popc(peers & lt);
+    if (p >= 0 && my_pref == 0) wcnt[p][warp] = __popc(peers);
     __syncthreads();
     if (p >= 0) {
       int off = base[p] + carry[p] + my_pref;
@@ -1095,19 +1094,23 @@ struct Tma {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int EPB = N1 == 2 ? 8 : (N1 == 4 ? 2 : 1);
   static constexpr int THREADS = EPB * N3;
-  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);  // resident CTAs per SM (shared-memory bound)
+  static constexpr int MINB_U = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);  // resident CTAs per SM (shared-memory bound)
+  static constexpr int MINB_G = N1 == 8 ? 1 : (N1 == 6 ? 3 : 2);
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3;  // state doubles per element
   static constexpr int TS = 5 * N2;  // trace slot
   static constexpr int FS = 4 * N2;  // Fv.n slot
   static constexpr int NB = TS + FS;
-  // update stage: U, reg, own Fv.n (6 slots), neighbour data (6 x NB)
-  static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
-  static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
-  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
-  // gradient stage: U, neighbour traces / lift (6 x TS)
+  // update: double-buffered stage {U, own Fv.n, neighbour (trace|flux, Fv.n|lift)} + single RK register
+  static constexpr int U_STAGE = EPB * (EL + 6 * FS + 6 * NB);
+  static constexpr int U_REG = EPB * EL;
+  static constexpr int U_WF = EPB * 16 * N3;  // q (4 N3) + gradient (12 N3), then F (15 N3), then traces
+  static constexpr int U_WORK = U_WF + EPB * 24 * N2;
+  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_REG + U_WORK) * 8 + 64;
+  // gradient: double-buffered {U, neighbour trace|lift}; own traces; q (then Fv.n out); gradient
   static constexpr int G_STAGE = EPB * (EL + 6 * TS);
-  static constexpr int G_WORK = EPB * (6 * TS + 24 * N2 + 4 * N3 + 12 * N3 + 6 * FS);
+  static constexpr int G_WQ = EPB * (4 * N3 > 6 * FS ? 4 * N3 : 6 * FS);
+  static constexpr int G_WORK = EPB * 6 * TS + G_WQ + EPB * 12 * N3;
   static constexpr int G_SMEM = (TAB + 2 * G_STAGE + G_WORK) * 8 + 64;
   static_assert(EL % 2 == 0 && TS % 2 == 0, "TMA path needs 16-byte blocks");
 };
@@ -1122,14 +1125,14 @@ __device__ __forceinline__ void prefetch_codes(const FieldPtrs& P, int tile, int
   cp_async_commit();
 }
 
-// Update-kernel loads of one tile (issued by one thread).
+// Update-kernel stage loads of one tile (issued by one thread).
 template <int N1, bool VISC>
 __device__ __forceinline__ void issue_update_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                    uint64_t* bar) {
   using D = Tma<N1>;
   const int e0 = tile * D::EPB;
   const int n = min(D::EPB, P.E - e0);
-  uint32_t bytes = 2u * n * D::EL * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
+  uint32_t bytes = n * D::EL * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
   for (int le = 0; le < n; ++le)
     for (int s = 0; s < 6; ++s) {
       const int typ = codes[8 * le + s] >> kCodeShift;
@@ -1137,11 +1140,9 @@ __device__ __forceinline__ void issue_update_loads(const FieldPtrs& P, int tile,
     }
   mbar_arrive_expect_tx(bar, bytes);
   double* sU = st;
-  double* sR = st + D::EPB * D::EL;
-  double* sFv = sR + D::EPB * D::EL;
+  double* sFv = sU + D::EPB * D::EL;
   double* sNb = sFv + D::EPB * 6 * D::FS;
   bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
-  bulk_g2s(sR, P.reg + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
   if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D::FS, n * 6u * D::FS * 8u, bar);
   for (int le = 0; le < n; ++le)
     for (int s = 0; s < 6; ++s) {
@@ -1171,10 +1172,365 @@ __device__ __forceinline__ double prolong_aos(const double* __restrict__ s, int 
   return acc;
 }
 
+// BR1 gradient by line tasks: task (d, c, line) loads q along the line once and
+// produces g[3c+d] on all N1 nodes of that line; D-hat, l(+-1) and 1/w enter as
+// compile-time-indexed kernel-parameter (constant bank) operands
+// (assemble_gradients, solver.cpp:729-768).  lift(s, c, f) = lift[s * ls + f * lf + c * lc].
+template <int N1>
+__device__ __forceinline__ void gradient_lines(const ElemConsts& C, const BandD& B, const double* __restrict__ q,
+                                               const double* __restrict__ lift, int ls, const int* lfs, int lc,
+                                               double* __restrict__ g, int t, int nt) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  for (int task = t; task < 12 * N2; task += nt) {
+    const int d = task / (4 * N2), rem = task - d * 4 * N2, c = rem / N2, f = rem - c * N2;
+    const int a = f / N1, b = f - a * N1;
+    const int base = d == 0 ? a * N1 + b : (d == 1 ? a * N2 + b : (a * N1 + b) * N1);
+    const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+    double x[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) x[m] = q[c * N3 + base + m * stride];
+    const double lm = lift[(2 * d) * ls + f * lfs[2 * d] + c * lc];
+    const double lp = lift[(2 * d + 1) * ls + f * lfs[2 * d + 1] + c * lc];
+    const double cd = B.cdir[d];
+    double* out = g + (3 * c + d) * N3 + base;
+#pragma unroll
+    for (int o = 0; o < N1; ++o) {
+      double vol = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) vol += C.dhat[o * kMaxN1 + m] * x[m];
+      const double surf = (lp * C.fr[o] - lm * C.fl[o]) * C.inv_w[o];
+      out[o * stride] = cd * (surf - vol);
+    }
+  }
+}
+
 template <int N1, bool VISC>
-__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_update_tma(const __grid_constant__ ElemConsts C, FieldPtrs P,
-                                                                 StageArgs A) {
+__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tma(const __grid_constant__ ElemConsts C,
+                                                                                  FieldPtrs P, StageArgs A) {
   using D = Tma<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* regb = stage0 + 2 * D::U_STAGE;
+  double* wF = regb + D::U_REG;
+  double* wLift = wF + D::U_WF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wLift + EPB * 24 * N2);
+  __shared__ __align__(16) int codes[2][8 * EPB];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E + EPB - 1) / EPB;
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < tiles) {
+    prefetch_codes<N1>(P, tile, codes[0]);
+    cp_async_wait_all();
+    issue_update_loads<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
+    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
+  }
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    const int sidx = it & 1;
+    double* st = stage0 + sidx * D::U_STAGE;
+    const int next = tile + gridDim.x;
+    const int e0 = tile * EPB;
+    const int n_el = min(EPB, P.E - e0);
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous tile's stores no longer read regb / wF / stage sidx^1
+      fence_proxy_async();
+      if (A.mode == 0) {
+        mbar_arrive_expect_tx(&bars[2], n_el * D::EL * 8u);
+        bulk_g2s(regb, P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u, &bars[2]);
+      }
+      if (next < tiles) {
+        cp_async_wait_all();  // codes of `next`
+        issue_update_loads<N1, VISC>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::U_STAGE,
+                                     &bars[sidx ^ 1]);
+        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
+      }
+    }
+    __syncthreads();
+    const int e = e0 + le;
+    const bool active = e < P.E;
+    double* sU = st + le * D::EL;
+    double* sFv = st + EPB * D::EL + le * 6 * D::FS;
+    double* sNb = st + EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
+    double* sR = regb + le * D::EL;
+    double* w = wF + le * 16 * N3;
+    double* lf = wLift + le * 24 * N2;
+    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+    mbar_wait(&bars[sidx], (it >> 1) & 1);
+
+    // Phase 1: face fluxes (in place over the neighbour data), lift*, q.
+    if (active) {
+      if (VISC) {
+        double u[5], qq[4];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+        prim4(u, C.gas, qq);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[c * N3 + t] = qq[c];
+      }
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        double* nb = sNb + s * D::NB;
+        const int code = P.side_code[8 * e + s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kSliding) {
+          if (VISC) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = nb[D::TS + f * 4 + c];
+          }
+          continue;
+        }
+        double own[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
+        double flux[5], lift[4];
+        bool ok;
+        const double vg = dir == 1 ? B.vg : 0.0;
+        if (typ == kConforming) {
+          double other[5];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
+          const double* um = (s & 1) ? own : other;
+          const double* up = (s & 1) ? other : own;
+          if (VISC) {
+            double qa[4], qb[4];
+            prim4(own, C.gas, qa);
+            prim4(other, C.gas, qb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+            double fa[4], fb[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              fa[c] = sFv[s * D::FS + f * 4 + c];
+              fb[c] = nb[D::TS + f * 4 + c];
+            }
+            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        } else {
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          const double* um = (s & 1) ? own : ext;
+          const double* up = (s & 1) ? ext : own;
+          if (VISC) {
+            prim4(ext, C.gas, lift);
+            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+            double gg[12];
+#pragma unroll
+            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+            double fm[4], fp[4];
+            fv_dir(um, gg, dir, C.gas, fm);
+            fv_dir(up, gg, dir, C.gas, fp);
+            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        }
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
+        if (VISC) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
+        }
+      }
+    }
+    __syncthreads();
+    // Phase 2: gradient (line tasks) into w[4 N3 ..], then pointwise fluxes.
+    if (VISC) {
+      const int one[6] = {1, 1, 1, 1, 1, 1};
+      if (active) gradient_lines<N1>(C, B, w, lf, 4 * N2, one, N2, w + 4 * N3, t, N3);
+      __syncthreads();
+    }
+    double F[3][5], u[5];
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      const double ir = __drcp_rn(u[0]);
+      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+      const double p = pressure(u, ir, C.gas);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double vgd = d == 1 ? B.vg : 0.0;
+        F[d][0] = u[0] * vv[d] - vgd * u[0];
+        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
+        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
+        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
+        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
+      }
+      if (VISC) {
+        double g[12];
+#pragma unroll
+        for (int c = 0; c < 12; ++c) g[c] = w[(4 + c) * N3 + t];
+        const double div = g[0] + g[4] + g[8];
+        const double mu = C.gas.mu, lam = C.gas.lam;
+        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
+                     t22 = 2.0 * mu * g[8] + lam * div;
+        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
+        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          F[d][1] -= tau[d][0];
+          F[d][2] -= tau[d][1];
+          F[d][3] -= tau[d][2];
+          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+        }
+      }
+    }
+    if (VISC) __syncthreads();  // all gradient reads done before F overwrites w
+    if (active) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) w[(d * 5 + v) * N3 + t] = F[d][v] * B.sj[d];
+    }
+    __syncthreads();
+    // Phase 3-5: weak divergence (all directions), surface lift, RK update, admissibility.
+    if (active) {
+      double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      const double* dh = tab;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ia = d == 0 ? i : (d == 1 ? j : k);
+        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          const double c = dh[ia * N1 + m];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) acc[v] += c * w[(d * 5 + v) * N3 + base + m * stride];
+        }
+      }
+      double du[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
+      const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int dir = s >> 1;
+        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
+        if (c != 0.0) {
+          const double* fl = sNb + s * D::NB + f * 5;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
+        }
+      }
+      if (A.mode == 1) {
+        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = du[v];
+      } else {
+        mbar_wait(&bars[2], it & 1);
+        double wv[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
+          wv[v] = u[v] + A.rk_b * rg;
+          sR[t * 5 + v] = rg;
+          sU[t * 5 + v] = wv[v];
+        }
+        const double p = pressure(wv, __drcp_rn(wv[0]), C.gas);
+        bool ok = wv[0] > 0.0 && p > 0.0;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ok = ok && isfinite(wv[v]);
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, wv);
+      }
+    }
+    if (A.mode == 1) {
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    // Phase 6: traces of the new state (into w), then bulk stores of U, reg and traces.
+    if (active) {
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) w[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n_el * D::EL * 8u);
+      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, regb, n_el * D::EL * 8u);
+      for (int l = 0; l < n_el; ++l)
+        bulk_s2g(P.trace + static_cast<size_t>(e0 + l) * 6 * D::TS, wF + l * 16 * N3, 6u * D::TS * 8u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+// Round-1 v2 layout: U and the RK register both double-buffered in the stage.
+template <int N1>
+struct TmaV2 {
+  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  static constexpr int EPB = Tma<N1>::EPB;
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);
+  static constexpr int TAB = Dim<N1>::TAB;
+  static constexpr int EL = 5 * N3, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
+  static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
+  static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
+  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
+};
+
+// Update-kernel loads of one tile (issued by one thread).
+template <int N1, bool VISC>
+__device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int tile, const int* codes, double* st,
+                                                   uint64_t* bar) {
+  using D2 = TmaV2<N1>;
+  const int e0 = tile * D2::EPB;
+  const int n = min(D2::EPB, P.E - e0);
+  uint32_t bytes = 2u * n * D2::EL * 8u + (VISC ? n * 6u * D2::FS * 8u : 0u);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int typ = codes[8 * le + s] >> kCodeShift;
+      if (typ != kDirichlet) bytes += (D2::TS + (VISC ? D2::FS : 0)) * 8u;
+    }
+  mbar_arrive_expect_tx(bar, bytes);
+  double* sU = st;
+  double* sR = st + D2::EPB * D2::EL;
+  double* sFv = sR + D2::EPB * D2::EL;
+  double* sNb = sFv + D2::EPB * 6 * D2::FS;
+  bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u, bar);
+  bulk_g2s(sR, P.reg + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u, bar);
+  if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D2::FS, n * 6u * D2::FS * 8u, bar);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int code = codes[8 * le + s];
+      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+      double* nb = sNb + (le * 6 + s) * D2::NB;
+      if (typ == kConforming) {
+        bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D2::TS, D2::TS * 8u, bar);
+        if (VISC) bulk_g2s(nb + D2::TS, P.fvn + static_cast<size_t>(idx) * D2::FS, D2::FS * 8u, bar);
+      } else if (typ == kSliding) {
+        bulk_g2s(nb, P.slide_flux + static_cast<size_t>(idx) * D2::TS, D2::TS * 8u, bar);
+        if (VISC) bulk_g2s(nb + D2::TS, P.slide_lift + static_cast<size_t>(idx) * D2::FS, D2::FS * 8u, bar);
+      }
+    }
+}
+
+template <int N1, bool VISC>
+__global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_tma_v2(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                                 StageArgs A) {
+  using D = TmaV2<N1>;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
   extern __shared__ __align__(128) double smem[];
   double* tab = smem;
@@ -1196,7 +1552,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_update_tma(
   if (threadIdx.x == 0 && tile < tiles) {
     prefetch_codes<N1>(P, tile, codes[0]);
     cp_async_wait_all();
-    issue_update_loads<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
+    issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
     if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
   }
   double* wF = work;                               // EPB x 5 N3 (q, then F_d, SoA)
@@ -1210,7 +1566,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_update_tma(
     if (threadIdx.x == 0 && next < tiles) {
       cp_async_wait_all();  // codes of `next`
       fence_proxy_async();
-      issue_update_loads<N1, VISC>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::U_STAGE,
+      issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::U_STAGE,
                                    &bars[sidx ^ 1]);
       if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
     }
@@ -1461,21 +1817,52 @@ __device__ __forceinline__ void issue_gradient_loads(const FieldPtrs& P, int til
     }
 }
 
+// Components of the gradient trace that Fv.n along `dir` needs (flux.cpp:23-42):
+// the divergence, the row/column of the velocity gradient and dT/d(dir).
+__host__ __device__ constexpr int fv_comp(int dir, int q) {
+  // dir 0: {0,1,2,3,4,6,8,9}  dir 1: {0,1,3,4,5,7,8,10}  dir 2: {0,2,4,5,6,7,8,11}
+  return dir == 0 ? (q < 5 ? q : (q == 5 ? 6 : (q == 6 ? 8 : 9)))
+                  : dir == 1 ? (q == 0 ? 0 : q == 1 ? 1 : q == 2 ? 3 : q == 3 ? 4 : q == 4 ? 5 : q == 5 ? 7 : q == 6 ? 8 : 10)
+                             : (q == 0 ? 0 : q == 1 ? 2 : q == 2 ? 4 : q == 3 ? 5 : q == 4 ? 6 : q == 5 ? 7 : q == 6 ? 8 : 11);
+}
+
+template <int N1, int DIR>
+__device__ __forceinline__ void fvn_item(const ElemConsts& C, const double* gS, const double* ell, int a, int b,
+                                         const double* own, double* out) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  const int base = DIR == 0 ? a * N1 + b : (DIR == 1 ? a * N2 + b : (a * N1 + b) * N1);
+  constexpr int stride = DIR == 0 ? N2 : (DIR == 1 ? N1 : 1);
+  double gt[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) gt[q] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = fv_comp(DIR, q);
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], gS[c * N3 + base + m * stride], acc);
+    gt[c] = acc;
+  }
+  fv_dir(own, gt, DIR, C.gas, out);
+}
+
 template <int N1>
-__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_gradient_tma(const __grid_constant__ ElemConsts C, FieldPtrs P,
-                                                                   StageArgs A) {
+__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_G) k_gradient_tma(const __grid_constant__ ElemConsts C,
+                                                                                    FieldPtrs P, StageArgs A) {
   using D = Tma<N1>;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
   extern __shared__ __align__(128) double smem[];
   double* tab = smem;
   double* stage0 = smem + D::TAB;
-  double* work = stage0 + 2 * D::G_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::G_WORK);
+  double* wTr = stage0 + 2 * D::G_STAGE;  // EPB x 6 TS (own traces, AoS)
+  double* wQ = wTr + EPB * 6 * D::TS;     // q (SoA), later the Fv.n output (slot layout)
+  double* wG = wQ + D::G_WQ;              // EPB x 12 N3 SoA
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wG + EPB * 12 * N3);
   __shared__ __align__(16) int codes[2][8 * EPB];
+  __shared__ int lstr[EPB][6];
   load_tables<N1>(C, tab);
   const int tiles = (P.E + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -1489,33 +1876,32 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_gradient_tm
     issue_gradient_loads<N1>(P, tile, codes[0], stage0, &bars[0]);
     if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
   }
-  double* wTr = work;                       // EPB x 6 TS (own traces, AoS)
-  double* wLift = wTr + EPB * 6 * D::TS;    // EPB x 24 N2 SoA
-  double* wQ = wLift + EPB * 24 * N2;       // EPB x 4 N3 SoA
-  double* wG = wQ + EPB * 4 * N3;           // EPB x 12 N3 SoA
-  double* wFv = wG + EPB * 12 * N3;         // EPB x 6 FS (global slot layout)
+  constexpr int WQ1 = D::G_WQ / EPB;
   for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
     const int sidx = it & 1;
     double* st = stage0 + sidx * D::G_STAGE;
     const int next = tile + gridDim.x;
-    if (threadIdx.x == 0) bulk_wait_read0();  // the previous Fv.n store has read wFv
-    if (threadIdx.x == 0 && next < tiles) {
-      cp_async_wait_all();
-      fence_proxy_async();
-      issue_gradient_loads<N1>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::G_STAGE, &bars[sidx ^ 1]);
-      if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous Fv.n store has read wQ
+      if (next < tiles) {
+        cp_async_wait_all();
+        fence_proxy_async();
+        issue_gradient_loads<N1>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::G_STAGE, &bars[sidx ^ 1]);
+        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
+      }
     }
+    __syncthreads();
     const int e0 = tile * EPB;
     const int e = e0 + le;
     const bool active = e < P.E;
     double* sU = st + le * D::EL;
     double* sNb = st + EPB * D::EL + le * 6 * D::TS;
     double* tr = wTr + le * 6 * D::TS;
-    double* lf = wLift + le * 24 * N2;
-    double* q = wQ + le * 4 * N3;
+    double* q = wQ + le * WQ1;
     double* gS = wG + le * 12 * N3;
-    double* fvo = wFv + le * 6 * D::FS;
+    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
     mbar_wait(&bars[sidx], (it >> 1) & 1);
+    // Phase 1: q, own traces, lift* (in place over the neighbour slot, stride 5).
     if (active) {
       double u[5], qq[4];
 #pragma unroll
@@ -1533,7 +1919,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_gradient_tm
         for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = own[v];
         const int code = P.side_code[8 * e + s];
         const int typ = code >> kCodeShift;
-        const double* nb = sNb + s * D::TS;
+        double* nb = sNb + s * D::TS;
         double lift[4];
         if (typ == kConforming) {
           double other[5], qa[4], qb[4];
@@ -1544,49 +1930,49 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_gradient_tm
 #pragma unroll
           for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
         } else if (typ == kSliding) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lift[c] = nb[f * 4 + c];
+          if (f == 0) lstr[le][s] = 4;  // back-projected lift* already in place, [N2][4]
+          continue;
         } else {
           double x[3], ext[5];
           face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
           eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
           prim4(ext, C.gas, lift);
         }
+        if (f == 0) lstr[le][s] = 5;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
+        for (int c = 0; c < 4; ++c) nb[f * 5 + c] = lift[c];  // in place over this node's trace
       }
     }
     __syncthreads();
-    if (active) {
-      double g[12];
-      node_gradient<N1>(tab, q, lf, C.bands[P.coords[4 * e]], i, j, k, g);
-#pragma unroll
-      for (int c = 0; c < 12; ++c) gS[c * N3 + t] = g[c];
-      if (P.grad_out != nullptr) {
-        double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
-#pragma unroll
-        for (int c = 0; c < 12; ++c) go[c] = g[c];
-      }
-    }
+    // Phase 2: gradient by line tasks.
+    if (active) gradient_lines<N1>(C, B, q, sNb, D::TS, lstr[le], 1, gS, t, N3);
     __syncthreads();
+    if (active && P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
+    }
+    // Phase 3: Fv.n on conforming sides (8 of the 12 trace components), full
+    // gradient traces on sliding / Dirichlet sides.
+    double* fvo = q;  // q is dead: reuse as the Fv.n output (global slot layout)
     if (active) {
       for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
         const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        double gt[12];
-#pragma unroll
-        for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(gS + c * N3, ell, s >> 1, a, b);
         const int code = P.side_code[8 * e + s];
         const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
         if (typ == kConforming) {
           double fv[4];
-          fv_dir(tr + s * D::TS + f * 5, gt, s >> 1, C.gas, fv);
+          const double* own = tr + s * D::TS + f * 5;
+          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, own, fv);
+          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, own, fv);
+          else fvn_item<N1, 2>(C, gS, ell, a, b, own, fv);
 #pragma unroll
           for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
         } else {
           double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
 #pragma unroll
-          for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+          for (int c = 0; c < 12; ++c) dst[c] = prolong1<N1>(gS + c * N3, ell, dir, a, b);
         }
       }
     }
@@ -1594,7 +1980,8 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB) k_gradient_tm
     __syncthreads();
     if (threadIdx.x == 0) {
       const int n = min(EPB, P.E - e0);
-      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, n * 6u * D::FS * 8u);
+      for (int l = 0; l < n; ++l)
+        bulk_s2g(P.fvn + static_cast<size_t>(e0 + l) * 6 * D::FS, wQ + l * WQ1, 6u * D::FS * 8u);
       bulk_commit();
     }
   }
@@ -1608,16 +1995,24 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
   } else {
     using D = Tma<N1>;
     const int tiles = (p.E + D::EPB - 1) / D::EPB;
-    auto kern = c.gas.viscous ? k_update_tma<N1, true> : k_update_tma<N1, false>;
-    static int occ_v = -1, occ_i = -1;
-    int& occ = c.gas.viscous ? occ_v : occ_i;
+    static int variant = -1;
+    if (variant < 0) {
+      const char* env = std::getenv("SDG_UPDATE_V");
+      variant = env ? std::atoi(env) : 2;
+    }
+    const bool v3 = variant == 3;
+    auto kern = v3 ? (c.gas.viscous ? k_update_tma<N1, true> : k_update_tma<N1, false>)
+                   : (c.gas.viscous ? k_update_tma_v2<N1, true> : k_update_tma_v2<N1, false>);
+    const int smem = v3 ? D::U_SMEM : TmaV2<N1>::U_SMEM;
+    static int occ_tab[4] = {-1, -1, -1, -1};
+    int& occ = occ_tab[(v3 ? 2 : 0) + (c.gas.viscous ? 1 : 0)];
     if (occ < 0) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, D::U_SMEM);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, smem);
       if (occ < 1) occ = 1;
     }
     const int grid = std::min(tiles, n_sm * occ);
-    kern<<<grid, D::THREADS, D::U_SMEM, st>>>(c, p, a);
+    kern<<<grid, D::THREADS, smem, st>>>(c, p, a);
     check_launch("k_update_tma");
     return true;
   }
