@@ -1846,9 +1846,9 @@ __device__ __forceinline__ void fvn_item(const ElemConsts& C, const double* gS, 
   fv_dir(own, gt, DIR, C.gas, out);
 }
 
-template <int N1>
-__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_G) k_gradient_tma(const __grid_constant__ ElemConsts C,
-                                                                                    FieldPtrs P, StageArgs A) {
+template <int N1, int MINB>
+__global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const __grid_constant__ ElemConsts C,
+                                                                        FieldPtrs P, StageArgs A) {
   using D = Tma<N1>;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
   extern __shared__ __align__(128) double smem[];
@@ -2024,14 +2024,22 @@ bool gradient_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a,
   } else {
     using D = Tma<N1>;
     const int tiles = (p.E + D::EPB - 1) / D::EPB;
-    static int occ = -1;
-    if (occ < 0) {
-      cudaFuncSetAttribute(k_gradient_tma<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gradient_tma<N1>, D::THREADS, D::G_SMEM);
-      if (occ < 1) occ = 1;
+    static int minb = -1;
+    if (minb < 0) {
+      const char* env = std::getenv("SDG_GRAD_MINB");
+      minb = env ? std::atoi(env) : D::MINB_G;
+      if (minb != 2 && minb != D::MINB_G) minb = D::MINB_G;
     }
-    const int grid = std::min(tiles, n_sm * occ);
-    k_gradient_tma<N1><<<grid, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+    auto kern = minb == D::MINB_G ? k_gradient_tma<N1, D::MINB_G> : k_gradient_tma<N1, 2>;
+    static int occ[2] = {-1, -1};
+    int& o = occ[minb == D::MINB_G ? 0 : 1];
+    if (o < 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, D::THREADS, D::G_SMEM);
+      if (o < 1) o = 1;
+    }
+    const int grid = std::min(tiles, n_sm * o);
+    kern<<<grid, D::THREADS, D::G_SMEM, st>>>(c, p, a);
     check_launch("k_gradient_tma");
     return true;
   }
