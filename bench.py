@@ -181,36 +181,49 @@ def reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def roofline_update(kt, conf, args, peaks):
-    """Dominant kernel (k_update): algorithmic bytes per launch / mean launch time."""
+def b_flow(degree, curved=False):
+    """algorithmic bytes per DOF-update of the reference's
+    five-pass phase structure (the contract figure)."""
+    n1 = degree + 1
+    return (400 + 2904 / n1) if curved else (240 + 2712 / n1)
+
+
+def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
+    """Contract roofline: achieved = DOF-updates/s x B_flow, over the
+    RK stage (the two fused element kernels + mortar kernels).  Per-kernel
+    numbers of this implementation's own fused dataflow are reported beside it."""
     n1 = args.degree + 1
     n2, n3 = n1 * n1, n1 ** 3
     E = conf["elements_per_gpu"]
-    # U r/w + reg r/w (20 n3) + per face node: neighbour trace 5 + own/neighbour Fv.n 8 + new trace 5
-    bytes_update = 8 * E * (20 * n3 + 6 * n2 * 18)
-    bytes_grad = 8 * E * (5 * n3 + 6 * n2 * 9)
-    ms, cnt = kt.get("update", (0.0, 0))
-    gms, gcnt = kt.get("gradient", (0.0, 0))
-    if cnt == 0:
-        return None, {}
-    t = ms / cnt / 1e3
-    ach = bytes_update / t / 1e9
+    dof = E * n3
+    peak = peaks.get("hbm_gbs", 6650.0)
+    bf = b_flow(args.degree)
+    stage_ms = ms_per_step / 5.0
+    ach = value_per_gpu * bf / 1e9
     traffic = None
-    prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*update_traffic*.json")))
+    prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*stage_traffic*.json")))
     if prof:
         try:
-            traffic = json.load(open(prof[-1])).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof[-1])).get("dram_bytes_per_stage")
         except Exception:
             traffic = None
-    peak = peaks.get("hbm_gbs", 6650.0)
     rl = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
-          "kernel": "k_update", "algorithmic_bytes_per_launch": bytes_update,
-          "mean_launch_ms": t * 1e3, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+          "kernel": "RK stage = k_gradient + k_update + mortar/pairing kernels (one right-hand side + update)",
+          "algorithmic_bytes_per_launch": bf * dof, "bytes_per_dof": bf,
+          "per_unit_source": "SURVEY.md §8(d) B_flow = 240 + 2712/(N+1) B per DOF-update (affine)",
+          "mean_launch_ms": stage_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
     extra = {}
-    if gcnt:
-        gt = gms / gcnt / 1e3
-        extra["k_gradient"] = {"achieved_gbs": bytes_grad / gt / 1e9, "mean_launch_ms": gt * 1e3,
-                               "algorithmic_bytes_per_launch": bytes_grad}
+    # This implementation's fused dataflow (DESIGN.md §4).
+    per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 18), "gradient": 8 * E * (5 * n3 + 6 * n2 * 9)}
+    for name, byts in per_kernel.items():
+        ms, cnt = kt.get(name, (0.0, 0))
+        if cnt:
+            t = ms / cnt / 1e3
+            extra["k_" + name] = {"mean_launch_ms": t * 1e3, "algorithmic_bytes_per_launch": byts,
+                                  "achieved_gbs": byts / t / 1e9, "frac_of_peak": byts / t / 1e9 / peak}
+    fused = (per_kernel["update"] + per_kernel["gradient"]) / dof
+    extra["fused_dataflow_bytes_per_dof"] = fused
+    extra["fused_dataflow_achieved_gbs"] = value_per_gpu * fused / 1e9
     total = sum(v[0] for v in kt.values())
     extra["share_of_step"] = {k: (v[0] / total if total else None) for k, v in kt.items()}
     extra["launches"] = {k: v[1] for k, v in kt.items()}
@@ -282,7 +295,7 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    roof, extra = roofline_update(kt, conf, args, peaks)
+    roof, extra = roofline(kt, conf, args, peaks, value / world, ms_max / args.steps)
 
     # End-to-end through the C-ABI with pinned host buffers: H2D state, step, D2H state.
     e2e = None

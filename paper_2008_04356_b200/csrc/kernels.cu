@@ -365,6 +365,40 @@ __device__ __forceinline__ void node_gradient(const double* tab, const double* s
   }
 }
 
+// Same, with lift*(s, c, f) at nb[s * nbs + off + f * 4 + c] (in place over Fv.n slots).
+template <int N1>
+__device__ __forceinline__ void node_gradient_nb(const double* tab, const double* sq, const double* nb, int nbs,
+                                                 int off, const BandD& B, int i, int j, int k, double* g) {
+  constexpr int N3 = N1 * N1 * N1;
+  const double* dh = tab;
+  const double* fl = tab + N1 * N1;
+  const double* fr = fl + N1;
+  const double* iw = fl + 4 * N1;
+  const double* lx0 = nb + 0 * nbs + off + (j * N1 + k) * 4;
+  const double* lx1 = nb + 1 * nbs + off + (j * N1 + k) * 4;
+  const double* ly0 = nb + 2 * nbs + off + (i * N1 + k) * 4;
+  const double* ly1 = nb + 3 * nbs + off + (i * N1 + k) * 4;
+  const double* lz0 = nb + 4 * nbs + off + (i * N1 + j) * 4;
+  const double* lz1 = nb + 5 * nbs + off + (i * N1 + j) * 4;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* q = sq + c * N3;
+    double vx = 0.0, vy = 0.0, vz = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      vx += dh[i * N1 + m] * q[(m * N1 + j) * N1 + k];
+      vy += dh[j * N1 + m] * q[(i * N1 + m) * N1 + k];
+      vz += dh[k * N1 + m] * q[(i * N1 + j) * N1 + m];
+    }
+    const double sx = (lx1[c] * fr[i] - lx0[c] * fl[i]) * iw[i];
+    const double sy = (ly1[c] * fr[j] - ly0[c] * fl[j]) * iw[j];
+    const double sz = (lz1[c] * fr[k] - lz0[c] * fl[k]) * iw[k];
+    g[3 * c + 0] = B.cdir[0] * (sx - vx);
+    g[3 * c + 1] = B.cdir[1] * (sy - vy);
+    g[3 * c + 2] = B.cdir[2] * (sz - vz);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // k_gradient: lift* -> gradient -> Fv.n (conforming sides) / gradient traces
 // (sliding and Dirichlet sides).  Also serves compute_gradients (grad_out).
@@ -1095,7 +1129,7 @@ struct Tma {
   static constexpr int EPB = N1 == 2 ? 8 : (N1 == 4 ? 2 : 1);
   static constexpr int THREADS = EPB * N3;
   static constexpr int MINB_U = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);  // resident CTAs per SM (shared-memory bound)
-  static constexpr int MINB_G = N1 == 8 ? 1 : (N1 == 6 ? 3 : 2);
+  static constexpr int MINB_G = N1 == 8 ? 1 : 2;
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3;  // state doubles per element
   static constexpr int TS = 5 * N2;  // trace slot
@@ -1109,8 +1143,8 @@ struct Tma {
   static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_REG + U_WORK) * 8 + 64;
   // gradient: double-buffered {U, neighbour trace|lift}; own traces; q (then Fv.n out); gradient
   static constexpr int G_STAGE = EPB * (EL + 6 * TS);
-  static constexpr int G_WQ = EPB * (4 * N3 > 6 * FS ? 4 * N3 : 6 * FS);
-  static constexpr int G_WORK = EPB * 6 * TS + G_WQ + EPB * 12 * N3;
+  static constexpr int G_WQ = EPB * 4 * N3;
+  static constexpr int G_WORK = EPB * 6 * TS + G_WQ + EPB * 12 * N3 + EPB * 6 * FS;
   static constexpr int G_SMEM = (TAB + 2 * G_STAGE + G_WORK) * 8 + 64;
   static_assert(EL % 2 == 0 && TS % 2 == 0, "TMA path needs 16-byte blocks");
 };
@@ -1204,7 +1238,7 @@ __device__ __forceinline__ void gradient_lines(const ElemConsts& C, const BandD&
   }
 }
 
-template <int N1, bool VISC>
+template <int N1, bool VISC, bool LINES>
 __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tma(const __grid_constant__ ElemConsts C,
                                                                                   FieldPtrs P, StageArgs A) {
   using D = Tma<N1>;
@@ -1349,7 +1383,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
     }
     __syncthreads();
     // Phase 2: gradient (line tasks) into w[4 N3 ..], then pointwise fluxes.
-    if (VISC) {
+    if (VISC && LINES) {
       const int one[6] = {1, 1, 1, 1, 1, 1};
       if (active) gradient_lines<N1>(C, B, w, lf, 4 * N2, one, N2, w + 4 * N3, t, N3);
       __syncthreads();
@@ -1372,8 +1406,12 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
       }
       if (VISC) {
         double g[12];
+        if (LINES) {
 #pragma unroll
-        for (int c = 0; c < 12; ++c) g[c] = w[(4 + c) * N3 + t];
+          for (int c = 0; c < 12; ++c) g[c] = w[(4 + c) * N3 + t];
+        } else {
+          node_gradient<N1>(tab, w, lf, B, i, j, k, g);
+        }
         const double div = g[0] + g[4] + g[8];
         const double mu = C.gas.mu, lam = C.gas.lam;
         const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
@@ -1857,7 +1895,8 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
   double* wTr = stage0 + 2 * D::G_STAGE;  // EPB x 6 TS (own traces, AoS)
   double* wQ = wTr + EPB * 6 * D::TS;     // q (SoA), later the Fv.n output (slot layout)
   double* wG = wQ + D::G_WQ;              // EPB x 12 N3 SoA
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wG + EPB * 12 * N3);
+  double* wFv = wG + EPB * 12 * N3;       // EPB x 6 FS Fv.n output (global slot layout)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wFv + EPB * 6 * D::FS);
   __shared__ __align__(16) int codes[2][8 * EPB];
   __shared__ int lstr[EPB][6];
   load_tables<N1>(C, tab);
@@ -1882,7 +1921,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
     double* st = stage0 + sidx * D::G_STAGE;
     const int next = tile + gridDim.x;
     if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous Fv.n store has read wQ
+      bulk_wait_read0();  // the previous Fv.n store has read wFv (rewritten two barriers later)
       if (next < tiles) {
         cp_async_wait_all();
         fence_proxy_async();
@@ -1890,7 +1929,6 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
         if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
       }
     }
-    __syncthreads();
     const int e0 = tile * EPB;
     const int e = e0 + le;
     const bool active = e < P.E;
@@ -1954,7 +1992,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
     }
     // Phase 3: Fv.n on conforming sides (8 of the 12 trace components), full
     // gradient traces on sliding / Dirichlet sides.
-    double* fvo = q;  // q is dead: reuse as the Fv.n output (global slot layout)
+    double* fvo = wFv + le * 6 * D::FS;
     if (active) {
       for (int itm = t; itm < 6 * N2; itm += N3) {
         const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
@@ -1980,12 +2018,544 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
     __syncthreads();
     if (threadIdx.x == 0) {
       const int n = min(EPB, P.E - e0);
-      for (int l = 0; l < n; ++l)
-        bulk_s2g(P.fvn + static_cast<size_t>(e0 + l) * 6 * D::FS, wQ + l * WQ1, 6u * D::FS * 8u);
+      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, n * 6u * D::FS * 8u);
       bulk_commit();
     }
   }
   if (threadIdx.x == 0) bulk_wait0();
+}
+
+// ============================================================================
+// v5 element kernels.  Differences from the kernels above:
+//  * the element's own face traces are staged by TMA (the slots the previous
+//    k_update wrote) instead of being recomputed — the own trace is then the
+//    very bits every neighbour reads;
+//  * side codes and the band index come from the cp.async-prefetched copy in
+//    shared memory (three rotating buffers), no global loads in the tile loop;
+//  * the RK register is single-buffered (own mbarrier, loaded during the tile);
+//  * new face traces are written in place over the consumed own-trace stage
+//    and bulk-stored; prolongation directions are compile-time.
+// ============================================================================
+template <int N1>
+struct T5 {
+  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  static constexpr int EPB = Tma<N1>::EPB;
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);
+  static constexpr int TAB = Dim<N1>::TAB;
+  static constexpr int EL = 5 * N3, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
+  // update stage: U | reg | own traces | own Fv.n | neighbour (trace|flux, Fv.n|lift)
+  static constexpr int U_STAGE = EPB * (2 * EL + 6 * TS + 6 * FS + 6 * NB);
+  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + EPB * 5 * N3) * 8 + 64;
+  // gradient stage: U | own traces | neighbour (trace|lift)
+  static constexpr int G_STAGE = EPB * (EL + 12 * TS);
+  static constexpr int G_SMEM = (TAB + 2 * G_STAGE + EPB * 4 * N3 + EPB * 12 * N3 + EPB * 6 * FS) * 8 + 64;
+};
+
+template <int N1, int DIR>
+__device__ __forceinline__ double prolong_aos_d(const double* __restrict__ s, int v, const double* __restrict__ ell,
+                                                int a, int b) {
+  constexpr int N2 = N1 * N1;
+  const int base = DIR == 0 ? a * N1 + b : (DIR == 1 ? a * N2 + b : (a * N1 + b) * N1);
+  constexpr int stride = DIR == 0 ? N2 : (DIR == 1 ? N1 : 1);
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[(base + m * stride) * 5 + v], acc);
+  return acc;
+}
+
+// New face traces of one element (AoS state in, trace slots out).
+template <int N1>
+__device__ __forceinline__ void write_traces(const double* tab, const double* sU, double* tr, int t, int nt) {
+  constexpr int N2 = N1 * N1, TS = 5 * N2;
+  for (int itm = t; itm < 6 * N2; itm += nt) {
+    const int s = itm / N2, f = itm - s * N2, a = f / N1, b = f - a * N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double* o = tr + s * TS + f * 5;
+    switch (s >> 1) {
+      case 0:
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = prolong_aos_d<N1, 0>(sU, v, ell, a, b);
+        break;
+      case 1:
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = prolong_aos_d<N1, 1>(sU, v, ell, a, b);
+        break;
+      default:
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = prolong_aos_d<N1, 2>(sU, v, ell, a, b);
+    }
+  }
+}
+
+template <int N1, bool VISC>
+__device__ __forceinline__ void issue_update_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
+                                                    uint64_t* bar) {
+  using D = T5<N1>;
+  const int e0 = tile * D::EPB;
+  const int n = min(D::EPB, P.E - e0);
+  uint32_t bytes = n * (2u * D::EL + 6u * D::TS) * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s)
+      if ((codes[8 * le + s] >> kCodeShift) != kDirichlet) bytes += (D::TS + (VISC ? D::FS : 0)) * 8u;
+  mbar_arrive_expect_tx(bar, bytes);
+  double* sU = st;
+  double* sRg = sU + D::EPB * D::EL;
+  double* sTr = sRg + D::EPB * D::EL;
+  double* sFv = sTr + D::EPB * 6 * D::TS;
+  double* sNb = sFv + D::EPB * 6 * D::FS;
+  bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
+  bulk_g2s(sRg, P.reg + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
+  bulk_g2s(sTr, P.trace + static_cast<size_t>(e0) * 6 * D::TS, n * 6u * D::TS * 8u, bar);
+  if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D::FS, n * 6u * D::FS * 8u, bar);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int code = codes[8 * le + s];
+      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+      double* nb = sNb + (le * 6 + s) * D::NB;
+      if (typ == kConforming) {
+        bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        if (VISC) bulk_g2s(nb + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+      } else if (typ == kSliding) {
+        bulk_g2s(nb, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        if (VISC) bulk_g2s(nb + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+      }
+    }
+}
+
+template <int N1, bool VISC>
+__global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const __grid_constant__ ElemConsts C,
+                                                                          FieldPtrs P, StageArgs A) {
+  using D = T5<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* wF = stage0 + 2 * D::U_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wF + EPB * 5 * N3);
+  __shared__ __align__(16) int codes[3][8 * EPB];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E + EPB - 1) / EPB;
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < tiles) {
+    prefetch_codes<N1>(P, tile, codes[0]);
+    cp_async_wait_all();
+    issue_update_loads5<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
+    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
+  }
+  __syncthreads();  // codes[0] visible to every thread
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    const int sidx = it & 1;
+    double* st = stage0 + sidx * D::U_STAGE;
+    const int next = tile + gridDim.x;
+    const int e0 = tile * EPB;
+    const int n_el = min(EPB, P.E - e0);
+    const int* cd = codes[it % 3];
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous tile's stores have read stage sidx^1
+      fence_proxy_async();
+      if (next < tiles) {
+        cp_async_wait_all();  // codes of `next`
+        issue_update_loads5<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::U_STAGE,
+                                      &bars[sidx ^ 1]);
+        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
+      }
+    }
+    const int e = e0 + le;
+    const bool active = le < n_el;
+    double* sU = st + le * D::EL;
+    double* sR = st + EPB * D::EL + le * D::EL;
+    double* sTr = st + EPB * 2 * D::EL + le * 6 * D::TS;
+    double* sFv = st + EPB * (2 * D::EL + 6 * D::TS) + le * 6 * D::FS;
+    double* sNb = st + EPB * (2 * D::EL + 6 * D::TS + 6 * D::FS) + le * 6 * D::NB;
+    double* q = wF + le * 5 * N3;
+    const int* myc = cd + 8 * le;
+    const BandD& B = C.bands[active ? myc[6] : 0];
+    mbar_wait(&bars[sidx], (it >> 1) & 1);
+
+    // Phase 1: face fluxes (in place over the neighbour data) and lift*.
+    if (active) {
+      if (VISC) {
+        double u[5], qq[4];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+        prim4(u, C.gas, qq);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+      }
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm - s * N2, dir = s >> 1;
+        double* nb = sNb + s * D::NB;
+        const int code = myc[s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kSliding) continue;  // flux and lift* arrived in place
+        double own[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) own[v] = sTr[s * D::TS + f * 5 + v];
+        double flux[5], lift[4];
+        bool ok;
+        const double vg = dir == 1 ? B.vg : 0.0;
+        if (typ == kConforming) {
+          double other[5];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
+          const double* um = (s & 1) ? own : other;
+          const double* up = (s & 1) ? other : own;
+          if (VISC) {
+            double qa[4], qb[4];
+            prim4(own, C.gas, qa);
+            prim4(other, C.gas, qb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+            double fa[4], fb[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              fa[c] = sFv[s * D::FS + f * 4 + c];
+              fb[c] = nb[D::TS + f * 4 + c];
+            }
+            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        } else {
+          const int a = f / N1, b = f - (f / N1) * N1;
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          const double* um = (s & 1) ? own : ext;
+          const double* up = (s & 1) ? ext : own;
+          if (VISC) {
+            prim4(ext, C.gas, lift);
+            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+            double gg[12];
+#pragma unroll
+            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+            double fm[4], fp[4];
+            fv_dir(um, gg, dir, C.gas, fm);
+            fv_dir(up, gg, dir, C.gas, fp);
+            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        }
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
+        if (VISC) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) nb[D::TS + f * 4 + c] = lift[c];
+        }
+      }
+    }
+    __syncthreads();
+
+    // Phase 2: pointwise volume flux (gradient recomputed from q and lift*).
+    double F[3][5], u[5];
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      const double ir = __drcp_rn(u[0]);
+      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+      const double p = pressure(u, ir, C.gas);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double vgd = d == 1 ? B.vg : 0.0;
+        F[d][0] = u[0] * vv[d] - vgd * u[0];
+        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
+        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
+        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
+        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
+      }
+      if (VISC) {
+        double g[12];
+        node_gradient_nb<N1>(tab, q, sNb, D::NB, D::TS, B, i, j, k, g);
+        const double div = g[0] + g[4] + g[8];
+        const double mu = C.gas.mu, lam = C.gas.lam;
+        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
+                     t22 = 2.0 * mu * g[8] + lam * div;
+        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
+        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          F[d][1] -= tau[d][0];
+          F[d][2] -= tau[d][1];
+          F[d][3] -= tau[d][2];
+          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+        }
+      }
+    }
+
+    // Phase 3: weak divergence per direction through shared memory.
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      __syncthreads();
+      if (active) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) q[v * N3 + t] = F[d][v] * B.sj[d];
+      }
+      __syncthreads();
+      if (active) {
+        const int ia = d == 0 ? i : (d == 1 ? j : k);
+        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          const double c = tab[ia * N1 + m];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
+        }
+      }
+    }
+
+    // Phase 4-5: surface lift, RK update in place, admissibility.
+    if (active) {
+      double du[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
+      const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int dir = s >> 1;
+        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
+        if (c != 0.0) {
+          const double* fl = sNb + s * D::NB + f * 5;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
+        }
+      }
+      if (A.mode == 1) {
+        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = du[v];
+      } else {
+        double wv[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
+          wv[v] = u[v] + A.rk_b * rg;
+          sR[t * 5 + v] = rg;
+          sU[t * 5 + v] = wv[v];
+        }
+        const double p = pressure(wv, __drcp_rn(wv[0]), C.gas);
+        bool ok = wv[0] > 0.0 && p > 0.0;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ok = ok && isfinite(wv[v]);
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, wv);
+      }
+    }
+    __syncthreads();
+    if (A.mode == 1) continue;
+    // Phase 6: traces of the new state in place over the consumed own traces.
+    if (active) write_traces<N1>(tab, sU, sTr, t, N3);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n_el * D::EL * 8u);
+      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n_el * D::EL * 8u);
+      bulk_s2g(P.trace + static_cast<size_t>(e0) * 6 * D::TS, st + EPB * 2 * D::EL, n_el * 6u * D::TS * 8u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+template <int N1>
+__device__ __forceinline__ void issue_gradient_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
+                                                      uint64_t* bar) {
+  using D = T5<N1>;
+  const int e0 = tile * D::EPB;
+  const int n = min(D::EPB, P.E - e0);
+  uint32_t bytes = n * (D::EL + 6u * D::TS) * 8u;
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int typ = codes[8 * le + s] >> kCodeShift;
+      if (typ == kConforming) bytes += D::TS * 8u;
+      else if (typ == kSliding) bytes += D::FS * 8u;
+    }
+  mbar_arrive_expect_tx(bar, bytes);
+  bulk_g2s(st, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
+  bulk_g2s(st + D::EPB * D::EL, P.trace + static_cast<size_t>(e0) * 6 * D::TS, n * 6u * D::TS * 8u, bar);
+  double* sNb = st + D::EPB * (D::EL + 6 * D::TS);
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int code = codes[8 * le + s];
+      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+      double* nb = sNb + (le * 6 + s) * D::TS;
+      if (typ == kConforming) bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+      else if (typ == kSliding) bulk_g2s(nb, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+    }
+}
+
+template <int N1>
+__global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(const __grid_constant__ ElemConsts C,
+                                                                            FieldPtrs P, StageArgs A) {
+  using D = T5<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* wQ = stage0 + 2 * D::G_STAGE;  // EPB x 4 N3
+  double* wG = wQ + EPB * 4 * N3;        // EPB x 12 N3
+  double* wFv = wG + EPB * 12 * N3;      // EPB x 6 FS
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wFv + EPB * 6 * D::FS);
+  __shared__ __align__(16) int codes[3][8 * EPB];
+  __shared__ int lstr[EPB][6];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E + EPB - 1) / EPB;
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < tiles) {
+    prefetch_codes<N1>(P, tile, codes[0]);
+    cp_async_wait_all();
+    issue_gradient_loads5<N1>(P, tile, codes[0], stage0, &bars[0]);
+    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
+  }
+  __syncthreads();
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    const int sidx = it & 1;
+    double* st = stage0 + sidx * D::G_STAGE;
+    const int next = tile + gridDim.x;
+    const int e0 = tile * EPB;
+    const int n_el = min(EPB, P.E - e0);
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous Fv.n store has read wFv
+      if (next < tiles) {
+        cp_async_wait_all();
+        fence_proxy_async();
+        issue_gradient_loads5<N1>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::G_STAGE, &bars[sidx ^ 1]);
+        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
+      }
+    }
+    const int e = e0 + le;
+    const bool active = le < n_el;
+    const int* myc = codes[it % 3] + 8 * le;
+    double* sU = st + le * D::EL;
+    double* sTr = st + EPB * D::EL + le * 6 * D::TS;
+    double* sNb = st + EPB * (D::EL + 6 * D::TS) + le * 6 * D::TS;
+    double* q = wQ + le * 4 * N3;
+    double* gS = wG + le * 12 * N3;
+    double* fvo = wFv + le * 6 * D::FS;
+    const BandD& B = C.bands[active ? myc[6] : 0];
+    mbar_wait(&bars[sidx], (it >> 1) & 1);
+    // Phase 1: q; lift* in place over the neighbour slot (stride 5), sliding lift* stays at stride 4.
+    if (active) {
+      double u[5], qq[4];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      prim4(u, C.gas, qq);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm - s * N2;
+        const int typ = myc[s] >> kCodeShift;
+        double* nb = sNb + s * D::TS;
+        if (typ == kSliding) {
+          if (f == 0) lstr[le][s] = 4;
+          continue;
+        }
+        double lift[4];
+        const double* own = sTr + s * D::TS + f * 5;
+        if (typ == kConforming) {
+          double ow[5], other[5], qa[4], qb[4];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            ow[v] = own[v];
+            other[v] = nb[f * 5 + v];
+          }
+          prim4(ow, C.gas, qa);
+          prim4(other, C.gas, qb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+        } else {
+          const int a = f / N1, b = f - (f / N1) * N1;
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          prim4(ext, C.gas, lift);
+        }
+        if (f == 0) lstr[le][s] = 5;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) nb[f * 5 + c] = lift[c];
+      }
+    }
+    __syncthreads();
+    if (active) gradient_lines<N1>(C, B, q, sNb, D::TS, lstr[le], 1, gS, t, N3);
+    __syncthreads();
+    if (active && P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
+    }
+    // Phase 3: Fv.n on conforming sides; full gradient traces on sliding / Dirichlet sides.
+    if (active) {
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm - s * N2, a = f / N1, b = f - a * N1, dir = s >> 1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        const int code = myc[s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kConforming) {
+          double fv[4];
+          const double* own = sTr + s * D::TS + f * 5;
+          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, own, fv);
+          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, own, fv);
+          else fvn_item<N1, 2>(C, gS, ell, a, b, own, fv);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
+        } else {
+          double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+          for (int c = 0; c < 12; ++c) dst[c] = prolong1<N1>(gS + c * N3, ell, dir, a, b);
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, n_el * 6u * D::FS * 8u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+template <int N1>
+bool v5_t(bool update, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = T5<N1>;
+    const int tiles = (p.E + D::EPB - 1) / D::EPB;
+    auto kern = update ? (c.gas.viscous ? k_update5<N1, true> : k_update5<N1, false>) : k_gradient5<N1>;
+    const int smem = update ? D::U_SMEM : D::G_SMEM;
+    static int occ_tab[3] = {-1, -1, -1};
+    int& occ = occ_tab[update ? (c.gas.viscous ? 1 : 2) : 0];
+    if (occ < 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, smem);
+      if (occ < 1) occ = 1;
+    }
+    const int grid = std::min(tiles, n_sm * occ);
+    kern<<<grid, D::THREADS, smem, st>>>(c, p, a);
+    check_launch(update ? "k_update5" : "k_gradient5");
+    return true;
+  }
 }
 
 template <int N1>
@@ -2000,12 +2570,13 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
       const char* env = std::getenv("SDG_UPDATE_V");
       variant = env ? std::atoi(env) : 2;
     }
-    const bool v3 = variant == 3;
-    auto kern = v3 ? (c.gas.viscous ? k_update_tma<N1, true> : k_update_tma<N1, false>)
-                   : (c.gas.viscous ? k_update_tma_v2<N1, true> : k_update_tma_v2<N1, false>);
+    const bool v3 = variant == 3 || variant == 4;
+    auto kern = variant == 3 ? (c.gas.viscous ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
+              : variant == 4 ? (c.gas.viscous ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
+                             : (c.gas.viscous ? k_update_tma_v2<N1, true> : k_update_tma_v2<N1, false>);
     const int smem = v3 ? D::U_SMEM : TmaV2<N1>::U_SMEM;
-    static int occ_tab[4] = {-1, -1, -1, -1};
-    int& occ = occ_tab[(v3 ? 2 : 0) + (c.gas.viscous ? 1 : 0)];
+    static int occ_tab[6] = {-1, -1, -1, -1, -1, -1};
+    int& occ = occ_tab[(variant == 3 ? 2 : variant == 4 ? 4 : 0) + (c.gas.viscous ? 1 : 0)];
     if (occ < 0) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, smem);
@@ -2129,10 +2700,19 @@ void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageA
   if (p.E == 0) return;
   SDG_DISPATCH(n1, (update_t<NN>(c, p, a, st)));
 }
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
 bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                          cudaStream_t st) {
   if (p.E == 0) return true;
   bool ok = false;
+  static const int gv = env_int("SDG_GRAD_V", 5);
+  if (gv == 5) {
+    SDG_DISPATCH(n1, (ok = v5_t<NN>(false, c, p, a, n_sm, st)));
+    return ok;
+  }
   SDG_DISPATCH(n1, (ok = gradient_tma_t<NN>(c, p, a, n_sm, st)));
   return ok;
 }
@@ -2140,6 +2720,11 @@ bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const St
                        cudaStream_t st) {
   if (p.E == 0) return true;
   bool ok = false;
+  static const int uv = env_int("SDG_UPDATE_V", 2);
+  if (uv == 5) {
+    SDG_DISPATCH(n1, (ok = v5_t<NN>(true, c, p, a, n_sm, st)));
+    return ok;
+  }
   SDG_DISPATCH(n1, (ok = update_tma_t<NN>(c, p, a, n_sm, st)));
   return ok;
 }

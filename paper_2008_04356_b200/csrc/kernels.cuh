@@ -57,7 +57,7 @@ struct FieldPtrs {
   const int8_t* side_type;   // E x 6
   const int* side_idx;       // E x 6
   const int* coords;         // E x 4 (band, ix, iy, iz)
-  const int* side_code;      // E x 8: idx | type << 29 for the 6 sides (+2 pad), 32 B per element
+  const int* side_code;      // E x 8: idx | type << 29 for the 6 sides, [6] = band, [7] pad (32 B/element)
   double* grad_out;          // optional E x N3 x 12
   ErrRec* err;
   int E;

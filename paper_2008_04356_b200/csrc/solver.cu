@@ -298,6 +298,7 @@ void GpuRankSolver::upload_topology() {
         if (idx < 0 || idx >= (1 << 29)) throw ConfigError("face index exceeds the side-code range");
         code[8 * e + q] = idx | (static_cast<int>(topo_.side_type[6 * e + q]) << 29);
       }
+    for (int e = 0; e < E_; ++e) code[8 * e + 6] = topo_.coords[4 * e];  // band of the element
     side_code_.upload(code, stream_);
   }
   coords_.upload(topo_.coords, stream_);
