@@ -108,6 +108,16 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
                        long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
                        int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry);
 
+/* Diagnostics on the device (integrate_mass_energy / error_norms /
+ * max_freestream_deviation, diagnostics.cpp:31-87): out[14] = mass, energy,
+ * volume, L2 error[5], Linf error[5], max deviation; the errors are against the
+ * exact case state at time t when with_exact != 0 (else zero). */
+int sdg_diagnostics(sdg_ctx* ctx, double t, int with_exact, double* out);
+/* SDGFLD1 snapshot of the global field (write_snapshot / read_snapshot,
+ * snapshot.cpp:10-56) with a 3D header; collective over ranks. */
+int sdg_write_snapshot(sdg_ctx* ctx, const char* path, double time);
+int sdg_read_snapshot(sdg_ctx* ctx, const char* path, double* time);
+
 /* Host-only partition / message plan of one rank (no GPU needed): JSON with the
  * local elements, the conforming halo peers and face keys in send order, and
  * the per-partner mortar blocks of both roles at interface displacement

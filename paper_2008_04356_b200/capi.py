@@ -75,6 +75,9 @@ def lib():
         L.sdg_pairing_device.argtypes = [C.c_int, _lp, C.c_long, C.c_long, _ip, C.c_long, C.c_int, C.c_int,
                                          C.c_int, _ip, _ip, _ip, _lp, _ip, _ip, _ip]
         L.sdg_plan_json.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_double, C.c_char_p, C.c_long, _lp]
+        L.sdg_diagnostics.argtypes = [_vp, C.c_double, C.c_int, _dp]
+        L.sdg_write_snapshot.argtypes = [_vp, C.c_char_p, C.c_double]
+        L.sdg_read_snapshot.argtypes = [_vp, C.c_char_p, _dp]
         L.sdg_stream.argtypes = [_vp]
         L.sdg_stream.restype = C.c_void_p
         L.sdg_kernel_launches.argtypes = [_vp]
@@ -92,7 +95,8 @@ EXPORTED = [
     "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
-    "sdg_pairing_device", "sdg_plan_json", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
+    "sdg_pairing_device", "sdg_plan_json", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
+    "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
 
@@ -226,6 +230,21 @@ class RankSolver:
         g = np.zeros(self.n_elements, dtype=np.int64)
         self.lib.sdg_local_element_ids(self.h, g.ctypes.data_as(_lp))
         return g
+
+    def diagnostics(self, t: float, exact: bool = True) -> dict:
+        """Device integrals and error norms (diagnostics.cpp:31-87)."""
+        out = np.zeros(14)
+        self._check(self.lib.sdg_diagnostics(self.h, t, int(exact), _d(out)))
+        return dict(mass=out[0], energy=out[1], volume=out[2], l2=out[3:8].copy(), linf=out[8:13].copy(),
+                    max_deviation=out[13])
+
+    def write_snapshot(self, path: str, time: float | None = None):
+        self._check(self.lib.sdg_write_snapshot(self.h, path.encode(), self.time() if time is None else time))
+
+    def read_snapshot(self, path: str) -> float:
+        t = C.c_double()
+        self._check(self.lib.sdg_read_snapshot(self.h, path.encode(), C.byref(t)))
+        return t.value
 
     # --- instrumentation -------------------------------------------------------
     def stream(self) -> int:

@@ -1043,6 +1043,65 @@ __global__ void k_mortar_flux(GasD g, MortarPtrs P, int max_mortars, ErrRec* err
   for (int v = 0; v < 5; ++v) P.flux[0][q * 5 + v] = f[v];
 }
 
+
+// ----------------------------------------------------------------------------
+// Diagnostics: quadrature integrals of mass and energy and the L2 / Linf
+// error against the exact case state (diagnostics.cpp:31-87).  Each block
+// reduces in a fixed tree and writes its partials; the host sums the
+// partials in block order, so results are run-to-run reproducible.
+// ----------------------------------------------------------------------------
+template <int N1>
+__global__ void __launch_bounds__(256) k_diag(const __grid_constant__ ElemConsts C, FieldPtrs P, double t,
+                                              int with_exact, double* partial) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  double a[kDiagVals];
+#pragma unroll
+  for (int q = 0; q < kDiagVals; ++q) a[q] = 0.0;
+  const long long nodes = static_cast<long long>(P.E) * N3;
+  for (long long nd = blockIdx.x * 256LL + threadIdx.x; nd < nodes; nd += 256LL * gridDim.x) {
+    const int e = static_cast<int>(nd / N3), r = static_cast<int>(nd % N3);
+    const int i = r / N2, j = (r / N1) % N1, k = r % N1;
+    const int* crd = P.coords + 4 * e;
+    const BandD& B = C.bands[crd[0]];
+    const double wq = C.w[i] * C.w[j] * C.w[k] * B.jac;
+    const double* u = P.U + nd * 5;
+    a[0] += wq * u[0];
+    a[1] += wq * u[4];
+    a[2] += wq;
+    if (with_exact) {
+      double x[3], ex[5];
+      x[0] = (B.x_lo + crd[1] * B.hx) + 0.5 * (C.x[i] + 1.0) * B.hx;
+      x[1] = (C.y0 + crd[2] * B.hy) + 0.5 * (C.x[j] + 1.0) * B.hy + B.vg * t;
+      x[2] = (C.z0 + crd[3] * B.hz) + 0.5 * (C.x[k] + 1.0) * B.hz;
+      eval_case(C.flow_case, x, t, C.gas, ex);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double d = u[v] - ex[v];
+        a[3 + v] += wq * d * d;
+        a[8 + v] = fmax(a[8 + v], fabs(d));
+      }
+    }
+  }
+  __shared__ double red[8][kDiagVals];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kDiagVals; ++q) {
+    double v = a[q];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_down_sync(0xffffffffu, v, o);
+      v = (q >= 8 && q < 13) ? fmax(v, y) : v + y;
+    }
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kDiagVals) {
+    const int q = threadIdx.x;
+    double v = red[0][q];
+    for (int w = 1; w < 8; ++w) v = (q >= 8 && q < 13) ? fmax(v, red[w][q]) : v + red[w][q];
+    partial[static_cast<size_t>(blockIdx.x) * kDiagVals + q] = v;
+  }
+}
+
 template <int N1>
 int smem_gradient() {
   constexpr int N2 = N1 * N1, N3 = N2 * N1;
@@ -2758,6 +2817,14 @@ void launch_mortar_flux(int n1, const GasD& g, int viscous, const MortarPtrs& p,
     SDG_DISPATCH(n1, (k_mortar_flux<NN, false><<<blocks, bs, 0, st>>>(g, p, max_mortars, err)));
   }
   check_launch("k_mortar_flux");
+}
+int launch_diagnostics(int n1, const ElemConsts& c, const FieldPtrs& p, double t, int with_exact, double* partial,
+                       int max_blocks, cudaStream_t st) {
+  const long long nodes = static_cast<long long>(p.E) * n1 * n1 * n1;
+  const int blocks = static_cast<int>(std::max(1LL, std::min<long long>(max_blocks, (nodes + 255) / 256)));
+  SDG_DISPATCH(n1, (k_diag<NN><<<blocks, 256, 0, st>>>(c, p, t, with_exact, partial)));
+  check_launch("k_diag");
+  return blocks;
 }
 void launch_suggest_dt(int n1, const ElemConsts& c, const FieldPtrs& p, double cfl, int degree,
                        unsigned long long* out, cudaStream_t st) {

@@ -17,7 +17,7 @@ struct GasD {
 
 struct BandD {
   double x_lo, hx, hy, hz, vg;
-  double inv_jac;
+  double jac, inv_jac;
   double cdir[3];  // sJ_d / J
   double sj[3];    // sJ_d
 };
@@ -28,6 +28,7 @@ struct ElemConsts {
   double fl[kMaxN1], fr[kMaxN1];  // l_j(-1), l_j(+1)
   double liftw[2][kMaxN1];        // l_j(-+1) / w_j
   double inv_w[kMaxN1];
+  double w[kMaxN1];
   double x[kMaxN1];
   BandD bands[SDG_MAX_BANDS];
   GasD gas;
@@ -157,6 +158,11 @@ void launch_mortar_backproject(int n1, int ncomp, const double* const src[2], do
                                const MortarPtrs& p, cudaStream_t st);
 void launch_mortar_flux(int n1, const GasD& g, int viscous, const MortarPtrs& p, int max_mortars, ErrRec* err,
                         cudaStream_t st);
+// Diagnostics (diagnostics.cpp:31-87): per-block partial sums of mass, energy,
+// volume and squared errors, and maxima of |errors| — kDiagVals per block.
+constexpr int kDiagVals = 14;
+int launch_diagnostics(int n1, const ElemConsts& c, const FieldPtrs& p, double t, int with_exact, double* partial,
+                       int max_blocks, cudaStream_t st);
 void launch_suggest_dt(int n1, const ElemConsts& c, const FieldPtrs& p, double cfl, int degree,
                        unsigned long long* out, cudaStream_t st);
 

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -107,6 +108,9 @@ class GpuRankSolver {
   void compute_residual(double t_stage, const double* d_u, double* d_dudt);
   void compute_gradients(double t_stage, const double* d_u, double* d_grad);
   double suggest_dt(double cfl);
+  void diagnostics(double t, int with_exact, double* out);
+  void write_snapshot(const char* path, double time);
+  double read_snapshot(const char* path);
   long total_rebuilds() const {
     long t = 0;
     for (const auto& s : sides_) t += s.rebuilds;
@@ -166,6 +170,7 @@ class GpuRankSolver {
   DevBuf<ErrRec> err_;
   ErrRec* err_host_ = nullptr;
   DevBuf<unsigned long long> dt_min_;
+  DevBuf<double> diag_partial_;
   DevBuf<double> send_buf_;
   DevBuf<int> send_slots_;
 
@@ -248,6 +253,7 @@ void GpuRankSolver::build_consts() {
     consts_.liftw[0][i] = basis_.fl[i] / basis_.w[i];
     consts_.liftw[1][i] = basis_.fr[i] / basis_.w[i];
     consts_.inv_w[i] = 1.0 / basis_.w[i];
+    consts_.w[i] = basis_.w[i];
     consts_.x[i] = basis_.x[i];
   }
   for (size_t b = 0; b < mesh_.bands.size(); ++b) {
@@ -259,6 +265,7 @@ void GpuRankSolver::build_consts() {
     d.hz = bg.hz;
     d.vg = bg.vg;
     const double jac = 0.125 * bg.hx * bg.hy * bg.hz;
+    d.jac = jac;
     d.inv_jac = 1.0 / jac;
     d.sj[0] = 0.25 * bg.hy * bg.hz;
     d.sj[1] = 0.25 * bg.hx * bg.hz;
@@ -931,6 +938,122 @@ double GpuRankSolver::suggest_dt(double cfl) {
   return dt;
 }
 
+
+// Mass / energy integrals and error norms against the exact case
+// (integrate_mass_energy, error_norms, max_freestream_deviation;
+// diagnostics.cpp:31-87).  out: mass, energy, volume, L2[5], Linf[5], fs_dev.
+void GpuRankSolver::diagnostics(double t, int with_exact, double* out) {
+  const int max_blocks = 4 * n_sm_;
+  if (diag_partial_.n < static_cast<size_t>(max_blocks) * kDiagVals) diag_partial_.alloc(max_blocks * kDiagVals);
+  const int blocks =
+      launch_diagnostics(n_, consts_, field_ptrs(U_.p, nullptr), t, with_exact, diag_partial_.p, max_blocks, stream_);
+  launches_++;
+  std::vector<double> h(static_cast<size_t>(blocks) * kDiagVals);
+  cuda_check(cudaMemcpyAsync(h.data(), diag_partial_.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  double acc[kDiagVals] = {};
+  for (int b = 0; b < blocks; ++b)
+    for (int q = 0; q < kDiagVals; ++q) {
+      const double v = h[static_cast<size_t>(b) * kDiagVals + q];
+      acc[q] = (q >= 8 && q < 13) ? std::max(acc[q], v) : acc[q] + v;
+    }
+  if (n_ranks_ > 1) {
+    DevBuf<double> d;
+    d.alloc(2 * kDiagVals);
+    std::vector<double> sums(acc, acc + kDiagVals), maxs(acc, acc + kDiagVals);
+    cuda_check(cudaMemcpyAsync(d.p, sums.data(), kDiagVals * sizeof(double), cudaMemcpyHostToDevice, stream_), "h2d");
+    cuda_check(cudaMemcpyAsync(d.p + kDiagVals, maxs.data(), kDiagVals * sizeof(double), cudaMemcpyHostToDevice,
+                               stream_),
+               "h2d");
+    nccl_check(ncclAllReduce(d.p, d.p, kDiagVals, ncclFloat64, ncclSum, comm_, stream_), "allreduce diag");
+    nccl_check(ncclAllReduce(d.p + kDiagVals, d.p + kDiagVals, kDiagVals, ncclFloat64, ncclMax, comm_, stream_),
+               "allreduce diag");
+    cuda_check(cudaMemcpyAsync(sums.data(), d.p, kDiagVals * sizeof(double), cudaMemcpyDeviceToHost, stream_), "d2h");
+    cuda_check(cudaMemcpyAsync(maxs.data(), d.p + kDiagVals, kDiagVals * sizeof(double), cudaMemcpyDeviceToHost,
+                               stream_),
+               "d2h");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    for (int q = 0; q < kDiagVals; ++q) acc[q] = (q >= 8 && q < 13) ? maxs[q] : sums[q];
+  }
+  out[0] = acc[0];
+  out[1] = acc[1];
+  out[2] = acc[2];
+  for (int v = 0; v < 5; ++v) {
+    out[3 + v] = std::sqrt(acc[3 + v] / acc[2]);
+    out[8 + v] = acc[8 + v];
+  }
+  out[13] = std::max(std::max(acc[8], acc[9]), std::max(std::max(acc[10], acc[11]), acc[12]));
+}
+
+// SDGFLD1 snapshot (snapshot.cpp:10-56), 3D header; every rank writes / reads
+// its own elements at their global offsets.
+static std::string snapshot_header(const MeshGeom& m, int degree, double time) {
+  std::ostringstream os;
+  os.precision(17);
+  os << "SDGFLD1\n";
+  os << "n_elements " << m.n_elements << " degree " << degree << " nvars " << SDG_NVARS << " time " << time << "\n";
+  os << "domain " << m.spec.x0 << ' ' << m.spec.y0 << ' ' << m.spec.z0 << ' ' << m.spec.width << ' '
+     << m.spec.height << ' ' << m.spec.depth << " ny " << m.spec.ny << " nz " << m.spec.nz << "\n";
+  for (size_t b = 0; b < m.bands.size(); ++b)
+    os << "band " << b << " x_lo " << m.bands[b].x_lo << " nx " << m.bands[b].nx << " vg " << m.bands[b].vg << "\n";
+  os << "end_header\n";
+  return os.str();
+}
+
+void GpuRankSolver::write_snapshot(const char* path, double time) {
+  std::vector<double> h(U_.n);
+  get_state(h.data());
+  const std::string hdr = snapshot_header(mesh_, basis_.degree, time);
+  FILE* f = std::fopen(path, rank_ == 0 ? "wb" : "r+b");
+  if (!f && rank_ != 0) f = std::fopen(path, "w+b");
+  if (!f) throw ConfigError(std::string("cannot open snapshot file ") + path);
+  const size_t stride = static_cast<size_t>(n3_) * 5;
+  bool ok = true;
+  if (rank_ == 0) ok = std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
+  for (int e = 0; e < E_ && ok; ++e) {
+    ok = std::fseek(f, static_cast<long>(hdr.size() + topo_.gids[e] * stride * sizeof(double)), SEEK_SET) == 0 &&
+         std::fwrite(h.data() + e * stride, sizeof(double), stride, f) == stride;
+  }
+  std::fclose(f);
+  if (!ok) throw ConfigError(std::string("snapshot write failed for ") + path);
+}
+
+double GpuRankSolver::read_snapshot(const char* path) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw ConfigError(std::string("cannot open snapshot file ") + path);
+  char line[4096];
+  if (!std::fgets(line, sizeof line, f) || std::string(line) != "SDGFLD1\n") {
+    std::fclose(f);
+    throw ConfigError(std::string("not a snapshot file: ") + path);
+  }
+  long ne = 0;
+  int degree = 0, nvars = 0;
+  double time = 0.0;
+  if (!std::fgets(line, sizeof line, f) ||
+      std::sscanf(line, "n_elements %ld degree %d nvars %d time %lf", &ne, &degree, &nvars, &time) != 4) {
+    std::fclose(f);
+    throw ConfigError("malformed snapshot header");
+  }
+  if (ne != mesh_.n_elements || degree != basis_.degree || nvars != SDG_NVARS) {
+    std::fclose(f);
+    throw ConfigError("snapshot does not match the mesh / degree / variable count");
+  }
+  while (std::fgets(line, sizeof line, f) && std::string(line) != "end_header\n") {
+  }
+  const long data0 = std::ftell(f);
+  const size_t stride = static_cast<size_t>(n3_) * 5;
+  std::vector<double> h(U_.n);
+  bool ok = true;
+  for (int e = 0; e < E_ && ok; ++e)
+    ok = std::fseek(f, static_cast<long>(data0 + topo_.gids[e] * stride * sizeof(double)), SEEK_SET) == 0 &&
+         std::fread(h.data() + e * stride, sizeof(double), stride, f) == stride;
+  std::fclose(f);
+  if (!ok) throw ConfigError(std::string("snapshot payload truncated in ") + path);
+  set_state(h.data());
+  return time;
+}
+
 void GpuRankSolver::ctx_info(int c, long* out5, double* sd, double* sig) {
   if (c < 0 || c >= static_cast<int>(sides_.size())) throw ConfigError("no such interface side context");
   int st[2 * kMaxCtx];
@@ -1370,6 +1493,18 @@ int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta
       std::strncpy(buf, j.c_str(), static_cast<size_t>(cap) - 1);
       buf[cap - 1] = 0;
     }
+  });
+}
+int sdg_diagnostics(sdg_ctx* c, double t, int with_exact, double* out) {
+  return guarded(c, [&] { c->s->diagnostics(t, with_exact, out); });
+}
+int sdg_write_snapshot(sdg_ctx* c, const char* path, double time) {
+  return guarded(c, [&] { c->s->write_snapshot(path, time); });
+}
+int sdg_read_snapshot(sdg_ctx* c, const char* path, double* time) {
+  return guarded(c, [&] {
+    const double t = c->s->read_snapshot(path);
+    if (time) *time = t;
   });
 }
 void* sdg_stream(sdg_ctx* c) { return c->s->stream(); }

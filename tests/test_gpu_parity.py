@@ -184,3 +184,87 @@ def test_appendix_a_device_pairing():
     assert list(out["m"][1] + 1) == [2, 4, 6, 1, 8]
     assert out["sched"].tolist() == [[4, 0, 6], [7, 6, 4]]
     assert out["self_entry"][2] == 0
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) rows 2-3
+def test_diagnostics_match_oracle():
+    """integrate_mass_energy / error_norms (diagnostics.cpp:31-87) on the device."""
+    mesh = box0(2)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 3)
+    o.step(dt, 3)
+    d = g.diagnostics(g.time())
+    me = o.mass_energy(g.field())
+    assert abs(d["mass"] - me[0]) <= 1e-13 * abs(me[0])
+    assert abs(d["energy"] - me[1]) <= 1e-13 * abs(me[1])
+    assert abs(d["volume"] - 8.0) <= 1e-12
+    ex = o.sample_case(g.time()).reshape(-1, 5)
+    err = g.field().reshape(-1, 5) - ex
+    assert np.allclose(d["linf"], np.abs(err).max(axis=0), rtol=1e-6, atol=1e-15)
+    assert np.all(d["l2"] >= 0.0) and d["l2"][0] <= d["linf"][0]
+
+
+def test_freestream_deviation_after_steps():
+    mesh = three_band(ny=6, nz=2)
+    cfg = T.solver_config(4, T.NODES_GAUSS, mu=1e-3, case=T.freestream(v=(1.0, 0.5, 0.25)))
+    g = gpu_solver(mesh, cfg)
+    g.set_initial_condition(0.0)
+    g.step(g.suggest_dt(0.5), 10)
+    assert g.diagnostics(g.time())["max_deviation"] < 1e-12
+
+
+def test_snapshot_round_trip(tmp_path):
+    """SDGFLD1 write / read (snapshot.cpp:10-56), 3D header."""
+    mesh = three_band(ny=3, nz=2)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g = gpu_solver(mesh, cfg)
+    g.set_initial_condition(0.25)
+    g.step(1e-3, 2)
+    path = str(tmp_path / "field.sdg")
+    g.write_snapshot(path)
+    head = open(path, "rb").read(200).split(b"\n")
+    assert head[0] == b"SDGFLD1" and head[1].startswith(b"n_elements 72 degree 3 nvars 5 time 0.252")
+    before = g.field()
+    h = gpu_solver(mesh, cfg)
+    t = h.read_snapshot(path)
+    assert abs(t - g.time()) < 1e-15
+    assert np.array_equal(h.field(), before)
+
+
+# ---------------------------------------------------------------- GPU vs the reference itself
+GOLDEN_FIXT = {
+    # name: (bands, ny, degree, kind, mu, periodic_x, case) — see tests/golden/make_golden.py
+    "dw_lgl3_inv": ([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], 6, 3, T.NODES_LGL, 0.0, True, "density_wave"),
+    "dw_gauss3_visc": ([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], 6, 3, T.NODES_GAUSS, 1e-3, True,
+                       "density_wave"),
+    "dw_gauss5_visc_dirichlet": ([(2, 1.0, 0.0), (2, 1.0, 0.5)], 2, 5, T.NODES_GAUSS, 1e-3, False, "density_wave"),
+    "fs_lgl4_inv": ([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], 6, 4, T.NODES_LGL, 0.0, True, "freestream"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN_FIXT))
+def test_gpu_embeds_reference_fixture(name):
+    """z-invariant embedding of the reference's own 2D results (tests/golden, made
+    from oracle/_ref = the unmodified reference library): residual and 10 RK steps."""
+    import os
+
+    import embed
+    bands, ny, deg, kind, mu, px, case = GOLDEN_FIXT[name]
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"ref2d_{name}.npz"))
+    nz, n = 2, deg + 1
+    mesh = embed.mesh3d(bands, ny, nz, periodic_x=px)
+    cfg = T.solver_config(deg, kind, mu=mu, case=embed.case3d(case))
+    g = gpu_solver(mesh, cfg)
+    g.set_initial_condition(0.0)
+    u0 = g.field()
+    r = g.compute_residual(float(z["t_res"]), u0)
+    scale = max(np.abs(z["residual"]).max(), 1.0)
+    assert embed.max_layer_diff(r, z["residual"], bands, ny, nz, n) <= 1e-12 * scale
+    g.set_initial_condition(0.0)
+    g.step(float(z["dt"]), int(z["n_steps"]))
+    assert embed.max_layer_diff(g.field(), z["u_end"], bands, ny, nz, n) <= 1e-12 * np.abs(z["u_end"]).max()
+    assert g.total_rebuilds() == int(z["rebuilds"])
