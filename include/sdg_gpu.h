@@ -58,6 +58,12 @@ typedef struct sdg_ctx sdg_ctx;
  * ncclUniqueId bytes shared by all ranks (NULL when n_ranks == 1). */
 int sdg_create(const sdg_mesh_spec* mesh, const sdg_solver_config* cfg, int n_ranks, int rank,
                int device, const void* nccl_id, sdg_ctx** out);
+/* Several ranks in one process sharing devices (one host thread per rank):
+ * the ranks named by the same `hub` exchange through event-ordered device
+ * copies instead of NCCL — the analogue of the reference's InProcHub
+ * (transport.hpp:83-120), used to test the multi-rank path on one GPU. */
+int sdg_create_inproc(const sdg_mesh_spec* mesh, const sdg_solver_config* cfg, int n_ranks, int rank, int device,
+                      const char* hub, sdg_ctx** out);
 void sdg_destroy(sdg_ctx* ctx);
 const char* sdg_last_error(const sdg_ctx* ctx);
 const char* sdg_global_error(void);

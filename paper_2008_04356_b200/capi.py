@@ -40,6 +40,8 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.sdg_create.argtypes = [C.POINTER(T.MeshSpec), C.POINTER(T.SolverConfig), C.c_int, C.c_int, C.c_int,
                                  C.c_void_p, C.POINTER(_vp)]
+        L.sdg_create_inproc.argtypes = [C.POINTER(T.MeshSpec), C.POINTER(T.SolverConfig), C.c_int, C.c_int,
+                                        C.c_int, C.c_char_p, C.POINTER(_vp)]
         L.sdg_destroy.argtypes = [_vp]
         L.sdg_last_error.argtypes = [_vp]
         L.sdg_last_error.restype = C.c_char_p
@@ -89,7 +91,7 @@ def lib():
 
 
 EXPORTED = [
-    "sdg_create", "sdg_destroy", "sdg_last_error", "sdg_global_error", "sdg_nccl_unique_id", "sdg_init_rank_maps",
+    "sdg_create", "sdg_create_inproc", "sdg_destroy", "sdg_last_error", "sdg_global_error", "sdg_nccl_unique_id", "sdg_init_rank_maps",
     "sdg_set_initial_condition", "sdg_n1", "sdg_n_local_elements", "sdg_n_global_elements",
     "sdg_local_element_ids", "sdg_set_state", "sdg_get_state", "sdg_get_register", "sdg_state_device_ptr",
     "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
@@ -114,11 +116,15 @@ class RankSolver:
     """One rank's share of the mesh on one GPU (mirror of sdg::RankSolver)."""
 
     def __init__(self, mesh: T.MeshSpec, cfg: T.SolverConfig, n_ranks: int = 1, rank: int = 0, device: int = 0,
-                 nccl_id: bytes | None = None, init_rank_maps: bool = True):
+                 nccl_id: bytes | None = None, init_rank_maps: bool = True, inproc_hub: str | None = None):
         self.lib = lib()
         h = _vp()
-        idp = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        code = self.lib.sdg_create(C.byref(mesh), C.byref(cfg), n_ranks, rank, device, idp, C.byref(h))
+        if inproc_hub is not None:
+            code = self.lib.sdg_create_inproc(C.byref(mesh), C.byref(cfg), n_ranks, rank, device,
+                                              inproc_hub.encode(), C.byref(h))
+        else:
+            idp = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+            code = self.lib.sdg_create(C.byref(mesh), C.byref(cfg), n_ranks, rank, device, idp, C.byref(h))
         T.raise_for(code, self.lib.sdg_global_error().decode())
         self.h = h
         self.n1 = self.lib.sdg_n1(h)
@@ -269,6 +275,45 @@ class RankSolver:
         self._check(self.lib.sdg_kernel_timing(self.h, names, 512, _d(ms), cnt.ctypes.data_as(_lp), 16, C.byref(n)))
         keys = names.value.decode().split(",")
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys[: n.value])}
+
+
+def run_inproc(mesh: T.MeshSpec, cfg: T.SolverConfig, n_ranks: int, body, device: int = 0, hub: str = "sdg"):
+    """Runs `body(solver)` on n_ranks in-process ranks (one host thread each) that
+    share `device`; returns the per-rank results.  Collective calls happen
+    inside `body` on every rank in the same order."""
+    import threading
+    out = [None] * n_ranks
+    err = [None] * n_ranks
+
+    def worker(r):
+        try:
+            s = RankSolver(mesh, cfg, n_ranks=n_ranks, rank=r, device=device, inproc_hub=hub, init_rank_maps=False)
+            s.init_rank_maps()
+            out[r] = body(s)
+            s.close()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    ths = [threading.Thread(target=worker, args=(r,)) for r in range(n_ranks)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def gather_global(parts, n_elements_global: int, n1: int) -> np.ndarray:
+    """Scatters per-rank (gids, local field) pairs into the global element order."""
+    per = n1 ** 3 * T.NVARS
+    g = np.full(n_elements_global * per, np.nan)
+    for gids, u in parts:
+        u = u.reshape(-1, per)
+        for q, gid in enumerate(gids):
+            g[gid * per:(gid + 1) * per] = u[q]
+    return g
 
 
 def plan(mesh: T.MeshSpec, n_ranks: int, rank: int, delta: float = 0.0) -> dict:

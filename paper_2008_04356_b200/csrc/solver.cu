@@ -14,7 +14,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <deque>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <sstream>
 #include <tuple>
@@ -60,6 +63,187 @@ struct DevBuf {
   }
 };
 
+
+// ----------------------------------------------------------------------------
+// Rank-to-rank transport behind one interface (the reference's Transport,
+// transport.hpp:43-80): NCCL over NVLink between processes / GPUs, or an
+// in-process hub for several ranks sharing one GPU (the analogue of the
+// reference's InProcHub, used to exercise the multi-rank data path on a single
+// device).  Every rank issues the same sequence of calls.
+// ----------------------------------------------------------------------------
+struct Xfer {
+  int partner;
+  double* ptr;  // send: source, recv: destination (device)
+  size_t count;
+};
+
+struct Comm {
+  virtual ~Comm() = default;
+  virtual void allgather_ints(const std::vector<int>& mine, std::vector<std::vector<int>>& all, cudaStream_t st) = 0;
+  // One grouped round: all sends and receives of this rank.
+  virtual void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t st) = 0;
+  // op: 0 sum, 1 max, 2 min (host values, every rank gets the result).
+  virtual void allreduce(double* vals, int n, int op, cudaStream_t st) = 0;
+};
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  int n_ranks;
+  NcclComm(const void* id_bytes, int n, int rank) : n_ranks(n) {
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    nccl_check(ncclCommInitRank(&comm, n, id, rank), "ncclCommInitRank");
+  }
+  ~NcclComm() override {
+    if (comm) ncclCommDestroy(comm);
+  }
+  void allgather_ints(const std::vector<int>& mine, std::vector<std::vector<int>>& all, cudaStream_t st) override {
+    DevBuf<int> d_cnt, d_all_cnt;
+    d_cnt.alloc(1);
+    d_all_cnt.alloc(n_ranks);
+    const int cnt = static_cast<int>(mine.size());
+    cuda_check(cudaMemcpyAsync(d_cnt.p, &cnt, sizeof(int), cudaMemcpyHostToDevice, st), "h2d");
+    nccl_check(ncclAllGather(d_cnt.p, d_all_cnt.p, 1, ncclInt32, comm, st), "allgather sizes");
+    std::vector<int> counts(n_ranks);
+    cuda_check(cudaMemcpyAsync(counts.data(), d_all_cnt.p, n_ranks * sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    const int mx = std::max(1, *std::max_element(counts.begin(), counts.end()));
+    std::vector<int> padded(mx, 0);
+    std::copy(mine.begin(), mine.end(), padded.begin());
+    DevBuf<int> d_mine, d_all;
+    d_mine.upload(padded, st);
+    d_all.alloc(static_cast<size_t>(mx) * n_ranks);
+    nccl_check(ncclAllGather(d_mine.p, d_all.p, mx, ncclInt32, comm, st), "allgather maps");
+    std::vector<int> h(static_cast<size_t>(mx) * n_ranks);
+    cuda_check(cudaMemcpyAsync(h.data(), d_all.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    all.assign(n_ranks, {});
+    for (int r = 0; r < n_ranks; ++r) all[r].assign(h.begin() + r * mx, h.begin() + r * mx + counts[r]);
+  }
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t st) override {
+    if (sends.empty() && recvs.empty()) return;
+    nccl_check(ncclGroupStart(), "group start");
+    for (const auto& x : sends) nccl_check(ncclSend(x.ptr, x.count, ncclFloat64, x.partner, comm, st), "send");
+    for (const auto& x : recvs) nccl_check(ncclRecv(x.ptr, x.count, ncclFloat64, x.partner, comm, st), "recv");
+    nccl_check(ncclGroupEnd(), "group end");
+  }
+  void allreduce(double* vals, int n, int op, cudaStream_t st) override {
+    DevBuf<double> d;
+    d.alloc(n);
+    cuda_check(cudaMemcpyAsync(d.p, vals, n * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    const ncclRedOp_t o = op == 0 ? ncclSum : (op == 1 ? ncclMax : ncclMin);
+    nccl_check(ncclAllReduce(d.p, d.p, n, ncclFloat64, o, comm, st), "allreduce");
+    cuda_check(cudaMemcpyAsync(vals, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  }
+};
+
+struct InProcHub {
+  int n;
+  std::mutex mu;
+  std::condition_variable cv;
+  long gen = 0;
+  int arrived = 0;
+  struct Msg {
+    const double* ptr;
+    size_t count;
+    cudaEvent_t ready;
+  };
+  std::vector<std::deque<Msg>> box;  // n*n channels (src*n + dst), FIFO as transport.cpp:46-75
+  std::vector<std::vector<int>> ints;
+  std::vector<std::vector<double>> vals;
+  explicit InProcHub(int n_) : n(n_), box(static_cast<size_t>(n_) * n_), ints(n_), vals(n_) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+std::mutex g_hubs_mu;
+std::map<std::string, std::weak_ptr<InProcHub>> g_hubs;
+
+struct InProcComm : Comm {
+  std::shared_ptr<InProcHub> hub;
+  int rank;
+  cudaEvent_t ev = nullptr;
+  InProcComm(const std::string& name, int n, int r) : rank(r) {
+    std::lock_guard<std::mutex> lk(g_hubs_mu);
+    auto& w = g_hubs[name];
+    hub = w.lock();
+    if (!hub) {
+      hub = std::make_shared<InProcHub>(n);
+      w = hub;
+    }
+    if (hub->n != n) throw ConfigError("in-process hub rank count mismatch");
+    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  }
+  ~InProcComm() override {
+    if (ev) cudaEventDestroy(ev);
+  }
+  void allgather_ints(const std::vector<int>& mine, std::vector<std::vector<int>>& all, cudaStream_t) override {
+    {
+      std::lock_guard<std::mutex> lk(hub->mu);
+      hub->ints[rank] = mine;
+    }
+    hub->barrier();
+    {
+      std::lock_guard<std::mutex> lk(hub->mu);
+      all = hub->ints;
+    }
+    hub->barrier();
+  }
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t st) override {
+    cuda_check(cudaEventRecord(ev, st), "event record");
+    {
+      std::lock_guard<std::mutex> lk(hub->mu);
+      for (const auto& x : sends) hub->box[static_cast<size_t>(rank) * hub->n + x.partner].push_back({x.ptr, x.count, ev});
+    }
+    hub->barrier();
+    for (const auto& x : recvs) {
+      InProcHub::Msg m;
+      {
+        std::lock_guard<std::mutex> lk(hub->mu);
+        auto& q = hub->box[static_cast<size_t>(x.partner) * hub->n + rank];
+        if (q.empty()) throw ProtocolError("in-process receive without a matching send");
+        m = q.front();
+        q.pop_front();
+      }
+      if (m.count != x.count) throw ProtocolError("message length mismatch");
+      cuda_check(cudaStreamWaitEvent(st, m.ready, 0), "wait event");
+      cuda_check(cudaMemcpyAsync(x.ptr, m.ptr, x.count * sizeof(double), cudaMemcpyDeviceToDevice, st), "d2d");
+    }
+    // Senders may reuse their buffers only after every receiver has copied.
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    hub->barrier();
+  }
+  void allreduce(double* v, int n, int op, cudaStream_t) override {
+    {
+      std::lock_guard<std::mutex> lk(hub->mu);
+      hub->vals[rank].assign(v, v + n);
+    }
+    hub->barrier();
+    {
+      std::lock_guard<std::mutex> lk(hub->mu);
+      for (int q = 0; q < n; ++q) {
+        double a = hub->vals[0][q];
+        for (int r = 1; r < hub->n; ++r) {
+          const double b = hub->vals[r][q];
+          a = op == 0 ? a + b : (op == 1 ? std::max(a, b) : std::min(a, b));
+        }
+        v[q] = a;
+      }
+    }
+    hub->barrier();
+  }
+};
+
 // Carpenter-Kennedy 5-stage 2N-storage RK4 (proj/src/lsrk.cpp:7-29).
 const double RK_A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
                         -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
@@ -95,7 +279,7 @@ enum KClass { KC_PROLONG, KC_PAIRING, KC_MORTAR, KC_GRADIENT, KC_UPDATE, KC_COPY
 class GpuRankSolver {
  public:
   GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& cfg, int n_ranks, int rank, int device,
-                const void* nccl_id);
+                const void* nccl_id, const char* inproc_hub = nullptr);
   ~GpuRankSolver();
 
   void init_rank_maps();
@@ -160,7 +344,7 @@ class GpuRankSolver {
   int rank_ = 0, n_ranks_ = 1, device_ = 0;
   bool lifting_ = false;
   cudaStream_t stream_ = nullptr;
-  ncclComm_t comm_ = nullptr;
+  std::unique_ptr<Comm> comm_;
 
   DevBuf<double> U_, reg_, dudt_, trace_, fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
   DevBuf<int8_t> side_type_;
@@ -202,7 +386,7 @@ class GpuRankSolver {
 };
 
 GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& cfg, int n_ranks, int rank,
-                             int device, const void* nccl_id)
+                             int device, const void* nccl_id, const char* inproc_hub)
     : mesh_(ms), part_(assign_ranks(mesh_, n_ranks)), topo_(build_topology(mesh_, part_, rank)),
       basis_(cfg.degree, cfg.node_kind), cfg_(cfg), rank_(rank), n_ranks_(n_ranks), device_(device) {
   const auto& g = cfg.gas;
@@ -221,10 +405,9 @@ GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& c
   cuda_check(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device), "device attribute");
   if (const char* env = std::getenv("SDG_NO_TMA")) use_tma_ = env[0] == '0';
   if (n_ranks > 1) {
-    if (!nccl_id) throw ConfigError("multi-rank context needs an NCCL unique id");
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
-    nccl_check(ncclCommInitRank(&comm_, n_ranks, id, rank), "ncclCommInitRank");
+    if (inproc_hub) comm_ = std::make_unique<InProcComm>(inproc_hub, n_ranks, rank);
+    else if (nccl_id) comm_ = std::make_unique<NcclComm>(nccl_id, n_ranks, rank);
+    else throw ConfigError("multi-rank context needs an NCCL unique id or an in-process hub name");
   }
   build_consts();
   upload_topology();
@@ -239,7 +422,7 @@ GpuRankSolver::~GpuRankSolver() {
     cudaEventDestroy(ev.second.first);
     cudaEventDestroy(ev.second.second);
   }
-  if (comm_) ncclCommDestroy(comm_);
+  comm_.reset();
   if (err_host_) cudaFreeHost(err_host_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -440,32 +623,8 @@ void GpuRankSolver::init_rank_maps() {
       mine.push_back(static_cast<int>(topo_.sliding[k].i_perp));
     }
   std::vector<std::vector<int>> all(n_ranks_);
-  if (n_ranks_ == 1) {
-    all[0] = mine;
-  } else {
-    // All-gather of the sizes, then of the padded payloads.
-    DevBuf<int> d_cnt, d_all_cnt;
-    d_cnt.alloc(1);
-    d_all_cnt.alloc(n_ranks_);
-    const int cnt = static_cast<int>(mine.size());
-    cuda_check(cudaMemcpyAsync(d_cnt.p, &cnt, sizeof(int), cudaMemcpyHostToDevice, stream_), "h2d");
-    nccl_check(ncclAllGather(d_cnt.p, d_all_cnt.p, 1, ncclInt32, comm_, stream_), "allgather sizes");
-    std::vector<int> counts(n_ranks_);
-    cuda_check(cudaMemcpyAsync(counts.data(), d_all_cnt.p, n_ranks_ * sizeof(int), cudaMemcpyDeviceToHost, stream_),
-               "d2h");
-    cuda_check(cudaStreamSynchronize(stream_), "sync");
-    const int mx = std::max(1, *std::max_element(counts.begin(), counts.end()));
-    std::vector<int> padded(mx, 0);
-    std::copy(mine.begin(), mine.end(), padded.begin());
-    DevBuf<int> d_mine, d_all;
-    d_mine.upload(padded, stream_);
-    d_all.alloc(static_cast<size_t>(mx) * n_ranks_);
-    nccl_check(ncclAllGather(d_mine.p, d_all.p, mx, ncclInt32, comm_, stream_), "allgather maps");
-    std::vector<int> h(static_cast<size_t>(mx) * n_ranks_);
-    cuda_check(cudaMemcpyAsync(h.data(), d_all.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
-    cuda_check(cudaStreamSynchronize(stream_), "sync");
-    for (int r = 0; r < n_ranks_; ++r) all[r].assign(h.begin() + r * mx, h.begin() + r * mx + counts[r]);
-  }
+  if (n_ranks_ == 1) all[0] = mine;
+  else comm_->allgather_ints(mine, all, stream_);
   const int ni = static_cast<int>(mesh_.ifaces.size());
   std::vector<std::vector<int>> smap(ni), mmap(ni);
   for (int ic = 0; ic < ni; ++ic) {
@@ -737,14 +896,11 @@ void GpuRankSolver::mortar_exchange(double* const src[2], double* dst, int nc, b
     mark(KC_COPY, false);
   }
   if (n_ranks_ == 1) return;
-  if (sched_[from].empty() && sched_[to].empty()) return;
+  std::vector<Xfer> sends, recvs;
+  for (const auto& e : sched_[from]) sends.push_back({e[0], src[from] + e[1] * node, e[2] * node});
+  for (const auto& e : sched_[to]) recvs.push_back({e[0], dst + e[1] * node, e[2] * node});
   mark(KC_HALO, true);
-  nccl_check(ncclGroupStart(), "group start");
-  for (const auto& e : sched_[from])
-    nccl_check(ncclSend(src[from] + e[1] * node, e[2] * node, ncclFloat64, e[0], comm_, stream_), "send");
-  for (const auto& e : sched_[to])
-    nccl_check(ncclRecv(dst + e[1] * node, e[2] * node, ncclFloat64, e[0], comm_, stream_), "recv");
-  nccl_check(ncclGroupEnd(), "group end");
+  comm_->exchange(sends, recvs, stream_);
   mark(KC_HALO, false);
 }
 
@@ -759,23 +915,23 @@ __global__ void k_gather_slots(const double* src, const int* slots, int n_slots,
 }
 
 void GpuRankSolver::halo_exchange(double* arr, int nc) {
-  if (n_ranks_ == 1 || topo_.peers.empty()) return;
+  if (n_ranks_ == 1) return;
   const int per = n2_ * nc;
   const int ns = static_cast<int>(send_slots_.n);
   mark(KC_HALO, true);
-  k_gather_slots<<<(ns * per + 255) / 256, 256, 0, stream_>>>(arr, send_slots_.p, ns, per, send_buf_.p);
-  launches_++;
-  nccl_check(ncclGroupStart(), "group start");
+  if (ns > 0) {
+    k_gather_slots<<<(ns * per + 255) / 256, 256, 0, stream_>>>(arr, send_slots_.p, ns, per, send_buf_.p);
+    launches_++;
+  }
+  std::vector<Xfer> sends, recvs;
   size_t off = 0;
   for (const auto& p : topo_.peers) {
     const size_t cnt = p.send_slots.size() * per;
-    nccl_check(ncclSend(send_buf_.p + off, cnt, ncclFloat64, p.partner, comm_, stream_), "halo send");
-    nccl_check(ncclRecv(arr + static_cast<size_t>(p.recv_slots.front()) * per, p.recv_slots.size() * per,
-                        ncclFloat64, p.partner, comm_, stream_),
-               "halo recv");
+    sends.push_back({p.partner, send_buf_.p + off, cnt});
+    recvs.push_back({p.partner, arr + static_cast<size_t>(p.recv_slots.front()) * per, p.recv_slots.size() * per});
     off += cnt;
   }
-  nccl_check(ncclGroupEnd(), "group end");
+  comm_->exchange(sends, recvs, stream_);
   mark(KC_HALO, false);
 }
 
@@ -927,14 +1083,7 @@ double GpuRankSolver::suggest_dt(double cfl) {
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   double dt;
   std::memcpy(&dt, &bits, sizeof(dt));
-  if (n_ranks_ > 1) {
-    DevBuf<double> d;
-    d.alloc(1);
-    cuda_check(cudaMemcpyAsync(d.p, &dt, sizeof(dt), cudaMemcpyHostToDevice, stream_), "h2d");
-    nccl_check(ncclAllReduce(d.p, d.p, 1, ncclFloat64, ncclMin, comm_, stream_), "allreduce dt");
-    cuda_check(cudaMemcpyAsync(&dt, d.p, sizeof(dt), cudaMemcpyDeviceToHost, stream_), "d2h");
-    cuda_check(cudaStreamSynchronize(stream_), "sync");
-  }
+  if (n_ranks_ > 1) comm_->allreduce(&dt, 1, 2, stream_);
   return dt;
 }
 
@@ -959,21 +1108,11 @@ void GpuRankSolver::diagnostics(double t, int with_exact, double* out) {
       acc[q] = (q >= 8 && q < 13) ? std::max(acc[q], v) : acc[q] + v;
     }
   if (n_ranks_ > 1) {
-    DevBuf<double> d;
-    d.alloc(2 * kDiagVals);
-    std::vector<double> sums(acc, acc + kDiagVals), maxs(acc, acc + kDiagVals);
-    cuda_check(cudaMemcpyAsync(d.p, sums.data(), kDiagVals * sizeof(double), cudaMemcpyHostToDevice, stream_), "h2d");
-    cuda_check(cudaMemcpyAsync(d.p + kDiagVals, maxs.data(), kDiagVals * sizeof(double), cudaMemcpyHostToDevice,
-                               stream_),
-               "h2d");
-    nccl_check(ncclAllReduce(d.p, d.p, kDiagVals, ncclFloat64, ncclSum, comm_, stream_), "allreduce diag");
-    nccl_check(ncclAllReduce(d.p + kDiagVals, d.p + kDiagVals, kDiagVals, ncclFloat64, ncclMax, comm_, stream_),
-               "allreduce diag");
-    cuda_check(cudaMemcpyAsync(sums.data(), d.p, kDiagVals * sizeof(double), cudaMemcpyDeviceToHost, stream_), "d2h");
-    cuda_check(cudaMemcpyAsync(maxs.data(), d.p + kDiagVals, kDiagVals * sizeof(double), cudaMemcpyDeviceToHost,
-                               stream_),
-               "d2h");
-    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    double sums[kDiagVals], maxs[kDiagVals];
+    std::copy(acc, acc + kDiagVals, sums);
+    std::copy(acc, acc + kDiagVals, maxs);
+    comm_->allreduce(sums, kDiagVals, 0, stream_);
+    comm_->allreduce(maxs, kDiagVals, 1, stream_);
     for (int q = 0; q < kDiagVals; ++q) acc[q] = (q >= 8 && q < 13) ? maxs[q] : sums[q];
   }
   out[0] = acc[0];
@@ -1357,6 +1496,20 @@ int sdg_create(const sdg_mesh_spec* mesh, const sdg_solver_config* cfg, int n_ra
     auto* c = new sdg_ctx{nullptr};
     try {
       c->s = new GpuRankSolver(*mesh, *cfg, n_ranks, rank, device, nccl_id);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+int sdg_create_inproc(const sdg_mesh_spec* mesh, const sdg_solver_config* cfg, int n_ranks, int rank, int device,
+                      const char* hub, sdg_ctx** out) {
+  return guarded(nullptr, [&] {
+    if (!mesh || !cfg || !out || !hub) throw sdg::ConfigError("null argument");
+    auto* c = new sdg_ctx{nullptr};
+    try {
+      c->s = new GpuRankSolver(*mesh, *cfg, n_ranks, rank, device, nullptr, hub);
     } catch (...) {
       delete c;
       throw;

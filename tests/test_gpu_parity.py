@@ -269,3 +269,26 @@ def test_gpu_embeds_reference_fixture(name):
     g.step(float(z["dt"]), int(z["n_steps"]))
     assert embed.max_layer_diff(g.field(), z["u_end"], bands, ny, nz, n) <= 1e-12 * np.abs(z["u_end"]).max()
     assert g.total_rebuilds() == int(z["rebuilds"])
+
+
+# ---------------------------------------------------------------- multi-rank data path on one GPU
+@pytest.mark.parametrize("ranks", [2, 3, 6])
+def test_rank_counts_do_not_change_the_bits(ranks):
+    """proj/tests/test_runner.cpp:32-50 on the B200 path: 1 rank vs 2/3/6 ranks
+    (in-process hub, same device) must give bitwise-identical fields.  Exercises
+    the partition, the halo slots of trace / Fv.n exchange and the per-partner
+    mortar blocks of the NCCL path's protocol."""
+    from paper_2008_04356_b200 import capi
+    mesh = T.mesh_spec([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], ny=6, nz=2, depth=1.0)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    n_el = 2 * 6 * 2 * 3
+
+    def body(s):
+        s.set_initial_condition(0.0)
+        s.step(0.004, 5)
+        return s.local_element_ids(), s.field()
+
+    ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub="r1"), n_el, 4)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"r{ranks}"), n_el, 4)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
