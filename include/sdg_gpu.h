@@ -131,6 +131,13 @@ int sdg_read_snapshot(sdg_ctx* ctx, const char* path, double* time);
  * partition.cpp:154-169).  *len receives the full length. */
 int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta, char* buf, long cap, long* len);
 
+/* Communication trace of this rank (TraceRow, transport.hpp:28-37): JSON rows
+ * [step, stage, src, dst, bytes, kind, is_send], step -1 = init; kinds follow
+ * MsgKind (transport.hpp:13-24).  sdg_inject_collective is the audit's
+ * negative-test hook (RankSolver::inject_collective, solver.cpp:961-964). */
+int sdg_trace_json(sdg_ctx* ctx, char* buf, long cap, long* len);
+int sdg_inject_collective(sdg_ctx* ctx);
+
 /* Instrumentation: the cudaStream_t the context enqueues on, the number of
  * kernels this library launched, and per-kernel-class CUDA-event timing of
  * the next sdg_steps_async call (ms, summed over launches). */

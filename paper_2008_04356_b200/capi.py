@@ -80,6 +80,8 @@ def lib():
         L.sdg_diagnostics.argtypes = [_vp, C.c_double, C.c_int, _dp]
         L.sdg_write_snapshot.argtypes = [_vp, C.c_char_p, C.c_double]
         L.sdg_read_snapshot.argtypes = [_vp, C.c_char_p, _dp]
+        L.sdg_trace_json.argtypes = [_vp, C.c_char_p, C.c_long, _lp]
+        L.sdg_inject_collective.argtypes = [_vp]
         L.sdg_stream.argtypes = [_vp]
         L.sdg_stream.restype = C.c_void_p
         L.sdg_kernel_launches.argtypes = [_vp]
@@ -98,7 +100,7 @@ EXPORTED = [
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
     "sdg_pairing_device", "sdg_plan_json", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
-    "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
+    "sdg_trace_json", "sdg_inject_collective", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
 
@@ -251,6 +253,18 @@ class RankSolver:
         t = C.c_double()
         self._check(self.lib.sdg_read_snapshot(self.h, path.encode(), C.byref(t)))
         return t.value
+
+    def trace(self) -> dict:
+        """Communication trace of this rank (TraceRow, transport.hpp:28-37)."""
+        import json
+        n = C.c_long()
+        self._check(self.lib.sdg_trace_json(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self._check(self.lib.sdg_trace_json(self.h, buf, n.value + 1, C.byref(n)))
+        return json.loads(buf.value.decode())
+
+    def inject_collective(self):
+        self._check(self.lib.sdg_inject_collective(self.h))
 
     # --- instrumentation -------------------------------------------------------
     def stream(self) -> int:

@@ -271,6 +271,10 @@ struct SideCtx {
   // per-partner mortar counts of this side (for the NCCL blocks)
 };
 
+// Message kinds of the trace (transport.hpp:13-24; this protocol sends Fv.n
+// instead of the primary's LiftConf / FluxConf replies).
+enum MsgKind { MK_INIT = 1, MK_SOL_CONF = 2, MK_SOL_MORTAR = 3, MK_LIFT_MORTAR = 5, MK_FVN_CONF = 6,
+               MK_GRAD_MORTAR = 7, MK_FLUX_MORTAR = 9, MK_DIAG = 10 };
 const char* kKernelClasses[] = {"prolong", "pairing", "mortar", "gradient", "update", "copy", "halo"};
 enum KClass { KC_PROLONG, KC_PAIRING, KC_MORTAR, KC_GRADIENT, KC_UPDATE, KC_COPY, KC_HALO, KC_N };
 
@@ -318,16 +322,26 @@ class GpuRankSolver {
   std::vector<std::pair<double, long>> timing_totals();
 
   std::string err;
+  std::string trace_json() const;
+  void inject_collective();
 
  private:
+  struct TraceRow {
+    int step, stage, src, dst;
+    long long count;
+    int kind;
+    bool is_send;
+  };
+  std::vector<TraceRow> comm_trace_;
+  void record(int kind, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs);
   void build_consts();
   void build_sides();
   void upload_topology();
   void stage(double t_stage, int mode, double rk_a, double rk_b, double dt, double* out, const double* u_override);
   void update_interfaces_host(double t_stage);
   void run_pairing(double t_stage);
-  void mortar_exchange(double* const src[2], double* dst_static, int ncomp, bool moving_to_static);
-  void halo_exchange(double* arr, int ncomp);
+  void mortar_exchange(double* const src[2], double* dst_static, int ncomp, bool moving_to_static, int kind);
+  void halo_exchange(double* arr, int ncomp, int kind);
   FieldPtrs field_ptrs(double* U, double* out);
   MortarPtrs mortar_ptrs();
   void check_error();
@@ -623,8 +637,13 @@ void GpuRankSolver::init_rank_maps() {
       mine.push_back(static_cast<int>(topo_.sliding[k].i_perp));
     }
   std::vector<std::vector<int>> all(n_ranks_);
-  if (n_ranks_ == 1) all[0] = mine;
-  else comm_->allgather_ints(mine, all, stream_);
+  if (n_ranks_ == 1) {
+    all[0] = mine;
+  } else {
+    for (int r = 0; r < n_ranks_; ++r)
+      if (r != rank_) comm_trace_.push_back({-1, 0, rank_, r, static_cast<long long>(mine.size()), MK_INIT, true});
+    comm_->allgather_ints(mine, all, stream_);
+  }
   const int ni = static_cast<int>(mesh_.ifaces.size());
   std::vector<std::vector<int>> smap(ni), mmap(ni);
   for (int ic = 0; ic < ni; ++ic) {
@@ -882,7 +901,7 @@ void GpuRankSolver::run_pairing(double t_stage) {
 // moving_to_static: src[1] blocks -> dst (static "theirs"); otherwise src[0]
 // blocks -> dst (moving array).  Self blocks are device copies, remote
 // blocks grouped NCCL send/recv in ascending partner order.
-void GpuRankSolver::mortar_exchange(double* const src[2], double* dst, int nc, bool moving_to_static) {
+void GpuRankSolver::mortar_exchange(double* const src[2], double* dst, int nc, bool moving_to_static, int kind) {
   const int from = moving_to_static ? 1 : 0, to = 1 - from;
   const size_t node = static_cast<size_t>(n2_) * nc;
   const auto& sf = self_[from];
@@ -899,6 +918,7 @@ void GpuRankSolver::mortar_exchange(double* const src[2], double* dst, int nc, b
   std::vector<Xfer> sends, recvs;
   for (const auto& e : sched_[from]) sends.push_back({e[0], src[from] + e[1] * node, e[2] * node});
   for (const auto& e : sched_[to]) recvs.push_back({e[0], dst + e[1] * node, e[2] * node});
+  record(kind, sends, recvs);
   mark(KC_HALO, true);
   comm_->exchange(sends, recvs, stream_);
   mark(KC_HALO, false);
@@ -914,7 +934,7 @@ __global__ void k_gather_slots(const double* src, const int* slots, int n_slots,
   dst[i] = src[static_cast<size_t>(slots[s]) * per_slot + q];
 }
 
-void GpuRankSolver::halo_exchange(double* arr, int nc) {
+void GpuRankSolver::halo_exchange(double* arr, int nc, int kind) {
   if (n_ranks_ == 1) return;
   const int per = n2_ * nc;
   const int ns = static_cast<int>(send_slots_.n);
@@ -931,6 +951,7 @@ void GpuRankSolver::halo_exchange(double* arr, int nc) {
     recvs.push_back({p.partner, arr + static_cast<size_t>(p.recv_slots.front()) * per, p.recv_slots.size() * per});
     off += cnt;
   }
+  record(kind, sends, recvs);
   comm_->exchange(sends, recvs, stream_);
   mark(KC_HALO, false);
 }
@@ -949,14 +970,14 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     mark(KC_PROLONG, false);
     launches_++;
   }
-  halo_exchange(trace_.p, 5);
+  halo_exchange(trace_.p, 5, MK_SOL_CONF);
   const MortarPtrs mp = mortar_ptrs();
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
   mark(KC_MORTAR, true);
   launch_mortar_fill(n_, 5, trace_.p, u_src, fwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
   launches_ += S_ > 0;
-  mortar_exchange(u_src, u_theirs_.p, 5, true);
+  mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
   StageArgs a{t_stage, dt, rk_a, rk_b, mode, step_index_, stage_index_};
   if (lifting_) {
     mark(KC_MORTAR, true);
@@ -964,7 +985,7 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     mark(KC_MORTAR, false);
     launches_ += max_mortars_[0] > 0;
     double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
-    mortar_exchange(l_src, mlift_[1].p, 4, false);
+    mortar_exchange(l_src, mlift_[1].p, 4, false, MK_LIFT_MORTAR);
     mark(KC_MORTAR, true);
     launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
@@ -973,20 +994,20 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     if (!(use_tma_ && launch_gradient_tma(n_, consts_, fp, a, n_sm_, stream_))) launch_gradient(n_, consts_, fp, a, stream_);
     mark(KC_GRADIENT, false);
     launches_++;
-    halo_exchange(fvn_.p, 4);
+    halo_exchange(fvn_.p, 4, MK_FVN_CONF);
     double* const g_src[2] = {g_mine_[0].p, g_mine_[1].p};
     mark(KC_MORTAR, true);
     launch_mortar_fill(n_, 12, slide_g_.p, g_src, fwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
     launches_ += S_ > 0;
-    mortar_exchange(g_src, g_theirs_.p, 12, true);
+    mortar_exchange(g_src, g_theirs_.p, 12, true, MK_GRAD_MORTAR);
   }
   mark(KC_MORTAR, true);
   launch_mortar_flux(n_, consts_.gas, lifting_ ? 1 : 0, mp, max_mortars_[0], err_.p, stream_);
   mark(KC_MORTAR, false);
   launches_ += max_mortars_[0] > 0;
   double* const f_src[2] = {mflux_[0].p, mflux_[1].p};
-  mortar_exchange(f_src, mflux_[1].p, 5, false);
+  mortar_exchange(f_src, mflux_[1].p, 5, false, MK_FLUX_MORTAR);
   mark(KC_MORTAR, true);
   launch_mortar_backproject(n_, 5, f_src, slide_flux_.p, bwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
@@ -996,6 +1017,36 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   mark(KC_UPDATE, false);
   launches_++;
   traces_valid_ = (mode == 0 && !u_override);
+}
+
+
+void GpuRankSolver::record(int kind, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs) {
+  for (const auto& x : sends)
+    comm_trace_.push_back({step_index_, stage_index_, rank_, x.partner, static_cast<long long>(x.count), kind, true});
+  for (const auto& x : recvs)
+    comm_trace_.push_back({step_index_, stage_index_, x.partner, rank_, static_cast<long long>(x.count), kind, false});
+}
+
+// Test hook (RankSolver::inject_collective, solver.cpp:961-964): one
+// unsanctioned collective after init, which the audit must flag.
+void GpuRankSolver::inject_collective() {
+  if (n_ranks_ == 1) return;
+  double v = 0.0;
+  for (int r = 0; r < n_ranks_; ++r)
+    if (r != rank_) comm_trace_.push_back({step_index_, stage_index_, rank_, r, 1, MK_INIT, true});
+  comm_->allreduce(&v, 1, 0, stream_);
+}
+
+std::string GpuRankSolver::trace_json() const {
+  std::ostringstream os;
+  os << "{\"rank\":" << rank_ << ",\"n_ranks\":" << n_ranks_ << ",\"n1\":" << n_ << ",\"rows\":[";
+  for (size_t i = 0; i < comm_trace_.size(); ++i) {
+    const auto& r = comm_trace_[i];
+    os << (i ? "," : "") << "[" << r.step << "," << r.stage << "," << r.src << "," << r.dst << "," << r.count * 8
+       << "," << r.kind << "," << (r.is_send ? 1 : 0) << "]";
+  }
+  os << "]}";
+  return os.str();
 }
 
 void GpuRankSolver::check_error() {
@@ -1054,14 +1105,14 @@ void GpuRankSolver::compute_gradients(double t_stage, const double* d_u, double*
   run_pairing(t_stage);
   FieldPtrs fp = field_ptrs(U, nullptr);
   launch_prolong(n_, consts_, fp, stream_);
-  halo_exchange(trace_.p, 5);
+  halo_exchange(trace_.p, 5, MK_SOL_CONF);
   const MortarPtrs mp = mortar_ptrs();
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
   launch_mortar_fill(n_, 5, trace_.p, u_src, fwd_ops_, mp, stream_);
-  mortar_exchange(u_src, u_theirs_.p, 5, true);
+  mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
   launch_mortar_lift(n_, consts_.gas, mp, max_mortars_[0], stream_);
   double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
-  mortar_exchange(l_src, mlift_[1].p, 4, false);
+  mortar_exchange(l_src, mlift_[1].p, 4, false, MK_LIFT_MORTAR);
   launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
   fp.grad_out = d_grad;
   ElemConsts c = consts_;
@@ -1636,6 +1687,19 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
     sdg::device_pairing(n_local, faces, n_par, n_perp, partner_ranks, n_delta, on_static, conforming, self_rank,
                         ncols, cols, m_rows, face_lo, nsched, sched, self_entry);
   });
+}
+int sdg_trace_json(sdg_ctx* c, char* buf, long cap, long* len) {
+  return guarded(c, [&] {
+    const std::string j = c->s->trace_json();
+    *len = static_cast<long>(j.size());
+    if (buf && cap > 0) {
+      std::strncpy(buf, j.c_str(), static_cast<size_t>(cap) - 1);
+      buf[cap - 1] = 0;
+    }
+  });
+}
+int sdg_inject_collective(sdg_ctx* c) {
+  return guarded(c, [&] { c->s->inject_collective(); });
 }
 int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta, char* buf, long cap,
                   long* len) {

@@ -292,3 +292,29 @@ def test_rank_counts_do_not_change_the_bits(ranks):
     got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"r{ranks}"), n_el, 4)
     assert not np.isnan(got).any()
     assert np.array_equal(got, ref)
+
+
+def test_communication_audit_passes_and_catches_injected_collective():
+    """audit_communication (audit.cpp:44-148) on the traces of a 3-rank run; the
+    inject_collective hook (solver.cpp:961-964) must make it fail."""
+    from paper_2008_04356_b200 import audit, capi
+    mesh = T.mesh_spec([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], ny=6, nz=2, depth=1.0)
+    cfg = T.solver_config(2, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+
+    def clean(s):
+        s.set_initial_condition(0.0)
+        s.step(0.004, 2)
+        return s.trace()
+
+    def dirty(s):
+        s.set_initial_condition(0.0)
+        s.step(0.004, 1)
+        s.inject_collective()
+        return s.trace()
+
+    rep = audit.audit(capi.run_inproc(mesh, cfg, 3, clean, hub="audit3"), mesh)
+    assert rep["passed"], rep["violations"]
+    assert rep["init_collective_sends"] == 3 * 2 and rep["post_init_collectives"] == 0
+    assert rep["data_messages"] > 0
+    bad = audit.audit(capi.run_inproc(mesh, cfg, 3, dirty, hub="audit3b"), mesh)
+    assert not bad["passed"] and bad["post_init_collectives"] > 0
