@@ -365,6 +365,40 @@ __device__ __forceinline__ void node_gradient(const double* tab, const double* s
   }
 }
 
+// Same, with q stored node-major at pitch 6 (two 128-bit loads per node).
+template <int N1>
+__device__ __forceinline__ void node_gradient_pk(const double* tab, const double* q6, const double* sLift,
+                                                 const BandD& B, int i, int j, int k, double* g) {
+  constexpr int N2 = N1 * N1;
+  const double* dh = tab;
+  const double* fl = tab + N1 * N1;
+  const double* fr = fl + N1;
+  const double* iw = fl + 4 * N1;
+  double vx[4] = {0, 0, 0, 0}, vy[4] = {0, 0, 0, 0}, vz[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    const double cx = dh[i * N1 + m], cy = dh[j * N1 + m], cz = dh[k * N1 + m];
+    const double* px = q6 + ((m * N1 + j) * N1 + k) * 6;
+    const double* py = q6 + ((i * N1 + m) * N1 + k) * 6;
+    const double* pz = q6 + ((i * N1 + j) * N1 + m) * 6;
+    const double2 x01 = *reinterpret_cast<const double2*>(px), x23 = *reinterpret_cast<const double2*>(px + 2);
+    const double2 y01 = *reinterpret_cast<const double2*>(py), y23 = *reinterpret_cast<const double2*>(py + 2);
+    const double2 z01 = *reinterpret_cast<const double2*>(pz), z23 = *reinterpret_cast<const double2*>(pz + 2);
+    vx[0] += cx * x01.x; vx[1] += cx * x01.y; vx[2] += cx * x23.x; vx[3] += cx * x23.y;
+    vy[0] += cy * y01.x; vy[1] += cy * y01.y; vy[2] += cy * y23.x; vy[3] += cy * y23.y;
+    vz[0] += cz * z01.x; vz[1] += cz * z01.y; vz[2] += cz * z23.x; vz[3] += cz * z23.y;
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double sx = (sLift[(1 * 4 + c) * N2 + j * N1 + k] * fr[i] - sLift[(0 * 4 + c) * N2 + j * N1 + k] * fl[i]) * iw[i];
+    const double sy = (sLift[(3 * 4 + c) * N2 + i * N1 + k] * fr[j] - sLift[(2 * 4 + c) * N2 + i * N1 + k] * fl[j]) * iw[j];
+    const double sz = (sLift[(5 * 4 + c) * N2 + i * N1 + j] * fr[k] - sLift[(4 * 4 + c) * N2 + i * N1 + j] * fl[k]) * iw[k];
+    g[3 * c + 0] = B.cdir[0] * (sx - vx[c]);
+    g[3 * c + 1] = B.cdir[1] * (sy - vy[c]);
+    g[3 * c + 2] = B.cdir[2] * (sz - vz[c]);
+  }
+}
+
 // Same, with lift*(s, c, f) at nb[s * nbs + off + f * 4 + c] (in place over Fv.n slots).
 template <int N1>
 __device__ __forceinline__ void node_gradient_nb(const double* tab, const double* sq, const double* nb, int nbs,
@@ -1586,6 +1620,7 @@ struct TmaV2 {
   static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
   static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
   static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
+  static constexpr int U_SMEM_PACK = U_SMEM + EPB * N3 * 8;  // node-major pitch-6 q / F staging
 };
 
 // Update-kernel loads of one tile (issued by one thread).
@@ -1624,7 +1659,7 @@ __device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int ti
     }
 }
 
-template <int N1, bool VISC>
+template <int N1, bool VISC, bool PACK>
 __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_tma_v2(const __grid_constant__ ElemConsts C, FieldPtrs P,
                                                                  StageArgs A) {
   using D = TmaV2<N1>;
@@ -1633,7 +1668,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
   double* tab = smem;
   double* stage0 = smem + D::TAB;
   double* work = stage0 + 2 * D::U_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 : 0));
   __shared__ __align__(16) int codes[2][8 * EPB];
   load_tables<N1>(C, tab);
   const int tiles = (P.E + EPB - 1) / EPB;
@@ -1652,8 +1687,9 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
     if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
   }
-  double* wF = work;                               // EPB x 5 N3 (q, then F_d, SoA)
-  double* wLift = work + EPB * 5 * N3;             // EPB x 24 N2, SoA [s][c][f]
+  constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
+  double* wF = work;
+  double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
   double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
   for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
     const int sidx = it & 1;
@@ -1674,7 +1710,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     double* sR = st + EPB * D::EL + le * D::EL;
     double* sFv = st + 2 * EPB * D::EL + le * 6 * D::FS;
     double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
-    double* q = wF + le * 5 * N3;
+    double* q = wF + le * WF;
     double* lf = wLift + le * 24 * N2;
     const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
     mbar_wait(&bars[sidx], (it >> 1) & 1);
@@ -1687,7 +1723,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
         for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
         prim4(u, C.gas, qq);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+        for (int c = 0; c < 4; ++c) q[PACK ? t * 6 + c : c * N3 + t] = qq[c];
       }
       for (int itm = t; itm < 6 * N2; itm += N3) {
         const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
@@ -1780,7 +1816,8 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       }
       if (VISC) {
         double g[12];
-        node_gradient<N1>(tab, q, lf, B, i, j, k, g);
+        if (PACK) node_gradient_pk<N1>(tab, q, lf, B, i, j, k, g);
+        else node_gradient<N1>(tab, q, lf, B, i, j, k, g);
         const double div = g[0] + g[4] + g[8];
         const double mu = C.gas.mu, lam = C.gas.lam;
         const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
@@ -1804,7 +1841,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       __syncthreads();
       if (active) {
 #pragma unroll
-        for (int v = 0; v < 5; ++v) q[v * N3 + t] = F[d][v] * B.sj[d];
+        for (int v = 0; v < 5; ++v) q[PACK ? t * 6 + v : v * N3 + t] = F[d][v] * B.sj[d];
       }
       __syncthreads();
       if (active) {
@@ -1814,8 +1851,19 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
           const double c = tab[ia * N1 + m];
+          if (PACK) {
+            const double* fp = q + (base + m * stride) * 6;
+            const double2 f01 = *reinterpret_cast<const double2*>(fp);
+            const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
+            acc[0] += c * f01.x;
+            acc[1] += c * f01.y;
+            acc[2] += c * f23.x;
+            acc[3] += c * f23.y;
+            acc[4] += c * fp[4];
+          } else {
 #pragma unroll
-          for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
+            for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
+          }
         }
       }
     }
@@ -2627,15 +2675,17 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
     static int variant = -1;
     if (variant < 0) {
       const char* env = std::getenv("SDG_UPDATE_V");
-      variant = env ? std::atoi(env) : 2;
+      variant = env ? std::atoi(env) : 6;
     }
     const bool v3 = variant == 3 || variant == 4;
+    const bool pack = variant == 6;
     auto kern = variant == 3 ? (c.gas.viscous ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
               : variant == 4 ? (c.gas.viscous ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
-                             : (c.gas.viscous ? k_update_tma_v2<N1, true> : k_update_tma_v2<N1, false>);
-    const int smem = v3 ? D::U_SMEM : TmaV2<N1>::U_SMEM;
-    static int occ_tab[6] = {-1, -1, -1, -1, -1, -1};
-    int& occ = occ_tab[(variant == 3 ? 2 : variant == 4 ? 4 : 0) + (c.gas.viscous ? 1 : 0)];
+              : pack ? (c.gas.viscous ? k_update_tma_v2<N1, true, true> : k_update_tma_v2<N1, false, true>)
+                     : (c.gas.viscous ? k_update_tma_v2<N1, true, false> : k_update_tma_v2<N1, false, false>);
+    const int smem = v3 ? D::U_SMEM : (pack ? TmaV2<N1>::U_SMEM_PACK : TmaV2<N1>::U_SMEM);
+    static int occ_tab[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+    int& occ = occ_tab[(variant == 3 ? 2 : variant == 4 ? 4 : pack ? 6 : 0) + (c.gas.viscous ? 1 : 0)];
     if (occ < 0) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, smem);
@@ -2779,7 +2829,7 @@ bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const St
                        cudaStream_t st) {
   if (p.E == 0) return true;
   bool ok = false;
-  static const int uv = env_int("SDG_UPDATE_V", 2);
+  static const int uv = env_int("SDG_UPDATE_V", 6);
   if (uv == 5) {
     SDG_DISPATCH(n1, (ok = v5_t<NN>(true, c, p, a, n_sm, st)));
     return ok;
