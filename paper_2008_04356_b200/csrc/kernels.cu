@@ -1621,6 +1621,7 @@ struct TmaV2 {
   static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
   static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
   static constexpr int U_SMEM_PACK = U_SMEM + EPB * N3 * 8;  // node-major pitch-6 q / F staging
+  static constexpr int U_SMEM_S1 = U_SMEM_PACK - U_STAGE * 8;  // single-buffered stage
 };
 
 // Update-kernel loads of one tile (issued by one thread).
@@ -1714,6 +1715,274 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     double* lf = wLift + le * 24 * N2;
     const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
     mbar_wait(&bars[sidx], (it >> 1) & 1);
+
+    // Phase 1: face fluxes (in place over the neighbour data) and lift*.
+    if (active) {
+      if (VISC) {
+        double u[5], qq[4];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+        prim4(u, C.gas, qq);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[PACK ? t * 6 + c : c * N3 + t] = qq[c];
+      }
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        double* nb = sNb + s * D::NB;
+        const int code = P.side_code[8 * e + s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kSliding) {
+          if (VISC) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = nb[D::TS + f * 4 + c];
+          }
+          continue;
+        }
+        double own[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
+        double flux[5], lift[4];
+        bool ok;
+        const double vg = dir == 1 ? B.vg : 0.0;
+        if (typ == kConforming) {
+          double other[5];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
+          const double* um = (s & 1) ? own : other;
+          const double* up = (s & 1) ? other : own;
+          if (VISC) {
+            double qa[4], qb[4];
+            prim4(own, C.gas, qa);
+            prim4(other, C.gas, qb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+            double fa[4], fb[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              fa[c] = sFv[s * D::FS + f * 4 + c];
+              fb[c] = nb[D::TS + f * 4 + c];
+            }
+            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        } else {
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          const double* um = (s & 1) ? own : ext;
+          const double* up = (s & 1) ? ext : own;
+          if (VISC) {
+            prim4(ext, C.gas, lift);
+            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+            double gg[12];
+#pragma unroll
+            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+            double fm[4], fp[4];
+            fv_dir(um, gg, dir, C.gas, fm);
+            fv_dir(up, gg, dir, C.gas, fp);
+            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+          } else {
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+          }
+        }
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
+        if (VISC) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
+        }
+      }
+    }
+    __syncthreads();
+
+    // Phase 2: volume flux at the node (gradient recomputed from q and lift*).
+    double F[3][5], u[5];
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      const double ir = __drcp_rn(u[0]);
+      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+      const double p = pressure(u, ir, C.gas);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double vgd = d == 1 ? B.vg : 0.0;
+        F[d][0] = u[0] * vv[d] - vgd * u[0];
+        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
+        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
+        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
+        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
+      }
+      if (VISC) {
+        double g[12];
+        if (PACK) node_gradient_pk<N1>(tab, q, lf, B, i, j, k, g);
+        else node_gradient<N1>(tab, q, lf, B, i, j, k, g);
+        const double div = g[0] + g[4] + g[8];
+        const double mu = C.gas.mu, lam = C.gas.lam;
+        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
+                     t22 = 2.0 * mu * g[8] + lam * div;
+        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
+        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          F[d][1] -= tau[d][0];
+          F[d][2] -= tau[d][1];
+          F[d][3] -= tau[d][2];
+          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+        }
+      }
+    }
+
+    // Phase 3: weak divergence per direction through shared memory.
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      __syncthreads();
+      if (active) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) q[PACK ? t * 6 + v : v * N3 + t] = F[d][v] * B.sj[d];
+      }
+      __syncthreads();
+      if (active) {
+        const int ia = d == 0 ? i : (d == 1 ? j : k);
+        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          const double c = tab[ia * N1 + m];
+          if (PACK) {
+            const double* fp = q + (base + m * stride) * 6;
+            const double2 f01 = *reinterpret_cast<const double2*>(fp);
+            const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
+            acc[0] += c * f01.x;
+            acc[1] += c * f01.y;
+            acc[2] += c * f23.x;
+            acc[3] += c * f23.y;
+            acc[4] += c * fp[4];
+          } else {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
+          }
+        }
+      }
+    }
+
+    // Phase 4 + 5: surface lift, RK update in place, admissibility.
+    if (active) {
+      double du[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
+      const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int dir = s >> 1;
+        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
+        if (c != 0.0) {
+          const double* fl = sNb + s * D::NB + f * 5;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
+        }
+      }
+      if (A.mode == 1) {
+        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = du[v];
+      } else {
+        double w[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
+          w[v] = u[v] + A.rk_b * rg;
+          sR[t * 5 + v] = rg;
+          sU[t * 5 + v] = w[v];
+        }
+        const double p = pressure(w, __drcp_rn(w[0]), C.gas);
+        bool ok = w[0] > 0.0 && p > 0.0;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
+        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+      }
+    }
+    if (A.mode == 1) {
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    // Phase 6: traces of the new state, then bulk stores of U, reg and traces.
+    if (active) {
+      double* tr = wTr + le * 6 * D::TS;
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int n = min(EPB, P.E - e0);
+      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
+      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
+      bulk_s2g(P.trace + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+template <int N1, bool VISC, bool PACK>
+__global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_update_tma_s1(const __grid_constant__ ElemConsts C, FieldPtrs P,
+                                                                 StageArgs A) {
+  using D = TmaV2<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* work = stage0 + D::U_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 : 0));
+  __shared__ __align__(16) int codes[2][8 * EPB];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E + EPB - 1) / EPB;
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < tiles) prefetch_codes<N1>(P, tile, codes[0]);
+  constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
+  double* wF = work;
+  double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
+  double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    double* st = stage0;
+    const int next = tile + gridDim.x;
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous tile's stores have read the stage and wTr
+      cp_async_wait_all();  // codes of this tile
+      fence_proxy_async();
+      issue_update_loads_v2<N1, VISC>(P, tile, codes[it & 1], stage0, &bars[0]);
+      if (next < tiles) prefetch_codes<N1>(P, next, codes[(it + 1) & 1]);
+    }
+    const int e0 = tile * EPB;
+    const int e = e0 + le;
+    const bool active = e < P.E;
+    double* sU = st + le * D::EL;
+    double* sR = st + EPB * D::EL + le * D::EL;
+    double* sFv = st + 2 * EPB * D::EL + le * 6 * D::FS;
+    double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
+    double* q = wF + le * WF;
+    double* lf = wLift + le * 24 * N2;
+    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+    mbar_wait(&bars[0], it & 1);
 
     // Phase 1: face fluxes (in place over the neighbour data) and lift*.
     if (active) {
@@ -2679,6 +2948,19 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
     }
     const bool v3 = variant == 3 || variant == 4;
     const bool pack = variant == 6;
+    if (variant == 7) {
+      auto k7 = c.gas.viscous ? k_update_tma_s1<N1, true, true> : k_update_tma_s1<N1, false, true>;
+      static int occ7[2] = {-1, -1};
+      int& o7 = occ7[c.gas.viscous ? 1 : 0];
+      if (o7 < 0) {
+        cudaFuncSetAttribute(k7, cudaFuncAttributeMaxDynamicSharedMemorySize, TmaV2<N1>::U_SMEM_S1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k7, D::THREADS, TmaV2<N1>::U_SMEM_S1);
+        if (o7 < 1) o7 = 1;
+      }
+      k7<<<std::min(tiles, n_sm * o7), D::THREADS, TmaV2<N1>::U_SMEM_S1, st>>>(c, p, a);
+      check_launch("k_update_tma_s1");
+      return true;
+    }
     auto kern = variant == 3 ? (c.gas.viscous ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
               : variant == 4 ? (c.gas.viscous ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
               : pack ? (c.gas.viscous ? k_update_tma_v2<N1, true, true> : k_update_tma_v2<N1, false, true>)

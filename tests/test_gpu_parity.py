@@ -318,3 +318,25 @@ def test_communication_audit_passes_and_catches_injected_collective():
     assert rep["data_messages"] > 0
     bad = audit.audit(capi.run_inproc(mesh, cfg, 3, dirty, hub="audit3b"), mesh)
     assert not bad["passed"] and bad["post_init_collectives"] > 0
+
+
+def test_baseline_config0_ten_steps():
+    """BASELINE.json configs[0] in full: [0,2]^3 split at the interface into two
+    4x4x4 blocks, upper block +0.5 along the slide, N=3 Gauss, mu=1e-3, Dirichlet
+    across the split, periodic otherwise, rho = 2 + 0.1 sin(pi(x+y+z)), u=v=w=1,
+    p=1, 10 low-storage RK steps at CFL 0.5 (axes relabelled, include/sdg_types.h)."""
+    mesh = box0(4)
+    cfg = T.solver_config(3, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1e-3, Pr=0.72, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    assert abs(g.suggest_dt(0.5) - dt) <= 1e-14 * dt
+    g.step(dt, 10)
+    o.step(dt, 10)
+    assert g.n_elements == 128
+    assert rel_linf(g.field(), o.field()) <= 1e-10
+    assert g.total_rebuilds() == o.total_rebuilds()
+    d = g.diagnostics(g.time())
+    me = o.mass_energy(o.field())
+    assert abs(d["mass"] - me[0]) <= 1e-12 * me[0]
