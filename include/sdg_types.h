@@ -67,6 +67,10 @@ typedef struct {
   int n_bands;
   sdg_band_spec bands[SDG_MAX_BANDS];
   int periodic_x, periodic_y, periodic_z;
+  /* Element order inside a band for the rank split: 0 = contiguous (ix, iy, iz)
+   * lexicographic blocks (proj/src/partition.cpp:48-81), 1 = Morton
+   * space-filling curve. */
+  int partition;
 } sdg_mesh_spec;
 
 typedef struct {

@@ -73,10 +73,40 @@ void MeshGeom::locate(long g, int& b, int& ix, int& iy, int& iz) const {
 
 // ---------------------------------------------------------------- partition
 int Partition::owner(int band, long local) const {
+  const long o = order_of[band].empty() ? local : order_of[band][local];
   for (const auto& blk : band_blocks[band])
-    if (local >= blk.start && local < blk.start + blk.count) return blk.rank;
+    if (o >= blk.start && o < blk.start + blk.count) return blk.rank;
   throw ProtocolError("ownership lookup outside any block");
 }
+
+namespace {
+unsigned long long spread3(unsigned long long v) {  // 21 bits -> every third bit
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+// Morton (Z-order) space-filling curve over a band's (ix, iy, iz) elements.
+void sfc_order(const MeshGeom& mesh, int b, std::vector<long>& lex_of, std::vector<long>& order_of) {
+  const long ny = mesh.spec.ny, nz = mesh.spec.nz, ne = mesh.bands[b].n_elements;
+  std::vector<std::pair<unsigned long long, long>> key(ne);
+  for (long l = 0; l < ne; ++l) {
+    const long ix = l / (ny * nz), iy = (l / nz) % ny, iz = l % nz;
+    key[l] = {spread3(ix) << 2 | spread3(iy) << 1 | spread3(iz), l};
+  }
+  std::sort(key.begin(), key.end());
+  lex_of.resize(ne);
+  order_of.resize(ne);
+  for (long o = 0; o < ne; ++o) {
+    lex_of[o] = key[o].second;
+    order_of[key[o].second] = o;
+  }
+}
+}  // namespace
 
 Partition assign_ranks(const MeshGeom& mesh, int n_ranks) {
   const int nb = static_cast<int>(mesh.bands.size());
@@ -84,6 +114,12 @@ Partition assign_ranks(const MeshGeom& mesh, int n_ranks) {
   Partition p;
   p.n_ranks = n_ranks;
   p.band_blocks.resize(nb);
+  p.lex_of.resize(nb);
+  p.order_of.resize(nb);
+  if (mesh.spec.partition == 1 && n_ranks > 1)
+    for (int b = 0; b < nb; ++b) sfc_order(mesh, b, p.lex_of[b], p.order_of[b]);
+  else if (mesh.spec.partition != 0 && mesh.spec.partition != 1)
+    throw ConfigError("partition must be 0 (lexicographic blocks) or 1 (space-filling curve)");
   if (n_ranks == 1) {
     for (int b = 0; b < nb; ++b) p.band_blocks[b].push_back({0, 0, mesh.bands[b].n_elements});
     return p;
@@ -175,8 +211,8 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
   for (int b = 0; b < nb; ++b)
     for (const auto& blk : part.band_blocks[b]) {
       if (blk.rank != rank) continue;
-      for (long e = blk.start; e < blk.start + blk.count; ++e) {
-        const long g = mesh.bands[b].off + e;
+      for (long o = blk.start; o < blk.start + blk.count; ++o) {
+        const long g = mesh.bands[b].off + part.lex(b, o);
         local_of[g] = static_cast<int>(t.gids.size());
         t.gids.push_back(g);
       }

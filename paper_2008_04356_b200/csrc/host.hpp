@@ -73,10 +73,14 @@ struct Partition {
   int n_ranks = 1;
   struct Block {
     int rank;
-    long start, count;  // band-local element range
+    long start, count;  // range of the band's element order (lexicographic or SFC)
   };
   std::vector<std::vector<Block>> band_blocks;
-  int owner(int band, long local) const;
+  // Element order of each band: lex_of[b][o] = band-local lexicographic index of
+  // position o, order_of[b][lex] the inverse (empty = identity).
+  std::vector<std::vector<long>> lex_of, order_of;
+  int owner(int band, long local) const;  // local = lexicographic index
+  long lex(int band, long o) const { return lex_of[band].empty() ? o : lex_of[band][o]; }
 };
 Partition assign_ranks(const MeshGeom& mesh, int n_ranks);
 

@@ -31,6 +31,7 @@ class MeshSpec(C.Structure):
         ("n_bands", C.c_int),
         ("bands", BandSpec * SDG_MAX_BANDS),
         ("periodic_x", C.c_int), ("periodic_y", C.c_int), ("periodic_z", C.c_int),
+        ("partition", C.c_int),
     ]
 
 
@@ -85,8 +86,11 @@ def raise_for(code: int, msg: str) -> None:
         raise ERRORS.get(code, SdgError)(msg)
 
 
+PARTITION_LEX, PARTITION_SFC = 0, 1
+
+
 def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z0=0.0,
-              periodic=(True, True, True)) -> MeshSpec:
+              periodic=(True, True, True), partition=PARTITION_LEX) -> MeshSpec:
     """bands: list of (nx, width_frac, vg_y) tuples, stacked along x."""
     if not 1 <= len(bands) <= SDG_MAX_BANDS:
         raise ConfigError("mesh needs 1..16 bands")
@@ -100,6 +104,7 @@ def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z
         nx, frac, vg = b[0], (b[1] if len(b) > 1 else 1.0), (b[2] if len(b) > 2 else 0.0)
         m.bands[i].nx, m.bands[i].width_frac, m.bands[i].vg_y = int(nx), float(frac), float(vg)
     m.periodic_x, m.periodic_y, m.periodic_z = (int(bool(p)) for p in periodic)
+    m.partition = int(partition)
     return m
 
 

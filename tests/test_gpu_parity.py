@@ -272,14 +272,15 @@ def test_gpu_embeds_reference_fixture(name):
 
 
 # ---------------------------------------------------------------- multi-rank data path on one GPU
+@pytest.mark.parametrize("partition", [T.PARTITION_LEX, T.PARTITION_SFC])
 @pytest.mark.parametrize("ranks", [2, 3, 6])
-def test_rank_counts_do_not_change_the_bits(ranks):
+def test_rank_counts_do_not_change_the_bits(ranks, partition):
     """proj/tests/test_runner.cpp:32-50 on the B200 path: 1 rank vs 2/3/6 ranks
     (in-process hub, same device) must give bitwise-identical fields.  Exercises
     the partition, the halo slots of trace / Fv.n exchange and the per-partner
     mortar blocks of the NCCL path's protocol."""
     from paper_2008_04356_b200 import capi
-    mesh = T.mesh_spec([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], ny=6, nz=2, depth=1.0)
+    mesh = T.mesh_spec([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], ny=6, nz=2, depth=1.0, partition=partition)
     cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
     n_el = 2 * 6 * 2 * 3
 
@@ -289,7 +290,7 @@ def test_rank_counts_do_not_change_the_bits(ranks):
         return s.local_element_ids(), s.field()
 
     ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub="r1"), n_el, 4)
-    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"r{ranks}"), n_el, 4)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"r{ranks}p{partition}"), n_el, 4)
     assert not np.isnan(got).any()
     assert np.array_equal(got, ref)
 

@@ -23,6 +23,10 @@ def meshes():
         "tgv3": T.mesh_spec([(3, 1.0, 0.0), (4, 1.0, 0.2), (3, 1.0, 0.0)], ny=4, nz=3, width=L, height=L, depth=L),
         "box0": T.mesh_spec([(4, 1.0, 0.0), (4, 1.0, 0.5)], ny=4, nz=4, periodic=(False, True, True)),
         "bands5": T.mesh_spec([(2, 1.0, 0.0), (3, 1.0, 1.0), (2, 2.0, 0.0), (2, 1.0, 0.0), (2, 1.0, 0.7)], ny=5, nz=2),
+        "tgv3_sfc": T.mesh_spec([(3, 1.0, 0.0), (4, 1.0, 0.2), (3, 1.0, 0.0)], ny=4, nz=3, width=L, height=L, depth=L,
+                                partition=T.PARTITION_SFC),
+        "box0_sfc": T.mesh_spec([(4, 1.0, 0.0), (4, 1.0, 0.5)], ny=4, nz=4, periodic=(False, True, True),
+                                partition=T.PARTITION_SFC),
     }
 
 
@@ -111,3 +115,16 @@ def test_two_ranks_over_three_bands_split_static_moving():
     mesh = meshes()["tgv3"]
     p0, p1 = capi.plan(mesh, 2, 0), capi.plan(mesh, 2, 1)
     assert len(p0["elements"]) == 2 * 3 * 4 * 3 and len(p1["elements"]) == 4 * 4 * 3
+
+
+def test_sfc_partition_reduces_the_halo():
+    """Space-filling-curve split inside a band: same elements per rank, fewer
+    halo faces than lexicographic slabs when a band is cut into many parts."""
+    def halo_faces(partition):
+        mesh = T.mesh_spec([(8, 1.0, 0.0), (8, 1.0, 0.5)], ny=8, nz=8, partition=partition)
+        plans = [capi.plan(mesh, 8, r) for r in range(8)]
+        return sum(len(h["keys"]) for p in plans for h in p["halo"]), [len(p["elements"]) for p in plans]
+    lex, n_lex = halo_faces(T.PARTITION_LEX)
+    sfc, n_sfc = halo_faces(T.PARTITION_SFC)
+    assert n_lex == n_sfc
+    assert sfc <= lex
