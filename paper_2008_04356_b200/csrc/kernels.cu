@@ -1219,10 +1219,10 @@ constexpr int kCodeShift = 29;
 template <int N1>
 struct Tma {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
-  static constexpr int EPB = N1 == 2 ? 8 : (N1 == 4 ? 2 : 1);
+  static constexpr int EPB = N1 == 2 ? 8 : 1;
   static constexpr int THREADS = EPB * N3;
-  static constexpr int MINB_U = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);  // resident CTAs per SM (shared-memory bound)
-  static constexpr int MINB_G = N1 == 8 ? 1 : 2;
+  static constexpr int MINB_U = N1 == 2 ? 3 : (N1 == 8 ? 1 : (N1 == 4 ? 4 : 2));  // resident CTAs per SM (smem bound)
+  static constexpr int MINB_G = N1 == 8 ? 1 : (N1 == 4 ? 4 : 2);
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3;  // state doubles per element
   static constexpr int TS = 5 * N2;  // trace slot
@@ -1614,7 +1614,7 @@ struct TmaV2 {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int EPB = Tma<N1>::EPB;
   static constexpr int THREADS = EPB * N3;
-  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);
+  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : (N1 == 4 ? 4 : 2));
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
   static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
@@ -2417,7 +2417,7 @@ struct T5 {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int EPB = Tma<N1>::EPB;
   static constexpr int THREADS = EPB * N3;
-  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : 2);
+  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : (N1 == 4 ? 4 : 2));
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
   // update stage: U | reg | own traces | own Fv.n | neighbour (trace|flux, Fv.n|lift)
