@@ -16,7 +16,7 @@ import numpy as np
 from . import types as T
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsdg_gpu.so")
+LIB_PATH = os.environ.get("SDG_GPU_LIB", os.path.join(HERE, "libsdg_gpu.so"))
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)

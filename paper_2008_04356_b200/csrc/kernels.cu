@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
   for (int it = t; it < 6 * N2; it += N3) {
     const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
-    double* dst = P.trace + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
+    double* dst = P.trace_out + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
 #pragma unroll
     for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
   }
@@ -1601,7 +1601,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n_el * D::EL * 8u);
       bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, regb, n_el * D::EL * 8u);
       for (int l = 0; l < n_el; ++l)
-        bulk_s2g(P.trace + static_cast<size_t>(e0 + l) * 6 * D::TS, wF + l * 16 * N3, 6u * D::TS * 8u);
+        bulk_s2g(P.trace_out + static_cast<size_t>(e0 + l) * 6 * D::TS, wF + l * 16 * N3, 6u * D::TS * 8u);
       bulk_commit();
     }
   }
@@ -1670,7 +1670,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
   double* stage0 = smem + D::TAB;
   double* work = stage0 + 2 * D::U_STAGE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 : 0));
-  __shared__ __align__(16) int codes[2][8 * EPB];
+  __shared__ __align__(16) int codes[3][8 * EPB];
   load_tables<N1>(C, tab);
   const int tiles = (P.E + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
@@ -1688,6 +1688,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
     if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
   }
+  __syncthreads();  // codes[0] visible to every thread
   constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
   double* wF = work;
   double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
@@ -1700,9 +1701,9 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     if (threadIdx.x == 0 && next < tiles) {
       cp_async_wait_all();  // codes of `next`
       fence_proxy_async();
-      issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::U_STAGE,
+      issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::U_STAGE,
                                    &bars[sidx ^ 1]);
-      if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
+      if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
     }
     const int e0 = tile * EPB;
     const int e = e0 + le;
@@ -1713,7 +1714,8 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
     double* q = wF + le * WF;
     double* lf = wLift + le * 24 * N2;
-    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+    const int* myc = codes[it % 3] + 8 * le;
+    const BandD& B = C.bands[active ? myc[6] : 0];
     mbar_wait(&bars[sidx], (it >> 1) & 1);
 
     // Phase 1: face fluxes (in place over the neighbour data) and lift*.
@@ -1730,7 +1732,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
         const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
         const double* ell = tab + N1 * N1 + (s & 1) * N1;
         double* nb = sNb + s * D::NB;
-        const int code = P.side_code[8 * e + s];
+        const int code = myc[s];
         const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
         if (typ == kSliding) {
           if (VISC) {
@@ -1928,7 +1930,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       const int n = min(EPB, P.E - e0);
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
       bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
-      bulk_s2g(P.trace + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
+      bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
       bulk_commit();
     }
   }
@@ -1945,7 +1947,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
   double* stage0 = smem + D::TAB;
   double* work = stage0 + D::U_STAGE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 : 0));
-  __shared__ __align__(16) int codes[2][8 * EPB];
+  __shared__ __align__(16) int codes[3][8 * EPB];
   load_tables<N1>(C, tab);
   const int tiles = (P.E + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
@@ -1981,7 +1983,8 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
     double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
     double* q = wF + le * WF;
     double* lf = wLift + le * 24 * N2;
-    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+    const int* myc = codes[it % 3] + 8 * le;
+    const BandD& B = C.bands[active ? myc[6] : 0];
     mbar_wait(&bars[0], it & 1);
 
     // Phase 1: face fluxes (in place over the neighbour data) and lift*.
@@ -1998,7 +2001,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
         const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
         const double* ell = tab + N1 * N1 + (s & 1) * N1;
         double* nb = sNb + s * D::NB;
-        const int code = P.side_code[8 * e + s];
+        const int code = myc[s];
         const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
         if (typ == kSliding) {
           if (VISC) {
@@ -2196,7 +2199,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
       const int n = min(EPB, P.E - e0);
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
       bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
-      bulk_s2g(P.trace + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
+      bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
       bulk_commit();
     }
   }
@@ -2739,7 +2742,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const
     if (threadIdx.x == 0) {
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n_el * D::EL * 8u);
       bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n_el * D::EL * 8u);
-      bulk_s2g(P.trace + static_cast<size_t>(e0) * 6 * D::TS, st + EPB * 2 * D::EL, n_el * 6u * D::TS * 8u);
+      bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, st + EPB * 2 * D::EL, n_el * 6u * D::TS * 8u);
       bulk_commit();
     }
   }

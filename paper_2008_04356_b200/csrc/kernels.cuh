@@ -49,7 +49,8 @@ struct FieldPtrs {
   double* U;
   double* reg;
   double* out;         // dudt (residual mode)
-  double* trace;       // (6E + H) slots x N2 x 5   face traces of U
+  double* trace;       // (6E + H) slots x N2 x 5   face traces of U (read: stage s)
+  double* trace_out;   // the other trace buffer (written: traces of the stage s+1 state)
   double* fvn;         // (6E + H) slots x N2 x 4   viscous normal flux (mom x,y,z, energy)
   const double* slide_lift;  // S x N2 x 4
   const double* slide_flux;  // S x N2 x 5

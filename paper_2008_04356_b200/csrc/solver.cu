@@ -360,7 +360,7 @@ class GpuRankSolver {
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Comm> comm_;
 
-  DevBuf<double> U_, reg_, dudt_, trace_, fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
+  DevBuf<double> U_, reg_, dudt_, trace_[2], fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
   DevBuf<int8_t> side_type_;
   DevBuf<int> side_idx_, coords_, side_code_;
   int n_sm_ = 148;
@@ -391,6 +391,7 @@ class GpuRankSolver {
   double time_ = 0.0;
   int step_index_ = 0, stage_index_ = 0;
   bool traces_valid_ = false;
+  int cur_trace_ = 0;  // traces of the current state live in trace_[cur_trace_]
   long launches_ = 0;
   bool timing_ = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events_;
@@ -484,9 +485,11 @@ void GpuRankSolver::upload_topology() {
   dudt_.alloc(U_.n);
   U_.zero(stream_);
   reg_.zero(stream_);
-  trace_.alloc(slots * n2_ * 5);
+  for (auto& t : trace_) {
+    t.alloc(slots * n2_ * 5);
+    t.zero(stream_);
+  }
   fvn_.alloc(slots * n2_ * 4);
-  trace_.zero(stream_);
   fvn_.zero(stream_);
   slide_lift_.alloc(static_cast<size_t>(S_) * n2_ * 4);
   slide_flux_.alloc(static_cast<size_t>(S_) * n2_ * 5);
@@ -727,7 +730,8 @@ FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
   p.U = U;
   p.reg = reg_.p;
   p.out = out;
-  p.trace = trace_.p;
+  p.trace = trace_[cur_trace_].p;
+  p.trace_out = trace_[cur_trace_ ^ 1].p;
   p.fvn = fvn_.p;
   p.slide_lift = slide_lift_.p;
   p.slide_flux = slide_flux_.p;
@@ -745,7 +749,7 @@ FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
 
 MortarPtrs GpuRankSolver::mortar_ptrs() {
   MortarPtrs p{};
-  p.trace = trace_.p;
+  p.trace = trace_[cur_trace_].p;
   for (int r = 0; r < 2; ++r) {
     p.u_mine[r] = u_mine_[r].p;
     p.lift[r] = mlift_[r].p;
@@ -970,11 +974,11 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     mark(KC_PROLONG, false);
     launches_++;
   }
-  halo_exchange(trace_.p, 5, MK_SOL_CONF);
+  halo_exchange(trace_[cur_trace_].p, 5, MK_SOL_CONF);
   const MortarPtrs mp = mortar_ptrs();
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
   mark(KC_MORTAR, true);
-  launch_mortar_fill(n_, 5, trace_.p, u_src, fwd_ops_, mp, stream_);
+  launch_mortar_fill(n_, 5, trace_[cur_trace_].p, u_src, fwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
   launches_ += S_ > 0;
   mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
@@ -1016,6 +1020,9 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm_, stream_))) launch_update(n_, consts_, fp, a, stream_);
   mark(KC_UPDATE, false);
   launches_++;
+  // The update wrote the new traces into the other buffer: neighbours processed
+  // later in the same launch still read this stage's traces.
+  if (mode == 0) cur_trace_ ^= 1;
   traces_valid_ = (mode == 0 && !u_override);
 }
 
@@ -1105,10 +1112,10 @@ void GpuRankSolver::compute_gradients(double t_stage, const double* d_u, double*
   run_pairing(t_stage);
   FieldPtrs fp = field_ptrs(U, nullptr);
   launch_prolong(n_, consts_, fp, stream_);
-  halo_exchange(trace_.p, 5, MK_SOL_CONF);
+  halo_exchange(trace_[cur_trace_].p, 5, MK_SOL_CONF);
   const MortarPtrs mp = mortar_ptrs();
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
-  launch_mortar_fill(n_, 5, trace_.p, u_src, fwd_ops_, mp, stream_);
+  launch_mortar_fill(n_, 5, trace_[cur_trace_].p, u_src, fwd_ops_, mp, stream_);
   mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
   launch_mortar_lift(n_, consts_.gas, mp, max_mortars_[0], stream_);
   double* const l_src[2] = {mlift_[0].p, mlift_[1].p};

@@ -341,3 +341,19 @@ def test_baseline_config0_ten_steps():
     d = g.diagnostics(g.time())
     me = o.mass_energy(o.field())
     assert abs(d["mass"] - me[0]) <= 1e-12 * me[0]
+
+
+@pytest.mark.parametrize("degree,nx,nyz", [(3, 6, 14), (5, 4, 8)])
+def test_multi_wave_meshes_match_oracle(degree, nx, nyz):
+    """Meshes with several times more element tiles than resident CTAs, so the
+    persistent kernels process neighbours in different waves: a neighbour must
+    still see this stage's traces (double-buffered trace slots)."""
+    mesh = T.mesh_spec([(nx, 1.0, 0.0), (nx, 1.0, 0.7), (nx, 1.0, 0.0)], ny=nyz, nz=nyz)
+    cfg = T.solver_config(degree, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 3)
+    o.step(dt, 3)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
