@@ -53,9 +53,34 @@ __device__ __forceinline__ double prolong1(const double* __restrict__ s, const d
   return acc;
 }
 
+// Call-free reciprocal / square root for the face-flux hot loop: the MUFU seed
+// refined by Newton steps (~1 ulp; the correctly rounded library versions
+// branch to out-of-line slow paths whose call ABI makes ptxas spill the
+// kernel's live state).  Arguments are positive and normal on every
+// admissible state; anything else yields NaN, which the admissibility checks
+// report.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = __fma_rn(y, __fma_rn(-x, y, 1.0), y);
+  y = __fma_rn(y, __fma_rn(-x, y, 1.0), y);
+  return __fma_rn(y, __fma_rn(-x, y, 1.0), y);
+}
+
+__device__ __forceinline__ double sqrt_nr(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * __fma_rn(-hx * r, r, 1.5);
+  r = r * __fma_rn(-hx * r, r, 1.5);
+  const double s = x * r;
+  const double v = __fma_rn(0.5 * r, __fma_rn(-s, s, x), s);
+  return x > 0.0 ? v : (x == 0.0 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll));
+}
+
 // (v1, v2, v3, T) of a conserved state (state.hpp:47-84).
 __device__ __forceinline__ void prim4(const double* u, const GasD& g, double* q) {
-  const double ir = __drcp_rn(u[0]);
+  const double ir = rcp_nr(u[0]);
   q[0] = __dmul_rn(u[1], ir);
   q[1] = __dmul_rn(u[2], ir);
   q[2] = __dmul_rn(u[3], ir);
@@ -72,7 +97,7 @@ __device__ __forceinline__ double pressure(const double* u, double ir, const Gas
 __device__ __forceinline__ double entropy_fix(double lam, double lam_l, double lam_r) {
   const double delta = fmax(0.0, fmax(lam - lam_l, lam_r - lam));
   const double a = fabs(lam);
-  return a < 2.0 * delta ? lam * lam / (4.0 * delta) + delta : a;
+  return a < 2.0 * delta ? lam * lam * rcp_nr(4.0 * delta) + delta : a;
 }
 
 // Roe flux, Harten-Hyman fix on acoustic waves, eigenvalues shifted by the
@@ -81,7 +106,7 @@ __device__ __forceinline__ double entropy_fix(double lam, double lam_l, double l
 __device__ __forceinline__ bool roe_flux(const double* ul, const double* ur, int dir, double vg, const GasD& g,
                                          double* f) {
   const double rl = ul[0], rr = ur[0];
-  const double irl = __drcp_rn(rl), irr = __drcp_rn(rr);
+  const double irl = rcp_nr(rl), irr = rcp_nr(rr);
   const double mnl = sel3(dir, ul[1], ul[2], ul[3]), mal = sel3(dir, ul[2], ul[3], ul[1]),
                mbl = sel3(dir, ul[3], ul[1], ul[2]);
   const double mnr = sel3(dir, ur[1], ur[2], ur[3]), mar = sel3(dir, ur[2], ur[3], ur[1]),
@@ -91,10 +116,10 @@ __device__ __forceinline__ bool roe_flux(const double* ul, const double* ur, int
   const double pl = g.gm1 * (ul[4] - 0.5 * (mnl * unl + mal * ual + mbl * ubl));
   const double pr = g.gm1 * (ur[4] - 0.5 * (mnr * unr + mar * uar + mbr * ubr));
   const double hl = (ul[4] + pl) * irl, hr = (ur[4] + pr) * irr;
-  const double cl = sqrt(g.gamma * pl * irl), cr = sqrt(g.gamma * pr * irr);
+  const double cl = sqrt_nr(g.gamma * pl * irl), cr = sqrt_nr(g.gamma * pr * irr);
 
-  const double sl = sqrt(rl), sr = sqrt(rr);
-  const double inv = __drcp_rn(sl + sr);
+  const double sl = sqrt_nr(rl), sr = sqrt_nr(rr);
+  const double inv = rcp_nr(sl + sr);
   const double un = (sl * unl + sr * unr) * inv;
   const double ua = (sl * ual + sr * uar) * inv;
   const double ub = (sl * ubl + sr * ubr) * inv;
@@ -102,8 +127,8 @@ __device__ __forceinline__ bool roe_flux(const double* ul, const double* ur, int
   const double q2 = un * un + ua * ua + ub * ub;
   const double c2 = g.gm1 * (h - 0.5 * q2);
   if (!(c2 > 0.0)) return false;
-  const double c = sqrt(c2);
-  const double ic2 = __drcp_rn(c2);
+  const double c = sqrt_nr(c2);
+  const double ic2 = rcp_nr(c2);
   const double rho = sl * sr;
 
   const double dp = pr - pl, dun = unr - unl, dua = uar - ual, dub = ubr - ubl, drho = rr - rl;
@@ -139,7 +164,7 @@ __device__ __forceinline__ bool roe_flux(const double* ul, const double* ur, int
 
 // Viscous flux along direction dir, components 1..4 (flux.cpp:23-42).
 __device__ __forceinline__ void fv_dir(const double* u, const double* gr, int dir, const GasD& g, double* o) {
-  const double ir = __drcp_rn(u[0]);
+  const double ir = rcp_nr(u[0]);
   const double v0 = u[1] * ir, v1 = u[2] * ir, v2 = u[3] * ir;
   const double div = gr[0] + gr[4] + gr[8];
   const double t00 = 2.0 * g.mu * gr[0] + g.lam * div;
@@ -248,6 +273,15 @@ __device__ __forceinline__ void load_tables(const ElemConsts& C, double* tab) {
     tab[N1 * N1 + 3 * N1 + q] = C.liftw[1][q];
     tab[N1 * N1 + 4 * N1 + q] = C.inv_w[q];
   }
+}
+
+// Band table in shared memory: a dynamically indexed kernel-parameter load
+// (C.bands[band]) goes through the constant cache with long-scoreboard latency.
+__device__ __forceinline__ void load_bands(const ElemConsts& C, BandD* sb) {
+  constexpr int W = sizeof(BandD) / sizeof(double);
+  const double* src = reinterpret_cast<const double*>(C.bands);
+  double* dst = reinterpret_cast<double*>(sb);
+  for (int q = threadIdx.x; q < SDG_MAX_BANDS * W; q += blockDim.x) dst[q] = src[q];
 }
 
 // Flat, coalesced load of EPB consecutive elements into SoA shared memory su[v][node].
@@ -628,7 +662,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
   if (active) {
 #pragma unroll
     for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
-    const double ir = __drcp_rn(u[0]);
+    const double ir = rcp_nr(u[0]);
     const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
     const double p = pressure(u, ir, C.gas);
     const double vgv[3] = {0.0, B.vg, 0.0};
@@ -738,7 +772,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
     double w[5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) w[v] = su[v * N3 + t];
-    const double p = pressure(w, __drcp_rn(w[0]), C.gas);
+    const double p = pressure(w, rcp_nr(w[0]), C.gas);
     bool ok = w[0] > 0.0 && p > 0.0;
 #pragma unroll
     for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
@@ -1485,7 +1519,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
     if (active) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = __drcp_rn(u[0]);
+      const double ir = rcp_nr(u[0]);
       const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
       const double p = pressure(u, ir, C.gas);
 #pragma unroll
@@ -1574,7 +1608,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
           sR[t * 5 + v] = rg;
           sU[t * 5 + v] = wv[v];
         }
-        const double p = pressure(wv, __drcp_rn(wv[0]), C.gas);
+        const double p = pressure(wv, rcp_nr(wv[0]), C.gas);
         bool ok = wv[0] > 0.0 && p > 0.0;
 #pragma unroll
         for (int v = 0; v < 5; ++v) ok = ok && isfinite(wv[v]);
@@ -1620,8 +1654,12 @@ struct TmaV2 {
   static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
   static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
   static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
-  static constexpr int U_SMEM_PACK = U_SMEM + EPB * N3 * 8;  // node-major pitch-6 q / F staging
-  static constexpr int U_SMEM_S1 = U_SMEM_PACK - U_STAGE * 8;  // single-buffered stage
+  // Node-major pitch-6 q / F staging.  With F3 the three volume-flux directions are staged
+  // at once over [q | lift* | traces] (18 N3 per element; N1 = 8 lacks the shared memory).
+  static constexpr bool F3 = N1 != 8;
+  static constexpr int F3_EXTRA = F3 && 18 * N3 > 6 * N3 + 54 * N2 ? EPB * (12 * N3 - 54 * N2) : 0;
+  static constexpr int U_SMEM_PACK = U_SMEM + (EPB * N3 + F3_EXTRA) * 8;
+  static constexpr int U_SMEM_S1 = U_SMEM + EPB * N3 * 8 - U_STAGE * 8;  // single-buffered stage
 };
 
 // Update-kernel loads of one tile (issued by one thread).
@@ -1669,7 +1707,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
   double* tab = smem;
   double* stage0 = smem + D::TAB;
   double* work = stage0 + 2 * D::U_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 + D::F3_EXTRA : 0));
   __shared__ __align__(16) int codes[3][8 * EPB];
   load_tables<N1>(C, tab);
   const int tiles = (P.E + EPB - 1) / EPB;
@@ -1759,13 +1797,11 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
             prim4(other, C.gas, qb);
 #pragma unroll
             for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-            double fa[4], fb[4];
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+            // Fv.n of both sides read only now (not live through the Roe solve); the sum is
+            // symmetric, so both elements of the face still produce identical bits.
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              fa[c] = sFv[s * D::FS + f * 4 + c];
-              fb[c] = nb[D::TS + f * 4 + c];
-            }
-            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (sFv[s * D::FS + f * 4 + c] + nb[D::TS + f * 4 + c]);
           } else {
             ok = roe_flux(um, up, dir, vg, C.gas, flux);
           }
@@ -1777,6 +1813,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
           const double* up = (s & 1) ? ext : own;
           if (VISC) {
             prim4(ext, C.gas, lift);
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
             const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
             double gg[12];
 #pragma unroll
@@ -1784,7 +1821,8 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
             double fm[4], fp[4];
             fv_dir(um, gg, dir, C.gas, fm);
             fv_dir(up, gg, dir, C.gas, fp);
-            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
           } else {
             ok = roe_flux(um, up, dir, vg, C.gas, flux);
           }
@@ -1800,75 +1838,103 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     }
     __syncthreads();
 
-    // Phase 2: volume flux at the node (gradient recomputed from q and lift*).
-    double F[3][5], u[5];
+    // Phase 2: viscous stress at the node (gradient recomputed from q and lift*); only tau and
+    // the heat flux (9 values) cross the barrier that frees q / lift* for the flux staging.
+    double tau[3][3], hq[3];
+    if (VISC && active) {
+      double g[12];
+      if (PACK) node_gradient_pk<N1>(tab, q, lf, B, i, j, k, g);
+      else node_gradient<N1>(tab, q, lf, B, i, j, k, g);
+      const double div = g[0] + g[4] + g[8];
+      const double mu = C.gas.mu, lam = C.gas.lam;
+      tau[0][0] = 2.0 * mu * g[0] + lam * div;
+      tau[1][1] = 2.0 * mu * g[4] + lam * div;
+      tau[2][2] = 2.0 * mu * g[8] + lam * div;
+      tau[0][1] = tau[1][0] = mu * (g[1] + g[3]);
+      tau[0][2] = tau[2][0] = mu * (g[2] + g[6]);
+      tau[1][2] = tau[2][1] = mu * (g[5] + g[7]);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) hq[d] = C.gas.kcond * g[9 + d];
+    }
+    __syncthreads();  // q and lift* reads done
+
+    // Phase 3: volume flux and weak divergence through shared memory.  F_x is staged over q,
+    // F_y over the dead lift* / trace scratch, then F_z over q: only F_z (5 values) stays in
+    // registers across a barrier.
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double* qy = work + EPB * WF + le * WF;  // wLift + wTr hold >= EPB x 6 N3 doubles for N1 <= 9
+    double Fz[5];
+    auto flux_dir = [&](const double* u, const double* vv, double p, int d, double* f) {
+      const double vgd = d == 1 ? B.vg : 0.0;
+      f[0] = u[0] * vv[d] - vgd * u[0];
+      f[1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
+      f[2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
+      f[3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
+      f[4] = (u[4] + p) * vv[d] - vgd * u[4];
+      if (VISC) {
+        f[1] -= tau[d][0];
+        f[2] -= tau[d][1];
+        f[3] -= tau[d][2];
+        f[4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + hq[d];
+      }
+    };
+    auto stage_flux = [&](double* buf, const double* f, double sj) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) buf[PACK ? t * 6 + v : v * N3 + t] = f[v] * sj;
+    };
+    auto divergence = [&](const double* buf, int d) {
+      const int ia = d == 0 ? i : (d == 1 ? j : k);
+      const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double c = tab[ia * N1 + m];
+        if (PACK) {
+          const double* fp = buf + (base + m * stride) * 6;
+          const double2 f01 = *reinterpret_cast<const double2*>(fp);
+          const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
+          acc[0] += c * f01.x;
+          acc[1] += c * f01.y;
+          acc[2] += c * f23.x;
+          acc[3] += c * f23.y;
+          acc[4] += c * fp[4];
+        } else {
+#pragma unroll
+          for (int v = 0; v < 5; ++v) acc[v] += c * buf[v * N3 + base + m * stride];
+        }
+      }
+    };
+    constexpr bool F3 = PACK && D::F3;
+    double* qz = work + (F3 ? 2 * EPB * WF : 0) + le * WF;
     if (active) {
+      double u[5], f[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = __drcp_rn(u[0]);
+      const double ir = rcp_nr(u[0]);
       const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
       const double p = pressure(u, ir, C.gas);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double vgd = d == 1 ? B.vg : 0.0;
-        F[d][0] = u[0] * vv[d] - vgd * u[0];
-        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
-        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
-        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
-        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
-      }
-      if (VISC) {
-        double g[12];
-        if (PACK) node_gradient_pk<N1>(tab, q, lf, B, i, j, k, g);
-        else node_gradient<N1>(tab, q, lf, B, i, j, k, g);
-        const double div = g[0] + g[4] + g[8];
-        const double mu = C.gas.mu, lam = C.gas.lam;
-        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
-                     t22 = 2.0 * mu * g[8] + lam * div;
-        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
-        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          F[d][1] -= tau[d][0];
-          F[d][2] -= tau[d][1];
-          F[d][3] -= tau[d][2];
-          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
-        }
+      flux_dir(u, vv, p, 0, f);
+      stage_flux(q, f, B.sj[0]);
+      flux_dir(u, vv, p, 1, f);
+      stage_flux(qy, f, B.sj[1]);
+      if (F3) {
+        flux_dir(u, vv, p, 2, f);
+        stage_flux(qz, f, B.sj[2]);
+      } else {
+        flux_dir(u, vv, p, 2, Fz);
       }
     }
-
-    // Phase 3: weak divergence per direction through shared memory.
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
+    __syncthreads();
+    if (active) {
+      divergence(q, 0);
+      divergence(qy, 1);
+      if (F3) divergence(qz, 2);
+    }
+    if (!F3) {
       __syncthreads();
-      if (active) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) q[PACK ? t * 6 + v : v * N3 + t] = F[d][v] * B.sj[d];
-      }
+      if (active) stage_flux(q, Fz, B.sj[2]);
       __syncthreads();
-      if (active) {
-        const int ia = d == 0 ? i : (d == 1 ? j : k);
-        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          const double c = tab[ia * N1 + m];
-          if (PACK) {
-            const double* fp = q + (base + m * stride) * 6;
-            const double2 f01 = *reinterpret_cast<const double2*>(fp);
-            const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
-            acc[0] += c * f01.x;
-            acc[1] += c * f01.y;
-            acc[2] += c * f23.x;
-            acc[3] += c * f23.y;
-            acc[4] += c * fp[4];
-          } else {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
-          }
-        }
-      }
+      if (active) divergence(q, 2);
     }
 
     // Phase 4 + 5: surface lift, RK update in place, admissibility.
@@ -1895,6 +1961,9 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
         for (int v = 0; v < 5; ++v) o[v] = du[v];
       } else {
         double w[5];
+        double u[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
           const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
@@ -1902,7 +1971,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
           sR[t * 5 + v] = rg;
           sU[t * 5 + v] = w[v];
         }
-        const double p = pressure(w, __drcp_rn(w[0]), C.gas);
+        const double p = pressure(w, rcp_nr(w[0]), C.gas);
         bool ok = w[0] > 0.0 && p > 0.0;
 #pragma unroll
         for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
@@ -1946,7 +2015,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
   double* tab = smem;
   double* stage0 = smem + D::TAB;
   double* work = stage0 + D::U_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 + D::F3_EXTRA : 0));
   __shared__ __align__(16) int codes[3][8 * EPB];
   load_tables<N1>(C, tab);
   const int tiles = (P.E + EPB - 1) / EPB;
@@ -2028,13 +2097,11 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
             prim4(other, C.gas, qb);
 #pragma unroll
             for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-            double fa[4], fb[4];
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
+            // Fv.n of both sides read only now (not live through the Roe solve); the sum is
+            // symmetric, so both elements of the face still produce identical bits.
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              fa[c] = sFv[s * D::FS + f * 4 + c];
-              fb[c] = nb[D::TS + f * 4 + c];
-            }
-            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
+            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (sFv[s * D::FS + f * 4 + c] + nb[D::TS + f * 4 + c]);
           } else {
             ok = roe_flux(um, up, dir, vg, C.gas, flux);
           }
@@ -2046,6 +2113,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
           const double* up = (s & 1) ? ext : own;
           if (VISC) {
             prim4(ext, C.gas, lift);
+            ok = roe_flux(um, up, dir, vg, C.gas, flux);
             const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
             double gg[12];
 #pragma unroll
@@ -2053,7 +2121,8 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
             double fm[4], fp[4];
             fv_dir(um, gg, dir, C.gas, fm);
             fv_dir(up, gg, dir, C.gas, fp);
-            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
           } else {
             ok = roe_flux(um, up, dir, vg, C.gas, flux);
           }
@@ -2074,7 +2143,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
     if (active) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = __drcp_rn(u[0]);
+      const double ir = rcp_nr(u[0]);
       const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
       const double p = pressure(u, ir, C.gas);
 #pragma unroll
@@ -2171,7 +2240,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_upd
           sR[t * 5 + v] = rg;
           sU[t * 5 + v] = w[v];
         }
-        const double p = pressure(w, __drcp_rn(w[0]), C.gas);
+        const double p = pressure(w, rcp_nr(w[0]), C.gas);
         bool ok = w[0] > 0.0 && p > 0.0;
 #pragma unroll
         for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
@@ -2641,7 +2710,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const
     if (active) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = __drcp_rn(u[0]);
+      const double ir = rcp_nr(u[0]);
       const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
       const double p = pressure(u, ir, C.gas);
 #pragma unroll
@@ -2726,7 +2795,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const
           sR[t * 5 + v] = rg;
           sU[t * 5 + v] = wv[v];
         }
-        const double p = pressure(wv, __drcp_rn(wv[0]), C.gas);
+        const double p = pressure(wv, rcp_nr(wv[0]), C.gas);
         bool ok = wv[0] > 0.0 && p > 0.0;
 #pragma unroll
         for (int v = 0; v < 5; ++v) ok = ok && isfinite(wv[v]);
@@ -2790,7 +2859,9 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
   uint64_t* bars = reinterpret_cast<uint64_t*>(wFv + EPB * 6 * D::FS);
   __shared__ __align__(16) int codes[3][8 * EPB];
   __shared__ int lstr[EPB][6];
+  __shared__ BandD sbands[SDG_MAX_BANDS];
   load_tables<N1>(C, tab);
+  load_bands(C, sbands);
   const int tiles = (P.E + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   if (threadIdx.x == 0) {
@@ -2831,7 +2902,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
     double* q = wQ + le * 4 * N3;
     double* gS = wG + le * 12 * N3;
     double* fvo = wFv + le * 6 * D::FS;
-    const BandD& B = C.bands[active ? myc[6] : 0];
+    const BandD& B = sbands[active ? myc[6] : 0];
     mbar_wait(&bars[sidx], (it >> 1) & 1);
     // Phase 1: q; lift* in place over the neighbour slot (stride 5), sliding lift* stays at stride 4.
     if (active) {
