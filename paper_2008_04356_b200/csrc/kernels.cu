@@ -1234,6 +1234,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
                : "memory");
@@ -1642,7 +1645,10 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
   if (threadIdx.x == 0) bulk_wait0();
 }
 
-// Round-1 v2 layout: U and the RK register both double-buffered in the stage.
+// v2 layout.  Stage (double-buffered, TMA): U, the element's own face traces (written by the
+// previous stage's phase 6 / k_prolong, so phase 1 needs no prolongation), own Fv.n and the
+// per-side neighbour trace + Fv.n (or mortar flux + lift*).  The RK register is not staged:
+// it is prefetched into L2 with the tile and read / written by the owning thread in phase 5.
 template <int N1>
 struct TmaV2 {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
@@ -1651,7 +1657,7 @@ struct TmaV2 {
   static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : (N1 == 4 ? 4 : 2));
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
-  static constexpr int U_STAGE = EPB * (2 * EL + 6 * FS + 6 * NB);
+  static constexpr int U_STAGE = EPB * (EL + 6 * TS + 6 * FS + 6 * NB);
   static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
   static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
   // Node-major pitch-6 q / F staging.  With F3 the three volume-flux directions are staged
@@ -1659,17 +1665,16 @@ struct TmaV2 {
   static constexpr bool F3 = N1 != 8;
   static constexpr int F3_EXTRA = F3 && 18 * N3 > 6 * N3 + 54 * N2 ? EPB * (12 * N3 - 54 * N2) : 0;
   static constexpr int U_SMEM_PACK = U_SMEM + (EPB * N3 + F3_EXTRA) * 8;
-  static constexpr int U_SMEM_S1 = U_SMEM + EPB * N3 * 8 - U_STAGE * 8;  // single-buffered stage
 };
 
 // Update-kernel loads of one tile (issued by one thread).
 template <int N1, bool VISC>
 __device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int tile, const int* codes, double* st,
-                                                   uint64_t* bar) {
+                                                   uint64_t* bar, bool want_reg) {
   using D2 = TmaV2<N1>;
   const int e0 = tile * D2::EPB;
   const int n = min(D2::EPB, P.E - e0);
-  uint32_t bytes = 2u * n * D2::EL * 8u + (VISC ? n * 6u * D2::FS * 8u : 0u);
+  uint32_t bytes = n * (D2::EL + 6u * D2::TS) * 8u + (VISC ? n * 6u * D2::FS * 8u : 0u);
   for (int le = 0; le < n; ++le)
     for (int s = 0; s < 6; ++s) {
       const int typ = codes[8 * le + s] >> kCodeShift;
@@ -1677,11 +1682,11 @@ __device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int ti
     }
   mbar_arrive_expect_tx(bar, bytes);
   double* sU = st;
-  double* sR = st + D2::EPB * D2::EL;
-  double* sFv = sR + D2::EPB * D2::EL;
+  double* sOwn = st + D2::EPB * D2::EL;
+  double* sFv = sOwn + D2::EPB * 6 * D2::TS;
   double* sNb = sFv + D2::EPB * 6 * D2::FS;
   bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u, bar);
-  bulk_g2s(sR, P.reg + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u, bar);
+  bulk_g2s(sOwn, P.trace + static_cast<size_t>(e0) * 6 * D2::TS, n * 6u * D2::TS * 8u, bar);
   if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D2::FS, n * 6u * D2::FS * 8u, bar);
   for (int le = 0; le < n; ++le)
     for (int s = 0; s < 6; ++s) {
@@ -1696,6 +1701,7 @@ __device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int ti
         if (VISC) bulk_g2s(nb + D2::TS, P.slide_lift + static_cast<size_t>(idx) * D2::FS, D2::FS * 8u, bar);
       }
     }
+  if (want_reg) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u);
 }
 
 template <int N1, bool VISC, bool PACK>
@@ -1719,11 +1725,14 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     mbar_fence_init();
   }
   __syncthreads();
+  // The RK register is read only when the stage's a-coefficient is non-zero (LSRK stage 1 has
+  // a = 0: the register is overwritten without being read).
+  const bool want_reg = A.mode == 0 && A.rk_a != 0.0;
   int tile = blockIdx.x;
   if (threadIdx.x == 0 && tile < tiles) {
     prefetch_codes<N1>(P, tile, codes[0]);
     cp_async_wait_all();
-    issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
+    issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0], want_reg);
     if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
   }
   __syncthreads();  // codes[0] visible to every thread
@@ -1740,16 +1749,16 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       cp_async_wait_all();  // codes of `next`
       fence_proxy_async();
       issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::U_STAGE,
-                                   &bars[sidx ^ 1]);
+                                   &bars[sidx ^ 1], want_reg);
       if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
     }
     const int e0 = tile * EPB;
     const int e = e0 + le;
     const bool active = e < P.E;
     double* sU = st + le * D::EL;
-    double* sR = st + EPB * D::EL + le * D::EL;
-    double* sFv = st + 2 * EPB * D::EL + le * 6 * D::FS;
-    double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
+    const double* sOwn = st + EPB * D::EL + le * 6 * D::TS;
+    double* sFv = st + EPB * (D::EL + 6 * D::TS) + le * 6 * D::FS;
+    double* sNb = st + EPB * (D::EL + 6 * D::TS + 6 * D::FS) + le * 6 * D::NB;
     double* q = wF + le * WF;
     double* lf = wLift + le * 24 * N2;
     const int* myc = codes[it % 3] + 8 * le;
@@ -1781,7 +1790,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
         }
         double own[5];
 #pragma unroll
-        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
+        for (int v = 0; v < 5; ++v) own[v] = sOwn[s * D::TS + f * 5 + v];
         double flux[5], lift[4];
         bool ok;
         const double vg = dir == 1 ? B.vg : 0.0;
@@ -1962,13 +1971,15 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       } else {
         double w[5];
         double u[5];
+        double* gR = P.reg + (static_cast<size_t>(e) * N3 + t) * 5;
 #pragma unroll
         for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
+          double rg = A.dt * du[v];
+          if (want_reg) rg = __fma_rn(A.rk_a, gR[v], rg);
           w[v] = u[v] + A.rk_b * rg;
-          sR[t * 5 + v] = rg;
+          gR[v] = rg;
           sU[t * 5 + v] = w[v];
         }
         const double p = pressure(w, rcp_nr(w[0]), C.gas);
@@ -1998,276 +2009,6 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     if (threadIdx.x == 0) {
       const int n = min(EPB, P.E - e0);
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
-      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
-      bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
-      bulk_commit();
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait0();
-}
-
-template <int N1, bool VISC, bool PACK>
-__global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB + 1) k_update_tma_s1(const __grid_constant__ ElemConsts C, FieldPtrs P,
-                                                                 StageArgs A) {
-  using D = TmaV2<N1>;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* stage0 = smem + D::TAB;
-  double* work = stage0 + D::U_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 + D::F3_EXTRA : 0));
-  __shared__ __align__(16) int codes[3][8 * EPB];
-  load_tables<N1>(C, tab);
-  const int tiles = (P.E + EPB - 1) / EPB;
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < tiles) prefetch_codes<N1>(P, tile, codes[0]);
-  constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
-  double* wF = work;
-  double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
-  double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
-  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-    double* st = stage0;
-    const int next = tile + gridDim.x;
-    if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous tile's stores have read the stage and wTr
-      cp_async_wait_all();  // codes of this tile
-      fence_proxy_async();
-      issue_update_loads_v2<N1, VISC>(P, tile, codes[it & 1], stage0, &bars[0]);
-      if (next < tiles) prefetch_codes<N1>(P, next, codes[(it + 1) & 1]);
-    }
-    const int e0 = tile * EPB;
-    const int e = e0 + le;
-    const bool active = e < P.E;
-    double* sU = st + le * D::EL;
-    double* sR = st + EPB * D::EL + le * D::EL;
-    double* sFv = st + 2 * EPB * D::EL + le * 6 * D::FS;
-    double* sNb = st + 2 * EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
-    double* q = wF + le * WF;
-    double* lf = wLift + le * 24 * N2;
-    const int* myc = codes[it % 3] + 8 * le;
-    const BandD& B = C.bands[active ? myc[6] : 0];
-    mbar_wait(&bars[0], it & 1);
-
-    // Phase 1: face fluxes (in place over the neighbour data) and lift*.
-    if (active) {
-      if (VISC) {
-        double u[5], qq[4];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-        prim4(u, C.gas, qq);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) q[PACK ? t * 6 + c : c * N3 + t] = qq[c];
-      }
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        double* nb = sNb + s * D::NB;
-        const int code = myc[s];
-        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-        if (typ == kSliding) {
-          if (VISC) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = nb[D::TS + f * 4 + c];
-          }
-          continue;
-        }
-        double own[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
-        double flux[5], lift[4];
-        bool ok;
-        const double vg = dir == 1 ? B.vg : 0.0;
-        if (typ == kConforming) {
-          double other[5];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
-          const double* um = (s & 1) ? own : other;
-          const double* up = (s & 1) ? other : own;
-          if (VISC) {
-            double qa[4], qb[4];
-            prim4(own, C.gas, qa);
-            prim4(other, C.gas, qb);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-            // Fv.n of both sides read only now (not live through the Roe solve); the sum is
-            // symmetric, so both elements of the face still produce identical bits.
-#pragma unroll
-            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (sFv[s * D::FS + f * 4 + c] + nb[D::TS + f * 4 + c]);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        } else {
-          double x[3], ext[5];
-          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-          const double* um = (s & 1) ? own : ext;
-          const double* up = (s & 1) ? ext : own;
-          if (VISC) {
-            prim4(ext, C.gas, lift);
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
-            double gg[12];
-#pragma unroll
-            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
-            double fm[4], fp[4];
-            fv_dir(um, gg, dir, C.gas, fm);
-            fv_dir(up, gg, dir, C.gas, fp);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        }
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
-        if (VISC) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
-        }
-      }
-    }
-    __syncthreads();
-
-    // Phase 2: volume flux at the node (gradient recomputed from q and lift*).
-    double F[3][5], u[5];
-    if (active) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = rcp_nr(u[0]);
-      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
-      const double p = pressure(u, ir, C.gas);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double vgd = d == 1 ? B.vg : 0.0;
-        F[d][0] = u[0] * vv[d] - vgd * u[0];
-        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
-        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
-        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
-        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
-      }
-      if (VISC) {
-        double g[12];
-        if (PACK) node_gradient_pk<N1>(tab, q, lf, B, i, j, k, g);
-        else node_gradient<N1>(tab, q, lf, B, i, j, k, g);
-        const double div = g[0] + g[4] + g[8];
-        const double mu = C.gas.mu, lam = C.gas.lam;
-        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
-                     t22 = 2.0 * mu * g[8] + lam * div;
-        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
-        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          F[d][1] -= tau[d][0];
-          F[d][2] -= tau[d][1];
-          F[d][3] -= tau[d][2];
-          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
-        }
-      }
-    }
-
-    // Phase 3: weak divergence per direction through shared memory.
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      __syncthreads();
-      if (active) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) q[PACK ? t * 6 + v : v * N3 + t] = F[d][v] * B.sj[d];
-      }
-      __syncthreads();
-      if (active) {
-        const int ia = d == 0 ? i : (d == 1 ? j : k);
-        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          const double c = tab[ia * N1 + m];
-          if (PACK) {
-            const double* fp = q + (base + m * stride) * 6;
-            const double2 f01 = *reinterpret_cast<const double2*>(fp);
-            const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
-            acc[0] += c * f01.x;
-            acc[1] += c * f01.y;
-            acc[2] += c * f23.x;
-            acc[3] += c * f23.y;
-            acc[4] += c * fp[4];
-          } else {
-#pragma unroll
-            for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
-          }
-        }
-      }
-    }
-
-    // Phase 4 + 5: surface lift, RK update in place, admissibility.
-    if (active) {
-      double du[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
-      const double* lw = tab + N1 * N1 + 2 * N1;
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int dir = s >> 1;
-        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
-        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
-        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
-        if (c != 0.0) {
-          const double* fl = sNb + s * D::NB + f * 5;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
-        }
-      }
-      if (A.mode == 1) {
-        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = du[v];
-      } else {
-        double w[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
-          w[v] = u[v] + A.rk_b * rg;
-          sR[t * 5 + v] = rg;
-          sU[t * 5 + v] = w[v];
-        }
-        const double p = pressure(w, rcp_nr(w[0]), C.gas);
-        bool ok = w[0] > 0.0 && p > 0.0;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
-      }
-    }
-    if (A.mode == 1) {
-      __syncthreads();
-      continue;
-    }
-    __syncthreads();
-    // Phase 6: traces of the new state, then bulk stores of U, reg and traces.
-    if (active) {
-      double* tr = wTr + le * 6 * D::TS;
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int n = min(EPB, P.E - e0);
-      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
-      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
       bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
       bulk_commit();
     }
@@ -3022,19 +2763,6 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
     }
     const bool v3 = variant == 3 || variant == 4;
     const bool pack = variant == 6;
-    if (variant == 7) {
-      auto k7 = c.gas.viscous ? k_update_tma_s1<N1, true, true> : k_update_tma_s1<N1, false, true>;
-      static int occ7[2] = {-1, -1};
-      int& o7 = occ7[c.gas.viscous ? 1 : 0];
-      if (o7 < 0) {
-        cudaFuncSetAttribute(k7, cudaFuncAttributeMaxDynamicSharedMemorySize, TmaV2<N1>::U_SMEM_S1);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k7, D::THREADS, TmaV2<N1>::U_SMEM_S1);
-        if (o7 < 1) o7 = 1;
-      }
-      k7<<<std::min(tiles, n_sm * o7), D::THREADS, TmaV2<N1>::U_SMEM_S1, st>>>(c, p, a);
-      check_launch("k_update_tma_s1");
-      return true;
-    }
     auto kern = variant == 3 ? (c.gas.viscous ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
               : variant == 4 ? (c.gas.viscous ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
               : pack ? (c.gas.viscous ? k_update_tma_v2<N1, true, true> : k_update_tma_v2<N1, false, true>)
