@@ -2626,7 +2626,6 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
     const int e0 = tile * EPB;
     const int n_el = min(EPB, P.E - e0);
     if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous Fv.n store has read wFv
       if (next < tiles) {
         cp_async_wait_all();
         fence_proxy_async();
@@ -2688,6 +2687,9 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
     }
     __syncthreads();
     if (active) gradient_lines<N1>(C, B, q, sNb, D::TS, lstr[le], 1, gS, t, N3);
+    // The previous tile's Fv.n store must have read wFv before phase 3 rewrites it; waiting
+    // here (not at the top of the tile) keeps warp 0 from holding up phase 1.
+    if (threadIdx.x == 0) bulk_wait_read0();
     __syncthreads();
     if (active && P.grad_out != nullptr) {
       double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
