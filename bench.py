@@ -160,9 +160,37 @@ def cpu_baseline(args, conf, timeout_s=20.0):
                 break
     except OSError:
         pass
-    return {"value": dof * 5 * steps / el, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same TGV case at "
-                      f"{e}^3 elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
+    out = {"value": dof * 5 * steps / el, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same TGV case at "
+                     f"{e}^3 elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
+    try:
+        out["reference_2d"] = reference_2d(args.degree, seconds=min(8.0, timeout_s))
+    except Exception as ex:  # supplementary: never fail the bench line over it
+        out["reference_2d"] = {"unavailable": str(ex)[:200]}
+    return out
+
+
+def reference_2d(degree, seconds=8.0):
+    """the UNMODIFIED reference library (oracle/_ref, compiled from
+    /root/reference/proj/src) on the 2D analog of configs[4]: 3 bands with the
+    middle one sliding at 0.2, viscous (mu = 1/1600), Gauss nodes, 48 x 48
+    elements (the reference has no TGV case; its density wave stands in), run by
+    the reference's own runner with one thread per rank (Backend::InProc).
+    Supplementary only: a 2D node carries 4 variables and 2 directions of work."""
+    from oracle import pyoracle as P
+    if not os.path.exists(P.REF_SO):
+        return {"unavailable": "oracle/_ref/libsdg_ref.so not built"}
+    ranks = max(3, min(os.cpu_count() or 1, 48))
+    spec = P.ref_spec([(16, 1.0, 0.0), (16, 1.0, 0.2), (16, 1.0, 0.0)], 48, degree, mu=1.0 / 1600.0)
+    ref = P.Ref2D(spec)
+    dt = 0.5 * ref.suggest_dt(0.5)
+    _, w = ref.run(dt, 2, ranks=ranks)
+    n = max(2, int(seconds / max(w / 2, 1e-6)))
+    _, wall = ref.run(dt, n, ranks=ranks)
+    nodes = 48 * 48 * (degree + 1) ** 2
+    return {"value": nodes * 5 * n / wall, "unit": "2D node-stage-updates/s", "ranks": ranks, "kind": "reference",
+            "sample": f"reference runner (InProc threads, {ranks} ranks), 2D 48x48 elements, N={degree} Gauss, "
+                      f"viscous, 3 bands, {n} RK steps in {wall:.1f} s (stepping-loop wall, runner.cpp:41-43)"}
 
 
 def reference_arm(args, world, rank):

@@ -551,4 +551,25 @@ void eval_case_host(const sdg_case& cs, const sdg_gas& g, const double* x, doubl
   u[3] = rho * v2;
   u[4] = p / gm1 + 0.5 * rho * (v0 * v0 + v1 * v1 + v2 * v2);
 }
+std::array<int, 2> interior_run(const LocalTopology& topo) {
+  const int E = static_cast<int>(topo.gids.size());
+  int best_lo = 0, best_len = 0, run_lo = 0;
+  for (int e = 0; e <= E; ++e) {
+    bool interior = e < E;
+    for (int s = 0; interior && s < 6; ++s) {
+      const size_t k = static_cast<size_t>(e) * 6 + s;
+      if (topo.side_type[k] == kSliding || (topo.side_type[k] == kConforming && topo.side_idx[k] >= 6 * E))
+        interior = false;
+    }
+    if (!interior) {
+      if (e - run_lo > best_len) {
+        best_len = e - run_lo;
+        best_lo = run_lo;
+      }
+      run_lo = e + 1;
+    }
+  }
+  return {best_lo, best_lo + best_len};
+}
+
 }  // namespace sdg

@@ -109,6 +109,9 @@ struct LocalTopology {
   std::vector<PeerFaces> peers;   // ascending partner
 };
 LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int rank);
+// Longest run [lo, hi) of local elements with no remote conforming and no sliding side: the
+// elements whose kernels can run while the halo exchange is in flight.
+std::array<int, 2> interior_run(const LocalTopology& topo);
 
 // Nodal basis (proj/src/nodal_basis.cpp:89-182, same published algorithm).
 struct Basis {

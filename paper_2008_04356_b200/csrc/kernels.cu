@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_prolong(const __grid_const
   double* elems = smem + TAB;
   constexpr int PER = 5 * N3;
   load_tables<N1>(C, tab);
-  const int e0 = blockIdx.x * EPB;
+  const int e0 = P.e_first + blockIdx.x * EPB;
   load_state<N1>(P.U, e0, P.E, elems, PER);
   __syncthreads();
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_gradient(const __grid_cons
   extern __shared__ double smem[];
   double* tab = smem;
   load_tables<N1>(C, tab);
-  const int e0 = blockIdx.x * EPB;
+  const int e0 = P.e_first + blockIdx.x * EPB;
   load_state<N1>(P.U, e0, P.E, smem + TAB, PER);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
   const bool active = e < P.E;
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
   extern __shared__ double smem[];
   double* tab = smem;
   load_tables<N1>(C, tab);
-  const int e0 = blockIdx.x * EPB;
+  const int e0 = P.e_first + blockIdx.x * EPB;
   load_state<N1>(P.U, e0, P.E, smem + TAB, PER);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
   const bool active = e < P.E;
@@ -1283,7 +1283,7 @@ struct Tma {
 template <int N1>
 __device__ __forceinline__ void prefetch_codes(const FieldPtrs& P, int tile, int* dst) {
   using D = Tma<N1>;
-  const int e0 = tile * D::EPB;
+  const int e0 = P.e_first + tile * D::EPB;
   const int n = min(D::EPB, P.E - e0);
   for (int q = 0; q < n * 2; ++q) cp_async16(dst + 4 * q, P.side_code + 8 * e0 + 4 * q);
   cp_async_commit();
@@ -1294,7 +1294,7 @@ template <int N1, bool VISC>
 __device__ __forceinline__ void issue_update_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                    uint64_t* bar) {
   using D = Tma<N1>;
-  const int e0 = tile * D::EPB;
+  const int e0 = P.e_first + tile * D::EPB;
   const int n = min(D::EPB, P.E - e0);
   uint32_t bytes = n * D::EL * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
   for (int le = 0; le < n; ++le)
@@ -1382,7 +1382,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
   uint64_t* bars = reinterpret_cast<uint64_t*>(wLift + EPB * 24 * N2);
   __shared__ __align__(16) int codes[2][8 * EPB];
   load_tables<N1>(C, tab);
-  const int tiles = (P.E + EPB - 1) / EPB;
+  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   if (threadIdx.x == 0) {
@@ -1403,7 +1403,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
     const int sidx = it & 1;
     double* st = stage0 + sidx * D::U_STAGE;
     const int next = tile + gridDim.x;
-    const int e0 = tile * EPB;
+    const int e0 = P.e_first + tile * EPB;
     const int n_el = min(EPB, P.E - e0);
     if (threadIdx.x == 0) {
       bulk_wait_read0();  // the previous tile's stores no longer read regb / wF / stage sidx^1
@@ -1672,7 +1672,7 @@ template <int N1, bool VISC>
 __device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                    uint64_t* bar, bool want_reg) {
   using D2 = TmaV2<N1>;
-  const int e0 = tile * D2::EPB;
+  const int e0 = P.e_first + tile * D2::EPB;
   const int n = min(D2::EPB, P.E - e0);
   uint32_t bytes = n * (D2::EL + 6u * D2::TS) * 8u + (VISC ? n * 6u * D2::FS * 8u : 0u);
   for (int le = 0; le < n; ++le)
@@ -1716,7 +1716,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
   uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 + D::F3_EXTRA : 0));
   __shared__ __align__(16) int codes[3][8 * EPB];
   load_tables<N1>(C, tab);
-  const int tiles = (P.E + EPB - 1) / EPB;
+  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   if (threadIdx.x == 0) {
@@ -1752,7 +1752,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
                                    &bars[sidx ^ 1], want_reg);
       if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
     }
-    const int e0 = tile * EPB;
+    const int e0 = P.e_first + tile * EPB;
     const int e = e0 + le;
     const bool active = e < P.E;
     double* sU = st + le * D::EL;
@@ -2022,7 +2022,7 @@ template <int N1>
 __device__ __forceinline__ void issue_gradient_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                      uint64_t* bar) {
   using D = Tma<N1>;
-  const int e0 = tile * D::EPB;
+  const int e0 = P.e_first + tile * D::EPB;
   const int n = min(D::EPB, P.E - e0);
   uint32_t bytes = n * D::EL * 8u;
   for (int le = 0; le < n; ++le)
@@ -2089,7 +2089,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
   __shared__ __align__(16) int codes[2][8 * EPB];
   __shared__ int lstr[EPB][6];
   load_tables<N1>(C, tab);
-  const int tiles = (P.E + EPB - 1) / EPB;
+  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -2118,7 +2118,7 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const _
         if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
       }
     }
-    const int e0 = tile * EPB;
+    const int e0 = P.e_first + tile * EPB;
     const int e = e0 + le;
     const bool active = e < P.E;
     double* sU = st + le * D::EL;
@@ -2281,7 +2281,7 @@ template <int N1, bool VISC>
 __device__ __forceinline__ void issue_update_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                     uint64_t* bar) {
   using D = T5<N1>;
-  const int e0 = tile * D::EPB;
+  const int e0 = P.e_first + tile * D::EPB;
   const int n = min(D::EPB, P.E - e0);
   uint32_t bytes = n * (2u * D::EL + 6u * D::TS) * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
   for (int le = 0; le < n; ++le)
@@ -2324,7 +2324,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const
   uint64_t* bars = reinterpret_cast<uint64_t*>(wF + EPB * 5 * N3);
   __shared__ __align__(16) int codes[3][8 * EPB];
   load_tables<N1>(C, tab);
-  const int tiles = (P.E + EPB - 1) / EPB;
+  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   if (threadIdx.x == 0) {
@@ -2345,7 +2345,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const
     const int sidx = it & 1;
     double* st = stage0 + sidx * D::U_STAGE;
     const int next = tile + gridDim.x;
-    const int e0 = tile * EPB;
+    const int e0 = P.e_first + tile * EPB;
     const int n_el = min(EPB, P.E - e0);
     const int* cd = codes[it % 3];
     if (threadIdx.x == 0) {
@@ -2563,7 +2563,7 @@ template <int N1>
 __device__ __forceinline__ void issue_gradient_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                       uint64_t* bar) {
   using D = T5<N1>;
-  const int e0 = tile * D::EPB;
+  const int e0 = P.e_first + tile * D::EPB;
   const int n = min(D::EPB, P.E - e0);
   uint32_t bytes = n * (D::EL + 6u * D::TS) * 8u;
   for (int le = 0; le < n; ++le)
@@ -2603,7 +2603,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
   __shared__ BandD sbands[SDG_MAX_BANDS];
   load_tables<N1>(C, tab);
   load_bands(C, sbands);
-  const int tiles = (P.E + EPB - 1) / EPB;
+  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -2623,7 +2623,7 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
     const int sidx = it & 1;
     double* st = stage0 + sidx * D::G_STAGE;
     const int next = tile + gridDim.x;
-    const int e0 = tile * EPB;
+    const int e0 = P.e_first + tile * EPB;
     const int n_el = min(EPB, P.E - e0);
     if (threadIdx.x == 0) {
       if (next < tiles) {
@@ -2734,7 +2734,7 @@ bool v5_t(bool update, const ElemConsts& c, const FieldPtrs& p, const StageArgs&
     return false;
   } else {
     using D = T5<N1>;
-    const int tiles = (p.E + D::EPB - 1) / D::EPB;
+    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
     auto kern = update ? (c.gas.viscous ? k_update5<N1, true> : k_update5<N1, false>) : k_gradient5<N1>;
     const int smem = update ? D::U_SMEM : D::G_SMEM;
     static int occ_tab[3] = {-1, -1, -1};
@@ -2757,7 +2757,7 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
     return false;
   } else {
     using D = Tma<N1>;
-    const int tiles = (p.E + D::EPB - 1) / D::EPB;
+    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
     static int variant = -1;
     if (variant < 0) {
       const char* env = std::getenv("SDG_UPDATE_V");
@@ -2789,7 +2789,7 @@ bool gradient_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a,
     return false;
   } else {
     using D = Tma<N1>;
-    const int tiles = (p.E + D::EPB - 1) / D::EPB;
+    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
     static int minb = -1;
     if (minb < 0) {
       const char* env = std::getenv("SDG_GRAD_MINB");
@@ -2819,7 +2819,7 @@ void set_smem(K kernel, int bytes) {
 
 template <int N1>
 void prolong_t(const ElemConsts& c, const FieldPtrs& p, cudaStream_t st) {
-  const int blocks = (p.E + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
+  const int blocks = (p.E - p.e_first + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
   const int sm = smem_prolong<N1>();
   set_smem(k_prolong<N1>, sm);
   k_prolong<N1><<<blocks, Dim<N1>::THREADS, sm, st>>>(c, p);
@@ -2827,7 +2827,7 @@ void prolong_t(const ElemConsts& c, const FieldPtrs& p, cudaStream_t st) {
 }
 template <int N1>
 void gradient_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  const int blocks = (p.E + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
+  const int blocks = (p.E - p.e_first + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
   const int sm = smem_gradient<N1>();
   set_smem(k_gradient<N1>, sm);
   k_gradient<N1><<<blocks, Dim<N1>::THREADS, sm, st>>>(c, p, a);
@@ -2835,7 +2835,7 @@ void gradient_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cud
 }
 template <int N1>
 void update_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  const int blocks = (p.E + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
+  const int blocks = (p.E - p.e_first + Dim<N1>::EPB - 1) / Dim<N1>::EPB;
   const int sm = smem_update<N1>();
   if (c.gas.viscous) {
     set_smem(k_update<N1, true>, sm);
@@ -2884,15 +2884,15 @@ void mortar_back_t(int nc, const double* const src[2], double* dst, const Mortar
 }  // namespace
 
 void launch_prolong(int n1, const ElemConsts& c, const FieldPtrs& p, cudaStream_t st) {
-  if (p.E == 0) return;
+  if (p.E <= p.e_first) return;
   SDG_DISPATCH(n1, (prolong_t<NN>(c, p, st)));
 }
 void launch_gradient(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  if (p.E == 0) return;
+  if (p.E <= p.e_first) return;
   SDG_DISPATCH(n1, (gradient_t<NN>(c, p, a, st)));
 }
 void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  if (p.E == 0) return;
+  if (p.E <= p.e_first) return;
   SDG_DISPATCH(n1, (update_t<NN>(c, p, a, st)));
 }
 static int env_int(const char* name, int dflt) {
@@ -2901,7 +2901,7 @@ static int env_int(const char* name, int dflt) {
 }
 bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                          cudaStream_t st) {
-  if (p.E == 0) return true;
+  if (p.E <= p.e_first) return true;
   bool ok = false;
   static const int gv = env_int("SDG_GRAD_V", 5);
   if (gv == 5) {
@@ -2913,7 +2913,7 @@ bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const 
 }
 bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                        cudaStream_t st) {
-  if (p.E == 0) return true;
+  if (p.E <= p.e_first) return true;
   bool ok = false;
   static const int uv = env_int("SDG_UPDATE_V", 6);
   if (uv == 5) {

@@ -62,7 +62,8 @@ struct FieldPtrs {
   const int* side_code;      // E x 8: idx | type << 29 for the 6 sides, [6] = band, [7] pad (32 B/element)
   double* grad_out;          // optional E x N3 x 12
   ErrRec* err;
-  int E;
+  int E;        // element kernels process local elements [e_first, E)
+  int e_first;  // (interior / boundary split for exchange overlap; 0 = all)
 };
 
 struct StageArgs {

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <condition_variable>
 #include <deque>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <memory>
@@ -341,7 +342,12 @@ class GpuRankSolver {
   void update_interfaces_host(double t_stage);
   void run_pairing(double t_stage);
   void mortar_exchange(double* const src[2], double* dst_static, int ncomp, bool moving_to_static, int kind);
-  void halo_exchange(double* arr, int ncomp, int kind);
+  void halo_exchange(double* arr, int ncomp, int kind, const std::function<void()>& overlap_work = {});
+  void comm_round(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, bool join,
+                  const std::function<void()>& overlap_work = {});
+  void join_comm();
+  void element_kernel(bool update, const FieldPtrs& fp, const StageArgs& a, int e_first, int e_end, int n_sm);
+  void find_interior_run();
   FieldPtrs field_ptrs(double* U, double* out);
   MortarPtrs mortar_ptrs();
   void check_error();
@@ -359,6 +365,14 @@ class GpuRankSolver {
   bool lifting_ = false;
   cudaStream_t stream_ = nullptr;
   std::unique_ptr<Comm> comm_;
+  // Exchange overlap: every comm round runs on comm_stream_ in issue order; the
+  // conforming halo rounds are joined only after the element kernel has processed the
+  // interior run [int_lo_, int_hi_) (elements with no remote or sliding side).
+  cudaStream_t comm_stream_ = nullptr;
+  cudaEvent_t ev_ready_ = nullptr, ev_comm_ = nullptr;
+  int int_lo_ = 0, int_hi_ = 0;
+  bool overlap_ = false;
+  int sm_reserve_ = 0;  // SMs left free for the NCCL kernels while the interior run computes
 
   DevBuf<double> U_, reg_, dudt_, trace_[2], fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
   DevBuf<int8_t> side_type_;
@@ -423,9 +437,14 @@ GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& c
     if (inproc_hub) comm_ = std::make_unique<InProcComm>(inproc_hub, n_ranks, rank);
     else if (nccl_id) comm_ = std::make_unique<NcclComm>(nccl_id, n_ranks, rank);
     else throw ConfigError("multi-rank context needs an NCCL unique id or an in-process hub name");
+    cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming), "event");
+    sm_reserve_ = inproc_hub ? 0 : 8;
   }
   build_consts();
   upload_topology();
+  find_interior_run();
   build_sides();
   cuda_check(cudaMallocHost(&err_host_, sizeof(ErrRec)), "cudaMallocHost");
   cuda_check(cudaStreamSynchronize(stream_), "setup sync");
@@ -437,9 +456,25 @@ GpuRankSolver::~GpuRankSolver() {
     cudaEventDestroy(ev.second.first);
     cudaEventDestroy(ev.second.second);
   }
+  if (comm_stream_) cudaStreamSynchronize(comm_stream_);
   comm_.reset();
+  if (ev_ready_) cudaEventDestroy(ev_ready_);
+  if (ev_comm_) cudaEventDestroy(ev_comm_);
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
   if (err_host_) cudaFreeHost(err_host_);
   if (stream_) cudaStreamDestroy(stream_);
+}
+
+// Interior run of this rank (host.cpp interior_run).  With the contiguous band-block
+// partition it is everything but the first and last planes of the rank's block.
+void GpuRankSolver::find_interior_run() {
+  int_lo_ = int_hi_ = 0;
+  overlap_ = false;
+  if (n_ranks_ == 1 || std::getenv("SDG_NO_OVERLAP")) return;
+  const auto run = interior_run(topo_);
+  int_lo_ = run[0];
+  int_hi_ = run[1];
+  overlap_ = int_hi_ > int_lo_;
 }
 
 void GpuRankSolver::build_consts() {
@@ -924,8 +959,45 @@ void GpuRankSolver::mortar_exchange(double* const src[2], double* dst, int nc, b
   for (const auto& e : sched_[to]) recvs.push_back({e[0], dst + e[1] * node, e[2] * node});
   record(kind, sends, recvs);
   mark(KC_HALO, true);
-  comm_->exchange(sends, recvs, stream_);
+  comm_round(sends, recvs, true);
   mark(KC_HALO, false);
+}
+
+// One grouped exchange on the comm stream, after everything stream_ has enqueued so far.
+// join: stream_ waits for it at once; otherwise join_comm() later.
+// overlap_work is enqueued on stream_ after the data-ready point and before the round is
+// issued, so it runs concurrently with the exchange even when the transport blocks the host.
+void GpuRankSolver::comm_round(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, bool join,
+                               const std::function<void()>& overlap_work) {
+  cuda_check(cudaEventRecord(ev_ready_, stream_), "event record");
+  if (overlap_work) overlap_work();
+  cuda_check(cudaStreamWaitEvent(comm_stream_, ev_ready_, 0), "wait event");
+  comm_->exchange(sends, recvs, comm_stream_);
+  cuda_check(cudaEventRecord(ev_comm_, comm_stream_), "event record");
+  if (join) join_comm();
+}
+
+// stream_ waits for every comm round issued so far (they run in order on comm_stream_).
+void GpuRankSolver::join_comm() {
+  if (comm_stream_) cuda_check(cudaStreamWaitEvent(stream_, ev_comm_, 0), "wait event");
+}
+
+// k_gradient / k_update over local elements [e_first, e_end).
+void GpuRankSolver::element_kernel(bool update, const FieldPtrs& fp0, const StageArgs& a, int e_first, int e_end,
+                                   int n_sm) {
+  if (e_end <= e_first) return;
+  FieldPtrs fp = fp0;
+  fp.e_first = e_first;
+  fp.E = e_end;
+  mark(update ? KC_UPDATE : KC_GRADIENT, true);
+  if (update) {
+    if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm, stream_))) launch_update(n_, consts_, fp, a, stream_);
+  } else {
+    if (!(use_tma_ && launch_gradient_tma(n_, consts_, fp, a, n_sm, stream_)))
+      launch_gradient(n_, consts_, fp, a, stream_);
+  }
+  mark(update ? KC_UPDATE : KC_GRADIENT, false);
+  launches_++;
 }
 
 // Conforming halo exchange of face data (traces or Fv.n): gather the local
@@ -938,8 +1010,11 @@ __global__ void k_gather_slots(const double* src, const int* slots, int n_slots,
   dst[i] = src[static_cast<size_t>(slots[s]) * per_slot + q];
 }
 
-void GpuRankSolver::halo_exchange(double* arr, int nc, int kind) {
-  if (n_ranks_ == 1) return;
+void GpuRankSolver::halo_exchange(double* arr, int nc, int kind, const std::function<void()>& overlap_work) {
+  if (n_ranks_ == 1) {
+    if (overlap_work) overlap_work();
+    return;
+  }
   const int per = n2_ * nc;
   const int ns = static_cast<int>(send_slots_.n);
   mark(KC_HALO, true);
@@ -956,8 +1031,8 @@ void GpuRankSolver::halo_exchange(double* arr, int nc, int kind) {
     off += cnt;
   }
   record(kind, sends, recvs);
-  comm_->exchange(sends, recvs, stream_);
   mark(KC_HALO, false);
+  comm_round(sends, recvs, !overlap_work, overlap_work);
 }
 
 // One right-hand-side evaluation (compute_residual, solver.cpp:846-870) with
@@ -974,7 +1049,6 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     mark(KC_PROLONG, false);
     launches_++;
   }
-  halo_exchange(trace_[cur_trace_].p, 5, MK_SOL_CONF);
   const MortarPtrs mp = mortar_ptrs();
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
   mark(KC_MORTAR, true);
@@ -983,6 +1057,21 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   launches_ += S_ > 0;
   mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
   StageArgs a{t_stage, dt, rk_a, rk_b, mode, step_index_, stage_index_};
+  // Element kernel over all local elements; with an exchange in flight, the interior run
+  // first (on all but sm_reserve_ SMs), then the join, then the two boundary ranges.
+  // Halo round of `arr` + element kernel: with overlap, the interior run is enqueued while the
+  // round is in flight (on all but sm_reserve_ SMs), then the join and the boundary ranges.
+  auto halo_and_elements = [&](double* arr, int nc, int kind, bool update) {
+    if (!overlap_) {
+      halo_exchange(arr, nc, kind);
+      element_kernel(update, fp, a, 0, E_, n_sm_);
+      return;
+    }
+    halo_exchange(arr, nc, kind, [&] { element_kernel(update, fp, a, int_lo_, int_hi_, n_sm_ - sm_reserve_); });
+    join_comm();
+    element_kernel(update, fp, a, 0, int_lo_, n_sm_);
+    element_kernel(update, fp, a, int_hi_, E_, n_sm_);
+  };
   if (lifting_) {
     mark(KC_MORTAR, true);
     launch_mortar_lift(n_, consts_.gas, mp, max_mortars_[0], stream_);
@@ -994,11 +1083,7 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
     launches_ += S_ > 0;
-    mark(KC_GRADIENT, true);
-    if (!(use_tma_ && launch_gradient_tma(n_, consts_, fp, a, n_sm_, stream_))) launch_gradient(n_, consts_, fp, a, stream_);
-    mark(KC_GRADIENT, false);
-    launches_++;
-    halo_exchange(fvn_.p, 4, MK_FVN_CONF);
+    halo_and_elements(trace_[cur_trace_].p, 5, MK_SOL_CONF, false);
     double* const g_src[2] = {g_mine_[0].p, g_mine_[1].p};
     mark(KC_MORTAR, true);
     launch_mortar_fill(n_, 12, slide_g_.p, g_src, fwd_ops_, mp, stream_);
@@ -1016,10 +1101,9 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   launch_mortar_backproject(n_, 5, f_src, slide_flux_.p, bwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
   launches_ += S_ > 0;
-  mark(KC_UPDATE, true);
-  if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm_, stream_))) launch_update(n_, consts_, fp, a, stream_);
-  mark(KC_UPDATE, false);
-  launches_++;
+  // Viscous: Fv.n of the remote faces; inviscid: the traces themselves.
+  if (lifting_) halo_and_elements(fvn_.p, 4, MK_FVN_CONF, true);
+  else halo_and_elements(trace_[cur_trace_].p, 5, MK_SOL_CONF, true);
   // The update wrote the new traces into the other buffer: neighbours processed
   // later in the same launch still read this stage's traces.
   if (mode == 0) cur_trace_ ^= 1;
@@ -1426,7 +1510,8 @@ static std::string plan_json(const sdg_mesh_spec& ms, int n_ranks, int rank, dou
   const Partition part = assign_ranks(mesh, n_ranks);
   const LocalTopology topo = build_topology(mesh, part, rank);
   std::ostringstream os;
-  os << "{\"rank\":" << rank << ",\"elements\":[";
+  const auto run = interior_run(topo);
+  os << "{\"rank\":" << rank << ",\"interior_run\":[" << run[0] << "," << run[1] << "],\"elements\":[";
   for (size_t i = 0; i < topo.gids.size(); ++i) os << (i ? "," : "") << topo.gids[i];
   os << "],\"halo\":[";
   const int ne = static_cast<int>(topo.gids.size());

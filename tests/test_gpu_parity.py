@@ -295,6 +295,34 @@ def test_rank_counts_do_not_change_the_bits(ranks, partition):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("bands,ranks,partition", [
+    ([(8, 1.0, 0.0)], 2, T.PARTITION_LEX),
+    ([(6, 1.0, 0.0), (6, 1.0, 0.3), (6, 1.0, 0.0)], 3, T.PARTITION_LEX),
+    ([(6, 1.0, 0.0), (6, 1.0, 0.3), (6, 1.0, 0.0)], 6, T.PARTITION_SFC),
+    ([(5, 1.0, 0.0), (7, 1.0, 0.3)], 4, T.PARTITION_LEX)])
+@pytest.mark.parametrize("mu", [0.0, 1e-3])
+def test_exchange_overlap_keeps_the_bits(bands, ranks, partition, mu):
+    """SURVEY §8(e) overlap: the interior element run is computed while the halo round is in
+    flight (comm stream), the boundary ranges after the join.  Ranks with a non-empty
+    interior run must still reproduce the single-rank bits, viscous and inviscid."""
+    from paper_2008_04356_b200 import capi
+    mesh = T.mesh_spec(bands, ny=4, nz=2, depth=1.0, partition=partition)
+    assert all(capi.plan(mesh, ranks, r)["interior_run"][1] > capi.plan(mesh, ranks, r)["interior_run"][0]
+               for r in range(ranks))
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=mu, case=T.density_wave())
+    n_el = sum(b[0] for b in bands) * 4 * 2
+
+    def body(s):
+        s.set_initial_condition(0.0)
+        s.step(0.004, 5)
+        return s.local_element_ids(), s.field()
+
+    ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub=f"ov1_{mu}"), n_el, 4)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"ov{ranks}_{partition}_{mu}"), n_el, 4)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
+
+
 def test_communication_audit_passes_and_catches_injected_collective():
     """audit_communication (audit.cpp:44-148) on the traces of a 3-rank run; the
     inject_collective hook (solver.cpp:961-964) must make it fail."""

@@ -128,3 +128,56 @@ def test_sfc_partition_reduces_the_halo():
     sfc, n_sfc = halo_faces(T.PARTITION_SFC)
     assert n_lex == n_sfc
     assert sfc <= lex
+
+
+def _neighbours(mesh, g):
+    """(band, ix, iy, iz) neighbours of global element g across its 6 sides, with the band
+    index of each (a band change means a sliding interface)."""
+    nb = [mesh.bands[b].nx for b in range(mesh.n_bands)]
+    off = [sum(nb[:b]) * mesh.ny * mesh.nz for b in range(mesh.n_bands)]
+    b = max(i for i in range(mesh.n_bands) if off[i] <= g)
+    r = g - off[b]
+    ix, iy, iz = r // (mesh.ny * mesh.nz), (r // mesh.nz) % mesh.ny, r % mesh.nz
+    out = []
+    for dx in (-1, 1):
+        jb, jx = b, ix + dx
+        if jx < 0:
+            jb = (b - 1) % mesh.n_bands
+            jx = nb[jb] - 1
+        elif jx >= nb[b]:
+            jb = (b + 1) % mesh.n_bands
+            jx = 0
+        out.append((jb, off[jb] + (jx * mesh.ny + iy) * mesh.nz + iz))
+    for dy in (-1, 1):
+        out.append((b, off[b] + (ix * mesh.ny + (iy + dy) % mesh.ny) * mesh.nz + iz))
+    for dz in (-1, 1):
+        out.append((b, off[b] + (ix * mesh.ny + iy) * mesh.nz + (iz + dz) % mesh.nz))
+    return b, out
+
+
+@pytest.mark.parametrize("partition", [T.PARTITION_LEX, T.PARTITION_SFC])
+@pytest.mark.parametrize("bands,ranks", [([(8, 1.0, 0.0)], 2), ([(6, 1.0, 0.0), (6, 1.0, 0.3), (6, 1.0, 0.0)], 3),
+                                         ([(6, 1.0, 0.0), (6, 1.0, 0.3), (6, 1.0, 0.0)], 6),
+                                         ([(5, 1.0, 0.0), (7, 1.0, 0.3)], 4)])
+def test_interior_run_has_only_local_conforming_neighbours(bands, ranks, partition):
+    """SURVEY §8(e) overlap: the element run whose kernels are launched while the halo
+    exchange is in flight must not touch remote or sliding faces, and must be maximal
+    among the runs of local-only elements."""
+    mesh = T.mesh_spec(bands, ny=4, nz=2, partition=partition)
+    plans = [capi.plan(mesh, ranks, r) for r in range(ranks)]
+    owner = {g: r for r, p in enumerate(plans) for g in p["elements"]}
+    for r, p in enumerate(plans):
+        els = p["elements"]
+        local_only = []
+        for g in els:
+            b, nbs = _neighbours(mesh, g)
+            local_only.append(all(jb == b and owner[jg] == r for jb, jg in nbs))
+        lo, hi = p["interior_run"]
+        assert all(local_only[lo:hi])
+        best, run = 0, 0
+        for f in local_only:
+            run = run + 1 if f else 0
+            best = max(best, run)
+        assert hi - lo == best
+    if bands == [(8, 1.0, 0.0)] and partition == T.PARTITION_LEX:
+        assert [p["interior_run"] for p in plans] == [[8, 24], [8, 24]]
