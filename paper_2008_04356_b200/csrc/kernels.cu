@@ -1647,8 +1647,8 @@ __global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tm
 
 // v2 layout.  Stage (double-buffered, TMA): U, the element's own face traces (written by the
 // previous stage's phase 6 / k_prolong, so phase 1 needs no prolongation), own Fv.n and the
-// per-side neighbour trace + Fv.n (or mortar flux + lift*).  The RK register is not staged:
-// it is prefetched into L2 with the tile and read / written by the owning thread in phase 5.
+// per-side neighbour trace + Fv.n (or mortar flux + lift*).  The RK register is prefetched into
+// L2 with the tile and copied (cp.async) over the consumed own-trace region after phase 1.
 template <int N1>
 struct TmaV2 {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
@@ -1846,6 +1846,16 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       }
     }
     __syncthreads();
+    // The own traces and own Fv.n are consumed: that stage region now receives the tile's RK
+    // register (coalesced 16-byte cp.async, L2-prefetched with the tile loads); it is read and
+    // rewritten in place in phase 5 and bulk-stored with U.
+    double* sRg = st + EPB * D::EL;  // EPB x EL <= EPB x (6 TS + 6 FS) for N1 <= 10
+    if (want_reg) {
+      const int n = min(EPB, P.E - e0);
+      const double* src = P.reg + static_cast<size_t>(e0) * D::EL;
+      for (int q = threadIdx.x; q < n * D::EL / 2; q += blockDim.x) cp_async16(sRg + 2 * q, src + 2 * q);
+      cp_async_commit();
+    }
 
     // Phase 2: viscous stress at the node (gradient recomputed from q and lift*); only tau and
     // the heat flux (9 values) cross the barrier that frees q / lift* for the flux staging.
@@ -1933,6 +1943,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
         flux_dir(u, vv, p, 2, Fz);
       }
     }
+    if (want_reg) cp_async_wait_all();  // this thread's register chunks; the barrier publishes them
     __syncthreads();
     if (active) {
       divergence(q, 0);
@@ -1971,15 +1982,15 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       } else {
         double w[5];
         double u[5];
-        double* gR = P.reg + (static_cast<size_t>(e) * N3 + t) * 5;
+        double* rgp = sRg + le * D::EL + t * 5;
 #pragma unroll
         for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
           double rg = A.dt * du[v];
-          if (want_reg) rg = __fma_rn(A.rk_a, gR[v], rg);
+          if (want_reg) rg = __fma_rn(A.rk_a, rgp[v], rg);
           w[v] = u[v] + A.rk_b * rg;
-          gR[v] = rg;
+          rgp[v] = rg;
           sU[t * 5 + v] = w[v];
         }
         const double p = pressure(w, rcp_nr(w[0]), C.gas);
@@ -2009,6 +2020,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     if (threadIdx.x == 0) {
       const int n = min(EPB, P.E - e0);
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
+      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, sRg, n * D::EL * 8u);
       bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
       bulk_commit();
     }
