@@ -2740,6 +2740,198 @@ __global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(con
   if (threadIdx.x == 0) bulk_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised k_gradient (SDG_GRAD_V=6): the same phases as k_gradient5 on
+// the consumer warps (EPB*N3 threads rounded up to whole warps, synchronised by
+// named barrier 1), plus one producer warp that owns every asynchronous copy:
+// side-code prefetch, the TMA stage loads (full[s] barriers), and the bulk
+// store of the tile's Fv.n once the consumers have released the tile
+// (empty[s]), followed by the wFv-free signal the next tile's phase 3 waits on.
+// No consumer thread ever waits on a copy it did not need.
+template <int N1>
+struct GWs {
+  static constexpr int CONSUMERS = (T5<N1>::THREADS + 31) / 32 * 32;
+  static constexpr int THREADS = CONSUMERS + 32;
+};
+
+__device__ __forceinline__ void consumer_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int N1>
+__global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(const __grid_constant__ ElemConsts C,
+                                                                              FieldPtrs P, StageArgs A) {
+  using D = T5<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, NC = GWs<N1>::CONSUMERS;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* stage0 = smem + D::TAB;
+  double* wQ = stage0 + 2 * D::G_STAGE;  // EPB x 4 N3
+  double* wG = wQ + EPB * 4 * N3;        // EPB x 12 N3
+  double* wFv = wG + EPB * 12 * N3;      // EPB x 6 FS
+  uint64_t* full = reinterpret_cast<uint64_t*>(wFv + EPB * 6 * D::FS);
+  uint64_t* empty = full + 2;
+  uint64_t* fv_free = full + 4;
+  __shared__ __align__(16) int codes[3][8 * EPB];
+  __shared__ int lstr[EPB][6];
+  load_tables<N1>(C, tab);
+  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    mbar_init(fv_free, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= NC) {
+    // ---------------- producer warp (one elected lane)
+    if (threadIdx.x != NC) return;
+    int tile = blockIdx.x;
+    if (tile < tiles) {
+      prefetch_codes<N1>(P, tile, codes[0]);
+      cp_async_wait_all();
+      issue_gradient_loads5<N1>(P, tile, codes[0], stage0, &full[0]);
+      if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
+    }
+    for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+      const int next = tile + gridDim.x;
+      if (next < tiles) {
+        cp_async_wait_all();  // codes of `next`
+        fence_proxy_async();
+        issue_gradient_loads5<N1>(P, next, codes[(it + 1) % 3], stage0 + ((it + 1) & 1) * D::G_STAGE,
+                                  &full[(it + 1) & 1]);
+        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
+      }
+      mbar_wait(&empty[it & 1], (it >> 1) & 1);  // tile consumed, its Fv.n assembled in wFv
+      const int e0 = P.e_first + tile * EPB;
+      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, min(EPB, P.E - e0) * 6u * D::FS * 8u);
+      bulk_commit();
+      bulk_wait_read0();
+      mbar_arrive(fv_free);
+    }
+    bulk_wait0();
+    return;
+  }
+  // ---------------- consumer warps
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
+  int tile = blockIdx.x;
+  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+    const int sidx = it & 1;
+    double* st = stage0 + sidx * D::G_STAGE;
+    const int e0 = P.e_first + tile * EPB;
+    const int n_el = min(EPB, P.E - e0);
+    const int e = e0 + le;
+    const bool active = le < n_el;
+    mbar_wait(&full[sidx], (it >> 1) & 1);
+    const int* myc = codes[it % 3] + 8 * le;
+    double* sU = st + le * D::EL;
+    double* sTr = st + EPB * D::EL + le * 6 * D::TS;
+    double* sNb = st + EPB * (D::EL + 6 * D::TS) + le * 6 * D::TS;
+    double* q = wQ + le * 4 * N3;
+    double* gS = wG + le * 12 * N3;
+    double* fvo = wFv + le * 6 * D::FS;
+    const BandD& B = C.bands[active ? myc[6] : 0];
+    // Phase 1: q; lift* in place over the neighbour slot (stride 5), sliding lift* stays at stride 4.
+    if (active) {
+      double u[5], qq[4];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+      prim4(u, C.gas, qq);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm - s * N2;
+        const int typ = myc[s] >> kCodeShift;
+        double* nb = sNb + s * D::TS;
+        if (typ == kSliding) {
+          if (f == 0) lstr[le][s] = 4;
+          continue;
+        }
+        double lift[4];
+        const double* own = sTr + s * D::TS + f * 5;
+        if (typ == kConforming) {
+          double ow[5], other[5], qa[4], qb[4];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            ow[v] = own[v];
+            other[v] = nb[f * 5 + v];
+          }
+          prim4(ow, C.gas, qa);
+          prim4(other, C.gas, qb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+        } else {
+          const int a = f / N1, b = f - (f / N1) * N1;
+          double x[3], ext[5];
+          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+          prim4(ext, C.gas, lift);
+        }
+        if (f == 0) lstr[le][s] = 5;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) nb[f * 5 + c] = lift[c];
+      }
+    }
+    consumer_sync(NC);
+    if (active) gradient_lines<N1>(C, B, q, sNb, D::TS, lstr[le], 1, gS, t, N3);
+    if (it > 0) mbar_wait(fv_free, (it - 1) & 1);  // the previous tile's Fv.n store has read wFv
+    consumer_sync(NC);
+    if (active && P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
+    }
+    // Phase 3: Fv.n on conforming sides; full gradient traces on sliding / Dirichlet sides.
+    if (active) {
+      for (int itm = t; itm < 6 * N2; itm += N3) {
+        const int s = itm / N2, f = itm - s * N2, a = f / N1, b = f - a * N1, dir = s >> 1;
+        const double* ell = tab + N1 * N1 + (s & 1) * N1;
+        const int code = myc[s];
+        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
+        if (typ == kConforming) {
+          double fv[4];
+          const double* own = sTr + s * D::TS + f * 5;
+          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, own, fv);
+          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, own, fv);
+          else fvn_item<N1, 2>(C, gS, ell, a, b, own, fv);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
+        } else {
+          double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+          for (int c = 0; c < 12; ++c) dst[c] = prolong1<N1>(gS + c * N3, ell, dir, a, b);
+        }
+      }
+    }
+    fence_proxy_async();
+    consumer_sync(NC);
+    if (threadIdx.x == 0) mbar_arrive(&empty[sidx]);
+  }
+}
+
+template <int N1>
+bool gws_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = T5<N1>;
+    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    auto kern = k_gradient_ws<N1>;
+    static int occ = -1;
+    if (occ < 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GWs<N1>::THREADS, D::G_SMEM);
+      if (occ < 1) occ = 1;
+    }
+    kern<<<std::min(tiles, n_sm * occ), GWs<N1>::THREADS, D::G_SMEM, st>>>(c, p, a);
+    check_launch("k_gradient_ws");
+    return true;
+  }
+}
+
 template <int N1>
 bool v5_t(bool update, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
   if constexpr (N1 % 2 != 0) {
@@ -2915,7 +3107,11 @@ bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const 
                          cudaStream_t st) {
   if (p.E <= p.e_first) return true;
   bool ok = false;
-  static const int gv = env_int("SDG_GRAD_V", 5);
+  static const int gv = env_int("SDG_GRAD_V", 6);
+  if (gv == 6) {
+    SDG_DISPATCH(n1, (ok = gws_t<NN>(c, p, a, n_sm, st)));
+    return ok;
+  }
   if (gv == 5) {
     SDG_DISPATCH(n1, (ok = v5_t<NN>(false, c, p, a, n_sm, st)));
     return ok;
