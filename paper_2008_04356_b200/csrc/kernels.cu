@@ -1251,6 +1251,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+__device__ __forceinline__ void consumer_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 constexpr int kCodeShift = 29;
 
 template <int N1>
@@ -1704,8 +1709,18 @@ __device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int ti
   if (want_reg) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u);
 }
 
-template <int N1, bool VISC, bool PACK>
-__global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_tma_v2(const __grid_constant__ ElemConsts C, FieldPtrs P,
+// WS = true: warp-specialised (as k_gradient_ws): the consumer warps run the phases and sync on
+// named barrier 1; one producer warp issues the stage loads (full[s] = bars[s]), waits for the
+// consumers to release a tile (empty[s] = bars[2 + s]), bulk-stores U, the register and the
+// new traces, and signals (bars[4]) once the trace buffer, which phase 3 reuses, has been read.
+template <int N1>
+struct UWs {
+  static constexpr int CONSUMERS = (TmaV2<N1>::THREADS + 31) / 32 * 32;
+  static constexpr int THREADS = CONSUMERS + 32;
+};
+
+template <int N1, bool VISC, bool PACK, bool WS>
+__global__ void __launch_bounds__(WS ? UWs<N1>::THREADS : TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_tma_v2(const __grid_constant__ ElemConsts C, FieldPtrs P,
                                                                  StageArgs A) {
   using D = TmaV2<N1>;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
@@ -1719,33 +1734,65 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
   const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
   const int le = threadIdx.x / N3, t = threadIdx.x % N3;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  constexpr int NC = UWs<N1>::CONSUMERS;
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int q = 0; q < (WS ? 5 : 2); ++q) mbar_init(&bars[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
+  auto csync = [&] {
+    if (WS) consumer_sync(NC);
+    else __syncthreads();
+  };
   // The RK register is read only when the stage's a-coefficient is non-zero (LSRK stage 1 has
   // a = 0: the register is overwritten without being read).
   const bool want_reg = A.mode == 0 && A.rk_a != 0.0;
+  constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
+  double* wF = work;
+  double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
+  double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
   int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < tiles) {
+  if (threadIdx.x == (WS ? NC : 0) && tile < tiles) {
     prefetch_codes<N1>(P, tile, codes[0]);
     cp_async_wait_all();
     issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0], want_reg);
     if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
   }
-  __syncthreads();  // codes[0] visible to every thread
-  constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
-  double* wF = work;
-  double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
-  double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
+  if (WS && threadIdx.x >= NC) {
+    // ---------------- producer warp (one elected lane)
+    if (threadIdx.x != NC) return;
+    for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
+      const int next = tile + gridDim.x;
+      if (next < tiles) {
+        cp_async_wait_all();  // codes of `next`
+        fence_proxy_async();
+        issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + ((it + 1) & 1) * D::U_STAGE,
+                                        &bars[(it + 1) & 1], want_reg);
+        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
+      }
+      mbar_wait(&bars[2 + (it & 1)], (it >> 1) & 1);  // tile released: outputs assembled in shared memory
+      if (A.mode == 0) {
+        const int e0 = P.e_first + tile * EPB;
+        const int n = min(EPB, P.E - e0);
+        double* st = stage0 + (it & 1) * D::U_STAGE;
+        bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
+        bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
+        bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
+        bulk_commit();
+        bulk_wait_read0();  // stage (it & 1) and the trace buffer are free again
+      }
+      mbar_arrive(&bars[4]);
+    }
+    bulk_wait0();
+    return;
+  }
+  if (!WS) __syncthreads();  // codes[0] visible to every thread
   for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
     const int sidx = it & 1;
     double* st = stage0 + sidx * D::U_STAGE;
     const int next = tile + gridDim.x;
-    if (threadIdx.x == 0) bulk_wait_read0();  // stores of the previous tile have read stage sidx^1 and wTr
-    if (threadIdx.x == 0 && next < tiles) {
+    if (!WS && threadIdx.x == 0) bulk_wait_read0();  // stores of the previous tile have read stage sidx^1 and wTr
+    if (!WS && threadIdx.x == 0 && next < tiles) {
       cp_async_wait_all();  // codes of `next`
       fence_proxy_async();
       issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::U_STAGE,
@@ -1754,16 +1801,18 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     }
     const int e0 = P.e_first + tile * EPB;
     const int e = e0 + le;
-    const bool active = e < P.E;
+    const bool active = le < EPB && e < P.E;  // WS: padding lanes of the last consumer warp idle
     double* sU = st + le * D::EL;
     const double* sOwn = st + EPB * D::EL + le * 6 * D::TS;
     double* sFv = st + EPB * (D::EL + 6 * D::TS) + le * 6 * D::FS;
     double* sNb = st + EPB * (D::EL + 6 * D::TS + 6 * D::FS) + le * 6 * D::NB;
     double* q = wF + le * WF;
     double* lf = wLift + le * 24 * N2;
+    // WS: the full barrier also publishes the tile's side codes, so wait before reading them.
+    if (WS) mbar_wait(&bars[sidx], (it >> 1) & 1);
     const int* myc = codes[it % 3] + 8 * le;
     const BandD& B = C.bands[active ? myc[6] : 0];
-    mbar_wait(&bars[sidx], (it >> 1) & 1);
+    if (!WS) mbar_wait(&bars[sidx], (it >> 1) & 1);
 
     // Phase 1: face fluxes (in place over the neighbour data) and lift*.
     if (active) {
@@ -1845,7 +1894,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
         }
       }
     }
-    __syncthreads();
+    csync();
     // The own traces and own Fv.n are consumed: that stage region now receives the tile's RK
     // register (coalesced 16-byte cp.async, L2-prefetched with the tile loads); it is read and
     // rewritten in place in phase 5 and bulk-stored with U.
@@ -1853,7 +1902,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
     if (want_reg) {
       const int n = min(EPB, P.E - e0);
       const double* src = P.reg + static_cast<size_t>(e0) * D::EL;
-      for (int q = threadIdx.x; q < n * D::EL / 2; q += blockDim.x) cp_async16(sRg + 2 * q, src + 2 * q);
+      for (int q = threadIdx.x; q < n * D::EL / 2; q += (WS ? NC : D::THREADS)) cp_async16(sRg + 2 * q, src + 2 * q);
       cp_async_commit();
     }
 
@@ -1875,7 +1924,8 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
 #pragma unroll
       for (int d = 0; d < 3; ++d) hq[d] = C.gas.kcond * g[9 + d];
     }
-    __syncthreads();  // q and lift* reads done
+    csync();  // q and lift* reads done
+    if (WS && it > 0) mbar_wait(&bars[4], (it - 1) & 1);  // previous tile's trace store has read wTr
 
     // Phase 3: volume flux and weak divergence through shared memory.  F_x is staged over q,
     // F_y over the dead lift* / trace scratch, then F_z over q: only F_z (5 values) stays in
@@ -1944,16 +1994,16 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       }
     }
     if (want_reg) cp_async_wait_all();  // this thread's register chunks; the barrier publishes them
-    __syncthreads();
+    csync();
     if (active) {
       divergence(q, 0);
       divergence(qy, 1);
       if (F3) divergence(qz, 2);
     }
     if (!F3) {
-      __syncthreads();
+      csync();
       if (active) stage_flux(q, Fz, B.sj[2]);
-      __syncthreads();
+      csync();
       if (active) divergence(q, 2);
     }
 
@@ -2001,10 +2051,12 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       }
     }
     if (A.mode == 1) {
-      __syncthreads();
+      fence_proxy_async();
+      csync();
+      if (WS && threadIdx.x == 0) mbar_arrive(&bars[2 + sidx]);
       continue;
     }
-    __syncthreads();
+    csync();
     // Phase 6: traces of the new state, then bulk stores of U, reg and traces.
     if (active) {
       double* tr = wTr + le * 6 * D::TS;
@@ -2016,8 +2068,10 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       }
     }
     fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    csync();
+    if (WS) {
+      if (threadIdx.x == 0) mbar_arrive(&bars[2 + sidx]);
+    } else if (threadIdx.x == 0) {
       const int n = min(EPB, P.E - e0);
       bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
       bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, sRg, n * D::EL * 8u);
@@ -2025,7 +2079,7 @@ __global__ void __launch_bounds__(TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_
       bulk_commit();
     }
   }
-  if (threadIdx.x == 0) bulk_wait0();
+  if (!WS && threadIdx.x == 0) bulk_wait0();
 }
 
 // Gradient-kernel loads of one tile: U and, per side, the neighbour trace
@@ -2754,10 +2808,6 @@ struct GWs {
   static constexpr int THREADS = CONSUMERS + 32;
 };
 
-__device__ __forceinline__ void consumer_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 template <int N1>
 __global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(const __grid_constant__ ElemConsts C,
@@ -2968,21 +3018,25 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
       variant = env ? std::atoi(env) : 6;
     }
     const bool v3 = variant == 3 || variant == 4;
-    const bool pack = variant == 6;
-    auto kern = variant == 3 ? (c.gas.viscous ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
-              : variant == 4 ? (c.gas.viscous ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
-              : pack ? (c.gas.viscous ? k_update_tma_v2<N1, true, true> : k_update_tma_v2<N1, false, true>)
-                     : (c.gas.viscous ? k_update_tma_v2<N1, true, false> : k_update_tma_v2<N1, false, false>);
+    const bool ws = variant == 8;
+    const bool pack = variant == 6 || ws;
+    const bool vis = c.gas.viscous != 0;
+    auto kern = variant == 3 ? (vis ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
+              : variant == 4 ? (vis ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
+              : ws ? (vis ? k_update_tma_v2<N1, true, true, true> : k_update_tma_v2<N1, false, true, true>)
+              : pack ? (vis ? k_update_tma_v2<N1, true, true, false> : k_update_tma_v2<N1, false, true, false>)
+                     : (vis ? k_update_tma_v2<N1, true, false, false> : k_update_tma_v2<N1, false, false, false>);
     const int smem = v3 ? D::U_SMEM : (pack ? TmaV2<N1>::U_SMEM_PACK : TmaV2<N1>::U_SMEM);
-    static int occ_tab[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
-    int& occ = occ_tab[(variant == 3 ? 2 : variant == 4 ? 4 : pack ? 6 : 0) + (c.gas.viscous ? 1 : 0)];
+    const int threads = ws ? UWs<N1>::THREADS : D::THREADS;
+    static int occ_tab[10] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    int& occ = occ_tab[(variant == 3 ? 2 : variant == 4 ? 4 : ws ? 8 : pack ? 6 : 0) + (vis ? 1 : 0)];
     if (occ < 0) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
       if (occ < 1) occ = 1;
     }
     const int grid = std::min(tiles, n_sm * occ);
-    kern<<<grid, D::THREADS, smem, st>>>(c, p, a);
+    kern<<<grid, threads, smem, st>>>(c, p, a);
     check_launch("k_update_tma");
     return true;
   }
