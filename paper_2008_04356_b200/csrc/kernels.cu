@@ -1341,6 +1341,31 @@ __device__ __forceinline__ double prolong_aos(const double* __restrict__ s, int 
   return acc;
 }
 
+// Face trace (all 5 variables) of one face node from an AoS [node][5] element block.  z-lines
+// are 5*N1 doubles apart, so a warp's loads of one line position would pile onto half the
+// banks; every other group of 8 face nodes starts the contraction one node later, which
+// spreads them over all banks (the summation order is fixed per face node).
+template <int N1>
+__device__ __forceinline__ void face_trace_aos(const double* __restrict__ s, const double* __restrict__ ell, int dir,
+                                               int a, int b, double* __restrict__ out) {
+  constexpr int N2 = N1 * N1;
+  const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
+  const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
+  const int rot = dir == 2 ? (((a * N1 + b) >> 3) & 1) : 0;
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    int mm = m + rot;
+    if (mm == N1) mm = 0;
+    const double c = ell[mm];
+    const double* p = s + (base + mm * stride) * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) acc[v] = __fma_rn(c, p[v], acc[v]);
+  }
+#pragma unroll
+  for (int v = 0; v < 5; ++v) out[v] = acc[v];
+}
+
 // BR1 gradient by line tasks: task (d, c, line) loads q along the line once and
 // produces g[3c+d] on all N1 nodes of that line; D-hat, l(+-1) and 1/w enter as
 // compile-time-indexed kernel-parameter (constant bank) operands
@@ -1858,8 +1883,13 @@ __global__ void __launch_bounds__(WS ? UWs<N1>::THREADS : TmaV2<N1>::THREADS, Tm
             ok = roe_flux(um, up, dir, vg, C.gas, flux);
             // Fv.n of both sides read only now (not live through the Roe solve); the sum is
             // symmetric, so both elements of the face still produce identical bits.
-#pragma unroll
-            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (sFv[s * D::FS + f * 4 + c] + nb[D::TS + f * 4 + c]);
+            const double2* fa = reinterpret_cast<const double2*>(sFv + s * D::FS + f * 4);
+            const double2* fb = reinterpret_cast<const double2*>(nb + D::TS + f * 4);
+            const double2 a01 = fa[0], a23 = fa[1], b01 = fb[0], b23 = fb[1];
+            flux[1] -= 0.5 * (a01.x + b01.x);
+            flux[2] -= 0.5 * (a01.y + b01.y);
+            flux[3] -= 0.5 * (a23.x + b23.x);
+            flux[4] -= 0.5 * (a23.y + b23.y);
           } else {
             ok = roe_flux(um, up, dir, vg, C.gas, flux);
           }
@@ -1966,7 +1996,7 @@ __global__ void __launch_bounds__(WS ? UWs<N1>::THREADS : TmaV2<N1>::THREADS, Tm
           acc[1] += c * f01.y;
           acc[2] += c * f23.x;
           acc[3] += c * f23.y;
-          acc[4] += c * fp[4];
+          acc[4] += c * reinterpret_cast<const double2*>(fp + 4)->x;  // 16-byte load: conflict-free at pitch 6
         } else {
 #pragma unroll
           for (int v = 0; v < 5; ++v) acc[v] += c * buf[v * N3 + base + m * stride];
@@ -2063,8 +2093,7 @@ __global__ void __launch_bounds__(WS ? UWs<N1>::THREADS : TmaV2<N1>::THREADS, Tm
       for (int itm = t; itm < 6 * N2; itm += N3) {
         const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
         const double* ell = tab + N1 * N1 + (s & 1) * N1;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+        face_trace_aos<N1>(sU, ell, s >> 1, a, b, tr + s * D::TS + f * 5);
       }
     }
     fence_proxy_async();
