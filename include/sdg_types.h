@@ -71,7 +71,25 @@ typedef struct {
    * lexicographic blocks (proj/src/partition.cpp:48-81), 1 = Morton
    * space-filling curve. */
   int partition;
+  /* Geometry of the elements: SDG_MAP_BOX (affine hexahedra, the reference's
+   * ElementMetrics, proj/src/mesh.cpp:102-111) or SDG_MAP_WARP (curved
+   * hexahedra: the box mapped by a smooth sinusoidal warp inside every band,
+   * see below), with `warp` the amplitude as a fraction of the element size. */
+  int mapping;
+  double warp;
 } sdg_mesh_spec;
+
+/* SDG_MAP_WARP: a box point (x, y, z) of band b maps to
+ *   X = x + A*hx*sp(tx)*s2(ty)*s2(tz),  Y = y + A*hy*sp(tx)*s2(tz),  Z = z + A*hz*sp(tx)*s2(ty)
+ * with tx = (ix + (xi+1)/2)/nx_b, ty = (iy + (eta+1)/2)/ny, tz = (iz + (zeta+1)/2)/nz,
+ * sp(t) = sin(pi t), s2(t) = sin(2 pi t) (both exactly 0 at integer multiples of
+ * their half period), A = warp.  The warp vanishes on every band boundary, so
+ * sliding interfaces stay planar and unwarped (BASELINE configs[3]: "interface
+ * faces left unwarped"), and it is periodic in y and z.  A moving band carries
+ * its warp rigidly (+vg t along y), so the metric terms are time-invariant.
+ * Metrics are the conservative curl form (Kopriva 2006) of the degree-N LGL
+ * interpolant of the mapping, evaluated at the solution nodes. */
+enum { SDG_MAP_BOX = 0, SDG_MAP_WARP = 1 };
 
 typedef struct {
   double gamma, R, mu, Pr;

@@ -217,6 +217,15 @@ class Oracle3D:
         self._check(self.lib.orc_integrate_mass_energy(self.h, _d(u), _d(out)))
         return out
 
+    def metrics(self):
+        """(met [E, N3, 10], fmet [E, 6, N2, 4]) of a curved (SDG_MAP_WARP) mesh."""
+        n1 = self.n1
+        met = np.zeros((self.n_elements, n1 ** 3, 10))
+        fmet = np.zeros((self.n_elements, 6, n1 * n1, 4))
+        self.lib.orc_get_metrics.argtypes = [C.c_void_p, _dp, _dp]
+        self._check(self.lib.orc_get_metrics(self.h, _d(met), _d(fmet)))
+        return met, fmet
+
     def sample_case(self, t):
         out = np.zeros(self.size)
         self._check(self.lib.orc_sample_case(self.h, t, _d(out)))

@@ -539,6 +539,100 @@ static void face_flux(const double* um, const double* up, int dir, double vg_n, 
 }
 
 // ---------------------------------------------------------------------------
+// Curved hexahedra (SDG_MAP_WARP, include/sdg_types.h).  The reference has
+// affine elements only (ElementMetrics, mesh.cpp:102-111); these are the
+// rotation-invariant forms of its flux functions for a general unit normal n,
+// which reduce to roe_flux / face_flux above for n = e_dir.
+// ---------------------------------------------------------------------------
+
+// sin(pi t), exactly 0 at integer t.
+static double sinpi_exact(double t) {
+  double r = std::fmod(t, 2.0);
+  if (r < 0.0) r += 2.0;
+  if (r == 0.0 || r == 1.0) return 0.0;
+  return std::sin(3.14159265358979323846 * r);
+}
+
+static long double sinpi_ld(long double t) {
+  long double r = std::fmod(t, 2.0L);
+  if (r < 0.0L) r += 2.0L;
+  if (r == 0.0L || r == 1.0L) return 0.0L;
+  return std::sin(3.14159265358979323846264338327950288L * r);
+}
+
+static inline void normal_flux_n(const double* u, const double* n, double vg_n, const Gas& g, double* f) {
+  const double rho = u[0];
+  const double v[3] = {u[1] / rho, u[2] / rho, u[3] / rho};
+  const double p = pressure(u, g);
+  const double vn = v[0] * n[0] + v[1] * n[1] + v[2] * n[2];
+  f[0] = rho * vn - vg_n * u[0];
+  for (int d = 0; d < 3; ++d) f[1 + d] = u[1 + d] * vn + p * n[d] - vg_n * u[1 + d];
+  f[4] = (u[4] + p) * vn - vg_n * u[4];
+}
+
+// Roe flux along the unit normal n (flux.cpp:68-133 in vector form: the two
+// shear waves carry rho * (dv - dun n)).
+static void roe_flux_n(const double* ul, const double* ur, const double* n, double vg_n, const Gas& g, double* f) {
+  const double rho_l = ul[0], rho_r = ur[0];
+  const double vl[3] = {ul[1] / rho_l, ul[2] / rho_l, ul[3] / rho_l};
+  const double vr[3] = {ur[1] / rho_r, ur[2] / rho_r, ur[3] / rho_r};
+  const double p_l = pressure(ul, g), p_r = pressure(ur, g);
+  const double h_l = (ul[4] + p_l) / rho_l, h_r = (ur[4] + p_r) / rho_r;
+  const double c_l = std::sqrt(g.gamma * p_l / rho_l), c_r = std::sqrt(g.gamma * p_r / rho_r);
+  const double un_l = vl[0] * n[0] + vl[1] * n[1] + vl[2] * n[2];
+  const double un_r = vr[0] * n[0] + vr[1] * n[1] + vr[2] * n[2];
+
+  const double sl = std::sqrt(rho_l), sr = std::sqrt(rho_r);
+  const double inv = 1.0 / (sl + sr);
+  double v[3];
+  for (int d = 0; d < 3; ++d) v[d] = (sl * vl[d] + sr * vr[d]) * inv;
+  const double h = (sl * h_l + sr * h_r) * inv;
+  const double un = v[0] * n[0] + v[1] * n[1] + v[2] * n[2];
+  const double q2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+  const double c2 = (g.gamma - 1.0) * (h - 0.5 * q2);
+  if (!(c2 > 0.0)) throw InvalidStateError("roe_flux: nonpositive Roe enthalpy average");
+  const double c = std::sqrt(c2);
+  const double rho = sl * sr;
+
+  const double dp = p_r - p_l, dun = un_r - un_l, drho = rho_r - rho_l;
+  double dvt[3];
+  for (int d = 0; d < 3; ++d) dvt[d] = (vr[d] - vl[d]) - dun * n[d];
+  const double alpha1 = (dp - rho * c * dun) / (2.0 * c2);
+  const double alpha2 = drho - dp / c2;
+  const double alpha4 = (dp + rho * c * dun) / (2.0 * c2);
+  const double a1 = entropy_fixed_abs(un - c - vg_n, un_l - c_l - vg_n, un_r - c_r - vg_n);
+  const double a2 = std::abs(un - vg_n);
+  const double a4 = entropy_fixed_abs(un + c - vg_n, un_l + c_l - vg_n, un_r + c_r - vg_n);
+  const double w1 = a1 * alpha1, w2 = a2 * alpha2, w4 = a4 * alpha4;
+  const double d0 = w1 + w2 + w4;
+  double dm[3];
+  for (int d = 0; d < 3; ++d) dm[d] = d0 * v[d] + (w4 - w1) * c * n[d] + a2 * rho * dvt[d];
+  const double dE = w1 * (h - un * c) + w2 * 0.5 * q2 + w4 * (h + un * c) +
+                    a2 * rho * (v[0] * dvt[0] + v[1] * dvt[1] + v[2] * dvt[2]);
+  double fl[NV], fr[NV];
+  normal_flux_n(ul, n, vg_n, g, fl);
+  normal_flux_n(ur, n, vg_n, g, fr);
+  f[0] = 0.5 * (fl[0] + fr[0] - d0);
+  for (int d = 0; d < 3; ++d) f[1 + d] = 0.5 * (fl[1 + d] + fr[1 + d] - dm[d]);
+  f[4] = 0.5 * (fl[4] + fr[4] - dE);
+}
+
+// face_numerical_flux (solver.cpp:308-321) along n: Roe minus the BR1 central
+// viscous normal flux 0.5 (Fv- + Fv+) . n.
+static void face_flux_n(const double* um, const double* up, const double* n, double vg_n, const double* gm,
+                        const double* gp, const Gas& g, double* f) {
+  roe_flux_n(um, up, n, vg_n, g, f);
+  if (g.viscous() && gm != nullptr && gp != nullptr) {
+    double fm[3][NV], fp[3][NV];
+    viscous_flux(um, gm, g, fm);
+    viscous_flux(up, gp, g, fp);
+    for (int v = 0; v < NV; ++v)
+      f[v] -= 0.5 * ((fm[0][v] * n[0] + fm[1][v] * n[1] + fm[2][v] * n[2]) +
+                     (fp[0][v] * n[0] + fp[1][v] * n[1] + fp[2][v] * n[2]));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exact solutions / cases: proj/src/exact_solutions.cpp:7-35, cases.hpp:18-25.
 // ---------------------------------------------------------------------------
 static State eval_case(const sdg_case& cs, const double* x, double t, const Gas& g) {
@@ -662,6 +756,10 @@ struct orc_solver {
   bool lifting = false;
 
   std::vector<double> field, reg, dudt, grad, trace, fflux, gtrace, lift;
+  // Curved elements (SDG_MAP_WARP): per node Ja^d_c (9, [3*d + c]) and 1/J;
+  // per side face node the unit normal along +xi_dir and the surface Jacobian sJ.
+  bool curved = false;
+  std::vector<double> met, fmet;
   double time = 0.0;
   int step_index = 0, stage_index = 0;
   std::string err;
@@ -676,6 +774,8 @@ struct orc_solver {
   double* ff(int e, int side) { return fflux.data() + (static_cast<size_t>(e) * 6 + side) * n2 * NV; }
   double* gt(int e, int side) { return gtrace.data() + (static_cast<size_t>(e) * 6 + side) * n2 * NG; }
   double* lf(int e, int side) { return lift.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4; }
+  const double* mt(int e, int nd) const { return met.data() + (static_cast<size_t>(e) * n3 + nd) * 10; }
+  const double* fm(int e, int side) const { return fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4; }
 
   void physical(int e, double xi, double eta, double zeta, double t, double* x) const {
     const Elem& el = elems[e];
@@ -683,9 +783,37 @@ struct orc_solver {
     const double ox = b.x_lo + el.ix * b.hx;
     const double oy = spec.y0 + el.iy * b.hy;
     const double oz = spec.z0 + el.iz * b.hz;
-    x[0] = ox + 0.5 * (xi + 1.0) * b.hx;
-    x[1] = oy + 0.5 * (eta + 1.0) * b.hy + b.vg * t;
-    x[2] = oz + 0.5 * (zeta + 1.0) * b.hz;
+    if (!curved) {
+      x[0] = ox + 0.5 * (xi + 1.0) * b.hx;
+      x[1] = oy + 0.5 * (eta + 1.0) * b.hy + b.vg * t;
+      x[2] = oz + 0.5 * (zeta + 1.0) * b.hz;
+      return;
+    }
+    // SDG_MAP_WARP (include/sdg_types.h).
+    const double tx = (el.ix + 0.5 * (xi + 1.0)) / b.nx;
+    const double ty = (el.iy + 0.5 * (eta + 1.0)) / spec.ny;
+    const double tz = (el.iz + 0.5 * (zeta + 1.0)) / spec.nz;
+    const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
+    const double A = spec.warp;
+    x[0] = (ox + 0.5 * (xi + 1.0) * b.hx) + A * b.hx * sp * sy * sz;
+    x[1] = (oy + 0.5 * (eta + 1.0) * b.hy) + A * b.hy * sp * sz + b.vg * t;
+    x[2] = (oz + 0.5 * (zeta + 1.0) * b.hz) + A * b.hz * sp * sy;
+  }
+  // Mapped position minus the mapped element centre, long double (metrics only).
+  void relative_position(int e, double xi, double eta, double zeta, ld* x) const {
+    const Elem& el = elems[e];
+    const Band& b = bands[el.band];
+    const ld h[3] = {b.hx, b.hy, b.hz};
+    const ld r[3] = {0.5L * xi, 0.5L * eta, 0.5L * zeta};
+    const ld t[3] = {(el.ix + 0.5L * (xi + 1.0L)) / b.nx, (el.iy + 0.5L * (eta + 1.0L)) / spec.ny,
+                     (el.iz + 0.5L * (zeta + 1.0L)) / spec.nz};
+    const ld tc[3] = {(el.ix + 0.5L) / b.nx, (el.iy + 0.5L) / spec.ny, (el.iz + 0.5L) / spec.nz};
+    const ld A = spec.warp;
+    const ld sp = sinpi_ld(t[0]), sy = sinpi_ld(2.0L * t[1]), sz = sinpi_ld(2.0L * t[2]);
+    const ld cp = sinpi_ld(tc[0]), cy = sinpi_ld(2.0L * tc[1]), cz = sinpi_ld(2.0L * tc[2]);
+    x[0] = r[0] * h[0] + A * h[0] * (sp * sy * sz - cp * cy * cz);
+    x[1] = r[1] * h[1] + A * h[1] * (sp * sz - cp * cz);
+    x[2] = r[2] * h[2] + A * h[2] * (sp * sy - cp * cy);
   }
   void face_node_position(int e, int side, int p, int q, double t, double* x) const {
     const double a = ns.x[p], c = ns.x[q];
@@ -700,6 +828,7 @@ struct orc_solver {
   }
 
   void build(const sdg_mesh_spec& s, const sdg_solver_config& cfg);
+  void build_metrics();
   void update_interfaces(double t_stage);
   void rebuild_role(Role& role, const std::vector<int>& ids);
   void prolong(const double* u);
@@ -707,6 +836,8 @@ struct orc_solver {
   void exchange_solution();
   void run_lifting(double t_stage, const double* u);
   void assemble_gradients(const double* u);
+  void assemble_gradients_curved(const double* u);
+  void prolong_gradients(int e);
   void send_gradients();
   void interior_flux();
   void volume(const double* u, double* out);
@@ -887,6 +1018,152 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
   fflux.assign(static_cast<size_t>(ne) * 6 * n2 * NV, 0.0);
   gtrace.assign(static_cast<size_t>(ne) * 6 * n2 * NG, 0.0);
   lift.assign(static_cast<size_t>(ne) * 6 * n2 * 4, 0.0);
+  if (s.mapping != SDG_MAP_BOX && s.mapping != SDG_MAP_WARP) throw ConfigError("unknown mesh mapping");
+  curved = s.mapping == SDG_MAP_WARP;
+  if (curved) {
+    if (!std::isfinite(s.warp)) throw ConfigError("warp amplitude must be finite");
+    build_metrics();
+  }
+}
+
+// Metric terms of the curved mapping: conservative curl form (Kopriva 2006)
+//   Ja^i_n = -e_i . curl_xi( I^N( X_l grad_xi X_m ) ),  (n, m, l) cyclic,
+// on the degree-N LGL interpolant of the mapping, then interpolated to the
+// solution nodes; J = det(dX/dxi) of the interpolant.  Assembled in long
+// double on coordinates relative to the element centre and rounded once, so
+// the discrete metric identities hold to the rounding of the stored terms
+// (free-stream preservation).  Face metrics (unit
+// normal along +xi_d and sJ) come from the Ja^d of the LGL face layer, which
+// depends on the face's geometry only; the minus element's values are copied
+// to the plus element so that both see identical bits.
+void orc_solver::build_metrics() {
+  const Nodes lgl(ns.degree, SDG_NODES_LGL);
+  const Basis bl = make_basis(lgl);
+  std::vector<double> Ld(static_cast<size_t>(n) * n);  // L[s][p] = l_p(x_s), LGL -> solution nodes
+  for (int a = 0; a < n; ++a) lgl.lagrange_all(ns.x[a], Ld.data() + a * n);
+  const std::vector<ld> L(Ld.begin(), Ld.end());
+  const std::vector<ld> DL(bl.D.begin(), bl.D.end());
+  const int ne = static_cast<int>(elems.size());
+  met.assign(static_cast<size_t>(ne) * n3 * 10, 0.0);
+  fmet.assign(static_cast<size_t>(ne) * 6 * n2 * 4, 0.0);
+  auto idx = [&](int p, int q, int r) { return (p * n + q) * n + r; };
+  // d/dxi_d of a grid function on the LGL grid.
+  auto deriv = [&](const ld* f, int d, ld* out) {
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          ld acc = 0.0L;
+          for (int m = 0; m < n; ++m) {
+            const ld dm = DL[(d == 0 ? p : (d == 1 ? q : r)) * n + m];
+            acc += dm * f[d == 0 ? idx(m, q, r) : (d == 1 ? idx(p, m, r) : idx(p, q, m))];
+          }
+          out[idx(p, q, r)] = acc;
+        }
+  };
+  // LGL grid -> solution nodes, one direction at a time.
+  auto interp3 = [&](const ld* f, ld* out) {
+    std::vector<ld> t1(n3), t2(n3);
+    for (int a = 0; a < n; ++a)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          ld acc = 0.0L;
+          for (int p = 0; p < n; ++p) acc += L[a * n + p] * f[idx(p, q, r)];
+          t1[idx(a, q, r)] = acc;
+        }
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b)
+        for (int r = 0; r < n; ++r) {
+          ld acc = 0.0L;
+          for (int q = 0; q < n; ++q) acc += L[b * n + q] * t1[idx(a, q, r)];
+          t2[idx(a, b, r)] = acc;
+        }
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b)
+        for (int c = 0; c < n; ++c) {
+          ld acc = 0.0L;
+          for (int r = 0; r < n; ++r) acc += L[c * n + r] * t2[idx(a, b, r)];
+          out[idx(a, b, c)] = acc;
+        }
+  };
+  std::exception_ptr first;
+#pragma omp parallel for schedule(static)
+  for (int e = 0; e < ne; ++e) try {
+    std::vector<ld> X(3 * n3), dX(9 * n3), V(3 * n3), dV(n3), JaL(9 * n3, 0.0L), Ja(9 * n3), dXs(9 * n3);
+    // Coordinates relative to the element centre, in long double (the curl
+    // form is translation invariant; the two elements of a face then see the
+    // same face geometry up to an exact translation).
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          ld x[3];
+          relative_position(e, lgl.x[p], lgl.x[q], lgl.x[r], x);
+          for (int c = 0; c < 3; ++c) X[c * n3 + idx(p, q, r)] = x[c];
+        }
+    for (int d = 0; d < 3; ++d)
+      for (int c = 0; c < 3; ++c) deriv(X.data() + c * n3, d, dX.data() + (3 * d + c) * n3);
+    for (int nn = 0; nn < 3; ++nn) {
+      const int m = (nn + 1) % 3, l = (nn + 2) % 3;
+      for (int d = 0; d < 3; ++d)
+        for (int g = 0; g < n3; ++g) V[d * n3 + g] = X[l * n3 + g] * dX[(3 * d + m) * n3 + g];
+      // Ja^i_nn = -(curl V)_i, (curl V)_i = d_{i+1} V_{i+2} - d_{i+2} V_{i+1}.
+      for (int i = 0; i < 3; ++i) {
+        const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+        ld* out = JaL.data() + (3 * i + nn) * n3;
+        deriv(V.data() + i2 * n3, i1, dV.data());
+        for (int g = 0; g < n3; ++g) out[g] = -dV[g];
+        deriv(V.data() + i1 * n3, i2, dV.data());
+        for (int g = 0; g < n3; ++g) out[g] += dV[g];
+      }
+    }
+    for (int c = 0; c < 9; ++c) {
+      interp3(JaL.data() + c * n3, Ja.data() + c * n3);
+      interp3(dX.data() + c * n3, dXs.data() + c * n3);
+    }
+    for (int g = 0; g < n3; ++g) {
+      double* o = met.data() + (static_cast<size_t>(e) * n3 + g) * 10;
+      for (int c = 0; c < 9; ++c) o[c] = static_cast<double>(Ja[c * n3 + g]);
+      // dXs[(3 d + c)] = dX_c / dxi_d; J = det.
+      const ld a00 = dXs[0 * n3 + g], a01 = dXs[1 * n3 + g], a02 = dXs[2 * n3 + g];
+      const ld a10 = dXs[3 * n3 + g], a11 = dXs[4 * n3 + g], a12 = dXs[5 * n3 + g];
+      const ld a20 = dXs[6 * n3 + g], a21 = dXs[7 * n3 + g], a22 = dXs[8 * n3 + g];
+      const ld jac = a00 * (a11 * a22 - a12 * a21) - a01 * (a10 * a22 - a12 * a20) + a02 * (a10 * a21 - a11 * a20);
+      if (!(jac > 0.0)) throw ConfigError("curved mapping has a non-positive Jacobian (warp too large)");
+      o[9] = static_cast<double>(1.0L / jac);
+    }
+    for (int side = 0; side < 6; ++side) {
+      const int d = side / 2, layer = (side & 1) ? n - 1 : 0;
+      double* o = fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4;
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+          ld ns3[3];
+          for (int c = 0; c < 3; ++c) {
+            const ld* f = JaL.data() + (3 * d + c) * n3;
+            ld acc = 0.0L;
+            for (int u = 0; u < n; ++u) {
+              ld inner = 0.0L;
+              for (int v = 0; v < n; ++v) {
+                const int g = d == 0 ? idx(layer, u, v) : (d == 1 ? idx(u, layer, v) : idx(u, v, layer));
+                inner += L[b * n + v] * f[g];
+              }
+              acc += L[a * n + u] * inner;
+            }
+            ns3[c] = acc;
+          }
+          const ld sj = std::sqrt(ns3[0] * ns3[0] + ns3[1] * ns3[1] + ns3[2] * ns3[2]);
+          double* q = o + (a * n + b) * 4;
+          for (int c = 0; c < 3; ++c) q[c] = static_cast<double>(ns3[c] / sj);
+          q[3] = static_cast<double>(sj);
+        }
+    }
+  } catch (...) {
+#pragma omp critical
+    if (!first) first = std::current_exception();
+  }
+  if (first) std::rethrow_exception(first);
+  for (const auto& f : interior) {
+    const double* src = fm(f.em, 2 * f.dir + 1);
+    std::copy(src, src + n2 * 4, fmet.data() + (static_cast<size_t>(f.ep) * 6 + 2 * f.dir) * n2 * 4);
+  }
 }
 
 // update_interfaces (solver.cpp:156-176).
@@ -1093,6 +1370,10 @@ void orc_solver::run_lifting(double t_stage, const double* u) {
 
 // assemble_gradients (solver.cpp:729-791): BR1 gradients of (v1, v2, v3, T).
 void orc_solver::assemble_gradients(const double* u) {
+  if (curved) {
+    assemble_gradients_curved(u);
+    return;
+  }
   const int ne = static_cast<int>(elems.size());
   const double* w = ns.w.data();
   const double* fl = basis.fl.data();
@@ -1133,7 +1414,15 @@ void orc_solver::assemble_gradients(const double* u) {
               g[3 * c + 2] = cz * (sz - vz);
             }
           }
-      // Prolong gradients to the faces (solver.cpp:770-790).
+      prolong_gradients(e);
+    }
+  }
+}
+
+// Prolong gradients to the faces (solver.cpp:770-790).
+void orc_solver::prolong_gradients(int e) {
+  const double* fl = basis.fl.data();
+  const double* fr = basis.fr.data();
       for (int a = 0; a < n; ++a)
         for (int bb = 0; bb < n; ++bb)
           for (int c = 0; c < NG; ++c) {
@@ -1157,6 +1446,53 @@ void orc_solver::assemble_gradients(const double* u) {
             gt(e, ZM)[fn * NG + c] = zm;
             gt(e, ZP)[fn * NG + c] = zp;
           }
+}
+
+// Curved BR1 gradient, conservative weak form (the metric inside the derivative):
+//   J g_c = sum_d [ (l_i(+1)/w_i) q*+ (n sJ)+_c - (l_i(-1)/w_i) q*- (n sJ)-_c
+//                   - sum_m Dhat(i,m) Ja^d_c(m) q(m) ],
+// with (n sJ) the +xi_d normal of the side; for affine metrics this is
+// assemble_gradients above (solver.cpp:729-768).
+void orc_solver::assemble_gradients_curved(const double* u) {
+  const int ne = static_cast<int>(elems.size());
+  const double* w = ns.w.data();
+  const double* fl = basis.fl.data();
+  const double* fr = basis.fr.data();
+#pragma omp parallel
+  {
+    std::vector<double> q(static_cast<size_t>(n3) * 4);
+#pragma omp for schedule(static)
+    for (int e = 0; e < ne; ++e) {
+      for (int nd = 0; nd < n3; ++nd) prim4(u + (static_cast<size_t>(e) * n3 + nd) * NV, gas, q.data() + nd * 4);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+          for (int k = 0; k < n; ++k) {
+            const int nd = (i * n + j) * n + k;
+            const int ia[3] = {i, j, k};
+            const int fidx[3] = {j * n + k, i * n + k, i * n + j};
+            double* g = grad.data() + node(e, i, j, k) * NG;
+            const double ij = mt(e, nd)[9];
+            for (int c = 0; c < 4; ++c)
+              for (int kk = 0; kk < 3; ++kk) {
+                double vol = 0.0;
+                for (int m = 0; m < n; ++m) {
+                  const int mx = (m * n + j) * n + k, my = (i * n + m) * n + k, mz = (i * n + j) * n + m;
+                  vol += wdiff[i * n + m] * mt(e, mx)[0 + kk] * q[mx * 4 + c] +
+                         wdiff[j * n + m] * mt(e, my)[3 + kk] * q[my * 4 + c] +
+                         wdiff[k * n + m] * mt(e, mz)[6 + kk] * q[mz * 4 + c];
+                }
+                double surf = 0.0;
+                for (int d = 0; d < 3; ++d) {
+                  const int f = fidx[d];
+                  const double* np = fm(e, 2 * d + 1) + f * 4;
+                  const double* nm = fm(e, 2 * d) + f * 4;
+                  surf += (lf(e, 2 * d + 1)[f * 4 + c] * np[kk] * np[3] * fr[ia[d]] -
+                           lf(e, 2 * d)[f * 4 + c] * nm[kk] * nm[3] * fl[ia[d]]) / w[ia[d]];
+                }
+                g[3 * c + kk] = ij * (surf - vol);
+              }
+          }
+      prolong_gradients(e);
     }
   }
 }
@@ -1199,6 +1535,11 @@ void orc_solver::interior_flux() {
     for (int k = 0; k < n2; ++k) {
       const double* gm = lifting ? gt(f.em, sm) + k * NG : nullptr;
       const double* gp = lifting ? gt(f.ep, sp) + k * NG : nullptr;
+      if (curved) {
+        // +xi normal of the face (identical in both slots); vg_n = vg . n.
+        const double* nrm = fm(f.em, sm) + k * 4;
+        face_flux_n(um + k * NV, up + k * NV, nrm, bands[elems[f.em].band].vg * nrm[1], gm, gp, gas, om + k * NV);
+      } else
       face_flux(um + k * NV, up + k * NV, f.dir, vg_n, gm, gp, gas, om + k * NV);
       for (int v = 0; v < NV; ++v) op[k * NV + v] = om[k * NV + v];
     }
@@ -1232,6 +1573,16 @@ void orc_solver::volume(const double* u, double* out) {
           for (int d = 0; d < 3; ++d)
             for (int v = 0; v < NV; ++v) f[d][v] -= fv[d][v];
         }
+        if (curved) {
+          // Contravariant flux Ja^d . F (the affine sJ_d F_d below).
+          const double* ja = mt(e, nd);
+          for (int v = 0; v < NV; ++v) {
+            fx[nd * NV + v] = ja[0] * f[0][v] + ja[1] * f[1][v] + ja[2] * f[2][v];
+            fy[nd * NV + v] = ja[3] * f[0][v] + ja[4] * f[1][v] + ja[5] * f[2][v];
+            fz[nd * NV + v] = ja[6] * f[0][v] + ja[7] * f[1][v] + ja[8] * f[2][v];
+          }
+          continue;
+        }
         for (int v = 0; v < NV; ++v) {
           fx[nd * NV + v] = f[0][v] * sjx;
           fy[nd * NV + v] = f[1][v] * sjy;
@@ -1249,7 +1600,7 @@ void orc_solver::volume(const double* u, double* out) {
                 acc += wdiff[i * n + m] * fx[((m * n + j) * n + k) * NV + v] +
                        wdiff[j * n + m] * fy[((i * n + m) * n + k) * NV + v] +
                        wdiff[k * n + m] * fz[((i * n + j) * n + m) * NV + v];
-              o[v] = acc * inv_jac;
+              o[v] = acc * (curved ? mt(e, (i * n + j) * n + k)[9] : inv_jac);
             }
           }
     }
@@ -1309,6 +1660,13 @@ void orc_solver::dirichlet_flux(double t_stage) {
         face_node_position(df.e, df.side, p, q, t_stage, x);
         const State ext = eval_case(flow_case, x, t_stage, gas);
         const double* g = lifting ? gt(df.e, df.side) + k * NG : nullptr;
+        if (curved) {
+          const double* nrm = fm(df.e, df.side) + k * 4;
+          const double vgn = bands[elems[df.e].band].vg * nrm[1];
+          if (plus) face_flux_n(mine + k * NV, ext.data(), nrm, vgn, g, g, gas, o + k * NV);
+          else face_flux_n(ext.data(), mine + k * NV, nrm, vgn, g, g, gas, o + k * NV);
+          continue;
+        }
         if (plus) face_flux(mine + k * NV, ext.data(), dir, vg_n, g, g, gas, o + k * NV);
         else face_flux(ext.data(), mine + k * NV, dir, vg_n, g, g, gas, o + k * NV);
       }
@@ -1340,7 +1698,11 @@ void orc_solver::apply_faces(double* out) {
             else if (dir == 1) { i = p; j = a; k = q; }
             else { i = p; j = q; k = a; }
             double* o = out + node(e, i, j, k) * NV;
-            for (int v = 0; v < NV; ++v) o[v] += c * line[(p * n + q) * NV + v];
+            // Curved: (sJ / J) of the face node and the volume node.
+            const double cc = curved ? sgn * (lift_v[a] / w[a]) * fm(e, side)[(p * n + q) * 4 + 3] *
+                                           mt(e, (i * n + j) * n + k)[9]
+                                     : c;
+            for (int v = 0; v < NV; ++v) o[v] += cc * line[(p * n + q) * NV + v];
           }
       }
     }
@@ -1602,6 +1964,14 @@ int orc_get_mapping(const orc_solver* s, int ctx, int* m) {
     for (size_t f = 0; f < nf; ++f) m[r * nf + f] = c.m[r].empty() ? -1 : c.m[r][f];
   return SDG_OK;
 }
+int orc_get_metrics(const orc_solver* s, double* met, double* fmet) {
+  return guard(const_cast<orc_solver*>(s), [&] {
+    if (!s->curved) throw ConfigError("metrics are stored for curved meshes only");
+    std::copy(s->met.begin(), s->met.end(), met);
+    std::copy(s->fmet.begin(), s->fmet.end(), fmet);
+  });
+}
+
 // integrate_mass_energy (diagnostics.cpp:31-50).
 int orc_integrate_mass_energy(const orc_solver* s, const double* u, double* out2) {
   const int n = s->n;
@@ -1613,7 +1983,8 @@ int orc_integrate_mass_energy(const orc_solver* s, const double* u, double* out2
       for (int j = 0; j < n; ++j)
         for (int k = 0; k < n; ++k) {
           const double* p = u + s->node(static_cast<int>(e), i, j, k) * NV;
-          const double wj = s->ns.w[i] * s->ns.w[j] * s->ns.w[k] * jac;
+          const double wj = s->ns.w[i] * s->ns.w[j] * s->ns.w[k] *
+                            (s->curved ? 1.0 / s->mt(static_cast<int>(e), (i * n + j) * n + k)[9] : jac);
           m += wj * p[0];
           en += wj * p[4];
         }

@@ -61,6 +61,10 @@ int orc_get_pairing(const orc_solver* s, int role, int* ncols, int* cols);
 /* m(i_sub, i_face) of one context: 2 rows of n_faces_local ints. */
 int orc_get_mapping(const orc_solver* s, int ctx, int* m);
 
+/* Curved metrics (SDG_MAP_WARP): met E x N3 x 10 (Ja^d_c at [3d+c], 1/J),
+ * fmet E x 6 x N2 x 4 (unit +xi normal, sJ).  ConfigError for affine meshes. */
+int orc_get_metrics(const orc_solver* s, double* met, double* fmet);
+
 /* Mass and energy integrals (proj/src/diagnostics.cpp:31-50). */
 int orc_integrate_mass_energy(const orc_solver* s, const double* u, double* out2);
 /* Exact case solution sampled at the nodes at time t (full field). */

@@ -32,6 +32,7 @@ class MeshSpec(C.Structure):
         ("bands", BandSpec * SDG_MAX_BANDS),
         ("periodic_x", C.c_int), ("periodic_y", C.c_int), ("periodic_z", C.c_int),
         ("partition", C.c_int),
+        ("mapping", C.c_int), ("warp", C.c_double),
     ]
 
 
@@ -87,11 +88,14 @@ def raise_for(code: int, msg: str) -> None:
 
 
 PARTITION_LEX, PARTITION_SFC = 0, 1
+MAP_BOX, MAP_WARP = 0, 1
 
 
 def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z0=0.0,
-              periodic=(True, True, True), partition=PARTITION_LEX) -> MeshSpec:
-    """bands: list of (nx, width_frac, vg_y) tuples, stacked along x."""
+              periodic=(True, True, True), partition=PARTITION_LEX, warp=None) -> MeshSpec:
+    """bands: list of (nx, width_frac, vg_y) tuples, stacked along x.  warp: None for
+    affine hexahedra, else the amplitude of the curved SDG_MAP_WARP mapping
+    (include/sdg_types.h; 0.0 gives the curved code path on an affine geometry)."""
     if not 1 <= len(bands) <= SDG_MAX_BANDS:
         raise ConfigError("mesh needs 1..16 bands")
     m = MeshSpec()
@@ -105,6 +109,8 @@ def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z
         m.bands[i].nx, m.bands[i].width_frac, m.bands[i].vg_y = int(nx), float(frac), float(vg)
     m.periodic_x, m.periodic_y, m.periodic_z = (int(bool(p)) for p in periodic)
     m.partition = int(partition)
+    m.mapping = MAP_BOX if warp is None else MAP_WARP
+    m.warp = 0.0 if warp is None else float(warp)
     return m
 
 

@@ -1,0 +1,133 @@
+"""Curved hexahedra (SDG_MAP_WARP) in the CPU oracle.
+
+The reference has affine elements only (ElementMetrics, proj/src/mesh.cpp:102-111),
+so the curved restatement is pinned by properties rather than by reference
+outputs:
+  * on an affine geometry the curved code path reproduces the affine path
+    (which is itself pinned to the reference, tests/test_oracle_pins.py);
+  * the discrete metric identities hold to rounding (conservative curl form);
+  * free-stream preservation across sliding interfaces at several offsets
+    (3D form of proj/tests/test_solver.cpp:78-101 on curved elements);
+  * conservation of mass and energy over 10 steps (test_solver.cpp:282-299);
+  * convergence of the advected density wave under refinement.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_linf
+from oracle import pyoracle as P
+from paper_2008_04356_b200 import types as T
+
+BANDS3 = [(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)]
+
+
+def _basis(degree, kind):
+    n = degree + 1
+    lib = P.oracle_lib()
+    x, w, D, fl, fr = (np.zeros(n), np.zeros(n), np.zeros(n * n), np.zeros(n), np.zeros(n))
+    assert lib.orc_nodes(degree, kind, P._d(x), P._d(w)) == 0
+    assert lib.orc_basis(degree, kind, P._d(D), P._d(fl), P._d(fr)) == 0
+    return x, w, D.reshape(n, n), fl, fr
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+@pytest.mark.parametrize("mu", [0.0, 1e-3])
+def test_curved_path_on_affine_geometry_matches_affine(kind, mu):
+    """warp = 0: metrics equal the affine ones up to rounding, so residual,
+    BR1 gradients and two RK steps agree with the affine (reference-pinned) path."""
+    per = (False, True, True)
+    cfg = T.solver_config(3, kind, mu=mu, case=T.density_wave(a=(1.0, 1.0, 0.5)))
+    a = P.Oracle3D(T.mesh_spec(BANDS3, ny=4, nz=3, depth=1.0, periodic=per), cfg)
+    c = P.Oracle3D(T.mesh_spec(BANDS3, ny=4, nz=3, depth=1.0, periodic=per, warp=0.0), cfg)
+    a.set_initial_condition(0.0)
+    c.set_initial_condition(0.0)
+    assert rel_linf(c.field(), a.field()) == 0.0
+    for t in (0.0, 0.37):
+        assert rel_linf(c.compute_residual(t), a.compute_residual(t)) < 1e-13
+    if mu > 0.0:
+        assert rel_linf(c.compute_gradients(0.37), a.compute_gradients(0.37)) < 1e-13
+    dt = a.suggest_dt(0.5)
+    a.step(dt, 2)
+    c.step(dt, 2)
+    assert rel_linf(c.field(), a.field()) < 1e-13
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+@pytest.mark.parametrize("degree", [3, 5])
+def test_discrete_metric_identities(kind, degree):
+    """sum_d [ l(+1)/w (n sJ)+ - l(-1)/w (n sJ)- - Dhat Ja^d ] = 0 at every node:
+    the condition for free-stream preservation of the weak-form DGSEM."""
+    n = degree + 1
+    x, w, D, fl, fr = _basis(degree, kind)
+    Dh = (w[None, :] * D.T) / w[:, None]
+    m = T.mesh_spec(BANDS3, ny=4, nz=3, depth=1.0, warp=0.3)
+    o = P.Oracle3D(m, T.solver_config(degree, kind, case=T.freestream()))
+    met, fmet = o.metrics()
+    E = met.shape[0]
+    Ja = met[:, :, :9].reshape(E, n, n, n, 3, 3)
+    NS = (fmet[:, :, :, :3] * fmet[:, :, :, 3:4]).reshape(E, 6, n, n, 3)
+    lw0, lw1 = fl / w, fr / w
+    res = -np.einsum("im,emjkc->eijkc", Dh, Ja[..., 0, :])
+    res -= np.einsum("jm,eimkc->eijkc", Dh, Ja[..., 1, :])
+    res -= np.einsum("km,eijmc->eijkc", Dh, Ja[..., 2, :])
+    res += lw1[None, :, None, None, None] * NS[:, 1, None] - lw0[None, :, None, None, None] * NS[:, 0, None]
+    res += lw1[None, None, :, None, None] * NS[:, 3, :, None] - lw0[None, None, :, None, None] * NS[:, 2, :, None]
+    res += lw1[None, None, None, :, None] * NS[:, 5, :, :, None] - lw0[None, None, None, :, None] * NS[:, 4, :, :, None]
+    assert np.abs(res).max() < 1e-14 * np.abs(Ja).max() * 100
+    # unit normals, positive Jacobians, genuinely curved geometry
+    assert np.allclose(np.linalg.norm(fmet[..., :3], axis=-1), 1.0, atol=1e-15)
+    assert (met[:, :, 9] > 0).all()
+    assert np.ptp(met[:, :, 9]) > 0.1 * met[:, :, 9].mean()
+
+
+def test_sliding_faces_stay_planar():
+    """The warp vanishes on band boundaries (BASELINE configs[3]: interface faces
+    left unwarped): x-faces on the interfaces have normal e_x and sJ = hy hz / 4."""
+    m = T.mesh_spec(BANDS3, ny=4, nz=3, depth=1.0, warp=0.3)
+    o = P.Oracle3D(m, T.solver_config(3, T.NODES_GAUSS, case=T.freestream()))
+    _, fmet = o.metrics()
+    hy, hz = 2.0 / 4, 1.0 / 3
+    # band 1 (moving) occupies gids 24..47; its x- faces (side 0) of ix = 0 sit on interface 0
+    for g in range(24, 24 + 12):
+        f = fmet[g, 0]
+        assert np.abs(f[:, 0] - 1.0).max() < 1e-15 and np.abs(f[:, 1:3]).max() < 1e-15
+        assert np.abs(f[:, 3] - 0.25 * hy * hz).max() < 1e-15
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+@pytest.mark.parametrize("mu", [0.0, 1e-3])
+def test_freestream_preservation_curved_sliding(kind, mu):
+    """3D curved form of proj/tests/test_solver.cpp:86-92 (7 interface offsets)."""
+    mesh = T.mesh_spec(BANDS3, ny=6, nz=3, depth=1.0, warp=0.2)
+    o = P.Oracle3D(mesh, T.solver_config(3, kind, mu=mu, case=T.freestream(v=(1.0, 0.5, 0.25))))
+    o.set_initial_condition(0.0)
+    for t in (0.0, 0.05, 1.0 / 3.0, 0.37, 0.99, 2.0, 5.0 + 1e-9):
+        assert np.abs(o.compute_residual(t)).max() < 1e-12
+
+
+def test_conservation_curved_sliding():
+    """3D curved form of proj/tests/test_solver.cpp:282-299 (J-weighted quadrature)."""
+    mesh = T.mesh_spec(BANDS3, ny=6, nz=2, depth=1.0, warp=0.25)
+    o = P.Oracle3D(mesh, T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave(a=(1.0, 1.0, 0.5))))
+    o.set_initial_condition(0.0)
+    before = o.mass_energy()
+    o.step(o.suggest_dt(0.4), 10)
+    after = o.mass_energy()
+    assert np.all(np.abs(after - before) / np.abs(before) < 1e-12)
+
+
+def test_density_wave_converges_on_curved_mesh():
+    """Inviscid density wave on a warped periodic box: the L_inf error after a
+    fixed time drops at (close to) the design order N+1 under h-refinement."""
+    errs = []
+    for ne in (2, 4):
+        mesh = T.mesh_spec([(ne, 1.0, 0.0), (ne, 1.0, 0.4)], ny=2 * ne, nz=2 * ne, warp=0.15)
+        o = P.Oracle3D(mesh, T.solver_config(3, T.NODES_GAUSS, case=T.density_wave(a=(1.0, 1.0, 0.5))))
+        o.set_initial_condition(0.0)
+        t_end = 0.1
+        dt0 = o.suggest_dt(0.25)
+        steps = int(np.ceil(t_end / dt0))
+        o.step(t_end / steps, steps)
+        errs.append(np.abs(o.field() - o.sample_case(t_end)).max())
+    rate = np.log2(errs[0] / errs[1])
+    assert rate > 3.0, (errs, rate)
