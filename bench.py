@@ -45,27 +45,37 @@ def parse():
     p.add_argument("--elems", type=int, default=64, help="elements per direction per GPU (weak scaling)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--mesh", default="tgv", choices=["tgv", "warped"],
+                   help="tgv: affine hexahedra (configs[4]); warped: the same case on curved hexahedra "
+                        "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3])")
     return p.parse_args()
 
 
-def tgv_mesh(T, elems_x, elems_yz):
+def tgv_mesh(T, elems_x, elems_yz, warp=None):
     """Three blocks along x (= BASELINE z); interfaces at 2pi/3, 4pi/3."""
     L = 2.0 * math.pi
     base, rem = divmod(elems_x, 3)
     n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
     bands = [(n[0], 1.0, 0.0), (n[1], 1.0, 0.2), (n[2], 1.0, 0.0)]
-    return T.mesh_spec(bands, ny=elems_yz, nz=elems_yz, width=L, height=L, depth=L), bands
+    return T.mesh_spec(bands, ny=elems_yz, nz=elems_yz, width=L, height=L, depth=L, warp=warp), bands
+
+
+WARP = 0.05  # BASELINE configs[3]: "sinusoidal mesh warping of amplitude 5% of element size"
 
 
 def workload(args, world):
     from paper_2008_04356_b200 import types as T
-    mesh, bands = tgv_mesh(T, args.elems * world, args.elems)
+    curved = args.mesh == "warped"
+    mesh, bands = tgv_mesh(T, args.elems * world, args.elems, warp=WARP if curved else None)
     cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
     n1 = args.degree + 1
     E = sum(b[0] for b in bands) * args.elems * args.elems
+    geom = (f"curved hexahedra (SDG_MAP_WARP, warp {WARP} of the element size, as BASELINE configs[3]; "
+            f"per-node metrics)" if curved else "affine hexahedra")
     conf = {
         "workload": f"BASELINE configs[4]: TGV M=0.1 Re=1600, 3 blocks, 2 planar sliding interfaces (middle +0.2), "
-                    f"{args.elems}^3 elements/GPU, N={args.degree} Gauss, viscous",
+                    f"{args.elems}^3 elements/GPU, N={args.degree} Gauss, viscous, {geom}",
+        "geometry": "curved" if curved else "affine",
         "elements": E,
         "elements_per_gpu": E // world,
         "degree": args.degree,
@@ -140,7 +150,8 @@ def cpu_baseline(args, conf, timeout_s=20.0):
     threads = os.cpu_count() or 1
     P.oracle_lib().orc_set_threads(threads)
     e = 6
-    mesh, bands = tgv_mesh(T, e, e)
+    curved = conf.get("geometry") == "curved"
+    mesh, bands = tgv_mesh(T, e, e, warp=WARP if curved else None)
     cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
     o = P.Oracle3D(mesh, cfg)
     o.set_initial_condition(0.0)
@@ -161,8 +172,8 @@ def cpu_baseline(args, conf, timeout_s=20.0):
     except OSError:
         pass
     out = {"value": dof * 5 * steps / el, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same TGV case at "
-                     f"{e}^3 elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
+           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same TGV case"
+                     f"{' (curved)' if curved else ''} at {e}^3 elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
     try:
         out["reference_2d"] = reference_2d(args.degree, seconds=min(8.0, timeout_s))
     except Exception as ex:  # supplementary: never fail the bench line over it
@@ -225,11 +236,13 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     E = conf["elements_per_gpu"]
     dof = E * n3
     peak = peaks.get("hbm_gbs", 6650.0)
-    bf = b_flow(args.degree)
+    curved = conf.get("geometry") == "curved"
+    bf = b_flow(args.degree, curved)
     stage_ms = ms_per_step / 5.0
     ach = value_per_gpu * bf / 1e9
     traffic = None
     prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*stage_traffic*.json")))
+    prof = [p for p in prof if ("curved" in os.path.basename(p)) == curved]
     if prof:
         try:
             traffic = json.load(open(prof[-1])).get("dram_bytes_per_stage")
@@ -238,11 +251,15 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     rl = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
           "kernel": "RK stage = k_gradient + k_update + mortar/pairing kernels (one right-hand side + update)",
           "algorithmic_bytes_per_launch": bf * dof, "bytes_per_dof": bf,
-          "per_unit_source": "SURVEY.md §8(d) B_flow = 240 + 2712/(N+1) B per DOF-update (affine)",
+          "per_unit_source": ("SURVEY.md §8(d) B_flow,curved = 400 + 2904/(N+1) B per DOF-update (curved)" if curved
+                              else "SURVEY.md §8(d) B_flow = 240 + 2712/(N+1) B per DOF-update (affine)"),
           "mean_launch_ms": stage_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
     extra = {}
     # This implementation's fused dataflow.
     per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 18), "gradient": 8 * E * (5 * n3 + 6 * n2 * 9)}
+    if curved:  # + per-node metrics (10 doubles) and per-side face metrics (4 doubles per face node), both kernels
+        for k in per_kernel:
+            per_kernel[k] += 8 * E * (10 * n3 + 6 * n2 * 4)
     for name, byts in per_kernel.items():
         ms, cnt = kt.get(name, (0.0, 0))
         if cnt:

@@ -131,6 +131,14 @@ int sdg_read_snapshot(sdg_ctx* ctx, const char* path, double* time);
  * partition.cpp:154-169).  *len receives the full length. */
 int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta, char* buf, long cap, long* len);
 
+/* Host-only curved metric terms of one rank's elements (no GPU needed), as
+ * uploaded by sdg_create for an SDG_MAP_WARP mesh: met n_local x N3 x 10
+ * (Ja^d_c at [3d + c], 1/J), fmet n_local x 6 x N2 x 4 (unit +xi normal, sJ).
+ * The reference's metrics are affine (ElementMetrics, proj/src/mesh.cpp:102-111).
+ * met/fmet may be NULL to query *n_local; elements in sdg_local_element_ids order. */
+int sdg_metrics_host(const sdg_mesh_spec* mesh, int degree, int node_kind, int n_ranks, int rank, double* met,
+                     double* fmet, long* n_local);
+
 /* Communication trace of this rank (TraceRow, transport.hpp:28-37): JSON rows
  * [step, stage, src, dst, bytes, kind, is_send], step -1 = init; kinds follow
  * MsgKind (transport.hpp:13-24).  sdg_inject_collective is the audit's

@@ -77,6 +77,7 @@ def lib():
         L.sdg_pairing_device.argtypes = [C.c_int, _lp, C.c_long, C.c_long, _ip, C.c_long, C.c_int, C.c_int,
                                          C.c_int, _ip, _ip, _ip, _lp, _ip, _ip, _ip]
         L.sdg_plan_json.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_double, C.c_char_p, C.c_long, _lp]
+        L.sdg_metrics_host.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _lp]
         L.sdg_diagnostics.argtypes = [_vp, C.c_double, C.c_int, _dp]
         L.sdg_write_snapshot.argtypes = [_vp, C.c_char_p, C.c_double]
         L.sdg_read_snapshot.argtypes = [_vp, C.c_char_p, _dp]
@@ -99,7 +100,7 @@ EXPORTED = [
     "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
-    "sdg_pairing_device", "sdg_plan_json", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
+    "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
     "sdg_trace_json", "sdg_inject_collective", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
@@ -340,6 +341,20 @@ def plan(mesh: T.MeshSpec, n_ranks: int, rank: int, delta: float = 0.0) -> dict:
     T.raise_for(lib().sdg_plan_json(C.byref(mesh), n_ranks, rank, delta, buf, n.value + 1, C.byref(n)),
                 lib().sdg_global_error().decode())
     return json.loads(buf.value.decode())
+
+
+def metrics_host(mesh: T.MeshSpec, degree: int, node_kind: int, n_ranks: int = 1, rank: int = 0):
+    """Host-only curved metrics of one rank (no GPU): (met [E, N3, 10], fmet [E, 6, N2, 4])."""
+    n = C.c_long()
+    L = lib()
+    T.raise_for(L.sdg_metrics_host(C.byref(mesh), degree, node_kind, n_ranks, rank, None, None, C.byref(n)),
+                L.sdg_global_error().decode())
+    n1 = degree + 1
+    met = np.zeros((n.value, n1 ** 3, 10))
+    fmet = np.zeros((n.value, 6, n1 * n1, 4))
+    T.raise_for(L.sdg_metrics_host(C.byref(mesh), degree, node_kind, n_ranks, rank, _d(met), _d(fmet), C.byref(n)),
+                L.sdg_global_error().decode())
+    return met, fmet
 
 
 def pairing_device(faces, n_par, n_perp, ranks, n_delta, on_static, conforming, self_rank):

@@ -1,0 +1,520 @@
+// Curved hexahedra (SDG_MAP_WARP, include/sdg_types.h): element kernels with
+// per-node metric terms.  Included by kernels.cu inside its anonymous
+// namespace (shares the flux helpers, tables and loaders defined there).
+//
+// The reference has affine elements only (ElementMetrics, mesh.cpp:102-111);
+// these kernels generalise its phases as follows:
+//   volume term   (1/J) sum_d Dhat (Ja^d . F)               (volume_kernel, solver.cpp:343-385)
+//   BR1 gradient  J g_c = sum_d [surface q* (n sJ)_c - Dhat (Ja^d_c q)]   (assemble_gradients, :729-768)
+//   face flux     Roe / viscous along the face's unit normal n, vg_n = vg . n   (flux.cpp:68-133)
+//   surface lift  +- (l(+-1)/w) (sJ / J) F*                  (apply_all_faces, :547-582)
+// Metrics per node: Ja^d_c at [3d + c] and 1/J (10 doubles, node-major);
+// per local side and face node: the unit normal along +xi_dir and sJ (4 doubles).
+// Both slots of a conforming face hold identical bits (host.cpp compute_metrics),
+// so both elements evaluate the face flux identically, as in the affine kernels.
+
+template <int N1>
+struct CDim {
+  static constexpr int N2 = N1 * N1;
+  static constexpr int N3 = N2 * N1;
+  static constexpr int EPB = N1 <= 4 ? Dim<N1>::EPB : 1;
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int PER_GRAD = 31 * N3 + 78 * N2;  // U, q, metrics, gradient | own traces, lift*, face metrics
+  static constexpr int PER_UPD = 20 * N3 + 78 * N2;   // U, staging, metrics | lift*, face flux, face metrics
+};
+
+// Flat, coalesced load of EPB consecutive elements' node-major NC-vectors into
+// SoA shared memory dst[le * per + c * N3 + node].
+template <int N1, int EPB, int NC>
+__device__ __forceinline__ void load_soa(const double* __restrict__ src, int e0, int E, double* dst, int per) {
+  constexpr int N3 = N1 * N1 * N1;
+  const int n_el = min(EPB, E - e0);
+  const double* s = src + static_cast<size_t>(e0) * NC * N3;
+  for (int f = threadIdx.x; f < n_el * NC * N3; f += blockDim.x) {
+    const int le = f / (NC * N3), r = f - le * NC * N3;
+    dst[le * per + (r % NC) * N3 + r / NC] = __ldg(s + f);
+  }
+}
+
+// Face metrics of EPB consecutive elements (6 x N2 x 4 contiguous per element).
+template <int N1, int EPB>
+__device__ __forceinline__ void load_fmet(const double* __restrict__ src, int e0, int E, double* dst, int per) {
+  constexpr int W = 6 * N1 * N1 * 4;
+  const int n_el = min(EPB, E - e0);
+  const double* s = src + static_cast<size_t>(e0) * W;
+  for (int f = threadIdx.x; f < n_el * W; f += blockDim.x) {
+    const int le = f / W;
+    dst[le * per + (f - le * W)] = __ldg(s + f);
+  }
+}
+
+// Roe flux along the unit normal n, Harten-Hyman fix on the acoustic waves,
+// eigenvalues shifted by vg_n (flux.cpp:68-133 in rotation-invariant vector
+// form: the shear waves carry rho (dv - dun n)).  False when c^2 <= 0.
+__device__ __forceinline__ bool roe_flux_n(const double* ul, const double* ur, const double* n, double vgn,
+                                           const GasD& g, double* f) {
+  const double rl = ul[0], rr = ur[0];
+  const double irl = rcp_nr(rl), irr = rcp_nr(rr);
+  const double vl0 = ul[1] * irl, vl1 = ul[2] * irl, vl2 = ul[3] * irl;
+  const double vr0 = ur[1] * irr, vr1 = ur[2] * irr, vr2 = ur[3] * irr;
+  const double pl = g.gm1 * (ul[4] - 0.5 * (ul[1] * vl0 + ul[2] * vl1 + ul[3] * vl2));
+  const double pr = g.gm1 * (ur[4] - 0.5 * (ur[1] * vr0 + ur[2] * vr1 + ur[3] * vr2));
+  const double hl = (ul[4] + pl) * irl, hr = (ur[4] + pr) * irr;
+  const double cl = sqrt_nr(g.gamma * pl * irl), cr = sqrt_nr(g.gamma * pr * irr);
+  const double unl = vl0 * n[0] + vl1 * n[1] + vl2 * n[2];
+  const double unr = vr0 * n[0] + vr1 * n[1] + vr2 * n[2];
+
+  const double sl = sqrt_nr(rl), sr = sqrt_nr(rr);
+  const double inv = rcp_nr(sl + sr);
+  const double v0 = (sl * vl0 + sr * vr0) * inv, v1 = (sl * vl1 + sr * vr1) * inv, v2 = (sl * vl2 + sr * vr2) * inv;
+  const double h = (sl * hl + sr * hr) * inv;
+  const double un = v0 * n[0] + v1 * n[1] + v2 * n[2];
+  const double q2 = v0 * v0 + v1 * v1 + v2 * v2;
+  const double c2 = g.gm1 * (h - 0.5 * q2);
+  if (!(c2 > 0.0)) return false;
+  const double c = sqrt_nr(c2);
+  const double ic2 = rcp_nr(c2);
+  const double rho = sl * sr;
+
+  const double dp = pr - pl, dun = unr - unl, drho = rr - rl;
+  const double dt0 = (vr0 - vl0) - dun * n[0], dt1 = (vr1 - vl1) - dun * n[1], dt2 = (vr2 - vl2) - dun * n[2];
+  const double a1 = (dp - rho * c * dun) * 0.5 * ic2;
+  const double a2 = drho - dp * ic2;
+  const double a4 = (dp + rho * c * dun) * 0.5 * ic2;
+  const double l1 = entropy_fix(un - c - vgn, unl - cl - vgn, unr - cr - vgn);
+  const double l2 = fabs(un - vgn);
+  const double l4 = entropy_fix(un + c - vgn, unl + cl - vgn, unr + cr - vgn);
+  const double w1 = l1 * a1, w2 = l2 * a2, w4 = l4 * a4;
+  const double d0 = w1 + w2 + w4;
+  const double wc = (w4 - w1) * c, lr = l2 * rho;
+  const double dm0 = d0 * v0 + wc * n[0] + lr * dt0;
+  const double dm1 = d0 * v1 + wc * n[1] + lr * dt1;
+  const double dm2 = d0 * v2 + wc * n[2] + lr * dt2;
+  const double dE = w1 * (h - un * c) + w2 * 0.5 * q2 + w4 * (h + un * c) + lr * (v0 * dt0 + v1 * dt1 + v2 * dt2);
+
+  f[0] = 0.5 * ((rl * unl - vgn * rl) + (rr * unr - vgn * rr) - d0);
+  f[1] = 0.5 * ((ul[1] * unl + pl * n[0] - vgn * ul[1]) + (ur[1] * unr + pr * n[0] - vgn * ur[1]) - dm0);
+  f[2] = 0.5 * ((ul[2] * unl + pl * n[1] - vgn * ul[2]) + (ur[2] * unr + pr * n[1] - vgn * ur[2]) - dm1);
+  f[3] = 0.5 * ((ul[3] * unl + pl * n[2] - vgn * ul[3]) + (ur[3] * unr + pr * n[2] - vgn * ur[3]) - dm2);
+  f[4] = 0.5 * (((ul[4] + pl) * unl - vgn * ul[4]) + ((ur[4] + pr) * unr - vgn * ur[4]) - dE);
+  return true;
+}
+
+// Viscous normal flux Fv . n, components 1..4 (flux.cpp:23-42 contracted with n).
+__device__ __forceinline__ void fv_n(const double* u, const double* gr, const double* n, const GasD& g, double* o) {
+  const double ir = rcp_nr(u[0]);
+  const double v0 = u[1] * ir, v1 = u[2] * ir, v2 = u[3] * ir;
+  const double div = gr[0] + gr[4] + gr[8];
+  const double t00 = 2.0 * g.mu * gr[0] + g.lam * div;
+  const double t11 = 2.0 * g.mu * gr[4] + g.lam * div;
+  const double t22 = 2.0 * g.mu * gr[8] + g.lam * div;
+  const double t01 = g.mu * (gr[1] + gr[3]);
+  const double t02 = g.mu * (gr[2] + gr[6]);
+  const double t12 = g.mu * (gr[5] + gr[7]);
+  const double r0 = t00 * n[0] + t01 * n[1] + t02 * n[2];
+  const double r1 = t01 * n[0] + t11 * n[1] + t12 * n[2];
+  const double r2 = t02 * n[0] + t12 * n[1] + t22 * n[2];
+  const double dT = gr[9] * n[0] + gr[10] * n[1] + gr[11] * n[2];
+  o[0] = r0;
+  o[1] = r1;
+  o[2] = r2;
+  o[3] = r0 * v0 + r1 * v1 + r2 * v2 + g.kcond * dT;
+}
+
+// Curved BR1 gradient at one node, conservative weak form:
+//   g_c = (1/J) sum_d [ lw1 q*+ (n sJ)+_c - lw0 q*- (n sJ)-_c - sum_m Dhat(ia, m) Ja^d_c(m) q(m) ].
+// sq [4][N3], sJa [10][N3] (Ja^d_c at 3d + c), sLift [6][4][N2], sfm [6][N2][4].
+template <int N1>
+__device__ __forceinline__ void node_gradient_curved(const double* tab, const double* sq, const double* sJa,
+                                                     const double* sLift, const double* sfm, int i, int j, int k,
+                                                     double* g) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  const double* dh = tab;
+  const double* lw = tab + N1 * N1 + 2 * N1;  // liftw[0][.], liftw[1][.]
+  double acc[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int ia = d == 0 ? i : (d == 1 ? j : k);
+    const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+    const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      const double c = dh[ia * N1 + m];
+      const int nd = base + m * stride;
+      const double ja0 = sJa[(3 * d + 0) * N3 + nd], ja1 = sJa[(3 * d + 1) * N3 + nd],
+                   ja2 = sJa[(3 * d + 2) * N3 + nd];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double cq = c * sq[q * N3 + nd];
+        acc[3 * q + 0] += cq * ja0;
+        acc[3 * q + 1] += cq * ja1;
+        acc[3 * q + 2] += cq * ja2;
+      }
+    }
+  }
+  const double ij = sJa[9 * N3 + (i * N1 + j) * N1 + k];
+  double surf[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) surf[q] = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int ia = d == 0 ? i : (d == 1 ? j : k);
+    const int f = d == 0 ? j * N1 + k : (d == 1 ? i * N1 + k : i * N1 + j);
+    const double* np = sfm + ((2 * d + 1) * N2 + f) * 4;
+    const double* nm = sfm + ((2 * d) * N2 + f) * 4;
+    const double sp = lw[N1 + ia] * np[3], sm = lw[ia] * nm[3];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double lp = sLift[((2 * d + 1) * 4 + q) * N2 + f] * sp;
+      const double lm = sLift[((2 * d) * 4 + q) * N2 + f] * sm;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) surf[3 * q + kk] += lp * np[kk] - lm * nm[kk];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) g[q] = ij * (surf[q] - acc[q]);
+}
+
+// ----------------------------------------------------------------------------
+// k_gradient_curved: lift* -> curved gradient -> Fv.n (conforming sides) /
+// gradient traces (sliding and Dirichlet sides); grad_out for compute_gradients.
+// ----------------------------------------------------------------------------
+template <int N1>
+__global__ void __launch_bounds__(CDim<N1>::THREADS) k_gradient_curved(const __grid_constant__ ElemConsts C,
+                                                                       FieldPtrs P, StageArgs A) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = CDim<N1>::EPB, TAB = Dim<N1>::TAB, PER = CDim<N1>::PER_GRAD;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  load_tables<N1>(C, tab);
+  const int e0 = P.e_first + blockIdx.x * EPB;
+  double* base = smem + TAB;
+  load_soa<N1, EPB, 5>(P.U, e0, P.E, base, PER);
+  load_soa<N1, EPB, 10>(P.met, e0, P.E, base + 9 * N3, PER);
+  load_fmet<N1, EPB>(P.fmet, e0, P.E, base + 31 * N3 + 54 * N2, PER);
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = e < P.E;
+  double* su = base + le * PER;
+  double* sq = su + 5 * N3;
+  double* sJa = sq + 4 * N3;
+  double* sG = sJa + 10 * N3;
+  double* sTr = sG + 12 * N3;
+  double* sLift = sTr + 30 * N2;
+  double* sfm = sLift + 24 * N2;
+  __syncthreads();
+  if (active) {
+    double u[5], q[4];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
+    prim4(u, C.gas, q);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sq[c * N3 + t] = q[c];
+    face_lift_phase<N1>(C, P, tab, su, e, A.t_stage, sLift, sTr);
+  }
+  __syncthreads();
+  if (active) {
+    const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+    double g[12];
+    node_gradient_curved<N1>(tab, sq, sJa, sLift, sfm, i, j, k, g);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
+    if (P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = g[c];
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double gt[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+    const int slot = e * 6 + s;
+    const int typ = P.side_type[slot], idx = P.side_idx[slot];
+    if (typ == kConforming) {
+      double fv[4];
+      fv_n(sTr + (s * N2 + f) * 5, gt, sfm + (s * N2 + f) * 4, C.gas, fv);
+      double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dst[c] = fv[c];
+    } else {
+      double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// k_update_curved: face fluxes, curved gradient, contravariant volume flux and
+// weak divergence, surface lift, low-storage RK update, admissibility and the
+// traces of the new state (the phases of k_update with metric terms).
+// ----------------------------------------------------------------------------
+template <int N1, bool VISC>
+__global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __grid_constant__ ElemConsts C,
+                                                                     FieldPtrs P, StageArgs A) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = CDim<N1>::EPB, TAB = Dim<N1>::TAB, PER = CDim<N1>::PER_UPD;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  load_tables<N1>(C, tab);
+  const int e0 = P.e_first + blockIdx.x * EPB;
+  double* elems = smem + TAB;
+  load_soa<N1, EPB, 5>(P.U, e0, P.E, elems, PER);
+  load_soa<N1, EPB, 10>(P.met, e0, P.E, elems + 10 * N3, PER);
+  load_fmet<N1, EPB>(P.fmet, e0, P.E, elems + 20 * N3 + 54 * N2, PER);
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = e < P.E;
+  double* su = elems + le * PER;
+  double* sF = su + 5 * N3;
+  double* sJa = sF + 5 * N3;
+  double* sLift = sJa + 10 * N3;
+  double* sFlux = sLift + 24 * N2;
+  double* sfm = sFlux + 30 * N2;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  __syncthreads();
+
+  // Phase 1: numerical flux along each face node's normal -> sFlux[s][v][f]; lift* -> sLift.
+  if (active) {
+    if (VISC) {
+      double u[5], q[4];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
+      prim4(u, C.gas, q);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
+    }
+    for (int it = t; it < 6 * N2; it += N3) {
+      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1, dir = s >> 1;
+      const double* ell = tab + N1 * N1 + (s & 1) * N1;
+      double own[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b);
+      const double* nrm = sfm + (s * N2 + f) * 4;
+      const double vgn = B.vg * nrm[1];
+      const int slot = e * 6 + s;
+      const int typ = P.side_type[slot], idx = P.side_idx[slot];
+      double flux[5], lift[4];
+      bool ok = true;
+      if (typ == kConforming) {
+        const double* nb = P.trace + static_cast<size_t>(idx) * N2 * 5 + f * 5;
+        double other[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) other[v] = nb[v];
+        const double* um = (s & 1) ? own : other;
+        const double* up = (s & 1) ? other : own;
+        ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
+        if (VISC) {
+          double qa[4], qb[4];
+          prim4(own, C.gas, qa);
+          prim4(other, C.gas, qb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+          const double* pa = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
+          const double* pb = P.fvn + (static_cast<size_t>(idx) * N2 + f) * 4;
+          const double* fm = (s & 1) ? pa : pb;
+          const double* fp = (s & 1) ? pb : pa;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
+        }
+      } else if (typ == kSliding) {
+        const double* sf = P.slide_flux + (static_cast<size_t>(idx) * N2 + f) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) flux[v] = sf[v];
+        if (VISC) {
+          const double* sl = P.slide_lift + (static_cast<size_t>(idx) * N2 + f) * 4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = sl[c];
+        }
+      } else {
+        double x[3], ext[5];
+        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        const double* um = (s & 1) ? own : ext;
+        const double* up = (s & 1) ? ext : own;
+        ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
+        if (VISC) {
+          prim4(ext, C.gas, lift);
+          const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+          double gg[12];
+#pragma unroll
+          for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+          double fm[4], fp[4];
+          fv_n(um, gg, nrm, C.gas, fm);
+          fv_n(up, gg, nrm, C.gas, fp);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
+        }
+      }
+      if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = flux[v];
+      if (VISC) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // Phase 2: pointwise flux (ALE convective minus viscous) -> contravariant Ja^d . F.
+  double Ft[3][5];
+  if (active) {
+    double u[5], F[3][5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = su[v * N3 + t];
+    const double ir = rcp_nr(u[0]);
+    const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+    const double p = pressure(u, ir, C.gas);
+    const double vgv[3] = {0.0, B.vg, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      F[d][0] = u[0] * vv[d];
+      F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0);
+      F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0);
+      F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0);
+      F[d][4] = (u[4] + p) * vv[d];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) F[d][v] -= vgv[d] * u[v];
+    }
+    if (VISC) {
+      double g[12];
+      node_gradient_curved<N1>(tab, sF, sJa, sLift, sfm, i, j, k, g);
+      const double div = g[0] + g[4] + g[8];
+      const double mu = C.gas.mu, lam = C.gas.lam;
+      const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
+                                {mu * (g[1] + g[3]), 2.0 * mu * g[4] + lam * div, mu * (g[5] + g[7])},
+                                {mu * (g[2] + g[6]), mu * (g[5] + g[7]), 2.0 * mu * g[8] + lam * div}};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        F[d][1] -= tau[d][0];
+        F[d][2] -= tau[d][1];
+        F[d][3] -= tau[d][2];
+        F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double ja0 = sJa[(3 * d) * N3 + t], ja1 = sJa[(3 * d + 1) * N3 + t], ja2 = sJa[(3 * d + 2) * N3 + t];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) Ft[d][v] = ja0 * F[0][v] + ja1 * F[1][v] + ja2 * F[2][v];
+    }
+  }
+
+  // Phase 3: weak divergence sum_m Dhat(i,m) Ft(m) per direction.
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double* dh = tab;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sF[v * N3 + t] = Ft[d][v];
+    }
+    __syncthreads();
+    if (active) {
+      const int ia = d == 0 ? i : (d == 1 ? j : k);
+      const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double c = dh[ia * N1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF[v * N3 + base + m * stride];
+      }
+    }
+  }
+
+  // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
+  double du[5];
+  if (active) {
+    const double ij = sJa[9 * N3 + t];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
+    const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int dir = s >> 1;
+      const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+      const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+      const double l = lw[(s & 1) * N1 + ia];
+      if (l != 0.0) {
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * 4 + 3] * ij;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) sF[v * N3 + t] = du[v];
+  }
+  __syncthreads();
+
+  // Phase 5: flat coalesced RK update (solver.cpp:912-917) or residual store.
+  const int n_el = min(EPB, P.E - e0);
+  const size_t gbase = static_cast<size_t>(e0) * 5 * N3;
+  if (A.mode == 1) {
+    for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
+      const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+      P.out[gbase + fI] = elems[l * PER + 5 * N3 + (r % 5) * N3 + r / 5];
+    }
+    return;
+  }
+  for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
+    const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+    double* us = elems + l * PER + (r % 5) * N3 + r / 5;
+    const double d = us[5 * N3];
+    const double rg = A.rk_a * P.reg[gbase + fI] + A.dt * d;
+    const double un = *us + A.rk_b * rg;
+    P.reg[gbase + fI] = rg;
+    P.U[gbase + fI] = un;
+    *us = un;
+  }
+  __syncthreads();
+  if (!active) return;
+  {
+    double w[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) w[v] = su[v * N3 + t];
+    const double p = pressure(w, rcp_nr(w[0]), C.gas);
+    bool ok = w[0] > 0.0 && p > 0.0;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
+    if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+  }
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double* dst = P.trace_out + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+  }
+}
+
+template <int N1>
+void gradient_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  const int blocks = (p.E - p.e_first + CDim<N1>::EPB - 1) / CDim<N1>::EPB;
+  const int sm = (Dim<N1>::TAB + CDim<N1>::EPB * CDim<N1>::PER_GRAD) * 8;
+  cudaFuncSetAttribute(k_gradient_curved<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  k_gradient_curved<N1><<<blocks, CDim<N1>::THREADS, sm, st>>>(c, p, a);
+  check_launch("k_gradient_curved");
+}
+template <int N1>
+void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  const int blocks = (p.E - p.e_first + CDim<N1>::EPB - 1) / CDim<N1>::EPB;
+  const int sm = (Dim<N1>::TAB + CDim<N1>::EPB * CDim<N1>::PER_UPD) * 8;
+  if (c.gas.viscous) {
+    cudaFuncSetAttribute(k_update_curved<N1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    k_update_curved<N1, true><<<blocks, CDim<N1>::THREADS, sm, st>>>(c, p, a);
+  } else {
+    cudaFuncSetAttribute(k_update_curved<N1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    k_update_curved<N1, false><<<blocks, CDim<N1>::THREADS, sm, st>>>(c, p, a);
+  }
+  check_launch("k_update_curved");
+}

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <string>
+#include <thread>
 #include <tuple>
 
 namespace sdg {
@@ -11,6 +13,8 @@ namespace sdg {
 // ---------------------------------------------------------------- mesh
 MeshGeom::MeshGeom(const sdg_mesh_spec& s) : spec(s) {
   if (s.n_bands < 1 || s.n_bands > SDG_MAX_BANDS) throw ConfigError("mesh needs 1..16 bands");
+  if (s.mapping != SDG_MAP_BOX && s.mapping != SDG_MAP_WARP) throw ConfigError("unknown mesh mapping");
+  if (s.mapping == SDG_MAP_WARP && !std::isfinite(s.warp)) throw ConfigError("warp amplitude must be finite");
   if (s.ny < 1 || s.nz < 1) throw ConfigError("mesh needs ny >= 1 and nz >= 1");
   if (!(s.width > 0.0) || !(s.height > 0.0) || !(s.depth > 0.0))
     throw ConfigError("mesh extents must be positive");
@@ -270,6 +274,269 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
     t.peers.back().recv_slots.push_back(6 * ne + h);
   }
   return t;
+}
+
+// ---------------------------------------------------------------- curved geometry
+namespace {
+// sin(pi t), exactly 0 at integer t (the warp must vanish on band boundaries
+// and be exactly periodic).
+template <class R>
+R sinpi_exact(R t) {
+  R r = std::fmod(t, R(2));
+  if (r < R(0)) r += R(2);
+  if (r == R(0) || r == R(1)) return R(0);
+  return std::sin(R(3.14159265358979323846264338327950288L) * r);
+}
+}  // namespace
+
+// SDG_MAP_WARP position (include/sdg_types.h) at time t; the box position when affine.
+void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, double eta, double zeta, double t,
+               double* x) {
+  const BandGeom& B = m.bands[b];
+  const double bx = (B.x_lo + ix * B.hx) + 0.5 * (xi + 1.0) * B.hx;
+  const double by = (m.spec.y0 + iy * B.hy) + 0.5 * (eta + 1.0) * B.hy;
+  const double bz = (m.spec.z0 + iz * B.hz) + 0.5 * (zeta + 1.0) * B.hz;
+  if (m.spec.mapping != SDG_MAP_WARP) {
+    x[0] = bx;
+    x[1] = by + B.vg * t;
+    x[2] = bz;
+    return;
+  }
+  const double tx = (ix + 0.5 * (xi + 1.0)) / B.nx, ty = (iy + 0.5 * (eta + 1.0)) / m.spec.ny,
+               tz = (iz + 0.5 * (zeta + 1.0)) / m.spec.nz;
+  const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
+  const double A = m.spec.warp;
+  x[0] = bx + A * B.hx * sp * sy * sz;
+  x[1] = by + A * B.hy * sp * sz + B.vg * t;
+  x[2] = bz + A * B.hz * sp * sy;
+}
+
+namespace {
+using ldm = long double;
+// Mapped position minus the mapped element centre, long double.  Two elements
+// sharing a face see its geometry up to an exact translation.
+void relative_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, double eta, double zeta, ldm* x) {
+  const BandGeom& B = m.bands[b];
+  const ldm h[3] = {B.hx, B.hy, B.hz};
+  const ldm t[3] = {(ix + 0.5L * (xi + 1.0L)) / B.nx, (iy + 0.5L * (eta + 1.0L)) / m.spec.ny,
+                    (iz + 0.5L * (zeta + 1.0L)) / m.spec.nz};
+  const ldm tc[3] = {(ix + 0.5L) / B.nx, (iy + 0.5L) / m.spec.ny, (iz + 0.5L) / m.spec.nz};
+  const ldm A = m.spec.warp;
+  const ldm sp = sinpi_exact<ldm>(t[0]), sy = sinpi_exact<ldm>(2.0L * t[1]), sz = sinpi_exact<ldm>(2.0L * t[2]);
+  const ldm cp = sinpi_exact<ldm>(tc[0]), cy = sinpi_exact<ldm>(2.0L * tc[1]), cz = sinpi_exact<ldm>(2.0L * tc[2]);
+  x[0] = 0.5L * xi * h[0] + A * h[0] * (sp * sy * sz - cp * cy * cz);
+  x[1] = 0.5L * eta * h[1] + A * h[1] * (sp * sz - cp * cz);
+  x[2] = 0.5L * zeta * h[2] + A * h[2] * (sp * sy - cp * cy);
+}
+
+// Metric terms of one element (conservative curl form, Kopriva 2006):
+//   Ja^i_c = -e_i . curl_xi( X_l grad_xi X_m ),  (c, m, l) cyclic,
+// on the degree-N LGL interpolant, in long double.  JaL: LGL grid values
+// [9][n^3] ([3 i + c]), dXL: dX_c/dxi_d [9][n^3] ([3 d + c]).
+struct ElemMetricBuilder {
+  int n, n3;
+  Basis lgl;
+  std::vector<ldm> DL, L;  // LGL differentiation; LGL -> solution interpolation L[s][p]
+  ElemMetricBuilder(const Basis& sol) : n(sol.n), n3(sol.n * sol.n * sol.n), lgl(sol.degree, SDG_NODES_LGL) {
+    DL.assign(lgl.D.begin(), lgl.D.end());
+    std::vector<double> row(n);
+    L.resize(static_cast<size_t>(n) * n);
+    for (int a = 0; a < n; ++a) {
+      lgl.lagrange(sol.x[a], row.data());
+      for (int p = 0; p < n; ++p) L[a * n + p] = row[p];
+    }
+  }
+  int idx(int p, int q, int r) const { return (p * n + q) * n + r; }
+  void deriv(const ldm* f, int d, ldm* out) const {
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          const int row = d == 0 ? p : (d == 1 ? q : r);
+          ldm acc = 0.0L;
+          for (int m = 0; m < n; ++m)
+            acc += DL[row * n + m] * f[d == 0 ? idx(m, q, r) : (d == 1 ? idx(p, m, r) : idx(p, q, m))];
+          out[idx(p, q, r)] = acc;
+        }
+  }
+  void interp3(const ldm* f, ldm* out) const {
+    std::vector<ldm> t1(n3), t2(n3);
+    for (int a = 0; a < n; ++a)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          ldm acc = 0.0L;
+          for (int p = 0; p < n; ++p) acc += L[a * n + p] * f[idx(p, q, r)];
+          t1[idx(a, q, r)] = acc;
+        }
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b)
+        for (int r = 0; r < n; ++r) {
+          ldm acc = 0.0L;
+          for (int q = 0; q < n; ++q) acc += L[b * n + q] * t1[idx(a, q, r)];
+          t2[idx(a, b, r)] = acc;
+        }
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b)
+        for (int c = 0; c < n; ++c) {
+          ldm acc = 0.0L;
+          for (int r = 0; r < n; ++r) acc += L[c * n + r] * t2[idx(a, b, r)];
+          out[idx(a, b, c)] = acc;
+        }
+  }
+  void build(const MeshGeom& m, int b, int ix, int iy, int iz, std::vector<ldm>& JaL, std::vector<ldm>& dXL) const {
+    std::vector<ldm> X(3 * n3), V(3 * n3), dV(n3);
+    JaL.assign(9 * n3, 0.0L);
+    dXL.assign(9 * n3, 0.0L);
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          ldm x[3];
+          relative_point(m, b, ix, iy, iz, lgl.x[p], lgl.x[q], lgl.x[r], x);
+          for (int c = 0; c < 3; ++c) X[c * n3 + idx(p, q, r)] = x[c];
+        }
+    for (int d = 0; d < 3; ++d)
+      for (int c = 0; c < 3; ++c) deriv(X.data() + c * n3, d, dXL.data() + (3 * d + c) * n3);
+    for (int c = 0; c < 3; ++c) {
+      const int mm = (c + 1) % 3, l = (c + 2) % 3;
+      for (int d = 0; d < 3; ++d)
+        for (int g = 0; g < n3; ++g) V[d * n3 + g] = X[l * n3 + g] * dXL[(3 * d + mm) * n3 + g];
+      for (int i = 0; i < 3; ++i) {
+        const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+        ldm* out = JaL.data() + (3 * i + c) * n3;
+        deriv(V.data() + i2 * n3, i1, dV.data());
+        for (int g = 0; g < n3; ++g) out[g] = -dV[g];
+        deriv(V.data() + i1 * n3, i2, dV.data());
+        for (int g = 0; g < n3; ++g) out[g] += dV[g];
+      }
+    }
+  }
+  // Unit +xi_d normal and sJ at the solution face nodes of `side`, from the
+  // face's own geometry only: the normal component of the curl needs the
+  // tangential derivatives on the face layer alone.  A face's two slots are
+  // filled from the same element and side, so they hold identical bits.
+  void face(const MeshGeom& m, int b, int ix, int iy, int iz, int side, double* out) const {
+    const int d = side / 2;
+    const double lay = (side & 1) ? 1.0 : -1.0;
+    const int p1 = d == 0 ? 1 : 0, p2 = d == 2 ? 1 : 2;  // face index (a, b) runs along (p1, p2)
+    const int n2 = n * n;
+    std::vector<ldm> X(3 * n2), D1(3 * n2), D2(3 * n2), V1(n2), V2(n2), J(3 * n2);
+    for (int u = 0; u < n; ++u)
+      for (int v = 0; v < n; ++v) {
+        double r[3];
+        r[d] = lay;
+        r[p1] = lgl.x[u];
+        r[p2] = lgl.x[v];
+        ldm x[3];
+        relative_point(m, b, ix, iy, iz, r[0], r[1], r[2], x);
+        for (int c = 0; c < 3; ++c) X[c * n2 + u * n + v] = x[c];
+      }
+    auto du = [&](const ldm* f, ldm* o) {
+      for (int u = 0; u < n; ++u)
+        for (int v = 0; v < n; ++v) {
+          ldm acc = 0.0L;
+          for (int q = 0; q < n; ++q) acc += DL[u * n + q] * f[q * n + v];
+          o[u * n + v] = acc;
+        }
+    };
+    auto dv = [&](const ldm* f, ldm* o) {
+      for (int u = 0; u < n; ++u)
+        for (int v = 0; v < n; ++v) {
+          ldm acc = 0.0L;
+          for (int q = 0; q < n; ++q) acc += DL[v * n + q] * f[u * n + q];
+          o[u * n + v] = acc;
+        }
+    };
+    for (int c = 0; c < 3; ++c) {
+      du(X.data() + c * n2, D1.data() + c * n2);
+      dv(X.data() + c * n2, D2.data() + c * n2);
+    }
+    // (curl V)_d = d_{p1} V_{p2} - d_{p2} V_{p1} for d = 0, 2 and its negative for d = 1.
+    const ldm sgn = d == 1 ? -1.0L : 1.0L;
+    std::vector<ldm> a1(n2), a2(n2);
+    for (int c = 0; c < 3; ++c) {
+      const int mm = (c + 1) % 3, l = (c + 2) % 3;
+      for (int g = 0; g < n2; ++g) {
+        V1[g] = X[l * n2 + g] * D1[mm * n2 + g];
+        V2[g] = X[l * n2 + g] * D2[mm * n2 + g];
+      }
+      du(V2.data(), a1.data());
+      dv(V1.data(), a2.data());
+      for (int g = 0; g < n2; ++g) J[c * n2 + g] = -sgn * (a1[g] - a2[g]);
+    }
+    for (int a = 0; a < n; ++a)
+      for (int bb = 0; bb < n; ++bb) {
+        ldm v[3];
+        for (int c = 0; c < 3; ++c) {
+          ldm acc = 0.0L;
+          for (int u = 0; u < n; ++u) {
+            ldm inner = 0.0L;
+            for (int w = 0; w < n; ++w) inner += L[bb * n + w] * J[c * n2 + u * n + w];
+            acc += L[a * n + u] * inner;
+          }
+          v[c] = acc;
+        }
+        const ldm sj = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        double* q = out + (a * n + bb) * 4;
+        for (int c = 0; c < 3; ++c) q[c] = static_cast<double>(v[c] / sj);
+        q[3] = static_cast<double>(sj);
+      }
+  }
+};
+}  // namespace
+
+CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTopology& topo) {
+  const int n = sol.n, n2 = n * n, n3 = n2 * n;
+  const int ne = static_cast<int>(topo.gids.size());
+  CurvedMetrics out;
+  out.met.assign(static_cast<size_t>(ne) * n3 * 10, 0.0);
+  out.fmet.assign(static_cast<size_t>(ne) * 6 * n2 * 4, 0.0);
+  const ElemMetricBuilder mb(sol);
+  // Elements are independent: split them over the host threads (setup only).
+  auto work = [&](int e_lo, int e_hi, std::string* err) {
+    try {
+      std::vector<ldm> JaL, dXL, Ja(9 * n3), dX(9 * n3);
+      for (int e = e_lo; e < e_hi; ++e) {
+        const int* c = topo.coords.data() + 4 * e;
+        mb.build(m, c[0], c[1], c[2], c[3], JaL, dXL);
+        for (int q = 0; q < 9; ++q) {
+          mb.interp3(JaL.data() + q * n3, Ja.data() + q * n3);
+          mb.interp3(dXL.data() + q * n3, dX.data() + q * n3);
+        }
+        for (int g = 0; g < n3; ++g) {
+          double* o = out.met.data() + (static_cast<size_t>(e) * n3 + g) * 10;
+          for (int q = 0; q < 9; ++q) o[q] = static_cast<double>(Ja[q * n3 + g]);
+          const ldm a00 = dX[0 * n3 + g], a01 = dX[1 * n3 + g], a02 = dX[2 * n3 + g];
+          const ldm a10 = dX[3 * n3 + g], a11 = dX[4 * n3 + g], a12 = dX[5 * n3 + g];
+          const ldm a20 = dX[6 * n3 + g], a21 = dX[7 * n3 + g], a22 = dX[8 * n3 + g];
+          const ldm jac = a00 * (a11 * a22 - a12 * a21) - a01 * (a10 * a22 - a12 * a20) + a02 * (a10 * a21 - a11 * a20);
+          if (!(jac > 0.0L)) throw ConfigError("curved mapping has a non-positive Jacobian (warp too large)");
+          o[9] = static_cast<double>(1.0L / jac);
+        }
+        for (int side = 0; side < 6; ++side) {
+          double* o = out.fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4;
+          const Nbr nb = neighbour(m, c[0], c[1], c[2], c[3], side);
+          if ((side & 1) == 0 && nb.kind == 0) {
+            // Minus side of a conforming face: the face's metrics are those of the
+            // minus element (whose plus side it is), bit for bit, on every rank.
+            mb.face(m, nb.band, nb.ix, nb.iy, nb.iz, nb.side, o);
+          } else {
+            mb.face(m, c[0], c[1], c[2], c[3], side, o);
+          }
+        }
+      }
+    } catch (const std::exception& ex) {
+      *err = ex.what();
+    }
+  };
+  const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()), (ne + 63) / 64));
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(nt);
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back(work, static_cast<int>(static_cast<long>(ne) * t / nt),
+                      static_cast<int>(static_cast<long>(ne) * (t + 1) / nt), &errs[t]);
+  for (auto& th : pool) th.join();
+  for (const auto& e : errs)
+    if (!e.empty()) throw ConfigError(e);
+  return out;
 }
 
 // ---------------------------------------------------------------- basis

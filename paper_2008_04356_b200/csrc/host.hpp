@@ -114,6 +114,19 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
 std::array<int, 2> interior_run(const LocalTopology& topo);
 
 // Nodal basis (proj/src/nodal_basis.cpp:89-182, same published algorithm).
+struct Basis;
+// Mapped position (SDG_MAP_WARP, include/sdg_types.h; the box otherwise) of a
+// reference point of element (b, ix, iy, iz) at time t.
+void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, double eta, double zeta, double t,
+               double* x);
+// Curved metric terms of the local elements (SDG_MAP_WARP): met E x N3 x 10
+// (Ja^d_c at [3d + c], 1/J), fmet 6E x N2 x 4 (unit +xi_dir normal, sJ) per local
+// side; a conforming face carries the minus element's values in both slots.
+struct CurvedMetrics {
+  std::vector<double> met, fmet;
+};
+CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTopology& topo);
+
 struct Basis {
   int degree = 0, kind = SDG_NODES_GAUSS, n = 0;
   std::vector<double> x, w, bary, D, fl, fr;

@@ -247,19 +247,42 @@ __device__ void eval_case(const sdg_case& cs, const double* x, double t, const G
   u[4] = p / g.gm1 + 0.5 * rho * (v0 * v0 + v1 * v1 + v2 * v2);
 }
 
-// Physical position of face node (a, b) of `side` at time t (mesh.cpp:118-122).
+// sin(pi t), exactly 0 at integer t (the warp vanishes on band boundaries).
+__device__ __forceinline__ double sinpi_exact(double t) {
+  double r = fmod(t, 2.0);
+  if (r < 0.0) r += 2.0;
+  return (r == 0.0 || r == 1.0) ? 0.0 : sinpi(r);
+}
+
+// Physical position of reference point (xi, eta, zeta) of an element at time t
+// (mesh.cpp:118-122; SDG_MAP_WARP adds the curved warp of include/sdg_types.h).
+__device__ __forceinline__ void map_position(const ElemConsts& C, const int* crd, double xi, double eta, double zeta,
+                                             double t, double* x) {
+  const BandD& B = C.bands[crd[0]];
+  x[0] = (B.x_lo + crd[1] * B.hx) + 0.5 * (xi + 1.0) * B.hx;
+  x[1] = (C.y0 + crd[2] * B.hy) + 0.5 * (eta + 1.0) * B.hy;
+  x[2] = (C.z0 + crd[3] * B.hz) + 0.5 * (zeta + 1.0) * B.hz;
+  if (C.mapping == SDG_MAP_WARP) {
+    const double tx = (crd[1] + 0.5 * (xi + 1.0)) / B.nxd, ty = (crd[2] + 0.5 * (eta + 1.0)) / C.ny,
+                 tz = (crd[3] + 0.5 * (zeta + 1.0)) / C.nz;
+    const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
+    x[0] += C.warp * B.hx * sp * sy * sz;
+    x[1] += C.warp * B.hy * sp * sz;
+    x[2] += C.warp * B.hz * sp * sy;
+  }
+  x[1] += B.vg * t;
+}
+
+// Physical position of face node (a, b) of `side` at time t.
 template <int N1>
 __device__ __forceinline__ void face_position(const ElemConsts& C, const int* crd, int side, int a, int b, double t,
                                               double* x) {
-  const BandD& B = C.bands[crd[0]];
   const int dir = side >> 1;
   const double pm = (side & 1) ? 1.0 : -1.0;
   const double xi = dir == 0 ? pm : C.x[a];
   const double eta = dir == 1 ? pm : (dir == 0 ? C.x[a] : C.x[b]);
   const double zeta = dir == 2 ? pm : C.x[b];
-  x[0] = (B.x_lo + crd[1] * B.hx) + 0.5 * (xi + 1.0) * B.hx;
-  x[1] = (C.y0 + crd[2] * B.hy) + 0.5 * (eta + 1.0) * B.hy + B.vg * t;
-  x[2] = (C.z0 + crd[3] * B.hz) + 0.5 * (zeta + 1.0) * B.hz;
+  map_position(C, crd, xi, eta, zeta, t, x);
 }
 
 template <int N1>
@@ -1131,16 +1154,14 @@ __global__ void __launch_bounds__(256) k_diag(const __grid_constant__ ElemConsts
     const int i = r / N2, j = (r / N1) % N1, k = r % N1;
     const int* crd = P.coords + 4 * e;
     const BandD& B = C.bands[crd[0]];
-    const double wq = C.w[i] * C.w[j] * C.w[k] * B.jac;
+    const double wq = C.w[i] * C.w[j] * C.w[k] * (C.mapping == SDG_MAP_WARP ? 1.0 / P.met[nd * 10 + 9] : B.jac);
     const double* u = P.U + nd * 5;
     a[0] += wq * u[0];
     a[1] += wq * u[4];
     a[2] += wq;
     if (with_exact) {
       double x[3], ex[5];
-      x[0] = (B.x_lo + crd[1] * B.hx) + 0.5 * (C.x[i] + 1.0) * B.hx;
-      x[1] = (C.y0 + crd[2] * B.hy) + 0.5 * (C.x[j] + 1.0) * B.hy + B.vg * t;
-      x[2] = (C.z0 + crd[3] * B.hz) + 0.5 * (C.x[k] + 1.0) * B.hz;
+      map_position(C, crd, C.x[i], C.x[j], C.x[k], t, x);
       eval_case(C.flow_case, x, t, C.gas, ex);
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
@@ -3156,6 +3177,8 @@ void mortar_back_t(int nc, const double* const src[2], double* dst, const Mortar
   check_launch("k_mortar_backproject");
 }
 
+#include "curved.cuh"
+
 #define SDG_DISPATCH(n1, CALL)                          \
   switch (n1) {                                         \
     case 2: { constexpr int NN = 2; CALL; break; }      \
@@ -3213,6 +3236,14 @@ bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const St
   }
   SDG_DISPATCH(n1, (ok = update_tma_t<NN>(c, p, a, n_sm, st)));
   return ok;
+}
+void launch_gradient_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (p.E <= p.e_first) return;
+  SDG_DISPATCH(n1, (gradient_curved_t<NN>(c, p, a, st)));
+}
+void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (p.E <= p.e_first) return;
+  SDG_DISPATCH(n1, (update_curved_t<NN>(c, p, a, st)));
 }
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
   k_pairing<<<2, kPairThreads, 0, st>>>(a, p);

@@ -20,6 +20,7 @@ struct BandD {
   double jac, inv_jac;
   double cdir[3];  // sJ_d / J
   double sj[3];    // sJ_d
+  double nxd;      // elements along x (curved mapping)
 };
 
 // Per-run constants, passed by value (__grid_constant__) to every element kernel.
@@ -34,6 +35,8 @@ struct ElemConsts {
   GasD gas;
   double y0, z0;
   sdg_case flow_case;
+  int mapping, ny, nz, pad;  // SDG_MAP_BOX / SDG_MAP_WARP (include/sdg_types.h)
+  double warp;
 };
 
 // Deferred admissibility / protocol error record (written by the first failing thread).
@@ -61,6 +64,8 @@ struct FieldPtrs {
   const int* coords;         // E x 4 (band, ix, iy, iz)
   const int* side_code;      // E x 8: idx | type << 29 for the 6 sides, [6] = band, [7] pad (32 B/element)
   double* grad_out;          // optional E x N3 x 12
+  const double* met;         // curved: E x N3 x 10 (Ja^d_c at 3d + c, 1/J)
+  const double* fmet;        // curved: 6E x N2 x 4 (unit +xi normal, sJ) per local side
   ErrRec* err;
   int E;        // element kernels process local elements [e_first, E)
   int e_first;  // (interior / boundary split for exchange overlap; 0 = all)
@@ -152,6 +157,9 @@ bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const 
                          cudaStream_t st);
 bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                        cudaStream_t st);
+// Curved-element kernels (SDG_MAP_WARP; csrc/curved.cuh).
+void launch_gradient_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);

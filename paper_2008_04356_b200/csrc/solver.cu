@@ -375,6 +375,9 @@ class GpuRankSolver {
   int sm_reserve_ = 0;  // SMs left free for the NCCL kernels while the interior run computes
 
   DevBuf<double> U_, reg_, dudt_, trace_[2], fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
+  // Curved elements (SDG_MAP_WARP): per-node metrics and per-side face metrics (host.cpp compute_metrics).
+  bool curved_ = false;
+  DevBuf<double> met_, fmet_;
   DevBuf<int8_t> side_type_;
   DevBuf<int> side_idx_, coords_, side_code_;
   int n_sm_ = 148;
@@ -504,7 +507,12 @@ void GpuRankSolver::build_consts() {
     d.sj[1] = 0.25 * bg.hx * bg.hz;
     d.sj[2] = 0.25 * bg.hx * bg.hy;
     for (int q = 0; q < 3; ++q) d.cdir[q] = d.sj[q] / jac;
+    d.nxd = bg.nx;
   }
+  consts_.mapping = mesh_.spec.mapping;
+  consts_.ny = mesh_.spec.ny;
+  consts_.nz = mesh_.spec.nz;
+  consts_.warp = mesh_.spec.mapping == SDG_MAP_WARP ? mesh_.spec.warp : 0.0;
   const auto& g = cfg_.gas;
   consts_.gas = {g.gamma, g.gamma - 1.0, g.R, 1.0 / g.R, g.mu, -2.0 / 3.0 * g.mu,
                  g.gamma * g.R * g.mu / ((g.gamma - 1.0) * g.Pr), g.mu > 0.0 ? 1 : 0};
@@ -544,6 +552,13 @@ void GpuRankSolver::upload_topology() {
     side_code_.upload(code, stream_);
   }
   coords_.upload(topo_.coords, stream_);
+  curved_ = mesh_.spec.mapping == SDG_MAP_WARP;
+  if (curved_) {
+    const CurvedMetrics cm = compute_metrics(mesh_, basis_, topo_);
+    met_.upload(cm.met, stream_);
+    fmet_.upload(cm.fmet, stream_);
+    cuda_check(cudaStreamSynchronize(stream_), "metric upload");
+  }
   err_.alloc(1);
   err_.zero(stream_);
   dt_min_.alloc(1);
@@ -725,14 +740,11 @@ void GpuRankSolver::set_initial_condition(double t0) {
   for (int e = 0; e < E_; ++e) {
     const int b = topo_.coords[4 * e], ix = topo_.coords[4 * e + 1], iy = topo_.coords[4 * e + 2],
               iz = topo_.coords[4 * e + 3];
-    const BandGeom& B = mesh_.bands[b];
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j)
         for (int k = 0; k < n; ++k) {
           double x[3];
-          x[0] = (B.x_lo + ix * B.hx) + 0.5 * (basis_.x[i] + 1.0) * B.hx;
-          x[1] = (mesh_.spec.y0 + iy * B.hy) + 0.5 * (basis_.x[j] + 1.0) * B.hy + B.vg * t0;
-          x[2] = (mesh_.spec.z0 + iz * B.hz) + 0.5 * (basis_.x[k] + 1.0) * B.hz;
+          map_point(mesh_, b, ix, iy, iz, basis_.x[i], basis_.x[j], basis_.x[k], t0, x);
           eval_case_host(cfg_.flow_case, cfg_.gas, x, t0, h.data() + ((static_cast<size_t>(e) * n3_) + (i * n + j) * n + k) * 5);
         }
   }
@@ -777,6 +789,8 @@ FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
   p.coords = coords_.p;
   p.side_code = side_code_.p;
   p.grad_out = nullptr;
+  p.met = met_.p;
+  p.fmet = fmet_.p;
   p.err = err_.p;
   p.E = E_;
   return p;
@@ -990,7 +1004,10 @@ void GpuRankSolver::element_kernel(bool update, const FieldPtrs& fp0, const Stag
   fp.e_first = e_first;
   fp.E = e_end;
   mark(update ? KC_UPDATE : KC_GRADIENT, true);
-  if (update) {
+  if (curved_) {
+    if (update) launch_update_curved(n_, consts_, fp, a, stream_);
+    else launch_gradient_curved(n_, consts_, fp, a, stream_);
+  } else if (update) {
     if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm, stream_))) launch_update(n_, consts_, fp, a, stream_);
   } else {
     if (!(use_tma_ && launch_gradient_tma(n_, consts_, fp, a, n_sm, stream_)))
@@ -1802,6 +1819,22 @@ int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta
       std::strncpy(buf, j.c_str(), static_cast<size_t>(cap) - 1);
       buf[cap - 1] = 0;
     }
+  });
+}
+int sdg_metrics_host(const sdg_mesh_spec* mesh, int degree, int node_kind, int n_ranks, int rank, double* met,
+                     double* fmet, long* n_local) {
+  return guarded(nullptr, [&] {
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) throw sdg::ConfigError("rank outside [0, n_ranks)");
+    const sdg::MeshGeom m(*mesh);
+    if (mesh->mapping != SDG_MAP_WARP) throw sdg::ConfigError("metrics are stored for curved meshes only");
+    const sdg::Partition part = sdg::assign_ranks(m, n_ranks);
+    const sdg::LocalTopology topo = sdg::build_topology(m, part, rank);
+    *n_local = static_cast<long>(topo.gids.size());
+    if (met == nullptr || fmet == nullptr) return;
+    const sdg::Basis basis(degree, node_kind);
+    const sdg::CurvedMetrics cm = sdg::compute_metrics(m, basis, topo);
+    std::copy(cm.met.begin(), cm.met.end(), met);
+    std::copy(cm.fmet.begin(), cm.fmet.end(), fmet);
   });
 }
 int sdg_diagnostics(sdg_ctx* c, double t, int with_exact, double* out) {

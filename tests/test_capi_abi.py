@@ -48,4 +48,4 @@ def test_struct_layout_matches_header():
     # sizes follow include/sdg_types.h field order (x86-64 ABI)
     assert ctypes.sizeof(T.BandSpec) == 24
     assert ctypes.sizeof(T.Gas) == 32
-    assert ctypes.sizeof(T.MeshSpec) == 6 * 8 + 3 * 4 + 4 + 16 * 24 + 4 * 4
+    assert ctypes.sizeof(T.MeshSpec) == 6 * 8 + 3 * 4 + 4 + 16 * 24 + 4 * 4 + 4 + 4 + 8

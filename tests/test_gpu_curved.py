@@ -1,0 +1,148 @@
+"""Curved hexahedra (SDG_MAP_WARP) on the CUDA path vs the CPU oracle, through
+the C-ABI (k_gradient_curved / k_update_curved, csrc/curved.cuh).
+
+Same tolerances as tests/test_gpu_parity.py: state relative Linf <= 1e-12
+after one stage / step, <= 1e-10 after 100 stages; free stream <= 1e-12.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_linf
+from oracle import pyoracle as P
+from paper_2008_04356_b200 import types as T
+
+pytestmark = pytest.mark.gpu
+
+BANDS3 = [(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)]
+
+
+def gpu_solver(mesh, cfg):
+    from paper_2008_04356_b200.capi import RankSolver
+    return RankSolver(mesh, cfg)
+
+
+def warped3(ny=4, nz=3, warp=0.2, periodic=(True, True, True), nx=2):
+    return T.mesh_spec([(nx, 1.0, 0.0), (nx, 1.0, 1.0), (nx, 1.0, 0.0)], ny=ny, nz=nz, depth=1.0, warp=warp,
+                       periodic=periodic)
+
+
+def box0_warped(n_per=2, warp=0.2):
+    """BASELINE config [0] geometry with curved elements (Dirichlet across the split axis)."""
+    return T.mesh_spec([(n_per, 1.0, 0.0), (n_per, 1.0, 0.5)], ny=n_per, nz=n_per, periodic=(False, True, True),
+                       warp=warp)
+
+
+CASES = {
+    "w3_gauss_visc": (warped3(), dict(degree=3, node_kind=T.NODES_GAUSS, mu=1e-3)),
+    "w3_lgl_inv": (warped3(), dict(degree=3, node_kind=T.NODES_LGL, mu=0.0)),
+    "box0w_gauss_visc_n5": (box0_warped(), dict(degree=5, node_kind=T.NODES_GAUSS, mu=1e-3)),
+    "box0w_lgl_visc": (box0_warped(), dict(degree=4, node_kind=T.NODES_LGL, mu=1e-3)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("t", [0.0, 0.37])
+def test_curved_residual_matches_oracle(name, t):
+    mesh, kw = CASES[name]
+    cfg = T.solver_config(case=T.density_wave(a=(1.0, 1.0, 0.5)), **kw)
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    g.set_initial_condition(0.0)
+    assert rel_linf(g.field(), o.field()) <= 1e-15
+    u = o.field()
+    assert rel_linf(g.compute_residual(t, u), o.compute_residual(t, u)) <= 1e-12
+
+
+@pytest.mark.parametrize("degree", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("kind", [T.NODES_LGL, T.NODES_GAUSS])
+def test_curved_all_degrees_one_step(degree, kind):
+    mesh = warped3(ny=3, nz=2, periodic=(False, True, True))
+    cfg = T.solver_config(degree, kind, mu=1e-3, case=T.density_wave(a=(1.0, 1.0, 0.5)))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.4)
+    g.step(dt)
+    o.step(dt)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+def test_curved_gradients_match_oracle():
+    mesh, kw = CASES["box0w_gauss_visc_n5"]
+    cfg = T.solver_config(case=T.density_wave(a=(1.0, 1.0, 0.5)), **kw)
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    u = o.field()
+    assert rel_linf(g.compute_gradients(0.2, u), o.compute_gradients(0.2, u)) <= 1e-12
+
+
+def test_curved_hundred_stages():
+    mesh = box0_warped(2, warp=0.25)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 20)
+    o.step(dt, 20)
+    assert rel_linf(g.field(), o.field()) <= 1e-10
+    assert g.total_rebuilds() == o.total_rebuilds()
+
+
+@pytest.mark.parametrize("kind", [T.NODES_LGL, T.NODES_GAUSS])
+def test_curved_freestream_preserved_across_sliding(kind):
+    mesh = warped3(ny=6, nz=3)
+    cfg = T.solver_config(3, kind, mu=1e-3, case=T.freestream(v=(1.0, 0.5, 0.25)))
+    g = gpu_solver(mesh, cfg)
+    g.set_initial_condition(0.0)
+    u = g.field()
+    for t in (0.0, 0.05, 1.0 / 3.0, 0.37, 0.99, 2.0):
+        assert np.abs(g.compute_residual(t, u)).max() < 1e-12
+    g.step(g.suggest_dt(0.5), 10)
+    assert g.diagnostics(g.time())["max_deviation"] < 1e-12
+
+
+def test_curved_conservation_and_diagnostics():
+    mesh = warped3(ny=6, nz=2, warp=0.25)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave(a=(1.0, 1.0, 0.5)))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    d0 = g.diagnostics(0.0)
+    me0 = o.mass_energy(g.field())
+    assert abs(d0["mass"] - me0[0]) <= 1e-13 * abs(me0[0])
+    assert abs(d0["volume"] - 4.0) <= 1e-12  # [0,2] x [0,2] x [0,1]: the warp preserves the volume
+    g.step(g.suggest_dt(0.4), 10)
+    d1 = g.diagnostics(g.time())
+    assert abs(d1["mass"] - d0["mass"]) <= 1e-12 * abs(d0["mass"])
+    assert abs(d1["energy"] - d0["energy"]) <= 1e-12 * abs(d0["energy"])
+
+
+@pytest.mark.parametrize("ranks,partition", [(3, T.PARTITION_LEX), (6, T.PARTITION_SFC)])
+def test_curved_rank_counts_do_not_change_the_bits(ranks, partition):
+    from paper_2008_04356_b200 import capi
+    mesh = T.mesh_spec(BANDS3, ny=6, nz=2, depth=1.0, partition=partition, warp=0.2)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    n_el = 2 * 6 * 2 * 3
+
+    def body(s):
+        s.set_initial_condition(0.0)
+        s.step(0.004, 5)
+        return s.local_element_ids(), s.field()
+
+    ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub="c1"), n_el, 4)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"c{ranks}p{partition}"), n_el, 4)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
+
+
+def test_curved_multi_wave_mesh_matches_oracle():
+    """More element tiles than resident CTAs (the double-buffered trace path)."""
+    mesh = T.mesh_spec([(6, 1.0, 0.0), (6, 1.0, 0.5), (6, 1.0, 0.0)], ny=8, nz=8, warp=0.1)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave(a=(1.0, 1.0, 0.5)))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.4)
+    g.step(dt, 2)
+    o.step(dt, 2)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
