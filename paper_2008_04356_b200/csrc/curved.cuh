@@ -518,3 +518,502 @@ void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a
   }
   check_launch("k_update_curved");
 }
+
+// ============================================================================
+// Bulk-loaded curved kernels (even N+1: every per-element and per-slot block is
+// a multiple of 16 bytes).  One thread issues cp.async.bulk copies of
+// everything the element tile reads — state, metrics, face metrics, its own
+// face traces (and Fv.n), and per side the neighbour's trace + Fv.n slot (or
+// the sliding face's back-projected flux + lift*) — completing on one
+// mbarrier, so the tile's global reads are in flight together instead of as
+// dependent load chains (ncu: 50% long-scoreboard stalls in the kernels above).
+// Own traces are staged from the trace buffer, so both elements of a face use
+// the same stored bits.  The RK register is prefetched into L2.
+// ============================================================================
+template <int N1>
+struct CB {
+  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  static constexpr int EPB = N1 == 2 ? 16 : CDim<N1>::EPB;  // shared memory: <= 227 KB per CTA
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int TAB = Dim<N1>::TAB;
+  static constexpr int EL = 5 * N3, ML = 10 * N3, FM = 24 * N2, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
+  // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
+  static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB + 5 * N3 + 24 * N2 + 30 * N2;
+  // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
+  static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 12 * N3 + 24 * N2;
+  static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
+  static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
+  static_assert(N1 % 2 == 0, "bulk path needs even N+1");
+  static_assert(U_SMEM <= 227 * 1024 && G_SMEM <= 227 * 1024, "shared memory per CTA");
+};
+
+// Gradient at one node from AoS metrics sM[node][10] and SoA q.
+template <int N1>
+__device__ __forceinline__ void node_gradient_curved_aos(const double* tab, const double* sq, const double* sM,
+                                                         const double* sLift, const double* sfm, int i, int j, int k,
+                                                         double* g) {
+  constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  const double* dh = tab;
+  const double* lw = tab + N1 * N1 + 2 * N1;
+  double acc[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int ia = d == 0 ? i : (d == 1 ? j : k);
+    const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+    const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      const double c = dh[ia * N1 + m];
+      const int nd = base + m * stride;
+      const double* ja = sM + nd * 10 + 3 * d;
+      const double ja0 = ja[0], ja1 = ja[1], ja2 = ja[2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double cq = c * sq[q * N3 + nd];
+        acc[3 * q + 0] += cq * ja0;
+        acc[3 * q + 1] += cq * ja1;
+        acc[3 * q + 2] += cq * ja2;
+      }
+    }
+  }
+  const double ij = sM[((i * N1 + j) * N1 + k) * 10 + 9];
+  double surf[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) surf[q] = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int ia = d == 0 ? i : (d == 1 ? j : k);
+    const int f = d == 0 ? j * N1 + k : (d == 1 ? i * N1 + k : i * N1 + j);
+    const double* np = sfm + ((2 * d + 1) * N2 + f) * 4;
+    const double* nm = sfm + ((2 * d) * N2 + f) * 4;
+    const double sp = lw[N1 + ia] * np[3], sm = lw[ia] * nm[3];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double lp = sLift[((2 * d + 1) * 4 + q) * N2 + f] * sp;
+      const double lm = sLift[((2 * d) * 4 + q) * N2 + f] * sm;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) surf[3 * q + kk] += lp * np[kk] - lm * nm[kk];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) g[q] = ij * (surf[q] - acc[q]);
+}
+
+// Issue the bulk copies of one element tile (thread 0).  GRAD: neighbour
+// trace (conforming) or lift* (sliding) only; else trace + Fv.n or flux + lift*.
+template <int N1, bool GRAD, bool VISC>
+__device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, int n, double* base, int per,
+                                                   uint64_t* bar) {
+  using D = CB<N1>;
+  uint32_t bytes = n * (D::EL + D::ML + D::FM + 6 * D::TS) * 8u;
+  if (!GRAD && VISC) bytes += n * 6u * D::FS * 8u;
+  for (int le = 0; le < n; ++le)
+    for (int s = 0; s < 6; ++s) {
+      const int typ = P.side_type[(e0 + le) * 6 + s];
+      if (typ == kDirichlet) continue;
+      if (GRAD) bytes += (typ == kConforming ? D::TS : D::FS) * 8u;
+      else bytes += (D::TS + (VISC ? D::FS : 0)) * 8u;
+    }
+  mbar_arrive_expect_tx(bar, bytes);
+  for (int le = 0; le < n; ++le) {
+    const int e = e0 + le;
+    double* b = base + le * per;
+    bulk_g2s(b, P.U + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
+    bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
+    bulk_g2s(b + D::EL + D::ML, P.fmet + static_cast<size_t>(e) * D::FM, D::FM * 8u, bar);
+    double* tr = b + D::EL + D::ML + D::FM;
+    bulk_g2s(tr, P.trace + static_cast<size_t>(e) * 6 * D::TS, 6 * D::TS * 8u, bar);
+    double* fv = tr + 6 * D::TS;
+    double* nb = GRAD ? fv : fv + 6 * D::FS;
+    if (!GRAD && VISC) bulk_g2s(fv, P.fvn + static_cast<size_t>(e) * 6 * D::FS, 6 * D::FS * 8u, bar);
+    for (int s = 0; s < 6; ++s) {
+      const int slot = e * 6 + s;
+      const int typ = P.side_type[slot], idx = P.side_idx[slot];
+      double* d = nb + s * (GRAD ? D::TS : D::NB);
+      if (typ == kConforming) {
+        bulk_g2s(d, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        if (!GRAD && VISC) bulk_g2s(d + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+      } else if (typ == kSliding) {
+        if (GRAD) {
+          bulk_g2s(d, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+        } else {
+          bulk_g2s(d, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+          if (VISC) bulk_g2s(d + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+        }
+      }
+    }
+  }
+}
+
+template <int N1>
+__global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
+                                                                       FieldPtrs P, StageArgs A) {
+  using D = CB<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::G_PER;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* base = smem + D::TAB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + EPB * PER);
+  const int e0 = P.e_first + blockIdx.x * EPB;
+  const int n_el = min(EPB, P.E - e0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+    curved_issue_loads<N1, true, true>(P, e0, n_el, base, PER, bar);
+  }
+  load_tables<N1>(C, tab);
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = le < n_el;
+  double* sU = base + le * PER;
+  double* sM = sU + D::EL;
+  double* sfm = sM + D::ML;
+  double* sTr = sfm + D::FM;
+  double* sNb = sTr + 6 * D::TS;
+  double* sq = sNb + 6 * D::TS;
+  double* sG = sq + 4 * N3;
+  double* sLift = sG + 12 * N3;
+  __syncthreads();  // barrier init visible, tables loaded
+  mbar_wait(bar, 0);
+  if (active) {
+    double q[4];
+    prim4(sU + t * 5, C.gas, q);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sq[c * N3 + t] = q[c];
+    // BR1 surface values lift* (run_lifting, solver.cpp:606-723).
+    for (int it = t; it < 6 * N2; it += N3) {
+      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+      const int typ = P.side_type[e * 6 + s];
+      const double* own = sTr + s * D::TS + f * 5;
+      double lift[4];
+      if (typ == kConforming) {
+        double qa[4], qb[4];
+        prim4(own, C.gas, qa);
+        prim4(sNb + s * D::TS + f * 5, C.gas, qb);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+      } else if (typ == kSliding) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lift[c] = sNb[s * D::TS + f * 4 + c];
+      } else {
+        double x[3], ext[5];
+        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        prim4(ext, C.gas, lift);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+    }
+  }
+  __syncthreads();
+  if (active) {
+    const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+    double g[12];
+    node_gradient_curved_aos<N1>(tab, sq, sM, sLift, sfm, i, j, k, g);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
+    if (P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = g[c];
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double gt[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+    const int slot = e * 6 + s;
+    const int typ = P.side_type[slot], idx = P.side_idx[slot];
+    if (typ == kConforming) {
+      double fv[4];
+      fv_n(sTr + s * D::TS + f * 5, gt, sfm + (s * N2 + f) * 4, C.gas, fv);
+      double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dst[c] = fv[c];
+    } else {
+      double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+    }
+  }
+}
+
+template <int N1, bool VISC>
+__global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __grid_constant__ ElemConsts C,
+                                                                     FieldPtrs P, StageArgs A) {
+  using D = CB<N1>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::U_PER;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* base = smem + D::TAB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + EPB * PER);
+  const int e0 = P.e_first + blockIdx.x * EPB;
+  const int n_el = min(EPB, P.E - e0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+    curved_issue_loads<N1, false, VISC>(P, e0, n_el, base, PER, bar);
+    if (A.mode == 0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
+  }
+  load_tables<N1>(C, tab);
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = le < n_el;
+  double* sU = base + le * PER;
+  double* sM = sU + D::EL;
+  double* sfm = sM + D::ML;
+  double* sTr = sfm + D::FM;
+  double* sFv = sTr + 6 * D::TS;
+  double* sNb = sFv + 6 * D::FS;
+  double* sF = sNb + 6 * D::NB;
+  double* sLift = sF + 5 * N3;
+  double* sFlux = sLift + 24 * N2;
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  __syncthreads();
+  mbar_wait(bar, 0);
+
+  // Phase 1: numerical flux along each face node's normal -> sFlux; lift* -> sLift.
+  if (active) {
+    if (VISC) {
+      double q[4];
+      prim4(sU + t * 5, C.gas, q);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
+    }
+    for (int it = t; it < 6 * N2; it += N3) {
+      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+      const double* own = sTr + s * D::TS + f * 5;
+      const double* nrm = sfm + (s * N2 + f) * 4;
+      const double vgn = B.vg * nrm[1];
+      const double* nb = sNb + s * D::NB;
+      const int typ = P.side_type[e * 6 + s];
+      double flux[5], lift[4];
+      bool ok = true;
+      if (typ == kConforming) {
+        const double* other = nb + f * 5;
+        const double* um = (s & 1) ? own : other;
+        const double* up = (s & 1) ? other : own;
+        ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
+        if (VISC) {
+          double qa[4], qb[4];
+          prim4(own, C.gas, qa);
+          prim4(other, C.gas, qb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+          const double* pa = sFv + s * D::FS + f * 4;
+          const double* pb = nb + D::TS + f * 4;
+          const double* fm = (s & 1) ? pa : pb;
+          const double* fp = (s & 1) ? pb : pa;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
+        }
+      } else if (typ == kSliding) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) flux[v] = nb[f * 5 + v];
+        if (VISC) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) lift[c] = nb[D::TS + f * 4 + c];
+        }
+      } else {
+        double x[3], ext[5];
+        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        const double* um = (s & 1) ? own : ext;
+        const double* up = (s & 1) ? ext : own;
+        ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
+        if (VISC) {
+          prim4(ext, C.gas, lift);
+          const int idx = P.side_idx[e * 6 + s];
+          const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+          double gg[12];
+#pragma unroll
+          for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+          double fm[4], fp[4];
+          fv_n(um, gg, nrm, C.gas, fm);
+          fv_n(up, gg, nrm, C.gas, fp);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
+        }
+      }
+      if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = flux[v];
+      if (VISC) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // Phase 2: pointwise flux -> contravariant Ja^d . F.
+  double Ft[3][5];
+  if (active) {
+    double u[5], F[3][5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+    const double ir = rcp_nr(u[0]);
+    const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+    const double p = pressure(u, ir, C.gas);
+    const double vgv[3] = {0.0, B.vg, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      F[d][0] = u[0] * vv[d];
+      F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0);
+      F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0);
+      F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0);
+      F[d][4] = (u[4] + p) * vv[d];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) F[d][v] -= vgv[d] * u[v];
+    }
+    if (VISC) {
+      double g[12];
+      node_gradient_curved_aos<N1>(tab, sF, sM, sLift, sfm, i, j, k, g);
+      const double div = g[0] + g[4] + g[8];
+      const double mu = C.gas.mu, lam = C.gas.lam;
+      const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
+                                {mu * (g[1] + g[3]), 2.0 * mu * g[4] + lam * div, mu * (g[5] + g[7])},
+                                {mu * (g[2] + g[6]), mu * (g[5] + g[7]), 2.0 * mu * g[8] + lam * div}};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        F[d][1] -= tau[d][0];
+        F[d][2] -= tau[d][1];
+        F[d][3] -= tau[d][2];
+        F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
+      }
+    }
+    const double* ja = sM + t * 10;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) Ft[d][v] = ja[3 * d] * F[0][v] + ja[3 * d + 1] * F[1][v] + ja[3 * d + 2] * F[2][v];
+    }
+  }
+
+  // Phase 3: weak divergence per direction through the SoA staging buffer.
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double* dh = tab;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sF[v * N3 + t] = Ft[d][v];
+    }
+    __syncthreads();
+    if (active) {
+      const int ia = d == 0 ? i : (d == 1 ? j : k);
+      const int bse = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double c = dh[ia * N1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF[v * N3 + bse + m * stride];
+      }
+    }
+  }
+
+  // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
+  double du[5];
+  if (active) {
+    const double ij = sM[t * 10 + 9];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
+    const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int dir = s >> 1;
+      const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+      const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+      const double l = lw[(s & 1) * N1 + ia];
+      if (l != 0.0) {
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * 4 + 3] * ij;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) sF[t * 5 + v] = du[v];  // AoS, like the global state
+  }
+  __syncthreads();
+
+  // Phase 5: flat coalesced RK update (solver.cpp:912-917) or residual store.
+  if (A.mode == 1) {
+    for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
+      const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+      P.out[static_cast<size_t>(e0) * 5 * N3 + fI] = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS +
+                                                          6 * D::NB + r];
+    }
+    return;
+  }
+  for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
+    const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+    double* us = base + l * PER + r;
+    const double dd = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + 6 * D::NB + r];
+    const size_t g = static_cast<size_t>(e0) * 5 * N3 + fI;
+    const double rg = A.rk_a * P.reg[g] + A.dt * dd;
+    const double un = *us + A.rk_b * rg;
+    P.reg[g] = rg;
+    P.U[g] = un;
+    *us = un;
+  }
+  __syncthreads();
+  if (!active) return;
+  {
+    double w[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) w[v] = sU[t * 5 + v];
+    const double p = pressure(w, rcp_nr(w[0]), C.gas);
+    bool ok = w[0] > 0.0 && p > 0.0;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
+    if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+  }
+  for (int it = t; it < 6 * N2; it += N3) {
+    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+    const double* ell = tab + N1 * N1 + (s & 1) * N1;
+    double tr[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) tr[v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+    double* dst = P.trace_out + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dst[v] = tr[v];
+  }
+}
+
+template <int N1>
+bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = CB<N1>;
+    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    cudaFuncSetAttribute(k_gradient_curved_b<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+    k_gradient_curved_b<N1><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+    check_launch("k_gradient_curved_b");
+    return true;
+  }
+}
+template <int N1>
+bool update_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = CB<N1>;
+    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    auto kern = c.gas.viscous ? k_update_curved_b<N1, true> : k_update_curved_b<N1, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
+    kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
+    check_launch("k_update_curved_b");
+    return true;
+  }
+}

@@ -3239,11 +3239,17 @@ bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const St
 }
 void launch_gradient_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if (p.E <= p.e_first) return;
-  SDG_DISPATCH(n1, (gradient_curved_t<NN>(c, p, a, st)));
+  static const int cv = env_int("SDG_CURVED_V", 2);  // 2: bulk-loaded (even N+1), 1: plain loads
+  bool done = false;
+  if (cv == 2) SDG_DISPATCH(n1, (done = gradient_curved_b_t<NN>(c, p, a, st)));
+  if (!done) SDG_DISPATCH(n1, (gradient_curved_t<NN>(c, p, a, st)));
 }
 void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if (p.E <= p.e_first) return;
-  SDG_DISPATCH(n1, (update_curved_t<NN>(c, p, a, st)));
+  static const int cv = env_int("SDG_CURVED_V", 2);
+  bool done = false;
+  if (cv == 2) SDG_DISPATCH(n1, (done = update_curved_b_t<NN>(c, p, a, st)));
+  if (!done) SDG_DISPATCH(n1, (update_curved_t<NN>(c, p, a, st)));
 }
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
   k_pairing<<<2, kPairThreads, 0, st>>>(a, p);

@@ -1226,7 +1226,8 @@ void GpuRankSolver::compute_gradients(double t_stage, const double* d_u, double*
   ElemConsts c = consts_;
   c.gas.viscous = 1;
   StageArgs a{t_stage, 0.0, 0.0, 0.0, 1, step_index_, stage_index_};
-  launch_gradient(n_, c, fp, a, stream_);
+  if (curved_) launch_gradient_curved(n_, c, fp, a, stream_);
+  else launch_gradient(n_, c, fp, a, stream_);
   launches_ += 6;
   traces_valid_ = false;
   check_error();

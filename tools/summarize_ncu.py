@@ -42,7 +42,10 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, vals = rows[0], rows[1], rows[2:]
     return [{h: (u, v) for h, u, v in zip(hdr, units, r)} for r in vals]
@@ -50,7 +53,8 @@ def raw(rep):
 
 def summarize(tag, dof):
     lines, kernels, bytes_k = [], [], []
-    for rep in sorted(f for f in os.listdir(OUT) if f.startswith(tag + "_") and f.endswith(".ncu-rep")):
+    for rep in sorted(f for f in os.listdir(OUT)
+                      if f.startswith(tag + "_") and (f.endswith(".ncu-rep") or f.endswith("_raw.csv"))):
         for rec in raw(os.path.join(OUT, rep)):
             name = rec["Kernel Name"][1]
             lines.append(f"---- {name}")
