@@ -89,7 +89,20 @@ typedef struct {
  * its warp rigidly (+vg t along y), so the metric terms are time-invariant.
  * Metrics are the conservative curl form (Kopriva 2006) of the degree-N LGL
  * interpolant of the mapping, evaluated at the solution nodes. */
-enum { SDG_MAP_BOX = 0, SDG_MAP_WARP = 1 };
+enum { SDG_MAP_BOX = 0, SDG_MAP_WARP = 1, SDG_MAP_ANNULUS = 2 };
+
+/* SDG_MAP_ANNULUS (BASELINE configs[2]/[3]: rotor/stator annulus): the warped
+ * box point (xw, yw, zw) above (A = warp, 0 for none) maps to cylindrical
+ * coordinates about the x axis,
+ *   X = xw,  Y = r sin(theta),  Z = r cos(theta),  theta = yw (+ vg t),  r = zw,
+ * so y is the angle (radians) and z the radius (z0 > 0).  A moving band
+ * ROTATES rigidly at angular velocity vg_y about the x axis (the sliding
+ * interfaces are x-normal annuli, the pairing runs along theta as before).  A
+ * periodic y direction must span the full circle (height = 2 pi): sector
+ * periodicity would need a rotation of the momentum across the seam.
+ * Metric terms rotate with the band, Ja(t) = R(vg t) Ja(0); the contravariant
+ * grid velocity Ja^d . vg is the discrete curl of I^N(omega r^2/2 grad_xi X),
+ * so the discrete geometric conservation law holds exactly (free stream). */
 
 typedef struct {
   double gamma, R, mu, Pr;

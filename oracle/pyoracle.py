@@ -135,6 +135,7 @@ class Oracle3D:
         self.n1 = self.lib.orc_n1(h)
         self.n_elements = self.lib.orc_n_elements(h)
         self.size = self.n_elements * self.n1 ** 3 * T.NVARS
+        self.widths = (13, 6) if mesh.mapping == T.MAP_ANNULUS else (10, 4)  # metric doubles per node / face node
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -220,8 +221,9 @@ class Oracle3D:
     def metrics(self):
         """(met [E, N3, 10], fmet [E, 6, N2, 4]) of a curved (SDG_MAP_WARP) mesh."""
         n1 = self.n1
-        met = np.zeros((self.n_elements, n1 ** 3, 10))
-        fmet = np.zeros((self.n_elements, 6, n1 * n1, 4))
+        mw, fw = self.widths
+        met = np.zeros((self.n_elements, n1 ** 3, mw))
+        fmet = np.zeros((self.n_elements, 6, n1 * n1, fw))
         self.lib.orc_get_metrics.argtypes = [C.c_void_p, _dp, _dp]
         self._check(self.lib.orc_get_metrics(self.h, _d(met), _d(fmet)))
         return met, fmet

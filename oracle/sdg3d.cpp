@@ -758,8 +758,12 @@ struct orc_solver {
   std::vector<double> field, reg, dudt, grad, trace, fflux, gtrace, lift;
   // Curved elements (SDG_MAP_WARP): per node Ja^d_c (9, [3*d + c]) and 1/J;
   // per side face node the unit normal along +xi_dir and the surface Jacobian sJ.
-  bool curved = false;
+  // SDG_MAP_ANNULUS adds per node the contravariant grid velocity per unit
+  // angular speed V^d (3) and per face node vg.n per unit angular speed.
+  bool curved = false, annulus = false;
+  int mw = 10, fw = 4;  // doubles per node / per face node
   std::vector<double> met, fmet;
+  double t_cur = 0.0;   // stage time of the residual being evaluated (band rotation)
   double time = 0.0;
   int step_index = 0, stage_index = 0;
   std::string err;
@@ -774,8 +778,39 @@ struct orc_solver {
   double* ff(int e, int side) { return fflux.data() + (static_cast<size_t>(e) * 6 + side) * n2 * NV; }
   double* gt(int e, int side) { return gtrace.data() + (static_cast<size_t>(e) * 6 + side) * n2 * NG; }
   double* lf(int e, int side) { return lift.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4; }
-  const double* mt(int e, int nd) const { return met.data() + (static_cast<size_t>(e) * n3 + nd) * 10; }
-  const double* fm(int e, int side) const { return fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4; }
+  const double* mt(int e, int nd) const { return met.data() + (static_cast<size_t>(e) * n3 + nd) * mw; }
+  const double* fm(int e, int side) const { return fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * fw; }
+  // Rotation of a rotating annulus band at the stage time: theta -> theta + phi,
+  // (Y, Z) -> (c Y + s Z, -s Y + c Z) with Y = r sin(theta), Z = r cos(theta).
+  void band_rot(int e, double& c, double& s) const {
+    const double phi = annulus ? bands[elems[e].band].vg * t_cur : 0.0;
+    c = std::cos(phi);
+    s = std::sin(phi);
+  }
+  static void rot3(double c, double s, const double* v, double* o) {
+    o[0] = v[0];
+    o[1] = c * v[1] + s * v[2];
+    o[2] = -s * v[1] + c * v[2];
+  }
+  // Ja^d_c of node nd at t_cur (rotated with the band).
+  void ja_at(int e, int nd, double* o9) const {
+    double c, s;
+    band_rot(e, c, s);
+    for (int d = 0; d < 3; ++d) rot3(c, s, mt(e, nd) + 3 * d, o9 + 3 * d);
+  }
+  // Unit +xi normal of face node f at t_cur, and vg . n.
+  void normal_at(int e, int side, int f, double* n3o, double& vgn) const {
+    const double* q = fm(e, side) + f * fw;
+    if (!annulus) {
+      for (int c = 0; c < 3; ++c) n3o[c] = q[c];
+      vgn = bands[elems[e].band].vg * q[1];
+      return;
+    }
+    double c, s;
+    band_rot(e, c, s);
+    rot3(c, s, q, n3o);
+    vgn = bands[elems[e].band].vg * q[4];
+  }
 
   void physical(int e, double xi, double eta, double zeta, double t, double* x) const {
     const Elem& el = elems[e];
@@ -798,6 +833,13 @@ struct orc_solver {
     x[0] = (ox + 0.5 * (xi + 1.0) * b.hx) + A * b.hx * sp * sy * sz;
     x[1] = (oy + 0.5 * (eta + 1.0) * b.hy) + A * b.hy * sp * sz + b.vg * t;
     x[2] = (oz + 0.5 * (zeta + 1.0) * b.hz) + A * b.hz * sp * sy;
+    if (annulus) {
+      // SDG_MAP_ANNULUS: (x, theta, r) -> (x, r sin theta, r cos theta); the band's
+      // rotation is the + vg t already in theta.
+      const double th = x[1], r = x[2];
+      x[1] = r * std::sin(th);
+      x[2] = r * std::cos(th);
+    }
   }
   // Mapped position minus the mapped element centre, long double (metrics only).
   void relative_position(int e, double xi, double eta, double zeta, ld* x) const {
@@ -814,6 +856,25 @@ struct orc_solver {
     x[0] = r[0] * h[0] + A * h[0] * (sp * sy * sz - cp * cy * cz);
     x[1] = r[1] * h[1] + A * h[1] * (sp * sz - cp * cz);
     x[2] = r[2] * h[2] + A * h[2] * (sp * sy - cp * cy);
+    if (annulus) {
+      // Polar map about the x axis, minus the mapped centre (theta at t = 0).
+      const ld th = spec.y0 + h[1] * (el.iy + 0.5L * (eta + 1.0L)) + A * h[1] * sp * sz;
+      const ld rr = spec.z0 + h[2] * (el.iz + 0.5L * (zeta + 1.0L)) + A * h[2] * sp * sy;
+      const ld thc = spec.y0 + h[1] * (el.iy + 0.5L) + A * h[1] * cp * cz;
+      const ld rc = spec.z0 + h[2] * (el.iz + 0.5L) + A * h[2] * cp * cy;
+      x[1] = rr * std::sin(th) - rc * std::sin(thc);
+      x[2] = rr * std::cos(th) - rc * std::cos(thc);
+    }
+  }
+  // Absolute radius of a reference point (annulus grid-velocity potential).
+  ld radius(int e, double xi, double eta, double zeta) const {
+    const Elem& el = elems[e];
+    const Band& b = bands[el.band];
+    const ld h[3] = {b.hx, b.hy, b.hz};
+    const ld t[3] = {(el.ix + 0.5L * (xi + 1.0L)) / b.nx, (el.iy + 0.5L * (eta + 1.0L)) / spec.ny,
+                     (el.iz + 0.5L * (zeta + 1.0L)) / spec.nz};
+    const ld sp = sinpi_ld(t[0]), sy = sinpi_ld(2.0L * t[1]);
+    return spec.z0 + h[2] * (el.iz + 0.5L * (zeta + 1.0L)) + static_cast<ld>(spec.warp) * h[2] * sp * sy;
   }
   void face_node_position(int e, int side, int p, int q, double t, double* x) const {
     const double a = ns.x[p], c = ns.x[q];
@@ -1018,8 +1079,18 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
   fflux.assign(static_cast<size_t>(ne) * 6 * n2 * NV, 0.0);
   gtrace.assign(static_cast<size_t>(ne) * 6 * n2 * NG, 0.0);
   lift.assign(static_cast<size_t>(ne) * 6 * n2 * 4, 0.0);
-  if (s.mapping != SDG_MAP_BOX && s.mapping != SDG_MAP_WARP) throw ConfigError("unknown mesh mapping");
-  curved = s.mapping == SDG_MAP_WARP;
+  if (s.mapping != SDG_MAP_BOX && s.mapping != SDG_MAP_WARP && s.mapping != SDG_MAP_ANNULUS)
+    throw ConfigError("unknown mesh mapping");
+  curved = s.mapping != SDG_MAP_BOX;
+  annulus = s.mapping == SDG_MAP_ANNULUS;
+  if (annulus) {
+    if (!(s.z0 > 0.0)) throw ConfigError("annulus needs a positive inner radius (z0 > 0)");
+    if (s.periodic_z) throw ConfigError("annulus: the radial direction cannot be periodic");
+    if (s.periodic_y && std::abs(s.height - 2.0 * 3.14159265358979323846) > 1e-12)
+      throw ConfigError("annulus: a periodic angle must span the full circle (height = 2 pi)");
+    mw = 13;
+    fw = 6;
+  }
   if (curved) {
     if (!std::isfinite(s.warp)) throw ConfigError("warp amplitude must be finite");
     build_metrics();
@@ -1044,8 +1115,8 @@ void orc_solver::build_metrics() {
   const std::vector<ld> L(Ld.begin(), Ld.end());
   const std::vector<ld> DL(bl.D.begin(), bl.D.end());
   const int ne = static_cast<int>(elems.size());
-  met.assign(static_cast<size_t>(ne) * n3 * 10, 0.0);
-  fmet.assign(static_cast<size_t>(ne) * 6 * n2 * 4, 0.0);
+  met.assign(static_cast<size_t>(ne) * n3 * mw, 0.0);
+  fmet.assign(static_cast<size_t>(ne) * 6 * n2 * fw, 0.0);
   auto idx = [&](int p, int q, int r) { return (p * n + q) * n + r; };
   // d/dxi_d of a grid function on the LGL grid.
   auto deriv = [&](const ld* f, int d, ld* out) {
@@ -1119,8 +1190,31 @@ void orc_solver::build_metrics() {
       interp3(JaL.data() + c * n3, Ja.data() + c * n3);
       interp3(dX.data() + c * n3, dXs.data() + c * n3);
     }
+    // Annulus: contravariant grid velocity per unit angular speed,
+    // V^d = Ja^d . (vg / omega) = [curl_xi I^N(psi grad_xi X)]_d with psi = r^2 / 2
+    // (vg / omega = curl(psi e_x) = (0, Z, -Y)), discretely divergence free.
+    std::vector<ld> VL(3 * n3, 0.0L), Vs(3 * n3, 0.0L);
+    if (annulus) {
+      std::vector<ld> At(3 * n3);
+      for (int p = 0; p < n; ++p)
+        for (int q = 0; q < n; ++q)
+          for (int r = 0; r < n; ++r) {
+            const ld rr = radius(e, lgl.x[p], lgl.x[q], lgl.x[r]);
+            for (int k = 0; k < 3; ++k) At[k * n3 + idx(p, q, r)] = 0.5L * rr * rr * dX[(3 * k + 0) * n3 + idx(p, q, r)];
+          }
+      for (int i = 0; i < 3; ++i) {
+        const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+        deriv(At.data() + i2 * n3, i1, dV.data());
+        for (int g = 0; g < n3; ++g) VL[i * n3 + g] = dV[g];
+        deriv(At.data() + i1 * n3, i2, dV.data());
+        for (int g = 0; g < n3; ++g) VL[i * n3 + g] -= dV[g];
+        interp3(VL.data() + i * n3, Vs.data() + i * n3);
+      }
+    }
     for (int g = 0; g < n3; ++g) {
-      double* o = met.data() + (static_cast<size_t>(e) * n3 + g) * 10;
+      double* o = met.data() + (static_cast<size_t>(e) * n3 + g) * mw;
+      if (annulus)
+        for (int i = 0; i < 3; ++i) o[10 + i] = static_cast<double>(Vs[i * n3 + g]);
       for (int c = 0; c < 9; ++c) o[c] = static_cast<double>(Ja[c * n3 + g]);
       // dXs[(3 d + c)] = dX_c / dxi_d; J = det.
       const ld a00 = dXs[0 * n3 + g], a01 = dXs[1 * n3 + g], a02 = dXs[2 * n3 + g];
@@ -1132,12 +1226,12 @@ void orc_solver::build_metrics() {
     }
     for (int side = 0; side < 6; ++side) {
       const int d = side / 2, layer = (side & 1) ? n - 1 : 0;
-      double* o = fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4;
+      double* o = fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * fw;
       for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
-          ld ns3[3];
-          for (int c = 0; c < 3; ++c) {
-            const ld* f = JaL.data() + (3 * d + c) * n3;
+          ld ns3[4];
+          for (int c = 0; c < (annulus ? 4 : 3); ++c) {
+            const ld* f = c < 3 ? JaL.data() + (3 * d + c) * n3 : VL.data() + d * n3;
             ld acc = 0.0L;
             for (int u = 0; u < n; ++u) {
               ld inner = 0.0L;
@@ -1150,9 +1244,10 @@ void orc_solver::build_metrics() {
             ns3[c] = acc;
           }
           const ld sj = std::sqrt(ns3[0] * ns3[0] + ns3[1] * ns3[1] + ns3[2] * ns3[2]);
-          double* q = o + (a * n + b) * 4;
+          double* q = o + (a * n + b) * fw;
           for (int c = 0; c < 3; ++c) q[c] = static_cast<double>(ns3[c] / sj);
           q[3] = static_cast<double>(sj);
+          if (annulus) q[4] = static_cast<double>(ns3[3] / sj);  // (vg / omega) . n
         }
     }
   } catch (...) {
@@ -1162,7 +1257,7 @@ void orc_solver::build_metrics() {
   if (first) std::rethrow_exception(first);
   for (const auto& f : interior) {
     const double* src = fm(f.em, 2 * f.dir + 1);
-    std::copy(src, src + n2 * 4, fmet.data() + (static_cast<size_t>(f.ep) * 6 + 2 * f.dir) * n2 * 4);
+    std::copy(src, src + n2 * fw, fmet.data() + (static_cast<size_t>(f.ep) * 6 + 2 * f.dir) * n2 * fw);
   }
 }
 
@@ -1464,6 +1559,15 @@ void orc_solver::assemble_gradients_curved(const double* u) {
 #pragma omp for schedule(static)
     for (int e = 0; e < ne; ++e) {
       for (int nd = 0; nd < n3; ++nd) prim4(u + (static_cast<size_t>(e) * n3 + nd) * NV, gas, q.data() + nd * 4);
+      std::vector<double> ja(static_cast<size_t>(n3) * 9), ns4(static_cast<size_t>(6) * n2 * 4);
+      for (int nd = 0; nd < n3; ++nd) ja_at(e, nd, ja.data() + nd * 9);
+      for (int sd = 0; sd < 6; ++sd)
+        for (int f = 0; f < n2; ++f) {
+          double vgn;
+          double* o = ns4.data() + (sd * n2 + f) * 4;
+          normal_at(e, sd, f, o, vgn);
+          o[3] = fm(e, sd)[f * fw + 3];
+        }
       for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j)
           for (int k = 0; k < n; ++k) {
@@ -1477,15 +1581,15 @@ void orc_solver::assemble_gradients_curved(const double* u) {
                 double vol = 0.0;
                 for (int m = 0; m < n; ++m) {
                   const int mx = (m * n + j) * n + k, my = (i * n + m) * n + k, mz = (i * n + j) * n + m;
-                  vol += wdiff[i * n + m] * mt(e, mx)[0 + kk] * q[mx * 4 + c] +
-                         wdiff[j * n + m] * mt(e, my)[3 + kk] * q[my * 4 + c] +
-                         wdiff[k * n + m] * mt(e, mz)[6 + kk] * q[mz * 4 + c];
+                  vol += wdiff[i * n + m] * ja[mx * 9 + 0 + kk] * q[mx * 4 + c] +
+                         wdiff[j * n + m] * ja[my * 9 + 3 + kk] * q[my * 4 + c] +
+                         wdiff[k * n + m] * ja[mz * 9 + 6 + kk] * q[mz * 4 + c];
                 }
                 double surf = 0.0;
                 for (int d = 0; d < 3; ++d) {
                   const int f = fidx[d];
-                  const double* np = fm(e, 2 * d + 1) + f * 4;
-                  const double* nm = fm(e, 2 * d) + f * 4;
+                  const double* np = ns4.data() + ((2 * d + 1) * n2 + f) * 4;
+                  const double* nm = ns4.data() + ((2 * d) * n2 + f) * 4;
                   surf += (lf(e, 2 * d + 1)[f * 4 + c] * np[kk] * np[3] * fr[ia[d]] -
                            lf(e, 2 * d)[f * 4 + c] * nm[kk] * nm[3] * fl[ia[d]]) / w[ia[d]];
                 }
@@ -1537,8 +1641,9 @@ void orc_solver::interior_flux() {
       const double* gp = lifting ? gt(f.ep, sp) + k * NG : nullptr;
       if (curved) {
         // +xi normal of the face (identical in both slots); vg_n = vg . n.
-        const double* nrm = fm(f.em, sm) + k * 4;
-        face_flux_n(um + k * NV, up + k * NV, nrm, bands[elems[f.em].band].vg * nrm[1], gm, gp, gas, om + k * NV);
+        double nrm[3], vgn;
+        normal_at(f.em, sm, k, nrm, vgn);
+        face_flux_n(um + k * NV, up + k * NV, nrm, vgn, gm, gp, gas, om + k * NV);
       } else
       face_flux(um + k * NV, up + k * NV, f.dir, vg_n, gm, gp, gas, om + k * NV);
       for (int v = 0; v < NV; ++v) op[k * NV + v] = om[k * NV + v];
@@ -1560,7 +1665,7 @@ void orc_solver::volume(const double* u, double* out) {
 #pragma omp for schedule(static)
     for (int e = 0; e < ne; ++e) {
       const Band& b = bands[elems[e].band];
-      const double vg[3] = {0.0, b.vg, 0.0};
+      const double vg[3] = {0.0, annulus ? 0.0 : b.vg, 0.0};
       const double jac = 0.125 * b.hx * b.hy * b.hz;
       const double sjx = 0.25 * b.hy * b.hz, sjy = 0.25 * b.hx * b.hz, sjz = 0.25 * b.hx * b.hy;
       for (int nd = 0; nd < n3; ++nd) {
@@ -1574,12 +1679,18 @@ void orc_solver::volume(const double* u, double* out) {
             for (int v = 0; v < NV; ++v) f[d][v] -= fv[d][v];
         }
         if (curved) {
-          // Contravariant flux Ja^d . F (the affine sJ_d F_d below).
-          const double* ja = mt(e, nd);
+          // Contravariant flux Ja^d . F (the affine sJ_d F_d below).  Annulus: F holds
+          // no grid velocity (vg = 0 above) and the rotating band's ALE term is
+          // omega V^d u with the contravariant grid velocity V^d.
+          double ja[9];
+          ja_at(e, nd, ja);
+          double wv[3] = {0.0, 0.0, 0.0};
+          if (annulus)
+            for (int d = 0; d < 3; ++d) wv[d] = b.vg * mt(e, nd)[10 + d];
           for (int v = 0; v < NV; ++v) {
-            fx[nd * NV + v] = ja[0] * f[0][v] + ja[1] * f[1][v] + ja[2] * f[2][v];
-            fy[nd * NV + v] = ja[3] * f[0][v] + ja[4] * f[1][v] + ja[5] * f[2][v];
-            fz[nd * NV + v] = ja[6] * f[0][v] + ja[7] * f[1][v] + ja[8] * f[2][v];
+            fx[nd * NV + v] = ja[0] * f[0][v] + ja[1] * f[1][v] + ja[2] * f[2][v] - wv[0] * s[v];
+            fy[nd * NV + v] = ja[3] * f[0][v] + ja[4] * f[1][v] + ja[5] * f[2][v] - wv[1] * s[v];
+            fz[nd * NV + v] = ja[6] * f[0][v] + ja[7] * f[1][v] + ja[8] * f[2][v] - wv[2] * s[v];
           }
           continue;
         }
@@ -1661,8 +1772,8 @@ void orc_solver::dirichlet_flux(double t_stage) {
         const State ext = eval_case(flow_case, x, t_stage, gas);
         const double* g = lifting ? gt(df.e, df.side) + k * NG : nullptr;
         if (curved) {
-          const double* nrm = fm(df.e, df.side) + k * 4;
-          const double vgn = bands[elems[df.e].band].vg * nrm[1];
+          double nrm[3], vgn;
+          normal_at(df.e, df.side, k, nrm, vgn);
           if (plus) face_flux_n(mine + k * NV, ext.data(), nrm, vgn, g, g, gas, o + k * NV);
           else face_flux_n(ext.data(), mine + k * NV, nrm, vgn, g, g, gas, o + k * NV);
           continue;
@@ -1699,7 +1810,7 @@ void orc_solver::apply_faces(double* out) {
             else { i = p; j = q; k = a; }
             double* o = out + node(e, i, j, k) * NV;
             // Curved: (sJ / J) of the face node and the volume node.
-            const double cc = curved ? sgn * (lift_v[a] / w[a]) * fm(e, side)[(p * n + q) * 4 + 3] *
+            const double cc = curved ? sgn * (lift_v[a] / w[a]) * fm(e, side)[(p * n + q) * fw + 3] *
                                            mt(e, (i * n + j) * n + k)[9]
                                      : c;
             for (int v = 0; v < NV; ++v) o[v] += cc * line[(p * n + q) * NV + v];
@@ -1711,6 +1822,7 @@ void orc_solver::apply_faces(double* out) {
 
 // compute_residual (solver.cpp:846-870), single rank.
 void orc_solver::residual(double t_stage, const double* u, double* out) {
+  t_cur = t_stage;
   update_interfaces(t_stage);
   prolong(u);
   fill_mortar_solution();
@@ -1782,14 +1894,16 @@ double orc_solver::suggest_dt(double cfl) const {
   double dt = std::numeric_limits<double>::max();
   for (size_t e = 0; e < elems.size(); ++e) {
     const Band& b = bands[elems[e].band];
-    const double vg[3] = {0.0, b.vg, 0.0};
+    const double vg[3] = {0.0, annulus ? 0.0 : b.vg, 0.0};
     double lmax = 0.0;
     for (int nd = 0; nd < n3; ++nd) {
       const double* s = field.data() + (e * n3 + nd) * NV;
       const double v1 = s[1] / s[0] - vg[0], v2 = s[2] / s[0] - vg[1], v3 = s[3] / s[0] - vg[2];
       lmax = std::max(lmax, std::sqrt(v1 * v1 + v2 * v2 + v3 * v3) + std::sqrt(gas.gamma * pressure(s, gas) / s[0]));
     }
-    const double h = std::min(b.hx, std::min(b.hy, b.hz));
+    // Annulus: the angular spacing times the inner radius, and the tip speed.
+    if (annulus) lmax += std::abs(b.vg) * (spec.z0 + spec.depth);
+    const double h = annulus ? std::min(b.hx, std::min(b.hy * spec.z0, b.hz)) : std::min(b.hx, std::min(b.hy, b.hz));
     dt = std::min(dt, cfl * h / (lmax * (2.0 * ns.degree + 1.0)));
   }
   return dt;

@@ -88,11 +88,11 @@ def raise_for(code: int, msg: str) -> None:
 
 
 PARTITION_LEX, PARTITION_SFC = 0, 1
-MAP_BOX, MAP_WARP = 0, 1
+MAP_BOX, MAP_WARP, MAP_ANNULUS = 0, 1, 2
 
 
 def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z0=0.0,
-              periodic=(True, True, True), partition=PARTITION_LEX, warp=None) -> MeshSpec:
+              periodic=(True, True, True), partition=PARTITION_LEX, warp=None, mapping=None) -> MeshSpec:
     """bands: list of (nx, width_frac, vg_y) tuples, stacked along x.  warp: None for
     affine hexahedra, else the amplitude of the curved SDG_MAP_WARP mapping
     (include/sdg_types.h; 0.0 gives the curved code path on an affine geometry)."""
@@ -109,9 +109,20 @@ def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z
         m.bands[i].nx, m.bands[i].width_frac, m.bands[i].vg_y = int(nx), float(frac), float(vg)
     m.periodic_x, m.periodic_y, m.periodic_z = (int(bool(p)) for p in periodic)
     m.partition = int(partition)
-    m.mapping = MAP_BOX if warp is None else MAP_WARP
+    m.mapping = (MAP_BOX if warp is None else MAP_WARP) if mapping is None else int(mapping)
     m.warp = 0.0 if warp is None else float(warp)
     return m
+
+
+def annulus_spec(bands, n_theta, n_r, r_in, r_out, length=2.0, warp=None, theta_span=2.0 * math.pi,
+                 partition=PARTITION_LEX) -> MeshSpec:
+    """Rotor/stator annulus (SDG_MAP_ANNULUS): bands (nx, width_frac, omega) stacked
+    along the axis x over [0, length], n_theta elements around, n_r radially in
+    [r_in, r_out]; full circle -> periodic in theta, radial walls Dirichlet."""
+    periodic_theta = abs(theta_span - 2.0 * math.pi) < 1e-15
+    return mesh_spec(bands, ny=n_theta, nz=n_r, width=length, height=theta_span, depth=r_out - r_in,
+                     z0=r_in, periodic=(False, periodic_theta, False), partition=partition, warp=warp,
+                     mapping=MAP_ANNULUS)
 
 
 def freestream(rho=1.0, v=(1.0, 0.5, 0.0), p=1.0) -> Case:
