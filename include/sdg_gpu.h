@@ -133,7 +133,9 @@ int sdg_plan_json(const sdg_mesh_spec* mesh, int n_ranks, int rank, double delta
 
 /* Host-only curved metric terms of one rank's elements (no GPU needed), as
  * uploaded by sdg_create for an SDG_MAP_WARP mesh: met n_local x N3 x 10
- * (Ja^d_c at [3d + c], 1/J), fmet n_local x 6 x N2 x 4 (unit +xi normal, sJ).
+ * (Ja^d_c at [3d + c], 1/J), fmet n_local x 6 x N2 x 4 (unit +xi normal, sJ);
+ * SDG_MAP_ANNULUS: 13 per node (+ contravariant grid velocity per unit omega)
+ * and 6 per face node (+ (vg / omega) . n, pad).
  * The reference's metrics are affine (ElementMetrics, proj/src/mesh.cpp:102-111).
  * met/fmet may be NULL to query *n_local; elements in sdg_local_element_ids order. */
 int sdg_metrics_host(const sdg_mesh_spec* mesh, int degree, int node_kind, int n_ranks, int rank, double* met,

@@ -350,8 +350,9 @@ def metrics_host(mesh: T.MeshSpec, degree: int, node_kind: int, n_ranks: int = 1
     T.raise_for(L.sdg_metrics_host(C.byref(mesh), degree, node_kind, n_ranks, rank, None, None, C.byref(n)),
                 L.sdg_global_error().decode())
     n1 = degree + 1
-    met = np.zeros((n.value, n1 ** 3, 10))
-    fmet = np.zeros((n.value, 6, n1 * n1, 4))
+    mw, fw = (13, 6) if mesh.mapping == T.MAP_ANNULUS else (10, 4)
+    met = np.zeros((n.value, n1 ** 3, mw))
+    fmet = np.zeros((n.value, 6, n1 * n1, fw))
     T.raise_for(L.sdg_metrics_host(C.byref(mesh), degree, node_kind, n_ranks, rank, _d(met), _d(fmet), C.byref(n)),
                 L.sdg_global_error().decode())
     return met, fmet

@@ -13,15 +13,52 @@
 // Both slots of a conforming face hold identical bits (host.cpp compute_metrics),
 // so both elements evaluate the face flux identically, as in the affine kernels.
 
-template <int N1>
+// Metric widths: per node Ja (9), 1/J [, V^d (3): annulus grid velocity per unit omega];
+// per face node unit normal (3), sJ [, (vg / omega) . n, pad: annulus].
+template <bool ROT>
+struct MWidth {
+  static constexpr int MW = ROT ? 13 : 10, FW = ROT ? 6 : 4;
+};
+
+template <int N1, bool ROT>
 struct CDim {
   static constexpr int N2 = N1 * N1;
   static constexpr int N3 = N2 * N1;
+  static constexpr int MW = MWidth<ROT>::MW, FW = MWidth<ROT>::FW;
   static constexpr int EPB = N1 <= 4 ? Dim<N1>::EPB : 1;
   static constexpr int THREADS = EPB * N3;
-  static constexpr int PER_GRAD = 31 * N3 + 78 * N2;  // U, q, metrics, gradient | own traces, lift*, face metrics
-  static constexpr int PER_UPD = 20 * N3 + 78 * N2;   // U, staging, metrics | lift*, face flux, face metrics
+  static constexpr int PER_GRAD = (21 + MW) * N3 + (54 + 6 * FW) * N2;  // U, q, metrics, gradient | traces, lift*, face metrics
+  static constexpr int PER_UPD = (10 + MW) * N3 + (54 + 6 * FW) * N2;   // U, staging, metrics | lift*, face flux, face metrics
 };
+
+// Rigid rotation of an annulus band at the stage time (SDG_MAP_ANNULUS): theta -> theta + phi,
+// (Y, Z) -> (c Y + s Z, -s Y + c Z).  Metric vectors rotate with the band: Ja(t) = R Ja(0), n(t) = R n(0).
+struct Rot {
+  double c, s;
+};
+__device__ __forceinline__ Rot band_rotation(bool rot, const BandD& B, double t) {
+  Rot r{1.0, 0.0};
+  if (rot) sincos(B.vg * t, &r.s, &r.c);
+  return r;
+}
+__device__ __forceinline__ void rotate_yz(const Rot& r, double& y, double& z) {
+  const double a = r.c * y + r.s * z, b = -r.s * y + r.c * z;
+  y = a;
+  z = b;
+}
+// Unit normal of a face node at the stage time and vg . n.
+template <bool ROT>
+__device__ __forceinline__ void face_normal(const double* q, const Rot& r, const BandD& B, double* n, double& vgn) {
+  n[0] = q[0];
+  n[1] = q[1];
+  n[2] = q[2];
+  if (ROT) {
+    rotate_yz(r, n[1], n[2]);
+    vgn = B.vg * q[4];
+  } else {
+    vgn = B.vg * q[1];
+  }
+}
 
 // Flat, coalesced load of EPB consecutive elements' node-major NC-vectors into
 // SoA shared memory dst[le * per + c * N3 + node].
@@ -37,9 +74,9 @@ __device__ __forceinline__ void load_soa(const double* __restrict__ src, int e0,
 }
 
 // Face metrics of EPB consecutive elements (6 x N2 x 4 contiguous per element).
-template <int N1, int EPB>
+template <int N1, int EPB, int FW>
 __device__ __forceinline__ void load_fmet(const double* __restrict__ src, int e0, int E, double* dst, int per) {
-  constexpr int W = 6 * N1 * N1 * 4;
+  constexpr int W = 6 * N1 * N1 * FW;
   const int n_el = min(EPB, E - e0);
   const double* s = src + static_cast<size_t>(e0) * W;
   for (int f = threadIdx.x; f < n_el * W; f += blockDim.x) {
@@ -124,10 +161,10 @@ __device__ __forceinline__ void fv_n(const double* u, const double* gr, const do
 // Curved BR1 gradient at one node, conservative weak form:
 //   g_c = (1/J) sum_d [ lw1 q*+ (n sJ)+_c - lw0 q*- (n sJ)-_c - sum_m Dhat(ia, m) Ja^d_c(m) q(m) ].
 // sq [4][N3], sJa [10][N3] (Ja^d_c at 3d + c), sLift [6][4][N2], sfm [6][N2][4].
-template <int N1>
+template <int N1, int FW, bool ROT>
 __device__ __forceinline__ void node_gradient_curved(const double* tab, const double* sq, const double* sJa,
                                                      const double* sLift, const double* sfm, int i, int j, int k,
-                                                     double* g) {
+                                                     const Rot& rot, double* g) {
   constexpr int N2 = N1 * N1, N3 = N2 * N1;
   const double* dh = tab;
   const double* lw = tab + N1 * N1 + 2 * N1;  // liftw[0][.], liftw[1][.]
@@ -162,8 +199,8 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
   for (int d = 0; d < 3; ++d) {
     const int ia = d == 0 ? i : (d == 1 ? j : k);
     const int f = d == 0 ? j * N1 + k : (d == 1 ? i * N1 + k : i * N1 + j);
-    const double* np = sfm + ((2 * d + 1) * N2 + f) * 4;
-    const double* nm = sfm + ((2 * d) * N2 + f) * 4;
+    const double* np = sfm + ((2 * d + 1) * N2 + f) * FW;
+    const double* nm = sfm + ((2 * d) * N2 + f) * FW;
     const double sp = lw[N1 + ia] * np[3], sm = lw[ia] * nm[3];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -175,33 +212,41 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) g[q] = ij * (surf[q] - acc[q]);
+  if (ROT) {  // computed with the t = 0 metrics: g(t) = R g
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rotate_yz(rot, g[3 * q + 1], g[3 * q + 2]);
+  }
 }
 
 // ----------------------------------------------------------------------------
 // k_gradient_curved: lift* -> curved gradient -> Fv.n (conforming sides) /
 // gradient traces (sliding and Dirichlet sides); grad_out for compute_gradients.
 // ----------------------------------------------------------------------------
-template <int N1>
-__global__ void __launch_bounds__(CDim<N1>::THREADS) k_gradient_curved(const __grid_constant__ ElemConsts C,
-                                                                       FieldPtrs P, StageArgs A) {
-  constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = CDim<N1>::EPB, TAB = Dim<N1>::TAB, PER = CDim<N1>::PER_GRAD;
+template <int N1, bool ROT>
+__global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(const __grid_constant__ ElemConsts C,
+                                                                            FieldPtrs P, StageArgs A) {
+  using D = CDim<N1, ROT>;
+  constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = D::EPB, TAB = Dim<N1>::TAB, PER = D::PER_GRAD;
+  constexpr int MW = D::MW, FW = D::FW;
   extern __shared__ double smem[];
   double* tab = smem;
   load_tables<N1>(C, tab);
   const int e0 = P.e_first + blockIdx.x * EPB;
   double* base = smem + TAB;
   load_soa<N1, EPB, 5>(P.U, e0, P.E, base, PER);
-  load_soa<N1, EPB, 10>(P.met, e0, P.E, base + 9 * N3, PER);
-  load_fmet<N1, EPB>(P.fmet, e0, P.E, base + 31 * N3 + 54 * N2, PER);
+  load_soa<N1, EPB, MW>(P.met, e0, P.E, base + 9 * N3, PER);
+  load_fmet<N1, EPB, FW>(P.fmet, e0, P.E, base + (21 + MW) * N3 + 54 * N2, PER);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
   const bool active = e < P.E;
   double* su = base + le * PER;
   double* sq = su + 5 * N3;
   double* sJa = sq + 4 * N3;
-  double* sG = sJa + 10 * N3;
+  double* sG = sJa + MW * N3;
   double* sTr = sG + 12 * N3;
   double* sLift = sTr + 30 * N2;
   double* sfm = sLift + 24 * N2;
+  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();
   if (active) {
     double u[5], q[4];
@@ -216,7 +261,7 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_gradient_curved(const __g
   if (active) {
     const int i = t / N2, j = (t / N1) % N1, k = t % N1;
     double g[12];
-    node_gradient_curved<N1>(tab, sq, sJa, sLift, sfm, i, j, k, g);
+    node_gradient_curved<N1, FW, ROT>(tab, sq, sJa, sLift, sfm, i, j, k, rot, g);
 #pragma unroll
     for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
     if (P.grad_out != nullptr) {
@@ -236,8 +281,9 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_gradient_curved(const __g
     const int slot = e * 6 + s;
     const int typ = P.side_type[slot], idx = P.side_idx[slot];
     if (typ == kConforming) {
-      double fv[4];
-      fv_n(sTr + (s * N2 + f) * 5, gt, sfm + (s * N2 + f) * 4, C.gas, fv);
+      double fv[4], nrm[3], vgn;
+      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
+      fv_n(sTr + (s * N2 + f) * 5, gt, nrm, C.gas, fv);
       double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
 #pragma unroll
       for (int c = 0; c < 4; ++c) dst[c] = fv[c];
@@ -254,28 +300,31 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_gradient_curved(const __g
 // weak divergence, surface lift, low-storage RK update, admissibility and the
 // traces of the new state (the phases of k_update with metric terms).
 // ----------------------------------------------------------------------------
-template <int N1, bool VISC>
-__global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __grid_constant__ ElemConsts C,
-                                                                     FieldPtrs P, StageArgs A) {
-  constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = CDim<N1>::EPB, TAB = Dim<N1>::TAB, PER = CDim<N1>::PER_UPD;
+template <int N1, bool VISC, bool ROT>
+__global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const __grid_constant__ ElemConsts C,
+                                                                          FieldPtrs P, StageArgs A) {
+  using D = CDim<N1, ROT>;
+  constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = D::EPB, TAB = Dim<N1>::TAB, PER = D::PER_UPD;
+  constexpr int MW = D::MW, FW = D::FW;
   extern __shared__ double smem[];
   double* tab = smem;
   load_tables<N1>(C, tab);
   const int e0 = P.e_first + blockIdx.x * EPB;
   double* elems = smem + TAB;
   load_soa<N1, EPB, 5>(P.U, e0, P.E, elems, PER);
-  load_soa<N1, EPB, 10>(P.met, e0, P.E, elems + 10 * N3, PER);
-  load_fmet<N1, EPB>(P.fmet, e0, P.E, elems + 20 * N3 + 54 * N2, PER);
+  load_soa<N1, EPB, MW>(P.met, e0, P.E, elems + 10 * N3, PER);
+  load_fmet<N1, EPB, FW>(P.fmet, e0, P.E, elems + (10 + MW) * N3 + 54 * N2, PER);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
   const bool active = e < P.E;
   double* su = elems + le * PER;
   double* sF = su + 5 * N3;
   double* sJa = sF + 5 * N3;
-  double* sLift = sJa + 10 * N3;
+  double* sLift = sJa + MW * N3;
   double* sFlux = sLift + 24 * N2;
   double* sfm = sFlux + 30 * N2;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();
 
   // Phase 1: numerical flux along each face node's normal -> sFlux[s][v][f]; lift* -> sLift.
@@ -294,8 +343,8 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __gri
       double own[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b);
-      const double* nrm = sfm + (s * N2 + f) * 4;
-      const double vgn = B.vg * nrm[1];
+      double nrm[3], vgn;
+      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
       const int slot = e * 6 + s;
       const int typ = P.side_type[slot], idx = P.side_idx[slot];
       double flux[5], lift[4];
@@ -370,7 +419,7 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __gri
     const double ir = rcp_nr(u[0]);
     const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
     const double p = pressure(u, ir, C.gas);
-    const double vgv[3] = {0.0, B.vg, 0.0};
+    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, 0.0};  // annulus: grid velocity enters through V^d below
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       F[d][0] = u[0] * vv[d];
@@ -383,7 +432,7 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __gri
     }
     if (VISC) {
       double g[12];
-      node_gradient_curved<N1>(tab, sF, sJa, sLift, sfm, i, j, k, g);
+      node_gradient_curved<N1, FW, ROT>(tab, sF, sJa, sLift, sfm, i, j, k, rot, g);
       const double div = g[0] + g[4] + g[8];
       const double mu = C.gas.mu, lam = C.gas.lam;
       const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
@@ -397,11 +446,16 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __gri
         F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
       }
     }
+    if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
+    }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const double ja0 = sJa[(3 * d) * N3 + t], ja1 = sJa[(3 * d + 1) * N3 + t], ja2 = sJa[(3 * d + 2) * N3 + t];
+      const double wv = ROT ? B.vg * sJa[(10 + d) * N3 + t] : 0.0;  // contravariant grid velocity
 #pragma unroll
-      for (int v = 0; v < 5; ++v) Ft[d][v] = ja0 * F[0][v] + ja1 * F[1][v] + ja2 * F[2][v];
+      for (int v = 0; v < 5; ++v) Ft[d][v] = ja0 * F[0][v] + ja1 * F[1][v] + ja2 * F[2][v] - wv * u[v];
     }
   }
 
@@ -443,7 +497,7 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __gri
       const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
       const double l = lw[(s & 1) * N1 + ia];
       if (l != 0.0) {
-        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * 4 + 3] * ij;
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * FW + 3] * ij;
 #pragma unroll
         for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
       }
@@ -497,26 +551,34 @@ __global__ void __launch_bounds__(CDim<N1>::THREADS) k_update_curved(const __gri
   }
 }
 
-template <int N1>
-void gradient_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  const int blocks = (p.E - p.e_first + CDim<N1>::EPB - 1) / CDim<N1>::EPB;
-  const int sm = (Dim<N1>::TAB + CDim<N1>::EPB * CDim<N1>::PER_GRAD) * 8;
-  cudaFuncSetAttribute(k_gradient_curved<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  k_gradient_curved<N1><<<blocks, CDim<N1>::THREADS, sm, st>>>(c, p, a);
+template <int N1, bool ROT>
+void gradient_curved_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  using D = CDim<N1, ROT>;
+  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+  const int sm = (Dim<N1>::TAB + D::EPB * D::PER_GRAD) * 8;
+  cudaFuncSetAttribute(k_gradient_curved<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  k_gradient_curved<N1, ROT><<<blocks, D::THREADS, sm, st>>>(c, p, a);
   check_launch("k_gradient_curved");
 }
 template <int N1>
-void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  const int blocks = (p.E - p.e_first + CDim<N1>::EPB - 1) / CDim<N1>::EPB;
-  const int sm = (Dim<N1>::TAB + CDim<N1>::EPB * CDim<N1>::PER_UPD) * 8;
-  if (c.gas.viscous) {
-    cudaFuncSetAttribute(k_update_curved<N1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    k_update_curved<N1, true><<<blocks, CDim<N1>::THREADS, sm, st>>>(c, p, a);
-  } else {
-    cudaFuncSetAttribute(k_update_curved<N1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    k_update_curved<N1, false><<<blocks, CDim<N1>::THREADS, sm, st>>>(c, p, a);
-  }
+void gradient_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (c.mapping == SDG_MAP_ANNULUS) gradient_curved_r<N1, true>(c, p, a, st);
+  else gradient_curved_r<N1, false>(c, p, a, st);
+}
+template <int N1, bool ROT>
+void update_curved_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  using D = CDim<N1, ROT>;
+  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+  const int sm = (Dim<N1>::TAB + D::EPB * D::PER_UPD) * 8;
+  auto kern = c.gas.viscous ? k_update_curved<N1, true, ROT> : k_update_curved<N1, false, ROT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  kern<<<blocks, D::THREADS, sm, st>>>(c, p, a);
   check_launch("k_update_curved");
+}
+template <int N1>
+void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (c.mapping == SDG_MAP_ANNULUS) update_curved_r<N1, true>(c, p, a, st);
+  else update_curved_r<N1, false>(c, p, a, st);
 }
 
 // ============================================================================
@@ -530,13 +592,14 @@ void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a
 // Own traces are staged from the trace buffer, so both elements of a face use
 // the same stored bits.  The RK register is prefetched into L2.
 // ============================================================================
-template <int N1>
+template <int N1, bool ROT>
 struct CB {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
-  static constexpr int EPB = N1 == 2 ? 16 : CDim<N1>::EPB;  // shared memory: <= 227 KB per CTA
+  static constexpr int MW = MWidth<ROT>::MW, FW = MWidth<ROT>::FW;
+  static constexpr int EPB = N1 == 2 ? 16 : CDim<N1, ROT>::EPB;  // shared memory: <= 227 KB per CTA
   static constexpr int THREADS = EPB * N3;
   static constexpr int TAB = Dim<N1>::TAB;
-  static constexpr int EL = 5 * N3, ML = 10 * N3, FM = 24 * N2, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
+  static constexpr int EL = 5 * N3, ML = MW * N3, FM = 6 * FW * N2, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
   // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
   static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB + 5 * N3 + 24 * N2 + 30 * N2;
   // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
@@ -548,10 +611,10 @@ struct CB {
 };
 
 // Gradient at one node from AoS metrics sM[node][10] and SoA q.
-template <int N1>
+template <int N1, int MW, int FW, bool ROT>
 __device__ __forceinline__ void node_gradient_curved_aos(const double* tab, const double* sq, const double* sM,
                                                          const double* sLift, const double* sfm, int i, int j, int k,
-                                                         double* g) {
+                                                         const Rot& rot, double* g) {
   constexpr int N2 = N1 * N1, N3 = N2 * N1;
   const double* dh = tab;
   const double* lw = tab + N1 * N1 + 2 * N1;
@@ -567,7 +630,7 @@ __device__ __forceinline__ void node_gradient_curved_aos(const double* tab, cons
     for (int m = 0; m < N1; ++m) {
       const double c = dh[ia * N1 + m];
       const int nd = base + m * stride;
-      const double* ja = sM + nd * 10 + 3 * d;
+      const double* ja = sM + nd * MW + 3 * d;
       const double ja0 = ja[0], ja1 = ja[1], ja2 = ja[2];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -578,7 +641,7 @@ __device__ __forceinline__ void node_gradient_curved_aos(const double* tab, cons
       }
     }
   }
-  const double ij = sM[((i * N1 + j) * N1 + k) * 10 + 9];
+  const double ij = sM[((i * N1 + j) * N1 + k) * MW + 9];
   double surf[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) surf[q] = 0.0;
@@ -586,8 +649,8 @@ __device__ __forceinline__ void node_gradient_curved_aos(const double* tab, cons
   for (int d = 0; d < 3; ++d) {
     const int ia = d == 0 ? i : (d == 1 ? j : k);
     const int f = d == 0 ? j * N1 + k : (d == 1 ? i * N1 + k : i * N1 + j);
-    const double* np = sfm + ((2 * d + 1) * N2 + f) * 4;
-    const double* nm = sfm + ((2 * d) * N2 + f) * 4;
+    const double* np = sfm + ((2 * d + 1) * N2 + f) * FW;
+    const double* nm = sfm + ((2 * d) * N2 + f) * FW;
     const double sp = lw[N1 + ia] * np[3], sm = lw[ia] * nm[3];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -599,14 +662,18 @@ __device__ __forceinline__ void node_gradient_curved_aos(const double* tab, cons
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) g[q] = ij * (surf[q] - acc[q]);
+  if (ROT) {  // computed with the t = 0 metrics: g(t) = R g
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rotate_yz(rot, g[3 * q + 1], g[3 * q + 2]);
+  }
 }
 
 // Issue the bulk copies of one element tile (thread 0).  GRAD: neighbour
 // trace (conforming) or lift* (sliding) only; else trace + Fv.n or flux + lift*.
-template <int N1, bool GRAD, bool VISC>
+template <int N1, bool ROT, bool GRAD, bool VISC>
 __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, int n, double* base, int per,
                                                    uint64_t* bar) {
-  using D = CB<N1>;
+  using D = CB<N1, ROT>;
   uint32_t bytes = n * (D::EL + D::ML + D::FM + 6 * D::TS) * 8u;
   if (!GRAD && VISC) bytes += n * 6u * D::FS * 8u;
   for (int le = 0; le < n; ++le)
@@ -647,10 +714,11 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
   }
 }
 
-template <int N1>
-__global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
-                                                                       FieldPtrs P, StageArgs A) {
-  using D = CB<N1>;
+template <int N1, bool ROT>
+__global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
+                                                                            FieldPtrs P, StageArgs A) {
+  using D = CB<N1, ROT>;
+  constexpr int MW = D::MW, FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::G_PER;
   extern __shared__ __align__(128) double smem[];
   double* tab = smem;
@@ -661,7 +729,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __g
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
-    curved_issue_loads<N1, true, true>(P, e0, n_el, base, PER, bar);
+    curved_issue_loads<N1, ROT, true, true>(P, e0, n_el, base, PER, bar);
   }
   load_tables<N1>(C, tab);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
@@ -674,6 +742,8 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __g
   double* sq = sNb + 6 * D::TS;
   double* sG = sq + 4 * N3;
   double* sLift = sG + 12 * N3;
+  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();  // barrier init visible, tables loaded
   mbar_wait(bar, 0);
   if (active) {
@@ -710,7 +780,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __g
   if (active) {
     const int i = t / N2, j = (t / N1) % N1, k = t % N1;
     double g[12];
-    node_gradient_curved_aos<N1>(tab, sq, sM, sLift, sfm, i, j, k, g);
+    node_gradient_curved_aos<N1, MW, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
 #pragma unroll
     for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
     if (P.grad_out != nullptr) {
@@ -730,8 +800,9 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __g
     const int slot = e * 6 + s;
     const int typ = P.side_type[slot], idx = P.side_idx[slot];
     if (typ == kConforming) {
-      double fv[4];
-      fv_n(sTr + s * D::TS + f * 5, gt, sfm + (s * N2 + f) * 4, C.gas, fv);
+      double fv[4], nrm[3], vgn;
+      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
+      fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
       double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
 #pragma unroll
       for (int c = 0; c < 4; ++c) dst[c] = fv[c];
@@ -743,10 +814,11 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_gradient_curved_b(const __g
   }
 }
 
-template <int N1, bool VISC>
-__global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __grid_constant__ ElemConsts C,
-                                                                     FieldPtrs P, StageArgs A) {
-  using D = CB<N1>;
+template <int N1, bool VISC, bool ROT>
+__global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_update_curved_b(const __grid_constant__ ElemConsts C,
+                                                                          FieldPtrs P, StageArgs A) {
+  using D = CB<N1, ROT>;
+  constexpr int MW = D::MW, FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::U_PER;
   extern __shared__ __align__(128) double smem[];
   double* tab = smem;
@@ -757,7 +829,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
-    curved_issue_loads<N1, false, VISC>(P, e0, n_el, base, PER, bar);
+    curved_issue_loads<N1, ROT, false, VISC>(P, e0, n_el, base, PER, bar);
     if (A.mode == 0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
   }
   load_tables<N1>(C, tab);
@@ -774,6 +846,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
   double* sFlux = sLift + 24 * N2;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
+  const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();
   mbar_wait(bar, 0);
 
@@ -788,8 +861,8 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
     for (int it = t; it < 6 * N2; it += N3) {
       const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
       const double* own = sTr + s * D::TS + f * 5;
-      const double* nrm = sfm + (s * N2 + f) * 4;
-      const double vgn = B.vg * nrm[1];
+      double nrm[3], vgn;
+      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
       const double* nb = sNb + s * D::NB;
       const int typ = P.side_type[e * 6 + s];
       double flux[5], lift[4];
@@ -860,7 +933,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
     const double ir = rcp_nr(u[0]);
     const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
     const double p = pressure(u, ir, C.gas);
-    const double vgv[3] = {0.0, B.vg, 0.0};
+    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, 0.0};  // annulus: grid velocity enters through V^d below
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       F[d][0] = u[0] * vv[d];
@@ -873,7 +946,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
     }
     if (VISC) {
       double g[12];
-      node_gradient_curved_aos<N1>(tab, sF, sM, sLift, sfm, i, j, k, g);
+      node_gradient_curved_aos<N1, MW, FW, ROT>(tab, sF, sM, sLift, sfm, i, j, k, rot, g);
       const double div = g[0] + g[4] + g[8];
       const double mu = C.gas.mu, lam = C.gas.lam;
       const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
@@ -887,11 +960,17 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
         F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
       }
     }
-    const double* ja = sM + t * 10;
+    const double* ja = sM + t * MW;
+    if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
+    }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
+      const double wv = ROT ? B.vg * ja[10 + d] : 0.0;  // contravariant grid velocity
 #pragma unroll
-      for (int v = 0; v < 5; ++v) Ft[d][v] = ja[3 * d] * F[0][v] + ja[3 * d + 1] * F[1][v] + ja[3 * d + 2] * F[2][v];
+      for (int v = 0; v < 5; ++v)
+        Ft[d][v] = ja[3 * d] * F[0][v] + ja[3 * d + 1] * F[1][v] + ja[3 * d + 2] * F[2][v] - wv * u[v];
     }
   }
 
@@ -922,7 +1001,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
   // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
   double du[5];
   if (active) {
-    const double ij = sM[t * 10 + 9];
+    const double ij = sM[t * MW + 9];
 #pragma unroll
     for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
     const double* lw = tab + N1 * N1 + 2 * N1;
@@ -933,7 +1012,7 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
       const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
       const double l = lw[(s & 1) * N1 + ia];
       if (l != 0.0) {
-        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * 4 + 3] * ij;
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * FW + 3] * ij;
 #pragma unroll
         for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
       }
@@ -990,30 +1069,40 @@ __global__ void __launch_bounds__(CB<N1>::THREADS) k_update_curved_b(const __gri
   }
 }
 
+template <int N1, bool ROT>
+void gradient_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  using D = CB<N1, ROT>;
+  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+  cudaFuncSetAttribute(k_gradient_curved_b<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+  k_gradient_curved_b<N1, ROT><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+  check_launch("k_gradient_curved_b");
+}
 template <int N1>
 bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if constexpr (N1 % 2 != 0) {
     return false;
   } else {
-    using D = CB<N1>;
-    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    cudaFuncSetAttribute(k_gradient_curved_b<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-    k_gradient_curved_b<N1><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
-    check_launch("k_gradient_curved_b");
+    if (c.mapping == SDG_MAP_ANNULUS) gradient_curved_b_r<N1, true>(c, p, a, st);
+    else gradient_curved_b_r<N1, false>(c, p, a, st);
     return true;
   }
+}
+template <int N1, bool ROT>
+void update_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  using D = CB<N1, ROT>;
+  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+  auto kern = c.gas.viscous ? k_update_curved_b<N1, true, ROT> : k_update_curved_b<N1, false, ROT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
+  kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
+  check_launch("k_update_curved_b");
 }
 template <int N1>
 bool update_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if constexpr (N1 % 2 != 0) {
     return false;
   } else {
-    using D = CB<N1>;
-    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    auto kern = c.gas.viscous ? k_update_curved_b<N1, true> : k_update_curved_b<N1, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
-    kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
-    check_launch("k_update_curved_b");
+    if (c.mapping == SDG_MAP_ANNULUS) update_curved_b_r<N1, true>(c, p, a, st);
+    else update_curved_b_r<N1, false>(c, p, a, st);
     return true;
   }
 }

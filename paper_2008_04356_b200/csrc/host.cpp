@@ -13,8 +13,15 @@ namespace sdg {
 // ---------------------------------------------------------------- mesh
 MeshGeom::MeshGeom(const sdg_mesh_spec& s) : spec(s) {
   if (s.n_bands < 1 || s.n_bands > SDG_MAX_BANDS) throw ConfigError("mesh needs 1..16 bands");
-  if (s.mapping != SDG_MAP_BOX && s.mapping != SDG_MAP_WARP) throw ConfigError("unknown mesh mapping");
-  if (s.mapping == SDG_MAP_WARP && !std::isfinite(s.warp)) throw ConfigError("warp amplitude must be finite");
+  if (s.mapping != SDG_MAP_BOX && s.mapping != SDG_MAP_WARP && s.mapping != SDG_MAP_ANNULUS)
+    throw ConfigError("unknown mesh mapping");
+  if (s.mapping != SDG_MAP_BOX && !std::isfinite(s.warp)) throw ConfigError("warp amplitude must be finite");
+  if (s.mapping == SDG_MAP_ANNULUS) {
+    if (!(s.z0 > 0.0)) throw ConfigError("annulus needs a positive inner radius (z0 > 0)");
+    if (s.periodic_z) throw ConfigError("annulus: the radial direction cannot be periodic");
+    if (s.periodic_y && std::abs(s.height - 2.0 * 3.14159265358979323846) > 1e-12)
+      throw ConfigError("annulus: a periodic angle must span the full circle (height = 2 pi)");
+  }
   if (s.ny < 1 || s.nz < 1) throw ConfigError("mesh needs ny >= 1 and nz >= 1");
   if (!(s.width > 0.0) || !(s.height > 0.0) || !(s.depth > 0.0))
     throw ConfigError("mesh extents must be positive");
@@ -296,7 +303,7 @@ void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, doub
   const double bx = (B.x_lo + ix * B.hx) + 0.5 * (xi + 1.0) * B.hx;
   const double by = (m.spec.y0 + iy * B.hy) + 0.5 * (eta + 1.0) * B.hy;
   const double bz = (m.spec.z0 + iz * B.hz) + 0.5 * (zeta + 1.0) * B.hz;
-  if (m.spec.mapping != SDG_MAP_WARP) {
+  if (m.spec.mapping == SDG_MAP_BOX) {
     x[0] = bx;
     x[1] = by + B.vg * t;
     x[2] = bz;
@@ -309,6 +316,11 @@ void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, doub
   x[0] = bx + A * B.hx * sp * sy * sz;
   x[1] = by + A * B.hy * sp * sz + B.vg * t;
   x[2] = bz + A * B.hz * sp * sy;
+  if (m.spec.mapping == SDG_MAP_ANNULUS) {  // (x, theta, r) -> (x, r sin theta, r cos theta)
+    const double th = x[1], r = x[2];
+    x[1] = r * std::sin(th);
+    x[2] = r * std::cos(th);
+  }
 }
 
 namespace {
@@ -327,6 +339,22 @@ void relative_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi,
   x[0] = 0.5L * xi * h[0] + A * h[0] * (sp * sy * sz - cp * cy * cz);
   x[1] = 0.5L * eta * h[1] + A * h[1] * (sp * sz - cp * cz);
   x[2] = 0.5L * zeta * h[2] + A * h[2] * (sp * sy - cp * cy);
+  if (m.spec.mapping == SDG_MAP_ANNULUS) {
+    const ldm th = m.spec.y0 + h[1] * (iy + 0.5L * (eta + 1.0L)) + A * h[1] * sp * sz;
+    const ldm rr = m.spec.z0 + h[2] * (iz + 0.5L * (zeta + 1.0L)) + A * h[2] * sp * sy;
+    const ldm thc = m.spec.y0 + h[1] * (iy + 0.5L) + A * h[1] * cp * cz;
+    const ldm rc = m.spec.z0 + h[2] * (iz + 0.5L) + A * h[2] * cp * cy;
+    x[1] = rr * std::sin(th) - rc * std::sin(thc);
+    x[2] = rr * std::cos(th) - rc * std::cos(thc);
+  }
+}
+
+// Absolute radius (annulus grid-velocity potential psi = r^2 / 2), long double.
+ldm radius_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, double eta, double zeta) {
+  const BandGeom& B = m.bands[b];
+  const ldm tx = (ix + 0.5L * (xi + 1.0L)) / B.nx, ty = (iy + 0.5L * (eta + 1.0L)) / m.spec.ny;
+  const ldm sp = sinpi_exact<ldm>(tx), sy = sinpi_exact<ldm>(2.0L * ty);
+  return m.spec.z0 + static_cast<ldm>(B.hz) * (iz + 0.5L * (zeta + 1.0L)) + static_cast<ldm>(m.spec.warp) * B.hz * sp * sy;
 }
 
 // Metric terms of one element (conservative curl form, Kopriva 2006):
@@ -382,6 +410,26 @@ struct ElemMetricBuilder {
           out[idx(a, b, c)] = acc;
         }
   }
+  // Annulus: contravariant grid velocity per unit omega on the LGL grid,
+  // VL^i = [curl_xi I^N(psi grad_xi X_0)]_i with psi = r^2 / 2 (vg / omega = curl(psi e_x)).
+  void grid_velocity(const MeshGeom& m, int b, int ix, int iy, int iz, const std::vector<ldm>& dXL,
+                     std::vector<ldm>& VL) const {
+    std::vector<ldm> At(3 * n3), dV(n3);
+    VL.assign(3 * n3, 0.0L);
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < n; ++q)
+        for (int r = 0; r < n; ++r) {
+          const ldm rr = radius_point(m, b, ix, iy, iz, lgl.x[p], lgl.x[q], lgl.x[r]);
+          for (int k = 0; k < 3; ++k) At[k * n3 + idx(p, q, r)] = 0.5L * rr * rr * dXL[(3 * k) * n3 + idx(p, q, r)];
+        }
+    for (int i = 0; i < 3; ++i) {
+      const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+      deriv(At.data() + i2 * n3, i1, dV.data());
+      for (int g = 0; g < n3; ++g) VL[i * n3 + g] = dV[g];
+      deriv(At.data() + i1 * n3, i2, dV.data());
+      for (int g = 0; g < n3; ++g) VL[i * n3 + g] -= dV[g];
+    }
+  }
   void build(const MeshGeom& m, int b, int ix, int iy, int iz, std::vector<ldm>& JaL, std::vector<ldm>& dXL) const {
     std::vector<ldm> X(3 * n3), V(3 * n3), dV(n3);
     JaL.assign(9 * n3, 0.0L);
@@ -413,7 +461,7 @@ struct ElemMetricBuilder {
   // face's own geometry only: the normal component of the curl needs the
   // tangential derivatives on the face layer alone.  A face's two slots are
   // filled from the same element and side, so they hold identical bits.
-  void face(const MeshGeom& m, int b, int ix, int iy, int iz, int side, double* out) const {
+  void face(const MeshGeom& m, int b, int ix, int iy, int iz, int side, double* out, int fw) const {
     const int d = side / 2;
     const double lay = (side & 1) ? 1.0 : -1.0;
     const int p1 = d == 0 ? 1 : 0, p2 = d == 2 ? 1 : 2;  // face index (a, b) runs along (p1, p2)
@@ -462,22 +510,45 @@ struct ElemMetricBuilder {
       dv(V1.data(), a2.data());
       for (int g = 0; g < n2; ++g) J[c * n2 + g] = -sgn * (a1[g] - a2[g]);
     }
+    // Annulus: normal grid velocity per unit omega, sJ (vg / omega) . n = [curl_xi (psi grad_xi X_0)]_d.
+    const bool ann = m.spec.mapping == SDG_MAP_ANNULUS;
+    std::vector<ldm> W(n2, 0.0L);
+    if (ann) {
+      for (int u = 0; u < n; ++u)
+        for (int v = 0; v < n; ++v) {
+          double r[3];
+          r[d] = lay;
+          r[p1] = lgl.x[u];
+          r[p2] = lgl.x[v];
+          const ldm rr = radius_point(m, b, ix, iy, iz, r[0], r[1], r[2]);
+          V1[u * n + v] = 0.5L * rr * rr * D1[u * n + v];  // psi dX_0/dxi_p1
+          V2[u * n + v] = 0.5L * rr * rr * D2[u * n + v];  // psi dX_0/dxi_p2
+        }
+      du(V2.data(), a1.data());
+      dv(V1.data(), a2.data());
+      for (int g = 0; g < n2; ++g) W[g] = sgn * (a1[g] - a2[g]);
+    }
     for (int a = 0; a < n; ++a)
       for (int bb = 0; bb < n; ++bb) {
-        ldm v[3];
-        for (int c = 0; c < 3; ++c) {
+        ldm v[4];
+        for (int c = 0; c < (ann ? 4 : 3); ++c) {
+          const ldm* src = c < 3 ? J.data() + c * n2 : W.data();
           ldm acc = 0.0L;
           for (int u = 0; u < n; ++u) {
             ldm inner = 0.0L;
-            for (int w = 0; w < n; ++w) inner += L[bb * n + w] * J[c * n2 + u * n + w];
+            for (int w = 0; w < n; ++w) inner += L[bb * n + w] * src[u * n + w];
             acc += L[a * n + u] * inner;
           }
           v[c] = acc;
         }
         const ldm sj = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-        double* q = out + (a * n + bb) * 4;
+        double* q = out + (a * n + bb) * fw;
         for (int c = 0; c < 3; ++c) q[c] = static_cast<double>(v[c] / sj);
         q[3] = static_cast<double>(sj);
+        if (ann) {
+          q[4] = static_cast<double>(v[3] / sj);
+          q[5] = 0.0;
+        }
       }
   }
 };
@@ -487,13 +558,17 @@ CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTo
   const int n = sol.n, n2 = n * n, n3 = n2 * n;
   const int ne = static_cast<int>(topo.gids.size());
   CurvedMetrics out;
-  out.met.assign(static_cast<size_t>(ne) * n3 * 10, 0.0);
-  out.fmet.assign(static_cast<size_t>(ne) * 6 * n2 * 4, 0.0);
+  const bool ann = m.spec.mapping == SDG_MAP_ANNULUS;
+  out.mw = ann ? 13 : 10;
+  out.fw = ann ? 6 : 4;
+  const int mw = out.mw, fw = out.fw;
+  out.met.assign(static_cast<size_t>(ne) * n3 * mw, 0.0);
+  out.fmet.assign(static_cast<size_t>(ne) * 6 * n2 * fw, 0.0);
   const ElemMetricBuilder mb(sol);
   // Elements are independent: split them over the host threads (setup only).
   auto work = [&](int e_lo, int e_hi, std::string* err) {
     try {
-      std::vector<ldm> JaL, dXL, Ja(9 * n3), dX(9 * n3);
+      std::vector<ldm> JaL, dXL, Ja(9 * n3), dX(9 * n3), VL, Vs(3 * n3);
       for (int e = e_lo; e < e_hi; ++e) {
         const int* c = topo.coords.data() + 4 * e;
         mb.build(m, c[0], c[1], c[2], c[3], JaL, dXL);
@@ -501,8 +576,14 @@ CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTo
           mb.interp3(JaL.data() + q * n3, Ja.data() + q * n3);
           mb.interp3(dXL.data() + q * n3, dX.data() + q * n3);
         }
+        if (ann) {
+          mb.grid_velocity(m, c[0], c[1], c[2], c[3], dXL, VL);
+          for (int i = 0; i < 3; ++i) mb.interp3(VL.data() + i * n3, Vs.data() + i * n3);
+        }
         for (int g = 0; g < n3; ++g) {
-          double* o = out.met.data() + (static_cast<size_t>(e) * n3 + g) * 10;
+          double* o = out.met.data() + (static_cast<size_t>(e) * n3 + g) * mw;
+          if (ann)
+            for (int i = 0; i < 3; ++i) o[10 + i] = static_cast<double>(Vs[i * n3 + g]);
           for (int q = 0; q < 9; ++q) o[q] = static_cast<double>(Ja[q * n3 + g]);
           const ldm a00 = dX[0 * n3 + g], a01 = dX[1 * n3 + g], a02 = dX[2 * n3 + g];
           const ldm a10 = dX[3 * n3 + g], a11 = dX[4 * n3 + g], a12 = dX[5 * n3 + g];
@@ -512,14 +593,14 @@ CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTo
           o[9] = static_cast<double>(1.0L / jac);
         }
         for (int side = 0; side < 6; ++side) {
-          double* o = out.fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * 4;
+          double* o = out.fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * fw;
           const Nbr nb = neighbour(m, c[0], c[1], c[2], c[3], side);
           if ((side & 1) == 0 && nb.kind == 0) {
             // Minus side of a conforming face: the face's metrics are those of the
             // minus element (whose plus side it is), bit for bit, on every rank.
-            mb.face(m, nb.band, nb.ix, nb.iy, nb.iz, nb.side, o);
+            mb.face(m, nb.band, nb.ix, nb.iy, nb.iz, nb.side, o, fw);
           } else {
-            mb.face(m, c[0], c[1], c[2], c[3], side, o);
+            mb.face(m, c[0], c[1], c[2], c[3], side, o, fw);
           }
         }
       }

@@ -124,6 +124,7 @@ void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, doub
 // side; a conforming face carries the minus element's values in both slots.
 struct CurvedMetrics {
   std::vector<double> met, fmet;
+  int mw = 10, fw = 4;  // doubles per node (Ja 9, 1/J [, V 3 annulus]) / per face node (n 3, sJ [, vg.n/omega, pad])
 };
 CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTopology& topo);
 

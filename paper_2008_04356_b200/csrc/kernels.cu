@@ -262,7 +262,7 @@ __device__ __forceinline__ void map_position(const ElemConsts& C, const int* crd
   x[0] = (B.x_lo + crd[1] * B.hx) + 0.5 * (xi + 1.0) * B.hx;
   x[1] = (C.y0 + crd[2] * B.hy) + 0.5 * (eta + 1.0) * B.hy;
   x[2] = (C.z0 + crd[3] * B.hz) + 0.5 * (zeta + 1.0) * B.hz;
-  if (C.mapping == SDG_MAP_WARP) {
+  if (C.mapping != SDG_MAP_BOX) {
     const double tx = (crd[1] + 0.5 * (xi + 1.0)) / B.nxd, ty = (crd[2] + 0.5 * (eta + 1.0)) / C.ny,
                  tz = (crd[3] + 0.5 * (zeta + 1.0)) / C.nz;
     const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
@@ -271,6 +271,13 @@ __device__ __forceinline__ void map_position(const ElemConsts& C, const int* crd
     x[2] += C.warp * B.hz * sp * sy;
   }
   x[1] += B.vg * t;
+  if (C.mapping == SDG_MAP_ANNULUS) {  // (x, theta, r) -> (x, r sin theta, r cos theta)
+    double sn, cs;
+    sincos(x[1], &sn, &cs);
+    const double r = x[2];
+    x[1] = r * sn;
+    x[2] = r * cs;
+  }
 }
 
 // Physical position of face node (a, b) of `side` at time t.
@@ -825,10 +832,12 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_suggest_dt(const __grid_co
   if (e < P.E) {
     const double* u = P.U + (static_cast<size_t>(e) * N3 + t) * 5;
     const BandD& B = C.bands[P.coords[4 * e]];
+    const bool ann = C.mapping == SDG_MAP_ANNULUS;
     const double ir = 1.0 / u[0];
-    const double a = u[1] * ir, b = u[2] * ir - B.vg, c = u[3] * ir;
+    const double a = u[1] * ir, b = u[2] * ir - (ann ? 0.0 : B.vg), c = u[3] * ir;
     const double p = pressure(u, ir, C.gas);
     lm = sqrt(a * a + b * b + c * c) + sqrt(C.gas.gamma * p * ir);
+    if (ann) lm += fabs(B.vg) * (C.z0 + B.hz * C.nz);  // tip speed of a rotating band
   }
   red[threadIdx.x] = lm;
   __syncthreads();
@@ -836,7 +845,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_suggest_dt(const __grid_co
     double m = 0.0;
     for (int q = 0; q < N3; ++q) m = fmax(m, red[le * N3 + q]);
     const BandD& B = C.bands[P.coords[4 * e]];
-    const double h = fmin(B.hx, fmin(B.hy, B.hz));
+    const double h = C.mapping == SDG_MAP_ANNULUS ? fmin(B.hx, fmin(B.hy * C.z0, B.hz)) : fmin(B.hx, fmin(B.hy, B.hz));
     const double dt = cfl * h / (m * (2.0 * degree + 1.0));
     atomicMin(out, static_cast<unsigned long long>(__double_as_longlong(dt)));
   }
@@ -1154,7 +1163,8 @@ __global__ void __launch_bounds__(256) k_diag(const __grid_constant__ ElemConsts
     const int i = r / N2, j = (r / N1) % N1, k = r % N1;
     const int* crd = P.coords + 4 * e;
     const BandD& B = C.bands[crd[0]];
-    const double wq = C.w[i] * C.w[j] * C.w[k] * (C.mapping == SDG_MAP_WARP ? 1.0 / P.met[nd * 10 + 9] : B.jac);
+    const int mw = C.mapping == SDG_MAP_ANNULUS ? 13 : 10;
+    const double wq = C.w[i] * C.w[j] * C.w[k] * (C.mapping != SDG_MAP_BOX ? 1.0 / P.met[nd * mw + 9] : B.jac);
     const double* u = P.U + nd * 5;
     a[0] += wq * u[0];
     a[1] += wq * u[4];

@@ -512,7 +512,7 @@ void GpuRankSolver::build_consts() {
   consts_.mapping = mesh_.spec.mapping;
   consts_.ny = mesh_.spec.ny;
   consts_.nz = mesh_.spec.nz;
-  consts_.warp = mesh_.spec.mapping == SDG_MAP_WARP ? mesh_.spec.warp : 0.0;
+  consts_.warp = mesh_.spec.mapping != SDG_MAP_BOX ? mesh_.spec.warp : 0.0;
   const auto& g = cfg_.gas;
   consts_.gas = {g.gamma, g.gamma - 1.0, g.R, 1.0 / g.R, g.mu, -2.0 / 3.0 * g.mu,
                  g.gamma * g.R * g.mu / ((g.gamma - 1.0) * g.Pr), g.mu > 0.0 ? 1 : 0};
@@ -552,7 +552,7 @@ void GpuRankSolver::upload_topology() {
     side_code_.upload(code, stream_);
   }
   coords_.upload(topo_.coords, stream_);
-  curved_ = mesh_.spec.mapping == SDG_MAP_WARP;
+  curved_ = mesh_.spec.mapping != SDG_MAP_BOX;
   if (curved_) {
     const CurvedMetrics cm = compute_metrics(mesh_, basis_, topo_);
     met_.upload(cm.met, stream_);
@@ -1827,7 +1827,7 @@ int sdg_metrics_host(const sdg_mesh_spec* mesh, int degree, int node_kind, int n
   return guarded(nullptr, [&] {
     if (n_ranks < 1 || rank < 0 || rank >= n_ranks) throw sdg::ConfigError("rank outside [0, n_ranks)");
     const sdg::MeshGeom m(*mesh);
-    if (mesh->mapping != SDG_MAP_WARP) throw sdg::ConfigError("metrics are stored for curved meshes only");
+    if (mesh->mapping == SDG_MAP_BOX) throw sdg::ConfigError("metrics are stored for curved meshes only");
     const sdg::Partition part = sdg::assign_ranks(m, n_ranks);
     const sdg::LocalTopology topo = sdg::build_topology(m, part, rank);
     *n_local = static_cast<long>(topo.gids.size());

@@ -73,3 +73,22 @@ def test_invalid_mapping_rejected():
         capi.metrics_host(T.mesh_spec(BANDS3, ny=4, nz=3, warp=5.0), 3, T.NODES_GAUSS)  # folded mapping
     with pytest.raises(T.ConfigError):
         capi.metrics_host(T.mesh_spec(BANDS3, ny=4, nz=3), 3, T.NODES_GAUSS)  # affine: no stored metrics
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+@pytest.mark.parametrize("degree", [2, 5])
+@pytest.mark.parametrize("warp", [None, 0.1])
+def test_product_annulus_metrics_match_oracle(kind, degree, warp):
+    """SDG_MAP_ANNULUS: metrics plus the contravariant grid velocity (per node) and
+    (vg / omega) . n (per face node) of the product host agree with the oracle."""
+    mesh = T.annulus_spec([(2, 1.0, 0.0), (2, 1.0, 0.8)], 8, 2, 0.5, 1.0, warp=warp)
+    met, fmet = capi.metrics_host(mesh, degree, kind)
+    o = P.Oracle3D(mesh, T.solver_config(degree, kind, case=T.freestream()))
+    omet, ofmet = o.metrics()
+    assert met.shape == omet.shape and met.shape[2] == 13 and fmet.shape[3] == 6
+    assert np.abs(met - omet).max() <= 1e-15 * np.abs(omet).max()
+    assert np.abs(fmet - ofmet).max() <= 1e-15 * np.abs(ofmet).max()
+    for r in range(3):
+        gids = np.array(capi.plan(mesh, 3, r)["elements"])
+        m3, f3 = capi.metrics_host(mesh, degree, kind, 3, r)
+        assert np.array_equal(m3, met[gids]) and np.array_equal(f3, fmet[gids])

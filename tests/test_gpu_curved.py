@@ -1,4 +1,4 @@
-"""Curved hexahedra (SDG_MAP_WARP) on the CUDA path vs the CPU oracle, through
+"""Curved hexahedra (SDG_MAP_WARP) and the rotating annulus (SDG_MAP_ANNULUS) on the CUDA path vs the CPU oracle, through
 the C-ABI (k_gradient_curved / k_update_curved, csrc/curved.cuh).
 
 Same tolerances as tests/test_gpu_parity.py: state relative Linf <= 1e-12
@@ -146,3 +146,81 @@ def test_curved_multi_wave_mesh_matches_oracle():
     g.step(dt, 2)
     o.step(dt, 2)
     assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+# ---------------------------------------------------------------- rotating annulus (SDG_MAP_ANNULUS)
+def rotor(ne=2, warp=0.1, omega=0.8):
+    """BASELINE configs[2] shape: stator | rotor annulus r in [0.5, 1], full circle, axial split."""
+    return T.annulus_spec([(ne, 1.0, 0.0), (ne, 1.0, omega)], 4 * ne, ne, 0.5, 1.0, warp=warp)
+
+
+AXIAL_WAVE = dict(a=(1.0, 0.0, 0.0), k=(1.0, 0.0, 0.0))
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+@pytest.mark.parametrize("mu", [0.0, 1e-3])
+@pytest.mark.parametrize("t", [0.0, 0.37, 3.1])
+def test_rotating_annulus_residual_matches_oracle(kind, mu, t):
+    mesh = rotor()
+    cfg = T.solver_config(3, kind, mu=mu, case=T.density_wave(**AXIAL_WAVE))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    g.set_initial_condition(0.0)
+    assert rel_linf(g.field(), o.field()) <= 1e-15
+    u = o.field()
+    assert rel_linf(g.compute_residual(t, u), o.compute_residual(t, u)) <= 1e-12
+    if mu > 0.0:
+        assert rel_linf(g.compute_gradients(t, u), o.compute_gradients(t, u)) <= 1e-12
+
+
+@pytest.mark.parametrize("degree", [1, 2, 3, 4, 5, 6, 7])
+def test_rotating_annulus_one_step_all_degrees(degree):
+    mesh = rotor(warp=0.05)
+    cfg = T.solver_config(degree, T.NODES_GAUSS, mu=1e-3, case=T.density_wave(**AXIAL_WAVE))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.4)
+    assert abs(g.suggest_dt(0.4) - dt) <= 1e-14 * dt
+    g.step(dt)
+    o.step(dt)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+def test_rotating_annulus_hundred_stages_and_free_stream():
+    mesh = rotor()
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave(**AXIAL_WAVE))
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt, 20)
+    o.step(dt, 20)
+    assert rel_linf(g.field(), o.field()) <= 1e-10
+    assert g.total_rebuilds() == o.total_rebuilds()
+    fs = gpu_solver(mesh, T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.freestream(v=(1.0, 0.0, 0.0))))
+    fs.set_initial_condition(0.0)
+    u = fs.field()
+    for t in (0.0, 0.2, 1.7):
+        assert np.abs(fs.compute_residual(t, u)).max() < 1e-12
+    fs.step(fs.suggest_dt(0.5), 10)
+    assert fs.diagnostics(fs.time())["max_deviation"] < 1e-12
+
+
+def test_rotating_annulus_rank_split_keeps_the_bits():
+    """Stator and rotor on different ranks (the mortar exchange carries the
+    rotor/stator coupling) equals one rank bit for bit."""
+    from paper_2008_04356_b200 import capi
+    mesh = rotor()
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave(**AXIAL_WAVE))
+    n_el = 2 * 2 * 8 * 2
+
+    def body(s):
+        s.set_initial_condition(0.0)
+        s.step(0.01, 5)
+        return s.local_element_ids(), s.field()
+
+    ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub="ann1"), n_el, 4)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, 2, body, hub="ann2"), n_el, 4)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
