@@ -45,9 +45,10 @@ def parse():
     p.add_argument("--elems", type=int, default=64, help="elements per direction per GPU (weak scaling)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--mesh", default="tgv", choices=["tgv", "warped"],
+    p.add_argument("--mesh", default="tgv", choices=["tgv", "warped", "rotor"],
                    help="tgv: affine hexahedra (configs[4]); warped: the same case on curved hexahedra "
-                        "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3])")
+                        "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3]); rotor: configs[3] "
+                        "stand-in, stator/rotor/stator annulus with a rotating middle block (SDG_MAP_ANNULUS)")
     return p.parse_args()
 
 
@@ -63,8 +64,54 @@ def tgv_mesh(T, elems_x, elems_yz, warp=None):
 WARP = 0.05  # BASELINE configs[3]: "sinusoidal mesh warping of amplitude 5% of element size"
 
 
+def rotor_workload(args, world):
+    """BASELINE configs[3] stand-in (turbine-scale synthetic): three axial blocks
+    (stator, rotor, stator) of an annulus r in [0.8, 1] with two sliding
+    interfaces, 5% warping inside the blocks, tip Mach 0.4, axial inflow M = 0.3,
+    Re = 8e5 on the mean-radius arc of a 20-degree sector.  The full circle
+    replaces the 20-degree periodic sector (rotational periodicity of the
+    momentum across a sector seam is not implemented).  Per GPU:
+    (elems) axial x (4 elems) around x (elems / 4) radial elements."""
+    from paper_2008_04356_b200 import types as T
+    gamma, mach, rho0, u0 = 1.4, 0.3, 2.0, 1.0
+    p0 = rho0 * u0 * u0 / (gamma * mach * mach)
+    c0 = math.sqrt(gamma * p0 / rho0)
+    r_in, r_out = 0.8, 1.0
+    omega = 0.4 * c0 / r_out
+    chord = 0.5 * (r_in + r_out) * math.pi / 9.0
+    mu = rho0 * u0 * chord / 8e5
+    nx = args.elems * world
+    base, rem = divmod(nx, 3)
+    n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
+    bands = [(n[0], 1.0, 0.0), (n[1], 1.0, omega), (n[2], 1.0, 0.0)]
+    n_theta, n_r = 4 * args.elems, max(1, args.elems // 4)
+    mesh = T.annulus_spec(bands, n_theta, n_r, r_in, r_out, length=1.0, warp=WARP)
+    cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=gamma, R=1.0, mu=mu, Pr=0.72,
+                          case=T.density_wave(alpha=0.02, a=(u0, 0.0, 0.0), k=(2.0, 0.0, 0.0), p0=p0))
+    n1 = args.degree + 1
+    E = nx * n_theta * n_r
+    conf = {
+        "workload": f"BASELINE configs[3] stand-in: stator/rotor/stator annulus r in [{r_in}, {r_out}] (full circle "
+                    f"for the 20-degree sector), 2 sliding interfaces, rotor omega {omega:.4f} (tip Mach 0.4), "
+                    f"warp {WARP}, axial M=0.3 density wave, Re=8e5, {nx // world}x{n_theta}x{n_r} elements/GPU, "
+                    f"N={args.degree} Gauss, viscous",
+        "geometry": "curved",
+        "elements": E,
+        "elements_per_gpu": E // world,
+        "degree": args.degree,
+        "nodes": "gauss",
+        "dof": E * n1 ** 3,
+        "bands_nx": n,
+        "l2_policy": "inputs larger than L2 (state %.0f MB per GPU)" % (E // world * n1 ** 3 * 40 / 1e6),
+        "parallelism": f"dp{world} (element partition, NCCL halo + mortar exchange)",
+    }
+    return mesh, cfg, conf, E * n1 ** 3
+
+
 def workload(args, world):
     from paper_2008_04356_b200 import types as T
+    if args.mesh == "rotor":
+        return rotor_workload(args, world)
     curved = args.mesh == "warped"
     mesh, bands = tgv_mesh(T, args.elems * world, args.elems, warp=WARP if curved else None)
     cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
@@ -151,8 +198,13 @@ def cpu_baseline(args, conf, timeout_s=20.0):
     P.oracle_lib().orc_set_threads(threads)
     e = 6
     curved = conf.get("geometry") == "curved"
-    mesh, bands = tgv_mesh(T, e, e, warp=WARP if curved else None)
-    cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
+    if args.mesh == "rotor":
+        small = argparse.Namespace(**{**vars(args), "elems": 8})
+        mesh, cfg, _, _ = rotor_workload(small, 1)
+        e = "8x32x2"
+    else:
+        mesh, bands = tgv_mesh(T, e, e, warp=WARP if curved else None)
+        cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
     o = P.Oracle3D(mesh, cfg)
     o.set_initial_condition(0.0)
     dt = 1e-3
@@ -172,8 +224,9 @@ def cpu_baseline(args, conf, timeout_s=20.0):
     except OSError:
         pass
     out = {"value": dof * 5 * steps / el, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same TGV case"
-                     f"{' (curved)' if curved else ''} at {e}^3 elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
+           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same "
+                     f"{'rotor annulus' if args.mesh == 'rotor' else 'TGV'} case"
+                     f"{' (curved)' if curved else ''} at {e if isinstance(e, str) else f'{e}^3'} elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
     try:
         out["reference_2d"] = reference_2d(args.degree, seconds=min(8.0, timeout_s))
     except Exception as ex:  # supplementary: never fail the bench line over it
@@ -257,9 +310,11 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     extra = {}
     # This implementation's fused dataflow.
     per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 18), "gradient": 8 * E * (5 * n3 + 6 * n2 * 9)}
-    if curved:  # + per-node metrics (10 doubles) and per-side face metrics (4 doubles per face node), both kernels
+    if curved:  # + per-node metrics (10 doubles, 13 on the annulus) and per-side face metrics (4 / 6 doubles per
+        # face node), read by both kernels
+        mw, fw = (13, 6) if args.mesh == "rotor" else (10, 4)
         for k in per_kernel:
-            per_kernel[k] += 8 * E * (10 * n3 + 6 * n2 * 4)
+            per_kernel[k] += 8 * E * (mw * n3 + 6 * n2 * fw)
     for name, byts in per_kernel.items():
         ms, cnt = kt.get(name, (0.0, 0))
         if cnt:
