@@ -601,9 +601,17 @@ struct CB {
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3, ML = MW * N3, FM = 6 * FW * N2, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
   // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
-  static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB + 5 * N3 + 24 * N2 + 30 * N2;
+  // (face flux and lift* are written over the element's own traces and Fv.n once phase 1 has read them)
+  static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB + 5 * N3;
   // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
-  static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 12 * N3 + 24 * N2;
+  // (the gradient is written over the state and metrics once every node's gradient is computed)
+  static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 24 * N2;
+  static constexpr int KF = (6 * N2 + N3 - 1) / N3;  // face nodes per thread
+#ifndef SDG_CURVED_MINB
+#define SDG_CURVED_MINB 3
+#endif
+  static constexpr int MINB = N1 == 6 ? SDG_CURVED_MINB : 1;  // resident CTAs per SM at N = 5 (shared memory fits 3)
+  static_assert(12 * N3 <= EL + ML, "gradient aliases state + metrics");
   static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
   static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
   static_assert(N1 % 2 == 0, "bulk path needs even N+1");
@@ -715,7 +723,7 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
 }
 
 template <int N1, bool ROT>
-__global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
+__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
                                                                             FieldPtrs P, StageArgs A) {
   using D = CB<N1, ROT>;
   constexpr int MW = D::MW, FW = D::FW;
@@ -740,8 +748,8 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_gradient_curved_b(cons
   double* sTr = sfm + D::FM;
   double* sNb = sTr + 6 * D::TS;
   double* sq = sNb + 6 * D::TS;
-  double* sG = sq + 4 * N3;
-  double* sLift = sG + 12 * N3;
+  double* sLift = sq + 4 * N3;
+  double* sG = sU;  // after the gradient phase
   const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
   const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();  // barrier init visible, tables loaded
@@ -777,17 +785,20 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_gradient_curved_b(cons
     }
   }
   __syncthreads();
+  double g[12];
   if (active) {
     const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-    double g[12];
     node_gradient_curved_aos<N1, MW, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
-#pragma unroll
-    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
     if (P.grad_out != nullptr) {
       double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
 #pragma unroll
       for (int c = 0; c < 12; ++c) go[c] = g[c];
     }
+  }
+  __syncthreads();  // every node's gradient is computed: state and metrics are dead
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
   }
   __syncthreads();
   if (!active) return;
@@ -815,7 +826,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_gradient_curved_b(cons
 }
 
 template <int N1, bool VISC, bool ROT>
-__global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_update_curved_b(const __grid_constant__ ElemConsts C,
+__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_update_curved_b(const __grid_constant__ ElemConsts C,
                                                                           FieldPtrs P, StageArgs A) {
   using D = CB<N1, ROT>;
   constexpr int MW = D::MW, FW = D::FW;
@@ -842,15 +853,18 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_update_curved_b(const 
   double* sFv = sTr + 6 * D::TS;
   double* sNb = sFv + 6 * D::FS;
   double* sF = sNb + 6 * D::NB;
-  double* sLift = sF + 5 * N3;
-  double* sFlux = sLift + 24 * N2;
+  double* sFlux = sTr;  // written after phase 1 has read the own traces / Fv.n
+  double* sLift = sFv;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
   const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
   const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();
   mbar_wait(bar, 0);
 
-  // Phase 1: numerical flux along each face node's normal -> sFlux; lift* -> sLift.
+  // Phase 1: numerical flux along each face node's normal and lift*, kept in
+  // registers until every thread has read its own traces / Fv.n, then stored
+  // over them (sFlux, sLift).
+  double rflux[D::KF][5], rlift[D::KF][4];
   if (active) {
     if (VISC) {
       double q[4];
@@ -858,7 +872,10 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_update_curved_b(const 
 #pragma unroll
       for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
     }
-    for (int it = t; it < 6 * N2; it += N3) {
+#pragma unroll
+    for (int kf = 0; kf < D::KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
       const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
       const double* own = sTr + s * D::TS + f * 5;
       double nrm[3], vgn;
@@ -915,10 +932,25 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS) k_update_curved_b(const 
       }
       if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own);
 #pragma unroll
-      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = flux[v];
+      for (int v = 0; v < 5; ++v) rflux[kf][v] = flux[v];
       if (VISC) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+        for (int c = 0; c < 4; ++c) rlift[kf][c] = lift[c];
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int kf = 0; kf < D::KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
+      const int s = it / N2, f = it % N2;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = rflux[kf][v];
+      if (VISC) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = rlift[kf][c];
       }
     }
   }
