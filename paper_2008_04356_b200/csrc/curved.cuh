@@ -8,8 +8,10 @@
 //   BR1 gradient  J g_c = sum_d [surface q* (n sJ)_c - Dhat (Ja^d_c q)]   (assemble_gradients, :729-768)
 //   face flux     Roe / viscous along the face's unit normal n, vg_n = vg . n   (flux.cpp:68-133)
 //   surface lift  +- (l(+-1)/w) (sJ / J) F*                  (apply_all_faces, :547-582)
-// Metrics per node: Ja^d_c at [3d + c] and 1/J (10 doubles, node-major);
-// per local side and face node: the unit normal along +xi_dir and sJ (4 doubles).
+// Device layout (solver.cu upload_topology), per element structure-of-arrays so
+// that the threads of a warp read consecutive words: met[e][c][node], c < MW
+// (Ja^d_c at c = 3d + c', 1/J at 9 [, V^d at 10 + d]); fmet[e][side][c][f], c < FW
+// (unit normal along +xi_dir at c < 3, sJ at 3 [, (vg / omega) . n at 4]).
 // Both slots of a conforming face hold identical bits (host.cpp compute_metrics),
 // so both elements evaluate the face flux identically, as in the affine kernels.
 
@@ -47,17 +49,23 @@ __device__ __forceinline__ void rotate_yz(const Rot& r, double& y, double& z) {
   z = b;
 }
 // Unit normal of a face node at the stage time and vg . n.
-template <bool ROT>
-__device__ __forceinline__ void face_normal(const double* q, const Rot& r, const BandD& B, double* n, double& vgn) {
+// sfm: one element's face metrics [side][c][f].
+template <int N2, int FW, bool ROT>
+__device__ __forceinline__ void face_normal(const double* sfm, int s, int f, const Rot& r, const BandD& B, double* n,
+                                            double& vgn) {
+  const double* q = sfm + s * FW * N2 + f;
   n[0] = q[0];
-  n[1] = q[1];
-  n[2] = q[2];
+  n[1] = q[N2];
+  n[2] = q[2 * N2];
   if (ROT) {
     rotate_yz(r, n[1], n[2]);
-    vgn = B.vg * q[4];
+    vgn = B.vg * q[4 * N2];
   } else {
-    vgn = B.vg * q[1];
+    vgn = B.vg * n[1];
   }
+}
+__device__ __forceinline__ double face_sj(const double* sfm, int s, int f, int n2, int fw) {
+  return sfm[(s * fw + 3) * n2 + f];
 }
 
 // Flat, coalesced load of EPB consecutive elements' node-major NC-vectors into
@@ -73,10 +81,9 @@ __device__ __forceinline__ void load_soa(const double* __restrict__ src, int e0,
   }
 }
 
-// Face metrics of EPB consecutive elements (6 x N2 x 4 contiguous per element).
-template <int N1, int EPB, int FW>
-__device__ __forceinline__ void load_fmet(const double* __restrict__ src, int e0, int E, double* dst, int per) {
-  constexpr int W = 6 * N1 * N1 * FW;
+// W contiguous doubles per element of EPB consecutive elements (metrics, face metrics).
+template <int W, int EPB>
+__device__ __forceinline__ void load_flat(const double* __restrict__ src, int e0, int E, double* dst, int per) {
   const int n_el = min(EPB, E - e0);
   const double* s = src + static_cast<size_t>(e0) * W;
   for (int f = threadIdx.x; f < n_el * W; f += blockDim.x) {
@@ -199,15 +206,15 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
   for (int d = 0; d < 3; ++d) {
     const int ia = d == 0 ? i : (d == 1 ? j : k);
     const int f = d == 0 ? j * N1 + k : (d == 1 ? i * N1 + k : i * N1 + j);
-    const double* np = sfm + ((2 * d + 1) * N2 + f) * FW;
-    const double* nm = sfm + ((2 * d) * N2 + f) * FW;
-    const double sp = lw[N1 + ia] * np[3], sm = lw[ia] * nm[3];
+    const double* np = sfm + (2 * d + 1) * FW * N2 + f;  // [c][f]
+    const double* nm = sfm + (2 * d) * FW * N2 + f;
+    const double sp = lw[N1 + ia] * np[3 * N2], sm = lw[ia] * nm[3 * N2];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const double lp = sLift[((2 * d + 1) * 4 + q) * N2 + f] * sp;
       const double lm = sLift[((2 * d) * 4 + q) * N2 + f] * sm;
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk) surf[3 * q + kk] += lp * np[kk] - lm * nm[kk];
+      for (int kk = 0; kk < 3; ++kk) surf[3 * q + kk] += lp * np[kk * N2] - lm * nm[kk * N2];
     }
   }
 #pragma unroll
@@ -234,8 +241,8 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(cons
   const int e0 = P.e_first + blockIdx.x * EPB;
   double* base = smem + TAB;
   load_soa<N1, EPB, 5>(P.U, e0, P.E, base, PER);
-  load_soa<N1, EPB, MW>(P.met, e0, P.E, base + 9 * N3, PER);
-  load_fmet<N1, EPB, FW>(P.fmet, e0, P.E, base + (21 + MW) * N3 + 54 * N2, PER);
+  load_flat<MW * N3, EPB>(P.met, e0, P.E, base + 9 * N3, PER);
+  load_flat<6 * FW * N2, EPB>(P.fmet, e0, P.E, base + (21 + MW) * N3 + 54 * N2, PER);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
   const bool active = e < P.E;
   double* su = base + le * PER;
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(cons
     const int typ = P.side_type[slot], idx = P.side_idx[slot];
     if (typ == kConforming) {
       double fv[4], nrm[3], vgn;
-      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
+      face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
       fv_n(sTr + (s * N2 + f) * 5, gt, nrm, C.gas, fv);
       double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
 #pragma unroll
@@ -312,8 +319,8 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
   const int e0 = P.e_first + blockIdx.x * EPB;
   double* elems = smem + TAB;
   load_soa<N1, EPB, 5>(P.U, e0, P.E, elems, PER);
-  load_soa<N1, EPB, MW>(P.met, e0, P.E, elems + 10 * N3, PER);
-  load_fmet<N1, EPB, FW>(P.fmet, e0, P.E, elems + (10 + MW) * N3 + 54 * N2, PER);
+  load_flat<MW * N3, EPB>(P.met, e0, P.E, elems + 10 * N3, PER);
+  load_flat<6 * FW * N2, EPB>(P.fmet, e0, P.E, elems + (10 + MW) * N3 + 54 * N2, PER);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
   const bool active = e < P.E;
   double* su = elems + le * PER;
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
 #pragma unroll
       for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b);
       double nrm[3], vgn;
-      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
+      face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
       const int slot = e * 6 + s;
       const int typ = P.side_type[slot], idx = P.side_idx[slot];
       double flux[5], lift[4];
@@ -497,7 +504,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
       const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
       const double l = lw[(s & 1) * N1 + ia];
       if (l != 0.0) {
-        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * FW + 3] * ij;
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * face_sj(sfm, s, f, N2, FW) * ij;
 #pragma unroll
         for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
       }
@@ -618,64 +625,6 @@ struct CB {
   static_assert(U_SMEM <= 227 * 1024 && G_SMEM <= 227 * 1024, "shared memory per CTA");
 };
 
-// Gradient at one node from AoS metrics sM[node][10] and SoA q.
-template <int N1, int MW, int FW, bool ROT>
-__device__ __forceinline__ void node_gradient_curved_aos(const double* tab, const double* sq, const double* sM,
-                                                         const double* sLift, const double* sfm, int i, int j, int k,
-                                                         const Rot& rot, double* g) {
-  constexpr int N2 = N1 * N1, N3 = N2 * N1;
-  const double* dh = tab;
-  const double* lw = tab + N1 * N1 + 2 * N1;
-  double acc[12];
-#pragma unroll
-  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const int ia = d == 0 ? i : (d == 1 ? j : k);
-    const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-    const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-    for (int m = 0; m < N1; ++m) {
-      const double c = dh[ia * N1 + m];
-      const int nd = base + m * stride;
-      const double* ja = sM + nd * MW + 3 * d;
-      const double ja0 = ja[0], ja1 = ja[1], ja2 = ja[2];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double cq = c * sq[q * N3 + nd];
-        acc[3 * q + 0] += cq * ja0;
-        acc[3 * q + 1] += cq * ja1;
-        acc[3 * q + 2] += cq * ja2;
-      }
-    }
-  }
-  const double ij = sM[((i * N1 + j) * N1 + k) * MW + 9];
-  double surf[12];
-#pragma unroll
-  for (int q = 0; q < 12; ++q) surf[q] = 0.0;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const int ia = d == 0 ? i : (d == 1 ? j : k);
-    const int f = d == 0 ? j * N1 + k : (d == 1 ? i * N1 + k : i * N1 + j);
-    const double* np = sfm + ((2 * d + 1) * N2 + f) * FW;
-    const double* nm = sfm + ((2 * d) * N2 + f) * FW;
-    const double sp = lw[N1 + ia] * np[3], sm = lw[ia] * nm[3];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double lp = sLift[((2 * d + 1) * 4 + q) * N2 + f] * sp;
-      const double lm = sLift[((2 * d) * 4 + q) * N2 + f] * sm;
-#pragma unroll
-      for (int kk = 0; kk < 3; ++kk) surf[3 * q + kk] += lp * np[kk] - lm * nm[kk];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 12; ++q) g[q] = ij * (surf[q] - acc[q]);
-  if (ROT) {  // computed with the t = 0 metrics: g(t) = R g
-#pragma unroll
-    for (int q = 0; q < 4; ++q) rotate_yz(rot, g[3 * q + 1], g[3 * q + 2]);
-  }
-}
-
 // Issue the bulk copies of one element tile (thread 0).  GRAD: neighbour
 // trace (conforming) or lift* (sliding) only; else trace + Fv.n or flux + lift*.
 template <int N1, bool ROT, bool GRAD, bool VISC>
@@ -788,7 +737,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_gra
   double g[12];
   if (active) {
     const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-    node_gradient_curved_aos<N1, MW, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
+    node_gradient_curved<N1, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
     if (P.grad_out != nullptr) {
       double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
 #pragma unroll
@@ -801,27 +750,38 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_gra
     for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
   }
   __syncthreads();
-  if (!active) return;
-  for (int it = t; it < 6 * N2; it += N3) {
-    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-    const double* ell = tab + N1 * N1 + (s & 1) * N1;
-    double gt[12];
+  // Fv.n of the 6 sides staged in the dead neighbour-trace region [side][f][4]
+  // (zero on sliding / Dirichlet sides) and bulk-stored as one contiguous block.
+  double* sOut = sNb;
+  if (active) {
+    for (int it = t; it < 6 * N2; it += N3) {
+      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+      const double* ell = tab + N1 * N1 + (s & 1) * N1;
+      double gt[12];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
-    const int slot = e * 6 + s;
-    const int typ = P.side_type[slot], idx = P.side_idx[slot];
-    if (typ == kConforming) {
-      double fv[4], nrm[3], vgn;
-      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
-      fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
-      double* dst = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
+      for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+      const int slot = e * 6 + s;
+      const int typ = P.side_type[slot], idx = P.side_idx[slot];
+      double fv[4] = {0.0, 0.0, 0.0, 0.0};
+      if (typ == kConforming) {
+        double nrm[3], vgn;
+        face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
+        fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
+      } else {
+        double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) dst[c] = fv[c];
-    } else {
-      double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+        for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+      }
 #pragma unroll
-      for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+      for (int c = 0; c < 4; ++c) sOut[s * D::FS + f * 4 + c] = fv[c];
     }
+    fence_proxy_async();
+  }
+  __syncthreads();
+  if (active && t == 0) {
+    bulk_s2g(P.fvn + static_cast<size_t>(e) * 6 * D::FS, sOut, 6 * D::FS * 8u);
+    bulk_commit();
+    bulk_wait_read0();
   }
 }
 
@@ -879,7 +839,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
       const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
       const double* own = sTr + s * D::TS + f * 5;
       double nrm[3], vgn;
-      face_normal<ROT>(sfm + (s * N2 + f) * FW, rot, B, nrm, vgn);
+      face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
       const double* nb = sNb + s * D::NB;
       const int typ = P.side_type[e * 6 + s];
       double flux[5], lift[4];
@@ -978,7 +938,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
     }
     if (VISC) {
       double g[12];
-      node_gradient_curved_aos<N1, MW, FW, ROT>(tab, sF, sM, sLift, sfm, i, j, k, rot, g);
+      node_gradient_curved<N1, FW, ROT>(tab, sF, sM, sLift, sfm, i, j, k, rot, g);
       const double div = g[0] + g[4] + g[8];
       const double mu = C.gas.mu, lam = C.gas.lam;
       const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
@@ -992,17 +952,17 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
         F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
       }
     }
-    const double* ja = sM + t * MW;
+    const double* ja = sM + t;  // [c][node]
     if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
 #pragma unroll
       for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const double wv = ROT ? B.vg * ja[10 + d] : 0.0;  // contravariant grid velocity
+      const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
+      const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
 #pragma unroll
-      for (int v = 0; v < 5; ++v)
-        Ft[d][v] = ja[3 * d] * F[0][v] + ja[3 * d + 1] * F[1][v] + ja[3 * d + 2] * F[2][v] - wv * u[v];
+      for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
     }
   }
 
@@ -1033,7 +993,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
   // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
   double du[5];
   if (active) {
-    const double ij = sM[t * MW + 9];
+    const double ij = sM[9 * N3 + t];
 #pragma unroll
     for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
     const double* lw = tab + N1 * N1 + 2 * N1;
@@ -1044,7 +1004,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
       const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
       const double l = lw[(s & 1) * N1 + ia];
       if (l != 0.0) {
-        const double c = ((s & 1) ? -1.0 : 1.0) * l * sfm[(s * N2 + f) * FW + 3] * ij;
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * face_sj(sfm, s, f, N2, FW) * ij;
 #pragma unroll
         for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
       }
@@ -1078,8 +1038,10 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
     *us = un;
   }
   __syncthreads();
-  if (!active) return;
-  {
+  // Admissibility (check_admissible, solver.cpp:892-906), then the traces of the
+  // new state staged in the dead neighbour region [side][f][5] and bulk-stored.
+  double* sOut = sNb;
+  if (active) {
     double w[5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) w[v] = sU[t * 5 + v];
@@ -1088,16 +1050,19 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_upd
 #pragma unroll
     for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
     if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+    for (int it = t; it < 6 * N2; it += N3) {
+      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
+      const double* ell = tab + N1 * N1 + (s & 1) * N1;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sOut[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+    }
+    fence_proxy_async();
   }
-  for (int it = t; it < 6 * N2; it += N3) {
-    const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-    const double* ell = tab + N1 * N1 + (s & 1) * N1;
-    double tr[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) tr[v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
-    double* dst = P.trace_out + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) dst[v] = tr[v];
+  __syncthreads();
+  if (active && t == 0) {
+    bulk_s2g(P.trace_out + static_cast<size_t>(e) * 6 * D::TS, sOut, 6 * D::TS * 8u);
+    bulk_commit();
+    bulk_wait_read0();
   }
 }
 

@@ -1163,8 +1163,9 @@ __global__ void __launch_bounds__(256) k_diag(const __grid_constant__ ElemConsts
     const int i = r / N2, j = (r / N1) % N1, k = r % N1;
     const int* crd = P.coords + 4 * e;
     const BandD& B = C.bands[crd[0]];
-    const int mw = C.mapping == SDG_MAP_ANNULUS ? 13 : 10;
-    const double wq = C.w[i] * C.w[j] * C.w[k] * (C.mapping != SDG_MAP_BOX ? 1.0 / P.met[nd * mw + 9] : B.jac);
+    const int mw = C.mapping == SDG_MAP_ANNULUS ? 13 : 10;  // device layout met[e][c][node] (curved.cuh)
+    const double wq = C.w[i] * C.w[j] * C.w[k] *
+                      (C.mapping != SDG_MAP_BOX ? 1.0 / P.met[(static_cast<size_t>(e) * mw + 9) * N3 + r] : B.jac);
     const double* u = P.U + nd * 5;
     a[0] += wq * u[0];
     a[1] += wq * u[4];

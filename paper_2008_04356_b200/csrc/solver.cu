@@ -555,8 +555,22 @@ void GpuRankSolver::upload_topology() {
   curved_ = mesh_.spec.mapping != SDG_MAP_BOX;
   if (curved_) {
     const CurvedMetrics cm = compute_metrics(mesh_, basis_, topo_);
-    met_.upload(cm.met, stream_);
-    fmet_.upload(cm.fmet, stream_);
+    // Device layout: per element structure-of-arrays, met[e][c][node] and
+    // fmet[e][side][c][f] (curved.cuh), so a warp's threads read consecutive words.
+    const int mw = cm.mw, fw = cm.fw;
+    std::vector<double> met(cm.met.size()), fmet(cm.fmet.size());
+    for (int e = 0; e < E_; ++e) {
+      for (int g = 0; g < n3_; ++g)
+        for (int c = 0; c < mw; ++c)
+          met[(static_cast<size_t>(e) * mw + c) * n3_ + g] = cm.met[(static_cast<size_t>(e) * n3_ + g) * mw + c];
+      for (int sd = 0; sd < 6; ++sd)
+        for (int f = 0; f < n2_; ++f)
+          for (int c = 0; c < fw; ++c)
+            fmet[((static_cast<size_t>(e) * 6 + sd) * fw + c) * n2_ + f] =
+                cm.fmet[((static_cast<size_t>(e) * 6 + sd) * n2_ + f) * fw + c];
+    }
+    met_.upload(met, stream_);
+    fmet_.upload(fmet, stream_);
     cuda_check(cudaStreamSynchronize(stream_), "metric upload");
   }
   err_.alloc(1);
