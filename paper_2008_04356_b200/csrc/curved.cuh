@@ -617,7 +617,9 @@ struct CB {
 #ifndef SDG_CURVED_MINB
 #define SDG_CURVED_MINB 3
 #endif
-  static constexpr int MINB = N1 == 6 ? SDG_CURVED_MINB : 1;  // resident CTAs per SM at N = 5 (shared memory fits 3)
+  // Resident CTAs per SM at N = 5: shared memory fits 3 (the annulus update kernel's 13 + 6-wide metrics: 2).
+  static constexpr int MINB_G = N1 == 6 ? SDG_CURVED_MINB : 1;
+  static constexpr int MINB_U = N1 == 6 ? (ROT ? 2 : SDG_CURVED_MINB) : 1;
   static_assert(12 * N3 <= EL + ML, "gradient aliases state + metrics");
   static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
   static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
@@ -672,7 +674,7 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
 }
 
 template <int N1, bool ROT>
-__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
+__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
                                                                             FieldPtrs P, StageArgs A) {
   using D = CB<N1, ROT>;
   constexpr int MW = D::MW, FW = D::FW;
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_gra
 }
 
 template <int N1, bool VISC, bool ROT>
-__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB) k_update_curved_b(const __grid_constant__ ElemConsts C,
+__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_update_curved_b(const __grid_constant__ ElemConsts C,
                                                                           FieldPtrs P, StageArgs A) {
   using D = CB<N1, ROT>;
   constexpr int MW = D::MW, FW = D::FW;
