@@ -609,7 +609,9 @@ struct CB {
   static constexpr int EL = 5 * N3, ML = MW * N3, FM = 6 * FW * N2, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
   // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
   // (face flux and lift* are written over the element's own traces and Fv.n once phase 1 has read them)
-  static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB + 5 * N3;
+  // (the staging buffer sF lives in the neighbour region, dead after phase 1)
+  static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB;
+  static_assert(5 * N3 <= 6 * NB, "staging buffer fits the neighbour region");
   // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
   // (the gradient is written over the state and metrics once every node's gradient is computed)
   static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 24 * N2;
@@ -617,9 +619,12 @@ struct CB {
 #ifndef SDG_CURVED_MINB
 #define SDG_CURVED_MINB 3
 #endif
+#ifndef SDG_CURVED_MINB_U
+#define SDG_CURVED_MINB_U 3
+#endif
   // Resident CTAs per SM at N = 5: shared memory fits 3 (the annulus update kernel's 13 + 6-wide metrics: 2).
   static constexpr int MINB_G = N1 == 6 ? SDG_CURVED_MINB : 1;
-  static constexpr int MINB_U = N1 == 6 ? (ROT ? 2 : SDG_CURVED_MINB) : 1;
+  static constexpr int MINB_U = N1 == 6 ? SDG_CURVED_MINB_U : 1;
   static_assert(12 * N3 <= EL + ML, "gradient aliases state + metrics");
   static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
   static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
@@ -814,7 +819,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
   double* sTr = sfm + D::FM;
   double* sFv = sTr + 6 * D::TS;
   double* sNb = sFv + 6 * D::FS;
-  double* sF = sNb + 6 * D::NB;
+  double* sF = sNb;  // q, flux staging and dudt: written only after phase 1 has read the neighbour slots
   double* sFlux = sTr;  // written after phase 1 has read the own traces / Fv.n
   double* sLift = sFv;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
@@ -828,12 +833,6 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
   // over them (sFlux, sLift).
   double rflux[D::KF][5], rlift[D::KF][4];
   if (active) {
-    if (VISC) {
-      double q[4];
-      prim4(sU + t * 5, C.gas, q);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
-    }
 #pragma unroll
     for (int kf = 0; kf < D::KF; ++kf) {
       const int it = t + kf * N3;
@@ -903,6 +902,12 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
   }
   __syncthreads();
   if (active) {
+    if (VISC) {
+      double q[4];
+      prim4(sU + t * 5, C.gas, q);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
+    }
 #pragma unroll
     for (int kf = 0; kf < D::KF; ++kf) {
       const int it = t + kf * N3;
@@ -1023,15 +1028,14 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
   if (A.mode == 1) {
     for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
       const int l = fI / (5 * N3), r = fI - l * 5 * N3;
-      P.out[static_cast<size_t>(e0) * 5 * N3 + fI] = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS +
-                                                          6 * D::NB + r];
+      P.out[static_cast<size_t>(e0) * 5 * N3 + fI] = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + r];
     }
     return;
   }
   for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
     const int l = fI / (5 * N3), r = fI - l * 5 * N3;
     double* us = base + l * PER + r;
-    const double dd = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + 6 * D::NB + r];
+    const double dd = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + r];
     const size_t g = static_cast<size_t>(e0) * 5 * N3 + fI;
     const double rg = A.rk_a * P.reg[g] + A.dt * dd;
     const double un = *us + A.rk_b * rg;
