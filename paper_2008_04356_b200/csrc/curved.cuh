@@ -599,14 +599,19 @@ void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a
 // Own traces are staged from the trace buffer, so both elements of a face use
 // the same stored bits.  The RK register is prefetched into L2.
 // ============================================================================
-template <int N1, bool ROT>
+// AFF: the same structure for affine elements (no metric arrays; the
+// reference's constant sJ / J per band) — an alternative to the persistent
+// TMA kernels of kernels.cu (SDG_AFFINE_B=1).
+template <int N1, bool ROT, bool AFF = false>
 struct CB {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int MW = MWidth<ROT>::MW, FW = MWidth<ROT>::FW;
   static constexpr int EPB = N1 == 2 ? 16 : CDim<N1, ROT>::EPB;  // shared memory: <= 227 KB per CTA
   static constexpr int THREADS = EPB * N3;
   static constexpr int TAB = Dim<N1>::TAB;
-  static constexpr int EL = 5 * N3, ML = MW * N3, FM = 6 * FW * N2, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
+  static constexpr int EL = 5 * N3, ML = AFF ? 0 : MW * N3, FM = AFF ? 0 : 6 * FW * N2, TS = 5 * N2, FS = 4 * N2,
+                       NB = TS + FS;
+  static constexpr int GX = AFF ? 12 * N3 : 0;  // affine: separate gradient buffer (no metrics to alias)
   // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
   // (face flux and lift* are written over the element's own traces and Fv.n once phase 1 has read them)
   // (the staging buffer sF lives in the neighbour region, dead after phase 1)
@@ -614,7 +619,7 @@ struct CB {
   static_assert(5 * N3 <= 6 * NB, "staging buffer fits the neighbour region");
   // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
   // (the gradient is written over the state and metrics once every node's gradient is computed)
-  static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 24 * N2;
+  static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 24 * N2 + GX;
   static constexpr int KF = (6 * N2 + N3 - 1) / N3;  // face nodes per thread
 #ifndef SDG_CURVED_MINB
 #define SDG_CURVED_MINB 3
@@ -622,10 +627,13 @@ struct CB {
 #ifndef SDG_CURVED_MINB_U
 #define SDG_CURVED_MINB_U 3
 #endif
+#ifndef SDG_AFFINE_MINB_U
+#define SDG_AFFINE_MINB_U 3
+#endif
   // Resident CTAs per SM at N = 5: shared memory fits 3 (the annulus update kernel's 13 + 6-wide metrics: 2).
   static constexpr int MINB_G = N1 == 6 ? SDG_CURVED_MINB : 1;
-  static constexpr int MINB_U = N1 == 6 ? SDG_CURVED_MINB_U : 1;
-  static_assert(12 * N3 <= EL + ML, "gradient aliases state + metrics");
+  static constexpr int MINB_U = N1 == 6 ? (AFF ? SDG_AFFINE_MINB_U : SDG_CURVED_MINB_U) : 1;
+  static_assert(AFF || 12 * N3 <= EL + ML, "gradient aliases state + metrics");
   static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
   static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
   static_assert(N1 % 2 == 0, "bulk path needs even N+1");
@@ -634,10 +642,10 @@ struct CB {
 
 // Issue the bulk copies of one element tile (thread 0).  GRAD: neighbour
 // trace (conforming) or lift* (sliding) only; else trace + Fv.n or flux + lift*.
-template <int N1, bool ROT, bool GRAD, bool VISC>
+template <int N1, bool ROT, bool GRAD, bool VISC, bool AFF = false>
 __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, int n, double* base, int per,
                                                    uint64_t* bar) {
-  using D = CB<N1, ROT>;
+  using D = CB<N1, ROT, AFF>;
   uint32_t bytes = n * (D::EL + D::ML + D::FM + 6 * D::TS) * 8u;
   if (!GRAD && VISC) bytes += n * 6u * D::FS * 8u;
   for (int le = 0; le < n; ++le)
@@ -652,8 +660,10 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
     const int e = e0 + le;
     double* b = base + le * per;
     bulk_g2s(b, P.U + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
-    bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
-    bulk_g2s(b + D::EL + D::ML, P.fmet + static_cast<size_t>(e) * D::FM, D::FM * 8u, bar);
+    if (!AFF) {
+      bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
+      bulk_g2s(b + D::EL + D::ML, P.fmet + static_cast<size_t>(e) * D::FM, D::FM * 8u, bar);
+    }
     double* tr = b + D::EL + D::ML + D::FM;
     bulk_g2s(tr, P.trace + static_cast<size_t>(e) * 6 * D::TS, 6 * D::TS * 8u, bar);
     double* fv = tr + 6 * D::TS;
@@ -678,10 +688,10 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
   }
 }
 
-template <int N1, bool ROT>
-__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_gradient_curved_b(const __grid_constant__ ElemConsts C,
-                                                                            FieldPtrs P, StageArgs A) {
-  using D = CB<N1, ROT>;
+template <int N1, bool ROT, bool AFF = false>
+__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_G) k_gradient_curved_b(
+    const __grid_constant__ ElemConsts C, FieldPtrs P, StageArgs A) {
+  using D = CB<N1, ROT, AFF>;
   constexpr int MW = D::MW, FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::G_PER;
   extern __shared__ __align__(128) double smem[];
@@ -693,7 +703,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_g
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
-    curved_issue_loads<N1, ROT, true, true>(P, e0, n_el, base, PER, bar);
+    curved_issue_loads<N1, ROT, true, true, AFF>(P, e0, n_el, base, PER, bar);
   }
   load_tables<N1>(C, tab);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
@@ -705,7 +715,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_g
   double* sNb = sTr + 6 * D::TS;
   double* sq = sNb + 6 * D::TS;
   double* sLift = sq + 4 * N3;
-  double* sG = sU;  // after the gradient phase
+  double* sG = AFF ? sLift + 24 * N2 : sU;  // curved: over the dead state + metrics after the gradient phase
   const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
   const Rot rot = band_rotation(ROT, B, A.t_stage);
   __syncthreads();  // barrier init visible, tables loaded
@@ -744,7 +754,8 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_g
   double g[12];
   if (active) {
     const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-    node_gradient_curved<N1, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
+    if constexpr (AFF) node_gradient<N1>(tab, sq, sLift, B, i, j, k, g);
+    else node_gradient_curved<N1, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
     if (P.grad_out != nullptr) {
       double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
 #pragma unroll
@@ -771,9 +782,13 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_g
       const int typ = P.side_type[slot], idx = P.side_idx[slot];
       double fv[4] = {0.0, 0.0, 0.0, 0.0};
       if (typ == kConforming) {
-        double nrm[3], vgn;
-        face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
-        fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
+        if constexpr (AFF) {
+          fv_dir(sTr + s * D::TS + f * 5, gt, s >> 1, C.gas, fv);
+        } else {
+          double nrm[3], vgn;
+          face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
+          fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
+        }
       } else {
         double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
 #pragma unroll
@@ -792,10 +807,10 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_G) k_g
   }
 }
 
-template <int N1, bool VISC, bool ROT>
-__global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_update_curved_b(const __grid_constant__ ElemConsts C,
-                                                                          FieldPtrs P, StageArgs A) {
-  using D = CB<N1, ROT>;
+template <int N1, bool VISC, bool ROT, bool AFF = false>
+__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_U) k_update_curved_b(
+    const __grid_constant__ ElemConsts C, FieldPtrs P, StageArgs A) {
+  using D = CB<N1, ROT, AFF>;
   constexpr int MW = D::MW, FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::U_PER;
   extern __shared__ __align__(128) double smem[];
@@ -807,7 +822,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
-    curved_issue_loads<N1, ROT, false, VISC>(P, e0, n_el, base, PER, bar);
+    curved_issue_loads<N1, ROT, false, VISC, AFF>(P, e0, n_el, base, PER, bar);
     if (A.mode == 0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
   }
   load_tables<N1>(C, tab);
@@ -840,7 +855,12 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
       const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
       const double* own = sTr + s * D::TS + f * 5;
       double nrm[3], vgn;
-      face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
+      const int dir = s >> 1;
+      if constexpr (AFF) {
+        vgn = dir == 1 ? B.vg : 0.0;
+      } else {
+        face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
+      }
       const double* nb = sNb + s * D::NB;
       const int typ = P.side_type[e * 6 + s];
       double flux[5], lift[4];
@@ -849,7 +869,8 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
         const double* other = nb + f * 5;
         const double* um = (s & 1) ? own : other;
         const double* up = (s & 1) ? other : own;
-        ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
+        if constexpr (AFF) ok = roe_flux(um, up, dir, vgn, C.gas, flux);
+        else ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
         if (VISC) {
           double qa[4], qb[4];
           prim4(own, C.gas, qa);
@@ -876,7 +897,8 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
         eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
         const double* um = (s & 1) ? own : ext;
         const double* up = (s & 1) ? ext : own;
-        ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
+        if constexpr (AFF) ok = roe_flux(um, up, dir, vgn, C.gas, flux);
+        else ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
         if (VISC) {
           prim4(ext, C.gas, lift);
           const int idx = P.side_idx[e * 6 + s];
@@ -885,8 +907,13 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
 #pragma unroll
           for (int c = 0; c < 12; ++c) gg[c] = gd[c];
           double fm[4], fp[4];
-          fv_n(um, gg, nrm, C.gas, fm);
-          fv_n(up, gg, nrm, C.gas, fp);
+          if constexpr (AFF) {
+            fv_dir(um, gg, dir, C.gas, fm);
+            fv_dir(up, gg, dir, C.gas, fp);
+          } else {
+            fv_n(um, gg, nrm, C.gas, fm);
+            fv_n(up, gg, nrm, C.gas, fp);
+          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
         }
@@ -945,7 +972,8 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
     }
     if (VISC) {
       double g[12];
-      node_gradient_curved<N1, FW, ROT>(tab, sF, sM, sLift, sfm, i, j, k, rot, g);
+      if constexpr (AFF) node_gradient<N1>(tab, sF, sLift, B, i, j, k, g);
+      else node_gradient_curved<N1, FW, ROT>(tab, sF, sM, sLift, sfm, i, j, k, rot, g);
       const double div = g[0] + g[4] + g[8];
       const double mu = C.gas.mu, lam = C.gas.lam;
       const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
@@ -959,17 +987,25 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
         F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
       }
     }
-    const double* ja = sM + t;  // [c][node]
-    if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
+    if constexpr (AFF) {  // contravariant flux sJ_d F_d (volume_kernel, solver.cpp:357-370)
 #pragma unroll
-      for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
-    }
+      for (int d = 0; d < 3; ++d) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
-      const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
+        for (int v = 0; v < 5; ++v) Ft[d][v] = F[d][v] * B.sj[d];
+      }
+    } else {
+      const double* ja = sM + t;  // [c][node]
+      if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
 #pragma unroll
-      for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
+        for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
+      }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
+        const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
+      }
     }
   }
 
@@ -1000,7 +1036,7 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
   // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
   double du[5];
   if (active) {
-    const double ij = sM[9 * N3 + t];
+    const double ij = AFF ? B.inv_jac : sM[9 * N3 + t];
 #pragma unroll
     for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
     const double* lw = tab + N1 * N1 + 2 * N1;
@@ -1011,7 +1047,8 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
       const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
       const double l = lw[(s & 1) * N1 + ia];
       if (l != 0.0) {
-        const double c = ((s & 1) ? -1.0 : 1.0) * l * face_sj(sfm, s, f, N2, FW) * ij;
+        const double c = AFF ? ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * l
+                             : ((s & 1) ? -1.0 : 1.0) * l * face_sj(sfm, s, f, N2, FW) * ij;
 #pragma unroll
         for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
       }
@@ -1069,6 +1106,34 @@ __global__ void __launch_bounds__(CB<N1, ROT>::THREADS, CB<N1, ROT>::MINB_U) k_u
     bulk_s2g(P.trace_out + static_cast<size_t>(e) * 6 * D::TS, sOut, 6 * D::TS * 8u);
     bulk_commit();
     bulk_wait_read0();
+  }
+}
+
+template <int N1>
+bool gradient_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = CB<N1, false, true>;
+    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    cudaFuncSetAttribute(k_gradient_curved_b<N1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+    k_gradient_curved_b<N1, false, true><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+    check_launch("k_gradient_affine_b");
+    return true;
+  }
+}
+template <int N1>
+bool update_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if constexpr (N1 % 2 != 0) {
+    return false;
+  } else {
+    using D = CB<N1, false, true>;
+    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    auto kern = c.gas.viscous ? k_update_curved_b<N1, true, false, true> : k_update_curved_b<N1, false, false, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
+    kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
+    check_launch("k_update_affine_b");
+    return true;
   }
 }
 

@@ -3262,6 +3262,18 @@ void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const
   if (cv == 2) SDG_DISPATCH(n1, (done = update_curved_b_t<NN>(c, p, a, st)));
   if (!done) SDG_DISPATCH(n1, (update_curved_t<NN>(c, p, a, st)));
 }
+bool launch_gradient_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (p.E <= p.e_first) return true;
+  bool done = false;
+  SDG_DISPATCH(n1, (done = gradient_affine_b_t<NN>(c, p, a, st)));
+  return done;
+}
+bool launch_update_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+  if (p.E <= p.e_first) return true;
+  bool done = false;
+  SDG_DISPATCH(n1, (done = update_affine_b_t<NN>(c, p, a, st)));
+  return done;
+}
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
   k_pairing<<<2, kPairThreads, 0, st>>>(a, p);
   check_launch("k_pairing");

@@ -160,6 +160,10 @@ bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const St
 // Curved-element kernels (SDG_MAP_WARP; csrc/curved.cuh).
 void launch_gradient_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+// Affine elements through the bulk-loaded, non-persistent kernel structure of curved.cuh (even N+1;
+// false when not applicable).  Selected with SDG_AFFINE_B=1 instead of the persistent TMA kernels.
+bool launch_gradient_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+bool launch_update_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);

@@ -1018,9 +1018,15 @@ void GpuRankSolver::element_kernel(bool update, const FieldPtrs& fp0, const Stag
   fp.e_first = e_first;
   fp.E = e_end;
   mark(update ? KC_UPDATE : KC_GRADIENT, true);
+  static const bool affine_b = [] {
+    const char* v = std::getenv("SDG_AFFINE_B");
+    return v != nullptr && v[0] == '1';
+  }();
   if (curved_) {
     if (update) launch_update_curved(n_, consts_, fp, a, stream_);
     else launch_gradient_curved(n_, consts_, fp, a, stream_);
+  } else if (affine_b && (update ? launch_update_affine_b(n_, consts_, fp, a, stream_)
+                                 : launch_gradient_affine_b(n_, consts_, fp, a, stream_))) {
   } else if (update) {
     if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm, stream_))) launch_update(n_, consts_, fp, a, stream_);
   } else {
