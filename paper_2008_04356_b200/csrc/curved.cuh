@@ -628,7 +628,7 @@ struct CB {
 #define SDG_CURVED_MINB_U 3
 #endif
 #ifndef SDG_AFFINE_MINB_U
-#define SDG_AFFINE_MINB_U 3
+#define SDG_AFFINE_MINB_U 4  // affine update: 40 KB per CTA; 4 CTAs at <= 72 registers (128 B spills) beat 3 and 5
 #endif
   // Resident CTAs per SM at N = 5: shared memory fits 3 (the annulus update kernel's 13 + 6-wide metrics: 2).
   static constexpr int MINB_G = N1 == 6 ? SDG_CURVED_MINB : 1;

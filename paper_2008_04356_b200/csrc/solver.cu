@@ -1018,15 +1018,20 @@ void GpuRankSolver::element_kernel(bool update, const FieldPtrs& fp0, const Stag
   fp.e_first = e_first;
   fp.E = e_end;
   mark(update ? KC_UPDATE : KC_GRADIENT, true);
-  static const bool affine_b = [] {
+  // Affine elements: the update runs in the bulk-loaded, non-persistent structure
+  // of curved.cuh at 4 CTAs/SM (6.61 vs 6.88 ms for the persistent TMA kernel at
+  // N=5), the gradient in the warp-specialised persistent kernel (2.79 vs 4.22 ms).
+  // SDG_AFFINE_B: u (default) = update only, 1 = both, g = gradient only, 0 = neither.
+  static const int affine_b = [] {
     const char* v = std::getenv("SDG_AFFINE_B");
-    return v != nullptr && v[0] == '1';
+    if (v == nullptr) return 1;
+    return v[0] == '1' ? 3 : (v[0] == 'u' ? 1 : (v[0] == 'g' ? 2 : 0));
   }();
   if (curved_) {
     if (update) launch_update_curved(n_, consts_, fp, a, stream_);
     else launch_gradient_curved(n_, consts_, fp, a, stream_);
-  } else if (affine_b && (update ? launch_update_affine_b(n_, consts_, fp, a, stream_)
-                                 : launch_gradient_affine_b(n_, consts_, fp, a, stream_))) {
+  } else if ((affine_b & (update ? 1 : 2)) && (update ? launch_update_affine_b(n_, consts_, fp, a, stream_)
+                                                      : launch_gradient_affine_b(n_, consts_, fp, a, stream_))) {
   } else if (update) {
     if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm, stream_))) launch_update(n_, consts_, fp, a, stream_);
   } else {
