@@ -22,6 +22,16 @@ struct MWidth {
   static constexpr int MW = ROT ? 13 : 10, FW = ROT ? 6 : 4;
 };
 
+// Opt a kernel in to more than 48 KB of dynamic shared memory; a failure (more than the
+// 227 KB a CTA may use) is reported instead of surfacing as a failed launch.
+template <class K>
+void set_smem_checked(K kernel, cudaFuncAttribute attr, int bytes) {
+  const cudaError_t e = cudaFuncSetAttribute(kernel, attr, bytes);
+  if (e != cudaSuccess)
+    throw DeviceError(SDG_ERR_CUDA, std::string("cudaFuncSetAttribute(") + std::to_string(bytes) +
+                                        " B shared): " + cudaGetErrorString(e));
+}
+
 template <int N1, bool ROT>
 struct CDim {
   static constexpr int N2 = N1 * N1;
@@ -563,7 +573,7 @@ void gradient_curved_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs&
   using D = CDim<N1, ROT>;
   const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
   const int sm = (Dim<N1>::TAB + D::EPB * D::PER_GRAD) * 8;
-  cudaFuncSetAttribute(k_gradient_curved<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  set_smem_checked(k_gradient_curved<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   k_gradient_curved<N1, ROT><<<blocks, D::THREADS, sm, st>>>(c, p, a);
   check_launch("k_gradient_curved");
 }
@@ -578,7 +588,7 @@ void update_curved_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a
   const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
   const int sm = (Dim<N1>::TAB + D::EPB * D::PER_UPD) * 8;
   auto kern = c.gas.viscous ? k_update_curved<N1, true, ROT> : k_update_curved<N1, false, ROT>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  set_smem_checked(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   kern<<<blocks, D::THREADS, sm, st>>>(c, p, a);
   check_launch("k_update_curved");
 }
@@ -689,10 +699,10 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
 }
 
 template <int N1, bool ROT, bool AFF = false>
-__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_G) k_gradient_curved_b(
+__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_G) k_gradient_bulk(
     const __grid_constant__ ElemConsts C, FieldPtrs P, StageArgs A) {
   using D = CB<N1, ROT, AFF>;
-  constexpr int MW = D::MW, FW = D::FW;
+  constexpr int FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::G_PER;
   extern __shared__ __align__(128) double smem[];
   double* tab = smem;
@@ -808,10 +818,10 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
 }
 
 template <int N1, bool VISC, bool ROT, bool AFF = false>
-__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_U) k_update_curved_b(
+__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_U) k_update_bulk(
     const __grid_constant__ ElemConsts C, FieldPtrs P, StageArgs A) {
   using D = CB<N1, ROT, AFF>;
-  constexpr int MW = D::MW, FW = D::FW;
+  constexpr int FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::U_PER;
   extern __shared__ __align__(128) double smem[];
   double* tab = smem;
@@ -1116,9 +1126,9 @@ bool gradient_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArg
   } else {
     using D = CB<N1, false, true>;
     const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    cudaFuncSetAttribute(k_gradient_curved_b<N1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-    k_gradient_curved_b<N1, false, true><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
-    check_launch("k_gradient_affine_b");
+    set_smem_checked(k_gradient_bulk<N1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+    k_gradient_bulk<N1, false, true><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+    check_launch("k_gradient_bulk (affine)");
     return true;
   }
 }
@@ -1129,10 +1139,10 @@ bool update_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs&
   } else {
     using D = CB<N1, false, true>;
     const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    auto kern = c.gas.viscous ? k_update_curved_b<N1, true, false, true> : k_update_curved_b<N1, false, false, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
+    auto kern = c.gas.viscous ? k_update_bulk<N1, true, false, true> : k_update_bulk<N1, false, false, true>;
+    set_smem_checked(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
     kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
-    check_launch("k_update_affine_b");
+    check_launch("k_update_bulk (affine)");
     return true;
   }
 }
@@ -1141,9 +1151,9 @@ template <int N1, bool ROT>
 void gradient_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   using D = CB<N1, ROT>;
   const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-  cudaFuncSetAttribute(k_gradient_curved_b<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-  k_gradient_curved_b<N1, ROT><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
-  check_launch("k_gradient_curved_b");
+  set_smem_checked(k_gradient_bulk<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
+  k_gradient_bulk<N1, ROT><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
+  check_launch("k_gradient_bulk");
 }
 template <int N1>
 bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
@@ -1159,10 +1169,10 @@ template <int N1, bool ROT>
 void update_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   using D = CB<N1, ROT>;
   const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-  auto kern = c.gas.viscous ? k_update_curved_b<N1, true, ROT> : k_update_curved_b<N1, false, ROT>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
+  auto kern = c.gas.viscous ? k_update_bulk<N1, true, ROT> : k_update_bulk<N1, false, ROT>;
+  set_smem_checked(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
   kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
-  check_launch("k_update_curved_b");
+  check_launch("k_update_bulk");
 }
 template <int N1>
 bool update_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
