@@ -50,7 +50,8 @@ enum {
   SDG_CASE_FREESTREAM = 0,
   SDG_CASE_DENSITY_WAVE = 1,
   SDG_CASE_VORTEX = 2, /* isentropic vortex in the x-y plane, z-invariant */
-  SDG_CASE_TGV = 3     /* Taylor-Green vortex in BASELINE axes (see above) */
+  SDG_CASE_TGV = 3,    /* Taylor-Green vortex in BASELINE axes (see above) */
+  SDG_CASE_SWIRL = 4   /* axial density wave with rigid swirl about the x axis (annulus tests) */
 };
 
 /* One band (block) of structured, axis-aligned hexahedra. */
@@ -118,6 +119,9 @@ typedef struct {
   double vx_eps, vx_rc, vx_rho_inf, vx_v_inf, vx_theta, vx_ma_inf, vx_center[2];
   /* Taylor-Green vortex: reference density, velocity, Mach number */
   double tgv_rho0, tgv_v0, tgv_mach;
+  /* swirl: rho = 2 + dw_alpha sin(pi dw_k[0] (x - dw_a[0] t)), v = (dw_a[0], sw_omega Z, -sw_omega Y),
+   * p = dw_p0 + sw_omega^2 (Y^2 + Z^2): axisymmetric, so periodic under any rotation about x */
+  double sw_omega;
 } sdg_case;
 
 typedef struct {

@@ -674,6 +674,13 @@ static State eval_case(const sdg_case& cs, const double* x, double t, const Gas&
       const double p = p0 + r0 * V0 * V0 / 16.0 * (std::cos(2.0 * X) + std::cos(2.0 * Y)) * (std::cos(2.0 * Z) + 2.0);
       return from_primitive(r0, 0.0, uX, uY, p, g);
     }
+    case SDG_CASE_SWIRL: {
+      // Axial density wave with rigid swirl about x (include/sdg_types.h).
+      const double om = cs.sw_omega;
+      const double rho = 2.0 + cs.dw_alpha * std::sin(pi * cs.dw_k[0] * (x[0] - cs.dw_a[0] * t));
+      const double p = cs.dw_p0 + om * om * (x[1] * x[1] + x[2] * x[2]);
+      return from_primitive(rho, cs.dw_a[0], om * x[2], -om * x[1], p, g);
+    }
   }
   throw ConfigError("unknown case kind");
 }
@@ -698,6 +705,7 @@ struct Elem {
 };
 struct InteriorFace {
   int em, ep, dir;
+  int seam = 0;  // annulus sector: the face crosses the theta seam (minus at theta ~ alpha, plus at ~ 0)
 };
 struct BoundaryFace {
   int e, side;
@@ -721,6 +729,8 @@ struct Ctx {
   long last_n = -1;
   bool last_conf = true, topo_valid = false;
   long rebuilds = 0;
+  long wraps = 0;  // periods subtracted from delta_base so far (annulus sector windings)
+  long K = 0;      // windings of the moving band at the stage: displacement = d + K * period
   int half(int i_sub) const { return on_static ? i_sub : 1 - i_sub; }
 };
 
@@ -761,6 +771,9 @@ struct orc_solver {
   // SDG_MAP_ANNULUS adds per node the contravariant grid velocity per unit
   // angular speed V^d (3) and per face node vg.n per unit angular speed.
   bool curved = false, annulus = false;
+  // Periodic annulus sector of angle alpha (< 2 pi): vectors crossing the theta seam rotate by alpha.
+  bool sector = false;
+  double alpha = 0.0;
   int mw = 10, fw = 4;  // doubles per node / per face node
   std::vector<double> met, fmet;
   double t_cur = 0.0;   // stage time of the residual being evaluated (band rotation)
@@ -791,6 +804,71 @@ struct orc_solver {
     o[0] = v[0];
     o[1] = c * v[1] + s * v[2];
     o[2] = -s * v[1] + c * v[2];
+  }
+  // Rotation by k sector angles (periodic annulus sectors): state momentum,
+  // primitive velocity, velocity-gradient tensor R G R^T and temperature gradient.
+  void sector_rot(int k, double& c, double& s) const {
+    c = std::cos(k * alpha);
+    s = std::sin(k * alpha);
+  }
+  void rot_state(int k, const double* u, double* o) const {
+    double c, s;
+    sector_rot(k, c, s);
+    o[0] = u[0];
+    rot3(c, s, u + 1, o + 1);
+    o[4] = u[4];
+  }
+  void rot_prim(int k, const double* q, double* o) const {
+    double c, s;
+    sector_rot(k, c, s);
+    rot3(c, s, q, o);
+    o[3] = q[3];
+  }
+  void rot_grad(int k, const double* g, double* o) const {
+    // G_qd = g[3q + d] (q velocity component, d direction): G' = R G R^T; grad T' = R grad T.
+    double c, s;
+    sector_rot(k, c, s);
+    double t[9];
+    for (int d = 0; d < 3; ++d) {  // each column (over q)
+      const double col[3] = {g[d], g[3 + d], g[6 + d]};
+      double r[3];
+      rot3(c, s, col, r);
+      t[d] = r[0];
+      t[3 + d] = r[1];
+      t[6 + d] = r[2];
+    }
+    for (int q = 0; q < 3; ++q) rot3(c, s, t + 3 * q, o + 3 * q);  // each row (over d)
+    rot3(c, s, g + 9, o + 9);
+  }
+  // The moving role's mortar data (computed by the static side in its frame) moved to the
+  // moving elements' positions: each mortar block rotated by +k alpha.  comps: first
+  // rotated component (0: primitive velocity, 1: momentum); nc values per node.
+  std::vector<double> to_moving_frame(const Role& role, const std::vector<double>& data, int nc, int comps) const {
+    std::vector<double> out(data);
+    if (!sector) return out;
+    for (int m = 0; m < role.n_mortars; ++m) {
+      const int k = mortar_k(role.cols[m]);
+      double c, s;
+      sector_rot(k, c, s);
+      for (int q = 0; q < n2; ++q) {
+        double* v = out.data() + (static_cast<size_t>(m) * n2 + q) * nc + comps;
+        const double in[3] = {0.0, v[0], v[1]};
+        const double in2[3] = {v[0], v[1], v[2]};
+        (void)in;
+        double r[3];
+        rot3(c, s, in2, r);
+        v[0] = r[0];
+        v[1] = r[1];
+        v[2] = r[2];
+      }
+    }
+    return out;
+  }
+  // Windings k of a mortar column (its moving partner sits at the static location + k alpha).
+  int mortar_k(const Tuple& t) const {
+    const Ctx& c = ctxs[t.ctx];
+    const long raw = t.i_par - c.st.n_delta + t.i_sub - 1;
+    return static_cast<int>(c.K + (raw < 0 ? 1 : 0));
   }
   // Ja^d_c of node nd at t_cur (rotated with the band).
   void ja_at(int e, int nd, double* o9) const {
@@ -831,7 +909,7 @@ struct orc_solver {
     const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
     const double A = spec.warp;
     x[0] = (ox + 0.5 * (xi + 1.0) * b.hx) + A * b.hx * sp * sy * sz;
-    x[1] = (oy + 0.5 * (eta + 1.0) * b.hy) + A * b.hy * sp * sz + b.vg * t;
+    x[1] = (oy + 0.5 * (eta + 1.0) * b.hy) + (annulus ? 0.0 : A * b.hy * sp * sz) + b.vg * t;  // annulus: no theta warp
     x[2] = (oz + 0.5 * (zeta + 1.0) * b.hz) + A * b.hz * sp * sy;
     if (annulus) {
       // SDG_MAP_ANNULUS: (x, theta, r) -> (x, r sin theta, r cos theta); the band's
@@ -857,14 +935,22 @@ struct orc_solver {
     x[1] = r[1] * h[1] + A * h[1] * (sp * sz - cp * cz);
     x[2] = r[2] * h[2] + A * h[2] * (sp * sy - cp * cy);
     if (annulus) {
-      // Polar map about the x axis, minus the mapped centre (theta at t = 0).
-      const ld th = spec.y0 + h[1] * (el.iy + 0.5L * (eta + 1.0L)) + A * h[1] * sp * sz;
+      // Polar map about the x axis, minus the mapped centre.
+      const ld th = spec.y0 + h[1] * (el.iy + 0.5L * (eta + 1.0L));  // theta faces stay meridional planes
       const ld rr = spec.z0 + h[2] * (el.iz + 0.5L * (zeta + 1.0L)) + A * h[2] * sp * sy;
-      const ld thc = spec.y0 + h[1] * (el.iy + 0.5L) + A * h[1] * cp * cz;
+      const ld thc = center_angle(e);
       const ld rc = spec.z0 + h[2] * (el.iz + 0.5L) + A * h[2] * cp * cy;
       x[1] = rr * std::sin(th) - rc * std::sin(thc);
       x[2] = rr * std::cos(th) - rc * std::cos(thc);
     }
+  }
+  // Angle of an annulus element's centre at t = 0.
+  ld center_angle(int e) const {
+    const Elem& el = elems[e];
+    const Band& b = bands[el.band];
+    const ld tc[3] = {(el.ix + 0.5L) / b.nx, (el.iy + 0.5L) / spec.ny, (el.iz + 0.5L) / spec.nz};
+    (void)tc;
+    return spec.y0 + static_cast<ld>(b.hy) * (el.iy + 0.5L);
   }
   // Absolute radius of a reference point (annulus grid-velocity potential).
   ld radius(int e, double xi, double eta, double zeta) const {
@@ -994,7 +1080,8 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
     const Band& bd = bands[el.band];
     // y
     if (el.iy + 1 == s.ny && !s.periodic_y) dirichlet.push_back({e, YP});
-    else interior.push_back({e, static_cast<int>(gid(el.band, el.ix, (el.iy + 1) % s.ny, el.iz)), 1});
+    else interior.push_back({e, static_cast<int>(gid(el.band, el.ix, (el.iy + 1) % s.ny, el.iz)), 1,
+                             (el.iy + 1 == s.ny) ? 1 : 0});
     if (el.iy == 0 && !s.periodic_y) dirichlet.push_back({e, YM});
     // z
     if (el.iz + 1 == s.nz && !s.periodic_z) dirichlet.push_back({e, ZP});
@@ -1086,8 +1173,13 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
   if (annulus) {
     if (!(s.z0 > 0.0)) throw ConfigError("annulus needs a positive inner radius (z0 > 0)");
     if (s.periodic_z) throw ConfigError("annulus: the radial direction cannot be periodic");
-    if (s.periodic_y && std::abs(s.height - 2.0 * 3.14159265358979323846) > 1e-12)
-      throw ConfigError("annulus: a periodic angle must span the full circle (height = 2 pi)");
+    if (s.periodic_y && std::abs(s.height - 2.0 * 3.14159265358979323846) > 1e-12) {
+      const double m = 2.0 * 3.14159265358979323846 / s.height;
+      if (!(std::abs(m - std::round(m)) < 1e-9) || m < 1.5)
+        throw ConfigError("annulus: a periodic sector must divide the full circle (height = 2 pi / m)");
+      sector = true;
+      alpha = s.height;
+    }
     mw = 13;
     fw = 6;
   }
@@ -1174,8 +1266,12 @@ void orc_solver::build_metrics() {
       for (int c = 0; c < 3; ++c) deriv(X.data() + c * n3, d, dX.data() + (3 * d + c) * n3);
     for (int nn = 0; nn < 3; ++nn) {
       const int m = (nn + 1) % 3, l = (nn + 2) % 3;
+      // Invariant curl form (Kopriva 2006): V = (X_l grad X_m - X_m grad X_l) / 2 is an
+      // antisymmetric bilinear form, so the metrics are covariant under rotations
+      // (a periodic annulus sector reproduces its part of the full annulus).
       for (int d = 0; d < 3; ++d)
-        for (int g = 0; g < n3; ++g) V[d * n3 + g] = X[l * n3 + g] * dX[(3 * d + m) * n3 + g];
+        for (int g = 0; g < n3; ++g)
+          V[d * n3 + g] = 0.5L * (X[l * n3 + g] * dX[(3 * d + m) * n3 + g] - X[m * n3 + g] * dX[(3 * d + l) * n3 + g]);
       // Ja^i_nn = -(curl V)_i, (curl V)_i = d_{i+1} V_{i+2} - d_{i+2} V_{i+1}.
       for (int i = 0; i < 3; ++i) {
         const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
@@ -1256,6 +1352,7 @@ void orc_solver::build_metrics() {
   }
   if (first) std::rethrow_exception(first);
   for (const auto& f : interior) {
+    if (sector && f.seam) continue;  // the two slots differ by the sector rotation
     const double* src = fm(f.em, 2 * f.dir + 1);
     std::copy(src, src + n2 * fw, fmet.data() + (static_cast<size_t>(f.ep) * 6 + 2 * f.dir) * n2 * fw);
   }
@@ -1269,6 +1366,13 @@ void orc_solver::update_interfaces(double t_stage) {
     const double delta = c.delta_base + f.vg_rel * (t_stage - time);
     c.st = displacement(delta, f.l_par, f.n_faces);
     c.conforming = c.st.conforming();
+    {  // windings of the moving band: delta = d + K * period (displacement() wraps d to [0, period))
+      const double period = f.l_par * static_cast<double>(f.n_faces);
+      double dd = std::fmod(delta, period);
+      if (dd < 0.0) dd += period;
+      c.K = c.wraps + std::lround((delta - dd) / period);
+      if (dd / f.l_par >= static_cast<double>(f.n_faces)) c.K += 1;  // d rounded up to the period
+    }
     const double sigma = 2.0 * c.st.s_delta - 1.0;
     c.sigma_side = c.on_static ? sigma : -sigma;
     if (!c.conforming) mortar_ops(ns, c.sigma_side, c.fwd.data(), c.bwd.data());
@@ -1417,10 +1521,19 @@ void orc_solver::run_lifting(double t_stage, const double* u) {
     const double* up = tr(f.ep, sp);
     double* lm = lf(f.em, sm);
     double* lp = lf(f.ep, sp);
+    const bool seam = sector && f.seam;
     for (int k = 0; k < n2; ++k) {
       double a[4], b[4];
       prim4(um + k * NV, gas, a);
       prim4(up + k * NV, gas, b);
+      if (seam) {  // the plus element's values at theta ~ 0 seen from theta ~ alpha, and back
+        double br[4], lmv[4];
+        rot_prim(1, b, br);
+        for (int c = 0; c < 4; ++c) lmv[c] = 0.5 * (a[c] + br[c]);
+        rot_prim(-1, lmv, lp + k * 4);
+        for (int c = 0; c < 4; ++c) lm[k * 4 + c] = lmv[c];
+        continue;
+      }
       for (int c = 0; c < 4; ++c) lm[k * 4 + c] = lp[k * 4 + c] = 0.5 * (a[c] + b[c]);
     }
   }
@@ -1428,9 +1541,12 @@ void orc_solver::run_lifting(double t_stage, const double* u) {
   if (statics.n_mortars > 0) {
     const size_t nodes = static_cast<size_t>(statics.n_mortars) * n2;
     for (size_t q = 0; q < nodes; ++q) {
-      double a[4], b[4];
+      double a[4], b[4], th[NV];
       prim4(statics.u_mine.data() + q * NV, gas, a);
-      prim4(statics.u_theirs.data() + q * NV, gas, b);
+      // the moving partner's state at the static location (periodic sector: R(-k alpha))
+      if (sector) rot_state(-mortar_k(statics.cols[q / n2]), statics.u_theirs.data() + q * NV, th);
+      else std::copy_n(statics.u_theirs.data() + q * NV, NV, th);
+      prim4(th, gas, b);
       for (int c = 0; c < 4; ++c) statics.lift[q * 4 + c] = 0.5 * (a[c] + b[c]);
     }
     if (statics.self.count > 0)
@@ -1438,15 +1554,16 @@ void orc_solver::run_lifting(double t_stage, const double* u) {
                   static_cast<size_t>(statics.self.count) * n2 * 4,
                   movings.lift.begin() + static_cast<size_t>(movings.self.offset) * n2 * 4);
   }
+  const std::vector<double> mv_lift = to_moving_frame(movings, movings.lift, 4, 0);
   for (const auto& c : ctxs) {
-    const Role& role = c.on_static ? statics : movings;
+    const double* data = c.on_static ? statics.lift.data() : mv_lift.data();
     for (size_t f = 0; f < c.faces.size(); ++f) {
       double* lout = lf(c.faces[f].e, c.faces[f].side);
       if (c.conforming) {
-        std::copy_n(role.lift.data() + static_cast<size_t>(c.m[1][f]) * n2 * 4, n2 * 4, lout);
+        std::copy_n(data + static_cast<size_t>(c.m[1][f]) * n2 * 4, n2 * 4, lout);
         continue;
       }
-      mortar_to_face(c, n, role.lift.data(), f, 4, lout);
+      mortar_to_face(c, n, data, f, 4, lout);
     }
   }
   for (const auto& df : dirichlet) {
@@ -1639,6 +1756,17 @@ void orc_solver::interior_flux() {
     for (int k = 0; k < n2; ++k) {
       const double* gm = lifting ? gt(f.em, sm) + k * NG : nullptr;
       const double* gp = lifting ? gt(f.ep, sp) + k * NG : nullptr;
+      if (curved && sector && f.seam) {
+        // theta seam of a periodic sector: the plus element's trace and gradient rotated
+        // into the minus element's frame; the plus side gets the flux rotated back.
+        double nrm[3], vgn, upr[NV], gpr[NG];
+        normal_at(f.em, sm, k, nrm, vgn);
+        rot_state(1, up + k * NV, upr);
+        if (gp) rot_grad(1, gp, gpr);
+        face_flux_n(um + k * NV, upr, nrm, vgn, gm, gp ? gpr : nullptr, gas, om + k * NV);
+        rot_state(-1, om + k * NV, op + k * NV);
+        continue;
+      }
       if (curved) {
         // +xi normal of the face (identical in both slots); vg_n = vg . n.
         double nrm[3], vgn;
@@ -1730,6 +1858,16 @@ void orc_solver::mortar_flux() {
       const double* theirs = statics.u_theirs.data() + q * NV;
       const double* gm = lifting ? statics.g_mine.data() + q * NG : nullptr;
       const double* gt_ = lifting ? statics.g_theirs.data() + q * NG : nullptr;
+      double thr[NV], gtr[NG];
+      if (sector) {  // the moving partner's values at the static location: R(-k alpha)
+        const int kk = -mortar_k(statics.cols[c]);
+        rot_state(kk, theirs, thr);
+        theirs = thr;
+        if (gt_) {
+          rot_grad(kk, gt_, gtr);
+          gt_ = gtr;
+        }
+      }
       double* o = statics.flux.data() + q * NV;
       if (static_left) face_flux(mine, theirs, 0, 0.0, gm, gt_, gas, o);
       else face_flux(theirs, mine, 0, 0.0, gt_, gm, gas, o);
@@ -1743,15 +1881,16 @@ void orc_solver::mortar_flux() {
 
 // mortar_apply_phase (solver.cpp:495-526).
 void orc_solver::mortar_apply() {
+  const std::vector<double> mv_flux = to_moving_frame(movings, movings.flux, NV, 1);
   for (const auto& c : ctxs) {
-    const Role& role = c.on_static ? statics : movings;
+    const double* data = c.on_static ? statics.flux.data() : mv_flux.data();
     for (size_t f = 0; f < c.faces.size(); ++f) {
       double* o = ff(c.faces[f].e, c.faces[f].side);
       if (c.conforming) {
-        std::copy_n(role.flux.data() + static_cast<size_t>(c.m[1][f]) * n2 * NV, n2 * NV, o);
+        std::copy_n(data + static_cast<size_t>(c.m[1][f]) * n2 * NV, n2 * NV, o);
         continue;
       }
-      mortar_to_face(c, n, role.flux.data(), f, NV, o);
+      mortar_to_face(c, n, data, f, NV, o);
     }
   }
 }
@@ -1885,7 +2024,10 @@ void orc_solver::step(double dt) {
     const Iface& f = ifaces[c.iface];
     c.delta_base += f.vg_rel * dt;
     const double period = f.l_par * static_cast<double>(f.n_faces);
-    while (c.delta_base >= period) c.delta_base -= period;
+    while (c.delta_base >= period) {
+      c.delta_base -= period;
+      ++c.wraps;
+    }
   }
 }
 

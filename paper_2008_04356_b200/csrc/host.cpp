@@ -314,7 +314,7 @@ void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, doub
   const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
   const double A = m.spec.warp;
   x[0] = bx + A * B.hx * sp * sy * sz;
-  x[1] = by + A * B.hy * sp * sz + B.vg * t;
+  x[1] = by + (m.spec.mapping == SDG_MAP_ANNULUS ? 0.0 : A * B.hy * sp * sz) + B.vg * t;  // annulus: no theta warp
   x[2] = bz + A * B.hz * sp * sy;
   if (m.spec.mapping == SDG_MAP_ANNULUS) {  // (x, theta, r) -> (x, r sin theta, r cos theta)
     const double th = x[1], r = x[2];
@@ -325,6 +325,13 @@ void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, doub
 
 namespace {
 using ldm = long double;
+// Angle of an annulus element's centre at t = 0.
+ldm center_angle(const MeshGeom& m, int b, int ix, int iy, int iz) {
+  (void)ix;
+  (void)iz;
+  return m.spec.y0 + static_cast<ldm>(m.bands[b].hy) * (iy + 0.5L);
+}
+
 // Mapped position minus the mapped element centre, long double.  Two elements
 // sharing a face see its geometry up to an exact translation.
 void relative_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, double eta, double zeta, ldm* x) {
@@ -340,9 +347,9 @@ void relative_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi,
   x[1] = 0.5L * eta * h[1] + A * h[1] * (sp * sz - cp * cz);
   x[2] = 0.5L * zeta * h[2] + A * h[2] * (sp * sy - cp * cy);
   if (m.spec.mapping == SDG_MAP_ANNULUS) {
-    const ldm th = m.spec.y0 + h[1] * (iy + 0.5L * (eta + 1.0L)) + A * h[1] * sp * sz;
+    const ldm th = m.spec.y0 + h[1] * (iy + 0.5L * (eta + 1.0L));  // theta faces stay meridional planes
     const ldm rr = m.spec.z0 + h[2] * (iz + 0.5L * (zeta + 1.0L)) + A * h[2] * sp * sy;
-    const ldm thc = m.spec.y0 + h[1] * (iy + 0.5L) + A * h[1] * cp * cz;
+    const ldm thc = center_angle(m, b, ix, iy, iz);
     const ldm rc = m.spec.z0 + h[2] * (iz + 0.5L) + A * h[2] * cp * cy;
     x[1] = rr * std::sin(th) - rc * std::sin(thc);
     x[2] = rr * std::cos(th) - rc * std::cos(thc);
@@ -446,7 +453,8 @@ struct ElemMetricBuilder {
     for (int c = 0; c < 3; ++c) {
       const int mm = (c + 1) % 3, l = (c + 2) % 3;
       for (int d = 0; d < 3; ++d)
-        for (int g = 0; g < n3; ++g) V[d * n3 + g] = X[l * n3 + g] * dXL[(3 * d + mm) * n3 + g];
+        for (int g = 0; g < n3; ++g)  // invariant form: rotation covariant (periodic annulus sectors)
+          V[d * n3 + g] = 0.5L * (X[l * n3 + g] * dXL[(3 * d + mm) * n3 + g] - X[mm * n3 + g] * dXL[(3 * d + l) * n3 + g]);
       for (int i = 0; i < 3; ++i) {
         const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
         ldm* out = JaL.data() + (3 * i + c) * n3;
@@ -503,8 +511,8 @@ struct ElemMetricBuilder {
     for (int c = 0; c < 3; ++c) {
       const int mm = (c + 1) % 3, l = (c + 2) % 3;
       for (int g = 0; g < n2; ++g) {
-        V1[g] = X[l * n2 + g] * D1[mm * n2 + g];
-        V2[g] = X[l * n2 + g] * D2[mm * n2 + g];
+        V1[g] = 0.5L * (X[l * n2 + g] * D1[mm * n2 + g] - X[mm * n2 + g] * D1[l * n2 + g]);
+        V2[g] = 0.5L * (X[l * n2 + g] * D2[mm * n2 + g] - X[mm * n2 + g] * D2[l * n2 + g]);
       }
       du(V2.data(), a1.data());
       dv(V1.data(), a2.data());
@@ -880,6 +888,16 @@ void eval_case_host(const sdg_case& cs, const sdg_gas& g, const double* x, doubl
       v2 = -V0 * std::cos(X) * std::sin(Y) * std::cos(Z);
       const double p0 = r0 * V0 * V0 / (g.gamma * cs.tgv_mach * cs.tgv_mach);
       p = p0 + r0 * V0 * V0 / 16.0 * (std::cos(2.0 * X) + std::cos(2.0 * Y)) * (std::cos(2.0 * Z) + 2.0);
+      break;
+    }
+    case SDG_CASE_SWIRL: {
+      const double pi = 3.14159265358979323846;
+      const double om = cs.sw_omega;
+      rho = 2.0 + cs.dw_alpha * std::sin(pi * cs.dw_k[0] * (x[0] - cs.dw_a[0] * t));
+      v0 = cs.dw_a[0];
+      v1 = om * x[2];
+      v2 = -om * x[1];
+      p = cs.dw_p0 + om * om * (x[1] * x[1] + x[2] * x[2]);
       break;
     }
     case SDG_CASE_FREESTREAM:

@@ -233,6 +233,15 @@ __device__ void eval_case(const sdg_case& cs, const double* x, double t, const G
       p = p0 + r0 * V0 * V0 / 16.0 * (cos(2.0 * X) + cos(2.0 * Y)) * (cos(2.0 * Z) + 2.0);
       break;
     }
+    case SDG_CASE_SWIRL: {
+      const double om = cs.sw_omega;
+      rho = 2.0 + cs.dw_alpha * sin(pi * cs.dw_k[0] * (x[0] - cs.dw_a[0] * t));
+      v0 = cs.dw_a[0];
+      v1 = om * x[2];
+      v2 = -om * x[1];
+      p = cs.dw_p0 + om * om * (x[1] * x[1] + x[2] * x[2]);
+      break;
+    }
     default:
       rho = cs.fs_rho;
       v0 = cs.fs_v[0];
@@ -267,7 +276,7 @@ __device__ __forceinline__ void map_position(const ElemConsts& C, const int* crd
                  tz = (crd[3] + 0.5 * (zeta + 1.0)) / C.nz;
     const double sp = sinpi_exact(tx), sy = sinpi_exact(2.0 * ty), sz = sinpi_exact(2.0 * tz);
     x[0] += C.warp * B.hx * sp * sy * sz;
-    x[1] += C.warp * B.hy * sp * sz;
+    if (C.mapping != SDG_MAP_ANNULUS) x[1] += C.warp * B.hy * sp * sz;  // annulus: no theta warp
     x[2] += C.warp * B.hz * sp * sy;
   }
   x[1] += B.vg * t;

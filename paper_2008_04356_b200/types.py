@@ -16,7 +16,7 @@ TUPLE_INTS = 7
 
 OK, ERR_CONFIG, ERR_INVALID_STATE, ERR_PROTOCOL, ERR_CUDA, ERR_NCCL = range(6)
 NODES_LGL, NODES_GAUSS = 0, 1
-CASE_FREESTREAM, CASE_DENSITY_WAVE, CASE_VORTEX, CASE_TGV = range(4)
+CASE_FREESTREAM, CASE_DENSITY_WAVE, CASE_VORTEX, CASE_TGV, CASE_SWIRL = range(5)
 
 
 class BandSpec(C.Structure):
@@ -48,6 +48,7 @@ class Case(C.Structure):
         ("vx_eps", C.c_double), ("vx_rc", C.c_double), ("vx_rho_inf", C.c_double), ("vx_v_inf", C.c_double),
         ("vx_theta", C.c_double), ("vx_ma_inf", C.c_double), ("vx_center", C.c_double * 2),
         ("tgv_rho0", C.c_double), ("tgv_v0", C.c_double), ("tgv_mach", C.c_double),
+        ("sw_omega", C.c_double),
     ]
 
 
@@ -115,11 +116,15 @@ def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z
 
 
 def annulus_spec(bands, n_theta, n_r, r_in, r_out, length=2.0, warp=None, theta_span=2.0 * math.pi,
-                 partition=PARTITION_LEX) -> MeshSpec:
+                 partition=PARTITION_LEX, periodic_theta=None) -> MeshSpec:
     """Rotor/stator annulus (SDG_MAP_ANNULUS): bands (nx, width_frac, omega) stacked
     along the axis x over [0, length], n_theta elements around, n_r radially in
-    [r_in, r_out]; full circle -> periodic in theta, radial walls Dirichlet."""
-    periodic_theta = abs(theta_span - 2.0 * math.pi) < 1e-15
+    [r_in, r_out]; radial walls and axial ends Dirichlet.  theta is periodic by
+    default when the span divides the full circle (a sector 2 pi / m is
+    rotationally periodic: vectors rotate by the sector angle across its seam)."""
+    if periodic_theta is None:
+        m = 2.0 * math.pi / theta_span
+        periodic_theta = abs(m - round(m)) < 1e-9
     return mesh_spec(bands, ny=n_theta, nz=n_r, width=length, height=theta_span, depth=r_out - r_in,
                      z0=r_in, periodic=(False, periodic_theta, False), partition=partition, warp=warp,
                      mapping=MAP_ANNULUS)
@@ -155,6 +160,15 @@ def tgv(rho0=1.0, v0=1.0, mach=0.1) -> Case:
     c = Case()
     c.kind = CASE_TGV
     c.tgv_rho0, c.tgv_v0, c.tgv_mach = rho0, v0, mach
+    return c
+
+
+def swirl(alpha=0.1, a=1.0, k=1.0, p0=5.0, omega=0.5) -> Case:
+    """Axial density wave with rigid swirl about x (include/sdg_types.h SDG_CASE_SWIRL)."""
+    c = Case()
+    c.kind = CASE_SWIRL
+    c.dw_alpha, c.dw_p0, c.sw_omega = alpha, p0, omega
+    c.dw_a[0], c.dw_k[0] = a, k
     return c
 
 

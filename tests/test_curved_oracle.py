@@ -168,7 +168,7 @@ def test_rotating_annulus_metrics():
         lo = 32 * b
         assert np.abs(fmet[lo:lo + 16, 0, :, 4]).max() < 1e-14
         assert np.abs(fmet[lo + 16:lo + 32, 1, :, 4]).max() < 1e-14
-    assert np.abs(fmet[:, :, :, 4]).max() <= 1.0 + 1e-12
+    assert np.abs(fmet[:, :, :, 4]).max() <= 1.0 + 0.1 * 0.25 + 1e-12  # |vg| / omega <= r, warped r <= 1 + A hz
     x, w, D, fl, fr = _basis(degree, T.NODES_GAUSS)
     Dh = (w[None, :] * D.T) / w[:, None]
     E = met.shape[0]
@@ -200,8 +200,63 @@ def test_rotating_annulus_density_wave_converges():
 
 
 def test_annulus_config_errors():
-    with pytest.raises(T.ConfigError):  # periodic sector smaller than the full circle
+    with pytest.raises(T.ConfigError):  # periodic sector that does not divide the full circle
         P.Oracle3D(T.mesh_spec(ROTOR, ny=8, nz=2, height=1.0, depth=0.5, z0=0.5, periodic=(False, True, False),
                                mapping=T.MAP_ANNULUS), T.solver_config(2))
     with pytest.raises(T.ConfigError):  # inner radius 0
         P.Oracle3D(T.annulus_spec(ROTOR, 8, 2, 0.0, 1.0), T.solver_config(2))
+
+
+# ---------------------------------------------------------------- periodic annulus sectors
+def _sector_pair(nth=3, m=8, bands=ROTOR, n_r=2):
+    full = T.annulus_spec(bands, m * nth, n_r, 0.5, 1.0)
+    sec = T.annulus_spec(bands, nth, n_r, 0.5, 1.0, theta_span=2.0 * np.pi / m)
+    assert sec.periodic_y == 1
+    return full, sec
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+@pytest.mark.parametrize("mu", [0.0, 1e-3])
+def test_periodic_sector_reproduces_full_annulus(kind, mu):
+    """A pi/4 sector with rotational periodicity (momentum, gradients and fluxes
+    rotated across the theta seam and across wrapped rotor/stator mortars) equals
+    the first sector of the full annulus for an axisymmetric swirling state; the
+    invariant curl form makes the metrics rotation covariant, so the two
+    discretisations coincide up to rounding."""
+    m, nth = 8, 3
+    full, sec = _sector_pair(nth, m)
+    cfg = T.solver_config(3, kind, mu=mu, case=T.swirl(omega=0.7))
+    of, osr = P.Oracle3D(full, cfg), P.Oracle3D(sec, cfg)
+    of.set_initial_condition(0.0)
+    osr.set_initial_condition(0.0)
+    n3 = 4 ** 3
+
+    def first(u):
+        return u.reshape(2, 2, m * nth, 2, n3 * 5)[:, :, :nth].reshape(-1)
+
+    assert np.array_equal(first(of.field()), osr.field())
+    for t in (0.0, 0.05, 0.3, 1.7):
+        rf, rs = first(of.compute_residual(t)), osr.compute_residual(t)
+        assert np.abs(rf - rs).max() <= 1e-12 * np.abs(rf).max()
+    dt = of.suggest_dt(0.4)
+    of.step(dt, 5)
+    osr.step(dt, 5)
+    assert rel_linf(osr.field(), first(of.field())) <= 1e-12
+
+
+def test_periodic_sector_windings():
+    """The rotor passes the sector seam several times (windings of the sliding
+    displacement): the sector still follows the full annulus."""
+    m, nth = 4, 2
+    full, sec = _sector_pair(nth, m, bands=[(1, 1.0, 0.0), (1, 1.0, 3.0)], n_r=1)
+    cfg = T.solver_config(2, T.NODES_GAUSS, mu=1e-3, case=T.swirl(omega=0.4))
+    of, osr = P.Oracle3D(full, cfg), P.Oracle3D(sec, cfg)
+    of.set_initial_condition(0.0)
+    osr.set_initial_condition(0.0)
+    n3 = 3 ** 3
+    dt = 0.5 * of.suggest_dt(0.4)
+    steps = int(np.ceil(3.0 * (np.pi / 2) / 3.0 / dt))  # about three sector passes
+    of.step(dt, steps)
+    osr.step(dt, steps)
+    first = of.field().reshape(2, m * nth, n3 * 5)[:, :nth].reshape(-1)
+    assert rel_linf(osr.field(), first) <= 1e-11
