@@ -368,9 +368,11 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
       bool ok = true;
       if (typ == kConforming) {
         const double* nb = P.trace + static_cast<size_t>(idx) * N2 * 5 + f * 5;
-        double other[5];
+        double other[5], fvo[4];
 #pragma unroll
         for (int v = 0; v < 5; ++v) other[v] = nb[v];
+        const int kr = ROT ? P.side_rot[slot] : 0;  // periodic annulus sector seam
+        if (kr != 0) rot_yz(C.sec_c, kr * C.sec_s, other[2], other[3]);
         const double* um = (s & 1) ? own : other;
         const double* up = (s & 1) ? other : own;
         ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
@@ -381,7 +383,10 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
 #pragma unroll
           for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
           const double* pa = P.fvn + (static_cast<size_t>(slot) * N2 + f) * 4;
-          const double* pb = P.fvn + (static_cast<size_t>(idx) * N2 + f) * 4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) fvo[c] = P.fvn[(static_cast<size_t>(idx) * N2 + f) * 4 + c];
+          if (kr != 0) rot_yz(C.sec_c, kr * C.sec_s, fvo[1], fvo[2]);
+          const double* pb = fvo;
           const double* fm = (s & 1) ? pa : pb;
           const double* fp = (s & 1) ? pb : pa;
 #pragma unroll
@@ -744,6 +749,10 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
       if (typ == kConforming) {
         double qa[4], qb[4];
         prim4(own, C.gas, qa);
+        if constexpr (ROT) {  // periodic annulus sector seam: rotate the neighbour trace in place
+          if (C.sec_s != 0.0 && P.side_rot[e * 6 + s] != 0)
+            rot_yz(C.sec_c, P.side_rot[e * 6 + s] * C.sec_s, sNb[s * D::TS + f * 5 + 2], sNb[s * D::TS + f * 5 + 3]);
+        }
         prim4(sNb + s * D::TS + f * 5, C.gas, qb);
 #pragma unroll
         for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
@@ -876,6 +885,17 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
       double flux[5], lift[4];
       bool ok = true;
       if (typ == kConforming) {
+        if constexpr (ROT) {  // periodic annulus sector seam: rotate the neighbour slot in place
+          if (C.sec_s != 0.0 && P.side_rot[e * 6 + s] != 0) {  // (only this thread reads it)
+            const double sn = P.side_rot[e * 6 + s] * C.sec_s;
+            double* o = sNb + s * D::NB + f * 5;
+            rot_yz(C.sec_c, sn, o[2], o[3]);
+            if (VISC) {
+              double* fv = sNb + s * D::NB + D::TS + f * 4;
+              rot_yz(C.sec_c, sn, fv[1], fv[2]);
+            }
+          }
+        }
         const double* other = nb + f * 5;
         const double* um = (s & 1) ? own : other;
         const double* up = (s & 1) ? other : own;

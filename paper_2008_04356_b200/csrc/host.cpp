@@ -20,7 +20,11 @@ MeshGeom::MeshGeom(const sdg_mesh_spec& s) : spec(s) {
     if (!(s.z0 > 0.0)) throw ConfigError("annulus needs a positive inner radius (z0 > 0)");
     if (s.periodic_z) throw ConfigError("annulus: the radial direction cannot be periodic");
     if (s.periodic_y && std::abs(s.height - 2.0 * 3.14159265358979323846) > 1e-12)
-      throw ConfigError("annulus: a periodic angle must span the full circle (height = 2 pi)");
+    {
+      const double mm = 2.0 * 3.14159265358979323846 / s.height;
+      if (!(std::abs(mm - std::round(mm)) < 1e-9) || mm < 1.5)
+        throw ConfigError("annulus: a periodic sector must divide the full circle (height = 2 pi / m)");
+    }
   }
   if (s.ny < 1 || s.nz < 1) throw ConfigError("mesh needs ny >= 1 and nz >= 1");
   if (!(s.width > 0.0) || !(s.height > 0.0) || !(s.depth > 0.0))
@@ -214,6 +218,12 @@ Nbr neighbour(const MeshGeom& m, int b, int ix, int iy, int iz, int side) {
 }
 }  // namespace
 
+double sector_angle(const MeshGeom& mesh) {
+  const auto& s = mesh.spec;
+  if (s.mapping != SDG_MAP_ANNULUS || !s.periodic_y) return 0.0;
+  return std::abs(s.height - 2.0 * 3.14159265358979323846) > 1e-12 ? s.height : 0.0;
+}
+
 LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int rank) {
   LocalTopology t;
   t.rank = rank;
@@ -231,6 +241,8 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
   const int ne = static_cast<int>(t.gids.size());
   t.coords.resize(4 * ne);
   t.side_type.assign(6 * ne, kConforming);
+  t.side_rot.assign(6 * ne, 0);
+  const bool sector = sector_angle(mesh) != 0.0;
   t.side_idx.assign(6 * ne, -1);
   struct Remote {
     int partner;
@@ -260,6 +272,8 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
         const long ng = mesh.gid(n.band, n.ix, n.iy, n.iz);
         const int owner = part.owner(n.band, ng - mesh.bands[n.band].off);
         t.side_type[slot] = kConforming;
+        if (sector && s == 2 && iy == 0) t.side_rot[slot] = -1;
+        if (sector && s == 3 && iy + 1 == mesh.spec.ny) t.side_rot[slot] = 1;
         if (owner == rank) {
           t.side_idx[slot] = 6 * local_of.at(ng) + n.side;
         } else {
@@ -603,7 +617,8 @@ CurvedMetrics compute_metrics(const MeshGeom& m, const Basis& sol, const LocalTo
         for (int side = 0; side < 6; ++side) {
           double* o = out.fmet.data() + (static_cast<size_t>(e) * 6 + side) * n2 * fw;
           const Nbr nb = neighbour(m, c[0], c[1], c[2], c[3], side);
-          if ((side & 1) == 0 && nb.kind == 0) {
+          const bool seam = topo.side_rot[6 * e + side] != 0;  // the two slots differ by the sector rotation
+          if ((side & 1) == 0 && nb.kind == 0 && !seam) {
             // Minus side of a conforming face: the face's metrics are those of the
             // minus element (whose plus side it is), bit for bit, on every rank.
             mb.face(m, nb.band, nb.ix, nb.iy, nb.iz, nb.side, o, fw);

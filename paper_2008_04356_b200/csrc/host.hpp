@@ -97,6 +97,10 @@ struct LocalTopology {
   std::vector<long> gids;            // local element -> global id
   std::vector<int> coords;           // 4 per element: band, ix, iy, iz
   std::vector<int8_t> side_type;     // 6 per element
+  // Periodic annulus sector (SDG_MAP_ANNULUS, height 2 pi / m): per side, the neighbour's
+  // vectors reach this element's frame after a rotation by side_rot * sector angle
+  // (-1 on the theta-minus side of the first theta row, +1 on the theta-plus side of the last).
+  std::vector<int8_t> side_rot;
   std::vector<int> side_idx;         // conforming: neighbour trace slot; sliding: sliding index; dirichlet: index
   std::vector<std::array<int, 2>> dirichlet;  // (elem, side)
   std::vector<SlidingFaceRec> sliding;        // compact sliding index -> record
@@ -109,6 +113,8 @@ struct LocalTopology {
   std::vector<PeerFaces> peers;   // ascending partner
 };
 LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int rank);
+// Sector angle of a rotationally periodic annulus sector, 0 otherwise.
+double sector_angle(const MeshGeom& mesh);
 // Longest run [lo, hi) of local elements with no remote conforming and no sliding side: the
 // elements whose kernels can run while the halo exchange is in flight.
 std::array<int, 2> interior_run(const LocalTopology& topo);

@@ -35,6 +35,14 @@ struct Dim {
 
 __device__ __forceinline__ double sel3(int d, double a, double b, double c) { return d == 0 ? a : (d == 1 ? b : c); }
 
+// Rotation of a (y, z) pair about the x axis by the angle with cosine c and sine s
+// (theta -> theta + angle with Y = r sin theta, Z = r cos theta; annulus sectors).
+__device__ __forceinline__ void rot_yz(double c, double s, double& y, double& z) {
+  const double a = c * y + s * z, b = -s * y + c * z;
+  y = a;
+  z = b;
+}
+
 // ----------------------------------------------------------------------------
 // Canonical quantities that two kernels must reproduce bit-identically are
 // written with explicit rounding intrinsics (no contraction freedom).
@@ -390,6 +398,8 @@ __device__ __forceinline__ void face_lift_phase(const ElemConsts& C, const Field
       double other[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) other[v] = nb[v];
+      if (C.sec_s != 0.0 && P.side_rot[slot] != 0)  // periodic annulus sector seam
+        rot_yz(C.sec_c, P.side_rot[slot] * C.sec_s, other[2], other[3]);
       double qa[4], qb[4];
       prim4(own, C.gas, qa);
       prim4(other, C.gas, qb);
@@ -1026,6 +1036,14 @@ __device__ __forceinline__ void load_ops(const MortarOps& ops, int n_ctx, double
   }
 }
 
+// Windings k of a mortar column of a periodic annulus sector (its moving partner sits at
+// the static location + k * sector angle).
+__device__ __forceinline__ int mortar_wind(const MortarPtrs& P, const int* cols, int mc) {
+  const int ci = cols[7 * mc + 6];
+  const int raw = cols[7 * mc + 2] - P.ctx_state[2 * ci] + cols[7 * mc + 4] - 1;
+  return P.wind[ci] + (raw < 0 ? 1 : 0);
+}
+
 template <int N1, int NC>
 __global__ void k_mortar_fill(const __grid_constant__ MortarOps ops, int n_ctx, MortarPtrs P, const double* src,
                               double* dst0, double* dst1) {
@@ -1070,9 +1088,16 @@ __global__ void k_mortar_lift(GasD g, MortarPtrs P, int max_mortars) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= max_mortars * N2 || item / N2 >= P.n_mortars[0]) return;
   const size_t q = static_cast<size_t>(item);
-  double a[4], b[4];
+  double a[4], b[4], th[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) th[v] = P.u_theirs[q * 5 + v];
+  if (P.sector) {  // the moving partner's state at the static location: R(-k alpha)
+    double sn, cs;
+    sincos(-mortar_wind(P, P.cols_static, item / N2) * P.alpha, &sn, &cs);
+    rot_yz(cs, sn, th[2], th[3]);
+  }
   prim4(P.u_mine[0] + q * 5, g, a);
-  prim4(P.u_theirs + q * 5, g, b);
+  prim4(th, g, b);
 #pragma unroll
   for (int c = 0; c < 4; ++c) P.lift[0][q * 4 + c] = __dmul_rn(0.5, __dadd_rn(a[c], b[c]));
 }
@@ -1094,10 +1119,22 @@ __global__ void k_mortar_backproject(const __grid_constant__ MortarOps ops, int 
   const int* mrow = P.m + 2 * P.ctx_face_off[ci];
   const int nf = P.ctx_nf[ci];
   double* d = dst + (static_cast<size_t>(ks) * N2 + node) * NC;
+  // Periodic annulus sector, moving role: each mortar's values (computed by the static side at
+  // its location) rotate by R(+k alpha) to the moving element; (y, z) at OY, OY + 1.
+  constexpr int OY = NC == 4 ? 1 : 2;
+  const bool rot = P.sector && role == 1;
   if (conf) {
     const double* s = src + (static_cast<size_t>(mrow[nf + f]) * N2 + node) * NC;
+    double o[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) d[c] = s[c];
+    for (int c = 0; c < NC; ++c) o[c] = s[c];
+    if (rot) {
+      double sn, cs;
+      sincos(mortar_wind(P, P.cols_moving, mrow[nf + f]) * P.alpha, &sn, &cs);
+      rot_yz(cs, sn, o[OY], o[OY + 1]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] = o[c];
     return;
   }
   double out[NC];
@@ -1117,6 +1154,11 @@ __global__ void k_mortar_backproject(const __grid_constant__ MortarOps ops, int 
 #pragma unroll
       for (int c = 0; c < NC; ++c) acc[c] += w * s[(jm * N1 + kk) * NC + c];
     }
+    if (rot) {
+      double sn, cs;
+      sincos(mortar_wind(P, P.cols_moving, mrow[sub * nf + f]) * P.alpha, &sn, &cs);
+      rot_yz(cs, sn, acc[OY], acc[OY + 1]);
+    }
 #pragma unroll
     for (int c = 0; c < NC; ++c) out[c] += acc[c];
   }
@@ -1135,13 +1177,22 @@ __global__ void k_mortar_flux(GasD g, MortarPtrs P, int max_mortars, ErrRec* err
   const bool static_left = P.ctx_static_left[ci] != 0;
   const size_t q = static_cast<size_t>(item);
   const double* mine = P.u_mine[0] + q * 5;
-  const double* theirs = P.u_theirs + q * 5;
+  double th[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) th[v] = P.u_theirs[q * 5 + v];
+  double sn = 0.0, cs = 1.0;
+  if (P.sector) {  // the moving partner's values at the static location: R(-k alpha)
+    sincos(-mortar_wind(P, P.cols_static, mc) * P.alpha, &sn, &cs);
+    rot_yz(cs, sn, th[2], th[3]);
+  }
+  const double* theirs = th;
   double f[5];
   bool ok;
   if (VISC) {
     double fm[4], ft[4];
     fv_dir(mine, P.g_mine[0] + q * 12, 0, g, fm);
-    fv_dir(theirs, P.g_theirs + q * 12, 0, g, ft);
+    fv_dir(P.u_theirs + q * 5, P.g_theirs + q * 12, 0, g, ft);  // Fv . e_x in the partner's frame ...
+    if (P.sector) rot_yz(cs, sn, ft[1], ft[2]);                // ... rotated (e_x is the rotation axis)
     ok = static_left ? face_flux_fv(mine, theirs, 0, 0.0, fm, ft, g, f)
                      : face_flux_fv(theirs, mine, 0, 0.0, ft, fm, g, f);
   } else {

@@ -35,8 +35,9 @@ struct ElemConsts {
   GasD gas;
   double y0, z0;
   sdg_case flow_case;
-  int mapping, ny, nz, pad;  // SDG_MAP_BOX / SDG_MAP_WARP (include/sdg_types.h)
+  int mapping, ny, nz, pad;  // SDG_MAP_BOX / SDG_MAP_WARP / SDG_MAP_ANNULUS (include/sdg_types.h)
   double warp;
+  double sec_c, sec_s;       // cos / sin of the periodic annulus sector angle (side_rot)
 };
 
 // Deferred admissibility / protocol error record (written by the first failing thread).
@@ -66,6 +67,7 @@ struct FieldPtrs {
   double* grad_out;          // optional E x N3 x 12
   const double* met;         // curved: E x N3 x 10 (Ja^d_c at 3d + c, 1/J)
   const double* fmet;        // curved: 6E x N2 x 4 (unit +xi normal, sJ) per local side
+  const int8_t* side_rot;    // E x 6: neighbour vectors rotate by side_rot * sector angle (annulus sectors)
   ErrRec* err;
   int E;        // element kernels process local elements [e_first, E)
   int e_first;  // (interior / boundary split for exchange overlap; 0 = all)
@@ -144,8 +146,15 @@ struct MortarPtrs {
   const int* ctx_state;    // per ctx: n_delta, conforming
   const int* n_mortars;    // 2
   const int* cols_static;  // ctx of each static mortar: cols[7*c + 6]
+  const int* cols_moving;  // moving role's columns
   const int* ctx_static_left;
   int S;
+  // Periodic annulus sector: a mortar's moving partner sits at the static location + k alpha,
+  // k = wind[ctx] + (i_par - n_delta + i_sub - 1 < 0): static-role kernels rotate the partner's
+  // values by R(-k alpha), the moving role's back projection by R(+k alpha).
+  int sector;
+  double alpha;
+  int wind[kMaxCtx];
 };
 
 // ---- launch wrappers (kernels.cu) ----

@@ -261,6 +261,8 @@ struct SideCtx {
   std::vector<int> slides;  // compact sliding indices, sorted by (i_par, i_perp)
   std::vector<int> static_map, moving_map;  // rank maps (r, r~), n_perp x n_par
   double delta_base = 0.0;
+  long wraps = 0;  // periods subtracted from delta_base (annulus sector windings)
+  long wind = 0;   // windings at the stage: displacement = d + wind * period
   Displacement st;
   double sigma_side = -1.0;
   bool conforming = true;
@@ -378,7 +380,7 @@ class GpuRankSolver {
   // Curved elements (SDG_MAP_WARP): per-node metrics and per-side face metrics (host.cpp compute_metrics).
   bool curved_ = false;
   DevBuf<double> met_, fmet_;
-  DevBuf<int8_t> side_type_;
+  DevBuf<int8_t> side_type_, side_rot_;
   DevBuf<int> side_idx_, coords_, side_code_;
   int n_sm_ = 148;
   bool use_tma_ = true;
@@ -513,6 +515,8 @@ void GpuRankSolver::build_consts() {
   consts_.ny = mesh_.spec.ny;
   consts_.nz = mesh_.spec.nz;
   consts_.warp = mesh_.spec.mapping != SDG_MAP_BOX ? mesh_.spec.warp : 0.0;
+  consts_.sec_c = std::cos(sector_angle(mesh_));
+  consts_.sec_s = std::sin(sector_angle(mesh_));
   const auto& g = cfg_.gas;
   consts_.gas = {g.gamma, g.gamma - 1.0, g.R, 1.0 / g.R, g.mu, -2.0 / 3.0 * g.mu,
                  g.gamma * g.R * g.mu / ((g.gamma - 1.0) * g.Pr), g.mu > 0.0 ? 1 : 0};
@@ -539,6 +543,7 @@ void GpuRankSolver::upload_topology() {
   slide_g_.alloc(static_cast<size_t>(S_) * n2_ * 12);
   dir_g_.alloc(static_cast<size_t>(ND_) * n2_ * 12);
   side_type_.upload(topo_.side_type, stream_);
+  side_rot_.upload(topo_.side_rot, stream_);
   side_idx_.upload(topo_.side_idx, stream_);
   {
     std::vector<int> code(static_cast<size_t>(E_) * 8, 0);
@@ -766,6 +771,7 @@ void GpuRankSolver::set_initial_condition(double t0) {
   reg_.zero(stream_);
   for (auto& c : sides_) {
     c.delta_base = mesh_.ifaces[c.iface].vg_rel * t0;
+    c.wraps = 0;
     c.topo_valid = false;
   }
   traces_valid_ = false;
@@ -805,6 +811,7 @@ FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
   p.grad_out = nullptr;
   p.met = met_.p;
   p.fmet = fmet_.p;
+  p.side_rot = side_rot_.p;
   p.err = err_.p;
   p.E = E_;
   return p;
@@ -835,8 +842,12 @@ MortarPtrs GpuRankSolver::mortar_ptrs() {
   p.ctx_state = ctx_state_.p;
   p.n_mortars = n_mortars_.p;
   p.cols_static = cols_[0].p;
+  p.cols_moving = cols_[1].p;
   p.ctx_static_left = ctx_static_left_.p;
   p.S = S_;
+  p.alpha = sector_angle(mesh_);
+  p.sector = p.alpha != 0.0;
+  for (size_t c = 0; c < sides_.size(); ++c) p.wind[c] = static_cast<int>(sides_[c].wind);
   return p;
 }
 
@@ -886,6 +897,13 @@ void GpuRankSolver::update_interfaces_host(double t_stage) {
     const double delta = sc.delta_base + f.vg_rel * (t_stage - time_);
     sc.st = displacement(delta, f.l_par, f.n_faces);
     sc.conforming = sc.st.conforming();
+    {  // windings: delta = d + wind * period (displacement() wraps d into [0, period))
+      const double period = f.l_par * static_cast<double>(f.n_faces);
+      double dd = std::fmod(delta, period);
+      if (dd < 0.0) dd += period;
+      sc.wind = sc.wraps + std::lround((delta - dd) / period);
+      if (dd / f.l_par >= static_cast<double>(f.n_faces)) sc.wind += 1;
+    }
     const double sigma = 2.0 * sc.st.s_delta - 1.0;
     sc.sigma_side = sc.on_static ? sigma : -sigma;
     if (!sc.conforming && sc.sigma_side != sc.ops_sigma) {
@@ -1220,7 +1238,10 @@ void GpuRankSolver::steps(double dt, int n, bool sync) {
       const IfaceGeom& f = mesh_.ifaces[c.iface];
       c.delta_base += f.vg_rel * dt;
       const double period = f.l_par * static_cast<double>(f.n_faces);
-      while (c.delta_base >= period) c.delta_base -= period;
+      while (c.delta_base >= period) {
+        c.delta_base -= period;
+        ++c.wraps;
+      }
     }
   }
   if (sync) check_error();
