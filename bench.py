@@ -47,8 +47,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--mesh", default="tgv", choices=["tgv", "warped", "rotor"],
                    help="tgv: affine hexahedra (configs[4]); warped: the same case on curved hexahedra "
-                        "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3]); rotor: configs[3] "
-                        "stand-in, stator/rotor/stator annulus with a rotating middle block (SDG_MAP_ANNULUS)")
+                        "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3]); rotor: configs[3], "
+                        "1.1M-element stator/rotor/stator 20-degree annulus sector (SDG_MAP_ANNULUS), strong scaling")
     return p.parse_args()
 
 
@@ -64,37 +64,37 @@ def tgv_mesh(T, elems_x, elems_yz, warp=None):
 WARP = 0.05  # BASELINE configs[3]: "sinusoidal mesh warping of amplitude 5% of element size"
 
 
-def rotor_workload(args, world):
-    """BASELINE configs[3] stand-in (turbine-scale synthetic): three axial blocks
-    (stator, rotor, stator) of an annulus r in [0.8, 1] with two sliding
-    interfaces, 5% warping inside the blocks, tip Mach 0.4, axial inflow M = 0.3,
-    Re = 8e5 on the mean-radius arc of a 20-degree sector.  The full circle
-    replaces the 20-degree periodic sector (rotational periodicity of the
-    momentum across a sector seam is not implemented).  Per GPU:
-    (elems) axial x (4 elems) around x (elems / 4) radial elements."""
+def rotor_workload(args, world, elements=None):
+    """BASELINE configs[3] (turbine-scale synthetic): three axial blocks (stator,
+    rotor, stator) of a 20-degree periodic annulus sector r in [0.8, 1] with two
+    sliding interfaces, 5% warping inside the blocks (x and r), tip Mach 0.4,
+    axial inflow M = 0.3 (density-wave perturbation 1e-2), Re = 8e5 on the
+    mean-radius arc of the sector, N = 5.  About 1.1M curved hexahedra in total
+    (192 axial x 96 around x 60 radial), partitioned over the GPUs (strong
+    scaling).  `elements` = (nx, n_theta, n_r) overrides the mesh (CPU sample)."""
     from paper_2008_04356_b200 import types as T
     gamma, mach, rho0, u0 = 1.4, 0.3, 2.0, 1.0
     p0 = rho0 * u0 * u0 / (gamma * mach * mach)
     c0 = math.sqrt(gamma * p0 / rho0)
     r_in, r_out = 0.8, 1.0
     omega = 0.4 * c0 / r_out
-    chord = 0.5 * (r_in + r_out) * math.pi / 9.0
+    span = math.pi / 9.0
+    chord = 0.5 * (r_in + r_out) * span
     mu = rho0 * u0 * chord / 8e5
-    nx = args.elems * world
+    nx, n_theta, n_r = elements or (192, 96, 60)
     base, rem = divmod(nx, 3)
     n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
     bands = [(n[0], 1.0, 0.0), (n[1], 1.0, omega), (n[2], 1.0, 0.0)]
-    n_theta, n_r = 4 * args.elems, max(1, args.elems // 4)
-    mesh = T.annulus_spec(bands, n_theta, n_r, r_in, r_out, length=1.0, warp=WARP)
+    mesh = T.annulus_spec(bands, n_theta, n_r, r_in, r_out, length=1.0, warp=WARP, theta_span=span)
     cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=gamma, R=1.0, mu=mu, Pr=0.72,
                           case=T.density_wave(alpha=0.02, a=(u0, 0.0, 0.0), k=(2.0, 0.0, 0.0), p0=p0))
     n1 = args.degree + 1
     E = nx * n_theta * n_r
     conf = {
-        "workload": f"BASELINE configs[3] stand-in: stator/rotor/stator annulus r in [{r_in}, {r_out}] (full circle "
-                    f"for the 20-degree sector), 2 sliding interfaces, rotor omega {omega:.4f} (tip Mach 0.4), "
-                    f"warp {WARP}, axial M=0.3 density wave, Re=8e5, {nx // world}x{n_theta}x{n_r} elements/GPU, "
-                    f"N={args.degree} Gauss, viscous",
+        "workload": f"BASELINE configs[3]: stator/rotor/stator annulus sector r in [{r_in}, {r_out}], 20 degrees "
+                    f"(rotationally periodic), 2 sliding interfaces, rotor omega {omega:.4f} (tip Mach 0.4), "
+                    f"warp {WARP}, axial M=0.3 inflow with 1e-2 density perturbation, Re=8e5, "
+                    f"{nx}x{n_theta}x{n_r} = {E} curved hexahedra over {world} GPU(s), N={args.degree} Gauss, viscous",
         "geometry": "curved",
         "elements": E,
         "elements_per_gpu": E // world,
@@ -104,6 +104,7 @@ def rotor_workload(args, world):
         "bands_nx": n,
         "l2_policy": "inputs larger than L2 (state %.0f MB per GPU)" % (E // world * n1 ** 3 * 40 / 1e6),
         "parallelism": f"dp{world} (element partition, NCCL halo + mortar exchange)",
+        "scaling": "strong",
     }
     return mesh, cfg, conf, E * n1 ** 3
 
@@ -199,15 +200,14 @@ def cpu_baseline(args, conf, timeout_s=20.0):
     e = 6
     curved = conf.get("geometry") == "curved"
     if args.mesh == "rotor":
-        small = argparse.Namespace(**{**vars(args), "elems": 8})
-        mesh, cfg, _, _ = rotor_workload(small, 1)
-        e = "8x32x2"
+        mesh, cfg, _, _ = rotor_workload(args, 1, elements=(9, 12, 4))
+        e = "9x12x4"
     else:
         mesh, bands = tgv_mesh(T, e, e, warp=WARP if curved else None)
         cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
     o = P.Oracle3D(mesh, cfg)
     o.set_initial_condition(0.0)
-    dt = 1e-3
+    dt = o.suggest_dt(0.5)
     o.step(dt, 1)  # warm-up
     steps, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < timeout_s or steps == 0:
@@ -266,7 +266,7 @@ def reference_arm(args, world, rank):
     mesh, cfg, conf, dof = workload(args, 1)
     base = cpu_baseline(args, conf, timeout_s=max(2.0, 3.0 * args.steps / max(args.steps + args.warmup, 1)))
     line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": conf.get("scaling", "weak"),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (TGV initial field, analytic)",
             "config": conf, "impl": "reference", "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -425,8 +425,8 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (TGV initial field, analytic)", "config": conf,
+                "scaling": conf.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (analytic initial field)", "config": conf,
                 "value_per_gpu": value / world, "dt": dt, "gpu_launches": launches,
                 "clocks": clk.summary(), "roofline": roof, "kernels": extra, "e2e": e2e}
         if world == 1 and not args.no_cpu_baseline:
