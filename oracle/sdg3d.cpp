@@ -851,12 +851,10 @@ struct orc_solver {
       double c, s;
       sector_rot(k, c, s);
       for (int q = 0; q < n2; ++q) {
-        double* v = out.data() + (static_cast<size_t>(m) * n2 + q) * nc + comps;
-        const double in[3] = {0.0, v[0], v[1]};
-        const double in2[3] = {v[0], v[1], v[2]};
-        (void)in;
+        double* v = out.data() + (static_cast<size_t>(m) * n2 + q) * nc + comps;  // (x, y, z) components
+        const double in[3] = {v[0], v[1], v[2]};
         double r[3];
-        rot3(c, s, in2, r);
+        rot3(c, s, in, r);
         v[0] = r[0];
         v[1] = r[1];
         v[2] = r[2];
