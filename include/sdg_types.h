@@ -70,7 +70,10 @@ typedef struct {
   int periodic_x, periodic_y, periodic_z;
   /* Element order inside a band for the rank split: 0 = contiguous (ix, iy, iz)
    * lexicographic blocks (proj/src/partition.cpp:48-81), 1 = Morton
-   * space-filling curve. */
+   * space-filling curve, 2 = slabs along y through all bands (every rank owns
+   * an equal share of every band and both sides of the sliding interfaces;
+   * the reference's rule of one side per rank is lifted, which the per-kind
+   * exchange rounds allow). */
   int partition;
   /* Geometry of the elements: SDG_MAP_BOX (affine hexahedra, the reference's
    * ElementMetrics, proj/src/mesh.cpp:102-111) or SDG_MAP_WARP (curved

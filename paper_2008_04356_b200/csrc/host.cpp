@@ -133,8 +133,37 @@ Partition assign_ranks(const MeshGeom& mesh, int n_ranks) {
   p.order_of.resize(nb);
   if (mesh.spec.partition == 1 && n_ranks > 1)
     for (int b = 0; b < nb; ++b) sfc_order(mesh, b, p.lex_of[b], p.order_of[b]);
-  else if (mesh.spec.partition != 0 && mesh.spec.partition != 1)
-    throw ConfigError("partition must be 0 (lexicographic blocks) or 1 (space-filling curve)");
+  else if (mesh.spec.partition < 0 || mesh.spec.partition > 2)
+    throw ConfigError("partition must be 0 (lexicographic blocks), 1 (space-filling curve) or 2 (y slabs)");
+  if (mesh.spec.partition == 2 && n_ranks > 1) {
+    // Slabs along the sliding direction through all bands: every rank owns the same share of
+    // every band, so any rank count balances exactly when it divides ny.  A rank then owns
+    // both sides of the sliding interfaces (rank-local mortars, the self block); mortars cross
+    // ranks only where a slab edge meets the sliding displacement.  Element order inside a
+    // band: iy major.
+    const int ny = mesh.spec.ny, nz = mesh.spec.nz;
+    if (n_ranks > ny) throw ConfigError("y-slab partition needs n_ranks <= ny");
+    for (int b = 0; b < nb; ++b) {
+      const int nx = mesh.bands[b].nx;
+      auto& lo = p.lex_of[b];
+      auto& ord = p.order_of[b];
+      lo.resize(static_cast<size_t>(nx) * ny * nz);
+      ord.resize(lo.size());
+      long o = 0;
+      for (int iy = 0; iy < ny; ++iy)
+        for (int ix = 0; ix < nx; ++ix)
+          for (int iz = 0; iz < nz; ++iz, ++o) {
+            const long lex = (static_cast<long>(ix) * ny + iy) * nz + iz;
+            lo[o] = lex;
+            ord[lex] = o;
+          }
+      for (int r = 0; r < n_ranks; ++r) {
+        const long y0 = static_cast<long>(ny) * r / n_ranks, y1 = static_cast<long>(ny) * (r + 1) / n_ranks;
+        p.band_blocks[b].push_back({r, y0 * nx * nz, (y1 - y0) * nx * nz});
+      }
+    }
+    return p;
+  }
   if (n_ranks == 1) {
     for (int b = 0; b < nb; ++b) p.band_blocks[b].push_back({0, 0, mesh.bands[b].n_elements});
     return p;

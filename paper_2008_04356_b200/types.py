@@ -88,7 +88,7 @@ def raise_for(code: int, msg: str) -> None:
         raise ERRORS.get(code, SdgError)(msg)
 
 
-PARTITION_LEX, PARTITION_SFC = 0, 1
+PARTITION_LEX, PARTITION_SFC, PARTITION_YSLAB = 0, 1, 2
 MAP_BOX, MAP_WARP, MAP_ANNULUS = 0, 1, 2
 
 

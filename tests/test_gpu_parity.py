@@ -272,7 +272,7 @@ def test_gpu_embeds_reference_fixture(name):
 
 
 # ---------------------------------------------------------------- multi-rank data path on one GPU
-@pytest.mark.parametrize("partition", [T.PARTITION_LEX, T.PARTITION_SFC])
+@pytest.mark.parametrize("partition", [T.PARTITION_LEX, T.PARTITION_SFC, T.PARTITION_YSLAB])
 @pytest.mark.parametrize("ranks", [2, 3, 6])
 def test_rank_counts_do_not_change_the_bits(ranks, partition):
     """proj/tests/test_runner.cpp:32-50 on the B200 path: 1 rank vs 2/3/6 ranks

@@ -27,6 +27,8 @@ def meshes():
                                 partition=T.PARTITION_SFC),
         "box0_sfc": T.mesh_spec([(4, 1.0, 0.0), (4, 1.0, 0.5)], ny=4, nz=4, periodic=(False, True, True),
                                 partition=T.PARTITION_SFC),
+        "tgv3_yslab": T.mesh_spec([(3, 1.0, 0.0), (4, 1.0, 0.2), (3, 1.0, 0.0)], ny=8, nz=3, width=L, height=L,
+                                  depth=L, partition=T.PARTITION_YSLAB),
     }
 
 
@@ -48,7 +50,7 @@ def check_plans(plans, n_ranks, mesh):
             if a == b:
                 back = [x for x in by_rank[a]["mortars"] if x["partner"] == a and x["role"] == 1 - m["role"]]
             assert len(back) == 1 and back[0]["keys"] == m["keys"], (a, b, m["role"])
-    if n_ranks > 1:
+    if n_ranks > 1 and mesh.partition != T.PARTITION_YSLAB:
         for p in plans:
             roles = {m["role"] for m in p["mortars"]}
             selfs = [m for m in p["mortars"] if m["partner"] == p["rank"]]
@@ -181,3 +183,19 @@ def test_interior_run_has_only_local_conforming_neighbours(bands, ranks, partiti
         assert hi - lo == best
     if bands == [(8, 1.0, 0.0)] and partition == T.PARTITION_LEX:
         assert [p["interior_run"] for p in plans] == [[8, 24], [8, 24]]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_yslab_partition_balances_every_band(world):
+    """Slabs along the sliding direction: every rank owns ny / world rows of every band (equal work for
+    any band layout), both sides of the sliding interfaces, and mortars still pair up across ranks."""
+    L = 2 * math.pi
+    mesh = T.mesh_spec([(3, 1.0, 0.0), (4, 1.0, 0.2), (3, 1.0, 0.0)], ny=8, nz=3, width=L, height=L, depth=L,
+                       partition=T.PARTITION_YSLAB)
+    plans = [capi.plan(mesh, world, r, 0.37) for r in range(world)]
+    check_plans(plans, world, mesh)
+    sizes = [len(p["elements"]) for p in plans]
+    assert max(sizes) - min(sizes) <= 10 * 3  # one y row of all bands
+    if 8 % world == 0:
+        assert len(set(sizes)) == 1
+    assert any(m["partner"] == p["rank"] for p in plans for m in p["mortars"])  # rank-local mortars
