@@ -52,13 +52,17 @@ def parse():
     return p.parse_args()
 
 
-def tgv_mesh(T, elems_x, elems_yz, warp=None):
-    """Three blocks along x (= BASELINE z); interfaces at 2pi/3, 4pi/3."""
+def tgv_mesh(T, elems_x, elems_yz, warp=None, copies=1):
+    """Three blocks along x (= BASELINE z); interfaces at 2pi/3, 4pi/3.  Weak scaling over
+    `copies` GPUs stacks that many periods of the (2 pi periodic) TGV along the sliding
+    direction y and splits it in y slabs through all three blocks (partition 2): every GPU
+    holds one identical 64^3 TGV box, both sliding interfaces included."""
     L = 2.0 * math.pi
     base, rem = divmod(elems_x, 3)
     n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
     bands = [(n[0], 1.0, 0.0), (n[1], 1.0, 0.2), (n[2], 1.0, 0.0)]
-    return T.mesh_spec(bands, ny=elems_yz, nz=elems_yz, width=L, height=L, depth=L, warp=warp), bands
+    return T.mesh_spec(bands, ny=elems_yz * copies, nz=elems_yz, width=L, height=L * copies, depth=L, warp=warp,
+                       partition=T.PARTITION_YSLAB if copies > 1 else T.PARTITION_LEX), bands
 
 
 WARP = 0.05  # BASELINE configs[3]: "sinusoidal mesh warping of amplitude 5% of element size"
@@ -114,10 +118,10 @@ def workload(args, world):
     if args.mesh == "rotor":
         return rotor_workload(args, world)
     curved = args.mesh == "warped"
-    mesh, bands = tgv_mesh(T, args.elems * world, args.elems, warp=WARP if curved else None)
+    mesh, bands = tgv_mesh(T, args.elems, args.elems, warp=WARP if curved else None, copies=world)
     cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
     n1 = args.degree + 1
-    E = sum(b[0] for b in bands) * args.elems * args.elems
+    E = sum(b[0] for b in bands) * args.elems * args.elems * world
     geom = (f"curved hexahedra (SDG_MAP_WARP, warp {WARP} of the element size, as BASELINE configs[3]; "
             f"per-node metrics)" if curved else "affine hexahedra")
     conf = {
@@ -132,7 +136,7 @@ def workload(args, world):
         "bands_nx": [b[0] for b in bands],
         "l2_policy": "inputs larger than L2 (state %.0f MB, face traces %.0f MB per GPU)" % (
             E // world * n1 ** 3 * 40 / 1e6, E // world * 6 * n1 ** 2 * 72 / 1e6),
-        "parallelism": f"dp{world} (element partition, NCCL halo + mortar exchange)",
+        "parallelism": (f"dp{world} (y slabs through all three blocks, NCCL halo + mortar exchange)" if world > 1 else "dp1"),
     }
     return mesh, cfg, conf, E * n1 ** 3
 
