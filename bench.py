@@ -211,11 +211,19 @@ def cpu_baseline(args, conf, timeout_s=20.0):
         cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
     o = P.Oracle3D(mesh, cfg)
     o.set_initial_condition(0.0)
-    dt = o.suggest_dt(0.5)
+    # A timing sample, not a simulation: a small fixed step (well inside the CFL limit) keeps
+    # the coarse sample admissible for the whole window (an under-resolved TGV at CFL 0.5
+    # leaves the admissible set after ~1000 steps).
+    dt = min(1e-3, 0.25 * o.suggest_dt(1.0))
     o.step(dt, 1)  # warm-up
     steps, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < timeout_s or steps == 0:
-        o.step(dt, 1)
+        try:
+            o.step(dt, 1)
+        except P.T.InvalidStateError if hasattr(P, "T") else Exception:
+            if steps == 0:
+                raise
+            break
         steps += 1
     el = time.perf_counter() - t0
     dof = o.n_elements * (args.degree + 1) ** 3
