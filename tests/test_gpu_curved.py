@@ -317,3 +317,23 @@ def test_baseline_config2_free_stream_and_parity():
     g2.step(dt)
     o.step(dt)
     assert rel_linf(g2.field(), o.field()) <= 1e-12
+
+
+@pytest.mark.parametrize("ranks", [3, 6])
+def test_periodic_sector_yslab_ranks_keep_the_bits(ranks):
+    """y slabs through a rotating annulus sector: every rank owns stator and rotor rows (rank-local
+    mortars), slab edges carry cross-rank mortars and seam faces; bitwise equal to one rank."""
+    from paper_2008_04356_b200 import capi
+    mesh = T.annulus_spec([(2, 1.0, 0.0), (2, 1.0, 0.8)], 6, 2, 0.5, 1.0, warp=0.05, theta_span=np.pi / 4,
+                          partition=T.PARTITION_YSLAB)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.swirl(omega=0.7))
+    n_el = 4 * 6 * 2
+
+    def body(s):
+        s.set_initial_condition(0.0)
+        s.step(0.01, 5)
+        return s.local_element_ids(), s.field()
+
+    ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub=f"ys1_{ranks}"), n_el, 4)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"ys{ranks}"), n_el, 4)
+    assert np.array_equal(got, ref)
