@@ -268,9 +268,13 @@ def test_periodic_sector_rank_split_keeps_the_bits():
     cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.swirl(omega=0.7))
     n_el = 2 * 2 * 3 * 2
 
+    dt = P.Oracle3D(mesh, cfg)
+    dt.set_initial_condition(0.0)
+    dt = dt.suggest_dt(0.4)
+
     def body(s):
         s.set_initial_condition(0.0)
-        s.step(0.01, 5)
+        s.step(dt, 5)
         return s.local_element_ids(), s.field()
 
     ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub="sec1"), n_el, 4)
@@ -329,9 +333,13 @@ def test_periodic_sector_yslab_ranks_keep_the_bits(ranks):
     cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.swirl(omega=0.7))
     n_el = 4 * 6 * 2
 
+    dt = P.Oracle3D(mesh, cfg)
+    dt.set_initial_condition(0.0)
+    dt = dt.suggest_dt(0.4)
+
     def body(s):
         s.set_initial_condition(0.0)
-        s.step(0.01, 5)
+        s.step(dt, 5)
         return s.local_element_ids(), s.field()
 
     ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub=f"ys1_{ranks}"), n_el, 4)
