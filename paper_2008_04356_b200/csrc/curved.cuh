@@ -630,7 +630,9 @@ struct CB {
   // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
   // (face flux and lift* are written over the element's own traces and Fv.n once phase 1 has read them)
   // (the staging buffer sF lives in the neighbour region, dead after phase 1)
-  static constexpr int U_PER = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB;
+  // affine: + the RK register, bulk-loaded with the tile (its L2-prefetched global read stalled 7 %)
+  static constexpr int RG = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB;
+  static constexpr int U_PER = RG + (AFF ? EL : 0);
   static_assert(5 * N3 <= 6 * NB, "staging buffer fits the neighbour region");
   // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
   // (the gradient is written over the state and metrics once every node's gradient is computed)
@@ -659,9 +661,10 @@ struct CB {
 // trace (conforming) or lift* (sliding) only; else trace + Fv.n or flux + lift*.
 template <int N1, bool ROT, bool GRAD, bool VISC, bool AFF = false>
 __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, int n, double* base, int per,
-                                                   uint64_t* bar) {
+                                                   uint64_t* bar, bool load_reg = false) {
   using D = CB<N1, ROT, AFF>;
   uint32_t bytes = n * (D::EL + D::ML + D::FM + 6 * D::TS) * 8u;
+  if (load_reg) bytes += n * D::EL * 8u;
   if (!GRAD && VISC) bytes += n * 6u * D::FS * 8u;
   for (int le = 0; le < n; ++le)
     for (int s = 0; s < 6; ++s) {
@@ -681,6 +684,7 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
     }
     double* tr = b + D::EL + D::ML + D::FM;
     bulk_g2s(tr, P.trace + static_cast<size_t>(e) * 6 * D::TS, 6 * D::TS * 8u, bar);
+    if (load_reg) bulk_g2s(b + D::RG, P.reg + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
     double* fv = tr + 6 * D::TS;
     double* nb = GRAD ? fv : fv + 6 * D::FS;
     if (!GRAD && VISC) bulk_g2s(fv, P.fvn + static_cast<size_t>(e) * 6 * D::FS, 6 * D::FS * 8u, bar);
@@ -841,8 +845,9 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
-    curved_issue_loads<N1, ROT, false, VISC, AFF>(P, e0, n_el, base, PER, bar);
-    if (A.mode == 0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
+    const bool load_reg = AFF && A.mode == 0 && A.rk_a != 0.0;
+    curved_issue_loads<N1, ROT, false, VISC, AFF>(P, e0, n_el, base, PER, bar, load_reg);
+    if (!AFF && A.mode == 0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
   }
   load_tables<N1>(C, tab);
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
@@ -1104,7 +1109,10 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
     double* us = base + l * PER + r;
     const double dd = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + r];
     const size_t g = static_cast<size_t>(e0) * 5 * N3 + fI;
-    const double rg = A.rk_a * P.reg[g] + A.dt * dd;
+    double rv;
+    if constexpr (AFF) rv = A.rk_a != 0.0 ? base[l * PER + D::RG + r] : 0.0;
+    else rv = P.reg[g];
+    const double rg = A.rk_a * rv + A.dt * dd;
     const double un = *us + A.rk_b * rg;
     P.reg[g] = rg;
     P.U[g] = un;
