@@ -1490,283 +1490,6 @@ __device__ __forceinline__ void gradient_lines(const ElemConsts& C, const BandD&
   }
 }
 
-template <int N1, bool VISC, bool LINES>
-__global__ void __launch_bounds__(Tma<N1>::THREADS, Tma<N1>::MINB_U) k_update_tma(const __grid_constant__ ElemConsts C,
-                                                                                  FieldPtrs P, StageArgs A) {
-  using D = Tma<N1>;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* stage0 = smem + D::TAB;
-  double* regb = stage0 + 2 * D::U_STAGE;
-  double* wF = regb + D::U_REG;
-  double* wLift = wF + D::U_WF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wLift + EPB * 24 * N2);
-  __shared__ __align__(16) int codes[2][8 * EPB];
-  load_tables<N1>(C, tab);
-  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < tiles) {
-    prefetch_codes<N1>(P, tile, codes[0]);
-    cp_async_wait_all();
-    issue_update_loads<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
-    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
-  }
-  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-    const int sidx = it & 1;
-    double* st = stage0 + sidx * D::U_STAGE;
-    const int next = tile + gridDim.x;
-    const int e0 = P.e_first + tile * EPB;
-    const int n_el = min(EPB, P.E - e0);
-    if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous tile's stores no longer read regb / wF / stage sidx^1
-      fence_proxy_async();
-      if (A.mode == 0) {
-        mbar_arrive_expect_tx(&bars[2], n_el * D::EL * 8u);
-        bulk_g2s(regb, P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u, &bars[2]);
-      }
-      if (next < tiles) {
-        cp_async_wait_all();  // codes of `next`
-        issue_update_loads<N1, VISC>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::U_STAGE,
-                                     &bars[sidx ^ 1]);
-        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
-      }
-    }
-    __syncthreads();
-    const int e = e0 + le;
-    const bool active = e < P.E;
-    double* sU = st + le * D::EL;
-    double* sFv = st + EPB * D::EL + le * 6 * D::FS;
-    double* sNb = st + EPB * D::EL + EPB * 6 * D::FS + le * 6 * D::NB;
-    double* sR = regb + le * D::EL;
-    double* w = wF + le * 16 * N3;
-    double* lf = wLift + le * 24 * N2;
-    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
-    mbar_wait(&bars[sidx], (it >> 1) & 1);
-
-    // Phase 1: face fluxes (in place over the neighbour data), lift*, q.
-    if (active) {
-      if (VISC) {
-        double u[5], qq[4];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-        prim4(u, C.gas, qq);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) w[c * N3 + t] = qq[c];
-      }
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        double* nb = sNb + s * D::NB;
-        const int code = P.side_code[8 * e + s];
-        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-        if (typ == kSliding) {
-          if (VISC) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = nb[D::TS + f * 4 + c];
-          }
-          continue;
-        }
-        double own[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
-        double flux[5], lift[4];
-        bool ok;
-        const double vg = dir == 1 ? B.vg : 0.0;
-        if (typ == kConforming) {
-          double other[5];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
-          const double* um = (s & 1) ? own : other;
-          const double* up = (s & 1) ? other : own;
-          if (VISC) {
-            double qa[4], qb[4];
-            prim4(own, C.gas, qa);
-            prim4(other, C.gas, qb);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-            double fa[4], fb[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              fa[c] = sFv[s * D::FS + f * 4 + c];
-              fb[c] = nb[D::TS + f * 4 + c];
-            }
-            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        } else {
-          double x[3], ext[5];
-          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-          const double* um = (s & 1) ? own : ext;
-          const double* up = (s & 1) ? ext : own;
-          if (VISC) {
-            prim4(ext, C.gas, lift);
-            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
-            double gg[12];
-#pragma unroll
-            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
-            double fm[4], fp[4];
-            fv_dir(um, gg, dir, C.gas, fm);
-            fv_dir(up, gg, dir, C.gas, fp);
-            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        }
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
-        if (VISC) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
-        }
-      }
-    }
-    __syncthreads();
-    // Phase 2: gradient (line tasks) into w[4 N3 ..], then pointwise fluxes.
-    if (VISC && LINES) {
-      const int one[6] = {1, 1, 1, 1, 1, 1};
-      if (active) gradient_lines<N1>(C, B, w, lf, 4 * N2, one, N2, w + 4 * N3, t, N3);
-      __syncthreads();
-    }
-    double F[3][5], u[5];
-    if (active) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = rcp_nr(u[0]);
-      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
-      const double p = pressure(u, ir, C.gas);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double vgd = d == 1 ? B.vg : 0.0;
-        F[d][0] = u[0] * vv[d] - vgd * u[0];
-        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
-        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
-        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
-        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
-      }
-      if (VISC) {
-        double g[12];
-        if (LINES) {
-#pragma unroll
-          for (int c = 0; c < 12; ++c) g[c] = w[(4 + c) * N3 + t];
-        } else {
-          node_gradient<N1>(tab, w, lf, B, i, j, k, g);
-        }
-        const double div = g[0] + g[4] + g[8];
-        const double mu = C.gas.mu, lam = C.gas.lam;
-        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
-                     t22 = 2.0 * mu * g[8] + lam * div;
-        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
-        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          F[d][1] -= tau[d][0];
-          F[d][2] -= tau[d][1];
-          F[d][3] -= tau[d][2];
-          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
-        }
-      }
-    }
-    if (VISC) __syncthreads();  // all gradient reads done before F overwrites w
-    if (active) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) w[(d * 5 + v) * N3 + t] = F[d][v] * B.sj[d];
-    }
-    __syncthreads();
-    // Phase 3-5: weak divergence (all directions), surface lift, RK update, admissibility.
-    if (active) {
-      double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      const double* dh = tab;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const int ia = d == 0 ? i : (d == 1 ? j : k);
-        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          const double c = dh[ia * N1 + m];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) acc[v] += c * w[(d * 5 + v) * N3 + base + m * stride];
-        }
-      }
-      double du[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
-      const double* lw = tab + N1 * N1 + 2 * N1;
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int dir = s >> 1;
-        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
-        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
-        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
-        if (c != 0.0) {
-          const double* fl = sNb + s * D::NB + f * 5;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
-        }
-      }
-      if (A.mode == 1) {
-        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = du[v];
-      } else {
-        mbar_wait(&bars[2], it & 1);
-        double wv[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
-          wv[v] = u[v] + A.rk_b * rg;
-          sR[t * 5 + v] = rg;
-          sU[t * 5 + v] = wv[v];
-        }
-        const double p = pressure(wv, rcp_nr(wv[0]), C.gas);
-        bool ok = wv[0] > 0.0 && p > 0.0;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ok = ok && isfinite(wv[v]);
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, wv);
-      }
-    }
-    if (A.mode == 1) {
-      __syncthreads();
-      continue;
-    }
-    __syncthreads();
-    // Phase 6: traces of the new state (into w), then bulk stores of U, reg and traces.
-    if (active) {
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) w[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n_el * D::EL * 8u);
-      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, regb, n_el * D::EL * 8u);
-      for (int l = 0; l < n_el; ++l)
-        bulk_s2g(P.trace_out + static_cast<size_t>(e0 + l) * 6 * D::TS, wF + l * 16 * N3, 6u * D::TS * 8u);
-      bulk_commit();
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait0();
-}
-
 // v2 layout.  Stage (double-buffered, TMA): U, the element's own face traces (written by the
 // previous stage's phase 6 / k_prolong, so phase 1 needs no prolongation), own Fv.n and the
 // per-side neighbour trace + Fv.n (or mortar flux + lift*).  The RK register is prefetched into
@@ -2260,147 +1983,6 @@ __device__ __forceinline__ void fvn_item(const ElemConsts& C, const double* gS, 
   fv_dir(own, gt, DIR, C.gas, out);
 }
 
-template <int N1, int MINB>
-__global__ void __launch_bounds__(Tma<N1>::THREADS, MINB) k_gradient_tma(const __grid_constant__ ElemConsts C,
-                                                                        FieldPtrs P, StageArgs A) {
-  using D = Tma<N1>;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* stage0 = smem + D::TAB;
-  double* wTr = stage0 + 2 * D::G_STAGE;  // EPB x 6 TS (own traces, AoS)
-  double* wQ = wTr + EPB * 6 * D::TS;     // q (SoA), later the Fv.n output (slot layout)
-  double* wG = wQ + D::G_WQ;              // EPB x 12 N3 SoA
-  double* wFv = wG + EPB * 12 * N3;       // EPB x 6 FS Fv.n output (global slot layout)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wFv + EPB * 6 * D::FS);
-  __shared__ __align__(16) int codes[2][8 * EPB];
-  __shared__ int lstr[EPB][6];
-  load_tables<N1>(C, tab);
-  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < tiles) {
-    prefetch_codes<N1>(P, tile, codes[0]);
-    cp_async_wait_all();
-    issue_gradient_loads<N1>(P, tile, codes[0], stage0, &bars[0]);
-    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
-  }
-  constexpr int WQ1 = D::G_WQ / EPB;
-  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-    const int sidx = it & 1;
-    double* st = stage0 + sidx * D::G_STAGE;
-    const int next = tile + gridDim.x;
-    if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous Fv.n store has read wFv (rewritten two barriers later)
-      if (next < tiles) {
-        cp_async_wait_all();
-        fence_proxy_async();
-        issue_gradient_loads<N1>(P, next, codes[(it + 1) & 1], stage0 + (sidx ^ 1) * D::G_STAGE, &bars[sidx ^ 1]);
-        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[it & 1]);
-      }
-    }
-    const int e0 = P.e_first + tile * EPB;
-    const int e = e0 + le;
-    const bool active = e < P.E;
-    double* sU = st + le * D::EL;
-    double* sNb = st + EPB * D::EL + le * 6 * D::TS;
-    double* tr = wTr + le * 6 * D::TS;
-    double* q = wQ + le * WQ1;
-    double* gS = wG + le * 12 * N3;
-    const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
-    mbar_wait(&bars[sidx], (it >> 1) & 1);
-    // Phase 1: q, own traces, lift* (in place over the neighbour slot, stride 5).
-    if (active) {
-      double u[5], qq[4];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      prim4(u, C.gas, qq);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        double own[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) own[v] = prolong_aos<N1>(sU, v, ell, dir, a, b);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) tr[s * D::TS + f * 5 + v] = own[v];
-        const int code = P.side_code[8 * e + s];
-        const int typ = code >> kCodeShift;
-        double* nb = sNb + s * D::TS;
-        double lift[4];
-        if (typ == kConforming) {
-          double other[5], qa[4], qb[4];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
-          prim4(own, C.gas, qa);
-          prim4(other, C.gas, qb);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-        } else if (typ == kSliding) {
-          if (f == 0) lstr[le][s] = 4;  // back-projected lift* already in place, [N2][4]
-          continue;
-        } else {
-          double x[3], ext[5];
-          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-          prim4(ext, C.gas, lift);
-        }
-        if (f == 0) lstr[le][s] = 5;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) nb[f * 5 + c] = lift[c];  // in place over this node's trace
-      }
-    }
-    __syncthreads();
-    // Phase 2: gradient by line tasks.
-    if (active) gradient_lines<N1>(C, B, q, sNb, D::TS, lstr[le], 1, gS, t, N3);
-    __syncthreads();
-    if (active && P.grad_out != nullptr) {
-      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
-#pragma unroll
-      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
-    }
-    // Phase 3: Fv.n on conforming sides (8 of the 12 trace components), full
-    // gradient traces on sliding / Dirichlet sides.
-    double* fvo = wFv + le * 6 * D::FS;
-    if (active) {
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        const int code = P.side_code[8 * e + s];
-        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-        if (typ == kConforming) {
-          double fv[4];
-          const double* own = tr + s * D::TS + f * 5;
-          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, own, fv);
-          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, own, fv);
-          else fvn_item<N1, 2>(C, gS, ell, a, b, own, fv);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
-        } else {
-          double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
-#pragma unroll
-          for (int c = 0; c < 12; ++c) dst[c] = prolong1<N1>(gS + c * N3, ell, dir, a, b);
-        }
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int n = min(EPB, P.E - e0);
-      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, n * 6u * D::FS * 8u);
-      bulk_commit();
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait0();
-}
-
 // ============================================================================
 // v5 element kernels.  Differences from the kernels above:
 //  * the element's own face traces are staged by TMA (the slots the previous
@@ -2499,253 +2081,6 @@ __device__ __forceinline__ void issue_update_loads5(const FieldPtrs& P, int tile
     }
 }
 
-template <int N1, bool VISC>
-__global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_update5(const __grid_constant__ ElemConsts C,
-                                                                          FieldPtrs P, StageArgs A) {
-  using D = T5<N1>;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* stage0 = smem + D::TAB;
-  double* wF = stage0 + 2 * D::U_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wF + EPB * 5 * N3);
-  __shared__ __align__(16) int codes[3][8 * EPB];
-  load_tables<N1>(C, tab);
-  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < tiles) {
-    prefetch_codes<N1>(P, tile, codes[0]);
-    cp_async_wait_all();
-    issue_update_loads5<N1, VISC>(P, tile, codes[0], stage0, &bars[0]);
-    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
-  }
-  __syncthreads();  // codes[0] visible to every thread
-  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-    const int sidx = it & 1;
-    double* st = stage0 + sidx * D::U_STAGE;
-    const int next = tile + gridDim.x;
-    const int e0 = P.e_first + tile * EPB;
-    const int n_el = min(EPB, P.E - e0);
-    const int* cd = codes[it % 3];
-    if (threadIdx.x == 0) {
-      bulk_wait_read0();  // the previous tile's stores have read stage sidx^1
-      fence_proxy_async();
-      if (next < tiles) {
-        cp_async_wait_all();  // codes of `next`
-        issue_update_loads5<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::U_STAGE,
-                                      &bars[sidx ^ 1]);
-        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
-      }
-    }
-    const int e = e0 + le;
-    const bool active = le < n_el;
-    double* sU = st + le * D::EL;
-    double* sR = st + EPB * D::EL + le * D::EL;
-    double* sTr = st + EPB * 2 * D::EL + le * 6 * D::TS;
-    double* sFv = st + EPB * (2 * D::EL + 6 * D::TS) + le * 6 * D::FS;
-    double* sNb = st + EPB * (2 * D::EL + 6 * D::TS + 6 * D::FS) + le * 6 * D::NB;
-    double* q = wF + le * 5 * N3;
-    const int* myc = cd + 8 * le;
-    const BandD& B = C.bands[active ? myc[6] : 0];
-    mbar_wait(&bars[sidx], (it >> 1) & 1);
-
-    // Phase 1: face fluxes (in place over the neighbour data) and lift*.
-    if (active) {
-      if (VISC) {
-        double u[5], qq[4];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-        prim4(u, C.gas, qq);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
-      }
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm - s * N2, dir = s >> 1;
-        double* nb = sNb + s * D::NB;
-        const int code = myc[s];
-        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-        if (typ == kSliding) continue;  // flux and lift* arrived in place
-        double own[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) own[v] = sTr[s * D::TS + f * 5 + v];
-        double flux[5], lift[4];
-        bool ok;
-        const double vg = dir == 1 ? B.vg : 0.0;
-        if (typ == kConforming) {
-          double other[5];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
-          const double* um = (s & 1) ? own : other;
-          const double* up = (s & 1) ? other : own;
-          if (VISC) {
-            double qa[4], qb[4];
-            prim4(own, C.gas, qa);
-            prim4(other, C.gas, qb);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-            double fa[4], fb[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              fa[c] = sFv[s * D::FS + f * 4 + c];
-              fb[c] = nb[D::TS + f * 4 + c];
-            }
-            ok = face_flux_fv(um, up, dir, vg, (s & 1) ? fa : fb, (s & 1) ? fb : fa, C.gas, flux);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        } else {
-          const int a = f / N1, b = f - (f / N1) * N1;
-          double x[3], ext[5];
-          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-          const double* um = (s & 1) ? own : ext;
-          const double* up = (s & 1) ? ext : own;
-          if (VISC) {
-            prim4(ext, C.gas, lift);
-            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
-            double gg[12];
-#pragma unroll
-            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
-            double fm[4], fp[4];
-            fv_dir(um, gg, dir, C.gas, fm);
-            fv_dir(up, gg, dir, C.gas, fp);
-            ok = face_flux_fv(um, up, dir, vg, fm, fp, C.gas, flux);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        }
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
-        if (VISC) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) nb[D::TS + f * 4 + c] = lift[c];
-        }
-      }
-    }
-    __syncthreads();
-
-    // Phase 2: pointwise volume flux (gradient recomputed from q and lift*).
-    double F[3][5], u[5];
-    if (active) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = rcp_nr(u[0]);
-      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
-      const double p = pressure(u, ir, C.gas);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double vgd = d == 1 ? B.vg : 0.0;
-        F[d][0] = u[0] * vv[d] - vgd * u[0];
-        F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
-        F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
-        F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
-        F[d][4] = (u[4] + p) * vv[d] - vgd * u[4];
-      }
-      if (VISC) {
-        double g[12];
-        node_gradient_nb<N1>(tab, q, sNb, D::NB, D::TS, B, i, j, k, g);
-        const double div = g[0] + g[4] + g[8];
-        const double mu = C.gas.mu, lam = C.gas.lam;
-        const double t00 = 2.0 * mu * g[0] + lam * div, t11 = 2.0 * mu * g[4] + lam * div,
-                     t22 = 2.0 * mu * g[8] + lam * div;
-        const double t01 = mu * (g[1] + g[3]), t02 = mu * (g[2] + g[6]), t12 = mu * (g[5] + g[7]);
-        const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          F[d][1] -= tau[d][0];
-          F[d][2] -= tau[d][1];
-          F[d][3] -= tau[d][2];
-          F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
-        }
-      }
-    }
-
-    // Phase 3: weak divergence per direction through shared memory.
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      __syncthreads();
-      if (active) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) q[v * N3 + t] = F[d][v] * B.sj[d];
-      }
-      __syncthreads();
-      if (active) {
-        const int ia = d == 0 ? i : (d == 1 ? j : k);
-        const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-        const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          const double c = tab[ia * N1 + m];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) acc[v] += c * q[v * N3 + base + m * stride];
-        }
-      }
-    }
-
-    // Phase 4-5: surface lift, RK update in place, admissibility.
-    if (active) {
-      double du[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
-      const double* lw = tab + N1 * N1 + 2 * N1;
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int dir = s >> 1;
-        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
-        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
-        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
-        if (c != 0.0) {
-          const double* fl = sNb + s * D::NB + f * 5;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
-        }
-      }
-      if (A.mode == 1) {
-        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = du[v];
-      } else {
-        double wv[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          const double rg = A.rk_a * sR[t * 5 + v] + A.dt * du[v];
-          wv[v] = u[v] + A.rk_b * rg;
-          sR[t * 5 + v] = rg;
-          sU[t * 5 + v] = wv[v];
-        }
-        const double p = pressure(wv, rcp_nr(wv[0]), C.gas);
-        bool ok = wv[0] > 0.0 && p > 0.0;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ok = ok && isfinite(wv[v]);
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, wv);
-      }
-    }
-    __syncthreads();
-    if (A.mode == 1) continue;
-    // Phase 6: traces of the new state in place over the consumed own traces.
-    if (active) write_traces<N1>(tab, sU, sTr, t, N3);
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n_el * D::EL * 8u);
-      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n_el * D::EL * 8u);
-      bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, st + EPB * 2 * D::EL, n_el * 6u * D::TS * 8u);
-      bulk_commit();
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait0();
-}
-
 template <int N1>
 __device__ __forceinline__ void issue_gradient_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
                                                       uint64_t* bar) {
@@ -2771,148 +2106,6 @@ __device__ __forceinline__ void issue_gradient_loads5(const FieldPtrs& P, int ti
       if (typ == kConforming) bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
       else if (typ == kSliding) bulk_g2s(nb, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
     }
-}
-
-template <int N1>
-__global__ void __launch_bounds__(T5<N1>::THREADS, T5<N1>::MINB) k_gradient5(const __grid_constant__ ElemConsts C,
-                                                                            FieldPtrs P, StageArgs A) {
-  using D = T5<N1>;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* stage0 = smem + D::TAB;
-  double* wQ = stage0 + 2 * D::G_STAGE;  // EPB x 4 N3
-  double* wG = wQ + EPB * 4 * N3;        // EPB x 12 N3
-  double* wFv = wG + EPB * 12 * N3;      // EPB x 6 FS
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wFv + EPB * 6 * D::FS);
-  __shared__ __align__(16) int codes[3][8 * EPB];
-  __shared__ int lstr[EPB][6];
-  __shared__ BandD sbands[SDG_MAX_BANDS];
-  load_tables<N1>(C, tab);
-  load_bands(C, sbands);
-  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  int tile = blockIdx.x;
-  if (threadIdx.x == 0 && tile < tiles) {
-    prefetch_codes<N1>(P, tile, codes[0]);
-    cp_async_wait_all();
-    issue_gradient_loads5<N1>(P, tile, codes[0], stage0, &bars[0]);
-    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
-  }
-  __syncthreads();
-  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-    const int sidx = it & 1;
-    double* st = stage0 + sidx * D::G_STAGE;
-    const int next = tile + gridDim.x;
-    const int e0 = P.e_first + tile * EPB;
-    const int n_el = min(EPB, P.E - e0);
-    if (threadIdx.x == 0) {
-      if (next < tiles) {
-        cp_async_wait_all();
-        fence_proxy_async();
-        issue_gradient_loads5<N1>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::G_STAGE, &bars[sidx ^ 1]);
-        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
-      }
-    }
-    const int e = e0 + le;
-    const bool active = le < n_el;
-    const int* myc = codes[it % 3] + 8 * le;
-    double* sU = st + le * D::EL;
-    double* sTr = st + EPB * D::EL + le * 6 * D::TS;
-    double* sNb = st + EPB * (D::EL + 6 * D::TS) + le * 6 * D::TS;
-    double* q = wQ + le * 4 * N3;
-    double* gS = wG + le * 12 * N3;
-    double* fvo = wFv + le * 6 * D::FS;
-    const BandD& B = sbands[active ? myc[6] : 0];
-    mbar_wait(&bars[sidx], (it >> 1) & 1);
-    // Phase 1: q; lift* in place over the neighbour slot (stride 5), sliding lift* stays at stride 4.
-    if (active) {
-      double u[5], qq[4];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      prim4(u, C.gas, qq);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm - s * N2;
-        const int typ = myc[s] >> kCodeShift;
-        double* nb = sNb + s * D::TS;
-        if (typ == kSliding) {
-          if (f == 0) lstr[le][s] = 4;
-          continue;
-        }
-        double lift[4];
-        const double* own = sTr + s * D::TS + f * 5;
-        if (typ == kConforming) {
-          double ow[5], other[5], qa[4], qb[4];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            ow[v] = own[v];
-            other[v] = nb[f * 5 + v];
-          }
-          prim4(ow, C.gas, qa);
-          prim4(other, C.gas, qb);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-        } else {
-          const int a = f / N1, b = f - (f / N1) * N1;
-          double x[3], ext[5];
-          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-          prim4(ext, C.gas, lift);
-        }
-        if (f == 0) lstr[le][s] = 5;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) nb[f * 5 + c] = lift[c];
-      }
-    }
-    __syncthreads();
-    if (active) gradient_lines<N1>(C, B, q, sNb, D::TS, lstr[le], 1, gS, t, N3);
-    // The previous tile's Fv.n store must have read wFv before phase 3 rewrites it; waiting
-    // here (not at the top of the tile) keeps warp 0 from holding up phase 1.
-    if (threadIdx.x == 0) bulk_wait_read0();
-    __syncthreads();
-    if (active && P.grad_out != nullptr) {
-      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
-#pragma unroll
-      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
-    }
-    // Phase 3: Fv.n on conforming sides; full gradient traces on sliding / Dirichlet sides.
-    if (active) {
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm - s * N2, a = f / N1, b = f - a * N1, dir = s >> 1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        const int code = myc[s];
-        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-        if (typ == kConforming) {
-          double fv[4];
-          const double* own = sTr + s * D::TS + f * 5;
-          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, own, fv);
-          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, own, fv);
-          else fvn_item<N1, 2>(C, gS, ell, a, b, own, fv);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
-        } else {
-          double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
-#pragma unroll
-          for (int c = 0; c < 12; ++c) dst[c] = prolong1<N1>(gS + c * N3, ell, dir, a, b);
-        }
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_s2g(P.fvn + static_cast<size_t>(e0) * 6 * D::FS, wFv, n_el * 6u * D::FS * 8u);
-      bulk_commit();
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -3103,28 +2296,6 @@ bool gws_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm
   }
 }
 
-template <int N1>
-bool v5_t(bool update, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
-  if constexpr (N1 % 2 != 0) {
-    return false;
-  } else {
-    using D = T5<N1>;
-    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    auto kern = update ? (c.gas.viscous ? k_update5<N1, true> : k_update5<N1, false>) : k_gradient5<N1>;
-    const int smem = update ? D::U_SMEM : D::G_SMEM;
-    static int occ_tab[3] = {-1, -1, -1};
-    int& occ = occ_tab[update ? (c.gas.viscous ? 1 : 2) : 0];
-    if (occ < 0) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, D::THREADS, smem);
-      if (occ < 1) occ = 1;
-    }
-    const int grid = std::min(tiles, n_sm * occ);
-    kern<<<grid, D::THREADS, smem, st>>>(c, p, a);
-    check_launch(update ? "k_update5" : "k_gradient5");
-    return true;
-  }
-}
 
 template <int N1>
 bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
@@ -3138,19 +2309,17 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
       const char* env = std::getenv("SDG_UPDATE_V");
       variant = env ? std::atoi(env) : 6;
     }
-    const bool v3 = variant == 3 || variant == 4;
+    // 6: node-major packed staging (default of this kernel), 8: warp-specialised, 2: SoA staging
     const bool ws = variant == 8;
-    const bool pack = variant == 6 || ws;
+    const bool pack = variant != 2;
     const bool vis = c.gas.viscous != 0;
-    auto kern = variant == 3 ? (vis ? k_update_tma<N1, true, true> : k_update_tma<N1, false, true>)
-              : variant == 4 ? (vis ? k_update_tma<N1, true, false> : k_update_tma<N1, false, false>)
-              : ws ? (vis ? k_update_tma_v2<N1, true, true, true> : k_update_tma_v2<N1, false, true, true>)
+    auto kern = ws ? (vis ? k_update_tma_v2<N1, true, true, true> : k_update_tma_v2<N1, false, true, true>)
               : pack ? (vis ? k_update_tma_v2<N1, true, true, false> : k_update_tma_v2<N1, false, true, false>)
                      : (vis ? k_update_tma_v2<N1, true, false, false> : k_update_tma_v2<N1, false, false, false>);
-    const int smem = v3 ? D::U_SMEM : (pack ? TmaV2<N1>::U_SMEM_PACK : TmaV2<N1>::U_SMEM);
+    const int smem = pack ? TmaV2<N1>::U_SMEM_PACK : TmaV2<N1>::U_SMEM;
     const int threads = ws ? UWs<N1>::THREADS : D::THREADS;
     static int occ_tab[10] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-    int& occ = occ_tab[(variant == 3 ? 2 : variant == 4 ? 4 : ws ? 8 : pack ? 6 : 0) + (vis ? 1 : 0)];
+    int& occ = occ_tab[(ws ? 8 : pack ? 6 : 0) + (vis ? 1 : 0)];
     if (occ < 0) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
@@ -3159,33 +2328,6 @@ bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, i
     const int grid = std::min(tiles, n_sm * occ);
     kern<<<grid, threads, smem, st>>>(c, p, a);
     check_launch("k_update_tma");
-    return true;
-  }
-}
-template <int N1>
-bool gradient_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
-  if constexpr (N1 % 2 != 0) {
-    return false;
-  } else {
-    using D = Tma<N1>;
-    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    static int minb = -1;
-    if (minb < 0) {
-      const char* env = std::getenv("SDG_GRAD_MINB");
-      minb = env ? std::atoi(env) : D::MINB_G;
-      if (minb != 2 && minb != D::MINB_G) minb = D::MINB_G;
-    }
-    auto kern = minb == D::MINB_G ? k_gradient_tma<N1, D::MINB_G> : k_gradient_tma<N1, 2>;
-    static int occ[2] = {-1, -1};
-    int& o = occ[minb == D::MINB_G ? 0 : 1];
-    if (o < 0) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, D::THREADS, D::G_SMEM);
-      if (o < 1) o = 1;
-    }
-    const int grid = std::min(tiles, n_sm * o);
-    kern<<<grid, D::THREADS, D::G_SMEM, st>>>(c, p, a);
-    check_launch("k_gradient_tma");
     return true;
   }
 }
@@ -3284,27 +2426,15 @@ bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const 
                          cudaStream_t st) {
   if (p.E <= p.e_first) return true;
   bool ok = false;
-  static const int gv = env_int("SDG_GRAD_V", 6);
-  if (gv == 6) {
-    SDG_DISPATCH(n1, (ok = gws_t<NN>(c, p, a, n_sm, st)));
-    return ok;
-  }
-  if (gv == 5) {
-    SDG_DISPATCH(n1, (ok = v5_t<NN>(false, c, p, a, n_sm, st)));
-    return ok;
-  }
-  SDG_DISPATCH(n1, (ok = gradient_tma_t<NN>(c, p, a, n_sm, st)));
+  static const int gv = env_int("SDG_GRAD_V", 6);  // 6: warp-specialised; anything else: the plain kernel
+  if (gv != 6) return false;
+  SDG_DISPATCH(n1, (ok = gws_t<NN>(c, p, a, n_sm, st)));
   return ok;
 }
 bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                        cudaStream_t st) {
   if (p.E <= p.e_first) return true;
   bool ok = false;
-  static const int uv = env_int("SDG_UPDATE_V", 6);
-  if (uv == 5) {
-    SDG_DISPATCH(n1, (ok = v5_t<NN>(true, c, p, a, n_sm, st)));
-    return ok;
-  }
   SDG_DISPATCH(n1, (ok = update_tma_t<NN>(c, p, a, n_sm, st)));
   return ok;
 }
