@@ -92,3 +92,24 @@ def test_product_annulus_metrics_match_oracle(kind, degree, warp):
         gids = np.array(capi.plan(mesh, 3, r)["elements"])
         m3, f3 = capi.metrics_host(mesh, degree, kind, 3, r)
         assert np.array_equal(m3, met[gids]) and np.array_equal(f3, fmet[gids])
+
+
+def test_sector_metrics_rotate_across_the_seam():
+    """Periodic annulus sector: the two slots of a seam face are not copied from one side; each
+    side's face metrics are its own, and (invariant curl form) they are exact rotations of each
+    other by the sector angle: n(theta = 0) = R(-alpha) n(theta = alpha)."""
+    alpha = np.pi / 4
+    mesh = T.annulus_spec([(2, 1.0, 0.0), (2, 1.0, 0.8)], 3, 2, 0.5, 1.0, theta_span=alpha)
+    assert mesh.periodic_y == 1
+    met, fmet = capi.metrics_host(mesh, 3, T.NODES_GAUSS)
+    c, s = np.cos(-alpha), np.sin(-alpha)
+    n_theta, n_r = 3, 2
+    for b in range(2):
+        for ix in range(2):
+            for ir in range(n_r):
+                lo = b * 2 * n_theta * n_r + (ix * n_theta + 0) * n_r + ir            # theta row 0, side YM (2)
+                hi = b * 2 * n_theta * n_r + (ix * n_theta + n_theta - 1) * n_r + ir  # last row, side YP (3)
+                n_lo, n_hi = fmet[lo, 2, :, :3], fmet[hi, 3, :, :3]
+                rot = np.stack([n_hi[:, 0], c * n_hi[:, 1] + s * n_hi[:, 2], -s * n_hi[:, 1] + c * n_hi[:, 2]], axis=1)
+                assert np.abs(rot - n_lo).max() < 1e-14
+                assert np.abs(fmet[lo, 2, :, 3] - fmet[hi, 3, :, 3]).max() < 1e-15 * fmet[lo, 2, :, 3].max()
