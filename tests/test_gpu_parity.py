@@ -5,6 +5,7 @@ step, <= 1e-10 after 100 stages; residuals compared relative to their own
 scale at 1e-12 (absolute 1e-12 for free-stream noise); pairing bit-exact.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -150,6 +151,25 @@ def test_tgv_three_blocks():
     dt = o.suggest_dt(0.5)
     g.step(dt, 2)
     o.step(dt, 2)
+    assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+@pytest.mark.parametrize("degree", [3, 5, 7])
+def test_baseline_config4_sweep_smallest_load(degree):
+    """BASELINE configs[4] sweep at its smallest load (8^3 elements, the bench's mesh builder:
+    three blocks along the split axis, middle block sliding at +0.2), N in {3, 5, 7}: one RK step
+    equal to the oracle."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    mesh, _ = bench.tgv_mesh(T, 8, 8)
+    cfg = T.solver_config(degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    dt = o.suggest_dt(0.5)
+    g.step(dt)
+    o.step(dt)
     assert rel_linf(g.field(), o.field()) <= 1e-12
 
 
