@@ -114,6 +114,21 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
                        long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
                        int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry);
 
+/* Host-only building blocks of non-matching sliding interfaces (BASELINE
+ * configs[1]; the reference requires equal face counts, proj/src/mesh.cpp:75-77):
+ * sdg_subrange_ops: face <-> mortar L2 operators (n x n each, row-major) of a
+ * mortar covering the face sub-range [lo, hi] of [-1, 1]; the reference's
+ * build_mortar_operators (mortar.cpp:79-134) is the pair [-1, sigma], [sigma, 1],
+ * reproduced bit for bit.
+ * sdg_mortar_intervals: the mortars of one periodic face row where side A has
+ * n_a faces of length l_a and side B n_b faces over the same period, displaced
+ * by delta: per mortar (A face, B face) in faces[2k..] and (a_lo, a_hi, b_lo,
+ * b_hi) in ranges[4k..], sorted by A face and position.  With n_a == n_b this
+ * is the reference's pairing (moving_index, sigma / -sigma, mortar.cpp:136-150).
+ * faces/ranges may be NULL to query *n_out (at most n_a + n_b). */
+int sdg_subrange_ops(int degree, int node_kind, double lo, double hi, double* fwd, double* bwd);
+int sdg_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges);
+
 /* Diagnostics on the device (integrate_mass_energy / error_norms /
  * max_freestream_deviation, diagnostics.cpp:31-87): out[14] = mass, energy,
  * volume, L2 error[5], Linf error[5], max deviation; the errors are against the

@@ -78,6 +78,8 @@ def oracle_lib():
         lib.orc_nodes.argtypes = [C.c_int, C.c_int, _dp, _dp]
         lib.orc_basis.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
         lib.orc_mortar_ops.argtypes = [C.c_int, C.c_int, C.c_double, _dp, _dp]
+        lib.orc_subrange_ops.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp]
+        lib.orc_mortar_intervals.argtypes = [C.c_long, C.c_long, C.c_double, C.c_double, _lp, _lp, _dp]
         lib.orc_displacement.argtypes = [C.c_double, C.c_double, C.c_long, _dp, _lp, _dp]
         lib.orc_moving_index.argtypes = [C.c_long, C.c_long, C.c_int, C.c_long]
         lib.orc_moving_index.restype = C.c_long
@@ -271,6 +273,26 @@ def oracle_mortar_ops(degree, kind, sigma):
     f, b = np.zeros((2, n, n)), np.zeros((2, n, n))
     T.raise_for(oracle_lib().orc_mortar_ops(degree, kind, sigma, _d(f), _d(b)), oracle_lib().orc_global_error().decode())
     return f, b
+
+
+def subrange_ops(degree, kind, lo, hi):
+    """Mortar operators of the face sub-range [lo, hi] (non-matching interfaces)."""
+    n = degree + 1
+    f, b = np.zeros((n, n)), np.zeros((n, n))
+    T.raise_for(oracle_lib().orc_subrange_ops(degree, kind, lo, hi, _d(f), _d(b)), oracle_lib().orc_global_error().decode())
+    return f, b
+
+
+def mortar_intervals(n_a, n_b, l_a, delta):
+    """Mortars of a non-matching periodic face row: faces [M, 2], ranges [M, 4]."""
+    L = oracle_lib()
+    n = C.c_long()
+    T.raise_for(L.orc_mortar_intervals(n_a, n_b, l_a, delta, C.byref(n), None, None), L.orc_global_error().decode())
+    faces = np.zeros((n.value, 2), dtype=np.int64)
+    ranges = np.zeros((n.value, 4))
+    T.raise_for(L.orc_mortar_intervals(n_a, n_b, l_a, delta, C.byref(n), faces.ctypes.data_as(_lp), _d(ranges)),
+                L.orc_global_error().decode())
+    return faces, ranges
 
 
 def ref_mortar_ops(degree, kind, sigma):

@@ -265,6 +265,48 @@ static void mortar_ops(const Nodes& ns, double sigma, double* fwd, double* bwd) 
   }
 }
 
+// General sub-range mortar (non-matching interfaces, BASELINE configs[1]): the same
+// construction as mortar_ops with the mortar on face coordinates [lo, hi].
+static void subrange_ops(const Nodes& ns, double lo, double hi, double* fwd, double* bwd) {
+  if (!(lo >= -1.0 && lo < hi && hi <= 1.0)) throw ConfigError("mortar sub-range must satisfy -1 <= lo < hi <= 1");
+  const int n = ns.count();
+  const Nodes gauss(ns.degree, SDG_NODES_GAUSS);
+  std::vector<ld> xs(ns.x.begin(), ns.x.end()), bw(n, 1.0L);
+  for (int j = 0; j < n; ++j) {
+    for (int k = 0; k < n; ++k)
+      if (k != j) bw[j] *= xs[j] - xs[k];
+    bw[j] = 1.0L / bw[j];
+  }
+  std::vector<ld> mass(n * n, 0.0L), lq(n), lx(n), s(n * n, 0.0L);
+  for (int q = 0; q < n; ++q) {
+    ld_lagrange(xs, bw, gauss.x[q], lq.data());
+    const ld wq = gauss.w[q];
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) mass[i * n + j] += wq * lq[i] * lq[j];
+  }
+  const ld frac = 0.5L * (static_cast<ld>(hi) - static_cast<ld>(lo));
+  for (int q = 0; q < n; ++q) {
+    const ld z = gauss.x[q];
+    ld_lagrange(xs, bw, static_cast<ld>(lo) + frac * (z + 1.0L), lx.data());
+    ld_lagrange(xs, bw, z, lq.data());
+    const ld wq = gauss.w[q];
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) s[i * n + j] += wq * lx[i] * lq[j];
+  }
+  std::vector<ld> st(n * n), sw(n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      st[i * n + j] = s[j * n + i];
+      sw[i * n + j] = frac * s[i * n + j];
+    }
+  ld_spd_solve(mass, st, n);
+  ld_spd_solve(mass, sw, n);
+  for (int i = 0; i < n * n; ++i) {
+    fwd[i] = static_cast<double>(st[i]);
+    bwd[i] = static_cast<double>(sw[i]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Interface kinematics and index algebra: proj/src/mesh.cpp:9-25,
 // proj/src/mortar.cpp:136-150.
@@ -300,6 +342,65 @@ static long moving_index(long i_par, long n_delta, int i_sub, long n_faces) {
 static long static_index(long i_moving, long n_delta, int i_sub, long n_faces) {
   const long raw = i_moving + n_delta - i_sub + 1;
   return ((raw % n_faces) + n_faces) % n_faces;
+}
+
+// Non-matching periodic face rows (BASELINE configs[1]; the reference needs equal
+// counts, proj/src/mesh.cpp:75-77).  Side A: n_a faces of length l_a; side B: n_b
+// faces over the same period, displaced by delta.  In A units, B edge j is
+// n_delta + k_j + (s + r_j / n_b) with j n_a = k_j n_b + r_j and (n_delta, s) the
+// reference's displacement split, so the equal-count limit keeps the reference's
+// s bits; A-local coordinate of a B edge 2F - 1 (sigma), B-local coordinate of an
+// A edge 1 - 2 (distance to B's right edge) / q (-sigma at equal counts).
+// Restated pairwise: every (A face, B face) overlap, instead of the product's sweep.
+struct Interval {
+  long fa, fb;
+  double r[4];
+};
+static std::vector<Interval> intervals(long n_a, long n_b, double l_a, double delta) {
+  if (n_a < 1 || n_b < 1 || !(l_a > 0.0)) throw ConfigError("bad face rows");
+  const Disp d = displacement(delta, l_a, n_a);
+  const double q = static_cast<double>(n_a) / static_cast<double>(n_b);
+  auto edge = [&](long j, long& I, double& F) {  // B edge j (0 <= j <= n_b), unwrapped
+    const long jj = j % n_b, wraps = j / n_b;
+    I = d.n_delta + (jj * n_a) / n_b + wraps * n_a;
+    F = d.s_delta + static_cast<double>((jj * n_a) % n_b) / static_cast<double>(n_b);
+    if (F >= 1.0) {
+      F -= 1.0;
+      I += 1;
+    }
+  };
+  auto less = [](long i1, double f1, long i2, double f2) { return i1 < i2 || (i1 == i2 && f1 < f2); };
+  std::vector<Interval> out;
+  for (long i = 0; i < n_a; ++i)
+    for (long j = 0; j < n_b; ++j) {
+      long I0, I1;
+      double F0, F1;
+      edge(j, I0, F0);
+      edge(j + 1, I1, F1);
+      for (long cp = 0; cp < 2; ++cp) {  // A face i and its copy one period on
+        const long ai = i + cp * n_a;
+        // overlap [max(ai, e_j), min(ai + 1, e_{j+1})]
+        const bool lo_is_b = less(ai, 0.0, I0, F0) || (ai == I0 && F0 == 0.0);
+        const long lo_i = lo_is_b ? I0 : ai;
+        const double lo_f = lo_is_b ? F0 : 0.0;
+        const bool hi_is_b = less(I1, F1, ai + 1, 0.0) || (I1 == ai + 1 && F1 == 0.0);
+        const long hi_i = hi_is_b ? I1 : ai + 1;
+        const double hi_f = hi_is_b ? F1 : 0.0;
+        if (!less(lo_i, lo_f, hi_i, hi_f)) continue;
+        Interval iv;
+        iv.fa = i;
+        iv.fb = j;
+        iv.r[0] = lo_is_b ? (F0 == 0.0 ? -1.0 : 2.0 * F0 - 1.0) : -1.0;
+        iv.r[1] = hi_is_b ? (F1 == 0.0 ? 1.0 : 2.0 * F1 - 1.0) : 1.0;
+        iv.r[2] = lo_is_b ? -1.0 : 1.0 - 2.0 * ((static_cast<double>(I1 - ai) + F1) / q);
+        iv.r[3] = hi_is_b ? 1.0 : 1.0 - 2.0 * ((static_cast<double>(I1 - (ai + 1)) + F1) / q);
+        out.push_back(iv);
+      }
+    }
+  std::sort(out.begin(), out.end(), [](const Interval& x, const Interval& y) {
+    return x.fa != y.fa ? x.fa < y.fa : x.r[0] < y.r[0];
+  });
+  return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -2268,6 +2369,21 @@ int orc_mortar_ops(int degree, int kind, double sigma, double* fwd, double* bwd)
   return guard(nullptr, [&] {
     const Nodes ns(degree, kind);
     mortar_ops(ns, sigma, fwd, bwd);
+  });
+}
+int orc_subrange_ops(int degree, int kind, double lo, double hi, double* fwd, double* bwd) {
+  return guard(nullptr, [&] { subrange_ops(Nodes(degree, kind), lo, hi, fwd, bwd); });
+}
+int orc_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges) {
+  return guard(nullptr, [&] {
+    const std::vector<Interval> iv = intervals(n_a, n_b, l_a, delta);
+    *n_out = static_cast<long>(iv.size());
+    if (!faces || !ranges) return;
+    for (size_t k = 0; k < iv.size(); ++k) {
+      faces[2 * k] = iv[k].fa;
+      faces[2 * k + 1] = iv[k].fb;
+      for (int c = 0; c < 4; ++c) ranges[4 * k + c] = iv[k].r[c];
+    }
   });
 }
 int orc_displacement(double delta, double l_par, long n_faces, double* d, long* n_delta, double* s_delta) {

@@ -76,6 +76,11 @@ int orc_nodes(int degree, int kind, double* nodes, double* weights);
 int orc_basis(int degree, int kind, double* diff, double* face_left, double* face_right);
 /* fwd/bwd: [2][n][n] (Lower, Upper), row-major. */
 int orc_mortar_ops(int degree, int kind, double sigma, double* fwd, double* bwd);
+/* Non-matching interfaces (BASELINE configs[1]): mortar operators of a face
+ * sub-range [lo, hi] (n*n each) and the mortars of one periodic face row,
+ * faces 2 and ranges 4 per mortar (see include/sdg_gpu.h sdg_mortar_intervals). */
+int orc_subrange_ops(int degree, int kind, double lo, double hi, double* fwd, double* bwd);
+int orc_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges);
 int orc_displacement(double delta, double l_par, long n_faces, double* d, long* n_delta,
                      double* s_delta);
 long orc_moving_index(long i_par, long n_delta, int i_sub, long n_faces);

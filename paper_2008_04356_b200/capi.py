@@ -78,6 +78,8 @@ def lib():
                                          C.c_int, _ip, _ip, _ip, _lp, _ip, _ip, _ip]
         L.sdg_plan_json.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_double, C.c_char_p, C.c_long, _lp]
         L.sdg_metrics_host.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _lp]
+        L.sdg_subrange_ops.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.sdg_mortar_intervals.argtypes = [C.c_long, C.c_long, C.c_double, C.c_double, _lp, _lp, _dp]
         L.sdg_diagnostics.argtypes = [_vp, C.c_double, C.c_int, _dp]
         L.sdg_write_snapshot.argtypes = [_vp, C.c_char_p, C.c_double]
         L.sdg_read_snapshot.argtypes = [_vp, C.c_char_p, _dp]
@@ -100,7 +102,8 @@ EXPORTED = [
     "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
-    "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
+    "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_subrange_ops",
+    "sdg_mortar_intervals", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
     "sdg_trace_json", "sdg_inject_collective", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
@@ -356,6 +359,28 @@ def metrics_host(mesh: T.MeshSpec, degree: int, node_kind: int, n_ranks: int = 1
     T.raise_for(L.sdg_metrics_host(C.byref(mesh), degree, node_kind, n_ranks, rank, _d(met), _d(fmet), C.byref(n)),
                 L.sdg_global_error().decode())
     return met, fmet
+
+
+def subrange_ops(degree: int, node_kind: int, lo: float, hi: float):
+    """Face <-> mortar operators (fwd, bwd), n x n each, of a mortar on face sub-range [lo, hi]."""
+    n1 = degree + 1
+    fwd, bwd = np.zeros((n1, n1)), np.zeros((n1, n1))
+    L = lib()
+    T.raise_for(L.sdg_subrange_ops(degree, node_kind, lo, hi, _d(fwd), _d(bwd)), L.sdg_global_error().decode())
+    return fwd, bwd
+
+
+def mortar_intervals(n_a: int, n_b: int, l_a: float, delta: float):
+    """Mortars of a non-matching periodic face row: (faces [M, 2] = (A face, B face),
+    ranges [M, 4] = (a_lo, a_hi, b_lo, b_hi)), sorted by A face and position."""
+    L = lib()
+    n = C.c_long()
+    T.raise_for(L.sdg_mortar_intervals(n_a, n_b, l_a, delta, C.byref(n), None, None), L.sdg_global_error().decode())
+    faces = np.zeros((n.value, 2), dtype=np.int64)
+    ranges = np.zeros((n.value, 4))
+    T.raise_for(L.sdg_mortar_intervals(n_a, n_b, l_a, delta, C.byref(n), faces.ctypes.data_as(_lp), _d(ranges)),
+                L.sdg_global_error().decode())
+    return faces, ranges
 
 
 def pairing_device(faces, n_par, n_perp, ranks, n_delta, on_static, conforming, self_rank):

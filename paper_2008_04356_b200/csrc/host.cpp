@@ -829,23 +829,32 @@ void chol_solve(std::vector<ld> a, std::vector<ld>& rhs, int n) {
 }
 }  // namespace
 
-void build_mortar_ops(const Basis& bs, double sigma, double* fwd, double* bwd) {
-  if (!(sigma >= -1.0 && sigma < 1.0)) throw ConfigError("mortar position sigma must lie in [-1, 1)");
-  const int n = bs.n;
-  const Basis gauss(bs.degree, SDG_NODES_GAUSS);
-  const LdLagrange lag(bs.x);
-  std::vector<ld> mass(n * n, 0.0L), la(n), lb(n);
-  for (int q = 0; q < n; ++q) {
-    lag.eval(gauss.x[q], la.data());
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < n; ++j) mass[i * n + j] += static_cast<ld>(gauss.w[q]) * la[i] * la[j];
+namespace {
+// Face <-> mortar operators for mortars covering sub-ranges of one face, sharing the
+// face mass matrix (n-point Gauss quadrature, exact for the degree-2N integrands).
+struct SubrangeBuilder {
+  const Basis& bs;
+  Basis gauss;
+  LdLagrange lag;
+  std::vector<ld> mass;
+  explicit SubrangeBuilder(const Basis& b) : bs(b), gauss(b.degree, SDG_NODES_GAUSS), lag(b.x), mass(b.n * b.n, 0.0L) {
+    const int n = bs.n;
+    std::vector<ld> la(n);
+    for (int q = 0; q < n; ++q) {
+      lag.eval(gauss.x[q], la.data());
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) mass[i * n + j] += static_cast<ld>(gauss.w[q]) * la[i] * la[j];
+    }
   }
-  const ld frac[2] = {0.5L * (1.0L + sigma), 0.5L * (1.0L - sigma)};
-  for (int h = 0; h < 2; ++h) {
-    std::vector<ld> s(n * n, 0.0L);
+  // Mortar on face coordinates [lo, hi]: fwd = M^-1 S^T (face -> mortar), bwd =
+  // (hi - lo)/2 M^-1 S (mortar -> face), S_ij = int l_i(xi(z)) l_j(z) dz.
+  void build(double lo, double hi, double* fwd, double* bwd) const {
+    const int n = bs.n;
+    const ld frac = 0.5L * (static_cast<ld>(hi) - static_cast<ld>(lo));
+    std::vector<ld> s(n * n, 0.0L), la(n), lb(n);
     for (int q = 0; q < n; ++q) {
       const ld z = gauss.x[q];
-      const ld xi = h == 0 ? -1.0L + frac[0] * (z + 1.0L) : static_cast<ld>(sigma) + frac[1] * (z + 1.0L);
+      const ld xi = static_cast<ld>(lo) + frac * (z + 1.0L);
       lag.eval(xi, la.data());
       lag.eval(z, lb.data());
       for (int i = 0; i < n; ++i)
@@ -855,15 +864,93 @@ void build_mortar_ops(const Basis& bs, double sigma, double* fwd, double* bwd) {
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) {
         f[i * n + j] = s[j * n + i];
-        bk[i * n + j] = frac[h] * s[i * n + j];
+        bk[i * n + j] = frac * s[i * n + j];
       }
     chol_solve(mass, f, n);
     chol_solve(mass, bk, n);
     for (int i = 0; i < n * n; ++i) {
-      fwd[h * n * n + i] = static_cast<double>(f[i]);
-      bwd[h * n * n + i] = static_cast<double>(bk[i]);
+      fwd[i] = static_cast<double>(f[i]);
+      bwd[i] = static_cast<double>(bk[i]);
     }
   }
+};
+}  // namespace
+
+// The reference's two mortars of a hanging node are the sub-ranges [-1, sigma] and
+// [sigma, 1] (proj/src/mortar.cpp:79-134); the general builder reproduces its bits
+// (-1 + (1 + sigma)/2 (z + 1) and sigma + (1 - sigma)/2 (z + 1) are the same roundings).
+void build_mortar_ops(const Basis& bs, double sigma, double* fwd, double* bwd) {
+  if (!(sigma >= -1.0 && sigma < 1.0)) throw ConfigError("mortar position sigma must lie in [-1, 1)");
+  const SubrangeBuilder sb(bs);
+  const int nn = bs.n * bs.n;
+  sb.build(-1.0, sigma, fwd, bwd);
+  sb.build(sigma, 1.0, fwd + nn, bwd + nn);
+}
+
+void build_subrange_ops(const Basis& bs, double lo, double hi, double* fwd, double* bwd) {
+  if (!(lo >= -1.0 && lo < hi && hi <= 1.0)) throw ConfigError("mortar sub-range must satisfy -1 <= lo < hi <= 1");
+  SubrangeBuilder(bs).build(lo, hi, fwd, bwd);
+}
+
+// Non-matching periodic face rows (BASELINE configs[1]).  Side A has n_a faces of
+// length l_a, side B n_b faces over the same period, displaced by delta.  The
+// displacement splits exactly as the reference's (proj/src/mesh.cpp:9-25) into
+// n_delta + s in A units; B edge j sits at n_delta + k_j + (s + r_j / n_b) with
+// j n_a = k_j n_b + r_j, so equal counts give edges n_delta + j + s with the
+// reference's own s bits, and local coordinates 2s - 1 (= sigma) on A and
+// 1 - 2s (= -sigma, proj/src/solver.cpp:162-163) on B.
+std::vector<MortarInterval> merge_intervals(long n_a, long n_b, double l_a, double delta) {
+  if (n_a < 1 || n_b < 1) throw ConfigError("interval merge needs at least one face per side");
+  if (!(l_a > 0.0)) throw ConfigError("face length must be positive");
+  const Displacement st = displacement(delta, l_a, n_a);
+  const double q = static_cast<double>(n_a) / static_cast<double>(n_b);  // B face length in A units
+  std::vector<long> ei(n_b + 1);
+  std::vector<double> ef(n_b + 1);
+  for (long j = 0; j < n_b; ++j) {
+    const long num = j * n_a;
+    long I = st.n_delta + num / n_b;
+    double f = st.s_delta + static_cast<double>(num % n_b) / static_cast<double>(n_b);
+    if (f >= 1.0) {
+      f -= 1.0;
+      ++I;
+    }
+    ei[j] = I;
+    ef[j] = f;
+  }
+  ei[n_b] = ei[0] + n_a;
+  ef[n_b] = ef[0];
+  std::vector<MortarInterval> out;
+  out.reserve(static_cast<size_t>(n_a + n_b));
+  for (long j = 0; j < n_b; ++j) {
+    // Breakpoints inside B face j: its left edge, the A edges strictly inside, its right edge.
+    const long m_first = ei[j] + 1;
+    const long m_last = ef[j + 1] == 0.0 ? ei[j + 1] - 1 : ei[j + 1];
+    auto b_local = [&](long m) { return 1.0 - 2.0 * ((static_cast<double>(ei[j + 1] - m) + ef[j + 1]) / q); };
+    long p_int = ei[j];
+    double a_lo = ef[j] == 0.0 ? -1.0 : 2.0 * ef[j] - 1.0, b_lo = -1.0;
+    for (long m = m_first; m <= m_last + 1; ++m) {
+      MortarInterval iv;
+      iv.face_a = ((p_int % n_a) + n_a) % n_a;
+      iv.face_b = j;
+      iv.a_lo = a_lo;
+      iv.b_lo = b_lo;
+      if (m <= m_last) {  // piece ends at A edge m
+        iv.a_hi = 1.0;
+        iv.b_hi = b_local(m);
+        a_lo = -1.0;
+        b_lo = iv.b_hi;
+        p_int = m;
+      } else {            // piece ends at B's right edge
+        iv.a_hi = ef[j + 1] == 0.0 ? 1.0 : 2.0 * ef[j + 1] - 1.0;
+        iv.b_hi = 1.0;
+      }
+      out.push_back(iv);
+    }
+  }
+  std::sort(out.begin(), out.end(), [](const MortarInterval& x, const MortarInterval& y) {
+    return x.face_a != y.face_a ? x.face_a < y.face_a : x.a_lo < y.a_lo;
+  });
+  return out;
 }
 
 // ---------------------------------------------------------------- kinematics

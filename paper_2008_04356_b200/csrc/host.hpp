@@ -145,6 +145,8 @@ struct Basis {
 // Face<->mortar L2 projections for hanging node sigma (proj/src/mortar.cpp:79-134),
 // long double assembly.  fwd/bwd [2][n*n] row-major (Lower, Upper).
 void build_mortar_ops(const Basis& b, double sigma, double* fwd, double* bwd);
+// General sub-range [lo, hi] of one face (non-matching interfaces): fwd/bwd n*n.
+void build_subrange_ops(const Basis& b, double lo, double hi, double* fwd, double* bwd);
 
 struct Displacement {
   double delta = 0.0;
@@ -158,6 +160,16 @@ Displacement displacement(double delta, double l_par, long n_faces);  // proj/sr
 // blocks (the device computes A/m itself): counts of mortars per partner.
 long moving_index(long i_par, long n_delta, int i_sub, long n_faces);
 long static_index(long i_moving, long n_delta, int i_sub, long n_faces);
+
+// One mortar of a non-matching periodic face row: the A face and B face it
+// joins and its extent in each face's reference coordinate.
+struct MortarInterval {
+  long face_a = 0, face_b = 0;
+  double a_lo = -1.0, a_hi = 1.0, b_lo = -1.0, b_hi = 1.0;
+};
+// Intersection of A's n_a faces of length l_a with B's n_b faces over the same
+// period, B displaced by delta; sorted by (A face, position).
+std::vector<MortarInterval> merge_intervals(long n_a, long n_b, double l_a, double delta);
 
 }  // namespace sdg
 

@@ -1887,6 +1887,27 @@ int sdg_metrics_host(const sdg_mesh_spec* mesh, int degree, int node_kind, int n
     std::copy(cm.fmet.begin(), cm.fmet.end(), fmet);
   });
 }
+int sdg_subrange_ops(int degree, int node_kind, double lo, double hi, double* fwd, double* bwd) {
+  return guarded(nullptr, [&] {
+    if (node_kind != SDG_NODES_GAUSS && node_kind != SDG_NODES_LGL) throw sdg::ConfigError("unknown node kind");
+    sdg::build_subrange_ops(sdg::Basis(degree, node_kind), lo, hi, fwd, bwd);
+  });
+}
+int sdg_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges) {
+  return guarded(nullptr, [&] {
+    const std::vector<sdg::MortarInterval> iv = sdg::merge_intervals(n_a, n_b, l_a, delta);
+    *n_out = static_cast<long>(iv.size());
+    if (faces == nullptr || ranges == nullptr) return;
+    for (size_t k = 0; k < iv.size(); ++k) {
+      faces[2 * k] = iv[k].face_a;
+      faces[2 * k + 1] = iv[k].face_b;
+      ranges[4 * k] = iv[k].a_lo;
+      ranges[4 * k + 1] = iv[k].a_hi;
+      ranges[4 * k + 2] = iv[k].b_lo;
+      ranges[4 * k + 3] = iv[k].b_hi;
+    }
+  });
+}
 int sdg_diagnostics(sdg_ctx* c, double t, int with_exact, double* out) {
   return guarded(c, [&] { c->s->diagnostics(t, with_exact, out); });
 }
