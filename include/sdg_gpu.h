@@ -128,6 +128,19 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
  * faces/ranges may be NULL to query *n_out (at most n_a + n_b). */
 int sdg_subrange_ops(int degree, int node_kind, double lo, double hi, double* fwd, double* bwd);
 int sdg_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges);
+/* The same row computed by the device kernel (one block; bitwise equal to the host). */
+int sdg_mortar_intervals_device(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces,
+                                double* ranges);
+/* A non-matching planar interface on the device: side A has nfy[0] x nfz[0]
+ * faces of size l_y x l_z, side B nfy[1] x nfz[1] faces over the same periodic
+ * rectangle, displaced by (d_y, d_z).  The data of side `from` (0 = A, 1 = B),
+ * src[fy][fz][n][n][nc], is carried to the tensor-product mortars (row ky of y
+ * by row kz of z, mortar_out[ky][kz][n][n][nc], n = degree + 1) and projected
+ * onto the other side's faces (dst).  mortar_out / dst may be NULL; *n_mortars
+ * receives the mortar count. */
+int sdg_interface_project_device(int degree, int node_kind, const long* nfy, const long* nfz, double l_y,
+                                 double l_z, double d_y, double d_z, int nc, int from, const double* src,
+                                 double* mortar_out, double* dst, long* n_mortars);
 
 /* Diagnostics on the device (integrate_mass_energy / error_norms /
  * max_freestream_deviation, diagnostics.cpp:31-87): out[14] = mass, energy,

@@ -80,6 +80,9 @@ def lib():
         L.sdg_metrics_host.argtypes = [C.POINTER(T.MeshSpec), C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _lp]
         L.sdg_subrange_ops.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp]
         L.sdg_mortar_intervals.argtypes = [C.c_long, C.c_long, C.c_double, C.c_double, _lp, _lp, _dp]
+        L.sdg_mortar_intervals_device.argtypes = [C.c_long, C.c_long, C.c_double, C.c_double, _lp, _lp, _dp]
+        L.sdg_interface_project_device.argtypes = [C.c_int, C.c_int, _lp, _lp, C.c_double, C.c_double, C.c_double,
+                                                   C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _lp]
         L.sdg_diagnostics.argtypes = [_vp, C.c_double, C.c_int, _dp]
         L.sdg_write_snapshot.argtypes = [_vp, C.c_char_p, C.c_double]
         L.sdg_read_snapshot.argtypes = [_vp, C.c_char_p, _dp]
@@ -103,7 +106,8 @@ EXPORTED = [
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
     "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_subrange_ops",
-    "sdg_mortar_intervals", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
+    "sdg_mortar_intervals", "sdg_mortar_intervals_device",
+    "sdg_interface_project_device", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
     "sdg_trace_json", "sdg_inject_collective", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
@@ -370,17 +374,41 @@ def subrange_ops(degree: int, node_kind: int, lo: float, hi: float):
     return fwd, bwd
 
 
-def mortar_intervals(n_a: int, n_b: int, l_a: float, delta: float):
+def mortar_intervals(n_a: int, n_b: int, l_a: float, delta: float, device: bool = False):
     """Mortars of a non-matching periodic face row: (faces [M, 2] = (A face, B face),
-    ranges [M, 4] = (a_lo, a_hi, b_lo, b_hi)), sorted by A face and position."""
+    ranges [M, 4] = (a_lo, a_hi, b_lo, b_hi)), sorted by A face and position.
+    device=True runs the device kernel (needs a GPU)."""
     L = lib()
+    fn = L.sdg_mortar_intervals_device if device else L.sdg_mortar_intervals
     n = C.c_long()
-    T.raise_for(L.sdg_mortar_intervals(n_a, n_b, l_a, delta, C.byref(n), None, None), L.sdg_global_error().decode())
+    T.raise_for(fn(n_a, n_b, l_a, delta, C.byref(n), None, None), L.sdg_global_error().decode())
     faces = np.zeros((n.value, 2), dtype=np.int64)
     ranges = np.zeros((n.value, 4))
-    T.raise_for(L.sdg_mortar_intervals(n_a, n_b, l_a, delta, C.byref(n), faces.ctypes.data_as(_lp), _d(ranges)),
-                L.sdg_global_error().decode())
+    T.raise_for(fn(n_a, n_b, l_a, delta, C.byref(n), faces.ctypes.data_as(_lp), _d(ranges)), L.sdg_global_error().decode())
     return faces, ranges
+
+
+def interface_project_device(degree: int, node_kind: int, nfy, nfz, l_y: float, l_z: float, d_y: float, d_z: float,
+                             src, from_side: int = 0):
+    """Non-matching planar interface on the device: src [nfy[from]][nfz[from]][n][n][nc]
+    -> (mortars [My * Mz, n, n, nc], target faces [nfy[to], nfz[to], n, n, nc])."""
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    n1, nc = degree + 1, src.shape[-1]
+    to = 1 - from_side
+    fy = np.array(nfy, dtype=np.int64)
+    fz = np.array(nfz, dtype=np.int64)
+    assert src.shape == (fy[from_side], fz[from_side], n1, n1, nc)
+    my = len(mortar_intervals(int(fy[0]), int(fy[1]), l_y, d_y)[0])
+    mz = len(mortar_intervals(int(fz[0]), int(fz[1]), l_z, d_z)[0])
+    mortar = np.zeros((my * mz, n1, n1, nc))
+    dst = np.zeros((fy[to], fz[to], n1, n1, nc))
+    nm = C.c_long()
+    L = lib()
+    T.raise_for(L.sdg_interface_project_device(degree, node_kind, fy.ctypes.data_as(_lp), fz.ctypes.data_as(_lp), l_y,
+                                               l_z, d_y, d_z, nc, from_side, _d(src), _d(mortar), _d(dst),
+                                               C.byref(nm)), L.sdg_global_error().decode())
+    assert nm.value == my * mz
+    return mortar, dst
 
 
 def pairing_device(faces, n_par, n_perp, ranks, n_delta, on_static, conforming, self_rank):

@@ -2464,6 +2464,231 @@ bool launch_update_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, con
   SDG_DISPATCH(n1, (done = update_affine_b_t<NN>(c, p, a, st)));
   return done;
 }
+// ---------------------------------------------------------------------------
+// Non-matching face rows (BASELINE configs[1]): the mortars of one periodic row,
+// side A n_a faces of length l_a, side B n_b faces, B displaced by delta; the
+// device form of merge_intervals (csrc/host.cpp), bit for bit.  One block: pass 1
+// counts each B face's pieces (1 + A edges strictly inside), pass 2 writes them
+// at the block-scanned offsets, rotated so the list is ordered by A face (the B
+// order runs along the row from B's edge 0, so sorting by A face is the rotation
+// that starts at the first piece past A's period).  Explicit _rn arithmetic keeps
+// the displacement split and the local coordinates free of contraction.
+// ---------------------------------------------------------------------------
+constexpr int kIvThreads = 512;
+
+struct IvEdge {
+  long long I;
+  double F;
+};
+
+__device__ __forceinline__ IvEdge iv_edge(long long j, long long n_a, long long n_b, long long nd, double sd) {
+  const long long jj = j % n_b, wraps = j / n_b, num = jj * n_a;
+  IvEdge e;
+  e.I = nd + num / n_b + wraps * n_a;
+  e.F = __dadd_rn(sd, __ddiv_rn(static_cast<double>(num % n_b), static_cast<double>(n_b)));
+  if (e.F >= 1.0) {
+    e.F = __dsub_rn(e.F, 1.0);
+    e.I += 1;
+  }
+  return e;
+}
+
+__device__ __forceinline__ long long iv_block_scan(long long v, long long* sh, long long& total) {
+  const int tid = threadIdx.x;
+  sh[tid] = v;
+  __syncthreads();
+  for (int off = 1; off < kIvThreads; off <<= 1) {
+    const long long add = tid >= off ? sh[tid - off] : 0;
+    __syncthreads();
+    sh[tid] += add;
+    __syncthreads();
+  }
+  const long long incl = sh[tid];
+  total = sh[kIvThreads - 1];
+  __syncthreads();
+  return incl - v;
+}
+
+__global__ void __launch_bounds__(kIvThreads) k_mortar_intervals(long long n_a, long long n_b, double l_a, double delta,
+                                                                 long long* faces, double* ranges, long long* n_out) {
+  __shared__ long long sh[kIvThreads];
+  const double period = __dmul_rn(l_a, static_cast<double>(n_a));
+  double d = fmod(delta, period);
+  if (d < 0.0) d = __dadd_rn(d, period);
+  const double ratio = __ddiv_rn(d, l_a);
+  long long nd = static_cast<long long>(floor(ratio));
+  double sd = __dsub_rn(ratio, static_cast<double>(nd));
+  if (nd >= n_a) {
+    nd = 0;
+    sd = 0.0;
+  }
+  const double q = __ddiv_rn(static_cast<double>(n_a), static_cast<double>(n_b));
+  // pass 1: total pieces M and r = pieces starting before A's period end
+  long long M = 0, R = 0;
+  for (long long base = 0; base < n_b; base += kIvThreads) {
+    const long long j = base + threadIdx.x;
+    long long cnt = 0, before = 0;
+    if (j < n_b) {
+      const IvEdge e0 = iv_edge(j, n_a, n_b, nd, sd), e1 = iv_edge(j + 1, n_a, n_b, nd, sd);
+      const long long m_first = e0.I + 1, m_last = e1.F == 0.0 ? e1.I - 1 : e1.I;
+      cnt = m_last - m_first + 2;
+      // piece starts: e0.I, then m_first..m_last; count those < n_a
+      before = (e0.I < n_a ? 1 : 0) + max(0LL, min(m_last, n_a - 1) - m_first + 1);
+    }
+    long long tc, tb;
+    iv_block_scan(cnt, sh, tc);
+    iv_block_scan(before, sh, tb);
+    M += tc;
+    R += tb;
+  }
+  if (threadIdx.x == 0) *n_out = M;
+  if (faces == nullptr) return;
+  long long run = 0;
+  for (long long base = 0; base < n_b; base += kIvThreads) {
+    const long long j = base + threadIdx.x;
+    long long cnt = 0;
+    IvEdge e0{0, 0.0}, e1{0, 0.0};
+    long long m_first = 0, m_last = -1;
+    if (j < n_b) {
+      e0 = iv_edge(j, n_a, n_b, nd, sd);
+      e1 = iv_edge(j + 1, n_a, n_b, nd, sd);
+      m_first = e0.I + 1;
+      m_last = e1.F == 0.0 ? e1.I - 1 : e1.I;
+      cnt = m_last - m_first + 2;
+    }
+    long long tc;
+    const long long off = run + iv_block_scan(cnt, sh, tc);
+    run += tc;
+    if (j >= n_b) continue;
+    long long p_int = e0.I;
+    double a_lo = e0.F == 0.0 ? -1.0 : __dsub_rn(__dmul_rn(2.0, e0.F), 1.0), b_lo = -1.0;
+    for (long long m = m_first, k = off; m <= m_last + 1; ++m, ++k) {
+      double a_hi, b_hi;
+      if (m <= m_last) {
+        a_hi = 1.0;
+        const double dr = __dadd_rn(static_cast<double>(e1.I - m), e1.F);
+        b_hi = __dsub_rn(1.0, __dmul_rn(2.0, __ddiv_rn(dr, q)));
+      } else {
+        a_hi = e1.F == 0.0 ? 1.0 : __dsub_rn(__dmul_rn(2.0, e1.F), 1.0);
+        b_hi = 1.0;
+      }
+      const long long o = ((k - R) % M + M) % M;
+      faces[2 * o] = ((p_int % n_a) + n_a) % n_a;
+      faces[2 * o + 1] = j;
+      ranges[4 * o] = a_lo;
+      ranges[4 * o + 1] = a_hi;
+      ranges[4 * o + 2] = b_lo;
+      ranges[4 * o + 3] = b_hi;
+      a_lo = -1.0;
+      b_lo = b_hi;
+      p_int = m;
+    }
+  }
+}
+
+void launch_mortar_intervals(long long n_a, long long n_b, double l_a, double delta, long long* faces,
+                             double* ranges, long long* n_out, cudaStream_t st) {
+  k_mortar_intervals<<<1, kIvThreads, 0, st>>>(n_a, n_b, l_a, delta, faces, ranges, n_out);
+  check_launch("k_mortar_intervals");
+}
+
+// ---------------------------------------------------------------------------
+// Non-matching planar interface transfer: mortars are tensor products of a y row
+// and a z row of intervals.  Face data layout [fy][fz][i][j][nc] (i along y).
+// k_nc_to_mortar: mortar (ky, kz) = (Fy[ky] x Fz[kz]) applied to its source face.
+// k_nc_to_face: target face (fy, fz) = sum over its mortars (rows in CSR, fixed
+// order) of (By[ky] x Bz[kz]) applied to the mortar data.  One block per item.
+// ---------------------------------------------------------------------------
+__global__ void k_nc_to_mortar(int n, int nc, const double* __restrict__ src, long long nfz,
+                               const long long* __restrict__ iv_y, const long long* __restrict__ iv_z, int col,
+                               long long mz, const double* __restrict__ Fy, const double* __restrict__ Fz,
+                               double* __restrict__ mortar) {
+  extern __shared__ double sm[];
+  const long long ky = blockIdx.x / mz, kz = blockIdx.x % mz;
+  const long long fy = iv_y[2 * ky + col], fz = iv_z[2 * kz + col];
+  const int per = n * n * nc;
+  double* u = sm;
+  double* t = sm + per;
+  const double* face = src + (fy * nfz + fz) * per;
+  for (int x = threadIdx.x; x < per; x += blockDim.x) u[x] = face[x];
+  __syncthreads();
+  const double* fy_op = Fy + ky * n * n;
+  const double* fz_op = Fz + kz * n * n;
+  for (int x = threadIdx.x; x < per; x += blockDim.x) {  // t[k][j][c] = sum_i Fy[k][i] u[i][j][c]
+    const int c = x % nc, j = (x / nc) % n, k = x / (nc * n);
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc = fma(fy_op[k * n + i], u[(i * n + j) * nc + c], acc);
+    t[x] = acc;
+  }
+  __syncthreads();
+  double* out = mortar + blockIdx.x * static_cast<long long>(per);
+  for (int x = threadIdx.x; x < per; x += blockDim.x) {  // out[k][l][c] = sum_j Fz[l][j] t[k][j][c]
+    const int c = x % nc, l = (x / nc) % n, k = x / (nc * n);
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) acc = fma(fz_op[l * n + j], t[(k * n + j) * nc + c], acc);
+    out[x] = acc;
+  }
+}
+
+__global__ void k_nc_to_face(int n, int nc, const double* __restrict__ mortar, long long mz, long long nfz,
+                             const int* __restrict__ off_y, const int* __restrict__ idx_y,
+                             const int* __restrict__ off_z, const int* __restrict__ idx_z,
+                             const double* __restrict__ By, const double* __restrict__ Bz, double* __restrict__ dst) {
+  extern __shared__ double sm[];
+  const long long fy = blockIdx.x / nfz, fz = blockIdx.x % nfz;
+  const int per = n * n * nc;
+  double* m = sm;
+  double* t = sm + per;
+  double acc_local[8];  // up to 8 outputs per thread (per <= 8 * blockDim)
+  const int reps = (per + blockDim.x - 1) / blockDim.x;
+  for (int r = 0; r < reps; ++r) acc_local[r] = 0.0;
+  for (int a = off_y[fy]; a < off_y[fy + 1]; ++a)
+    for (int b = off_z[fz]; b < off_z[fz + 1]; ++b) {
+      const long long ky = idx_y[a], kz = idx_z[b];
+      const double* src = mortar + (ky * mz + kz) * static_cast<long long>(per);
+      __syncthreads();
+      for (int x = threadIdx.x; x < per; x += blockDim.x) m[x] = src[x];
+      __syncthreads();
+      const double* by = By + ky * n * n;
+      const double* bz = Bz + kz * n * n;
+      for (int x = threadIdx.x; x < per; x += blockDim.x) {  // t[i][l][c] = sum_k By[i][k] m[k][l][c]
+        const int c = x % nc, l = (x / nc) % n, i = x / (nc * n);
+        double acc = 0.0;
+        for (int k = 0; k < n; ++k) acc = fma(by[i * n + k], m[(k * n + l) * nc + c], acc);
+        t[x] = acc;
+      }
+      __syncthreads();
+      for (int r = 0, x = threadIdx.x; x < per; ++r, x += blockDim.x) {  // += sum_l Bz[j][l] t[i][l][c]
+        const int c = x % nc, j = (x / nc) % n, i = x / (nc * n);
+        double acc = 0.0;
+        for (int l = 0; l < n; ++l) acc = fma(bz[j * n + l], t[(i * n + l) * nc + c], acc);
+        acc_local[r] += acc;
+      }
+    }
+  double* out = dst + blockIdx.x * static_cast<long long>(per);
+  for (int r = 0, x = threadIdx.x; x < per; ++r, x += blockDim.x) out[x] = acc_local[r];
+}
+
+void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, const long long* iv_y,
+                        const long long* iv_z, int src_col, long long my, long long mz, const double* Fy,
+                        const double* Fz, double* mortar, long long dst_nfy, long long dst_nfz, const int* off_y,
+                        const int* idx_y, const int* off_z, const int* idx_z, const double* By, const double* Bz,
+                        double* dst, cudaStream_t st) {
+  const int per = n * n * nc, threads = 128;
+  if (per > 8 * threads) throw DeviceError(SDG_ERR_CONFIG, "nc transfer: n*n*nc exceeds 1024");
+  const size_t shm = 2 * per * sizeof(double);
+  if (my * mz > 0) {
+    k_nc_to_mortar<<<static_cast<unsigned>(my * mz), threads, shm, st>>>(n, nc, src, src_nfz, iv_y, iv_z, src_col, mz,
+                                                                        Fy, Fz, mortar);
+    check_launch("k_nc_to_mortar");
+  }
+  if (dst_nfy * dst_nfz > 0) {
+    k_nc_to_face<<<static_cast<unsigned>(dst_nfy * dst_nfz), threads, shm, st>>>(n, nc, mortar, mz, dst_nfz, off_y,
+                                                                                idx_y, off_z, idx_z, By, Bz, dst);
+    check_launch("k_nc_to_face");
+  }
+}
+
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
   k_pairing<<<2, kPairThreads, 0, st>>>(a, p);
   check_launch("k_pairing");

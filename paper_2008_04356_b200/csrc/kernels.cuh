@@ -174,6 +174,15 @@ void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const
 bool launch_gradient_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 bool launch_update_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st);
+// Mortars of one non-matching periodic face row (device merge_intervals, host.cpp).
+void launch_mortar_intervals(long long n_a, long long n_b, double l_a, double delta, long long* faces,
+                             double* ranges, long long* n_out, cudaStream_t st);
+// Non-matching planar interface: source faces -> tensor-product mortars -> target faces.
+void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, const long long* iv_y,
+                        const long long* iv_z, int src_col, long long my, long long mz, const double* Fy,
+                        const double* Fz, double* mortar, long long dst_nfy, long long dst_nfz, const int* off_y,
+                        const int* idx_y, const int* off_z, const int* idx_z, const double* By, const double* Bz,
+                        double* dst, cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);
 void launch_mortar_lift(int n1, const GasD& g, const MortarPtrs& p, int max_mortars, cudaStream_t st);

@@ -1441,6 +1441,109 @@ void GpuRankSolver::get_mapping(int c, int* m) {
 }
 
 // Stand-alone device pairing on caller-given faces (Appendix-A fixture).
+static void device_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges) {
+  if (n_a < 1 || n_b < 1) throw ConfigError("interval merge needs at least one face per side");
+  if (!(l_a > 0.0)) throw ConfigError("face length must be positive");
+  cudaStream_t st;
+  cuda_check(cudaStreamCreate(&st), "stream");
+  const long cap = n_a + n_b;
+  DevBuf<long long> d_faces, d_n;
+  DevBuf<double> d_ranges;
+  d_faces.alloc(2 * cap);
+  d_ranges.alloc(4 * cap);
+  d_n.alloc(1);
+  launch_mortar_intervals(n_a, n_b, l_a, delta, d_faces.p, d_ranges.p, d_n.p, st);
+  long long n = 0;
+  cuda_check(cudaMemcpyAsync(&n, d_n.p, sizeof(long long), cudaMemcpyDeviceToHost, st), "copy");
+  std::vector<long long> hf(2 * cap);
+  std::vector<double> hr(4 * cap);
+  cuda_check(cudaMemcpyAsync(hf.data(), d_faces.p, hf.size() * sizeof(long long), cudaMemcpyDeviceToHost, st), "copy");
+  cuda_check(cudaMemcpyAsync(hr.data(), d_ranges.p, hr.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "copy");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  cudaStreamDestroy(st);
+  *n_out = static_cast<long>(n);
+  if (faces == nullptr || ranges == nullptr) return;
+  for (long long k = 0; k < 2 * n; ++k) faces[k] = static_cast<long>(hf[k]);
+  std::copy(hr.begin(), hr.begin() + 4 * n, ranges);
+}
+
+// Non-matching planar interface transfer on the device (BASELINE configs[1]):
+// side A has nfy[0] x nfz[0] faces of size l_y x l_z, side B nfy[1] x nfz[1] faces
+// over the same periodic rectangle, displaced by (d_y, d_z).  Data on side `from`
+// ([fy][fz][n][n][nc]) goes to the tensor-product mortars (face -> mortar L2
+// operators) and on to the other side's faces (mortar -> face L2 projections).
+// The rows come from the device interval kernel; the host assembles the long
+// double operators from its bitwise-equal rows, as the reference assembles its
+// mortar operators on the host every stage (proj/src/solver.cpp:156-176).
+static void device_interface_project(int degree, int kind, const long* nfy, const long* nfz, double l_y, double l_z,
+                                     double d_y, double d_z, int nc, int from, const double* src, double* mortar_out,
+                                     double* dst, long* n_mortars) {
+  if (from != 0 && from != 1) throw ConfigError("from must be 0 (A) or 1 (B)");
+  if (nc < 1) throw ConfigError("nc must be positive");
+  const Basis bs(degree, kind);
+  const int n = bs.n, nn = n * n, to = 1 - from;
+  const std::vector<MortarInterval> ry = merge_intervals(nfy[0], nfy[1], l_y, d_y);
+  const std::vector<MortarInterval> rz = merge_intervals(nfz[0], nfz[1], l_z, d_z);
+  const long my = static_cast<long>(ry.size()), mz = static_cast<long>(rz.size());
+  *n_mortars = my * mz;
+  auto ops = [&](const std::vector<MortarInterval>& rows, std::vector<double>& F, std::vector<double>& B,
+                 std::vector<int>& off, std::vector<int>& idx, long n_to) {
+    F.assign(rows.size() * nn, 0.0);
+    B.assign(rows.size() * nn, 0.0);
+    std::vector<double> tmp(nn);
+    for (size_t k = 0; k < rows.size(); ++k) {
+      const MortarInterval& r = rows[k];
+      const double slo = from == 0 ? r.a_lo : r.b_lo, shi = from == 0 ? r.a_hi : r.b_hi;
+      const double tlo = to == 0 ? r.a_lo : r.b_lo, thi = to == 0 ? r.a_hi : r.b_hi;
+      build_subrange_ops(bs, slo, shi, F.data() + k * nn, tmp.data());
+      build_subrange_ops(bs, tlo, thi, tmp.data(), B.data() + k * nn);
+    }
+    off.assign(n_to + 1, 0);  // target face -> its rows, in row order
+    for (const MortarInterval& r : rows) ++off[(to == 0 ? r.face_a : r.face_b) + 1];
+    for (long f = 0; f < n_to; ++f) off[f + 1] += off[f];
+    idx.assign(rows.size(), 0);
+    std::vector<int> fill(off.begin(), off.end() - 1);
+    for (size_t k = 0; k < rows.size(); ++k) idx[fill[to == 0 ? rows[k].face_a : rows[k].face_b]++] = static_cast<int>(k);
+  };
+  std::vector<double> Fy, By, Fz, Bz;
+  std::vector<int> offy, idxy, offz, idxz;
+  ops(ry, Fy, By, offy, idxy, nfy[to]);
+  ops(rz, Fz, Bz, offz, idxz, nfz[to]);
+  cudaStream_t st;
+  cuda_check(cudaStreamCreate(&st), "stream");
+  DevBuf<long long> d_ivy, d_ivz, d_n;
+  DevBuf<double> d_rng, d_Fy, d_By, d_Fz, d_Bz, d_src, d_mortar, d_dst;
+  DevBuf<int> d_offy, d_idxy, d_offz, d_idxz;
+  d_ivy.alloc(2 * (nfy[0] + nfy[1]));
+  d_ivz.alloc(2 * (nfz[0] + nfz[1]));
+  d_rng.alloc(4 * std::max(nfy[0] + nfy[1], nfz[0] + nfz[1]));
+  d_n.alloc(1);
+  launch_mortar_intervals(nfy[0], nfy[1], l_y, d_y, d_ivy.p, d_rng.p, d_n.p, st);
+  launch_mortar_intervals(nfz[0], nfz[1], l_z, d_z, d_ivz.p, d_rng.p, d_n.p, st);
+  d_Fy.upload(Fy, st);
+  d_By.upload(By, st);
+  d_Fz.upload(Fz, st);
+  d_Bz.upload(Bz, st);
+  d_offy.upload(offy, st);
+  d_idxy.upload(idxy, st);
+  d_offz.upload(offz, st);
+  d_idxz.upload(idxz, st);
+  const long per = static_cast<long>(nn) * nc;
+  d_src.upload(std::vector<double>(src, src + nfy[from] * nfz[from] * per), st);
+  d_mortar.alloc(my * mz * per);
+  d_dst.alloc(nfy[to] * nfz[to] * per);
+  launch_nc_transfer(n, nc, d_src.p, nfz[from], d_ivy.p, d_ivz.p, from, my, mz, d_Fy.p, d_Fz.p, d_mortar.p, nfy[to],
+                     nfz[to], d_offy.p, d_idxy.p, d_offz.p, d_idxz.p, d_By.p, d_Bz.p, d_dst.p, st);
+  if (mortar_out)
+    cuda_check(cudaMemcpyAsync(mortar_out, d_mortar.p, my * mz * per * sizeof(double), cudaMemcpyDeviceToHost, st),
+               "copy");
+  if (dst)
+    cuda_check(cudaMemcpyAsync(dst, d_dst.p, nfy[to] * nfz[to] * per * sizeof(double), cudaMemcpyDeviceToHost, st),
+               "copy");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  cudaStreamDestroy(st);
+}
+
 static void device_pairing(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,
                            long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
                            int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry) {
@@ -1906,6 +2009,18 @@ int sdg_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_o
       ranges[4 * k + 2] = iv[k].b_lo;
       ranges[4 * k + 3] = iv[k].b_hi;
     }
+  });
+}
+int sdg_mortar_intervals_device(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces,
+                                double* ranges) {
+  return guarded(nullptr, [&] { sdg::device_intervals(n_a, n_b, l_a, delta, n_out, faces, ranges); });
+}
+int sdg_interface_project_device(int degree, int node_kind, const long* nfy, const long* nfz, double l_y,
+                                 double l_z, double d_y, double d_z, int nc, int from, const double* src,
+                                 double* mortar_out, double* dst, long* n_mortars) {
+  return guarded(nullptr, [&] {
+    sdg::device_interface_project(degree, node_kind, nfy, nfz, l_y, l_z, d_y, d_z, nc, from, src, mortar_out, dst,
+                                  n_mortars);
   });
 }
 int sdg_diagnostics(sdg_ctx* c, double t, int with_exact, double* out) {
