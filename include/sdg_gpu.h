@@ -123,7 +123,7 @@ int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, 
  * sdg_mortar_intervals: the mortars of one periodic face row where side A has
  * n_a faces of length l_a and side B n_b faces over the same period, displaced
  * by delta: per mortar (A face, B face) in faces[2k..] and (a_lo, a_hi, b_lo,
- * b_hi) in ranges[4k..], sorted by A face and position.  With n_a == n_b this
+ * b_hi) in ranges[4k..], in A order (by A face, then along it).  With n_a == n_b this
  * is the reference's pairing (moving_index, sigma / -sigma, mortar.cpp:136-150).
  * faces/ranges may be NULL to query *n_out (at most n_a + n_b). */
 int sdg_subrange_ops(int degree, int node_kind, double lo, double hi, double* fwd, double* bwd);

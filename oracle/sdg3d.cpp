@@ -353,8 +353,8 @@ static long static_index(long i_moving, long n_delta, int i_sub, long n_faces) {
 // A edge 1 - 2 (distance to B's right edge) / q (-sigma at equal counts).
 // Restated pairwise: every (A face, B face) overlap, instead of the product's sweep.
 struct Interval {
-  long fa, fb;
-  double r[4];
+  long fa, fb, cp, lo_i;
+  double lo_f, r[4];
 };
 static std::vector<Interval> intervals(long n_a, long n_b, double l_a, double delta) {
   if (n_a < 1 || n_b < 1 || !(l_a > 0.0)) throw ConfigError("bad face rows");
@@ -390,6 +390,9 @@ static std::vector<Interval> intervals(long n_a, long n_b, double l_a, double de
         Interval iv;
         iv.fa = i;
         iv.fb = j;
+        iv.cp = cp;
+        iv.lo_i = lo_i;
+        iv.lo_f = lo_f;
         iv.r[0] = lo_is_b ? (F0 == 0.0 ? -1.0 : 2.0 * F0 - 1.0) : -1.0;
         iv.r[1] = hi_is_b ? (F1 == 0.0 ? 1.0 : 2.0 * F1 - 1.0) : 1.0;
         iv.r[2] = lo_is_b ? -1.0 : 1.0 - 2.0 * ((static_cast<double>(I1 - ai) + F1) / q);
@@ -397,8 +400,12 @@ static std::vector<Interval> intervals(long n_a, long n_b, double l_a, double de
         out.push_back(iv);
       }
     }
+  // A order: by A face, then along it -- the copy one period on (the part of the face
+  // before B's edge 0) first, then by the exact start (integer, fraction).
   std::sort(out.begin(), out.end(), [](const Interval& x, const Interval& y) {
-    return x.fa != y.fa ? x.fa < y.fa : x.r[0] < y.r[0];
+    if (x.fa != y.fa) return x.fa < y.fa;
+    if (x.cp != y.cp) return x.cp > y.cp;
+    return x.lo_i != y.lo_i ? x.lo_i < y.lo_i : x.lo_f < y.lo_f;
   });
   return out;
 }

@@ -376,7 +376,7 @@ def subrange_ops(degree: int, node_kind: int, lo: float, hi: float):
 
 def mortar_intervals(n_a: int, n_b: int, l_a: float, delta: float, device: bool = False):
     """Mortars of a non-matching periodic face row: (faces [M, 2] = (A face, B face),
-    ranges [M, 4] = (a_lo, a_hi, b_lo, b_hi)), sorted by A face and position.
+    ranges [M, 4] = (a_lo, a_hi, b_lo, b_hi)), in A order (by A face, then along it).
     device=True runs the device kernel (needs a GPU)."""
     L = lib()
     fn = L.sdg_mortar_intervals_device if device else L.sdg_mortar_intervals

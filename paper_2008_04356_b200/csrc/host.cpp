@@ -921,6 +921,7 @@ std::vector<MortarInterval> merge_intervals(long n_a, long n_b, double l_a, doub
   ef[n_b] = ef[0];
   std::vector<MortarInterval> out;
   out.reserve(static_cast<size_t>(n_a + n_b));
+  long n_before = 0;  // pieces starting before A's period end
   for (long j = 0; j < n_b; ++j) {
     // Breakpoints inside B face j: its left edge, the A edges strictly inside, its right edge.
     const long m_first = ei[j] + 1;
@@ -929,6 +930,7 @@ std::vector<MortarInterval> merge_intervals(long n_a, long n_b, double l_a, doub
     long p_int = ei[j];
     double a_lo = ef[j] == 0.0 ? -1.0 : 2.0 * ef[j] - 1.0, b_lo = -1.0;
     for (long m = m_first; m <= m_last + 1; ++m) {
+      if (p_int < n_a) ++n_before;
       MortarInterval iv;
       iv.face_a = ((p_int % n_a) + n_a) % n_a;
       iv.face_b = j;
@@ -947,9 +949,10 @@ std::vector<MortarInterval> merge_intervals(long n_a, long n_b, double l_a, doub
       out.push_back(iv);
     }
   }
-  std::sort(out.begin(), out.end(), [](const MortarInterval& x, const MortarInterval& y) {
-    return x.face_a != y.face_a ? x.face_a < y.face_a : x.a_lo < y.a_lo;
-  });
+  // The walk runs along the row from B's edge 0 (inside A face n_delta); A order starts
+  // with the pieces past A's period end (faces 0 .. n_delta), so it is a rotation.
+  // (Not a sort by a_lo: a sub-ulp s makes 2s - 1 round to -1 and would tie.)
+  std::rotate(out.begin(), out.begin() + n_before, out.end());
   return out;
 }
 

@@ -168,7 +168,7 @@ struct MortarInterval {
   double a_lo = -1.0, a_hi = 1.0, b_lo = -1.0, b_hi = 1.0;
 };
 // Intersection of A's n_a faces of length l_a with B's n_b faces over the same
-// period, B displaced by delta; sorted by (A face, position).
+// period, B displaced by delta; in A order (by A face, then along the face).
 std::vector<MortarInterval> merge_intervals(long n_a, long n_b, double l_a, double delta);
 
 }  // namespace sdg
