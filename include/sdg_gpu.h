@@ -142,6 +142,20 @@ int sdg_interface_project_device(int degree, int node_kind, const long* nfy, con
                                  double l_z, double d_y, double d_z, int nc, int from, const double* src,
                                  double* mortar_out, double* dst, long* n_mortars);
 
+/* The surface flux of a non-matching planar interface with normal +x, side A
+ * (nfy[0] x nfz[0] faces) below and side B (nfy[1] x nfz[1]) above, displaced by
+ * (d_y, d_z): both sides' traces u_a / u_b ([fy][fz][n][n][5]) and, when the gas
+ * is viscous and both are non-NULL, gradients g_a / g_b ([..][12], d(u,v,w)/dx_j
+ * then dT/dx_j) go to the tensor-product mortars; the two-sided Roe + central
+ * viscous flux (face_numerical_flux, solver.cpp:308-321) is evaluated at the
+ * mortar nodes (flux_mortar[M][n][n][5], may be NULL) and L2-projected back onto
+ * both sides' faces (flux_a, flux_b; the flux along +x on both).  With equal
+ * counts this is the reference's mortar chain (solver.cpp:156-176). */
+int sdg_interface_flux_device(const sdg_gas* gas, int degree, int node_kind, const long* nfy, const long* nfz,
+                              double l_y, double l_z, double d_y, double d_z, const double* u_a, const double* u_b,
+                              const double* g_a, const double* g_b, double* flux_mortar, double* flux_a,
+                              double* flux_b, long* n_mortars);
+
 /* Diagnostics on the device (integrate_mass_energy / error_norms /
  * max_freestream_deviation, diagnostics.cpp:31-87): out[14] = mass, energy,
  * volume, L2 error[5], Linf error[5], max deviation; the errors are against the

@@ -2689,6 +2689,42 @@ void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, con
   }
 }
 
+// Two-sided numerical flux at the nodes of the tensor-product mortars of a
+// non-matching planar interface with normal e_dir, side A on the minus side:
+// face_numerical_flux (solver.cpp:308-321) on both sides' mortar traces, the
+// viscous normal fluxes from the mortar gradients when given (ga/gb non-null).
+// One thread per mortar node; *bad counts nodes with a non-positive Roe c^2.
+__global__ void k_nc_mortar_flux(long long nodes, GasD g, int dir, double vg, const double* __restrict__ ua,
+                                 const double* __restrict__ ub, const double* __restrict__ ga,
+                                 const double* __restrict__ gb, double* __restrict__ flux, int* bad) {
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= nodes) return;
+  double um[5], up[5], f[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    um[v] = ua[q * 5 + v];
+    up[v] = ub[q * 5 + v];
+  }
+  double fvm[4], fvp[4];
+  const bool vis = ga != nullptr && g.viscous;
+  if (vis) {
+    fv_dir(um, ga + q * 12, dir, g, fvm);
+    fv_dir(up, gb + q * 12, dir, g, fvp);
+  }
+  if (!face_flux_fv(um, up, dir, vg, vis ? fvm : nullptr, fvp, g, f)) atomicAdd(bad, 1);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) flux[q * 5 + v] = f[v];
+}
+
+void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, const double* ua, const double* ub,
+                           const double* ga, const double* gb, double* flux, int* bad, cudaStream_t st) {
+  if (nodes <= 0) return;
+  const int threads = 128;
+  k_nc_mortar_flux<<<static_cast<unsigned>((nodes + threads - 1) / threads), threads, 0, st>>>(nodes, g, dir, vg, ua,
+                                                                                              ub, ga, gb, flux, bad);
+  check_launch("k_nc_mortar_flux");
+}
+
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {
   k_pairing<<<2, kPairThreads, 0, st>>>(a, p);
   check_launch("k_pairing");

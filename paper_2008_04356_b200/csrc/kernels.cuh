@@ -183,6 +183,9 @@ void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, con
                         const double* Fz, double* mortar, long long dst_nfy, long long dst_nfz, const int* off_y,
                         const int* idx_y, const int* off_z, const int* idx_z, const double* By, const double* Bz,
                         double* dst, cudaStream_t st);
+// Two-sided Riemann (+ viscous) flux at the mortar nodes of a non-matching interface.
+void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, const double* ua, const double* ub,
+                           const double* ga, const double* gb, double* flux, int* bad, cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);
 void launch_mortar_lift(int n1, const GasD& g, const MortarPtrs& p, int max_mortars, cudaStream_t st);

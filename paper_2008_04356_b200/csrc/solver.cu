@@ -1544,6 +1544,116 @@ static void device_interface_project(int degree, int kind, const long* nfy, cons
   cudaStreamDestroy(st);
 }
 
+// The operators of one side s of a mortar row: face -> mortar (F) and mortar ->
+// face (B) for each row's sub-range on s, and the CSR list face -> rows (row order).
+struct NcSideOps {
+  std::vector<double> F, B;
+  std::vector<int> off, idx;
+};
+static NcSideOps nc_side_ops(const Basis& bs, const std::vector<MortarInterval>& rows, int s, long n_faces) {
+  const int nn = bs.n * bs.n;
+  NcSideOps o;
+  o.F.assign(rows.size() * nn, 0.0);
+  o.B.assign(rows.size() * nn, 0.0);
+  o.off.assign(n_faces + 1, 0);
+  for (size_t k = 0; k < rows.size(); ++k) {
+    const MortarInterval& r = rows[k];
+    build_subrange_ops(bs, s == 0 ? r.a_lo : r.b_lo, s == 0 ? r.a_hi : r.b_hi, o.F.data() + k * nn,
+                       o.B.data() + k * nn);
+    ++o.off[(s == 0 ? r.face_a : r.face_b) + 1];
+  }
+  for (long f = 0; f < n_faces; ++f) o.off[f + 1] += o.off[f];
+  o.idx.assign(rows.size(), 0);
+  std::vector<int> fill(o.off.begin(), o.off.end() - 1);
+  for (size_t k = 0; k < rows.size(); ++k) o.idx[fill[s == 0 ? rows[k].face_a : rows[k].face_b]++] = static_cast<int>(k);
+  return o;
+}
+
+// The surface flux of a non-matching planar interface with normal +x (side A
+// below, side B above), on the device: both sides' traces (and gradients, for
+// the viscous part) go to the tensor-product mortars, the two-sided numerical
+// flux is evaluated at the mortar nodes and L2-projected back onto the faces of
+// both sides.  This is the reference's mortar chain (solver.cpp:156-176 fill,
+// 308-321 flux, mortar.cpp:79-134 projections) on non-aligned face rows.
+static void device_interface_flux(const sdg_gas& gas, int degree, int kind, const long* nfy, const long* nfz,
+                                  double l_y, double l_z, double d_y, double d_z, const double* u_a,
+                                  const double* u_b, const double* g_a, const double* g_b, double* flux_mortar,
+                                  double* flux_a, double* flux_b, long* n_mortars) {
+  if ((g_a == nullptr) != (g_b == nullptr)) throw ConfigError("gradients must be given for both sides or neither");
+  const Basis bs(degree, kind);
+  const int n = bs.n, nn = n * n;
+  const std::vector<MortarInterval> ry = merge_intervals(nfy[0], nfy[1], l_y, d_y);
+  const std::vector<MortarInterval> rz = merge_intervals(nfz[0], nfz[1], l_z, d_z);
+  const long my = static_cast<long>(ry.size()), mz = static_cast<long>(rz.size());
+  *n_mortars = my * mz;
+  NcSideOps oy[2] = {nc_side_ops(bs, ry, 0, nfy[0]), nc_side_ops(bs, ry, 1, nfy[1])};
+  NcSideOps oz[2] = {nc_side_ops(bs, rz, 0, nfz[0]), nc_side_ops(bs, rz, 1, nfz[1])};
+  cudaStream_t st;
+  cuda_check(cudaStreamCreate(&st), "stream");
+  DevBuf<long long> d_ivy, d_ivz, d_n;
+  DevBuf<double> d_rng;
+  d_ivy.alloc(2 * (nfy[0] + nfy[1]));
+  d_ivz.alloc(2 * (nfz[0] + nfz[1]));
+  d_rng.alloc(4 * std::max(nfy[0] + nfy[1], nfz[0] + nfz[1]));
+  d_n.alloc(1);
+  launch_mortar_intervals(nfy[0], nfy[1], l_y, d_y, d_ivy.p, d_rng.p, d_n.p, st);
+  launch_mortar_intervals(nfz[0], nfz[1], l_z, d_z, d_ivz.p, d_rng.p, d_n.p, st);
+  DevBuf<double> d_F[2][2], d_B[2][2];  // [side][y/z]
+  DevBuf<int> d_off[2][2], d_idx[2][2];
+  for (int s = 0; s < 2; ++s) {
+    d_F[s][0].upload(oy[s].F, st);
+    d_B[s][0].upload(oy[s].B, st);
+    d_off[s][0].upload(oy[s].off, st);
+    d_idx[s][0].upload(oy[s].idx, st);
+    d_F[s][1].upload(oz[s].F, st);
+    d_B[s][1].upload(oz[s].B, st);
+    d_off[s][1].upload(oz[s].off, st);
+    d_idx[s][1].upload(oz[s].idx, st);
+  }
+  const long nm = my * mz;
+  const bool vis = g_a != nullptr;
+  DevBuf<double> d_u[2], d_g[2], d_mu[2], d_mg[2], d_flux, d_face[2];
+  const double* u_in[2] = {u_a, u_b};
+  const double* g_in[2] = {g_a, g_b};
+  for (int s = 0; s < 2; ++s) {
+    const long nf = nfy[s] * nfz[s];
+    d_u[s].upload(std::vector<double>(u_in[s], u_in[s] + nf * nn * 5), st);
+    d_mu[s].alloc(nm * nn * 5);
+    launch_nc_transfer(n, 5, d_u[s].p, nfz[s], d_ivy.p, d_ivz.p, s, my, mz, d_F[s][0].p, d_F[s][1].p, d_mu[s].p, 0,
+                       0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+    if (vis) {
+      d_g[s].upload(std::vector<double>(g_in[s], g_in[s] + nf * nn * 12), st);
+      d_mg[s].alloc(nm * nn * 12);
+      launch_nc_transfer(n, 12, d_g[s].p, nfz[s], d_ivy.p, d_ivz.p, s, my, mz, d_F[s][0].p, d_F[s][1].p, d_mg[s].p,
+                         0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+    }
+  }
+  const GasD g{gas.gamma, gas.gamma - 1.0, gas.R, 1.0 / gas.R, gas.mu, -2.0 / 3.0 * gas.mu,
+               gas.gamma * gas.R * gas.mu / ((gas.gamma - 1.0) * gas.Pr), gas.mu > 0.0 ? 1 : 0};
+  DevBuf<int> d_bad;
+  d_bad.upload(std::vector<int>{0}, st);
+  d_flux.alloc(nm * nn * 5);
+  launch_nc_mortar_flux(nm * nn, g, 0, 0.0, d_mu[0].p, d_mu[1].p, vis ? d_mg[0].p : nullptr,
+                        vis ? d_mg[1].p : nullptr, d_flux.p, d_bad.p, st);
+  double* out[2] = {flux_a, flux_b};
+  for (int s = 0; s < 2; ++s) {
+    d_face[s].alloc(nfy[s] * nfz[s] * nn * 5);
+    launch_nc_transfer(n, 5, d_flux.p, mz, nullptr, nullptr, 0, 0, mz, nullptr, nullptr, d_flux.p, nfy[s], nfz[s],
+                       d_off[s][0].p, d_idx[s][0].p, d_off[s][1].p, d_idx[s][1].p, d_B[s][0].p, d_B[s][1].p,
+                       d_face[s].p, st);
+    if (out[s])
+      cuda_check(cudaMemcpyAsync(out[s], d_face[s].p, d_face[s].n * sizeof(double), cudaMemcpyDeviceToHost, st),
+                 "copy");
+  }
+  if (flux_mortar)
+    cuda_check(cudaMemcpyAsync(flux_mortar, d_flux.p, d_flux.n * sizeof(double), cudaMemcpyDeviceToHost, st), "copy");
+  int bad = 0;
+  cuda_check(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  cudaStreamDestroy(st);
+  if (bad) throw InvalidStateError("interface flux: non-positive Roe-averaged c^2 at " + std::to_string(bad) + " mortar nodes");
+}
+
 static void device_pairing(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,
                            long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
                            int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry) {
@@ -2021,6 +2131,16 @@ int sdg_interface_project_device(int degree, int node_kind, const long* nfy, con
   return guarded(nullptr, [&] {
     sdg::device_interface_project(degree, node_kind, nfy, nfz, l_y, l_z, d_y, d_z, nc, from, src, mortar_out, dst,
                                   n_mortars);
+  });
+}
+int sdg_interface_flux_device(const sdg_gas* gas, int degree, int node_kind, const long* nfy, const long* nfz,
+                              double l_y, double l_z, double d_y, double d_z, const double* u_a, const double* u_b,
+                              const double* g_a, const double* g_b, double* flux_mortar, double* flux_a,
+                              double* flux_b, long* n_mortars) {
+  return guarded(nullptr, [&] {
+    if (gas == nullptr) throw sdg::ConfigError("gas is NULL");
+    sdg::device_interface_flux(*gas, degree, node_kind, nfy, nfz, l_y, l_z, d_y, d_z, u_a, u_b, g_a, g_b,
+                               flux_mortar, flux_a, flux_b, n_mortars);
   });
 }
 int sdg_diagnostics(sdg_ctx* c, double t, int with_exact, double* out) {
