@@ -156,6 +156,13 @@ int sdg_interface_flux_device(const sdg_gas* gas, int degree, int node_kind, con
                               const double* g_a, const double* g_b, double* flux_mortar, double* flux_a,
                               double* flux_b, long* n_mortars);
 
+/* The same interface's lifting mean: the mean of both sides' primitive
+ * (u, v, w, T) at the mortar nodes (lift_mortar[M][n][n][4], may be NULL; run_lifting,
+ * solver.cpp:597-727), L2-projected back onto both sides' faces (lift_a, lift_b). */
+int sdg_interface_lift_device(const sdg_gas* gas, int degree, int node_kind, const long* nfy, const long* nfz,
+                              double l_y, double l_z, double d_y, double d_z, const double* u_a, const double* u_b,
+                              double* lift_mortar, double* lift_a, double* lift_b, long* n_mortars);
+
 /* Diagnostics on the device (integrate_mass_energy / error_norms /
  * max_freestream_deviation, diagnostics.cpp:31-87): out[14] = mass, energy,
  * volume, L2 error[5], Linf error[5], max deviation; the errors are against the

@@ -85,6 +85,8 @@ def lib():
                                                    C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _lp]
         L.sdg_interface_flux_device.argtypes = [C.POINTER(T.Gas), C.c_int, C.c_int, _lp, _lp, C.c_double, C.c_double,
                                                 C.c_double, C.c_double, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _lp]
+        L.sdg_interface_lift_device.argtypes = [C.POINTER(T.Gas), C.c_int, C.c_int, _lp, _lp, C.c_double, C.c_double,
+                                                C.c_double, C.c_double, _dp, _dp, _dp, _dp, _dp, _lp]
         L.sdg_diagnostics.argtypes = [_vp, C.c_double, C.c_int, _dp]
         L.sdg_write_snapshot.argtypes = [_vp, C.c_char_p, C.c_double]
         L.sdg_read_snapshot.argtypes = [_vp, C.c_char_p, _dp]
@@ -109,7 +111,8 @@ EXPORTED = [
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
     "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_subrange_ops",
     "sdg_mortar_intervals", "sdg_mortar_intervals_device",
-    "sdg_interface_project_device", "sdg_interface_flux_device", "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
+    "sdg_interface_project_device", "sdg_interface_flux_device", "sdg_interface_lift_device",
+    "sdg_diagnostics", "sdg_write_snapshot", "sdg_read_snapshot",
     "sdg_trace_json", "sdg_inject_collective", "sdg_stream", "sdg_kernel_launches", "sdg_enable_kernel_timing", "sdg_kernel_timing",
 ]
 
@@ -440,6 +443,31 @@ def interface_flux_device(gas, degree: int, node_kind: int, nfy, nfz, l_y: float
                 L.sdg_global_error().decode())
     assert nm.value == my * mz
     return fm, fa, fb
+
+
+def interface_lift_device(gas, degree: int, node_kind: int, nfy, nfz, l_y: float, l_z: float, d_y: float,
+                          d_z: float, u_a, u_b):
+    """Lifting mean of a non-matching planar interface on the device: -> (mortar
+    means [My * Mz, n, n, 4] of (u, v, w, T), their projections onto A's and B's faces)."""
+    n1 = degree + 1
+    fy = np.array(nfy, dtype=np.int64)
+    fz = np.array(nfz, dtype=np.int64)
+    u = [np.ascontiguousarray(x, dtype=np.float64) for x in (u_a, u_b)]
+    for s in (0, 1):
+        assert u[s].shape == (fy[s], fz[s], n1, n1, 5)
+    my = len(mortar_intervals(int(fy[0]), int(fy[1]), l_y, d_y)[0])
+    mz = len(mortar_intervals(int(fz[0]), int(fz[1]), l_z, d_z)[0])
+    lm = np.zeros((my * mz, n1, n1, 4))
+    la = np.zeros((fy[0], fz[0], n1, n1, 4))
+    lb = np.zeros((fy[1], fz[1], n1, n1, 4))
+    nm = C.c_long()
+    L = lib()
+    T.raise_for(L.sdg_interface_lift_device(C.byref(gas), degree, node_kind, fy.ctypes.data_as(_lp),
+                                            fz.ctypes.data_as(_lp), l_y, l_z, d_y, d_z, _d(u[0]), _d(u[1]), _d(lm),
+                                            _d(la), _d(lb), C.byref(nm)),
+                L.sdg_global_error().decode())
+    assert nm.value == my * mz
+    return lm, la, lb
 
 
 def pairing_device(faces, n_par, n_perp, ranks, n_delta, on_static, conforming, self_rank):

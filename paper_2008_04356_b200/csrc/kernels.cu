@@ -2716,6 +2716,27 @@ __global__ void k_nc_mortar_flux(long long nodes, GasD g, int dir, double vg, co
   for (int v = 0; v < 5; ++v) flux[q * 5 + v] = f[v];
 }
 
+// The lifting mean at the mortar nodes of a non-matching interface: the mean of
+// both sides' primitive (u, v, w, T) (run_lifting, solver.cpp:597-727).
+__global__ void k_nc_mortar_lift(long long nodes, GasD g, const double* __restrict__ ua, const double* __restrict__ ub,
+                                 double* __restrict__ lift) {
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= nodes) return;
+  double a[4], b[4];
+  prim4(ua + q * 5, g, a);
+  prim4(ub + q * 5, g, b);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) lift[q * 4 + c] = __dmul_rn(0.5, __dadd_rn(a[c], b[c]));
+}
+
+void launch_nc_mortar_lift(long long nodes, const GasD& g, const double* ua, const double* ub, double* lift,
+                           cudaStream_t st) {
+  if (nodes <= 0) return;
+  const int threads = 128;
+  k_nc_mortar_lift<<<static_cast<unsigned>((nodes + threads - 1) / threads), threads, 0, st>>>(nodes, g, ua, ub, lift);
+  check_launch("k_nc_mortar_lift");
+}
+
 void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, const double* ua, const double* ub,
                            const double* ga, const double* gb, double* flux, int* bad, cudaStream_t st) {
   if (nodes <= 0) return;

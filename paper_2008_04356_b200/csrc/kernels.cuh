@@ -186,6 +186,8 @@ void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, con
 // Two-sided Riemann (+ viscous) flux at the mortar nodes of a non-matching interface.
 void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, const double* ua, const double* ub,
                            const double* ga, const double* gb, double* flux, int* bad, cudaStream_t st);
+void launch_nc_mortar_lift(long long nodes, const GasD& g, const double* ua, const double* ub, double* lift,
+                           cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);
 void launch_mortar_lift(int n1, const GasD& g, const MortarPtrs& p, int max_mortars, cudaStream_t st);

@@ -1575,10 +1575,11 @@ static NcSideOps nc_side_ops(const Basis& bs, const std::vector<MortarInterval>&
 // flux is evaluated at the mortar nodes and L2-projected back onto the faces of
 // both sides.  This is the reference's mortar chain (solver.cpp:156-176 fill,
 // 308-321 flux, mortar.cpp:79-134 projections) on non-aligned face rows.
+// lift != 0: the lifting mean of the primitive (u, v, w, T) instead (4 components).
 static void device_interface_flux(const sdg_gas& gas, int degree, int kind, const long* nfy, const long* nfz,
                                   double l_y, double l_z, double d_y, double d_z, const double* u_a,
                                   const double* u_b, const double* g_a, const double* g_b, double* flux_mortar,
-                                  double* flux_a, double* flux_b, long* n_mortars) {
+                                  double* flux_a, double* flux_b, long* n_mortars, int lift = 0) {
   if ((g_a == nullptr) != (g_b == nullptr)) throw ConfigError("gradients must be given for both sides or neither");
   const Basis bs(degree, kind);
   const int n = bs.n, nn = n * n;
@@ -1632,13 +1633,17 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
                gas.gamma * gas.R * gas.mu / ((gas.gamma - 1.0) * gas.Pr), gas.mu > 0.0 ? 1 : 0};
   DevBuf<int> d_bad;
   d_bad.upload(std::vector<int>{0}, st);
-  d_flux.alloc(nm * nn * 5);
-  launch_nc_mortar_flux(nm * nn, g, 0, 0.0, d_mu[0].p, d_mu[1].p, vis ? d_mg[0].p : nullptr,
-                        vis ? d_mg[1].p : nullptr, d_flux.p, d_bad.p, st);
+  const int nco = lift ? 4 : 5;
+  d_flux.alloc(nm * nn * nco);
+  if (lift)
+    launch_nc_mortar_lift(nm * nn, g, d_mu[0].p, d_mu[1].p, d_flux.p, st);
+  else
+    launch_nc_mortar_flux(nm * nn, g, 0, 0.0, d_mu[0].p, d_mu[1].p, vis ? d_mg[0].p : nullptr,
+                          vis ? d_mg[1].p : nullptr, d_flux.p, d_bad.p, st);
   double* out[2] = {flux_a, flux_b};
   for (int s = 0; s < 2; ++s) {
-    d_face[s].alloc(nfy[s] * nfz[s] * nn * 5);
-    launch_nc_transfer(n, 5, d_flux.p, mz, nullptr, nullptr, 0, 0, mz, nullptr, nullptr, d_flux.p, nfy[s], nfz[s],
+    d_face[s].alloc(nfy[s] * nfz[s] * nn * nco);
+    launch_nc_transfer(n, nco, d_flux.p, mz, nullptr, nullptr, 0, 0, mz, nullptr, nullptr, d_flux.p, nfy[s], nfz[s],
                        d_off[s][0].p, d_idx[s][0].p, d_off[s][1].p, d_idx[s][1].p, d_B[s][0].p, d_B[s][1].p,
                        d_face[s].p, st);
     if (out[s])
@@ -2141,6 +2146,15 @@ int sdg_interface_flux_device(const sdg_gas* gas, int degree, int node_kind, con
     if (gas == nullptr) throw sdg::ConfigError("gas is NULL");
     sdg::device_interface_flux(*gas, degree, node_kind, nfy, nfz, l_y, l_z, d_y, d_z, u_a, u_b, g_a, g_b,
                                flux_mortar, flux_a, flux_b, n_mortars);
+  });
+}
+int sdg_interface_lift_device(const sdg_gas* gas, int degree, int node_kind, const long* nfy, const long* nfz,
+                              double l_y, double l_z, double d_y, double d_z, const double* u_a, const double* u_b,
+                              double* lift_mortar, double* lift_a, double* lift_b, long* n_mortars) {
+  return guarded(nullptr, [&] {
+    if (gas == nullptr) throw sdg::ConfigError("gas is NULL");
+    sdg::device_interface_flux(*gas, degree, node_kind, nfy, nfz, l_y, l_z, d_y, d_z, u_a, u_b, nullptr, nullptr,
+                               lift_mortar, lift_a, lift_b, n_mortars, 1);
   });
 }
 int sdg_diagnostics(sdg_ctx* c, double t, int with_exact, double* out) {

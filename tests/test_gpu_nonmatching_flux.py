@@ -147,3 +147,47 @@ def test_interface_flux_rejects_nonphysical_state():
         u[s][..., 4] = -1.0  # negative energy -> negative Roe-averaged enthalpy
     with pytest.raises(Exception):
         capi.interface_flux_device(GAS_EULER, degree, T.NODES_GAUSS, [2, 2], [2, 2], 1.0, 1.0, 0.3, 0.0, u[0], u[1])
+
+
+def _prim4(u, gas):
+    v = u[..., 1:4] / u[..., :1]
+    p = (gas.gamma - 1.0) * (u[..., 4] - 0.5 * (u[..., 1:4] ** 2).sum(-1) / u[..., 0])
+    return np.concatenate([v, (p / (u[..., 0] * gas.R))[..., None]], axis=-1)
+
+
+@pytest.mark.parametrize("kind", [T.NODES_GAUSS, T.NODES_LGL])
+def test_config1_interface_lift_matches_numpy(kind):
+    """The lifting mean on the configs[1] interface (N = 7): both sides' traces to
+    the mortars, mean of the primitive (u, v, w, T) there (the oracle's
+    run_lifting, oracle/sdg3d.cpp, after solver.cpp:597-727), projected back."""
+    degree, n = 7, 8
+    nfy, nfz = [16, 12], [16, 12]
+    l = 2.0 / 16
+    d_y, d_z = 0.37 * 1.3, 0.11 * 1.3
+    rng = np.random.default_rng(31 + kind)
+    u = [_states(rng, (nfy[s], nfz[s], n, n)) for s in (0, 1)]
+    lm, la, lb = capi.interface_lift_device(GAS_VISC, degree, kind, nfy, nfz, l, l, d_y, d_z, u[0], u[1])
+    fy, oy = _rows_ops(degree, kind, nfy[0], nfy[1], l, d_y)
+    fz, oz = _rows_ops(degree, kind, nfz[0], nfz[1], l, d_z)
+    ref = [np.zeros((nfy[s], nfz[s], n, n, 4)) for s in (0, 1)]
+    for ky, kz in itertools.product(range(len(fy)), range(len(fz))):
+        mu = [np.einsum("ki,lj,ijc->klc", oy[s][ky][0], oz[s][kz][0], u[s][fy[ky, s], fz[kz, s]]) for s in (0, 1)]
+        mean = 0.5 * (_prim4(mu[0], GAS_VISC) + _prim4(mu[1], GAS_VISC))
+        m = ky * len(fz) + kz
+        assert np.abs(lm[m] - mean).max() <= 1e-12 * np.abs(mean).max()
+        for s in (0, 1):
+            ref[s][fy[ky, s], fz[kz, s]] += np.einsum("ik,jl,klc->ijc", oy[s][ky][1], oz[s][kz][1], mean)
+    for got, want in zip((la, lb), ref):
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_interface_lift_uniform_state_is_exact():
+    degree, n = 5, 6
+    nfy, nfz = [16, 12], [16, 12]
+    state = np.array([1.2, 0.36, -0.24, 0.12, 0.9 / 0.4 + 0.5 * 1.2 * 0.14])
+    u = [np.broadcast_to(state, (nfy[s], nfz[s], n, n, 5)).copy() for s in (0, 1)]
+    _, la, lb = capi.interface_lift_device(GAS_VISC, degree, T.NODES_GAUSS, nfy, nfz, 0.125, 0.125, 0.481, 0.143,
+                                           u[0], u[1])
+    want = _prim4(state, GAS_VISC)
+    for f in (la, lb):
+        assert np.abs(f - want).max() <= 1e-13 * np.abs(want).max()
