@@ -191,3 +191,41 @@ def test_interface_lift_uniform_state_is_exact():
     want = _prim4(state, GAS_VISC)
     for f in (la, lb):
         assert np.abs(f - want).max() <= 1e-13 * np.abs(want).max()
+
+
+def test_equal_counts_flux_is_reference_mortar_chain():
+    """Equal counts, displacement along y only: the interface flux equals the
+    reference's mortar chain built from the oracle-restated pieces: the static side
+    A's halves fwd(sigma)[sub] of face i, the moving side B's fwd(-sigma)[1 - sub] of
+    face moving_index(i, n_delta, sub) (mortar.cpp:136-150), face_numerical_flux at
+    the mortar nodes, and bwd(sigma)[sub] / bwd(-sigma)[1 - sub] back (solver.cpp:156-176)."""
+    degree, n, kind = 3, 4, T.NODES_GAUSS
+    nf, l, d = 4, 0.5, 0.3
+    rng = np.random.default_rng(11)
+    u = [_states(rng, (nf, nf, n, n)) for _ in (0, 1)]
+    g = [0.1 * rng.standard_normal((nf, nf, n, n, 12)) for _ in (0, 1)]
+    _, fa, fb = capi.interface_flux_device(GAS_VISC, degree, kind, [nf, nf], [nf, nf], l, l, d, 0.0, u[0], u[1],
+                                           g[0], g[1])
+    _, n_delta, s_delta = P.oracle_displacement(d, l, nf)
+    sigma = 2.0 * s_delta - 1.0
+    fwd_a, bwd_a = P.oracle_mortar_ops(degree, kind, sigma)
+    fwd_b, bwd_b = P.oracle_mortar_ops(degree, kind, -sigma)
+    lib = P.oracle_lib()
+    ea, eb = np.zeros_like(fa), np.zeros_like(fb)
+    f = np.zeros(5)
+    for i in range(nf):
+        for sub in (0, 1):
+            j = lib.orc_moving_index(i, n_delta, sub, nf)
+            mu = [np.einsum("ki,zijc->zkjc", fwd_a[sub], u[0][i]), np.einsum("ki,zijc->zkjc", fwd_b[1 - sub], u[1][j])]
+            mg = [np.einsum("ki,zijc->zkjc", fwd_a[sub], g[0][i]), np.einsum("ki,zijc->zkjc", fwd_b[1 - sub], g[1][j])]
+            fm = np.zeros((nf, n, n, 5))
+            for idx in itertools.product(range(nf), range(n), range(n)):
+                args = [np.ascontiguousarray(x[idx]) for x in (mu[0], mu[1], mg[0], mg[1])]
+                assert lib.orc_face_flux(C_gas(GAS_VISC), P._d(args[0]), P._d(args[1]), 0, 0.0, P._d(args[2]),
+                                         P._d(args[3]), P._d(f)) == 0
+                fm[idx] = f
+            ea[i] += np.einsum("ik,zkjc->zijc", bwd_a[sub], fm)
+            eb[j] += np.einsum("ik,zkjc->zijc", bwd_b[1 - sub], fm)
+    scale = np.abs(ea).max()
+    assert np.abs(fa - ea).max() <= 1e-12 * scale
+    assert np.abs(fb - eb).max() <= 1e-12 * scale
