@@ -2674,8 +2674,11 @@ void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, con
                         const double* Fz, double* mortar, long long dst_nfy, long long dst_nfz, const int* off_y,
                         const int* idx_y, const int* off_z, const int* idx_z, const double* By, const double* Bz,
                         double* dst, cudaStream_t st) {
-  const int per = n * n * nc, threads = 128;
-  if (per > 8 * threads) throw DeviceError(SDG_ERR_CONFIG, "nc transfer: n*n*nc exceeds 1024");
+  // One thread per output value of a face / mortar (up to 1024): the CSR gather of
+  // k_nc_to_face is a serial loop over a face's mortars, so the per-mortar
+  // contraction must be as wide as the face.
+  const int per = n * n * nc, threads = std::min(1024, (per + 31) / 32 * 32);
+  if (per > 1024) throw DeviceError(SDG_ERR_CONFIG, "nc transfer: n*n*nc exceeds 1024");
   const size_t shm = 2 * per * sizeof(double);
   if (my * mz > 0) {
     k_nc_to_mortar<<<static_cast<unsigned>(my * mz), threads, shm, st>>>(n, nc, src, src_nfz, iv_y, iv_z, src_col, mz,
