@@ -2599,12 +2599,13 @@ void launch_mortar_intervals(long long n_a, long long n_b, double l_a, double de
 // k_nc_to_face: target face (fy, fz) = sum over its mortars (rows in CSR, fixed
 // order) of (By[ky] x Bz[kz]) applied to the mortar data.  One block per item.
 // ---------------------------------------------------------------------------
-__global__ void k_nc_to_mortar(int n, int nc, const double* __restrict__ src, long long nfz,
-                               const long long* __restrict__ iv_y, const long long* __restrict__ iv_z, int col,
-                               long long mz, const double* __restrict__ Fy, const double* __restrict__ Fz,
-                               double* __restrict__ mortar) {
+__device__ __forceinline__ void nc_to_mortar_body(long long blk, int n, int nc, const double* __restrict__ src,
+                                                  long long nfz, const long long* __restrict__ iv_y,
+                                                  const long long* __restrict__ iv_z, int col, long long mz,
+                                                  const double* __restrict__ Fy, const double* __restrict__ Fz,
+                                                  double* __restrict__ mortar) {
   extern __shared__ double sm[];
-  const long long ky = blockIdx.x / mz, kz = blockIdx.x % mz;
+  const long long ky = blk / mz, kz = blk % mz;
   const long long fy = iv_y[2 * ky + col], fz = iv_z[2 * kz + col];
   const int per = n * n * nc;
   double* u = sm;
@@ -2621,7 +2622,7 @@ __global__ void k_nc_to_mortar(int n, int nc, const double* __restrict__ src, lo
     t[x] = acc;
   }
   __syncthreads();
-  double* out = mortar + blockIdx.x * static_cast<long long>(per);
+  double* out = mortar + blk * static_cast<long long>(per);
   for (int x = threadIdx.x; x < per; x += blockDim.x) {  // out[k][l][c] = sum_j Fz[l][j] t[k][j][c]
     const int c = x % nc, l = (x / nc) % n, k = x / (nc * n);
     double acc = 0.0;
@@ -2630,12 +2631,27 @@ __global__ void k_nc_to_mortar(int n, int nc, const double* __restrict__ src, lo
   }
 }
 
-__global__ void k_nc_to_face(int n, int nc, const double* __restrict__ mortar, long long mz, long long nfz,
-                             const int* __restrict__ off_y, const int* __restrict__ idx_y,
-                             const int* __restrict__ off_z, const int* __restrict__ idx_z,
-                             const double* __restrict__ By, const double* __restrict__ Bz, double* __restrict__ dst) {
+__global__ void k_nc_to_mortar(int n, int nc, const double* __restrict__ src, long long nfz,
+                               const long long* __restrict__ iv_y, const long long* __restrict__ iv_z, int col,
+                               long long mz, const double* __restrict__ Fy, const double* __restrict__ Fz,
+                               double* __restrict__ mortar) {
+  nc_to_mortar_body(blockIdx.x, n, nc, src, nfz, iv_y, iv_z, col, mz, Fy, Fz, mortar);
+}
+
+// Several face -> mortar transfers of one interface in one launch (blockIdx.y = job).
+__global__ void k_nc_to_mortar_batch(int n, const long long* __restrict__ iv_y, const long long* __restrict__ iv_z,
+                                     long long mz, const __grid_constant__ NcMortarJobs jobs) {
+  const NcMortarJob& j = jobs.job[blockIdx.y];
+  nc_to_mortar_body(blockIdx.x, n, j.nc, j.src, j.src_nfz, iv_y, iv_z, j.col, mz, j.Fy, j.Fz, j.out);
+}
+
+__device__ __forceinline__ void nc_to_face_body(long long blk, int n, int nc, const double* __restrict__ mortar,
+                                                long long mz, long long nfz, const int* __restrict__ off_y,
+                                                const int* __restrict__ idx_y, const int* __restrict__ off_z,
+                                                const int* __restrict__ idx_z, const double* __restrict__ By,
+                                                const double* __restrict__ Bz, double* __restrict__ dst) {
   extern __shared__ double sm[];
-  const long long fy = blockIdx.x / nfz, fz = blockIdx.x % nfz;
+  const long long fy = blk / nfz, fz = blk % nfz;
   const int per = n * n * nc;
   double* m = sm;
   double* t = sm + per;
@@ -2665,8 +2681,49 @@ __global__ void k_nc_to_face(int n, int nc, const double* __restrict__ mortar, l
         acc_local[r] += acc;
       }
     }
-  double* out = dst + blockIdx.x * static_cast<long long>(per);
+  double* out = dst + blk * static_cast<long long>(per);
   for (int r = 0, x = threadIdx.x; x < per; ++r, x += blockDim.x) out[x] = acc_local[r];
+}
+
+__global__ void k_nc_to_face(int n, int nc, const double* __restrict__ mortar, long long mz, long long nfz,
+                             const int* __restrict__ off_y, const int* __restrict__ idx_y,
+                             const int* __restrict__ off_z, const int* __restrict__ idx_z,
+                             const double* __restrict__ By, const double* __restrict__ Bz, double* __restrict__ dst) {
+  nc_to_face_body(blockIdx.x, n, nc, mortar, mz, nfz, off_y, idx_y, off_z, idx_z, By, Bz, dst);
+}
+
+// Mortar -> face projections onto several face sets in one launch (blockIdx.y = job;
+// blocks past a job's face count exit before any barrier).
+__global__ void k_nc_to_face_batch(int n, int nc, const double* __restrict__ mortar, long long mz,
+                                   const __grid_constant__ NcFaceJobs jobs) {
+  const NcFaceJob& j = jobs.job[blockIdx.y];
+  if (blockIdx.x >= j.nfy * j.nfz) return;
+  nc_to_face_body(blockIdx.x, n, nc, mortar, mz, j.nfz, j.off_y, j.idx_y, j.off_z, j.idx_z, j.By, j.Bz, j.dst);
+}
+
+static int nc_threads(int per) { return std::min(1024, (per + 31) / 32 * 32); }
+
+void launch_nc_to_mortar_batch(int n, const long long* iv_y, const long long* iv_z, long long my, long long mz,
+                               const NcMortarJobs& jobs, cudaStream_t st) {
+  int per = 0;
+  for (int k = 0; k < jobs.n; ++k) per = std::max(per, n * n * jobs.job[k].nc);
+  if (per > 1024) throw DeviceError(SDG_ERR_CONFIG, "nc transfer: n*n*nc exceeds 1024");
+  if (my * mz == 0 || jobs.n == 0) return;
+  k_nc_to_mortar_batch<<<dim3(static_cast<unsigned>(my * mz), jobs.n), nc_threads(per), 2 * per * sizeof(double),
+                         st>>>(n, iv_y, iv_z, mz, jobs);
+  check_launch("k_nc_to_mortar_batch");
+}
+
+void launch_nc_to_face_batch(int n, int nc, const double* mortar, long long mz, const NcFaceJobs& jobs,
+                             cudaStream_t st) {
+  const int per = n * n * nc;
+  if (per > 1024) throw DeviceError(SDG_ERR_CONFIG, "nc transfer: n*n*nc exceeds 1024");
+  long long faces = 0;
+  for (int k = 0; k < jobs.n; ++k) faces = std::max(faces, jobs.job[k].nfy * jobs.job[k].nfz);
+  if (faces == 0) return;
+  k_nc_to_face_batch<<<dim3(static_cast<unsigned>(faces), jobs.n), nc_threads(per), 2 * per * sizeof(double), st>>>(
+      n, nc, mortar, mz, jobs);
+  check_launch("k_nc_to_face_batch");
 }
 
 void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, const long long* iv_y,

@@ -183,6 +183,33 @@ void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, con
                         const double* Fz, double* mortar, long long dst_nfy, long long dst_nfz, const int* off_y,
                         const int* idx_y, const int* off_z, const int* idx_z, const double* By, const double* Bz,
                         double* dst, cudaStream_t st);
+// Batched transfers of one non-matching interface (up to 4 face -> mortar jobs, up to
+// 2 mortar -> face jobs per launch).
+struct NcMortarJob {
+  const double* src;
+  long long src_nfz;
+  int col, nc;
+  const double *Fy, *Fz;
+  double* out;
+};
+struct NcMortarJobs {
+  NcMortarJob job[4];
+  int n;
+};
+struct NcFaceJob {
+  long long nfy, nfz;
+  const int *off_y, *idx_y, *off_z, *idx_z;
+  const double *By, *Bz;
+  double* dst;
+};
+struct NcFaceJobs {
+  NcFaceJob job[2];
+  int n;
+};
+void launch_nc_to_mortar_batch(int n, const long long* iv_y, const long long* iv_z, long long my, long long mz,
+                               const NcMortarJobs& jobs, cudaStream_t st);
+void launch_nc_to_face_batch(int n, int nc, const double* mortar, long long mz, const NcFaceJobs& jobs,
+                             cudaStream_t st);
 // Two-sided Riemann (+ viscous) flux at the mortar nodes of a non-matching interface.
 void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, const double* ua, const double* ub,
                            const double* ga, const double* gb, double* flux, int* bad, cudaStream_t st);

@@ -1616,19 +1616,19 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
   DevBuf<double> d_u[2], d_g[2], d_mu[2], d_mg[2], d_flux, d_face[2];
   const double* u_in[2] = {u_a, u_b};
   const double* g_in[2] = {g_a, g_b};
+  NcMortarJobs mj{};
   for (int s = 0; s < 2; ++s) {
     const long nf = nfy[s] * nfz[s];
     d_u[s].upload(std::vector<double>(u_in[s], u_in[s] + nf * nn * 5), st);
     d_mu[s].alloc(nm * nn * 5);
-    launch_nc_transfer(n, 5, d_u[s].p, nfz[s], d_ivy.p, d_ivz.p, s, my, mz, d_F[s][0].p, d_F[s][1].p, d_mu[s].p, 0,
-                       0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+    mj.job[mj.n++] = NcMortarJob{d_u[s].p, nfz[s], s, 5, d_F[s][0].p, d_F[s][1].p, d_mu[s].p};
     if (vis) {
       d_g[s].upload(std::vector<double>(g_in[s], g_in[s] + nf * nn * 12), st);
       d_mg[s].alloc(nm * nn * 12);
-      launch_nc_transfer(n, 12, d_g[s].p, nfz[s], d_ivy.p, d_ivz.p, s, my, mz, d_F[s][0].p, d_F[s][1].p, d_mg[s].p,
-                         0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+      mj.job[mj.n++] = NcMortarJob{d_g[s].p, nfz[s], s, 12, d_F[s][0].p, d_F[s][1].p, d_mg[s].p};
     }
   }
+  launch_nc_to_mortar_batch(n, d_ivy.p, d_ivz.p, my, mz, mj, st);
   const GasD g{gas.gamma, gas.gamma - 1.0, gas.R, 1.0 / gas.R, gas.mu, -2.0 / 3.0 * gas.mu,
                gas.gamma * gas.R * gas.mu / ((gas.gamma - 1.0) * gas.Pr), gas.mu > 0.0 ? 1 : 0};
   DevBuf<int> d_bad;
@@ -1641,15 +1641,17 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
     launch_nc_mortar_flux(nm * nn, g, 0, 0.0, d_mu[0].p, d_mu[1].p, vis ? d_mg[0].p : nullptr,
                           vis ? d_mg[1].p : nullptr, d_flux.p, d_bad.p, st);
   double* out[2] = {flux_a, flux_b};
+  NcFaceJobs fj{};
   for (int s = 0; s < 2; ++s) {
     d_face[s].alloc(nfy[s] * nfz[s] * nn * nco);
-    launch_nc_transfer(n, nco, d_flux.p, mz, nullptr, nullptr, 0, 0, mz, nullptr, nullptr, d_flux.p, nfy[s], nfz[s],
-                       d_off[s][0].p, d_idx[s][0].p, d_off[s][1].p, d_idx[s][1].p, d_B[s][0].p, d_B[s][1].p,
-                       d_face[s].p, st);
+    fj.job[fj.n++] = NcFaceJob{nfy[s], nfz[s], d_off[s][0].p, d_idx[s][0].p, d_off[s][1].p, d_idx[s][1].p,
+                               d_B[s][0].p, d_B[s][1].p, d_face[s].p};
+  }
+  launch_nc_to_face_batch(n, nco, d_flux.p, mz, fj, st);
+  for (int s = 0; s < 2; ++s)
     if (out[s])
       cuda_check(cudaMemcpyAsync(out[s], d_face[s].p, d_face[s].n * sizeof(double), cudaMemcpyDeviceToHost, st),
                  "copy");
-  }
   if (flux_mortar)
     cuda_check(cudaMemcpyAsync(flux_mortar, d_flux.p, d_flux.n * sizeof(double), cudaMemcpyDeviceToHost, st), "copy");
   int bad = 0;
