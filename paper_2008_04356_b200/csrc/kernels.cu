@@ -2509,9 +2509,9 @@ __device__ __forceinline__ long long iv_block_scan(long long v, long long* sh, l
   return incl - v;
 }
 
-__global__ void __launch_bounds__(kIvThreads) k_mortar_intervals(long long n_a, long long n_b, double l_a, double delta,
-                                                                 long long* faces, double* ranges, long long* n_out) {
-  __shared__ long long sh[kIvThreads];
+__device__ __forceinline__ void mortar_intervals_row(long long n_a, long long n_b, double l_a, double delta,
+                                                     long long* faces, double* ranges, long long* n_out,
+                                                     long long* sh) {
   const double period = __dmul_rn(l_a, static_cast<double>(n_a));
   double d = fmod(delta, period);
   if (d < 0.0) d = __dadd_rn(d, period);
@@ -2584,6 +2584,24 @@ __global__ void __launch_bounds__(kIvThreads) k_mortar_intervals(long long n_a, 
       p_int = m;
     }
   }
+}
+
+__global__ void __launch_bounds__(kIvThreads) k_mortar_intervals(long long n_a, long long n_b, double l_a, double delta,
+                                                                 long long* faces, double* ranges, long long* n_out) {
+  __shared__ long long sh[kIvThreads];
+  mortar_intervals_row(n_a, n_b, l_a, delta, faces, ranges, n_out, sh);
+}
+
+// Both rows (y and z) of a non-matching interface in one launch, one block per row.
+__global__ void __launch_bounds__(kIvThreads) k_mortar_intervals2(const __grid_constant__ IvRows rows) {
+  __shared__ long long sh[kIvThreads];
+  const IvRow& r = rows.row[blockIdx.x];
+  mortar_intervals_row(r.n_a, r.n_b, r.l_a, r.delta, r.faces, r.ranges, r.n_out, sh);
+}
+
+void launch_mortar_intervals2(const IvRows& rows, cudaStream_t st) {
+  k_mortar_intervals2<<<2, kIvThreads, 0, st>>>(rows);
+  check_launch("k_mortar_intervals2");
 }
 
 void launch_mortar_intervals(long long n_a, long long n_b, double l_a, double delta, long long* faces,
@@ -2709,7 +2727,8 @@ void launch_nc_to_mortar_batch(int n, const long long* iv_y, const long long* iv
   for (int k = 0; k < jobs.n; ++k) per = std::max(per, n * n * jobs.job[k].nc);
   if (per > 1024) throw DeviceError(SDG_ERR_CONFIG, "nc transfer: n*n*nc exceeds 1024");
   if (my * mz == 0 || jobs.n == 0) return;
-  k_nc_to_mortar_batch<<<dim3(static_cast<unsigned>(my * mz), jobs.n), nc_threads(per), 2 * per * sizeof(double),
+  // No serial loop here (one mortar per block): narrow blocks keep more mortars resident per SM.
+  k_nc_to_mortar_batch<<<dim3(static_cast<unsigned>(my * mz), jobs.n), 128, 2 * per * sizeof(double),
                          st>>>(n, iv_y, iv_z, mz, jobs);
   check_launch("k_nc_to_mortar_batch");
 }

@@ -183,6 +183,18 @@ void launch_nc_transfer(int n, int nc, const double* src, long long src_nfz, con
                         const double* Fz, double* mortar, long long dst_nfy, long long dst_nfz, const int* off_y,
                         const int* idx_y, const int* off_z, const int* idx_z, const double* By, const double* Bz,
                         double* dst, cudaStream_t st);
+// The y and z rows of one interface in one launch (separate output buffers).
+struct IvRow {
+  long long n_a, n_b;
+  double l_a, delta;
+  long long* faces;
+  double* ranges;
+  long long* n_out;
+};
+struct IvRows {
+  IvRow row[2];
+};
+void launch_mortar_intervals2(const IvRows& rows, cudaStream_t st);
 // Batched transfers of one non-matching interface (up to 4 face -> mortar jobs, up to
 // 2 mortar -> face jobs per launch).
 struct NcMortarJob {

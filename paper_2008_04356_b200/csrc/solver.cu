@@ -1595,10 +1595,13 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
   DevBuf<double> d_rng;
   d_ivy.alloc(2 * (nfy[0] + nfy[1]));
   d_ivz.alloc(2 * (nfz[0] + nfz[1]));
-  d_rng.alloc(4 * std::max(nfy[0] + nfy[1], nfz[0] + nfz[1]));
-  d_n.alloc(1);
-  launch_mortar_intervals(nfy[0], nfy[1], l_y, d_y, d_ivy.p, d_rng.p, d_n.p, st);
-  launch_mortar_intervals(nfz[0], nfz[1], l_z, d_z, d_ivz.p, d_rng.p, d_n.p, st);
+  const long rmax = 4 * std::max(nfy[0] + nfy[1], nfz[0] + nfz[1]);
+  d_rng.alloc(2 * rmax);
+  d_n.alloc(2);
+  IvRows rows{};
+  rows.row[0] = IvRow{nfy[0], nfy[1], l_y, d_y, d_ivy.p, d_rng.p, d_n.p};
+  rows.row[1] = IvRow{nfz[0], nfz[1], l_z, d_z, d_ivz.p, d_rng.p + rmax, d_n.p + 1};
+  launch_mortar_intervals2(rows, st);
   DevBuf<double> d_F[2][2], d_B[2][2];  // [side][y/z]
   DevBuf<int> d_off[2][2], d_idx[2][2];
   for (int s = 0; s < 2; ++s) {
