@@ -1440,12 +1440,24 @@ void GpuRankSolver::get_mapping(int c, int* m) {
   cuda_check(cudaStreamSynchronize(stream_), "sync");
 }
 
+// A stream owned by one host-side call, released on every exit path (exceptions included).
+struct OwnedStream {
+  cudaStream_t s{};
+  OwnedStream() { cuda_check(cudaStreamCreate(&s), "stream"); }
+  ~OwnedStream() {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  OwnedStream(const OwnedStream&) = delete;
+  OwnedStream& operator=(const OwnedStream&) = delete;
+  operator cudaStream_t() const { return s; }
+};
+
 // Stand-alone device pairing on caller-given faces (Appendix-A fixture).
 static void device_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges) {
   if (n_a < 1 || n_b < 1) throw ConfigError("interval merge needs at least one face per side");
   if (!(l_a > 0.0)) throw ConfigError("face length must be positive");
-  cudaStream_t st;
-  cuda_check(cudaStreamCreate(&st), "stream");
+  const OwnedStream st;
   const long cap = n_a + n_b;
   DevBuf<long long> d_faces, d_n;
   DevBuf<double> d_ranges;
@@ -1460,7 +1472,6 @@ static void device_intervals(long n_a, long n_b, double l_a, double delta, long*
   cuda_check(cudaMemcpyAsync(hf.data(), d_faces.p, hf.size() * sizeof(long long), cudaMemcpyDeviceToHost, st), "copy");
   cuda_check(cudaMemcpyAsync(hr.data(), d_ranges.p, hr.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "copy");
   cuda_check(cudaStreamSynchronize(st), "sync");
-  cudaStreamDestroy(st);
   *n_out = static_cast<long>(n);
   if (faces == nullptr || ranges == nullptr) return;
   for (long long k = 0; k < 2 * n; ++k) faces[k] = static_cast<long>(hf[k]);
@@ -1509,8 +1520,7 @@ static void device_interface_project(int degree, int kind, const long* nfy, cons
   std::vector<int> offy, idxy, offz, idxz;
   ops(ry, Fy, By, offy, idxy, nfy[to]);
   ops(rz, Fz, Bz, offz, idxz, nfz[to]);
-  cudaStream_t st;
-  cuda_check(cudaStreamCreate(&st), "stream");
+  const OwnedStream st;
   DevBuf<long long> d_ivy, d_ivz, d_n;
   DevBuf<double> d_rng, d_Fy, d_By, d_Fz, d_Bz, d_src, d_mortar, d_dst;
   DevBuf<int> d_offy, d_idxy, d_offz, d_idxz;
@@ -1541,7 +1551,6 @@ static void device_interface_project(int degree, int kind, const long* nfy, cons
     cuda_check(cudaMemcpyAsync(dst, d_dst.p, nfy[to] * nfz[to] * per * sizeof(double), cudaMemcpyDeviceToHost, st),
                "copy");
   cuda_check(cudaStreamSynchronize(st), "sync");
-  cudaStreamDestroy(st);
 }
 
 // The operators of one side s of a mortar row: face -> mortar (F) and mortar ->
@@ -1589,8 +1598,7 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
   *n_mortars = my * mz;
   NcSideOps oy[2] = {nc_side_ops(bs, ry, 0, nfy[0]), nc_side_ops(bs, ry, 1, nfy[1])};
   NcSideOps oz[2] = {nc_side_ops(bs, rz, 0, nfz[0]), nc_side_ops(bs, rz, 1, nfz[1])};
-  cudaStream_t st;
-  cuda_check(cudaStreamCreate(&st), "stream");
+  const OwnedStream st;
   DevBuf<long long> d_ivy, d_ivz, d_n;
   DevBuf<double> d_rng;
   d_ivy.alloc(2 * (nfy[0] + nfy[1]));
@@ -1660,15 +1668,13 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
   int bad = 0;
   cuda_check(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
   cuda_check(cudaStreamSynchronize(st), "sync");
-  cudaStreamDestroy(st);
   if (bad) throw InvalidStateError("interface flux: non-positive Roe-averaged c^2 at " + std::to_string(bad) + " mortar nodes");
 }
 
 static void device_pairing(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,
                            long n_delta, int on_static, int conforming, int self_rank, int* ncols, int* cols,
                            int* m_rows, long* face_lo, int* nsched, int* sched, int* self_entry) {
-  cudaStream_t st;
-  cuda_check(cudaStreamCreate(&st), "stream");
+  const OwnedStream st;
   PairingArgs a{};
   a.n_ctx = 1;
   a.n_ifaces = 1;
@@ -1743,7 +1749,6 @@ static void device_pairing(int n_local, const long* faces, long n_par, long n_pe
   std::vector<int> hc(7 * static_cast<size_t>(std::max(nm[role], 1))), hm(2 * static_cast<size_t>(n_local) + 1);
   cuda_check(cudaMemcpy(hc.data(), d_cols.p, sizeof(int) * 7 * nm[role], cudaMemcpyDeviceToHost), "d2h");
   cuda_check(cudaMemcpy(hm.data(), d_m.p, sizeof(int) * 2 * n_local, cudaMemcpyDeviceToHost), "d2h");
-  cudaStreamDestroy(st);
   if (er.flag != 0) throw ProtocolError("rank map lookup hit an unset entry");
   // Caller face ids ride along passively (build_mapping, partition.cpp:124-141).
   long lo = 0, hi = -1;
