@@ -54,11 +54,19 @@ enum {
   SDG_CASE_SWIRL = 4   /* axial density wave with rigid swirl about the x axis (annulus tests) */
 };
 
-/* One band (block) of structured, axis-aligned hexahedra. */
+/* One band (block) of structured, axis-aligned hexahedra (BandSpec, mesh.hpp:12-17). */
 typedef struct {
   int nx;            /* elements along x */
   double width_frac; /* relative width, normalised over all bands */
   double vg_y;       /* rigid translation speed along +y (0 = static) */
+  /* Per-band element counts along y and z; 0 uses the mesh-wide ny / nz (the
+   * reference's BandSpec::ny override).  Bands with different counts meet at
+   * a non-matching sliding interface (BASELINE configs[1]); the reference
+   * requires equal counts (mesh.cpp:75-77). */
+  int ny, nz;
+  /* Rigid translation speed along +z (the second tangential direction of the
+   * x-normal interfaces; BASELINE configs[1] slides obliquely).  SDG_MAP_BOX only. */
+  double vg_z;
 } sdg_band_spec;
 
 typedef struct {

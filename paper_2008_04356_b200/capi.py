@@ -63,6 +63,9 @@ def lib():
         L.sdg_steps.argtypes = [_vp, C.c_double, C.c_int]
         L.sdg_steps_async.argtypes = [_vp, C.c_double, C.c_int]
         L.sdg_synchronize.argtypes = [_vp]
+        L.sdg_rk_stage.argtypes = [_vp, C.c_int, C.c_double, C.c_double]
+        L.sdg_rk_coefficients.argtypes = [_dp, _dp, _dp]
+        L.sdg_update_interfaces.argtypes = [_vp, C.c_double, _dp]
         L.sdg_compute_residual.argtypes = [_vp, C.c_double, C.c_void_p, C.c_void_p]
         L.sdg_compute_residual_host.argtypes = [_vp, C.c_double, _dp, _dp]
         L.sdg_compute_gradients_host.argtypes = [_vp, C.c_double, _dp, _dp]
@@ -106,7 +109,8 @@ EXPORTED = [
     "sdg_create", "sdg_create_inproc", "sdg_destroy", "sdg_last_error", "sdg_global_error", "sdg_nccl_unique_id", "sdg_init_rank_maps",
     "sdg_set_initial_condition", "sdg_n1", "sdg_n_local_elements", "sdg_n_global_elements",
     "sdg_local_element_ids", "sdg_set_state", "sdg_get_state", "sdg_get_register", "sdg_state_device_ptr",
-    "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_compute_residual",
+    "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_rk_stage", "sdg_rk_coefficients",
+    "sdg_update_interfaces", "sdg_compute_residual",
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
     "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_subrange_ops",
@@ -119,6 +123,13 @@ EXPORTED = [
 
 def _d(a):
     return a.ctypes.data_as(_dp)
+
+
+def rk_coefficients():
+    """(a, b, c) of the 5-stage low-storage RK scheme (lsrk.cpp:7-29)."""
+    a, b, c = np.zeros(5), np.zeros(5), np.zeros(5)
+    lib().sdg_rk_coefficients(_d(a), _d(b), _d(c))
+    return a, b, c
 
 
 def nccl_unique_id() -> bytes:
@@ -187,6 +198,18 @@ class RankSolver:
 
     def steps_async(self, dt: float, n: int):
         self._check(self.lib.sdg_steps_async(self.h, dt, n))
+
+    def rk_stage(self, s: int, t: float, dt: float):
+        """One stage of the low-storage RK step starting at t (lsrk_step, lsrk.hpp:20-21)."""
+        self._check(self.lib.sdg_rk_stage(self.h, s, t, dt))
+
+    def update_interfaces(self, t_stage: float) -> np.ndarray:
+        """RankSolver::update_interfaces (solver.cpp:156-176); returns the per-context
+        operators [ctx][fwd lower, fwd upper, bwd lower, bwd upper][n][n]."""
+        n = self.lib.sdg_n1(self.h)
+        ops = np.zeros((max(self.n_contexts(), 1), 4, n, n))
+        self._check(self.lib.sdg_update_interfaces(self.h, t_stage, _d(ops)))
+        return ops[: self.n_contexts()]
 
     def synchronize(self):
         self._check(self.lib.sdg_synchronize(self.h))

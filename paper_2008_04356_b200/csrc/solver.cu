@@ -295,6 +295,8 @@ class GpuRankSolver {
   void get_state(double* h);
   void get_register(double* h);
   void steps(double dt, int n, bool sync);
+  void rk_stage(int s, double t, double dt);
+  void update_interfaces(double t_stage, double* ops);
   void synchronize();
   void compute_residual(double t_stage, const double* d_u, double* d_dudt);
   void compute_gradients(double t_stage, const double* d_u, double* d_grad);
@@ -312,6 +314,7 @@ class GpuRankSolver {
   void get_mapping(int c, int* m);
 
   int n1() const { return n_; }
+  int device() const { return device_; }
   long n_local() const { return E_; }
   long n_global() const { return mesh_.n_elements; }
   const std::vector<long>& gids() const { return topo_.gids; }
@@ -354,6 +357,8 @@ class GpuRankSolver {
   MortarPtrs mortar_ptrs();
   void check_error();
   void mark(int cls, bool begin);
+  void reset_clock(double t0);
+  void snapshot_barrier(double& flag);
 
   MeshGeom mesh_;
   Partition part_;
@@ -409,6 +414,7 @@ class GpuRankSolver {
 
   double time_ = 0.0;
   int step_index_ = 0, stage_index_ = 0;
+  int next_stage_ = 0;  // the RK stage rk_stage expects next
   bool traces_valid_ = false;
   int cur_trace_ = 0;  // traces of the current state live in trace_[cur_trace_]
   long launches_ = 0;
@@ -755,8 +761,6 @@ void GpuRankSolver::init_rank_maps() {
 }
 
 void GpuRankSolver::set_initial_condition(double t0) {
-  time_ = t0;
-  step_index_ = 0;
   std::vector<double> h(static_cast<size_t>(E_) * n3_ * 5);
   const int n = n_;
   for (int e = 0; e < E_; ++e) {
@@ -771,14 +775,22 @@ void GpuRankSolver::set_initial_condition(double t0) {
         }
   }
   cuda_check(cudaMemcpyAsync(U_.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, stream_), "h2d");
+  reset_clock(t0);
+  traces_valid_ = false;
+  cuda_check(cudaStreamSynchronize(stream_), "set_initial_condition");
+}
+
+// Time, step counter, RK register and interface offsets of a run starting at t0.
+void GpuRankSolver::reset_clock(double t0) {
+  time_ = t0;
+  step_index_ = 0;
+  next_stage_ = 0;
   reg_.zero(stream_);
   for (auto& c : sides_) {
     c.delta_base = mesh_.ifaces[c.iface].vg_rel * t0;
     c.wraps = 0;
     c.topo_valid = false;
   }
-  traces_valid_ = false;
-  cuda_check(cudaStreamSynchronize(stream_), "set_initial_condition");
 }
 
 void GpuRankSolver::set_state(const double* h) {
@@ -1230,24 +1242,52 @@ void GpuRankSolver::synchronize() { check_error(); }
 
 // step (solver.cpp:908-927), n times without host synchronisation.
 void GpuRankSolver::steps(double dt, int n, bool sync) {
-  for (int it = 0; it < n; ++it) {
-    for (int s = 0; s < 5; ++s) {
-      stage_index_ = s;
-      stage(time_ + RK_C[s] * dt, 0, RK_A[s], RK_B[s], dt, nullptr, nullptr);
-    }
-    time_ += dt;
-    step_index_++;
-    for (auto& c : sides_) {
-      const IfaceGeom& f = mesh_.ifaces[c.iface];
-      c.delta_base += f.vg_rel * dt;
-      const double period = f.l_par * static_cast<double>(f.n_faces);
-      while (c.delta_base >= period) {
-        c.delta_base -= period;
-        ++c.wraps;
-      }
+  if (next_stage_ != 0) throw ConfigError("step: an RK step begun with rk_stage is unfinished");
+  for (int it = 0; it < n; ++it)
+    for (int s = 0; s < 5; ++s) rk_stage(s, time_, dt);
+  if (sync) check_error();
+}
+
+// One stage of the 5-stage low-storage RK step that starts at t (lsrk_step,
+// lsrk.hpp:20-21 / lsrk.cpp:31-44, as RankSolver::step runs it, solver.cpp:908-927):
+// reg = a_s reg + dt R(u, t + c_s dt); u += b_s reg, then the admissibility check.
+// The last stage completes the step: time, step index and the sliding offsets
+// (delta_base += vg dt, wrapped by repeated subtraction, solver.cpp:922-926).
+void GpuRankSolver::rk_stage(int s, double t, double dt) {
+  if (s != next_stage_) throw ConfigError("rk_stage: stages run in order 0..4; expected stage " + std::to_string(next_stage_));
+  if (t != time_) throw ConfigError("rk_stage: t must be the time the step starts at (time())");
+  stage_index_ = s;
+  stage(time_ + RK_C[s] * dt, 0, RK_A[s], RK_B[s], dt, nullptr, nullptr);
+  next_stage_ = (s + 1) % 5;
+  if (s < 4) return;
+  time_ += dt;
+  step_index_++;
+  for (auto& c : sides_) {
+    const IfaceGeom& f = mesh_.ifaces[c.iface];
+    c.delta_base += f.vg_rel * dt;
+    const double period = f.l_par * static_cast<double>(f.n_faces);
+    while (c.delta_base >= period) {
+      c.delta_base -= period;
+      ++c.wraps;
     }
   }
-  if (sync) check_error();
+}
+
+// update_interfaces (solver.cpp:156-176) as an entry point: displacement, sigma
+// and the long-double operators on the host, the pairing on the device.
+// ops (may be NULL): per interface-side context, the lower / upper forward
+// (face -> mortar) and the lower / upper backward (mortar -> face) n x n
+// operators, row-major (MortarOperators, mortar.hpp).
+void GpuRankSolver::update_interfaces(double t_stage, double* ops) {
+  update_interfaces_host(t_stage);
+  run_pairing(t_stage);
+  if (ops == nullptr) return;
+  for (size_t c = 0; c < sides_.size(); ++c) {
+    double* o = ops + c * 4 * n2_;
+    std::copy(sides_[c].fwd.begin(), sides_[c].fwd.end(), o);
+    std::copy(sides_[c].bwd.begin(), sides_[c].bwd.end(), o + 2 * n2_);
+  }
+  check_error();
 }
 
 void GpuRankSolver::compute_residual(double t_stage, const double* d_u, double* d_dudt) {
@@ -1349,24 +1389,50 @@ static std::string snapshot_header(const MeshGeom& m, int degree, double time) {
   return os.str();
 }
 
+// Collective: rank 0 writes the header and sizes the file; after a barrier every
+// rank writes its elements in place ("r+b", never truncating); a second barrier
+// makes the file complete on every rank when the call returns.  The barriers
+// are I/O-phase synchronisation (like the diagnostics reductions), not part of
+// the stepping protocol, so the communication trace does not list them.
 void GpuRankSolver::write_snapshot(const char* path, double time) {
   std::vector<double> h(U_.n);
   get_state(h.data());
   const std::string hdr = snapshot_header(mesh_, basis_.degree, time);
-  FILE* f = std::fopen(path, rank_ == 0 ? "wb" : "r+b");
-  if (!f && rank_ != 0) f = std::fopen(path, "w+b");
-  if (!f) throw ConfigError(std::string("cannot open snapshot file ") + path);
   const size_t stride = static_cast<size_t>(n3_) * 5;
-  bool ok = true;
-  if (rank_ == 0) ok = std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
+  const long total = static_cast<long>(hdr.size() + static_cast<size_t>(mesh_.n_elements) * stride * sizeof(double));
+  double status = 0.0;  // max over ranks: 1 = some rank failed
+  if (rank_ == 0) {
+    FILE* f = std::fopen(path, "wb");
+    bool ok = f != nullptr && std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
+    if (ok && total > static_cast<long>(hdr.size())) {
+      const char zero = 0;  // pre-size: the last byte of the payload
+      ok = std::fseek(f, total - 1, SEEK_SET) == 0 && std::fwrite(&zero, 1, 1, f) == 1;
+    }
+    if (f) ok = (std::fclose(f) == 0) && ok;
+    status = ok ? 0.0 : 1.0;
+  }
+  snapshot_barrier(status);
+  if (status != 0.0) throw ConfigError(std::string("cannot create snapshot file ") + path);
+  FILE* f = std::fopen(path, "r+b");
+  bool ok = f != nullptr;
   for (int e = 0; e < E_ && ok; ++e) {
     ok = std::fseek(f, static_cast<long>(hdr.size() + topo_.gids[e] * stride * sizeof(double)), SEEK_SET) == 0 &&
          std::fwrite(h.data() + e * stride, sizeof(double), stride, f) == stride;
   }
-  std::fclose(f);
-  if (!ok) throw ConfigError(std::string("snapshot write failed for ") + path);
+  if (f) ok = (std::fclose(f) == 0) && ok;
+  status = ok ? 0.0 : 1.0;
+  snapshot_barrier(status);
+  if (status != 0.0) throw ConfigError(std::string("snapshot write failed for ") + path);
 }
 
+// Max of `flag` over ranks; a barrier between the snapshot phases.
+void GpuRankSolver::snapshot_barrier(double& flag) {
+  if (n_ranks_ > 1) comm_->allreduce(&flag, 1, 1, stream_);
+}
+
+// Restores the field, the time and the sliding-interface offsets (as
+// set_initial_condition(t) does, solver.cpp:73-90 / 156-176): the run continues
+// from the snapshot's time with delta_base = vg t.
 double GpuRankSolver::read_snapshot(const char* path) {
   FILE* f = std::fopen(path, "rb");
   if (!f) throw ConfigError(std::string("cannot open snapshot file ") + path);
@@ -1399,6 +1465,7 @@ double GpuRankSolver::read_snapshot(const char* path) {
   std::fclose(f);
   if (!ok) throw ConfigError(std::string("snapshot payload truncated in ") + path);
   set_state(h.data());
+  reset_clock(time);
   return time;
 }
 
@@ -1439,6 +1506,31 @@ void GpuRankSolver::get_mapping(int c, int* m) {
   cuda_check(cudaMemcpyAsync(m, m_.p + 2 * off, sizeof(int) * 2 * nf, cudaMemcpyDeviceToHost, stream_), "d2h");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
 }
+
+// A device buffer ordered on one stream (cudaMallocAsync / cudaFreeAsync): the
+// caller's host data is copied in, used by kernels and copied back in stream
+// order, pageable host memory included (the copy is staged before return).
+struct StreamBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  cudaStream_t st;
+  StreamBuf(size_t count, cudaStream_t s) : n(count), st(s) {
+    cuda_check(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(double), st), "cudaMallocAsync");
+  }
+  ~StreamBuf() {
+    cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+  }
+  StreamBuf(const StreamBuf&) = delete;
+  StreamBuf& operator=(const StreamBuf&) = delete;
+  void from_host(const double* h) {
+    cuda_check(cudaMemcpyAsync(p, h, n * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+  }
+  void to_host(double* h) {
+    cuda_check(cudaMemcpyAsync(h, p, n * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    cuda_check(cudaStreamSynchronize(st), "d2h sync");
+  }
+};
 
 // A stream owned by one host-side call, released on every exit path (exceptions included).
 struct OwnedStream {
@@ -1900,10 +1992,24 @@ struct sdg_ctx {
 namespace {
 thread_local std::string g_error;
 
+// Makes the context's device current for the duration of one entry point and
+// restores the caller's afterwards (one host thread may drive several GPUs).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const sdg_ctx* c) {
+    if (c && c->s && cudaGetDevice(&prev) == cudaSuccess && prev != c->s->device()) cudaSetDevice(c->s->device());
+    else prev = -1;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 int guarded(const sdg_ctx* c, F&& fn) {
   std::string* sink = c && c->s ? &c->s->err : &g_error;
   try {
+    DeviceScope dev(c);
     fn();
     return SDG_OK;
   } catch (const sdg::ConfigError& e) {
@@ -2004,6 +2110,20 @@ int sdg_steps(sdg_ctx* c, double dt, int n) {
 int sdg_steps_async(sdg_ctx* c, double dt, int n) {
   return guarded(c, [&] { c->s->steps(dt, n, false); });
 }
+int sdg_rk_stage(sdg_ctx* c, int s, double t, double dt) {
+  return guarded(c, [&] { c->s->rk_stage(s, t, dt); });
+}
+int sdg_rk_coefficients(double* a, double* b, double* cc) {
+  for (int s = 0; s < 5; ++s) {
+    if (a) a[s] = sdg::RK_A[s];
+    if (b) b[s] = sdg::RK_B[s];
+    if (cc) cc[s] = sdg::RK_C[s];
+  }
+  return SDG_OK;
+}
+int sdg_update_interfaces(sdg_ctx* c, double t_stage, double* ops) {
+  return guarded(c, [&] { c->s->update_interfaces(t_stage, ops); });
+}
 int sdg_synchronize(sdg_ctx* c) {
   return guarded(c, [&] { c->s->synchronize(); });
 }
@@ -2013,39 +2133,19 @@ int sdg_compute_residual(sdg_ctx* c, double t, const double* d_u, double* d_dudt
 int sdg_compute_residual_host(sdg_ctx* c, double t, const double* h_u, double* h_dudt) {
   return guarded(c, [&] {
     const size_t n = static_cast<size_t>(c->s->n_local()) * c->s->n1() * c->s->n1() * c->s->n1() * 5;
-    double *du = nullptr, *dd = nullptr;
-    sdg::cuda_check(cudaMalloc(&du, n * sizeof(double)), "malloc");
-    sdg::cuda_check(cudaMalloc(&dd, n * sizeof(double)), "malloc");
-    try {
-      sdg::cuda_check(cudaMemcpy(du, h_u, n * sizeof(double), cudaMemcpyHostToDevice), "h2d");
-      c->s->compute_residual(t, du, dd);
-      sdg::cuda_check(cudaMemcpy(h_dudt, dd, n * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-    } catch (...) {
-      cudaFree(du);
-      cudaFree(dd);
-      throw;
-    }
-    cudaFree(du);
-    cudaFree(dd);
+    sdg::StreamBuf du(n, c->s->stream()), dd(n, c->s->stream());
+    du.from_host(h_u);
+    c->s->compute_residual(t, du.p, dd.p);
+    dd.to_host(h_dudt);
   });
 }
 int sdg_compute_gradients_host(sdg_ctx* c, double t, const double* h_u, double* h_grad) {
   return guarded(c, [&] {
     const size_t nodes = static_cast<size_t>(c->s->n_local()) * c->s->n1() * c->s->n1() * c->s->n1();
-    double *du = nullptr, *dg = nullptr;
-    sdg::cuda_check(cudaMalloc(&du, nodes * 5 * sizeof(double)), "malloc");
-    sdg::cuda_check(cudaMalloc(&dg, nodes * 12 * sizeof(double)), "malloc");
-    try {
-      sdg::cuda_check(cudaMemcpy(du, h_u, nodes * 5 * sizeof(double), cudaMemcpyHostToDevice), "h2d");
-      c->s->compute_gradients(t, du, dg);
-      sdg::cuda_check(cudaMemcpy(h_grad, dg, nodes * 12 * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-    } catch (...) {
-      cudaFree(du);
-      cudaFree(dg);
-      throw;
-    }
-    cudaFree(du);
-    cudaFree(dg);
+    sdg::StreamBuf du(nodes * 5, c->s->stream()), dg(nodes * 12, c->s->stream());
+    du.from_host(h_u);
+    c->s->compute_gradients(t, du.p, dg.p);
+    dg.to_host(h_grad);
   });
 }
 int sdg_suggest_dt(sdg_ctx* c, double cfl, double* dt) {

@@ -20,7 +20,8 @@ CASE_FREESTREAM, CASE_DENSITY_WAVE, CASE_VORTEX, CASE_TGV, CASE_SWIRL = range(5)
 
 
 class BandSpec(C.Structure):
-    _fields_ = [("nx", C.c_int), ("width_frac", C.c_double), ("vg_y", C.c_double)]
+    _fields_ = [("nx", C.c_int), ("width_frac", C.c_double), ("vg_y", C.c_double), ("ny", C.c_int), ("nz", C.c_int),
+                ("vg_z", C.c_double)]
 
 
 class MeshSpec(C.Structure):
@@ -94,7 +95,9 @@ MAP_BOX, MAP_WARP, MAP_ANNULUS = 0, 1, 2
 
 def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z0=0.0,
               periodic=(True, True, True), partition=PARTITION_LEX, warp=None, mapping=None) -> MeshSpec:
-    """bands: list of (nx, width_frac, vg_y) tuples, stacked along x.  warp: None for
+    """bands: list of (nx, width_frac, vg_y[, ny, nz, vg_z]) tuples, stacked along x
+    (ny / nz = 0: the mesh-wide counts; bands with other counts meet at a
+    non-matching sliding interface; vg_z: slide along z).  warp: None for
     affine hexahedra, else the amplitude of the curved SDG_MAP_WARP mapping
     (include/sdg_types.h; 0.0 gives the curved code path on an affine geometry)."""
     if not 1 <= len(bands) <= SDG_MAX_BANDS:
@@ -108,6 +111,9 @@ def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z
         b = tuple(b)
         nx, frac, vg = b[0], (b[1] if len(b) > 1 else 1.0), (b[2] if len(b) > 2 else 0.0)
         m.bands[i].nx, m.bands[i].width_frac, m.bands[i].vg_y = int(nx), float(frac), float(vg)
+        m.bands[i].ny = int(b[3]) if len(b) > 3 else 0
+        m.bands[i].nz = int(b[4]) if len(b) > 4 else 0
+        m.bands[i].vg_z = float(b[5]) if len(b) > 5 else 0.0
     m.periodic_x, m.periodic_y, m.periodic_z = (int(bool(p)) for p in periodic)
     m.partition = int(partition)
     m.mapping = (MAP_BOX if warp is None else MAP_WARP) if mapping is None else int(mapping)

@@ -253,6 +253,41 @@ def test_snapshot_round_trip(tmp_path):
     t = h.read_snapshot(path)
     assert abs(t - g.time()) < 1e-15
     assert np.array_equal(h.field(), before)
+    # the restored context continues from the snapshot's time and interface offset
+    assert h.time() == t
+    g.step(1e-3, 2)
+    h.step(1e-3, 2)
+    assert rel_linf(h.field(), g.field()) <= 1e-13
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_snapshot_multi_rank_equals_single_rank(tmp_path, ranks):
+    """Collective snapshot: every rank writes its elements in place after rank 0
+    has created and sized the file; the file equals a single-rank write, and a
+    multi-rank read restores every rank's field."""
+    from paper_2008_04356_b200 import capi
+    mesh = T.mesh_spec([(2, 1.0, 0.0), (2, 1.0, 1.0), (2, 1.0, 0.0)], ny=6, nz=2, depth=1.0)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    one, many = str(tmp_path / "one.sdg"), str(tmp_path / "many.sdg")
+
+    def write(path):
+        def body(s):
+            s.set_initial_condition(0.0)
+            s.step(0.004, 2)
+            s.write_snapshot(path)
+            return s.local_element_ids(), s.field()
+        return body
+
+    def read(s):
+        t = s.read_snapshot(many)
+        return s.local_element_ids(), s.field(), t
+
+    capi.run_inproc(mesh, cfg, 1, write(one), hub="snap1")
+    parts = capi.run_inproc(mesh, cfg, ranks, write(many), hub=f"snap{ranks}")
+    assert open(one, "rb").read() == open(many, "rb").read()
+    back = capi.run_inproc(mesh, cfg, ranks, read, hub=f"snapr{ranks}")
+    for (ids, u), (ids2, u2, t) in zip(parts, back):
+        assert np.array_equal(ids, ids2) and np.array_equal(u, u2) and t == 0.008
 
 
 # ---------------------------------------------------------------- GPU vs the reference itself
@@ -405,3 +440,57 @@ def test_multi_wave_meshes_match_oracle(degree, nx, nyz):
     g.step(dt, 3)
     o.step(dt, 3)
     assert rel_linf(g.field(), o.field()) <= 1e-12
+
+
+# ---------------------------------------------------------------- RK-stage and interface entry points
+def test_rk_stages_equal_one_step_bitwise():
+    """sdg_rk_stage x5 (lsrk_step, lsrk.hpp:20-21) is bitwise sdg_step, and the
+    oracle's step agrees; stages out of order or at the wrong time are refused."""
+    from paper_2008_04356_b200 import capi
+    mesh = three_band(ny=4, nz=2, vg=0.7)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    a, b = gpu_solver(mesh, cfg), gpu_solver(mesh, cfg)
+    a.set_initial_condition(0.1)
+    b.set_initial_condition(0.1)
+    dt = a.suggest_dt(0.5)
+    for step in range(3):
+        a.step(dt)
+        t = b.time()
+        for s in range(5):
+            b.rk_stage(s, t, dt)
+        assert b.time() == a.time() and b.step_index() == a.step_index() == step + 1
+    assert np.array_equal(a.field(), b.field())
+    assert np.array_equal(a.register(), b.register())
+    assert a.total_rebuilds() == b.total_rebuilds()
+    with pytest.raises(T.ConfigError):
+        b.rk_stage(1, b.time(), dt)
+    with pytest.raises(T.ConfigError):
+        b.rk_stage(0, b.time() + dt, dt)
+    b.rk_stage(0, b.time(), dt)
+    with pytest.raises(T.ConfigError):
+        b.step(dt)  # an unfinished step
+
+
+@pytest.mark.parametrize("t", [0.0, 0.13, 0.5, 1.71])
+def test_update_interfaces_matches_oracle_and_reference(t):
+    """sdg_update_interfaces (solver.cpp:156-176): the device displacement / sigma of
+    every side context and the host long-double operators equal the oracle's, and
+    the operators are the reference library's build_mortar_operators bits."""
+    mesh = three_band(ny=4, nz=2, vg=0.7)
+    cfg = T.solver_config(3, T.NODES_GAUSS, mu=1e-3, case=T.density_wave())
+    g, o = gpu_solver(mesh, cfg), P.Oracle3D(mesh, cfg)
+    g.set_initial_condition(0.0)
+    o.set_initial_condition(0.0)
+    ops = g.update_interfaces(t)
+    o.compute_residual(t)  # the oracle updates its interfaces at the stage time
+    assert g.n_contexts() == o.n_contexts() == 4
+    for c in range(g.n_contexts()):
+        gi, oi = g.ctx_info(c), o.ctx_info(c)
+        assert gi == oi, (c, gi, oi)
+        if not gi["conforming"]:
+            f, bwd = P.oracle_mortar_ops(3, T.NODES_GAUSS, gi["sigma_side"])
+            assert np.array_equal(ops[c, :2], f) and np.array_equal(ops[c, 2:], bwd)
+            if P.ref_available():
+                rf, rb = P.ref_mortar_ops(3, T.NODES_GAUSS, gi["sigma_side"])
+                assert np.array_equal(ops[c, :2], rf) and np.array_equal(ops[c, 2:], rb)
+        assert np.array_equal(g.mapping(c), o.mapping(c))
