@@ -133,6 +133,16 @@ SDG_API int sdg_ctx_info(sdg_ctx* ctx, int ctx_id, long* out5, double* s_delta, 
 SDG_API int sdg_get_pairing(sdg_ctx* ctx, int role, int* ncols, int* cols);
 SDG_API int sdg_get_mapping(sdg_ctx* ctx, int ctx_id, int* m);
 
+/* Non-matching / obliquely sliding interfaces (BASELINE configs[1]; per-band ny / nz
+ * or vg_z in sdg_band_spec).  Their pairing is the pair of face-interval rows (y, z)
+ * recomputed on the device every stage; sdg_nc_rows reads back the device row of
+ * direction dir (0: y, 1: z) of the last stage: per mortar the A face and B face
+ * (faces[2k..]) and the sub-ranges (a_lo, a_hi, b_lo, b_hi) (ranges[4k..]), and the
+ * displacement of side B it was built for (delta).  faces / ranges may be NULL to
+ * query *n_out. */
+SDG_API int sdg_n_nc_interfaces(const sdg_ctx* ctx);
+SDG_API int sdg_nc_rows(sdg_ctx* ctx, int iface, int dir, long* n_out, long* faces, double* ranges, double* delta);
+
 /* The device pairing kernel on an arbitrary face set (same contract as
  * rebuild_index_arrays + build_schedule, partition.cpp:143-169). */
 SDG_API int sdg_pairing_device(int n_local, const long* faces, long n_par, long n_perp, const int* partner_ranks,

@@ -31,6 +31,7 @@ extern "C" {
 
 #define SDG_MAX_BANDS 16
 #define SDG_NVARS 5
+#define SDG_PT_MAX_MODES 8
 #define SDG_NGRAD 12 /* (v1, v2, v3, T) x (d/dx, d/dy, d/dz): g[3*q + dir] */
 
 /* Status codes of every C entry point (0 = success). The C++ facade maps
@@ -89,7 +90,16 @@ typedef struct {
    * see below), with `warp` the amplitude as a fraction of the element size. */
   int mapping;
   double warp;
+  /* Mortars of the sliding interfaces: SDG_MORTARS_AUTO uses the reference's
+   * (solver.cpp:156-526) wherever the face counts match and the slide is along y,
+   * and the tensor-product (non-matching) mortars otherwise; SDG_MORTARS_TENSOR
+   * routes every sliding interface through the tensor-product path (SDG_MAP_BOX),
+   * which at equal counts must reproduce the reference's mortars. */
+  int mortars;
+  int pad_;
 } sdg_mesh_spec;
+
+enum { SDG_MORTARS_AUTO = 0, SDG_MORTARS_TENSOR = 1 };
 
 /* SDG_MAP_WARP: a box point (x, y, z) of band b maps to
  *   X = x + A*hx*sp(tx)*s2(ty)*s2(tz),  Y = y + A*hy*sp(tx)*s2(tz),  Z = z + A*hz*sp(tx)*s2(ty)
@@ -133,6 +143,17 @@ typedef struct {
   /* swirl: rho = 2 + dw_alpha sin(pi dw_k[0] (x - dw_a[0] t)), v = (dw_a[0], sw_omega Z, -sw_omega Y),
    * p = dw_p0 + sw_omega^2 (Y^2 + Z^2): axisymmetric, so periodic under any rotation about x */
   double sw_omega;
+  /* Seeded perturbation added to the density of the case above (SURVEY §8d,
+   * BASELINE configs[1] and [3]): rho += pt_amp * sum_m pt_a[m] sin(2 pi k_m . xh + pt_phi[m]),
+   * xh = (c - pt_x0) / pt_len per direction with c the point x - pt_adv t (pt_coords 0)
+   * or its cylindrical coordinates about the x axis (x, theta = atan2(Y, Z), r) (pt_coords 1,
+   * annulus meshes: periodic across a sector seam).  Velocity and pressure are the
+   * case's, so with the case's uniform velocity as pt_adv the perturbed density wave /
+   * free stream stays an exact Euler solution.  pt_modes = 0: none. */
+  int pt_modes, pt_coords;
+  double pt_amp;
+  double pt_x0[3], pt_len[3], pt_adv[3];
+  double pt_k[SDG_PT_MAX_MODES][3], pt_a[SDG_PT_MAX_MODES], pt_phi[SDG_PT_MAX_MODES];
 } sdg_case;
 
 typedef struct {

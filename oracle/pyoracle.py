@@ -89,6 +89,8 @@ def oracle_lib():
                                     _ip, _ip, _ip, _lp, _ip, _ip, _ip]
         lib.orc_face_flux.argtypes = [C.POINTER(T.Gas), _dp, _dp, C.c_int, C.c_double, _dp, _dp, _dp]
         lib.orc_set_threads.argtypes = [C.c_int]
+        lib.orc_n_nc_interfaces.argtypes = [vp]
+        lib.orc_nc_rows.argtypes = [vp, C.c_int, C.c_int, _lp, _lp, _dp, _dp]
         _oracle_lib = lib
     return _oracle_lib
 
@@ -200,6 +202,19 @@ class Oracle3D:
         self._check(self.lib.orc_ctx_info(self.h, ctx, o, C.byref(sd), C.byref(sg)))
         return dict(iface=o[0], on_static=bool(o[1]), n_delta=o[2], conforming=bool(o[3]), n_faces=o[4],
                     s_delta=sd.value, sigma_side=sg.value)
+
+    def n_nc_interfaces(self):
+        return self.lib.orc_n_nc_interfaces(self.h)
+
+    def nc_rows(self, iface, direction):
+        """Rows of a non-matching interface at the last residual: faces, ranges, displacement."""
+        n, d = C.c_long(), C.c_double()
+        self._check(self.lib.orc_nc_rows(self.h, iface, direction, C.byref(n), None, None, C.byref(d)))
+        faces = np.zeros((n.value, 2), dtype=np.int64)
+        ranges = np.zeros((n.value, 4))
+        self._check(self.lib.orc_nc_rows(self.h, iface, direction, C.byref(n), faces.ctypes.data_as(_lp), _d(ranges),
+                                         C.byref(d)))
+        return faces, ranges, d.value
 
     def pairing(self, role):
         nc = C.c_int()

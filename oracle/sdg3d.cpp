@@ -13,6 +13,7 @@
 #include "sdg3d.h"
 
 #include <algorithm>
+#include <functional>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -743,7 +744,38 @@ static void face_flux_n(const double* um, const double* up, const double* n, dou
 // ---------------------------------------------------------------------------
 // Exact solutions / cases: proj/src/exact_solutions.cpp:7-35, cases.hpp:18-25.
 // ---------------------------------------------------------------------------
+// The seeded density perturbation (include/sdg_types.h sdg_case.pt_*):
+// A sum_m a_m sin(2 pi k_m . xh + phi_m), xh the advected point normalised per direction.
+static double perturbation(const sdg_case& cs, const double* x, double t) {
+  const double two_pi = 6.283185307179586476925286766559;
+  double c[3];
+  for (int d = 0; d < 3; ++d) c[d] = x[d] - cs.pt_adv[d] * t;
+  if (cs.pt_coords == 1) {  // (x, theta, r) about the x axis, theta measured from +Z towards +Y
+    const double th = std::atan2(c[1], c[2]), r = std::sqrt(c[1] * c[1] + c[2] * c[2]);
+    c[1] = th;
+    c[2] = r;
+  }
+  double arg[SDG_PT_MAX_MODES];
+  double acc = 0.0;
+  for (int m = 0; m < cs.pt_modes; ++m) {
+    arg[m] = 0.0;
+    for (int d = 0; d < 3; ++d) arg[m] += cs.pt_k[m][d] * ((c[d] - cs.pt_x0[d]) / cs.pt_len[d]);
+    acc += cs.pt_a[m] * std::sin(two_pi * arg[m] + cs.pt_phi[m]);
+  }
+  return cs.pt_amp * acc;
+}
+
+static State eval_base(const sdg_case& cs, const double* x, double t, const Gas& g);
+// The case state plus its seeded density perturbation (velocity and pressure kept).
 static State eval_case(const sdg_case& cs, const double* x, double t, const Gas& g) {
+  State u = eval_base(cs, x, t, g);
+  if (cs.pt_modes <= 0) return u;
+  if (cs.pt_modes > SDG_PT_MAX_MODES) throw ConfigError("perturbation: 0..8 modes");
+  const double v1 = u[1] / u[0], v2 = u[2] / u[0], v3 = u[3] / u[0];
+  return from_primitive(u[0] + perturbation(cs, x, t), v1, v2, v3, pressure(u.data(), g), g);
+}
+
+static State eval_base(const sdg_case& cs, const double* x, double t, const Gas& g) {
   const double pi = 3.14159265358979323846;
   switch (cs.kind) {
     case SDG_CASE_FREESTREAM:
@@ -800,6 +832,8 @@ static State eval_case(const sdg_case& cs, const double* x, double t, const Gas&
 struct Band {
   double x_lo, x_hi, hx, hy, hz, vg;
   int nx, off;
+  int ny = 0, nz = 0;  // per-band counts (BandSpec::ny, mesh.hpp:16; nz its 3D analogue)
+  double vgz = 0.0;    // translation along +z (oblique sliding)
 };
 struct Iface {
   int left, right;
@@ -810,6 +844,23 @@ struct Iface {
 };
 struct Elem {
   int band, ix, iy, iz;
+};
+// Non-matching / obliquely sliding interface (BASELINE configs[1]): side A = the
+// left band's x+ faces, B = the right band's x- faces, B displaced by
+// (vy_rel, vz_rel) t.  Mortars: every pair of a y-row interval and a z-row
+// interval (intervals() above), with the sub-range operators of both sides.
+struct NcIface {
+  int left = 0, right = 0;
+  long nfy[2] = {0, 0}, nfz[2] = {0, 0};
+  double ly[2] = {0, 0}, lz[2] = {0, 0};
+  double vy_rel = 0.0, vz_rel = 0.0;
+  std::vector<int> elem[2], side[2];  // per side, face fy * nfz + fz -> (element, side)
+  double dy_base = 0.0, dz_base = 0.0;
+  // current stage
+  double dy = 0.0, dz = 0.0;
+  std::vector<Interval> rows[2];
+  std::vector<double> F[2][2], B[2][2];  // [side][dir]: per row n x n
+  std::vector<double> u[2], g[2];        // mortar traces / gradients per side
 };
 struct InteriorFace {
   int em, ep, dir;
@@ -868,6 +919,7 @@ struct orc_solver {
   std::vector<InteriorFace> interior;
   std::vector<BoundaryFace> dirichlet;
   std::vector<std::vector<SlidingFace>> sliding;
+  std::vector<NcIface> ncs;
   std::vector<Ctx> ctxs;
   std::vector<int> static_ids, moving_ids;
   Role statics, movings;
@@ -892,7 +944,7 @@ struct orc_solver {
   int nz() const { return spec.nz; }
   int ny() const { return spec.ny; }
   long gid(int b, int ix, int iy, int iz) const {
-    return bands[b].off + (static_cast<long>(ix) * spec.ny + iy) * spec.nz + iz;
+    return bands[b].off + (static_cast<long>(ix) * bands[b].ny + iy) * bands[b].nz + iz;
   }
   size_t node(int e, int i, int j, int k) const { return ((static_cast<size_t>(e) * n + i) * n + j) * n + k; }
   double* tr(int e, int side) { return trace.data() + (static_cast<size_t>(e) * 6 + side) * n2 * NV; }
@@ -1005,7 +1057,7 @@ struct orc_solver {
     if (!curved) {
       x[0] = ox + 0.5 * (xi + 1.0) * b.hx;
       x[1] = oy + 0.5 * (eta + 1.0) * b.hy + b.vg * t;
-      x[2] = oz + 0.5 * (zeta + 1.0) * b.hz;
+      x[2] = oz + 0.5 * (zeta + 1.0) * b.hz + b.vgz * t;
       return;
     }
     // SDG_MAP_WARP (include/sdg_types.h).
@@ -1099,6 +1151,9 @@ struct orc_solver {
   void dirichlet_flux(double t_stage);
   void apply_faces(double* out);
   void residual(double t_stage, const double* u, double* out);
+  void nc_update(double t_stage);
+  void nc_lift();
+  void nc_flux();
   void check_admissible(const double* u) const;
   void step(double dt);
   double suggest_dt(double cfl) const;
@@ -1142,15 +1197,22 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
     bd.x_hi = (b == nb - 1) ? s.x0 + s.width : s.x0 + s.width * acc / frac_sum;
     x = bd.x_hi;
     bd.nx = s.bands[b].nx;
+    bd.ny = s.bands[b].ny > 0 ? s.bands[b].ny : s.ny;
+    bd.nz = s.bands[b].nz > 0 ? s.bands[b].nz : s.nz;
+    if (s.bands[b].ny < 0 || s.bands[b].nz < 0) throw ConfigError("band ny / nz must be >= 0");
     bd.hx = (bd.x_hi - bd.x_lo) / bd.nx;
-    bd.hy = s.height / s.ny;
-    bd.hz = s.depth / s.nz;
+    bd.hy = s.height / bd.ny;
+    bd.hz = s.depth / bd.nz;
     bd.vg = s.bands[b].vg_y;
+    bd.vgz = s.bands[b].vg_z;
     bd.off = off;
-    off += bd.nx * s.ny * s.nz;
-    if (bd.vg != 0.0 && bd.vg < 0.0) throw ConfigError("moving bands must translate toward +y");
+    off += bd.nx * bd.ny * bd.nz;
+    if (bd.vg < 0.0 || bd.vgz < 0.0) throw ConfigError("moving bands must translate toward +y / +z");
     if (bd.vg != 0.0 && !s.periodic_y)
       throw ConfigError("a moving band requires periodicity along the movement direction");
+    if (bd.vgz != 0.0 && !s.periodic_z) throw ConfigError("a band moving along z requires periodicity along z");
+    if ((bd.ny != s.ny || bd.nz != s.nz || bd.vgz != 0.0 || s.mortars != 0) && s.mapping != SDG_MAP_BOX)
+      throw ConfigError("per-band ny / nz and sliding along z need affine hexahedra (SDG_MAP_BOX)");
   }
   const int n_pairs = s.periodic_x ? nb : nb - 1;
   for (int p = 0; p < n_pairs; ++p) {
@@ -1158,6 +1220,28 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
     if (nb == 1 && left == right) continue;
     const Band& bl = bands[left];
     const Band& br = bands[right];
+    if (bl.ny != br.ny || bl.nz != br.nz || bl.vgz != 0.0 || br.vgz != 0.0 || s.mortars == SDG_MORTARS_TENSOR) {
+      if (bl.ny == br.ny && bl.nz == br.nz && bl.vg == br.vg && bl.vgz == br.vgz) continue;
+      NcIface f;
+      f.left = left;
+      f.right = right;
+      f.nfy[0] = bl.ny;
+      f.nfz[0] = bl.nz;
+      f.nfy[1] = br.ny;
+      f.nfz[1] = br.nz;
+      f.ly[0] = bl.hy;
+      f.lz[0] = bl.hz;
+      f.ly[1] = br.hy;
+      f.lz[1] = br.hz;
+      f.vy_rel = br.vg - bl.vg;
+      f.vz_rel = br.vgz - bl.vgz;
+      for (int sd = 0; sd < 2; ++sd) {
+        f.elem[sd].assign(f.nfy[sd] * f.nfz[sd], -1);
+        f.side[sd].assign(f.nfy[sd] * f.nfz[sd], -1);
+      }
+      ncs.push_back(std::move(f));
+      continue;
+    }
     if (bl.vg == br.vg) continue;
     if (bl.vg != 0.0 && br.vg != 0.0) throw ConfigError("sliding interface requires one static side");
     Iface f;
@@ -1165,8 +1249,8 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
     f.right = right;
     f.static_is_left = (bl.vg == 0.0);
     f.l_par = bl.hy;
-    f.n_faces = s.ny;
-    f.n_perp = s.nz;
+    f.n_faces = bl.ny;
+    f.n_perp = bl.nz;
     f.vg_rel = f.static_is_left ? br.vg : bl.vg;
     ifaces.push_back(f);
   }
@@ -1174,8 +1258,8 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
   // Elements in global id order (single rank owns everything).
   for (int b = 0; b < nb; ++b)
     for (int ix = 0; ix < bands[b].nx; ++ix)
-      for (int iy = 0; iy < s.ny; ++iy)
-        for (int iz = 0; iz < s.nz; ++iz) elems.push_back({b, ix, iy, iz});
+      for (int iy = 0; iy < bands[b].ny; ++iy)
+        for (int iz = 0; iz < bands[b].nz; ++iz) elems.push_back({b, ix, iy, iz});
   const int ne = static_cast<int>(elems.size());
 
   // Faces (face_topology.cpp:55-150): y and z within the band (periodic or
@@ -1185,18 +1269,18 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
     const Elem& el = elems[e];
     const Band& bd = bands[el.band];
     // y
-    if (el.iy + 1 == s.ny && !s.periodic_y) dirichlet.push_back({e, YP});
-    else interior.push_back({e, static_cast<int>(gid(el.band, el.ix, (el.iy + 1) % s.ny, el.iz)), 1,
-                             (el.iy + 1 == s.ny) ? 1 : 0});
+    if (el.iy + 1 == bd.ny && !s.periodic_y) dirichlet.push_back({e, YP});
+    else interior.push_back({e, static_cast<int>(gid(el.band, el.ix, (el.iy + 1) % bd.ny, el.iz)), 1,
+                             (el.iy + 1 == bd.ny) ? 1 : 0});
     if (el.iy == 0 && !s.periodic_y) dirichlet.push_back({e, YM});
     // z
-    if (el.iz + 1 == s.nz && !s.periodic_z) dirichlet.push_back({e, ZP});
-    else interior.push_back({e, static_cast<int>(gid(el.band, el.ix, el.iy, (el.iz + 1) % s.nz)), 2});
+    if (el.iz + 1 == bd.nz && !s.periodic_z) dirichlet.push_back({e, ZP});
+    else interior.push_back({e, static_cast<int>(gid(el.band, el.ix, el.iy, (el.iz + 1) % bd.nz)), 2});
     if (el.iz == 0 && !s.periodic_z) dirichlet.push_back({e, ZM});
     // x
     for (const bool plus : {true, false}) {
       int ob = -1, oix = 0;
-      int iface = -1;
+      int iface = -1, nci = -1;
       bool exists = true;
       if (plus && el.ix + 1 < bd.nx) {
         ob = el.band;
@@ -1219,6 +1303,8 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
             const int right = plus ? other : el.band;
             for (size_t i = 0; i < ifaces.size(); ++i)
               if (ifaces[i].left == left && ifaces[i].right == right) iface = static_cast<int>(i);
+            for (size_t i = 0; i < ncs.size(); ++i)
+              if (ncs[i].left == left && ncs[i].right == right) nci = static_cast<int>(i);
             ob = other;
             oix = plus ? 0 : bands[other].nx - 1;
           }
@@ -1230,6 +1316,13 @@ void orc_solver::build(const sdg_mesh_spec& s, const sdg_solver_config& cfg) {
       }
       if (iface >= 0) {
         sliding[iface].push_back({e, plus ? XP : XM, el.iy, el.iz});
+        continue;
+      }
+      if (nci >= 0) {
+        NcIface& f = ncs[nci];
+        const int sd = plus ? 0 : 1;  // A: the left band's x+ faces
+        f.elem[sd][el.iy * f.nfz[sd] + el.iz] = e;
+        f.side[sd][el.iy * f.nfz[sd] + el.iz] = plus ? XP : XM;
         continue;
       }
       if (plus) interior.push_back({e, static_cast<int>(gid(ob, oix, el.iy, el.iz)), 0});
@@ -1672,6 +1765,7 @@ void orc_solver::run_lifting(double t_stage, const double* u) {
       mortar_to_face(c, n, data, f, 4, lout);
     }
   }
+  nc_lift();
   for (const auto& df : dirichlet) {
     double* lout = lf(df.e, df.side);
     for (int p = 0; p < n; ++p)
@@ -1856,7 +1950,8 @@ void orc_solver::interior_flux() {
     const int sm = 2 * f.dir + 1, sp = 2 * f.dir;
     const double* um = tr(f.em, sm);
     const double* up = tr(f.ep, sp);
-    const double vg_n = f.dir == 1 ? bands[elems[f.em].band].vg : 0.0;
+    const Band& bm = bands[elems[f.em].band];
+    const double vg_n = f.dir == 1 ? bm.vg : (f.dir == 2 ? bm.vgz : 0.0);
     double* om = ff(f.em, sm);
     double* op = ff(f.ep, sp);
     for (int k = 0; k < n2; ++k) {
@@ -1899,7 +1994,7 @@ void orc_solver::volume(const double* u, double* out) {
 #pragma omp for schedule(static)
     for (int e = 0; e < ne; ++e) {
       const Band& b = bands[elems[e].band];
-      const double vg[3] = {0.0, annulus ? 0.0 : b.vg, 0.0};
+      const double vg[3] = {0.0, annulus ? 0.0 : b.vg, annulus ? 0.0 : b.vgz};
       const double jac = 0.125 * b.hx * b.hy * b.hz;
       const double sjx = 0.25 * b.hy * b.hz, sjy = 0.25 * b.hx * b.hz, sjz = 0.25 * b.hx * b.hy;
       for (int nd = 0; nd < n3; ++nd) {
@@ -2008,7 +2103,8 @@ void orc_solver::dirichlet_flux(double t_stage) {
     double* o = ff(df.e, df.side);
     const int dir = df.side / 2;
     const bool plus = (df.side % 2) == 1;
-    const double vg_n = dir == 1 ? bands[elems[df.e].band].vg : 0.0;
+    const Band& bd = bands[elems[df.e].band];
+    const double vg_n = dir == 1 ? bd.vg : (dir == 2 ? bd.vgz : 0.0);
     for (int p = 0; p < n; ++p)
       for (int q = 0; q < n; ++q) {
         const int k = p * n + q;
@@ -2072,13 +2168,122 @@ void orc_solver::residual(double t_stage, const double* u, double* out) {
   prolong(u);
   fill_mortar_solution();
   exchange_solution();
+  nc_update(t_stage);
   if (lifting) run_lifting(t_stage, u);
   interior_flux();
   volume(u, out);
   mortar_flux();
   mortar_apply();
+  nc_flux();
   dirichlet_flux(t_stage);
   apply_faces(out);
+}
+
+// ---------------------------------------------------------------------------
+// Non-matching / oblique interfaces: the reference's mortar chain (fill
+// solver.cpp:234-252, lifting mean :597-727, flux :442-479, apply :495-526) on
+// the tensor-product mortars of a y row and a z row of face intervals.
+// ---------------------------------------------------------------------------
+// (Fy x Fz) applied to one face's n x n x nc block: out[k][l] = sum_ij Fy[k][i] Fz[l][j] in[i][j].
+static void tensor_apply(const double* fy, const double* fz, int n, const double* in, double* out, int nc) {
+  for (int k = 0; k < n; ++k)
+    for (int l = 0; l < n; ++l)
+      for (int c = 0; c < nc; ++c) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) acc += fy[k * n + i] * fz[l * n + j] * in[(i * n + j) * nc + c];
+        out[(k * n + l) * nc + c] = acc;
+      }
+}
+
+// Displacement, rows and operators of the stage; the mortar traces of both sides.
+void orc_solver::nc_update(double t_stage) {
+  for (auto& f : ncs) {
+    f.dy = f.dy_base + f.vy_rel * (t_stage - time);
+    f.dz = f.dz_base + f.vz_rel * (t_stage - time);
+    f.rows[0] = intervals(f.nfy[0], f.nfy[1], f.ly[0], f.dy);
+    f.rows[1] = intervals(f.nfz[0], f.nfz[1], f.lz[0], f.dz);
+    for (int d = 0; d < 2; ++d)
+      for (int sd = 0; sd < 2; ++sd) {
+        const size_t m = f.rows[d].size();
+        f.F[sd][d].assign(m * n2, 0.0);
+        f.B[sd][d].assign(m * n2, 0.0);
+        for (size_t k = 0; k < m; ++k) {
+          const double* r = f.rows[d][k].r;
+          subrange_ops(ns, r[2 * sd], r[2 * sd + 1], f.F[sd][d].data() + k * n2, f.B[sd][d].data() + k * n2);
+        }
+      }
+    const size_t my = f.rows[0].size(), mz = f.rows[1].size();
+    for (int sd = 0; sd < 2; ++sd) {
+      f.u[sd].assign(my * mz * n2 * NV, 0.0);
+      for (size_t ky = 0; ky < my; ++ky)
+        for (size_t kz = 0; kz < mz; ++kz) {
+          const long fy = sd ? f.rows[0][ky].fb : f.rows[0][ky].fa, fz = sd ? f.rows[1][kz].fb : f.rows[1][kz].fa;
+          const size_t face = fy * f.nfz[sd] + fz;
+          tensor_apply(f.F[sd][0].data() + ky * n2, f.F[sd][1].data() + kz * n2, n, tr(f.elem[sd][face], f.side[sd][face]),
+                       f.u[sd].data() + (ky * mz + kz) * n2 * NV, NV);
+        }
+    }
+  }
+}
+
+// Mortar data back onto both sides' faces (the sum over each face's mortars).
+static void nc_project(const NcIface& f, int n, const std::vector<double>& mortar, int nc,
+                       const std::function<double*(int, size_t)>& face_out) {
+  const int n2 = n * n;
+  const size_t my = f.rows[0].size(), mz = f.rows[1].size();
+  std::vector<double> tmp(static_cast<size_t>(n2) * nc);
+  for (int sd = 0; sd < 2; ++sd) {
+    for (size_t face = 0; face < static_cast<size_t>(f.nfy[sd] * f.nfz[sd]); ++face)
+      std::fill_n(face_out(sd, face), n2 * nc, 0.0);
+    for (size_t ky = 0; ky < my; ++ky)
+      for (size_t kz = 0; kz < mz; ++kz) {
+        const long fy = sd ? f.rows[0][ky].fb : f.rows[0][ky].fa, fz = sd ? f.rows[1][kz].fb : f.rows[1][kz].fa;
+        tensor_apply(f.B[sd][0].data() + ky * n2, f.B[sd][1].data() + kz * n2, n,
+                     mortar.data() + (ky * mz + kz) * n2 * nc, tmp.data(), nc);
+        double* o = face_out(sd, fy * f.nfz[sd] + fz);
+        for (int q = 0; q < n2 * nc; ++q) o[q] += tmp[q];
+      }
+  }
+}
+
+// Lifting mean of the primitives at the mortar nodes, back onto both sides.
+void orc_solver::nc_lift() {
+  for (auto& f : ncs) {
+    const size_t nodes = f.u[0].size() / NV;
+    std::vector<double> lm(nodes * 4);
+    for (size_t q = 0; q < nodes; ++q) {
+      double a[4], b[4];
+      prim4(f.u[0].data() + q * NV, gas, a);
+      prim4(f.u[1].data() + q * NV, gas, b);
+      for (int c = 0; c < 4; ++c) lm[q * 4 + c] = 0.5 * (a[c] + b[c]);
+    }
+    nc_project(f, n, lm, 4, [&](int sd, size_t face) { return lf(f.elem[sd][face], f.side[sd][face]); });
+  }
+}
+
+// Two-sided Roe + central viscous flux at the mortar nodes (normal +x, vg_n = 0,
+// A on the minus side), back onto both sides.
+void orc_solver::nc_flux() {
+  for (auto& f : ncs) {
+    const size_t my = f.rows[0].size(), mz = f.rows[1].size(), nodes = my * mz * n2;
+    if (lifting)
+      for (int sd = 0; sd < 2; ++sd) {
+        f.g[sd].assign(nodes * NG, 0.0);
+        for (size_t ky = 0; ky < my; ++ky)
+          for (size_t kz = 0; kz < mz; ++kz) {
+            const long fy = sd ? f.rows[0][ky].fb : f.rows[0][ky].fa, fz = sd ? f.rows[1][kz].fb : f.rows[1][kz].fa;
+            const size_t face = fy * f.nfz[sd] + fz;
+            tensor_apply(f.F[sd][0].data() + ky * n2, f.F[sd][1].data() + kz * n2, n,
+                         gt(f.elem[sd][face], f.side[sd][face]), f.g[sd].data() + (ky * mz + kz) * n2 * NG, NG);
+          }
+      }
+    std::vector<double> fl(nodes * NV);
+    for (size_t q = 0; q < nodes; ++q)
+      face_flux(f.u[0].data() + q * NV, f.u[1].data() + q * NV, 0, 0.0, lifting ? f.g[0].data() + q * NG : nullptr,
+                lifting ? f.g[1].data() + q * NG : nullptr, gas, fl.data() + q * NV);
+    nc_project(f, n, fl, NV, [&](int sd, size_t face) { return ff(f.elem[sd][face], f.side[sd][face]); });
+  }
 }
 
 // check_admissible (solver.cpp:892-906).
@@ -2126,6 +2331,15 @@ void orc_solver::step(double dt) {
   }
   time += dt;
   step_index++;
+  for (auto& f : ncs) {  // both directions of an oblique slide, wrapped like delta_base
+    f.dy_base += f.vy_rel * dt;
+    f.dz_base += f.vz_rel * dt;
+    const double py = f.ly[0] * static_cast<double>(f.nfy[0]), pz = f.lz[0] * static_cast<double>(f.nfz[0]);
+    while (f.dy_base >= py) f.dy_base -= py;
+    while (f.dy_base < 0.0) f.dy_base += py;
+    while (f.dz_base >= pz) f.dz_base -= pz;
+    while (f.dz_base < 0.0) f.dz_base += pz;
+  }
   for (auto& c : ctxs) {
     const Iface& f = ifaces[c.iface];
     c.delta_base += f.vg_rel * dt;
@@ -2142,7 +2356,7 @@ double orc_solver::suggest_dt(double cfl) const {
   double dt = std::numeric_limits<double>::max();
   for (size_t e = 0; e < elems.size(); ++e) {
     const Band& b = bands[elems[e].band];
-    const double vg[3] = {0.0, annulus ? 0.0 : b.vg, 0.0};
+    const double vg[3] = {0.0, annulus ? 0.0 : b.vg, annulus ? 0.0 : b.vgz};
     double lmax = 0.0;
     for (int nd = 0; nd < n3; ++nd) {
       const double* s = field.data() + (e * n3 + nd) * NV;
@@ -2229,6 +2443,10 @@ int orc_set_initial_condition(orc_solver* s, double t0) {
       c.delta_base = s->ifaces[c.iface].vg_rel * t0;
       c.topo_valid = false;
     }
+    for (auto& f : s->ncs) {
+      f.dy_base = f.vy_rel * t0;
+      f.dz_base = f.vz_rel * t0;
+    }
     std::fill(s->reg.begin(), s->reg.end(), 0.0);
   });
 }
@@ -2267,6 +2485,7 @@ int orc_compute_gradients(orc_solver* s, double t_stage, const double* u, double
     s->prolong(u);
     s->fill_mortar_solution();
     s->exchange_solution();
+    s->nc_update(t_stage);
     s->run_lifting(t_stage, u);
     std::copy(s->grad.begin(), s->grad.end(), grad);
   });
@@ -2380,6 +2599,23 @@ int orc_mortar_ops(int degree, int kind, double sigma, double* fwd, double* bwd)
 }
 int orc_subrange_ops(int degree, int kind, double lo, double hi, double* fwd, double* bwd) {
   return guard(nullptr, [&] { subrange_ops(Nodes(degree, kind), lo, hi, fwd, bwd); });
+}
+int orc_n_nc_interfaces(const orc_solver* s) { return static_cast<int>(s->ncs.size()); }
+int orc_nc_rows(const orc_solver* s, int iface, int dir, long* n_out, long* faces, double* ranges, double* delta) {
+  return guard(const_cast<orc_solver*>(s), [&] {
+    if (iface < 0 || iface >= static_cast<int>(s->ncs.size()) || dir < 0 || dir > 1)
+      throw ConfigError("no such non-matching interface / direction");
+    const NcIface& f = s->ncs[iface];
+    const auto& rows = f.rows[dir];
+    *n_out = static_cast<long>(rows.size());
+    if (delta) *delta = dir == 0 ? f.dy : f.dz;
+    if (!faces || !ranges) return;
+    for (size_t k = 0; k < rows.size(); ++k) {
+      faces[2 * k] = rows[k].fa;
+      faces[2 * k + 1] = rows[k].fb;
+      for (int c = 0; c < 4; ++c) ranges[4 * k + c] = rows[k].r[c];
+    }
+  });
 }
 int orc_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges) {
   return guard(nullptr, [&] {

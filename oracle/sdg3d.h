@@ -80,6 +80,10 @@ int orc_mortar_ops(int degree, int kind, double sigma, double* fwd, double* bwd)
  * sub-range [lo, hi] (n*n each) and the mortars of one periodic face row,
  * faces 2 and ranges 4 per mortar (see include/sdg_gpu.h sdg_mortar_intervals). */
 int orc_subrange_ops(int degree, int kind, double lo, double hi, double* fwd, double* bwd);
+/* Non-matching / oblique interfaces: the rows (y: dir 0, z: dir 1) of the last
+ * residual evaluation, as sdg_nc_rows on the device. */
+int orc_n_nc_interfaces(const orc_solver* s);
+int orc_nc_rows(const orc_solver* s, int iface, int dir, long* n_out, long* faces, double* ranges, double* delta);
 int orc_mortar_intervals(long n_a, long n_b, double l_a, double delta, long* n_out, long* faces, double* ranges);
 int orc_displacement(double delta, double l_par, long n_faces, double* d, long* n_delta,
                      double* s_delta);

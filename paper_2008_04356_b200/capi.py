@@ -76,6 +76,8 @@ def lib():
         L.sdg_n_contexts.argtypes = [_vp]
         L.sdg_ctx_info.argtypes = [_vp, C.c_int, _lp, _dp, _dp]
         L.sdg_get_pairing.argtypes = [_vp, C.c_int, _ip, _ip]
+        L.sdg_n_nc_interfaces.argtypes = [_vp]
+        L.sdg_nc_rows.argtypes = [_vp, C.c_int, C.c_int, _lp, _lp, _dp, _dp]
         L.sdg_get_mapping.argtypes = [_vp, C.c_int, _ip]
         L.sdg_pairing_device.argtypes = [C.c_int, _lp, C.c_long, C.c_long, _ip, C.c_long, C.c_int, C.c_int,
                                          C.c_int, _ip, _ip, _ip, _lp, _ip, _ip, _ip]
@@ -113,6 +115,7 @@ EXPORTED = [
     "sdg_update_interfaces", "sdg_compute_residual",
     "sdg_compute_residual_host", "sdg_compute_gradients_host", "sdg_suggest_dt", "sdg_time",
     "sdg_total_rebuilds", "sdg_n_contexts", "sdg_ctx_info", "sdg_get_pairing", "sdg_get_mapping",
+    "sdg_n_nc_interfaces", "sdg_nc_rows",
     "sdg_pairing_device", "sdg_plan_json", "sdg_metrics_host", "sdg_subrange_ops",
     "sdg_mortar_intervals", "sdg_mortar_intervals_device",
     "sdg_interface_project_device", "sdg_interface_flux_device", "sdg_interface_lift_device",
@@ -256,6 +259,20 @@ class RankSolver:
         self._check(self.lib.sdg_ctx_info(self.h, ctx, o, C.byref(sd), C.byref(sg)))
         return dict(iface=o[0], on_static=bool(o[1]), n_delta=o[2], conforming=bool(o[3]), n_faces=o[4],
                     s_delta=sd.value, sigma_side=sg.value)
+
+    def n_nc_interfaces(self) -> int:
+        return self.lib.sdg_n_nc_interfaces(self.h)
+
+    def nc_rows(self, iface: int, direction: int):
+        """Device rows of a non-matching interface at the last stage: faces [M, 2]
+        (A face, B face), ranges [M, 4] (a_lo, a_hi, b_lo, b_hi), displacement."""
+        n, d = C.c_long(), C.c_double()
+        self._check(self.lib.sdg_nc_rows(self.h, iface, direction, C.byref(n), None, None, C.byref(d)))
+        faces = np.zeros((n.value, 2), dtype=np.int64)
+        ranges = np.zeros((n.value, 4))
+        self._check(self.lib.sdg_nc_rows(self.h, iface, direction, C.byref(n), faces.ctypes.data_as(_lp), _d(ranges),
+                                         C.byref(d)))
+        return faces, ranges, d.value
 
     def pairing(self, role: int) -> np.ndarray:
         nc = C.c_int()

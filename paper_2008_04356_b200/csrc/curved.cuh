@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
     const double ir = rcp_nr(u[0]);
     const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
     const double p = pressure(u, ir, C.gas);
-    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, 0.0};  // annulus: grid velocity enters through V^d below
+    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, ROT ? 0.0 : B.vgz};  // annulus: grid velocity enters through V^d below
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       F[d][0] = u[0] * vv[d];
@@ -881,7 +881,7 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
       double nrm[3], vgn;
       const int dir = s >> 1;
       if constexpr (AFF) {
-        vgn = dir == 1 ? B.vg : 0.0;
+        vgn = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
       } else {
         face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
       }
@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
     const double ir = rcp_nr(u[0]);
     const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
     const double p = pressure(u, ir, C.gas);
-    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, 0.0};  // annulus: grid velocity enters through V^d below
+    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, ROT ? 0.0 : B.vgz};  // annulus: grid velocity enters through V^d below
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       F[d][0] = u[0] * vv[d];
@@ -1147,19 +1147,6 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
   }
 }
 
-template <int N1>
-bool gradient_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  if constexpr (N1 % 2 != 0) {
-    return false;
-  } else {
-    using D = CB<N1, false, true>;
-    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    set_smem_checked(k_gradient_bulk<N1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-    k_gradient_bulk<N1, false, true><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
-    check_launch("k_gradient_bulk (affine)");
-    return true;
-  }
-}
 template <int N1>
 bool update_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if constexpr (N1 % 2 != 0) {

@@ -33,10 +33,12 @@ MeshGeom::MeshGeom(const sdg_mesh_spec& s) : spec(s) {
   for (int b = 0; b < s.n_bands; ++b) {
     if (s.bands[b].nx < 1) throw ConfigError("band element count nx must be >= 1");
     if (!(s.bands[b].width_frac > 0.0)) throw ConfigError("band width fraction must be positive");
+    if (s.bands[b].ny < 0 || s.bands[b].nz < 0) throw ConfigError("band ny / nz must be >= 0 (0 = the mesh-wide count)");
     frac_sum += s.bands[b].width_frac;
   }
   const int nb = s.n_bands;
   double x = s.x0, acc = 0.0;
+  bool uniform = true;
   for (int b = 0; b < nb; ++b) {
     BandGeom g{};
     g.x_lo = x;
@@ -44,46 +46,80 @@ MeshGeom::MeshGeom(const sdg_mesh_spec& s) : spec(s) {
     g.x_hi = (b == nb - 1) ? s.x0 + s.width : s.x0 + s.width * acc / frac_sum;
     x = g.x_hi;
     g.nx = s.bands[b].nx;
+    g.ny = s.bands[b].ny > 0 ? s.bands[b].ny : s.ny;
+    g.nz = s.bands[b].nz > 0 ? s.bands[b].nz : s.nz;
     g.hx = (g.x_hi - g.x_lo) / g.nx;
-    g.hy = s.height / s.ny;
-    g.hz = s.depth / s.nz;
+    g.hy = s.height / g.ny;
+    g.hz = s.depth / g.nz;
     g.vg = s.bands[b].vg_y;
+    g.vgz = s.bands[b].vg_z;
     g.off = n_elements;
-    g.n_elements = static_cast<long>(g.nx) * s.ny * s.nz;
+    g.n_elements = static_cast<long>(g.nx) * g.ny * g.nz;
     n_elements += g.n_elements;
-    if (g.vg < 0.0) throw ConfigError("moving bands must translate toward +y");
+    if (g.vg < 0.0 || g.vgz < 0.0) throw ConfigError("moving bands must translate toward +y / +z");
+    if (!std::isfinite(g.vg) || !std::isfinite(g.vgz)) throw ConfigError("band velocities must be finite");
     if (g.vg != 0.0 && !s.periodic_y)
       throw ConfigError("a moving band requires periodicity along the movement direction");
+    if (g.vgz != 0.0 && !s.periodic_z)
+      throw ConfigError("a band moving along z requires periodicity along z");
+    uniform = uniform && g.ny == s.ny && g.nz == s.nz && g.vgz == 0.0;
     bands.push_back(g);
   }
+  if (s.mortars != SDG_MORTARS_AUTO && s.mortars != SDG_MORTARS_TENSOR) throw ConfigError("unknown mortar kind");
+  if ((!uniform || s.mortars == SDG_MORTARS_TENSOR) && s.mapping != SDG_MAP_BOX)
+    throw ConfigError("per-band ny / nz, sliding along z and tensor-product mortars need affine hexahedra (SDG_MAP_BOX)");
   const int n_pairs = s.periodic_x ? nb : nb - 1;
   for (int p = 0; p < n_pairs; ++p) {
     const int l = p, r = (p + 1) % nb;
     if (nb == 1) continue;
-    if (bands[l].vg == bands[r].vg) continue;
-    if (bands[l].vg != 0.0 && bands[r].vg != 0.0)
+    const BandGeom &L = bands[l], &R = bands[r];
+    const bool matching = L.ny == R.ny && L.nz == R.nz;
+    if (!matching || L.vgz != 0.0 || R.vgz != 0.0 || s.mortars == SDG_MORTARS_TENSOR) {
+      // Non-matching and / or oblique: the tensor-product mortar path.
+      if (matching && L.vg == R.vg && L.vgz == R.vgz) continue;  // conforming, moving together
+      NcIfaceGeom f{};
+      f.left = l;
+      f.right = r;
+      f.nfy[0] = L.ny;
+      f.nfz[0] = L.nz;
+      f.nfy[1] = R.ny;
+      f.nfz[1] = R.nz;
+      f.ly[0] = L.hy;
+      f.lz[0] = L.hz;
+      f.ly[1] = R.hy;
+      f.lz[1] = R.hz;
+      f.vy_rel = R.vg - L.vg;
+      f.vz_rel = R.vgz - L.vgz;
+      nc_ifaces.push_back(f);
+      continue;
+    }
+    if (L.vg == R.vg) continue;
+    if (L.vg != 0.0 && R.vg != 0.0)
       throw ConfigError("sliding interface requires one static side");
     IfaceGeom f{};
     f.left = l;
     f.right = r;
-    f.static_is_left = bands[l].vg == 0.0;
-    f.l_par = bands[l].hy;
-    f.n_faces = s.ny;
-    f.n_perp = s.nz;
-    f.vg_rel = f.static_is_left ? bands[r].vg : bands[l].vg;
+    f.static_is_left = L.vg == 0.0;
+    f.l_par = L.hy;
+    f.n_faces = L.ny;
+    f.n_perp = L.nz;
+    f.vg_rel = f.static_is_left ? R.vg : L.vg;
     ifaces.push_back(f);
   }
   if (ifaces.size() * 2 > static_cast<size_t>(kMaxCtx)) throw ConfigError("at most 4 sliding interfaces");
+  if (nc_ifaces.size() > static_cast<size_t>(kMaxNcIfaces))
+    throw ConfigError("at most " + std::to_string(kMaxNcIfaces) + " non-matching interfaces");
 }
 
 void MeshGeom::locate(long g, int& b, int& ix, int& iy, int& iz) const {
   b = 0;
   while (b + 1 < static_cast<int>(bands.size()) && g >= bands[b + 1].off) ++b;
   long loc = g - bands[b].off;
-  iz = static_cast<int>(loc % spec.nz);
-  loc /= spec.nz;
-  iy = static_cast<int>(loc % spec.ny);
-  ix = static_cast<int>(loc / spec.ny);
+  const int ny = bands[b].ny, nz = bands[b].nz;
+  iz = static_cast<int>(loc % nz);
+  loc /= nz;
+  iy = static_cast<int>(loc % ny);
+  ix = static_cast<int>(loc / ny);
 }
 
 // ---------------------------------------------------------------- partition
@@ -107,7 +143,7 @@ unsigned long long spread3(unsigned long long v) {  // 21 bits -> every third bi
 
 // Morton (Z-order) space-filling curve over a band's (ix, iy, iz) elements.
 void sfc_order(const MeshGeom& mesh, int b, std::vector<long>& lex_of, std::vector<long>& order_of) {
-  const long ny = mesh.spec.ny, nz = mesh.spec.nz, ne = mesh.bands[b].n_elements;
+  const long ny = mesh.bands[b].ny, nz = mesh.bands[b].nz, ne = mesh.bands[b].n_elements;
   std::vector<std::pair<unsigned long long, long>> key(ne);
   for (long l = 0; l < ne; ++l) {
     const long ix = l / (ny * nz), iy = (l / nz) % ny, iz = l % nz;
@@ -143,6 +179,8 @@ Partition assign_ranks(const MeshGeom& mesh, int n_ranks) {
     // band: iy major.
     const int ny = mesh.spec.ny, nz = mesh.spec.nz;
     if (n_ranks > ny) throw ConfigError("y-slab partition needs n_ranks <= ny");
+    for (const auto& B : mesh.bands)
+      if (B.ny != ny || B.nz != nz) throw ConfigError("y-slab partition needs the same ny / nz in every band");
     for (int b = 0; b < nb; ++b) {
       const int nx = mesh.bands[b].nx;
       auto& lo = p.lex_of[b];
@@ -211,6 +249,7 @@ namespace {
 struct Nbr {
   int kind;  // 0 conforming, 1 sliding, 2 dirichlet
   int band, ix, iy, iz, side, iface;
+  bool nc = false;  // iface indexes MeshGeom::nc_ifaces
 };
 
 // Neighbour across `side` (3D form of face_topology.cpp:14-46 + 64-121).
@@ -219,15 +258,16 @@ Nbr neighbour(const MeshGeom& m, int b, int ix, int iy, int iz, int side) {
   const int dir = side / 2;
   const bool plus = side & 1;
   const int opp = side ^ 1;
+  const int ny = m.bands[b].ny, nz = m.bands[b].nz;
   if (dir == 1) {
-    if (plus && iy + 1 == s.ny && !s.periodic_y) return {2, 0, 0, 0, 0, 0, -1};
+    if (plus && iy + 1 == ny && !s.periodic_y) return {2, 0, 0, 0, 0, 0, -1};
     if (!plus && iy == 0 && !s.periodic_y) return {2, 0, 0, 0, 0, 0, -1};
-    return {0, b, ix, plus ? (iy + 1) % s.ny : (iy - 1 + s.ny) % s.ny, iz, opp, -1};
+    return {0, b, ix, plus ? (iy + 1) % ny : (iy - 1 + ny) % ny, iz, opp, -1};
   }
   if (dir == 2) {
-    if (plus && iz + 1 == s.nz && !s.periodic_z) return {2, 0, 0, 0, 0, 0, -1};
+    if (plus && iz + 1 == nz && !s.periodic_z) return {2, 0, 0, 0, 0, 0, -1};
     if (!plus && iz == 0 && !s.periodic_z) return {2, 0, 0, 0, 0, 0, -1};
-    return {0, b, ix, iy, plus ? (iz + 1) % s.nz : (iz - 1 + s.nz) % s.nz, opp, -1};
+    return {0, b, ix, iy, plus ? (iz + 1) % nz : (iz - 1 + nz) % nz, opp, -1};
   }
   const int nb = static_cast<int>(m.bands.size());
   const int nx = m.bands[b].nx;
@@ -243,6 +283,9 @@ Nbr neighbour(const MeshGeom& m, int b, int ix, int iy, int iz, int side) {
   for (size_t i = 0; i < m.ifaces.size(); ++i)
     if (m.ifaces[i].left == left && m.ifaces[i].right == right)
       return {1, other, 0, iy, iz, opp, static_cast<int>(i)};
+  for (size_t i = 0; i < m.nc_ifaces.size(); ++i)
+    if (m.nc_ifaces[i].left == left && m.nc_ifaces[i].right == right)
+      return {1, other, 0, iy, iz, opp, static_cast<int>(i), true};
   return {0, other, plus ? 0 : m.bands[other].nx - 1, iy, iz, opp, -1};
 }
 }  // namespace
@@ -296,13 +339,13 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
       } else if (n.kind == 1) {
         t.side_type[slot] = kSliding;
         t.side_idx[slot] = static_cast<int>(t.sliding.size());
-        t.sliding.push_back({n.iface, e, s, iy, iz});
+        t.sliding.push_back({n.iface, e, s, iy, iz, n.nc});
       } else {
         const long ng = mesh.gid(n.band, n.ix, n.iy, n.iz);
         const int owner = part.owner(n.band, ng - mesh.bands[n.band].off);
         t.side_type[slot] = kConforming;
         if (sector && s == 2 && iy == 0) t.side_rot[slot] = -1;
-        if (sector && s == 3 && iy + 1 == mesh.spec.ny) t.side_rot[slot] = 1;
+        if (sector && s == 3 && iy + 1 == mesh.bands[b].ny) t.side_rot[slot] = 1;
         if (owner == rank) {
           t.side_idx[slot] = 6 * local_of.at(ng) + n.side;
         } else {
@@ -349,7 +392,7 @@ void map_point(const MeshGeom& m, int b, int ix, int iy, int iz, double xi, doub
   if (m.spec.mapping == SDG_MAP_BOX) {
     x[0] = bx;
     x[1] = by + B.vg * t;
-    x[2] = bz;
+    x[2] = bz + B.vgz * t;
     return;
   }
   const double tx = (ix + 0.5 * (xi + 1.0)) / B.nx, ty = (iy + 0.5 * (eta + 1.0)) / m.spec.ny,
@@ -982,6 +1025,23 @@ long static_index(long i_moving, long n_delta, int i_sub, long n_faces) {
 }  // namespace sdg
 
 namespace sdg {
+// Seeded density perturbation of include/sdg_types.h (sdg_case.pt_*).
+static double case_perturbation(const sdg_case& cs, const double* x, double t) {
+  const double two_pi = 6.283185307179586476925286766559;
+  double c[3] = {x[0] - cs.pt_adv[0] * t, x[1] - cs.pt_adv[1] * t, x[2] - cs.pt_adv[2] * t};
+  if (cs.pt_coords == 1) {
+    const double th = std::atan2(c[1], c[2]), r = std::sqrt(c[1] * c[1] + c[2] * c[2]);
+    c[1] = th;
+    c[2] = r;
+  }
+  double xh[3];
+  for (int d = 0; d < 3; ++d) xh[d] = (c[d] - cs.pt_x0[d]) / cs.pt_len[d];
+  double acc = 0.0;
+  for (int m = 0; m < cs.pt_modes; ++m)
+    acc += cs.pt_a[m] * std::sin(two_pi * (cs.pt_k[m][0] * xh[0] + cs.pt_k[m][1] * xh[1] + cs.pt_k[m][2] * xh[2]) + cs.pt_phi[m]);
+  return cs.pt_amp * acc;
+}
+
 void eval_case_host(const sdg_case& cs, const sdg_gas& g, const double* x, double t, double* u) {
   const double pi = 3.14159265358979323846;
   const double gm1 = g.gamma - 1.0;
@@ -1044,6 +1104,8 @@ void eval_case_host(const sdg_case& cs, const sdg_gas& g, const double* x, doubl
     default:
       throw ConfigError("unknown case kind");
   }
+  if (cs.pt_modes < 0 || cs.pt_modes > SDG_PT_MAX_MODES) throw ConfigError("perturbation: 0..8 modes");
+  if (cs.pt_modes > 0) rho += case_perturbation(cs, x, t);
   if (!(rho > 0.0) || !(p > 0.0)) throw InvalidStateError("primitive state requires rho > 0 and p > 0");
   u[0] = rho;
   u[1] = rho * v0;

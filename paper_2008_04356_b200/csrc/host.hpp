@@ -32,6 +32,7 @@ struct DeviceError : std::runtime_error {
 constexpr int kMaxN1 = 8;       // N <= 7 on the device path
 constexpr int kMaxCtx = 8;      // interface sides per rank (4 interfaces)
 constexpr int kMaxPartners = 32;
+constexpr int kMaxNcIfaces = 4;  // non-matching / oblique interfaces per mesh
 
 enum SideType : int8_t { kConforming = 0, kSliding = 1, kDirichlet = 2 };
 
@@ -40,6 +41,8 @@ struct BandGeom {
   int nx;
   long off;  // first global element id
   long n_elements;
+  int ny, nz;   // per-band counts (BandSpec::ny, mesh.hpp:16; nz the 3D analogue)
+  double vgz;   // translation speed along +z (oblique sliding, SDG_MAP_BOX only)
 };
 
 struct IfaceGeom {
@@ -52,16 +55,30 @@ struct IfaceGeom {
   int moving_band() const { return static_is_left ? right : left; }
 };
 
+// A non-matching and/or obliquely sliding planar interface (BASELINE configs[1];
+// the reference requires equal face counts, mesh.cpp:75-77, and motion along y
+// only, mesh.hpp:12-17).  Side A = the left band's x+ faces, side B = the right
+// band's x- faces; B is displaced by (vy_rel, vz_rel) t relative to A.  Its
+// mortars are the tensor products of the y and z rows of face intervals
+// (merge_intervals), recomputed every stage.
+struct NcIfaceGeom {
+  int left, right;
+  long nfy[2], nfz[2];  // faces per side along y and z
+  double ly[2], lz[2];  // face sizes
+  double vy_rel, vz_rel;
+};
+
 // Structured multi-band hexahedral mesh (3D form of proj/src/mesh.cpp:27-92).
 struct MeshGeom {
   sdg_mesh_spec spec;
   std::vector<BandGeom> bands;
-  std::vector<IfaceGeom> ifaces;
+  std::vector<IfaceGeom> ifaces;      // the reference's sliding interfaces (equal counts, y motion)
+  std::vector<NcIfaceGeom> nc_ifaces; // non-matching / oblique ones
   long n_elements = 0;
 
   explicit MeshGeom(const sdg_mesh_spec& s);
   long gid(int b, int ix, int iy, int iz) const {
-    return bands[b].off + (static_cast<long>(ix) * spec.ny + iy) * spec.nz + iz;
+    return bands[b].off + (static_cast<long>(ix) * bands[b].ny + iy) * bands[b].nz + iz;
   }
   void locate(long g, int& b, int& ix, int& iy, int& iz) const;
 };
@@ -85,10 +102,11 @@ struct Partition {
 Partition assign_ranks(const MeshGeom& mesh, int n_ranks);
 
 struct SlidingFaceRec {
-  int iface;
-  int elem;  // local element
-  int side;  // 0 (x-) or 1 (x+)
+  int iface;  // index into MeshGeom::ifaces, or MeshGeom::nc_ifaces when nc
+  int elem;   // local element
+  int side;   // 0 (x-) or 1 (x+)
   long i_par, i_perp;
+  bool nc = false;
 };
 
 // Flat per-rank topology consumed by the kernels.

@@ -200,6 +200,23 @@ __device__ __forceinline__ bool face_flux_fv(const double* um, const double* up,
   return ok;
 }
 
+// Seeded density perturbation of include/sdg_types.h (sdg_case.pt_*).
+__device__ double case_perturbation(const sdg_case& cs, const double* x, double t) {
+  const double two_pi = 6.283185307179586476925286766559;
+  double c[3] = {x[0] - cs.pt_adv[0] * t, x[1] - cs.pt_adv[1] * t, x[2] - cs.pt_adv[2] * t};
+  if (cs.pt_coords == 1) {
+    const double th = atan2(c[1], c[2]), r = sqrt(c[1] * c[1] + c[2] * c[2]);
+    c[1] = th;
+    c[2] = r;
+  }
+  double xh[3];
+  for (int d = 0; d < 3; ++d) xh[d] = (c[d] - cs.pt_x0[d]) / cs.pt_len[d];
+  double acc = 0.0;
+  for (int m = 0; m < cs.pt_modes; ++m)
+    acc += cs.pt_a[m] * sin(two_pi * (cs.pt_k[m][0] * xh[0] + cs.pt_k[m][1] * xh[1] + cs.pt_k[m][2] * xh[2]) + cs.pt_phi[m]);
+  return cs.pt_amp * acc;
+}
+
 // Exact solutions (exact_solutions.cpp:7-35; TGV in BASELINE axes).
 __device__ void eval_case(const sdg_case& cs, const double* x, double t, const GasD& g, double* u) {
   const double pi = 3.14159265358979323846;
@@ -257,6 +274,7 @@ __device__ void eval_case(const sdg_case& cs, const double* x, double t, const G
       v2 = cs.fs_v[2];
       p = cs.fs_p;
   }
+  if (cs.pt_modes > 0) rho += case_perturbation(cs, x, t);
   u[0] = rho;
   u[1] = rho * v0;
   u[2] = rho * v1;
@@ -288,6 +306,7 @@ __device__ __forceinline__ void map_position(const ElemConsts& C, const int* crd
     x[2] += C.warp * B.hz * sp * sy;
   }
   x[1] += B.vg * t;
+  x[2] += B.vgz * t;
   if (C.mapping == SDG_MAP_ANNULUS) {  // (x, theta, r) -> (x, r sin theta, r cos theta)
     double sn, cs;
     sincos(x[1], &sn, &cs);
@@ -643,7 +662,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
         double other[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) other[v] = nb[v];
-        const double vg = dir == 1 ? B.vg : 0.0;
+        const double vg = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
         const double* um = (s & 1) ? own : other;
         const double* up = (s & 1) ? other : own;
         if (VISC) {
@@ -677,7 +696,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
         double x[3], ext[5];
         face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
         eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-        const double vg = dir == 1 ? B.vg : 0.0;
+        const double vg = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
         const double* um = (s & 1) ? own : ext;
         const double* up = (s & 1) ? ext : own;
         if (VISC) {
@@ -714,7 +733,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
     const double ir = rcp_nr(u[0]);
     const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
     const double p = pressure(u, ir, C.gas);
-    const double vgv[3] = {0.0, B.vg, 0.0};
+    const double vgv[3] = {0.0, B.vg, B.vgz};
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       F[d][0] = u[0] * vv[d];
@@ -853,7 +872,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_suggest_dt(const __grid_co
     const BandD& B = C.bands[P.coords[4 * e]];
     const bool ann = C.mapping == SDG_MAP_ANNULUS;
     const double ir = 1.0 / u[0];
-    const double a = u[1] * ir, b = u[2] * ir - (ann ? 0.0 : B.vg), c = u[3] * ir;
+    const double a = u[1] * ir, b = u[2] * ir - (ann ? 0.0 : B.vg), c = u[3] * ir - (ann ? 0.0 : B.vgz);
     const double p = pressure(u, ir, C.gas);
     lm = sqrt(a * a + b * b + c * c) + sqrt(C.gas.gamma * p * ir);
     if (ann) lm += fabs(B.vg) * (C.z0 + B.hz * C.nz);  // tip speed of a rotating band
@@ -1055,6 +1074,7 @@ __global__ void k_mortar_fill(const __grid_constant__ MortarOps ops, int n_ctx, 
   if (item >= P.S * 2 * N2) return;
   const int ks = item / (2 * N2), sub = (item / N2) & 1, node = item % N2, jm = node / N1, kk = node % N1;
   const int ci = P.slide_ctx[ks], f = P.slide_f[ks];
+  if (ci < 0) return;  // a face of a non-matching interface (tensor-product chain)
   const int conf = P.ctx_state[2 * ci + 1];
   if (conf && sub == 0) return;
   const int role = P.ctx_role[ci];
@@ -1113,6 +1133,7 @@ __global__ void k_mortar_backproject(const __grid_constant__ MortarOps ops, int 
   if (item >= P.S * N2) return;
   const int ks = item / N2, node = item % N2, jj = node / N1, kk = node % N1;
   const int ci = P.slide_ctx[ks], f = P.slide_f[ks];
+  if (ci < 0) return;  // a face of a non-matching interface (tensor-product chain)
   const int conf = P.ctx_state[2 * ci + 1];
   const int role = P.ctx_role[ci];
   const double* src = role == 0 ? src0 : src1;
@@ -1386,40 +1407,6 @@ __device__ __forceinline__ void prefetch_codes(const FieldPtrs& P, int tile, int
   cp_async_commit();
 }
 
-// Update-kernel stage loads of one tile (issued by one thread).
-template <int N1, bool VISC>
-__device__ __forceinline__ void issue_update_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
-                                                   uint64_t* bar) {
-  using D = Tma<N1>;
-  const int e0 = P.e_first + tile * D::EPB;
-  const int n = min(D::EPB, P.E - e0);
-  uint32_t bytes = n * D::EL * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int typ = codes[8 * le + s] >> kCodeShift;
-      if (typ != kDirichlet) bytes += (D::TS + (VISC ? D::FS : 0)) * 8u;
-    }
-  mbar_arrive_expect_tx(bar, bytes);
-  double* sU = st;
-  double* sFv = sU + D::EPB * D::EL;
-  double* sNb = sFv + D::EPB * 6 * D::FS;
-  bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
-  if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D::FS, n * 6u * D::FS * 8u, bar);
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int code = codes[8 * le + s];
-      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-      double* nb = sNb + (le * 6 + s) * D::NB;
-      if (typ == kConforming) {
-        bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-        if (VISC) bulk_g2s(nb + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-      } else if (typ == kSliding) {
-        bulk_g2s(nb, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-        if (VISC) bulk_g2s(nb + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-      }
-    }
-}
-
 // Prolongation of one variable from an AoS [node][5] element block.
 template <int N1>
 __device__ __forceinline__ double prolong_aos(const double* __restrict__ s, int v, const double* __restrict__ ell,
@@ -1431,31 +1418,6 @@ __device__ __forceinline__ double prolong_aos(const double* __restrict__ s, int 
 #pragma unroll
   for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[(base + m * stride) * 5 + v], acc);
   return acc;
-}
-
-// Face trace (all 5 variables) of one face node from an AoS [node][5] element block.  z-lines
-// are 5*N1 doubles apart, so a warp's loads of one line position would pile onto half the
-// banks; every other group of 8 face nodes starts the contraction one node later, which
-// spreads them over all banks (the summation order is fixed per face node).
-template <int N1>
-__device__ __forceinline__ void face_trace_aos(const double* __restrict__ s, const double* __restrict__ ell, int dir,
-                                               int a, int b, double* __restrict__ out) {
-  constexpr int N2 = N1 * N1;
-  const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
-  const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
-  const int rot = dir == 2 ? (((a * N1 + b) >> 3) & 1) : 0;
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    int mm = m + rot;
-    if (mm == N1) mm = 0;
-    const double c = ell[mm];
-    const double* p = s + (base + mm * stride) * 5;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) acc[v] = __fma_rn(c, p[v], acc[v]);
-  }
-#pragma unroll
-  for (int v = 0; v < 5; ++v) out[v] = acc[v];
 }
 
 // BR1 gradient by line tasks: task (d, c, line) loads q along the line once and
@@ -1488,470 +1450,6 @@ __device__ __forceinline__ void gradient_lines(const ElemConsts& C, const BandD&
       out[o * stride] = cd * (surf - vol);
     }
   }
-}
-
-// v2 layout.  Stage (double-buffered, TMA): U, the element's own face traces (written by the
-// previous stage's phase 6 / k_prolong, so phase 1 needs no prolongation), own Fv.n and the
-// per-side neighbour trace + Fv.n (or mortar flux + lift*).  The RK register is prefetched into
-// L2 with the tile and copied (cp.async) over the consumed own-trace region after phase 1.
-template <int N1>
-struct TmaV2 {
-  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
-  static constexpr int EPB = Tma<N1>::EPB;
-  static constexpr int THREADS = EPB * N3;
-  static constexpr int MINB = N1 == 2 ? 3 : (N1 == 8 ? 1 : (N1 == 4 ? 4 : 2));
-  static constexpr int TAB = Dim<N1>::TAB;
-  static constexpr int EL = 5 * N3, TS = 5 * N2, FS = 4 * N2, NB = TS + FS;
-  static constexpr int U_STAGE = EPB * (EL + 6 * TS + 6 * FS + 6 * NB);
-  static constexpr int U_WORK = EPB * (5 * N3 + 24 * N2 + 6 * TS);
-  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_WORK) * 8 + 64;
-  // Node-major pitch-6 q / F staging.  With F3 the three volume-flux directions are staged
-  // at once over [q | lift* | traces] (18 N3 per element; N1 = 8 lacks the shared memory).
-  static constexpr bool F3 = N1 != 8;
-  static constexpr int F3_EXTRA = F3 && 18 * N3 > 6 * N3 + 54 * N2 ? EPB * (12 * N3 - 54 * N2) : 0;
-  static constexpr int U_SMEM_PACK = U_SMEM + (EPB * N3 + F3_EXTRA) * 8;
-};
-
-// Update-kernel loads of one tile (issued by one thread).
-template <int N1, bool VISC>
-__device__ __forceinline__ void issue_update_loads_v2(const FieldPtrs& P, int tile, const int* codes, double* st,
-                                                   uint64_t* bar, bool want_reg) {
-  using D2 = TmaV2<N1>;
-  const int e0 = P.e_first + tile * D2::EPB;
-  const int n = min(D2::EPB, P.E - e0);
-  uint32_t bytes = n * (D2::EL + 6u * D2::TS) * 8u + (VISC ? n * 6u * D2::FS * 8u : 0u);
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int typ = codes[8 * le + s] >> kCodeShift;
-      if (typ != kDirichlet) bytes += (D2::TS + (VISC ? D2::FS : 0)) * 8u;
-    }
-  mbar_arrive_expect_tx(bar, bytes);
-  double* sU = st;
-  double* sOwn = st + D2::EPB * D2::EL;
-  double* sFv = sOwn + D2::EPB * 6 * D2::TS;
-  double* sNb = sFv + D2::EPB * 6 * D2::FS;
-  bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u, bar);
-  bulk_g2s(sOwn, P.trace + static_cast<size_t>(e0) * 6 * D2::TS, n * 6u * D2::TS * 8u, bar);
-  if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D2::FS, n * 6u * D2::FS * 8u, bar);
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int code = codes[8 * le + s];
-      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-      double* nb = sNb + (le * 6 + s) * D2::NB;
-      if (typ == kConforming) {
-        bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D2::TS, D2::TS * 8u, bar);
-        if (VISC) bulk_g2s(nb + D2::TS, P.fvn + static_cast<size_t>(idx) * D2::FS, D2::FS * 8u, bar);
-      } else if (typ == kSliding) {
-        bulk_g2s(nb, P.slide_flux + static_cast<size_t>(idx) * D2::TS, D2::TS * 8u, bar);
-        if (VISC) bulk_g2s(nb + D2::TS, P.slide_lift + static_cast<size_t>(idx) * D2::FS, D2::FS * 8u, bar);
-      }
-    }
-  if (want_reg) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D2::EL, n * D2::EL * 8u);
-}
-
-// WS = true: warp-specialised (as k_gradient_ws): the consumer warps run the phases and sync on
-// named barrier 1; one producer warp issues the stage loads (full[s] = bars[s]), waits for the
-// consumers to release a tile (empty[s] = bars[2 + s]), bulk-stores U, the register and the
-// new traces, and signals (bars[4]) once the trace buffer, which phase 3 reuses, has been read.
-template <int N1>
-struct UWs {
-  static constexpr int CONSUMERS = (TmaV2<N1>::THREADS + 31) / 32 * 32;
-  static constexpr int THREADS = CONSUMERS + 32;
-};
-
-template <int N1, bool VISC, bool PACK, bool WS>
-__global__ void __launch_bounds__(WS ? UWs<N1>::THREADS : TmaV2<N1>::THREADS, TmaV2<N1>::MINB) k_update_tma_v2(const __grid_constant__ ElemConsts C, FieldPtrs P,
-                                                                 StageArgs A) {
-  using D = TmaV2<N1>;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* stage0 = smem + D::TAB;
-  double* work = stage0 + 2 * D::U_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + D::U_WORK + (PACK ? EPB * N3 + D::F3_EXTRA : 0));
-  __shared__ __align__(16) int codes[3][8 * EPB];
-  load_tables<N1>(C, tab);
-  const int tiles = (P.E - P.e_first + EPB - 1) / EPB;
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3;
-  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  constexpr int NC = UWs<N1>::CONSUMERS;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < (WS ? 5 : 2); ++q) mbar_init(&bars[q], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  auto csync = [&] {
-    if (WS) consumer_sync(NC);
-    else __syncthreads();
-  };
-  // The RK register is read only when the stage's a-coefficient is non-zero (LSRK stage 1 has
-  // a = 0: the register is overwritten without being read).
-  const bool want_reg = A.mode == 0 && A.rk_a != 0.0;
-  constexpr int WF = PACK ? 6 * N3 : 5 * N3;      // per element: q, then F_d (SoA, or node-major pitch 6)
-  double* wF = work;
-  double* wLift = work + EPB * WF;                 // EPB x 24 N2, SoA [s][c][f]
-  double* wTr = wLift + EPB * 24 * N2;             // EPB x 6 TS, global slot layout
-  int tile = blockIdx.x;
-  if (threadIdx.x == (WS ? NC : 0) && tile < tiles) {
-    prefetch_codes<N1>(P, tile, codes[0]);
-    cp_async_wait_all();
-    issue_update_loads_v2<N1, VISC>(P, tile, codes[0], stage0, &bars[0], want_reg);
-    if (tile + gridDim.x < tiles) prefetch_codes<N1>(P, tile + gridDim.x, codes[1]);
-  }
-  if (WS && threadIdx.x >= NC) {
-    // ---------------- producer warp (one elected lane)
-    if (threadIdx.x != NC) return;
-    for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-      const int next = tile + gridDim.x;
-      if (next < tiles) {
-        cp_async_wait_all();  // codes of `next`
-        fence_proxy_async();
-        issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + ((it + 1) & 1) * D::U_STAGE,
-                                        &bars[(it + 1) & 1], want_reg);
-        if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
-      }
-      mbar_wait(&bars[2 + (it & 1)], (it >> 1) & 1);  // tile released: outputs assembled in shared memory
-      if (A.mode == 0) {
-        const int e0 = P.e_first + tile * EPB;
-        const int n = min(EPB, P.E - e0);
-        double* st = stage0 + (it & 1) * D::U_STAGE;
-        bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
-        bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, st + EPB * D::EL, n * D::EL * 8u);
-        bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
-        bulk_commit();
-        bulk_wait_read0();  // stage (it & 1) and the trace buffer are free again
-      }
-      mbar_arrive(&bars[4]);
-    }
-    bulk_wait0();
-    return;
-  }
-  if (!WS) __syncthreads();  // codes[0] visible to every thread
-  for (int it = 0; tile < tiles; ++it, tile += gridDim.x) {
-    const int sidx = it & 1;
-    double* st = stage0 + sidx * D::U_STAGE;
-    const int next = tile + gridDim.x;
-    if (!WS && threadIdx.x == 0) bulk_wait_read0();  // stores of the previous tile have read stage sidx^1 and wTr
-    if (!WS && threadIdx.x == 0 && next < tiles) {
-      cp_async_wait_all();  // codes of `next`
-      fence_proxy_async();
-      issue_update_loads_v2<N1, VISC>(P, next, codes[(it + 1) % 3], stage0 + (sidx ^ 1) * D::U_STAGE,
-                                   &bars[sidx ^ 1], want_reg);
-      if (next + gridDim.x < tiles) prefetch_codes<N1>(P, next + gridDim.x, codes[(it + 2) % 3]);
-    }
-    const int e0 = P.e_first + tile * EPB;
-    const int e = e0 + le;
-    const bool active = le < EPB && e < P.E;  // WS: padding lanes of the last consumer warp idle
-    double* sU = st + le * D::EL;
-    const double* sOwn = st + EPB * D::EL + le * 6 * D::TS;
-    double* sFv = st + EPB * (D::EL + 6 * D::TS) + le * 6 * D::FS;
-    double* sNb = st + EPB * (D::EL + 6 * D::TS + 6 * D::FS) + le * 6 * D::NB;
-    double* q = wF + le * WF;
-    double* lf = wLift + le * 24 * N2;
-    // WS: the full barrier also publishes the tile's side codes, so wait before reading them.
-    if (WS) mbar_wait(&bars[sidx], (it >> 1) & 1);
-    const int* myc = codes[it % 3] + 8 * le;
-    const BandD& B = C.bands[active ? myc[6] : 0];
-    if (!WS) mbar_wait(&bars[sidx], (it >> 1) & 1);
-
-    // Phase 1: face fluxes (in place over the neighbour data) and lift*.
-    if (active) {
-      if (VISC) {
-        double u[5], qq[4];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-        prim4(u, C.gas, qq);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) q[PACK ? t * 6 + c : c * N3 + t] = qq[c];
-      }
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1, dir = s >> 1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        double* nb = sNb + s * D::NB;
-        const int code = myc[s];
-        const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-        if (typ == kSliding) {
-          if (VISC) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = nb[D::TS + f * 4 + c];
-          }
-          continue;
-        }
-        double own[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) own[v] = sOwn[s * D::TS + f * 5 + v];
-        double flux[5], lift[4];
-        bool ok;
-        const double vg = dir == 1 ? B.vg : 0.0;
-        if (typ == kConforming) {
-          double other[5];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
-          const double* um = (s & 1) ? own : other;
-          const double* up = (s & 1) ? other : own;
-          if (VISC) {
-            double qa[4], qb[4];
-            prim4(own, C.gas, qa);
-            prim4(other, C.gas, qb);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-            // Fv.n of both sides read only now (not live through the Roe solve); the sum is
-            // symmetric, so both elements of the face still produce identical bits.
-            const double2* fa = reinterpret_cast<const double2*>(sFv + s * D::FS + f * 4);
-            const double2* fb = reinterpret_cast<const double2*>(nb + D::TS + f * 4);
-            const double2 a01 = fa[0], a23 = fa[1], b01 = fb[0], b23 = fb[1];
-            flux[1] -= 0.5 * (a01.x + b01.x);
-            flux[2] -= 0.5 * (a01.y + b01.y);
-            flux[3] -= 0.5 * (a23.x + b23.x);
-            flux[4] -= 0.5 * (a23.y + b23.y);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        } else {
-          double x[3], ext[5];
-          face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-          eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-          const double* um = (s & 1) ? own : ext;
-          const double* up = (s & 1) ? ext : own;
-          if (VISC) {
-            prim4(ext, C.gas, lift);
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-            const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
-            double gg[12];
-#pragma unroll
-            for (int c = 0; c < 12; ++c) gg[c] = gd[c];
-            double fm[4], fp[4];
-            fv_dir(um, gg, dir, C.gas, fm);
-            fv_dir(up, gg, dir, C.gas, fp);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
-          } else {
-            ok = roe_flux(um, up, dir, vg, C.gas, flux);
-          }
-        }
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - itm, own);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) nb[f * 5 + v] = flux[v];
-        if (VISC) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lf[(s * 4 + c) * N2 + f] = lift[c];
-        }
-      }
-    }
-    csync();
-    // The own traces and own Fv.n are consumed: that stage region now receives the tile's RK
-    // register (coalesced 16-byte cp.async, L2-prefetched with the tile loads); it is read and
-    // rewritten in place in phase 5 and bulk-stored with U.
-    double* sRg = st + EPB * D::EL;  // EPB x EL <= EPB x (6 TS + 6 FS) for N1 <= 10
-    if (want_reg) {
-      const int n = min(EPB, P.E - e0);
-      const double* src = P.reg + static_cast<size_t>(e0) * D::EL;
-      for (int q = threadIdx.x; q < n * D::EL / 2; q += (WS ? NC : D::THREADS)) cp_async16(sRg + 2 * q, src + 2 * q);
-      cp_async_commit();
-    }
-
-    // Phase 2: viscous stress at the node (gradient recomputed from q and lift*); only tau and
-    // the heat flux (9 values) cross the barrier that frees q / lift* for the flux staging.
-    double tau[3][3], hq[3];
-    if (VISC && active) {
-      double g[12];
-      if (PACK) node_gradient_pk<N1>(tab, q, lf, B, i, j, k, g);
-      else node_gradient<N1>(tab, q, lf, B, i, j, k, g);
-      const double div = g[0] + g[4] + g[8];
-      const double mu = C.gas.mu, lam = C.gas.lam;
-      tau[0][0] = 2.0 * mu * g[0] + lam * div;
-      tau[1][1] = 2.0 * mu * g[4] + lam * div;
-      tau[2][2] = 2.0 * mu * g[8] + lam * div;
-      tau[0][1] = tau[1][0] = mu * (g[1] + g[3]);
-      tau[0][2] = tau[2][0] = mu * (g[2] + g[6]);
-      tau[1][2] = tau[2][1] = mu * (g[5] + g[7]);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) hq[d] = C.gas.kcond * g[9 + d];
-    }
-    csync();  // q and lift* reads done
-    if (WS && it > 0) mbar_wait(&bars[4], (it - 1) & 1);  // previous tile's trace store has read wTr
-
-    // Phase 3: volume flux and weak divergence through shared memory.  F_x is staged over q,
-    // F_y over the dead lift* / trace scratch, then F_z over q: only F_z (5 values) stays in
-    // registers across a barrier.
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    double* qy = work + EPB * WF + le * WF;  // wLift + wTr hold >= EPB x 6 N3 doubles for N1 <= 9
-    double Fz[5];
-    auto flux_dir = [&](const double* u, const double* vv, double p, int d, double* f) {
-      const double vgd = d == 1 ? B.vg : 0.0;
-      f[0] = u[0] * vv[d] - vgd * u[0];
-      f[1] = u[1] * vv[d] + (d == 0 ? p : 0.0) - vgd * u[1];
-      f[2] = u[2] * vv[d] + (d == 1 ? p : 0.0) - vgd * u[2];
-      f[3] = u[3] * vv[d] + (d == 2 ? p : 0.0) - vgd * u[3];
-      f[4] = (u[4] + p) * vv[d] - vgd * u[4];
-      if (VISC) {
-        f[1] -= tau[d][0];
-        f[2] -= tau[d][1];
-        f[3] -= tau[d][2];
-        f[4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + hq[d];
-      }
-    };
-    auto stage_flux = [&](double* buf, const double* f, double sj) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) buf[PACK ? t * 6 + v : v * N3 + t] = f[v] * sj;
-    };
-    auto divergence = [&](const double* buf, int d) {
-      const int ia = d == 0 ? i : (d == 1 ? j : k);
-      const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-      for (int m = 0; m < N1; ++m) {
-        const double c = tab[ia * N1 + m];
-        if (PACK) {
-          const double* fp = buf + (base + m * stride) * 6;
-          const double2 f01 = *reinterpret_cast<const double2*>(fp);
-          const double2 f23 = *reinterpret_cast<const double2*>(fp + 2);
-          acc[0] += c * f01.x;
-          acc[1] += c * f01.y;
-          acc[2] += c * f23.x;
-          acc[3] += c * f23.y;
-          acc[4] += c * reinterpret_cast<const double2*>(fp + 4)->x;  // 16-byte load: conflict-free at pitch 6
-        } else {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) acc[v] += c * buf[v * N3 + base + m * stride];
-        }
-      }
-    };
-    constexpr bool F3 = PACK && D::F3;
-    double* qz = work + (F3 ? 2 * EPB * WF : 0) + le * WF;
-    if (active) {
-      double u[5], f[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-      const double ir = rcp_nr(u[0]);
-      const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
-      const double p = pressure(u, ir, C.gas);
-      flux_dir(u, vv, p, 0, f);
-      stage_flux(q, f, B.sj[0]);
-      flux_dir(u, vv, p, 1, f);
-      stage_flux(qy, f, B.sj[1]);
-      if (F3) {
-        flux_dir(u, vv, p, 2, f);
-        stage_flux(qz, f, B.sj[2]);
-      } else {
-        flux_dir(u, vv, p, 2, Fz);
-      }
-    }
-    if (want_reg) cp_async_wait_all();  // this thread's register chunks; the barrier publishes them
-    csync();
-    if (active) {
-      divergence(q, 0);
-      divergence(qy, 1);
-      if (F3) divergence(qz, 2);
-    }
-    if (!F3) {
-      csync();
-      if (active) stage_flux(q, Fz, B.sj[2]);
-      csync();
-      if (active) divergence(q, 2);
-    }
-
-    // Phase 4 + 5: surface lift, RK update in place, admissibility.
-    if (active) {
-      double du[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) du[v] = acc[v] * B.inv_jac;
-      const double* lw = tab + N1 * N1 + 2 * N1;
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int dir = s >> 1;
-        const int ia = dir == 0 ? i : (dir == 1 ? j : k);
-        const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
-        const double c = ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * lw[(s & 1) * N1 + ia];
-        if (c != 0.0) {
-          const double* fl = sNb + s * D::NB + f * 5;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) du[v] += c * fl[v];
-        }
-      }
-      if (A.mode == 1) {
-        double* o = P.out + (static_cast<size_t>(e) * N3 + t) * 5;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = du[v];
-      } else {
-        double w[5];
-        double u[5];
-        double* rgp = sRg + le * D::EL + t * 5;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          double rg = A.dt * du[v];
-          if (want_reg) rg = __fma_rn(A.rk_a, rgp[v], rg);
-          w[v] = u[v] + A.rk_b * rg;
-          rgp[v] = rg;
-          sU[t * 5 + v] = w[v];
-        }
-        const double p = pressure(w, rcp_nr(w[0]), C.gas);
-        bool ok = w[0] > 0.0 && p > 0.0;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
-        if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
-      }
-    }
-    if (A.mode == 1) {
-      fence_proxy_async();
-      csync();
-      if (WS && threadIdx.x == 0) mbar_arrive(&bars[2 + sidx]);
-      continue;
-    }
-    csync();
-    // Phase 6: traces of the new state, then bulk stores of U, reg and traces.
-    if (active) {
-      double* tr = wTr + le * 6 * D::TS;
-      for (int itm = t; itm < 6 * N2; itm += N3) {
-        const int s = itm / N2, f = itm % N2, a = f / N1, b = f % N1;
-        const double* ell = tab + N1 * N1 + (s & 1) * N1;
-        face_trace_aos<N1>(sU, ell, s >> 1, a, b, tr + s * D::TS + f * 5);
-      }
-    }
-    fence_proxy_async();
-    csync();
-    if (WS) {
-      if (threadIdx.x == 0) mbar_arrive(&bars[2 + sidx]);
-    } else if (threadIdx.x == 0) {
-      const int n = min(EPB, P.E - e0);
-      bulk_s2g(P.U + static_cast<size_t>(e0) * D::EL, st, n * D::EL * 8u);
-      bulk_s2g(P.reg + static_cast<size_t>(e0) * D::EL, sRg, n * D::EL * 8u);
-      bulk_s2g(P.trace_out + static_cast<size_t>(e0) * 6 * D::TS, wTr, n * 6u * D::TS * 8u);
-      bulk_commit();
-    }
-  }
-  if (!WS && threadIdx.x == 0) bulk_wait0();
-}
-
-// Gradient-kernel loads of one tile: U and, per side, the neighbour trace
-// (conforming) or the back-projected lift* (sliding).
-template <int N1>
-__device__ __forceinline__ void issue_gradient_loads(const FieldPtrs& P, int tile, const int* codes, double* st,
-                                                     uint64_t* bar) {
-  using D = Tma<N1>;
-  const int e0 = P.e_first + tile * D::EPB;
-  const int n = min(D::EPB, P.E - e0);
-  uint32_t bytes = n * D::EL * 8u;
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int typ = codes[8 * le + s] >> kCodeShift;
-      if (typ == kConforming) bytes += D::TS * 8u;
-      else if (typ == kSliding) bytes += D::FS * 8u;
-    }
-  mbar_arrive_expect_tx(bar, bytes);
-  bulk_g2s(st, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
-  double* sNb = st + D::EPB * D::EL;
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int code = codes[8 * le + s];
-      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-      double* nb = sNb + (le * 6 + s) * D::TS;
-      if (typ == kConforming) bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-      else if (typ == kSliding) bulk_g2s(nb, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-    }
 }
 
 // Components of the gradient trace that Fv.n along `dir` needs (flux.cpp:23-42):
@@ -2020,65 +1518,6 @@ __device__ __forceinline__ double prolong_aos_d(const double* __restrict__ s, in
 #pragma unroll
   for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[(base + m * stride) * 5 + v], acc);
   return acc;
-}
-
-// New face traces of one element (AoS state in, trace slots out).
-template <int N1>
-__device__ __forceinline__ void write_traces(const double* tab, const double* sU, double* tr, int t, int nt) {
-  constexpr int N2 = N1 * N1, TS = 5 * N2;
-  for (int itm = t; itm < 6 * N2; itm += nt) {
-    const int s = itm / N2, f = itm - s * N2, a = f / N1, b = f - a * N1;
-    const double* ell = tab + N1 * N1 + (s & 1) * N1;
-    double* o = tr + s * TS + f * 5;
-    switch (s >> 1) {
-      case 0:
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = prolong_aos_d<N1, 0>(sU, v, ell, a, b);
-        break;
-      case 1:
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = prolong_aos_d<N1, 1>(sU, v, ell, a, b);
-        break;
-      default:
-#pragma unroll
-        for (int v = 0; v < 5; ++v) o[v] = prolong_aos_d<N1, 2>(sU, v, ell, a, b);
-    }
-  }
-}
-
-template <int N1, bool VISC>
-__device__ __forceinline__ void issue_update_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
-                                                    uint64_t* bar) {
-  using D = T5<N1>;
-  const int e0 = P.e_first + tile * D::EPB;
-  const int n = min(D::EPB, P.E - e0);
-  uint32_t bytes = n * (2u * D::EL + 6u * D::TS) * 8u + (VISC ? n * 6u * D::FS * 8u : 0u);
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s)
-      if ((codes[8 * le + s] >> kCodeShift) != kDirichlet) bytes += (D::TS + (VISC ? D::FS : 0)) * 8u;
-  mbar_arrive_expect_tx(bar, bytes);
-  double* sU = st;
-  double* sRg = sU + D::EPB * D::EL;
-  double* sTr = sRg + D::EPB * D::EL;
-  double* sFv = sTr + D::EPB * 6 * D::TS;
-  double* sNb = sFv + D::EPB * 6 * D::FS;
-  bulk_g2s(sU, P.U + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
-  bulk_g2s(sRg, P.reg + static_cast<size_t>(e0) * D::EL, n * D::EL * 8u, bar);
-  bulk_g2s(sTr, P.trace + static_cast<size_t>(e0) * 6 * D::TS, n * 6u * D::TS * 8u, bar);
-  if (VISC) bulk_g2s(sFv, P.fvn + static_cast<size_t>(e0) * 6 * D::FS, n * 6u * D::FS * 8u, bar);
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int code = codes[8 * le + s];
-      const int typ = code >> kCodeShift, idx = code & ((1 << kCodeShift) - 1);
-      double* nb = sNb + (le * 6 + s) * D::NB;
-      if (typ == kConforming) {
-        bulk_g2s(nb, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-        if (VISC) bulk_g2s(nb + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-      } else if (typ == kSliding) {
-        bulk_g2s(nb, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-        if (VISC) bulk_g2s(nb + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-      }
-    }
 }
 
 template <int N1>
@@ -2297,41 +1736,6 @@ bool gws_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm
 }
 
 
-template <int N1>
-bool update_tma_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm, cudaStream_t st) {
-  if constexpr (N1 % 2 != 0) {
-    return false;
-  } else {
-    using D = Tma<N1>;
-    const int tiles = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    static int variant = -1;
-    if (variant < 0) {
-      const char* env = std::getenv("SDG_UPDATE_V");
-      variant = env ? std::atoi(env) : 6;
-    }
-    // 6: node-major packed staging (default of this kernel), 8: warp-specialised, 2: SoA staging
-    const bool ws = variant == 8;
-    const bool pack = variant != 2;
-    const bool vis = c.gas.viscous != 0;
-    auto kern = ws ? (vis ? k_update_tma_v2<N1, true, true, true> : k_update_tma_v2<N1, false, true, true>)
-              : pack ? (vis ? k_update_tma_v2<N1, true, true, false> : k_update_tma_v2<N1, false, true, false>)
-                     : (vis ? k_update_tma_v2<N1, true, false, false> : k_update_tma_v2<N1, false, false, false>);
-    const int smem = pack ? TmaV2<N1>::U_SMEM_PACK : TmaV2<N1>::U_SMEM;
-    const int threads = ws ? UWs<N1>::THREADS : D::THREADS;
-    static int occ_tab[10] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-    int& occ = occ_tab[(ws ? 8 : pack ? 6 : 0) + (vis ? 1 : 0)];
-    if (occ < 0) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-      if (occ < 1) occ = 1;
-    }
-    const int grid = std::min(tiles, n_sm * occ);
-    kern<<<grid, threads, smem, st>>>(c, p, a);
-    check_launch("k_update_tma");
-    return true;
-  }
-}
-
 template <class K>
 void set_smem(K kernel, int bytes) {
   static_assert(sizeof(K) > 0, "");
@@ -2418,45 +1822,26 @@ void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageA
   if (p.E <= p.e_first) return;
   SDG_DISPATCH(n1, (update_t<NN>(c, p, a, st)));
 }
-static int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
 bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                          cudaStream_t st) {
   if (p.E <= p.e_first) return true;
   bool ok = false;
-  static const int gv = env_int("SDG_GRAD_V", 6);  // 6: warp-specialised; anything else: the plain kernel
-  if (gv != 6) return false;
   SDG_DISPATCH(n1, (ok = gws_t<NN>(c, p, a, n_sm, st)));
   return ok;
 }
-bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
-                       cudaStream_t st) {
-  if (p.E <= p.e_first) return true;
-  bool ok = false;
-  SDG_DISPATCH(n1, (ok = update_tma_t<NN>(c, p, a, n_sm, st)));
-  return ok;
-}
+// Curved elements: the bulk-loaded kernels for even N+1 (every block a multiple of
+// 16 bytes, as cp.async.bulk needs), the plain-load ones otherwise.
 void launch_gradient_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if (p.E <= p.e_first) return;
-  static const int cv = env_int("SDG_CURVED_V", 2);  // 2: bulk-loaded (even N+1), 1: plain loads
   bool done = false;
-  if (cv == 2) SDG_DISPATCH(n1, (done = gradient_curved_b_t<NN>(c, p, a, st)));
+  SDG_DISPATCH(n1, (done = gradient_curved_b_t<NN>(c, p, a, st)));
   if (!done) SDG_DISPATCH(n1, (gradient_curved_t<NN>(c, p, a, st)));
 }
 void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if (p.E <= p.e_first) return;
-  static const int cv = env_int("SDG_CURVED_V", 2);
   bool done = false;
-  if (cv == 2) SDG_DISPATCH(n1, (done = update_curved_b_t<NN>(c, p, a, st)));
+  SDG_DISPATCH(n1, (done = update_curved_b_t<NN>(c, p, a, st)));
   if (!done) SDG_DISPATCH(n1, (update_curved_t<NN>(c, p, a, st)));
-}
-bool launch_gradient_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  if (p.E <= p.e_first) return true;
-  bool done = false;
-  SDG_DISPATCH(n1, (done = gradient_affine_b_t<NN>(c, p, a, st)));
-  return done;
 }
 bool launch_update_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if (p.E <= p.e_first) return true;
@@ -2823,6 +2208,166 @@ void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, c
   k_nc_mortar_flux<<<static_cast<unsigned>((nodes + threads - 1) / threads), threads, 0, st>>>(nodes, g, dir, vg, ua,
                                                                                               ub, ga, gb, flux, bad);
   check_launch("k_nc_mortar_flux");
+}
+
+// ---------------------------------------------------------------------------
+// Non-matching / oblique interfaces inside the stage (BASELINE configs[1]).
+// Face data are read from / written to the resident arrays through per-face
+// slot tables (trace slots 6e + side, or compact sliding indices), so no
+// gather copies are needed; the tensor-product contractions are those of
+// nc_to_mortar_body / nc_to_face_body above.
+// ---------------------------------------------------------------------------
+// Both rows of one interface recomputed on the device every stage and compared
+// with the rows the host built its operators from: a mismatch is a protocol error.
+__global__ void __launch_bounds__(kIvThreads) k_nc_rows(const __grid_constant__ NcStage S, int iface, ErrRec* err) {
+  __shared__ long long sh[kIvThreads];
+  __shared__ int bad;
+  const int d = blockIdx.x;
+  if (threadIdx.x == 0) bad = 0;
+  mortar_intervals_row(S.n_a[d], S.n_b[d], S.l_a[d], S.delta[d], S.d_faces[d], S.d_ranges[d], S.d_n + d, sh);
+  __syncthreads();
+  const long long m = d == 0 ? S.my : S.mz;
+  if (S.d_n[d] != m) bad = 1;
+  for (long long k = threadIdx.x; k < m; k += blockDim.x) {
+    if (S.d_faces[d][2 * k] != S.h_faces[d][2 * k] || S.d_faces[d][2 * k + 1] != S.h_faces[d][2 * k + 1]) bad = 1;
+    for (int q = 0; q < 4; ++q)
+      if (S.d_ranges[d][4 * k + q] != S.h_ranges[d][4 * k + q]) bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bad && atomicCAS(&err->flag, 0, 4) == 0) {
+    err->elem = iface;
+    err->node = d;
+  }
+}
+
+// Face -> mortar for both sides (blockIdx.y = side): mortar (ky, kz) of side s is
+// (F_y[s][ky] x F_z[s][kz]) applied to its face, located by the DEVICE rows.
+__global__ void k_nc_fill(int n, int nc, const double* __restrict__ src, const __grid_constant__ NcStage S,
+                          const int* __restrict__ tab0, const int* __restrict__ tab1, double* __restrict__ out0,
+                          double* __restrict__ out1) {
+  extern __shared__ double sm[];
+  const int s = blockIdx.y;
+  const long long blk = blockIdx.x, ky = blk / S.mz, kz = blk % S.mz;
+  const long long fy = S.d_faces[0][2 * ky + s], fz = S.d_faces[1][2 * kz + s];
+  const int* tab = s ? tab1 : tab0;
+  const int per = n * n * nc;
+  double* u = sm;
+  double* t = sm + per;
+  const double* face = src + static_cast<long long>(tab[fy * S.nfz[s] + fz]) * per;
+  for (int x = threadIdx.x; x < per; x += blockDim.x) u[x] = face[x];
+  __syncthreads();
+  const double* fy_op = S.F[s][0] + ky * n * n;
+  const double* fz_op = S.F[s][1] + kz * n * n;
+  for (int x = threadIdx.x; x < per; x += blockDim.x) {  // t[k][j][c] = sum_i Fy[k][i] u[i][j][c]
+    const int c = x % nc, j = (x / nc) % n, k = x / (nc * n);
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc = fma(fy_op[k * n + i], u[(i * n + j) * nc + c], acc);
+    t[x] = acc;
+  }
+  __syncthreads();
+  double* o = (s ? out1 : out0) + blk * static_cast<long long>(per);
+  for (int x = threadIdx.x; x < per; x += blockDim.x) {  // o[k][l][c] = sum_j Fz[l][j] t[k][j][c]
+    const int c = x % nc, l = (x / nc) % n, k = x / (nc * n);
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) acc = fma(fz_op[l * n + j], t[(k * n + j) * nc + c], acc);
+    o[x] = acc;
+  }
+}
+
+// Mortar -> face for both sides (blocks over the faces of A, then of B): each face
+// sums (B_y[s][ky] x B_z[s][kz]) applied to its mortars in the fixed CSR order.
+__global__ void k_nc_project(int n, int nc, const double* __restrict__ mortar, const __grid_constant__ NcStage S,
+                             const int* __restrict__ tab0, const int* __restrict__ tab1, double* __restrict__ dst) {
+  extern __shared__ double sm[];
+  const long long nf0 = S.nfy[0] * S.nfz[0];
+  const int s = blockIdx.x < nf0 ? 0 : 1;
+  const long long f = s ? blockIdx.x - nf0 : blockIdx.x;
+  const long long fy = f / S.nfz[s], fz = f % S.nfz[s];
+  const int per = n * n * nc;
+  double* m = sm;
+  double* t = sm + per;
+  double acc_local[8];
+  const int reps = (per + blockDim.x - 1) / blockDim.x;
+  for (int r = 0; r < reps; ++r) acc_local[r] = 0.0;
+  const int *offy = S.off[s][0], *offz = S.off[s][1], *idy = S.idx[s][0], *idz = S.idx[s][1];
+  for (int a = offy[fy]; a < offy[fy + 1]; ++a)
+    for (int b = offz[fz]; b < offz[fz + 1]; ++b) {
+      const long long ky = idy[a], kz = idz[b];
+      const double* src = mortar + (ky * S.mz + kz) * static_cast<long long>(per);
+      __syncthreads();
+      for (int x = threadIdx.x; x < per; x += blockDim.x) m[x] = src[x];
+      __syncthreads();
+      const double* by = S.B[s][0] + ky * n * n;
+      const double* bz = S.B[s][1] + kz * n * n;
+      for (int x = threadIdx.x; x < per; x += blockDim.x) {  // t[i][l][c] = sum_k By[i][k] m[k][l][c]
+        const int c = x % nc, l = (x / nc) % n, i = x / (nc * n);
+        double acc = 0.0;
+        for (int k = 0; k < n; ++k) acc = fma(by[i * n + k], m[(k * n + l) * nc + c], acc);
+        t[x] = acc;
+      }
+      __syncthreads();
+      for (int r = 0, x = threadIdx.x; x < per; ++r, x += blockDim.x) {  // += sum_l Bz[j][l] t[i][l][c]
+        const int c = x % nc, j = (x / nc) % n, i = x / (nc * n);
+        double acc = 0.0;
+        for (int l = 0; l < n; ++l) acc = fma(bz[j * n + l], t[(i * n + l) * nc + c], acc);
+        acc_local[r] += acc;
+      }
+    }
+  double* out = dst + static_cast<long long>((s ? tab1 : tab0)[f]) * per;
+  for (int r = 0, x = threadIdx.x; x < per; ++r, x += blockDim.x) out[x] = acc_local[r];
+}
+
+// Two-sided Roe (+ central viscous) flux at the mortar nodes, A on the minus side,
+// normal +x, vg_n = 0 (tangential sliding); failures go to the stage's error record.
+__global__ void k_nc_flux(long long nodes, GasD g, const double* __restrict__ ua, const double* __restrict__ ub,
+                          const double* __restrict__ ga, const double* __restrict__ gb, double* __restrict__ flux,
+                          ErrRec* err) {
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= nodes) return;
+  double um[5], up[5], f[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    um[v] = ua[q * 5 + v];
+    up[v] = ub[q * 5 + v];
+  }
+  double fvm[4], fvp[4];
+  const bool vis = ga != nullptr && g.viscous;
+  if (vis) {
+    fv_dir(um, ga + q * 12, 0, g, fvm);
+    fv_dir(up, gb + q * 12, 0, g, fvp);
+  }
+  if (!face_flux_fv(um, up, 0, 0.0, vis ? fvm : nullptr, fvp, g, f)) record_error(err, 2, -1, -1, -1, -1, um);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) flux[q * 5 + v] = f[v];
+}
+
+void launch_nc_rows(const NcStage& S, int iface, ErrRec* err, cudaStream_t st) {
+  k_nc_rows<<<2, kIvThreads, 0, st>>>(S, iface, err);
+  check_launch("k_nc_rows");
+}
+void launch_nc_fill(int n, int nc, const double* src, const NcStage& S, const int* const tab[2], double* const out[2],
+                    cudaStream_t st) {
+  const int per = n * n * nc;
+  if (per > 1024) throw DeviceError(SDG_ERR_CONFIG, "nc fill: n*n*nc exceeds 1024");
+  if (S.my * S.mz == 0) return;
+  k_nc_fill<<<dim3(static_cast<unsigned>(S.my * S.mz), 2), 128, 2 * per * sizeof(double), st>>>(
+      n, nc, src, S, tab[0], tab[1], out[0], out[1]);
+  check_launch("k_nc_fill");
+}
+void launch_nc_project(int n, int nc, const double* mortar, const NcStage& S, const int* const tab[2], double* dst,
+                       cudaStream_t st) {
+  const int per = n * n * nc;
+  if (per > 1024) throw DeviceError(SDG_ERR_CONFIG, "nc projection: n*n*nc exceeds 1024");
+  const long long faces = S.nfy[0] * S.nfz[0] + S.nfy[1] * S.nfz[1];
+  k_nc_project<<<static_cast<unsigned>(faces), nc_threads(per), 2 * per * sizeof(double), st>>>(n, nc, mortar, S,
+                                                                                              tab[0], tab[1], dst);
+  check_launch("k_nc_project");
+}
+void launch_nc_flux(long long nodes, const GasD& g, const double* ua, const double* ub, const double* ga,
+                    const double* gb, double* flux, ErrRec* err, cudaStream_t st) {
+  if (nodes <= 0) return;
+  k_nc_flux<<<static_cast<unsigned>((nodes + 127) / 128), 128, 0, st>>>(nodes, g, ua, ub, ga, gb, flux, err);
+  check_launch("k_nc_flux");
 }
 
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st) {

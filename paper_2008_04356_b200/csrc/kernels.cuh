@@ -17,6 +17,7 @@ struct GasD {
 
 struct BandD {
   double x_lo, hx, hy, hz, vg;
+  double vgz;      // translation speed along +z (oblique sliding, affine only)
   double jac, inv_jac;
   double cdir[3];  // sJ_d / J
   double sj[3];    // sJ_d
@@ -161,17 +162,15 @@ struct MortarPtrs {
 void launch_prolong(int n1, const ElemConsts& c, const FieldPtrs& p, cudaStream_t st);
 void launch_gradient(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_update(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
-// Persistent TMA-pipelined element kernels (even N+1); return false when not applicable.
+// The warp-specialised persistent TMA gradient kernel for affine elements (even N+1);
+// false when not applicable (the plain launch_gradient then runs).
 bool launch_gradient_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
                          cudaStream_t st);
-bool launch_update_tma(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, int n_sm,
-                       cudaStream_t st);
-// Curved-element kernels (SDG_MAP_WARP; csrc/curved.cuh).
+// Curved-element kernels (SDG_MAP_WARP / SDG_MAP_ANNULUS; csrc/curved.cuh).
 void launch_gradient_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_update_curved(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
-// Affine elements through the bulk-loaded, non-persistent kernel structure of curved.cuh (even N+1;
-// false when not applicable).  Selected with SDG_AFFINE_B=1 instead of the persistent TMA kernels.
-bool launch_gradient_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
+// Affine update in the bulk-loaded, non-persistent structure of curved.cuh (even N+1;
+// false when not applicable: the plain launch_update then runs).
 bool launch_update_affine_b(int n1, const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st);
 void launch_pairing(const PairingArgs& a, const PairingPtrs& p, cudaStream_t st);
 // Mortars of one non-matching periodic face row (device merge_intervals, host.cpp).
@@ -227,6 +226,32 @@ void launch_nc_mortar_flux(long long nodes, const GasD& g, int dir, double vg, c
                            const double* ga, const double* gb, double* flux, int* bad, cudaStream_t st);
 void launch_nc_mortar_lift(long long nodes, const GasD& g, const double* ua, const double* ub, double* lift,
                            cudaStream_t st);
+// One non-matching / oblique interface at one stage, as the in-stage kernels see it.
+// Rows per direction d (0: y, 1: z): the host's (h_*, from which its operators were
+// built) and the device's (d_*, recomputed by k_nc_rows and used for indexing).
+// Side s = 0 (A, the left band's x+ faces) / 1 (B, the right band's x- faces).
+struct NcStage {
+  long long nfy[2], nfz[2];  // faces per side
+  long long my, mz;          // mortars per direction
+  long long n_a[2], n_b[2];  // row parameters per direction
+  double l_a[2], delta[2];
+  const long long* h_faces[2];
+  const double* h_ranges[2];
+  long long* d_faces[2];
+  double* d_ranges[2];
+  long long* d_n;                    // 2
+  const double* F[2][2];             // [side][dir]: forward (face -> mortar) n x n per row
+  const double* B[2][2];             // [side][dir]: backward (mortar -> face) n x n per row
+  const int* off[2][2];              // [side][dir]: CSR offsets over the side's face rows
+  const int* idx[2][2];              // [side][dir]: CSR row indices
+};
+void launch_nc_rows(const NcStage& S, int iface, ErrRec* err, cudaStream_t st);
+void launch_nc_fill(int n, int nc, const double* src, const NcStage& S, const int* const tab[2], double* const out[2],
+                    cudaStream_t st);
+void launch_nc_project(int n, int nc, const double* mortar, const NcStage& S, const int* const tab[2], double* dst,
+                       cudaStream_t st);
+void launch_nc_flux(long long nodes, const GasD& g, const double* ua, const double* ub, const double* ga,
+                    const double* gb, double* flux, ErrRec* err, cudaStream_t st);
 void launch_mortar_fill(int n1, int ncomp, const double* src, double* const dst[2], const MortarOps& ops,
                         const MortarPtrs& p, cudaStream_t st);
 void launch_mortar_lift(int n1, const GasD& g, const MortarPtrs& p, int max_mortars, cudaStream_t st);

@@ -46,6 +46,10 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
   ~DevBuf() {
     if (p) cudaFree(p);
   }
@@ -310,6 +314,8 @@ class GpuRankSolver {
     return t;
   }
   void ctx_info(int c, long* out5, double* sd, double* sig);
+  void nc_rows(int i, int dir, long* n_out, long* faces, double* ranges, double* delta);
+  int n_nc() const { return static_cast<int>(nc_.size()); }
   void get_pairing(int role, int* ncols, int* cols);
   void get_mapping(int c, int* m);
 
@@ -388,7 +394,6 @@ class GpuRankSolver {
   DevBuf<int8_t> side_type_, side_rot_;
   DevBuf<int> side_idx_, coords_, side_code_;
   int n_sm_ = 148;
-  bool use_tma_ = true;
   DevBuf<ErrRec> err_;
   ErrRec* err_host_ = nullptr;
   DevBuf<unsigned long long> dt_min_;
@@ -411,6 +416,30 @@ class GpuRankSolver {
   // per role: mortar blocks per partner (partner, offset, count) + self
   std::vector<std::array<int, 3>> sched_[2];
   std::array<int, 3> self_[2] = {{0, 0, 0}, {0, 0, 0}};
+
+  // Non-matching / oblique interfaces (BASELINE configs[1]; tensor-product mortars).
+  struct NcRuntime {
+    int iface = 0;                     // index into mesh_.nc_ifaces
+    double dy_base = 0.0, dz_base = 0.0;  // relative displacement of side B at time_ (per step)
+    double dy = 0.0, dz = 0.0;         // at the current stage
+    long long max_m[2] = {0, 0};       // row capacity per direction
+    DevBuf<int> slot[2], kidx[2];      // per side: face (fy * nfz + fz) -> trace slot / sliding index
+    DevBuf<long long> d_faces[2], d_n;
+    DevBuf<double> d_ranges[2];
+    DevBuf<double> mu[2], mg[2], mlift, mflux;  // mortar data [M][n2][nc]
+    NcStage S{};                       // tables of the current stage
+    size_t blob_off = 0, blob_bytes = 0;  // this interface's part of the per-stage upload
+  };
+  std::vector<NcRuntime> nc_;
+  DevBuf<unsigned char> nc_blob_;      // per-stage rows / operators / CSR of all NC interfaces
+  std::vector<unsigned char*> nc_pinned_;  // pinned staging ring for nc_blob_
+  std::vector<cudaEvent_t> nc_pinned_ev_;
+  int nc_ring_ = 0;
+  void build_nc();
+  void nc_prepare(double t_stage);
+  void nc_fill(bool grad);
+  void nc_lift();
+  void nc_flux();
 
   double time_ = 0.0;
   int step_index_ = 0, stage_index_ = 0;
@@ -443,7 +472,6 @@ GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& c
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaDeviceGetAttribute(&n_sm_, cudaDevAttrMultiProcessorCount, device), "device attribute");
-  if (const char* env = std::getenv("SDG_NO_TMA")) use_tma_ = env[0] == '0';
   if (n_ranks > 1) {
     if (inproc_hub) comm_ = std::make_unique<InProcComm>(inproc_hub, n_ranks, rank);
     else if (nccl_id) comm_ = std::make_unique<NcclComm>(nccl_id, n_ranks, rank);
@@ -453,10 +481,13 @@ GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& c
     cuda_check(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming), "event");
     sm_reserve_ = inproc_hub ? 0 : 8;
   }
+  if (n_ranks > 1 && !mesh_.nc_ifaces.empty())
+    throw ConfigError("non-matching / obliquely sliding interfaces run on a single rank");
   build_consts();
   upload_topology();
   find_interior_run();
   build_sides();
+  build_nc();
   cuda_check(cudaMallocHost(&err_host_, sizeof(ErrRec)), "cudaMallocHost");
   cuda_check(cudaStreamSynchronize(stream_), "setup sync");
 }
@@ -472,6 +503,8 @@ GpuRankSolver::~GpuRankSolver() {
   if (ev_ready_) cudaEventDestroy(ev_ready_);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  for (auto* p : nc_pinned_) cudaFreeHost(p);
+  for (auto ev : nc_pinned_ev_) cudaEventDestroy(ev);
   if (err_host_) cudaFreeHost(err_host_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -508,6 +541,7 @@ void GpuRankSolver::build_consts() {
     d.hy = bg.hy;
     d.hz = bg.hz;
     d.vg = bg.vg;
+    d.vgz = bg.vgz;
     const double jac = 0.125 * bg.hx * bg.hy * bg.hz;
     d.jac = jac;
     d.inv_jac = 1.0 / jac;
@@ -606,7 +640,7 @@ void GpuRankSolver::build_sides() {
       c.iface = ic;
       for (int k = 0; k < S_; ++k) {
         const auto& r = topo_.sliding[k];
-        if (r.iface == ic && (r.side == 1) == left) c.slides.push_back(k);
+        if (!r.nc && r.iface == ic && (r.side == 1) == left) c.slides.push_back(k);
       }
       if (c.slides.empty()) continue;
       c.on_static = mesh_.ifaces[ic].static_is_left == left;
@@ -791,6 +825,10 @@ void GpuRankSolver::reset_clock(double t0) {
     c.wraps = 0;
     c.topo_valid = false;
   }
+  for (auto& r : nc_) {
+    r.dy_base = mesh_.nc_ifaces[r.iface].vy_rel * t0;
+    r.dz_base = mesh_.nc_ifaces[r.iface].vz_rel * t0;
+  }
 }
 
 void GpuRankSolver::set_state(const double* h) {
@@ -899,6 +937,251 @@ std::vector<std::pair<double, long>> GpuRankSolver::timing_totals() {
     class_n_[c] = 0;
   }
   return out;
+}
+
+// ---------------------------------------------------------------------------
+// Non-matching / oblique interfaces (BASELINE configs[1]).  Per stage the host
+// displaces side B by (dy, dz), merges the face rows (merge_intervals) and builds
+// the long-double sub-range operators of every row and the face -> row CSR
+// lists; one upload carries them.  The device recomputes both rows
+// (k_nc_rows, checked against the host's: a mismatch is a ProtocolError) and
+// indexes the faces through its own rows.  Chain (the reference's mortar chain,
+// solver.cpp:234-252, 597-727, 442-526, on tensor-product mortars): traces ->
+// mortars -> lifting mean -> back to both sides (slide_lift); gradients ->
+// mortars -> two-sided Roe + viscous flux -> back to both sides (slide_flux).
+// The element kernels read slide_lift / slide_flux exactly as for the
+// reference's mortars.
+// ---------------------------------------------------------------------------
+void GpuRankSolver::build_nc() {
+  const int ni = static_cast<int>(mesh_.nc_ifaces.size());
+  if (ni == 0) return;
+  nc_.resize(ni);
+  size_t blob = 0;
+  for (int i = 0; i < ni; ++i) {
+    NcRuntime& r = nc_[i];
+    const NcIfaceGeom& f = mesh_.nc_ifaces[i];
+    r.iface = i;
+    std::vector<int> slot[2], kidx[2];
+    for (int s = 0; s < 2; ++s) {
+      slot[s].assign(f.nfy[s] * f.nfz[s], -1);
+      kidx[s].assign(f.nfy[s] * f.nfz[s], -1);
+    }
+    for (int k = 0; k < S_; ++k) {
+      const SlidingFaceRec& rec = topo_.sliding[k];
+      if (!rec.nc || rec.iface != i) continue;
+      const int s = rec.side == 1 ? 0 : 1;  // A: the left band's x+ faces
+      const long face = rec.i_par * f.nfz[s] + rec.i_perp;
+      slot[s][face] = 6 * rec.elem + rec.side;
+      kidx[s][face] = k;
+    }
+    for (int s = 0; s < 2; ++s) {
+      for (int v : slot[s])
+        if (v < 0) throw ConfigError("non-matching interface side is not complete on this rank");
+      r.slot[s].upload(slot[s], stream_);
+      r.kidx[s].upload(kidx[s], stream_);
+    }
+    r.max_m[0] = f.nfy[0] + f.nfy[1];
+    r.max_m[1] = f.nfz[0] + f.nfz[1];
+    for (int d = 0; d < 2; ++d) {
+      r.d_faces[d].alloc(2 * r.max_m[d]);
+      r.d_ranges[d].alloc(4 * r.max_m[d]);
+    }
+    r.d_n.alloc(2);
+    const size_t nodes = static_cast<size_t>(r.max_m[0] * r.max_m[1]) * n2_;
+    for (int s = 0; s < 2; ++s) {
+      r.mu[s].alloc(nodes * 5);
+      if (lifting_) r.mg[s].alloc(nodes * 12);
+    }
+    r.mlift.alloc(nodes * 4);
+    r.mflux.alloc(nodes * 5);
+    // Upload capacity: host rows, operators (F, B per side and row) and CSR.
+    size_t bytes = 0;
+    for (int d = 0; d < 2; ++d) {
+      const long long m = r.max_m[d];
+      const long long nf = d == 0 ? std::max(f.nfy[0], f.nfy[1]) : std::max(f.nfz[0], f.nfz[1]);
+      bytes += m * 2 * sizeof(long long) + m * 4 * sizeof(double);
+      bytes += 2 * 2 * m * n2_ * sizeof(double);
+      bytes += 2 * ((nf + 1 + m) * sizeof(int) + 8);
+    }
+    r.blob_off = blob;
+    r.blob_bytes = bytes + 256;  // + alignment of the 20 tables
+    blob += r.blob_bytes;
+  }
+  nc_blob_.alloc(blob);
+  for (int k = 0; k < 4; ++k) {
+    unsigned char* p = nullptr;
+    cuda_check(cudaMallocHost(&p, blob), "cudaMallocHost");
+    nc_pinned_.push_back(p);
+    cudaEvent_t ev;
+    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    nc_pinned_ev_.push_back(ev);
+  }
+}
+
+void GpuRankSolver::nc_prepare(double t_stage) {
+  const int slot = nc_ring_;
+  nc_ring_ = (nc_ring_ + 1) % static_cast<int>(nc_pinned_.size());
+  cuda_check(cudaEventSynchronize(nc_pinned_ev_[slot]), "nc staging reuse");
+  unsigned char* host = nc_pinned_[slot];
+  const int nn = n2_;
+  for (auto& r : nc_) {
+    const NcIfaceGeom& f = mesh_.nc_ifaces[r.iface];
+    r.dy = r.dy_base + f.vy_rel * (t_stage - time_);
+    r.dz = r.dz_base + f.vz_rel * (t_stage - time_);
+    NcStage& S = r.S;
+    S = NcStage{};
+    size_t off = r.blob_off;
+    auto take = [&](size_t bytes) {
+      off = (off + 7) & ~static_cast<size_t>(7);
+      const size_t o = off;
+      off += bytes;
+      if (off > r.blob_off + r.blob_bytes) throw ProtocolError("non-matching interface tables overflow");
+      return o;
+    };
+    for (int s = 0; s < 2; ++s) {
+      S.nfy[s] = f.nfy[s];
+      S.nfz[s] = f.nfz[s];
+    }
+    std::map<std::pair<double, double>, int> cache;
+    std::vector<double> opsF, opsB;
+    for (int d = 0; d < 2; ++d) {
+      const long n_a = d == 0 ? f.nfy[0] : f.nfz[0], n_b = d == 0 ? f.nfy[1] : f.nfz[1];
+      const double l_a = d == 0 ? f.ly[0] : f.lz[0], delta = d == 0 ? r.dy : r.dz;
+      const std::vector<MortarInterval> rows = merge_intervals(n_a, n_b, l_a, delta);
+      const long long m = static_cast<long long>(rows.size());
+      if (m > r.max_m[d]) throw ProtocolError("non-matching interface row exceeds its capacity");
+      (d == 0 ? S.my : S.mz) = m;
+      S.n_a[d] = n_a;
+      S.n_b[d] = n_b;
+      S.l_a[d] = l_a;
+      S.delta[d] = delta;
+      const size_t o_faces = take(m * 2 * sizeof(long long)), o_rng = take(m * 4 * sizeof(double));
+      auto* hf = reinterpret_cast<long long*>(host + o_faces);
+      auto* hr = reinterpret_cast<double*>(host + o_rng);
+      for (long long k = 0; k < m; ++k) {
+        hf[2 * k] = rows[k].face_a;
+        hf[2 * k + 1] = rows[k].face_b;
+        hr[4 * k] = rows[k].a_lo;
+        hr[4 * k + 1] = rows[k].a_hi;
+        hr[4 * k + 2] = rows[k].b_lo;
+        hr[4 * k + 3] = rows[k].b_hi;
+      }
+      S.h_faces[d] = reinterpret_cast<const long long*>(nc_blob_.p + o_faces);
+      S.h_ranges[d] = reinterpret_cast<const double*>(nc_blob_.p + o_rng);
+      S.d_faces[d] = r.d_faces[d].p;
+      S.d_ranges[d] = r.d_ranges[d].p;
+      for (int s = 0; s < 2; ++s) {
+        const size_t oF = take(m * nn * sizeof(double)), oB = take(m * nn * sizeof(double));
+        auto* F = reinterpret_cast<double*>(host + oF);
+        auto* B = reinterpret_cast<double*>(host + oB);
+        for (long long k = 0; k < m; ++k) {
+          const double lo = s == 0 ? rows[k].a_lo : rows[k].b_lo, hi = s == 0 ? rows[k].a_hi : rows[k].b_hi;
+          // Distinct sub-ranges of a row repeat with the face-count ratio: build each once.
+          auto it = cache.find({lo, hi});
+          if (it == cache.end()) {
+            const int id = static_cast<int>(opsF.size() / nn);
+            opsF.resize(opsF.size() + nn);
+            opsB.resize(opsB.size() + nn);
+            build_subrange_ops(basis_, lo, hi, opsF.data() + static_cast<size_t>(id) * nn,
+                               opsB.data() + static_cast<size_t>(id) * nn);
+            it = cache.emplace(std::make_pair(lo, hi), id).first;
+          }
+          std::copy_n(opsF.data() + static_cast<size_t>(it->second) * nn, nn, F + k * nn);
+          std::copy_n(opsB.data() + static_cast<size_t>(it->second) * nn, nn, B + k * nn);
+        }
+        S.F[s][d] = reinterpret_cast<const double*>(nc_blob_.p + oF);
+        S.B[s][d] = reinterpret_cast<const double*>(nc_blob_.p + oB);
+        // Face -> rows CSR of this side, rows in ascending order (a fixed summation order).
+        const long nf = s == 0 ? n_a : n_b;
+        const size_t oO = take((nf + 1) * sizeof(int)), oI = take(m * sizeof(int));
+        int* O = reinterpret_cast<int*>(host + oO);
+        int* I = reinterpret_cast<int*>(host + oI);
+        std::fill(O, O + nf + 1, 0);
+        for (long long k = 0; k < m; ++k) ++O[(s == 0 ? rows[k].face_a : rows[k].face_b) + 1];
+        for (long q = 0; q < nf; ++q) O[q + 1] += O[q];
+        std::vector<int> fill(O, O + nf);
+        for (long long k = 0; k < m; ++k) I[fill[s == 0 ? rows[k].face_a : rows[k].face_b]++] = static_cast<int>(k);
+        S.off[s][d] = reinterpret_cast<const int*>(nc_blob_.p + oO);
+        S.idx[s][d] = reinterpret_cast<const int*>(nc_blob_.p + oI);
+      }
+    }
+    S.d_n = r.d_n.p;
+  }
+  const size_t total = nc_blob_.n;
+  cuda_check(cudaMemcpyAsync(nc_blob_.p, host, total, cudaMemcpyHostToDevice, stream_), "nc tables h2d");
+  cuda_check(cudaEventRecord(nc_pinned_ev_[slot], stream_), "event record");
+  mark(KC_PAIRING, true);
+  for (auto& r : nc_) launch_nc_rows(r.S, r.iface, err_.p, stream_);
+  mark(KC_PAIRING, false);
+  launches_ += static_cast<long>(nc_.size());
+}
+
+// Face -> mortar of both sides: the traces (grad = false) or the gradient traces.
+void GpuRankSolver::nc_fill(bool grad) {
+  if (nc_.empty() || (grad && !lifting_)) return;
+  mark(KC_MORTAR, true);
+  for (auto& r : nc_) {
+    if (grad) {
+      const int* tab[2] = {r.kidx[0].p, r.kidx[1].p};
+      double* out[2] = {r.mg[0].p, r.mg[1].p};
+      launch_nc_fill(n_, 12, slide_g_.p, r.S, tab, out, stream_);
+    } else {
+      const int* tab[2] = {r.slot[0].p, r.slot[1].p};
+      double* out[2] = {r.mu[0].p, r.mu[1].p};
+      launch_nc_fill(n_, 5, trace_[cur_trace_].p, r.S, tab, out, stream_);
+    }
+    launches_++;
+  }
+  mark(KC_MORTAR, false);
+}
+
+// Lifting mean at the mortar nodes, projected back onto both sides (slide_lift).
+void GpuRankSolver::nc_lift() {
+  if (nc_.empty()) return;
+  mark(KC_MORTAR, true);
+  for (auto& r : nc_) {
+    const long long nodes = r.S.my * r.S.mz * n2_;
+    launch_nc_mortar_lift(nodes, consts_.gas, r.mu[0].p, r.mu[1].p, r.mlift.p, stream_);
+    const int* tab[2] = {r.kidx[0].p, r.kidx[1].p};
+    launch_nc_project(n_, 4, r.mlift.p, r.S, tab, slide_lift_.p, stream_);
+    launches_ += 2;
+  }
+  mark(KC_MORTAR, false);
+}
+
+// Two-sided flux at the mortar nodes, projected back onto both sides (slide_flux).
+void GpuRankSolver::nc_flux() {
+  if (nc_.empty()) return;
+  mark(KC_MORTAR, true);
+  for (auto& r : nc_) {
+    const long long nodes = r.S.my * r.S.mz * n2_;
+    launch_nc_flux(nodes, consts_.gas, r.mu[0].p, r.mu[1].p, lifting_ ? r.mg[0].p : nullptr,
+                   lifting_ ? r.mg[1].p : nullptr, r.mflux.p, err_.p, stream_);
+    const int* tab[2] = {r.kidx[0].p, r.kidx[1].p};
+    launch_nc_project(n_, 5, r.mflux.p, r.S, tab, slide_flux_.p, stream_);
+    launches_ += 2;
+  }
+  mark(KC_MORTAR, false);
+}
+
+// Device rows of the last stage (the pairing of a non-matching interface).
+void GpuRankSolver::nc_rows(int i, int dir, long* n_out, long* faces, double* ranges, double* delta) {
+  if (i < 0 || i >= static_cast<int>(nc_.size()) || dir < 0 || dir > 1)
+    throw ConfigError("no such non-matching interface / direction");
+  const NcRuntime& r = nc_[i];
+  long long n[2] = {0, 0};
+  cuda_check(cudaMemcpyAsync(n, r.d_n.p, sizeof(n), cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  *n_out = static_cast<long>(n[dir]);
+  if (delta) *delta = dir == 0 ? r.dy : r.dz;
+  if (faces == nullptr || ranges == nullptr || n[dir] <= 0) return;
+  std::vector<long long> f(2 * n[dir]);
+  cuda_check(cudaMemcpyAsync(f.data(), r.d_faces[dir].p, f.size() * sizeof(long long), cudaMemcpyDeviceToHost, stream_),
+             "d2h");
+  cuda_check(cudaMemcpyAsync(ranges, r.d_ranges[dir].p, 4 * n[dir] * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  for (size_t q = 0; q < f.size(); ++q) faces[q] = static_cast<long>(f[q]);
 }
 
 // update_interfaces (solver.cpp:156-176) on the host: displacement, sigma,
@@ -1051,25 +1334,16 @@ void GpuRankSolver::element_kernel(bool update, const FieldPtrs& fp0, const Stag
   fp.e_first = e_first;
   fp.E = e_end;
   mark(update ? KC_UPDATE : KC_GRADIENT, true);
-  // Affine elements: the update runs in the bulk-loaded, non-persistent structure
-  // of curved.cuh at 4 CTAs/SM (6.61 vs 6.88 ms for the persistent TMA kernel at
-  // N=5), the gradient in the warp-specialised persistent kernel (2.79 vs 4.22 ms).
-  // SDG_AFFINE_B: u (default) = update only, 1 = both, g = gradient only, 0 = neither.
-  static const int affine_b = [] {
-    const char* v = std::getenv("SDG_AFFINE_B");
-    if (v == nullptr) return 1;
-    return v[0] == '1' ? 3 : (v[0] == 'u' ? 1 : (v[0] == 'g' ? 2 : 0));
-  }();
+  // Affine elements (even N+1): the update in the bulk-loaded, non-persistent structure
+  // of curved.cuh at 4 CTAs/SM, the gradient in the warp-specialised persistent kernel
+  // (DESIGN.md §4); the plain kernels for odd N+1.
   if (curved_) {
     if (update) launch_update_curved(n_, consts_, fp, a, stream_);
     else launch_gradient_curved(n_, consts_, fp, a, stream_);
-  } else if ((affine_b & (update ? 1 : 2)) && (update ? launch_update_affine_b(n_, consts_, fp, a, stream_)
-                                                      : launch_gradient_affine_b(n_, consts_, fp, a, stream_))) {
   } else if (update) {
-    if (!(use_tma_ && launch_update_tma(n_, consts_, fp, a, n_sm, stream_))) launch_update(n_, consts_, fp, a, stream_);
+    if (!launch_update_affine_b(n_, consts_, fp, a, stream_)) launch_update(n_, consts_, fp, a, stream_);
   } else {
-    if (!(use_tma_ && launch_gradient_tma(n_, consts_, fp, a, n_sm, stream_)))
-      launch_gradient(n_, consts_, fp, a, stream_);
+    if (!launch_gradient_tma(n_, consts_, fp, a, n_sm, stream_)) launch_gradient(n_, consts_, fp, a, stream_);
   }
   mark(update ? KC_UPDATE : KC_GRADIENT, false);
   launches_++;
@@ -1127,10 +1401,14 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   const MortarPtrs mp = mortar_ptrs();
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
   mark(KC_MORTAR, true);
-  launch_mortar_fill(n_, 5, trace_[cur_trace_].p, u_src, fwd_ops_, mp, stream_);
+  if (!sides_.empty()) launch_mortar_fill(n_, 5, trace_[cur_trace_].p, u_src, fwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
-  launches_ += S_ > 0;
+  launches_ += !sides_.empty();
   mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
+  if (!nc_.empty()) {
+    nc_prepare(t_stage);
+    nc_fill(false);
+  }
   StageArgs a{t_stage, dt, rk_a, rk_b, mode, step_index_, stage_index_};
   // Element kernel over all local elements; with an exchange in flight, the interior run
   // first (on all but sm_reserve_ SMs), then the join, then the two boundary ranges.
@@ -1155,15 +1433,17 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
     mortar_exchange(l_src, mlift_[1].p, 4, false, MK_LIFT_MORTAR);
     mark(KC_MORTAR, true);
-    launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
+    if (!sides_.empty()) launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
-    launches_ += S_ > 0;
+    launches_ += !sides_.empty();
+    nc_lift();
     halo_and_elements(trace_[cur_trace_].p, 5, MK_SOL_CONF, false);
+    nc_fill(true);
     double* const g_src[2] = {g_mine_[0].p, g_mine_[1].p};
     mark(KC_MORTAR, true);
-    launch_mortar_fill(n_, 12, slide_g_.p, g_src, fwd_ops_, mp, stream_);
+    if (!sides_.empty()) launch_mortar_fill(n_, 12, slide_g_.p, g_src, fwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
-    launches_ += S_ > 0;
+    launches_ += !sides_.empty();
     mortar_exchange(g_src, g_theirs_.p, 12, true, MK_GRAD_MORTAR);
   }
   mark(KC_MORTAR, true);
@@ -1173,9 +1453,10 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
   double* const f_src[2] = {mflux_[0].p, mflux_[1].p};
   mortar_exchange(f_src, mflux_[1].p, 5, false, MK_FLUX_MORTAR);
   mark(KC_MORTAR, true);
-  launch_mortar_backproject(n_, 5, f_src, slide_flux_.p, bwd_ops_, mp, stream_);
+  if (!sides_.empty()) launch_mortar_backproject(n_, 5, f_src, slide_flux_.p, bwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
-  launches_ += S_ > 0;
+  launches_ += !sides_.empty();
+  nc_flux();
   // Viscous: Fv.n of the remote faces; inviscid: the traces themselves.
   if (lifting_) halo_and_elements(fvn_.p, 4, MK_FVN_CONF, true);
   else halo_and_elements(trace_[cur_trace_].p, 5, MK_SOL_CONF, true);
@@ -1223,6 +1504,11 @@ void GpuRankSolver::check_error() {
   err_.zero(stream_);
   cuda_check(cudaStreamSynchronize(stream_), "stream sync");
   std::ostringstream os;
+  if (r.flag == 4) {
+    os << "device rows of non-matching interface " << r.elem << " (" << (r.node ? "z" : "y")
+       << ") disagree with the host's";
+    throw ProtocolError(os.str());
+  }
   if (r.flag == 3) {
     os << "device pairing disagrees with the host schedule (role " << r.elem << ", " << r.node << " mortars)";
     throw ProtocolError(os.str());
@@ -1271,6 +1557,16 @@ void GpuRankSolver::rk_stage(int s, double t, double dt) {
       ++c.wraps;
     }
   }
+  for (auto& r : nc_) {  // the same bookkeeping for both directions of an oblique slide
+    const NcIfaceGeom& f = mesh_.nc_ifaces[r.iface];
+    r.dy_base += f.vy_rel * dt;
+    r.dz_base += f.vz_rel * dt;
+    const double py = f.ly[0] * static_cast<double>(f.nfy[0]), pz = f.lz[0] * static_cast<double>(f.nfz[0]);
+    while (r.dy_base >= py) r.dy_base -= py;
+    while (r.dy_base < 0.0) r.dy_base += py;
+    while (r.dz_base >= pz) r.dz_base -= pz;
+    while (r.dz_base < 0.0) r.dz_base += pz;
+  }
 }
 
 // update_interfaces (solver.cpp:156-176) as an entry point: displacement, sigma
@@ -1311,6 +1607,11 @@ void GpuRankSolver::compute_gradients(double t_stage, const double* d_u, double*
   double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
   mortar_exchange(l_src, mlift_[1].p, 4, false, MK_LIFT_MORTAR);
   launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
+  if (!nc_.empty()) {
+    nc_prepare(t_stage);
+    nc_fill(false);
+    nc_lift();
+  }
   fp.grad_out = d_grad;
   ElemConsts c = consts_;
   c.gas.viscous = 1;
@@ -2160,6 +2461,10 @@ long sdg_total_rebuilds(const sdg_ctx* c) { return c->s->total_rebuilds(); }
 int sdg_n_contexts(const sdg_ctx* c) { return c->s->n_contexts(); }
 int sdg_ctx_info(sdg_ctx* c, int id, long* out5, double* sd, double* sig) {
   return guarded(c, [&] { c->s->ctx_info(id, out5, sd, sig); });
+}
+int sdg_n_nc_interfaces(const sdg_ctx* c) { return c->s->n_nc(); }
+int sdg_nc_rows(sdg_ctx* c, int iface, int dir, long* n_out, long* faces, double* ranges, double* delta) {
+  return guarded(c, [&] { c->s->nc_rows(iface, dir, n_out, faces, ranges, delta); });
 }
 int sdg_get_pairing(sdg_ctx* c, int role, int* ncols, int* cols) {
   return guarded(c, [&] { c->s->get_pairing(role, ncols, cols); });

@@ -16,6 +16,7 @@ TUPLE_INTS = 7
 
 OK, ERR_CONFIG, ERR_INVALID_STATE, ERR_PROTOCOL, ERR_CUDA, ERR_NCCL = range(6)
 NODES_LGL, NODES_GAUSS = 0, 1
+MORTARS_AUTO, MORTARS_TENSOR = 0, 1
 CASE_FREESTREAM, CASE_DENSITY_WAVE, CASE_VORTEX, CASE_TGV, CASE_SWIRL = range(5)
 
 
@@ -34,6 +35,7 @@ class MeshSpec(C.Structure):
         ("periodic_x", C.c_int), ("periodic_y", C.c_int), ("periodic_z", C.c_int),
         ("partition", C.c_int),
         ("mapping", C.c_int), ("warp", C.c_double),
+        ("mortars", C.c_int), ("pad_", C.c_int),
     ]
 
 
@@ -50,6 +52,9 @@ class Case(C.Structure):
         ("vx_theta", C.c_double), ("vx_ma_inf", C.c_double), ("vx_center", C.c_double * 2),
         ("tgv_rho0", C.c_double), ("tgv_v0", C.c_double), ("tgv_mach", C.c_double),
         ("sw_omega", C.c_double),
+        ("pt_modes", C.c_int), ("pt_coords", C.c_int), ("pt_amp", C.c_double),
+        ("pt_x0", C.c_double * 3), ("pt_len", C.c_double * 3), ("pt_adv", C.c_double * 3),
+        ("pt_k", (C.c_double * 3) * 8), ("pt_a", C.c_double * 8), ("pt_phi", C.c_double * 8),
     ]
 
 
@@ -94,7 +99,8 @@ MAP_BOX, MAP_WARP, MAP_ANNULUS = 0, 1, 2
 
 
 def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z0=0.0,
-              periodic=(True, True, True), partition=PARTITION_LEX, warp=None, mapping=None) -> MeshSpec:
+              periodic=(True, True, True), partition=PARTITION_LEX, warp=None, mapping=None,
+              mortars=0) -> MeshSpec:
     """bands: list of (nx, width_frac, vg_y[, ny, nz, vg_z]) tuples, stacked along x
     (ny / nz = 0: the mesh-wide counts; bands with other counts meet at a
     non-matching sliding interface; vg_z: slide along z).  warp: None for
@@ -118,6 +124,7 @@ def mesh_spec(bands, ny, nz, width=2.0, height=2.0, depth=2.0, x0=0.0, y0=0.0, z
     m.partition = int(partition)
     m.mapping = (MAP_BOX if warp is None else MAP_WARP) if mapping is None else int(mapping)
     m.warp = 0.0 if warp is None else float(warp)
+    m.mortars = int(mortars)
     return m
 
 
@@ -175,6 +182,84 @@ def swirl(alpha=0.1, a=1.0, k=1.0, p0=5.0, omega=0.5) -> Case:
     c.kind = CASE_SWIRL
     c.dw_alpha, c.dw_p0, c.sw_omega = alpha, p0, omega
     c.dw_a[0], c.dw_k[0] = a, k
+    return c
+
+
+class MT19937_64:
+    """std::mt19937_64 (the 64-bit Mersenne Twister of C++11 <random>), so the seeded
+    inputs of SURVEY §8(d) -- mt19937_64(2008043560 + config index) -- are the same
+    numbers a C++ harness would draw."""
+    N, M = 312, 156
+    MATRIX_A, UPPER, LOWER = 0xB5026F5AA96619E9, 0xFFFFFFFF80000000, 0x7FFFFFFF
+    MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        self.mt = [0] * self.N
+        self.mt[0] = seed & self.MASK
+        for i in range(1, self.N):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & self.MASK
+        self.idx = self.N
+
+    def __call__(self) -> int:
+        if self.idx >= self.N:
+            mt = self.mt
+            for i in range(self.N):
+                x = (mt[i] & self.UPPER) | (mt[(i + 1) % self.N] & self.LOWER)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= self.MATRIX_A
+                mt[i] = mt[(i + self.M) % self.N] ^ xa
+            self.idx = 0
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self.MASK
+
+    def uniform(self) -> float:
+        """[0, 1) with 53 random bits."""
+        return (self() >> 11) * (1.0 / 9007199254740992.0)
+
+
+SEED_BASE = 2008043560
+
+
+def seeded_modes(config_index: int, kmax: int, n_modes: int = 8):
+    """The 8 Fourier modes of SURVEY §8(d): draw with mt19937_64(2008043560 + i), per
+    mode k in {-kmax..kmax}^3 minus 0 (k_d = draw mod (2 kmax + 1) - kmax, redrawn
+    while k = 0), a ~ U(-1, 1), phi ~ U[0, 2 pi); a normalised to sum |a| = 1.
+    Returns (k [n,3], a [n], phi [n])."""
+    rng = MT19937_64(SEED_BASE + config_index)
+    ks, a, phi = [], [], []
+    for _ in range(n_modes):
+        while True:
+            k = [int(rng() % (2 * kmax + 1)) - kmax for _ in range(3)]
+            if any(k):
+                break
+        ks.append(k)
+        a.append(2.0 * rng.uniform() - 1.0)
+        phi.append(2.0 * math.pi * rng.uniform())
+    s = sum(abs(x) for x in a)
+    return ks, [x / s for x in a], phi
+
+
+def perturbed(case: Case, config_index: int, amp: float, kmax: int, x0, length, adv=(0.0, 0.0, 0.0),
+              cylindrical: bool = False) -> Case:
+    """`case` plus the seeded density perturbation of SURVEY §8(d) (include/sdg_types.h
+    sdg_case.pt_*): amp * sum_m a_m sin(2 pi k_m . xh + phi_m), xh = (c - x0) / length with
+    c the point advected by `adv` (cylindrical: (x, theta, r) about the x axis)."""
+    ks, a, phi = seeded_modes(config_index, kmax)
+    c = Case()
+    C.pointer(c)[0] = case
+    c.pt_modes, c.pt_coords, c.pt_amp = len(ks), 1 if cylindrical else 0, amp
+    for d in range(3):
+        c.pt_x0[d], c.pt_len[d], c.pt_adv[d] = x0[d], length[d], adv[d]
+    for m in range(len(ks)):
+        for d in range(3):
+            c.pt_k[m][d] = ks[m][d]
+        c.pt_a[m], c.pt_phi[m] = a[m], phi[m]
     return c
 
 

@@ -49,7 +49,7 @@ def test_struct_layout_matches_header():
     # sizes follow include/sdg_types.h field order (x86-64 ABI)
     assert ctypes.sizeof(T.BandSpec) == 40
     assert ctypes.sizeof(T.Gas) == 32
-    assert ctypes.sizeof(T.MeshSpec) == 6 * 8 + 3 * 4 + 4 + 16 * 40 + 4 * 4 + 4 + 4 + 8
+    assert ctypes.sizeof(T.MeshSpec) == 6 * 8 + 3 * 4 + 4 + 16 * 40 + 4 * 4 + 4 + 4 + 8 + 4 + 4
 
 
 def test_library_exports_nothing_but_the_c_abi():
