@@ -1,17 +1,22 @@
 """Benchmark of the B200 sliding-mesh DG right-hand side + RK step.
 
-Workload (BASELINE.json configs[4], the largest configuration the reference's
-algorithm covers on one GPU — configs[1]-[3] need non-matching / oblique /
-curved / rotating interfaces that neither the reference nor this round
-implements): Taylor-Green vortex in [0, 2pi]^3 at M=0.1,
-Re=1600, three blocks stacked along BASELINE z with two planar sliding
-interfaces at 2pi/3 and 4pi/3, middle block sliding at +0.2 along BASELINE x;
-64^3 elements per GPU, N=5 Gauss nodes, fp64, viscous.  One "step" = one
-5-stage low-storage RK step (5 right-hand sides + mortars + updates).
+Default workload: BASELINE.json configs[3], the turbine-scale synthetic the
+north star's targets are quoted on -- a 20-degree rotationally periodic annulus
+sector, stator / rotor / stator, two sliding interfaces, 1.1M curved hexahedra
+(5% warp), N=5 Gauss, fp64, viscous, seeded broadband 1e-2 initial perturbation
+(SURVEY §8(d)), strong scaling over the GPUs.  --mesh tgv runs configs[4] (TGV,
+affine hexahedra, 64^3 elements per GPU, weak scaling); --mesh warped the same
+TGV on curved hexahedra.  configs[0]-[2] are parity cases (tests/).  One "step"
+= one 5-stage low-storage RK step (5 right-hand sides + mortars + updates).
 
-metric: DOF-updates/s = E*(N+1)^3 * 5 * steps / time, whole job over all GPUs.
+metric: BASELINE's "DOF-updates/s (1/PID) per GPU" quantity; `value` is the
+whole-job aggregate over all GPUs (E*(N+1)^3 * 5 * steps / time, max over
+ranks), `value_per_gpu` = value / n_gpus.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mesh rotor|tgv|warped]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
@@ -45,7 +50,8 @@ def parse():
     p.add_argument("--elems", type=int, default=64, help="elements per direction per GPU (weak scaling)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--mesh", default="tgv", choices=["tgv", "warped", "rotor"],
+    p.add_argument("--dry-run", action="store_true", help="stop before the first CUDA call (launcher test)")
+    p.add_argument("--mesh", default="rotor", choices=["tgv", "warped", "rotor"],
                    help="tgv: affine hexahedra (configs[4]); warped: the same case on curved hexahedra "
                         "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3]); rotor: configs[3], "
                         "1.1M-element stator/rotor/stator 20-degree annulus sector (SDG_MAP_ANNULUS), strong scaling")
@@ -68,37 +74,47 @@ def tgv_mesh(T, elems_x, elems_yz, warp=None, copies=1):
 WARP = 0.05  # BASELINE configs[3]: "sinusoidal mesh warping of amplitude 5% of element size"
 
 
-def rotor_workload(args, world, elements=None):
+def rotor_workload(args, world, elements=None, span_div=1):
     """BASELINE configs[3] (turbine-scale synthetic): three axial blocks (stator,
     rotor, stator) of a 20-degree periodic annulus sector r in [0.8, 1] with two
     sliding interfaces, 5% warping inside the blocks (x and r), tip Mach 0.4,
-    axial inflow M = 0.3 (density-wave perturbation 1e-2), Re = 8e5 on the
-    mean-radius arc of the sector, N = 5.  About 1.1M curved hexahedra in total
-    (192 axial x 96 around x 60 radial), partitioned over the GPUs (strong
-    scaling).  `elements` = (nx, n_theta, n_r) overrides the mesh (CPU sample)."""
+    axial free stream M = 0.3 with the seeded broadband perturbation of SURVEY
+    §8(d) (amplitude 1e-2, 8 modes |k| <= 8 in the sector's (x, theta, r),
+    mt19937_64(2008043560 + 3)), Re = 8e5 on the mean-radius arc of the sector,
+    N = 5.  About 1.1M curved hexahedra (192 axial x 96 around x 60 radial),
+    partitioned over the GPUs (strong scaling).  `elements` = (nx, n_theta, n_r)
+    and `span_div` (a periodic 1/span_div slice of the sector, same element size)
+    shape the CPU sample."""
     from paper_2008_04356_b200 import types as T
-    gamma, mach, rho0, u0 = 1.4, 0.3, 2.0, 1.0
+    gamma, mach, rho0, u0 = 1.4, 0.3, 1.0, 1.0
     p0 = rho0 * u0 * u0 / (gamma * mach * mach)
     c0 = math.sqrt(gamma * p0 / rho0)
     r_in, r_out = 0.8, 1.0
     omega = 0.4 * c0 / r_out
-    span = math.pi / 9.0
-    chord = 0.5 * (r_in + r_out) * span
+    sector = math.pi / 9.0
+    span = sector / span_div
+    chord = 0.5 * (r_in + r_out) * sector
     mu = rho0 * u0 * chord / 8e5
     nx, n_theta, n_r = elements or (192, 96, 60)
     base, rem = divmod(nx, 3)
     n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
     bands = [(n[0], 1.0, 0.0), (n[1], 1.0, omega), (n[2], 1.0, 0.0)]
-    mesh = T.annulus_spec(bands, n_theta, n_r, r_in, r_out, length=1.0, warp=WARP, theta_span=span)
-    cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=gamma, R=1.0, mu=mu, Pr=0.72,
-                          case=T.density_wave(alpha=0.02, a=(u0, 0.0, 0.0), k=(2.0, 0.0, 0.0), p0=p0))
+    # Over several GPUs: theta slabs through all three blocks (partition 2), equal work per
+    # GPU and rotor/stator mortars mostly rank-local; one GPU: the whole sector.
+    mesh = T.annulus_spec(bands, n_theta, n_r, r_in, r_out, length=1.0, warp=WARP, theta_span=span,
+                          partition=T.PARTITION_YSLAB if world > 1 else T.PARTITION_LEX)
+    case = T.perturbed(T.freestream(rho=rho0, v=(u0, 0.0, 0.0), p=p0), 3, 1e-2, 8, (0.0, 0.0, r_in),
+                       (1.0, sector, r_out - r_in), adv=(u0, 0.0, 0.0), cylindrical=True)
+    cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=gamma, R=1.0, mu=mu, Pr=0.72, case=case)
     n1 = args.degree + 1
     E = nx * n_theta * n_r
     conf = {
         "workload": f"BASELINE configs[3]: stator/rotor/stator annulus sector r in [{r_in}, {r_out}], 20 degrees "
                     f"(rotationally periodic), 2 sliding interfaces, rotor omega {omega:.4f} (tip Mach 0.4), "
-                    f"warp {WARP}, axial M=0.3 inflow with 1e-2 density perturbation, Re=8e5, "
+                    f"warp {WARP}, axial M=0.3 free stream + seeded broadband 1e-2 density perturbation "
+                    f"(8 modes |k|<=8, mt19937_64 seed 2008043563), Re=8e5, "
                     f"{nx}x{n_theta}x{n_r} = {E} curved hexahedra over {world} GPU(s), N={args.degree} Gauss, viscous",
+        "mesh": "rotor",
         "geometry": "curved",
         "elements": E,
         "elements_per_gpu": E // world,
@@ -107,7 +123,8 @@ def rotor_workload(args, world, elements=None):
         "dof": E * n1 ** 3,
         "bands_nx": n,
         "l2_policy": "inputs larger than L2 (state %.0f MB per GPU)" % (E // world * n1 ** 3 * 40 / 1e6),
-        "parallelism": f"dp{world} (element partition, NCCL halo + mortar exchange)",
+        "parallelism": (f"dp{world} (theta slabs through all three blocks, NCCL halo + mortar exchange)"
+                        if world > 1 else "dp1"),
         "scaling": "strong",
     }
     return mesh, cfg, conf, E * n1 ** 3
@@ -127,6 +144,7 @@ def workload(args, world):
     conf = {
         "workload": f"BASELINE configs[4]: TGV M=0.1 Re=1600, 3 blocks, 2 planar sliding interfaces (middle +0.2), "
                     f"{args.elems}^3 elements/GPU, N={args.degree} Gauss, viscous, {geom}",
+        "mesh": args.mesh,
         "geometry": "curved" if curved else "affine",
         "elements": E,
         "elements_per_gpu": E // world,
@@ -194,53 +212,67 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(args, conf, timeout_s=20.0):
-    """The 3D CPU oracle (restatement of the reference path, 'port') on a bounded
-    sample of the same workload: same case/degree, reduced mesh, all host threads."""
-    from oracle import pyoracle as P
-    from paper_2008_04356_b200 import types as T
-    threads = os.cpu_count() or 1
-    P.oracle_lib().orc_set_threads(threads)
-    e = 6
-    curved = conf.get("geometry") == "curved"
-    if args.mesh == "rotor":
-        mesh, cfg, _, _ = rotor_workload(args, 1, elements=(9, 12, 4))
-        e = "9x12x4"
-    else:
-        mesh, bands = tgv_mesh(T, e, e, warp=WARP if curved else None)
-        cfg = T.solver_config(args.degree, T.NODES_GAUSS, mu=1.0 / 1600.0, case=T.tgv())
-    o = P.Oracle3D(mesh, cfg)
-    o.set_initial_condition(0.0)
-    # A timing sample, not a simulation: a small fixed step (well inside the CFL limit) keeps
-    # the coarse sample admissible for the whole window (an under-resolved TGV at CFL 0.5
-    # leaves the admissible set after ~1000 steps).
-    dt = min(1e-3, 0.25 * o.suggest_dt(1.0))
-    o.step(dt, 1)  # warm-up
-    steps, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < timeout_s or steps == 0:
-        try:
-            o.step(dt, 1)
-        except P.T.InvalidStateError if hasattr(P, "T") else Exception:
-            if steps == 0:
-                raise
-            break
-        steps += 1
-    el = time.perf_counter() - t0
-    dof = o.n_elements * (args.degree + 1) ** 3
-    model = ""
+def host_model():
     try:
         for ln in open("/proc/cpuinfo"):
             if ln.startswith("model name"):
-                model = ln.split(":", 1)[1].strip()
-                break
+                return ln.split(":", 1)[1].strip()
     except OSError:
         pass
+    return ""
+
+
+def cpu_sample(args, conf):
+    """The oracle on the printed workload: the full mesh for the TGV cases (one step
+    of 64^3 elements is ~15 s on 16 host threads); for configs[3] a periodic 1/8
+    theta slice of the sector -- all 192 axial x 60 radial elements, 12 of the 96
+    around, the same element geometry, case and degree (the whole 1.1M-element mesh
+    would need ~140 GB of host memory in the oracle).  Per-DOF work is identical, so
+    DOF-updates/s compare directly.  Returns (oracle, description)."""
+    from oracle import pyoracle as P
+    from paper_2008_04356_b200 import types as T
+    if args.mesh == "rotor":
+        mesh, cfg, sconf, _ = rotor_workload(args, 1, elements=(192, 12, 60), span_div=8)
+        desc = f"configs[3] periodic 1/8 theta slice (192x12x60 = {sconf['elements']} elements of the full mesh's geometry)"
+    else:
+        curved = args.mesh == "warped"
+        mesh, _ = tgv_mesh(T, args.elems, args.elems, warp=WARP if curved else None)
+        cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
+        desc = f"the full printed mesh ({conf['elements_per_gpu']} elements)"
+    o = P.Oracle3D(mesh, cfg)
+    o.set_initial_condition(0.0)
+    return o, desc
+
+
+def time_oracle(o, args, max_steps, budget_s, warmup=1):
+    dt = 0.25 * o.suggest_dt(0.5)
+    for _ in range(warmup):
+        o.step(dt, 1)
+    steps, t0 = 0, time.perf_counter()
+    while steps < max_steps and (steps == 0 or time.perf_counter() - t0 < budget_s):
+        o.step(dt, 1)
+        steps += 1
+    return steps, time.perf_counter() - t0
+
+
+def cpu_baseline(args, conf, budget_s=20.0, max_steps=100, warmup=1):
+    """The 3D CPU oracle (restatement of the reference path, 'port'; the reference
+    library itself is 2D) with all host threads on the printed workload
+    (cpu_sample), timed over whole RK steps after `warmup` steps."""
+    from oracle import pyoracle as P
+    threads = os.cpu_count() or 1
+    P.oracle_lib().orc_set_threads(threads)
+    t_setup = time.perf_counter()
+    o, desc = cpu_sample(args, conf)
+    setup = time.perf_counter() - t_setup
+    steps, el = time_oracle(o, args, max_steps, budget_s, warmup)
+    dof = o.n_elements * (args.degree + 1) ** 3
     out = {"value": dof * 5 * steps / el, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {model}) on the same "
-                     f"{'rotor annulus' if args.mesh == 'rotor' else 'TGV'} case"
-                     f"{' (curved)' if curved else ''} at {e if isinstance(e, str) else f'{e}^3'} elements (N={args.degree}, {dof} DOF), {steps} RK steps in {el:.1f} s"}
+           "sample": f"oracle/sdg3d.cpp (OpenMP, {threads} threads, {host_model()}) on {desc}, N={args.degree}, "
+                     f"{dof} DOF: {steps} RK step(s) in {el:.1f} s after {warmup} warm-up step(s) "
+                     f"(setup {setup:.0f} s untimed)"}
     try:
-        out["reference_2d"] = reference_2d(args.degree, seconds=min(8.0, timeout_s))
+        out["reference_2d"] = reference_2d(args.degree, seconds=8.0)
     except Exception as ex:  # supplementary: never fail the bench line over it
         out["reference_2d"] = {"unavailable": str(ex)[:200]}
     return out
@@ -270,16 +302,18 @@ def reference_2d(degree, seconds=8.0):
 
 
 def reference_arm(args, world, rank):
-    """--impl reference: the CPU implementation of the path on the host cores.
-    The reference library itself is 2D-only, so the 3D restatement
-    of its algorithm (oracle/sdg3d.cpp, 'port') runs this arm."""
+    """--impl reference: the CPU implementation of the path on the host cores, on
+    this arm's workload (cpu_sample).  The reference library itself is 2D-only
+    (SURVEY §0), so the 3D restatement of its algorithm (oracle/sdg3d.cpp, 'port')
+    runs this arm.  Steps are whole RK steps of the sample; K and W are capped so
+    the run stays within a few minutes."""
     if rank != 0:
         return
-    mesh, cfg, conf, dof = workload(args, 1)
-    base = cpu_baseline(args, conf, timeout_s=max(2.0, 3.0 * args.steps / max(args.steps + args.warmup, 1)))
+    mesh, cfg, conf, dof = workload(args, world)
+    base = cpu_baseline(args, conf, budget_s=60.0, max_steps=args.steps, warmup=min(args.warmup, 1))
     line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": conf.get("scaling", "weak"),
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (TGV initial field, analytic)",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded analytic initial field)",
             "config": conf, "impl": "reference", "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -305,20 +339,24 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     bf = b_flow(args.degree, curved)
     stage_ms = ms_per_step / 5.0
     ach = value_per_gpu * bf / 1e9
-    traffic = None
-    prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*stage_traffic*.json")))
-    prof = [p for p in prof if ("curved" in os.path.basename(p)) == curved]
-    if prof:
+    # ncu DRAM bytes of the stage's element kernels, from a capture of this exact
+    # workload (tools/summarize_ncu.py writes the workload key into the file).
+    traffic, traffic_src = None, None
+    key = {"mesh": conf.get("mesh"), "degree": args.degree, "elements_per_gpu": E}
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_stage_traffic.json")), key=os.path.getmtime):
         try:
-            traffic = json.load(open(prof[-1])).get("dram_bytes_per_stage")
+            d = json.load(open(p))
         except Exception:
-            traffic = None
+            continue
+        if d.get("workload") == key:
+            traffic, traffic_src = d.get("dram_bytes_per_stage"), os.path.relpath(p, ROOT)
     rl = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
           "kernel": "RK stage = k_gradient + k_update + mortar/pairing kernels (one right-hand side + update)",
           "algorithmic_bytes_per_launch": bf * dof, "bytes_per_dof": bf,
           "per_unit_source": ("SURVEY.md §8(d) B_flow,curved = 400 + 2904/(N+1) B per DOF-update (curved)" if curved
                               else "SURVEY.md §8(d) B_flow = 240 + 2712/(N+1) B per DOF-update (affine)"),
-          "mean_launch_ms": stage_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+          "mean_launch_ms": stage_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
+          "traffic_source": traffic_src}
     extra = {}
     # This implementation's fused dataflow.
     per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 18), "gradient": 8 * E * (5 * n3 + 6 * n2 * 9)}
@@ -342,11 +380,27 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     return rl, extra
 
 
+def relaunch(args):
+    """`--gpus N` outside torchrun: N ranks through torch.distributed.run (the
+    driver's own launch line), one per GPU."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         reference_arm(args, world, rank)
         return
@@ -354,7 +408,6 @@ def main():
     import torch
     from paper_2008_04356_b200 import capi
 
-    torch.cuda.set_device(local)
     nccl_id = None
     dist = None
     if world > 1:
@@ -365,6 +418,17 @@ def main():
         nccl_id = obj[0]
 
     mesh, cfg, conf, dof = workload(args, world)
+    if args.dry_run:
+        # Everything up to the first CUDA call: the rank's share of the partition.
+        plan = capi.plan(mesh, world, rank)
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "nccl_id_bytes": len(nccl_id or b""),
+                          "elements": len(plan["elements"]), "interior_run": plan["interior_run"],
+                          "halo_peers": [h["partner"] for h in plan["halo"]], "config": conf}), flush=True)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    torch.cuda.set_device(local)
     s = capi.RankSolver(mesh, cfg, n_ranks=world, rank=rank, device=local, nccl_id=nccl_id)
     s.set_initial_condition(0.0)
     dt = s.suggest_dt(0.5)
@@ -438,7 +502,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": conf.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (analytic initial field)", "config": conf,
+                "data": "synthetic (seeded analytic initial field; no dataset)", "config": conf,
+                "metric_note": "value = whole-job aggregate over n_gpus; value_per_gpu = value / n_gpus",
                 "value_per_gpu": value / world, "dt": dt, "gpu_launches": launches,
                 "clocks": clk.summary(), "roofline": roof, "kernels": extra, "e2e": e2e}
         if world == 1 and not args.no_cpu_baseline:

@@ -304,12 +304,30 @@ LocalTopology build_topology(const MeshGeom& mesh, const Partition& part, int ra
   for (int b = 0; b < nb; ++b)
     for (const auto& blk : part.band_blocks[b]) {
       if (blk.rank != rank) continue;
-      for (long o = blk.start; o < blk.start + blk.count; ++o) {
-        const long g = mesh.bands[b].off + part.lex(b, o);
-        local_of[g] = static_cast<int>(t.gids.size());
-        t.gids.push_back(g);
-      }
+      for (long o = blk.start; o < blk.start + blk.count; ++o) t.gids.push_back(mesh.bands[b].off + part.lex(b, o));
     }
+  // Local order: elements whose six neighbours are all on this rank first (stable), then
+  // the rank-boundary elements, so the element kernels can run the interior as one range
+  // while the halo exchange is in flight (interior_run).
+  if (part.n_ranks > 1) {
+    std::vector<long> inner, outer;
+    for (const long g : t.gids) {
+      int b, ix, iy, iz;
+      mesh.locate(g, b, ix, iy, iz);
+      bool remote = false;
+      for (int s = 0; s < 6 && !remote; ++s) {
+        const Nbr n = neighbour(mesh, b, ix, iy, iz, s);
+        if (n.kind == 0) {
+          const long ng = mesh.gid(n.band, n.ix, n.iy, n.iz);
+          remote = part.owner(n.band, ng - mesh.bands[n.band].off) != rank;
+        }
+      }
+      (remote ? outer : inner).push_back(g);
+    }
+    t.gids = inner;
+    t.gids.insert(t.gids.end(), outer.begin(), outer.end());
+  }
+  for (size_t q = 0; q < t.gids.size(); ++q) local_of[t.gids[q]] = static_cast<int>(q);
   const int ne = static_cast<int>(t.gids.size());
   t.coords.resize(4 * ne);
   t.side_type.assign(6 * ne, kConforming);
@@ -1120,8 +1138,9 @@ std::array<int, 2> interior_run(const LocalTopology& topo) {
     bool interior = e < E;
     for (int s = 0; interior && s < 6; ++s) {
       const size_t k = static_cast<size_t>(e) * 6 + s;
-      if (topo.side_type[k] == kSliding || (topo.side_type[k] == kConforming && topo.side_idx[k] >= 6 * E))
-        interior = false;
+      // Mortar data are complete before the element kernels (the mortar rounds are joined
+      // at once); only remote conforming neighbours arrive with the overlapped halo round.
+      if (topo.side_type[k] == kConforming && topo.side_idx[k] >= 6 * E) interior = false;
     }
     if (!interior) {
       if (e - run_lo > best_len) {

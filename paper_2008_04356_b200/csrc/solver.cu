@@ -476,7 +476,11 @@ GpuRankSolver::GpuRankSolver(const sdg_mesh_spec& ms, const sdg_solver_config& c
     if (inproc_hub) comm_ = std::make_unique<InProcComm>(inproc_hub, n_ranks, rank);
     else if (nccl_id) comm_ = std::make_unique<NcclComm>(nccl_id, n_ranks, rank);
     else throw ConfigError("multi-rank context needs an NCCL unique id or an in-process hub name");
-    cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    // Highest priority: the NCCL kernels of an overlapped round take the SM slots the
+    // element kernel's CTAs free first, instead of queueing behind the whole grid.
+    int lo_prio = 0, hi_prio = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "stream priority range");
+    cuda_check(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
     cuda_check(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming), "event");
     sm_reserve_ = inproc_hub ? 0 : 8;

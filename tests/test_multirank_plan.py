@@ -157,32 +157,31 @@ def _neighbours(mesh, g):
     return b, out
 
 
-@pytest.mark.parametrize("partition", [T.PARTITION_LEX, T.PARTITION_SFC])
+@pytest.mark.parametrize("partition", [T.PARTITION_LEX, T.PARTITION_SFC, T.PARTITION_YSLAB])
 @pytest.mark.parametrize("bands,ranks", [([(8, 1.0, 0.0)], 2), ([(6, 1.0, 0.0), (6, 1.0, 0.3), (6, 1.0, 0.0)], 3),
                                          ([(6, 1.0, 0.0), (6, 1.0, 0.3), (6, 1.0, 0.0)], 6),
                                          ([(5, 1.0, 0.0), (7, 1.0, 0.3)], 4)])
 def test_interior_run_has_only_local_conforming_neighbours(bands, ranks, partition):
     """SURVEY §8(e) overlap: the element run whose kernels are launched while the halo
-    exchange is in flight must not touch remote or sliding faces, and must be maximal
-    among the runs of local-only elements."""
+    exchange is in flight must not touch a remote conforming face (mortar data are
+    complete before the element kernels); the local order puts every such element
+    first, so the run is [0, number of local-only elements)."""
+    if partition == T.PARTITION_YSLAB and ranks > 4:
+        pytest.skip("y slabs need n_ranks <= ny")
     mesh = T.mesh_spec(bands, ny=4, nz=2, partition=partition)
     plans = [capi.plan(mesh, ranks, r) for r in range(ranks)]
     owner = {g: r for r, p in enumerate(plans) for g in p["elements"]}
+    vg = [mesh.bands[b].vg_y for b in range(mesh.n_bands)]
     for r, p in enumerate(plans):
         els = p["elements"]
         local_only = []
         for g in els:
             b, nbs = _neighbours(mesh, g)
-            local_only.append(all(jb == b and owner[jg] == r for jb, jg in nbs))
+            # sliding neighbours (another band moving at another speed) come through mortars
+            local_only.append(all(owner[jg] == r for jb, jg in nbs if jb == b or vg[jb] == vg[b]))
         lo, hi = p["interior_run"]
-        assert all(local_only[lo:hi])
-        best, run = 0, 0
-        for f in local_only:
-            run = run + 1 if f else 0
-            best = max(best, run)
-        assert hi - lo == best
-    if bands == [(8, 1.0, 0.0)] and partition == T.PARTITION_LEX:
-        assert [p["interior_run"] for p in plans] == [[8, 24], [8, 24]]
+        assert lo == 0 and hi == sum(local_only)
+        assert all(local_only[lo:hi]) and not any(local_only[hi:])
 
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])

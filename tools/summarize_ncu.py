@@ -10,6 +10,7 @@
 usage: tools/summarize_ncu.py <tag> [dof]
 """
 import csv
+import re
 import io
 import json
 import os
@@ -53,8 +54,10 @@ def raw(rep):
 
 def summarize(tag, dof):
     lines, kernels, bytes_k = [], [], []
-    for rep in sorted(f for f in os.listdir(OUT)
-                      if f.startswith(tag + "_") and (f.endswith(".ncu-rep") or f.endswith("_raw.csv"))):
+    # Exactly this pass's element-kernel captures (measure.sh names them <tag>_<kernel>_raw.csv);
+    # a bare prefix match would also take another pass's files whose tag extends this one.
+    pat = re.compile(re.escape(tag) + r"_k_[a-z0-9_]+?(_raw\.csv|\.ncu-rep)$")
+    for rep in sorted(f for f in os.listdir(OUT) if pat.fullmatch(f) and not f.startswith(tag + "_k_launch")):
         for rec in raw(os.path.join(OUT, rep)):
             name = rec["Kernel Name"][1]
             lines.append(f"---- {name}")
@@ -81,8 +84,18 @@ def summarize(tag, dof):
         f.write(f"# {tag}: ncu --set full --clock-control none --import-source on, one launch per kernel\n")
         f.write("# command: tools/measure.sh (python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e)\n")
         f.write("\n".join(lines) + "\n")
+    # The workload the captures ran (bench.py keys its roofline.traffic lookup on it).
+    key, bj = None, os.path.join(OUT, f"{tag}_bench.json")
+    if os.path.exists(bj):
+        try:
+            c = json.loads(open(bj).read())["config"]
+            key = {"mesh": c.get("mesh"), "degree": c.get("degree"), "elements_per_gpu": c.get("elements_per_gpu")}
+            dof = c.get("elements_per_gpu", 0) * (c.get("degree", 0) + 1) ** 3 or dof
+        except Exception:
+            key = None
     if kernels:
         tr = {
+            "workload": key,
             "kernels": kernels,
             "bytes_per_kernel": bytes_k,
             "dram_bytes_per_stage": sum(bytes_k),
