@@ -120,8 +120,9 @@ enum { SDG_MAP_BOX = 0, SDG_MAP_WARP = 1, SDG_MAP_ANNULUS = 2 };
  * so y is the angle (radians) and z the radius (z0 > 0).  A moving band
  * ROTATES rigidly at angular velocity vg_y about the x axis (the sliding
  * interfaces are x-normal annuli, the pairing runs along theta as before).  A
- * periodic y direction must span the full circle (height = 2 pi): sector
- * periodicity would need a rotation of the momentum across the seam.
+ * periodic y direction spans the full circle (height = 2 pi) or a rotationally
+ * periodic sector 2 pi / m: vectors crossing the sector seam (momentum, Fv.n,
+ * gradients, the moving side's mortar data) rotate by the sector angle.
  * Metric terms rotate with the band, Ja(t) = R(vg t) Ja(0); the contravariant
  * grid velocity Ja^d . vg is the discrete curl of I^N(omega r^2/2 grad_xi X),
  * so the discrete geometric conservation law holds exactly (free stream). */

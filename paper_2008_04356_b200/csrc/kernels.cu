@@ -341,14 +341,6 @@ __device__ __forceinline__ void load_tables(const ElemConsts& C, double* tab) {
   }
 }
 
-// Band table in shared memory: a dynamically indexed kernel-parameter load
-// (C.bands[band]) goes through the constant cache with long-scoreboard latency.
-__device__ __forceinline__ void load_bands(const ElemConsts& C, BandD* sb) {
-  constexpr int W = sizeof(BandD) / sizeof(double);
-  const double* src = reinterpret_cast<const double*>(C.bands);
-  double* dst = reinterpret_cast<double*>(sb);
-  for (int q = threadIdx.x; q < SDG_MAX_BANDS * W; q += blockDim.x) dst[q] = src[q];
-}
 
 // Flat, coalesced load of EPB consecutive elements into SoA shared memory su[v][node].
 template <int N1>
@@ -1371,30 +1363,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 constexpr int kCodeShift = 29;
 
+// Element tiles of the persistent TMA gradient kernel (k_gradient_ws): one element
+// per tile, eight at N = 1.
 template <int N1>
 struct Tma {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int EPB = N1 == 2 ? 8 : 1;
-  static constexpr int THREADS = EPB * N3;
-  static constexpr int MINB_U = N1 == 2 ? 3 : (N1 == 8 ? 1 : (N1 == 4 ? 4 : 2));  // resident CTAs per SM (smem bound)
-  static constexpr int MINB_G = N1 == 8 ? 1 : (N1 == 4 ? 4 : 2);
-  static constexpr int TAB = Dim<N1>::TAB;
-  static constexpr int EL = 5 * N3;  // state doubles per element
-  static constexpr int TS = 5 * N2;  // trace slot
-  static constexpr int FS = 4 * N2;  // Fv.n slot
-  static constexpr int NB = TS + FS;
-  // update: double-buffered stage {U, own Fv.n, neighbour (trace|flux, Fv.n|lift)} + single RK register
-  static constexpr int U_STAGE = EPB * (EL + 6 * FS + 6 * NB);
-  static constexpr int U_REG = EPB * EL;
-  static constexpr int U_WF = EPB * 16 * N3;  // q (4 N3) + gradient (12 N3), then F (15 N3), then traces
-  static constexpr int U_WORK = U_WF + EPB * 24 * N2;
-  static constexpr int U_SMEM = (TAB + 2 * U_STAGE + U_REG + U_WORK) * 8 + 64;
-  // gradient: double-buffered {U, neighbour trace|lift}; own traces; q (then Fv.n out); gradient
-  static constexpr int G_STAGE = EPB * (EL + 6 * TS);
-  static constexpr int G_WQ = EPB * 4 * N3;
-  static constexpr int G_WORK = EPB * 6 * TS + G_WQ + EPB * 12 * N3 + EPB * 6 * FS;
-  static constexpr int G_SMEM = (TAB + 2 * G_STAGE + G_WORK) * 8 + 64;
-  static_assert(EL % 2 == 0 && TS % 2 == 0, "TMA path needs 16-byte blocks");
 };
 
 // Side codes of one tile (8 ints per element) into shared memory, asynchronously.
