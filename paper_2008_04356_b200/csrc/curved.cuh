@@ -663,48 +663,72 @@ template <int N1, bool ROT, bool GRAD, bool VISC, bool AFF = false>
 __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, int n, double* base, int per,
                                                    uint64_t* bar, bool load_reg = false) {
   using D = CB<N1, ROT, AFF>;
-  uint32_t bytes = n * (D::EL + D::ML + D::FM + 6 * D::TS) * 8u;
+  constexpr int N2 = D::N2, N3 = D::N3;
+  // The gradient needs Ja and 1/J of the node metrics and the normal and sJ of the face
+  // metrics: the annulus's grid-velocity rows (V^d, (vg / omega) . n and the pad) stay in HBM.
+  constexpr int ML_USED = (GRAD && !AFF) ? 10 * N3 : D::ML;
+  constexpr int FW_USED = (GRAD && !AFF) ? 4 : D::FW;
+  constexpr int FM_USED = AFF ? 0 : 6 * FW_USED * N2;
+  // The element's own blocks go first -- they need no table lookup -- so most of the
+  // tile is in flight while the side codes (one 32-byte read per element) arrive; the
+  // transaction count is announced with the single arrival at the end (it may run
+  // ahead of the completions: the phase cannot complete before the arrival).
+  uint32_t bytes = n * (D::EL + ML_USED + FM_USED + 6 * D::TS) * 8u;
   if (load_reg) bytes += n * D::EL * 8u;
   if (!GRAD && VISC) bytes += n * 6u * D::FS * 8u;
-  for (int le = 0; le < n; ++le)
-    for (int s = 0; s < 6; ++s) {
-      const int typ = P.side_type[(e0 + le) * 6 + s];
-      if (typ == kDirichlet) continue;
-      if (GRAD) bytes += (typ == kConforming ? D::TS : D::FS) * 8u;
-      else bytes += (D::TS + (VISC ? D::FS : 0)) * 8u;
-    }
-  mbar_arrive_expect_tx(bar, bytes);
   for (int le = 0; le < n; ++le) {
     const int e = e0 + le;
     double* b = base + le * per;
     bulk_g2s(b, P.U + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
     if (!AFF) {
-      bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
-      bulk_g2s(b + D::EL + D::ML, P.fmet + static_cast<size_t>(e) * D::FM, D::FM * 8u, bar);
+      bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, ML_USED * 8u, bar);
+      if (FW_USED == D::FW) {
+        bulk_g2s(b + D::EL + D::ML, P.fmet + static_cast<size_t>(e) * D::FM, D::FM * 8u, bar);
+      } else {  // [side][c][f]: the first FW_USED rows of every side
+        for (int sd = 0; sd < 6; ++sd)
+          bulk_g2s(b + D::EL + D::ML + sd * D::FW * N2, P.fmet + static_cast<size_t>(e) * D::FM + sd * D::FW * N2,
+                   FW_USED * N2 * 8u, bar);
+      }
     }
     double* tr = b + D::EL + D::ML + D::FM;
     bulk_g2s(tr, P.trace + static_cast<size_t>(e) * 6 * D::TS, 6 * D::TS * 8u, bar);
     if (load_reg) bulk_g2s(b + D::RG, P.reg + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
-    double* fv = tr + 6 * D::TS;
-    double* nb = GRAD ? fv : fv + 6 * D::FS;
-    if (!GRAD && VISC) bulk_g2s(fv, P.fvn + static_cast<size_t>(e) * 6 * D::FS, 6 * D::FS * 8u, bar);
+    if (!GRAD && VISC) bulk_g2s(tr + 6 * D::TS, P.fvn + static_cast<size_t>(e) * 6 * D::FS, 6 * D::FS * 8u, bar);
+  }
+  constexpr int MASK = (1 << kCodeShift) - 1;
+  for (int le = 0; le < n; ++le) {
+    const int e = e0 + le;
+    const int4 c0 = *reinterpret_cast<const int4*>(P.side_code + 8 * e);
+    const int2 c1 = *reinterpret_cast<const int2*>(P.side_code + 8 * e + 4);
+    const int code[6] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y};
+    double* nb = base + le * per + D::EL + D::ML + D::FM + 6 * D::TS + (GRAD ? 0 : 6 * D::FS);
+#pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const int slot = e * 6 + s;
-      const int typ = P.side_type[slot], idx = P.side_idx[slot];
+      const int typ = code[s] >> kCodeShift, idx = code[s] & MASK;
       double* d = nb + s * (GRAD ? D::TS : D::NB);
       if (typ == kConforming) {
         bulk_g2s(d, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-        if (!GRAD && VISC) bulk_g2s(d + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+        bytes += D::TS * 8u;
+        if (!GRAD && VISC) {
+          bulk_g2s(d + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+          bytes += D::FS * 8u;
+        }
       } else if (typ == kSliding) {
         if (GRAD) {
           bulk_g2s(d, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+          bytes += D::FS * 8u;
         } else {
           bulk_g2s(d, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-          if (VISC) bulk_g2s(d + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+          bytes += D::TS * 8u;
+          if (VISC) {
+            bulk_g2s(d + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+            bytes += D::FS * 8u;
+          }
         }
       }
     }
   }
+  mbar_arrive_expect_tx(bar, bytes);
 }
 
 template <int N1, bool ROT, bool AFF = false>
