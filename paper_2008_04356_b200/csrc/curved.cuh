@@ -48,10 +48,8 @@ struct CDim {
 struct Rot {
   double c, s;
 };
-__device__ __forceinline__ Rot band_rotation(bool rot, const BandD& B, double t) {
-  Rot r{1.0, 0.0};
-  if (rot) sincos(B.vg * t, &r.s, &r.c);
-  return r;
+__device__ __forceinline__ Rot band_rotation(bool rot, const StageArgs& A, int band) {
+  return rot ? Rot{A.rot_c[band], A.rot_s[band]} : Rot{1.0, 0.0};  // (cos, sin)(vg t_stage), solver.cu stage_args
 }
 __device__ __forceinline__ void rotate_yz(const Rot& r, double& y, double& z) {
   const double a = r.c * y + r.s * z, b = -r.s * y + r.c * z;
@@ -175,6 +173,23 @@ __device__ __forceinline__ void fv_n(const double* u, const double* gr, const do
   o[3] = r0 * v0 + r1 * v1 + r2 * v2 + g.kcond * dT;
 }
 
+// Viscous stress tensor (tau_00, tau_01, tau_02, tau_11, tau_12, tau_22) and heat flux
+// k dT/dx_d of a node from its BR1 gradient g[3 q + d] = d q / d x_d, q = (v1, v2, v3, T)
+// (viscous_flux, flux.cpp:23-42).
+__device__ __forceinline__ void visc_terms(const double* g, const GasD& gas, double* o) {
+  const double div = g[0] + g[4] + g[8];
+  const double mu = gas.mu, lam = gas.lam;
+  o[0] = 2.0 * mu * g[0] + lam * div;
+  o[1] = mu * (g[1] + g[3]);
+  o[2] = mu * (g[2] + g[6]);
+  o[3] = 2.0 * mu * g[4] + lam * div;
+  o[4] = mu * (g[5] + g[7]);
+  o[5] = 2.0 * mu * g[8] + lam * div;
+  o[6] = gas.kcond * g[9];
+  o[7] = gas.kcond * g[10];
+  o[8] = gas.kcond * g[11];
+}
+
 // Curved BR1 gradient at one node, conservative weak form:
 //   g_c = (1/J) sum_d [ lw1 q*+ (n sJ)+_c - lw0 q*- (n sJ)-_c - sum_m Dhat(ia, m) Ja^d_c(m) q(m) ].
 // sq [4][N3], sJa [10][N3] (Ja^d_c at 3d + c), sLift [6][4][N2], sfm [6][N2][4].
@@ -208,10 +223,7 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
       }
     }
   }
-  const double ij = sJa[9 * N3 + (i * N1 + j) * N1 + k];
-  double surf[12];
-#pragma unroll
-  for (int q = 0; q < 12; ++q) surf[q] = 0.0;
+  // The surface terms go into the same accumulators (volume minus surface): 12 live values, not 24.
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int ia = d == 0 ? i : (d == 1 ? j : k);
@@ -224,11 +236,12 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
       const double lp = sLift[((2 * d + 1) * 4 + q) * N2 + f] * sp;
       const double lm = sLift[((2 * d) * 4 + q) * N2 + f] * sm;
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk) surf[3 * q + kk] += lp * np[kk * N2] - lm * nm[kk * N2];
+      for (int kk = 0; kk < 3; ++kk) acc[3 * q + kk] += lm * nm[kk * N2] - lp * np[kk * N2];
     }
   }
+  const double nij = -sJa[9 * N3 + (i * N1 + j) * N1 + k];
 #pragma unroll
-  for (int q = 0; q < 12; ++q) g[q] = ij * (surf[q] - acc[q]);
+  for (int q = 0; q < 12; ++q) g[q] = nij * acc[q];
   if (ROT) {  // computed with the t = 0 metrics: g(t) = R g
 #pragma unroll
     for (int q = 0; q < 4; ++q) rotate_yz(rot, g[3 * q + 1], g[3 * q + 2]);
@@ -241,7 +254,7 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
 // ----------------------------------------------------------------------------
 template <int N1, bool ROT>
 __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(const __grid_constant__ ElemConsts C,
-                                                                            FieldPtrs P, StageArgs A) {
+                                                                            FieldPtrs P, const __grid_constant__ StageArgs A) {
   using D = CDim<N1, ROT>;
   constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = D::EPB, TAB = Dim<N1>::TAB, PER = D::PER_GRAD;
   constexpr int MW = D::MW, FW = D::FW;
@@ -262,8 +275,9 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(cons
   double* sTr = sG + 12 * N3;
   double* sLift = sTr + 30 * N2;
   double* sfm = sLift + 24 * N2;
-  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
-  const Rot rot = band_rotation(ROT, B, A.t_stage);
+  const int band = active ? P.coords[4 * e] : 0;
+  const BandD& B = C.bands[band];
+  const Rot rot = band_rotation(ROT, A, band);
   __syncthreads();
   if (active) {
     double u[5], q[4];
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(cons
 // ----------------------------------------------------------------------------
 template <int N1, bool VISC, bool ROT>
 __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const __grid_constant__ ElemConsts C,
-                                                                          FieldPtrs P, StageArgs A) {
+                                                                          FieldPtrs P, const __grid_constant__ StageArgs A) {
   using D = CDim<N1, ROT>;
   constexpr int N2 = N1 * N1, N3 = N2 * N1, EPB = D::EPB, TAB = Dim<N1>::TAB, PER = D::PER_UPD;
   constexpr int MW = D::MW, FW = D::FW;
@@ -340,8 +354,9 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
   double* sFlux = sLift + 24 * N2;
   double* sfm = sFlux + 30 * N2;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
-  const Rot rot = band_rotation(ROT, B, A.t_stage);
+  const int band = active ? P.coords[4 * e] : 0;
+  const BandD& B = C.bands[band];
+  const Rot rot = band_rotation(ROT, A, band);
   __syncthreads();
 
   // Phase 1: numerical flux along each face node's normal -> sFlux[s][v][f]; lift* -> sLift.
@@ -649,7 +664,16 @@ struct CB {
 #endif
   // Resident CTAs per SM at N = 5: shared memory fits 3 (the annulus update kernel's 13 + 6-wide metrics: 2).
   static constexpr int MINB_G = N1 == 6 ? SDG_CURVED_MINB : 1;
-  static constexpr int MINB_U = N1 == 6 ? (AFF ? SDG_AFFINE_MINB_U : SDG_CURVED_MINB_U) : 1;
+#ifndef SDG_AFF_MINB8
+#define SDG_AFF_MINB8 2  // affine update, N = 7: 110 registers x 512 threads left one CTA (16 warps) per SM
+#endif
+#ifndef SDG_AFF_MINB4
+#define SDG_AFF_MINB4 3  // affine update, N = 3: 4 elements per CTA, 136 registers x 256 threads left one CTA (8 warps) per SM
+#endif
+  static constexpr int MINB_U = N1 == 6   ? (AFF ? SDG_AFFINE_MINB_U : SDG_CURVED_MINB_U)
+                                : N1 == 8 ? (AFF ? SDG_AFF_MINB8 : 1)
+                                : N1 == 4 ? (AFF ? SDG_AFF_MINB4 : 1)
+                                          : 1;
   static_assert(AFF || 12 * N3 <= EL + ML, "gradient aliases state + metrics");
   static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
   static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
@@ -733,7 +757,7 @@ __device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, i
 
 template <int N1, bool ROT, bool AFF = false>
 __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_G) k_gradient_bulk(
-    const __grid_constant__ ElemConsts C, FieldPtrs P, StageArgs A) {
+    const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
   using D = CB<N1, ROT, AFF>;
   constexpr int FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::G_PER;
@@ -759,8 +783,16 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
   double* sq = sNb + 6 * D::TS;
   double* sLift = sq + 4 * N3;
   double* sG = AFF ? sLift + 24 * N2 : sU;  // curved: over the dead state + metrics after the gradient phase
-  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
-  const Rot rot = band_rotation(ROT, B, A.t_stage);
+  const int band = active ? P.coords[4 * e] : 0;
+  const BandD& B = C.bands[band];
+  const Rot rot = band_rotation(ROT, A, band);
+  // Side types of this thread's face nodes, fetched while the tile's bulk loads are in flight.
+  int typs[D::KF];
+#pragma unroll
+  for (int kf = 0; kf < D::KF; ++kf) {
+    const int it = t + kf * N3;
+    typs[kf] = (active && it < 6 * N2) ? P.side_type[e * 6 + it / N2] : 0;
+  }
   __syncthreads();  // barrier init visible, tables loaded
   mbar_wait(bar, 0);
   if (active) {
@@ -769,9 +801,12 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
 #pragma unroll
     for (int c = 0; c < 4; ++c) sq[c * N3 + t] = q[c];
     // BR1 surface values lift* (run_lifting, solver.cpp:606-723).
-    for (int it = t; it < 6 * N2; it += N3) {
+#pragma unroll
+    for (int kf = 0; kf < D::KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
       const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-      const int typ = P.side_type[e * 6 + s];
+      const int typ = typs[kf];
       const double* own = sTr + s * D::TS + f * 5;
       double lift[4];
       if (typ == kConforming) {
@@ -808,6 +843,16 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
 #pragma unroll
       for (int c = 0; c < 12; ++c) go[c] = g[c];
     }
+    if constexpr (!AFF) {
+      // Viscous stress and heat flux of the node for k_update_cv (coalesced rows [c][node]).
+      if (P.visc != nullptr) {
+        double vs[9];
+        visc_terms(g, C.gas, vs);
+        double* vo = P.visc + static_cast<size_t>(e) * 9 * N3 + t;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) vo[c * N3] = vs[c];
+      }
+    }
   }
   __syncthreads();  // every node's gradient is computed: state and metrics are dead
   if (active) {
@@ -819,14 +864,16 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
   // (zero on sliding / Dirichlet sides) and bulk-stored as one contiguous block.
   double* sOut = sNb;
   if (active) {
-    for (int it = t; it < 6 * N2; it += N3) {
+#pragma unroll
+    for (int kf = 0; kf < D::KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
       const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
       const double* ell = tab + N1 * N1 + (s & 1) * N1;
       double gt[12];
 #pragma unroll
       for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
-      const int slot = e * 6 + s;
-      const int typ = P.side_type[slot], idx = P.side_idx[slot];
+      const int typ = typs[kf];
       double fv[4] = {0.0, 0.0, 0.0, 0.0};
       if (typ == kConforming) {
         if constexpr (AFF) {
@@ -837,6 +884,7 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
           fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
         }
       } else {
+        const int idx = P.side_idx[e * 6 + s];
         double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
 #pragma unroll
         for (int c = 0; c < 12; ++c) dst[c] = gt[c];
@@ -856,7 +904,7 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
 
 template <int N1, bool VISC, bool ROT, bool AFF = false>
 __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_U) k_update_bulk(
-    const __grid_constant__ ElemConsts C, FieldPtrs P, StageArgs A) {
+    const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
   using D = CB<N1, ROT, AFF>;
   constexpr int FW = D::FW;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::U_PER;
@@ -886,8 +934,9 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
   double* sFlux = sTr;  // written after phase 1 has read the own traces / Fv.n
   double* sLift = sFv;
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  const BandD& B = C.bands[active ? P.coords[4 * e] : 0];
-  const Rot rot = band_rotation(ROT, B, A.t_stage);
+  const int band = active ? P.coords[4 * e] : 0;
+  const BandD& B = C.bands[band];
+  const Rot rot = band_rotation(ROT, A, band);
   __syncthreads();
   mbar_wait(bar, 0);
 
@@ -1171,6 +1220,596 @@ __global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::M
   }
 }
 
+
+// ============================================================================
+// k_gradient_cv: k_gradient_bulk for curved elements at a smaller footprint
+// (N = 5: 55 KB of shared memory and <= 72 registers, 4 CTAs per SM instead of 3).
+//   * the node's state is read by its own thread (it is only needed for the
+//     primitive variables), not staged;
+//   * only the metric rows the gradient uses are staged: Ja and 1/J of the node
+//     metrics, unit normal and sJ of the face metrics (compact [side][4][f]);
+//   * the gradient is accumulated in one set of 12 registers (volume minus surface).
+// Shared memory per element: met (Ja, 1/J) | q  (later the gradient [12][node]) |
+// face metrics | own traces | neighbour trace / lift* (later Fv.n) | lift*.
+// ============================================================================
+template <int N1, bool ROT>
+struct CG {
+  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  static constexpr int MWG = MWidth<ROT>::MW, FWG = MWidth<ROT>::FW;  // row counts in global memory
+  static constexpr int EPB = CB<N1, ROT>::EPB;
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int TAB = Dim<N1>::TAB;
+  static constexpr int EL = 5 * N3, ML = 10 * N3, SQ = 4 * N3, FMC = 6 * 4 * N2, TS = 5 * N2, FS = 4 * N2;
+  static constexpr int PER = ML + SQ + FMC + 6 * TS + 6 * TS + 6 * FS;
+  static constexpr int KF = (6 * N2 + N3 - 1) / N3;
+#ifndef SDG_CG_MINB
+#define SDG_CG_MINB 4
+#endif
+  static constexpr int MINB = N1 == 6 ? SDG_CG_MINB : 1;
+  static constexpr int SMEM = (TAB + EPB * PER) * 8 + 16;
+  static_assert(12 * N3 <= ML + SQ, "gradient aliases metrics + q");
+  static_assert(N1 % 2 == 0, "bulk path needs even N+1");
+  static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
+};
+
+template <int N1, bool ROT>
+__device__ __forceinline__ void cg_issue_loads(const FieldPtrs& P, int e0, int n, double* base, uint64_t* bar) {
+  using D = CG<N1, ROT>;
+  constexpr int N2 = D::N2;
+  uint32_t bytes = n * (D::ML + D::FMC + 6 * D::TS) * 8u;
+  for (int le = 0; le < n; ++le) {
+    const int e = e0 + le;
+    double* b = base + le * D::PER;
+    bulk_g2s(b, P.met + static_cast<size_t>(e) * D::MWG * D::N3, D::ML * 8u, bar);
+    for (int sd = 0; sd < 6; ++sd)  // [side][c][f]: normal and sJ rows of every side
+      bulk_g2s(b + D::ML + D::SQ + sd * 4 * N2, P.fmet + (static_cast<size_t>(e) * 6 + sd) * D::FWG * N2, 4 * N2 * 8u,
+               bar);
+    bulk_g2s(b + D::ML + D::SQ + D::FMC, P.trace + static_cast<size_t>(e) * 6 * D::TS, 6 * D::TS * 8u, bar);
+  }
+  constexpr int MASK = (1 << kCodeShift) - 1;
+  for (int le = 0; le < n; ++le) {
+    const int e = e0 + le;
+    const int4 c0 = *reinterpret_cast<const int4*>(P.side_code + 8 * e);
+    const int2 c1 = *reinterpret_cast<const int2*>(P.side_code + 8 * e + 4);
+    const int code[6] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y};
+    double* nb = base + le * D::PER + D::ML + D::SQ + D::FMC + 6 * D::TS;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int typ = code[s] >> kCodeShift, idx = code[s] & MASK;
+      if (typ == kConforming) {
+        bulk_g2s(nb + s * D::TS, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        bytes += D::TS * 8u;
+      } else if (typ == kSliding) {
+        bulk_g2s(nb + s * D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+        bytes += D::FS * 8u;
+      }
+    }
+  }
+  mbar_arrive_expect_tx(bar, bytes);
+}
+
+template <int N1, bool ROT>
+__global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gradient_cv(
+    const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
+  using D = CG<N1, ROT>;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::PER, KF = D::KF;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* base = smem + D::TAB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + EPB * PER);
+  const int e0 = P.e_first + blockIdx.x * EPB;
+  const int n_el = min(EPB, P.E - e0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+    cg_issue_loads<N1, ROT>(P, e0, n_el, base, bar);
+  }
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = le < n_el;
+  double* sM = base + le * PER;   // [c][node], c < 10
+  double* sq = sM + D::ML;        // [c][node], c < 4
+  double* sfm = sq + D::SQ;       // [side][c][f], c < 4
+  double* sTr = sfm + D::FMC;     // [side][f][5]
+  double* sNb = sTr + 6 * D::TS;  // [side]: trace [f][5] or lift* [f][4]
+  double* sLift = sNb + 6 * D::TS;
+  double* sG = sM;                // [c][node], c < 12, once every node's gradient is computed
+  const int band = active ? P.coords[4 * e] : 0;
+  const Rot rot = band_rotation(ROT, A, band);
+  // While the bulk copies are in flight: this node's state and this thread's side types.
+  double u[5];
+  int typs[KF], rots[KF];
+  if (active) {
+    const double* up = P.U + (static_cast<size_t>(e) * N3 + t) * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = __ldg(up + v);
+  }
+#pragma unroll
+  for (int kf = 0; kf < KF; ++kf) {
+    const int it = t + kf * N3;
+    const bool on = active && it < 6 * N2;
+    typs[kf] = on ? P.side_type[e * 6 + it / N2] : 0;
+    rots[kf] = (ROT && on) ? P.side_rot[e * 6 + it / N2] : 0;
+  }
+  load_tables<N1>(C, tab);
+  __syncthreads();  // barrier init visible, tables loaded
+  mbar_wait(bar, 0);
+  if (active) {
+    double q[4];
+    prim4(u, C.gas, q);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sq[c * N3 + t] = q[c];
+    // BR1 surface values lift* (run_lifting, solver.cpp:606-723).
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
+      const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
+      const int typ = typs[kf];
+      double lift[4];
+      if (typ == kConforming) {
+        double other[5], qa[4], qb[4];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) other[v] = sNb[it * 5 + v];
+        if constexpr (ROT) {  // periodic annulus sector seam
+          if (rots[kf] != 0) rot_yz(C.sec_c, rots[kf] * C.sec_s, other[2], other[3]);
+        }
+        prim4(sTr + it * 5, C.gas, qa);
+        prim4(other, C.gas, qb);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
+      } else if (typ == kSliding) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lift[c] = sNb[s * D::TS + f * 4 + c];
+      } else {
+        double x[3], ext[5];
+        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        prim4(ext, C.gas, lift);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
+    }
+  }
+  __syncthreads();
+  double g[12];
+  if (active) {
+    const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+    node_gradient_curved<N1, 4, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
+    if (P.grad_out != nullptr) {
+      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) go[c] = g[c];
+    }
+    if (P.visc != nullptr) {  // stress and heat flux of the node for k_update_cv (coalesced rows [c][node])
+      double vs[9];
+      visc_terms(g, C.gas, vs);
+      double* vo = P.visc + static_cast<size_t>(e) * 9 * N3 + t;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) vo[c * N3] = vs[c];
+    }
+  }
+  __syncthreads();  // every node's gradient is computed: metrics and q are dead
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
+  }
+  __syncthreads();
+  // Fv.n of the 6 sides staged in the dead neighbour-trace region [side][f][4]
+  // (zero on sliding / Dirichlet sides) and bulk-stored as one contiguous block.
+  double* sOut = sNb;
+  if (active) {
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
+      const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
+      const double* ell = tab + N1 * N1 + (s & 1) * N1;
+      double gt[12];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+      const int typ = typs[kf];
+      double fv[4] = {0.0, 0.0, 0.0, 0.0};
+      if (typ == kConforming) {
+        const double* fm = sfm + s * 4 * N2 + f;
+        double nrm[3] = {fm[0], fm[N2], fm[2 * N2]};
+        if (ROT) rotate_yz(rot, nrm[1], nrm[2]);
+        fv_n(sTr + it * 5, gt, nrm, C.gas, fv);
+      } else {
+        const int idx = P.side_idx[e * 6 + s];
+        double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) dst[c] = gt[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sOut[it * 4 + c] = fv[c];
+    }
+    fence_proxy_async();
+  }
+  __syncthreads();
+  if (active && t == 0) {
+    bulk_s2g(P.fvn + static_cast<size_t>(e) * 6 * D::FS, sOut, 6 * D::FS * 8u);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+}
+
+// ============================================================================
+// k_update_cv: the update kernel of curved elements (even N+1).
+//   * The node's viscous stress and heat flux come from k_gradient_bulk (P.visc),
+//     so the BR1 gradient is evaluated once per stage, not again here.
+//   * What only one thread reads is loaded by that thread while the tile's bulk
+//     copies are in flight: a face node's own trace, Fv.n and face metrics.
+//     State, node metrics, stresses and the neighbour slots are bulk-copied onto
+//     one mbarrier.
+//   * The three contravariant flux directions are staged at once over the node's
+//     own metric / stress columns (thread-local aliasing: no barrier between the
+//     pointwise flux and the staging), so one CTA barrier separates the face and
+//     pointwise phases from the weak divergence.
+//   * The RK register is L2-prefetched with the tile and fetched into registers
+//     before that barrier.
+// Shared memory per element: U | met, visc (later 3 x 5 staged fluxes) | face flux
+// | face sJ | neighbour slots (later dudt, then the new traces).
+// ============================================================================
+template <int N1, bool ROT, bool VISC>
+struct CV {
+  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
+  static constexpr int MW = MWidth<ROT>::MW, FW = MWidth<ROT>::FW;
+  static constexpr int EPB = CB<N1, ROT>::EPB;
+  static constexpr int THREADS = EPB * N3;
+  static constexpr int TAB = Dim<N1>::TAB;
+  static constexpr int EL = 5 * N3, ML = MW * N3, VL = VISC ? 9 * N3 : 0;
+  static constexpr int MV = (ML + VL > 15 * N3 ? ML + VL : 15 * N3);
+  static constexpr int TS = 5 * N2, FS = 4 * N2, NB = TS + (VISC ? FS : 0);
+  static constexpr int FX = 6 * TS, SJ = 6 * N2;
+  static constexpr int NBR = 6 * NB > EL ? 6 * NB : EL;
+  static constexpr int PER = EL + MV + FX + SJ + NBR;
+  static constexpr int KF = (6 * N2 + N3 - 1) / N3;  // face nodes per thread
+  static constexpr int FM = 6 * FW * N2;
+#ifndef SDG_CV_MINB
+#define SDG_CV_MINB 3
+#endif
+  static constexpr int MINB = N1 == 6 ? SDG_CV_MINB : 1;
+  static constexpr int SMEM = (TAB + EPB * PER) * 8 + 16;
+  static_assert(N1 % 2 == 0, "bulk path needs even N+1");
+  static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
+  static_assert(6 * TS <= NBR, "new traces fit the neighbour region");
+};
+
+template <int N1, bool ROT, bool VISC>
+__device__ __forceinline__ void cv_issue_loads(const FieldPtrs& P, int e0, int n, double* base, uint64_t* bar) {
+  using D = CV<N1, ROT, VISC>;
+  uint32_t bytes = n * (D::EL + D::ML + D::VL) * 8u;
+  for (int le = 0; le < n; ++le) {
+    const int e = e0 + le;
+    double* b = base + le * D::PER;
+    bulk_g2s(b, P.U + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
+    bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
+    if (VISC) bulk_g2s(b + D::EL + D::ML, P.visc + static_cast<size_t>(e) * D::VL, D::VL * 8u, bar);
+  }
+  constexpr int MASK = (1 << kCodeShift) - 1;
+  for (int le = 0; le < n; ++le) {
+    const int e = e0 + le;
+    const int4 c0 = *reinterpret_cast<const int4*>(P.side_code + 8 * e);
+    const int2 c1 = *reinterpret_cast<const int2*>(P.side_code + 8 * e + 4);
+    const int code[6] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y};
+    double* nb = base + le * D::PER + D::EL + D::MV + D::FX + D::SJ;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int typ = code[s] >> kCodeShift, idx = code[s] & MASK;
+      double* d = nb + s * D::NB;
+      if (typ == kConforming) {
+        bulk_g2s(d, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        bytes += D::TS * 8u;
+        if (VISC) {
+          bulk_g2s(d + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
+          bytes += D::FS * 8u;
+        }
+      } else if (typ == kSliding) {
+        bulk_g2s(d, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
+        bytes += D::TS * 8u;
+      }
+    }
+  }
+  mbar_arrive_expect_tx(bar, bytes);
+}
+
+template <int N1, bool VISC, bool ROT>
+__global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>::MINB) k_update_cv(
+    const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
+  using D = CV<N1, ROT, VISC>;
+  constexpr int FW = D::FW, KF = D::KF;
+  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::PER, THREADS = D::THREADS;
+  extern __shared__ __align__(128) double smem[];
+  double* tab = smem;
+  double* base = smem + D::TAB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + EPB * PER);
+  const int e0 = P.e_first + blockIdx.x * EPB;
+  const int n_el = min(EPB, P.E - e0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+    cv_issue_loads<N1, ROT, VISC>(P, e0, n_el, base, bar);
+    if (A.mode == 0 && A.rk_a != 0.0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
+  }
+  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
+  const bool active = le < n_el;
+  double* sU = base + le * PER;
+  double* sM = sU + D::EL;           // [c][node], c < MW
+  double* sV = sM + D::ML;           // [c][node], c < 9
+  double* sF3 = sM;                  // [d][v][node] once the node's own columns are consumed
+  double* sFlux = sM + D::MV;        // [side][v][f]
+  double* sSJ = sFlux + D::FX;       // [side][f]
+  double* sNb = sSJ + D::SJ;         // [side]: trace [f][5] | Fv.n [f][4]  (sliding: flux [f][5])
+  double* sD = sNb;                  // dudt [node][5], after the face phase
+  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
+  const int band = active ? P.coords[4 * e] : 0;
+  const BandD& B = C.bands[band];
+  const Rot rot = band_rotation(ROT, A, band);
+
+  // This thread's face nodes: own trace, own Fv.n, unit normal, sJ and vg.n straight from
+  // global memory (nobody else reads them), in flight together with the bulk copies.
+  double own[KF][5], ofv[KF][4], nrm[KF][3], vgn[KF], sjf[KF];
+  int typs[KF], rots[KF];
+#pragma unroll
+  for (int kf = 0; kf < KF; ++kf) {
+    const int it = t + kf * N3;
+    typs[kf] = 0;
+    rots[kf] = 0;
+    if (active && it < 6 * N2) {
+      const int s = it / N2, f = it - s * N2;
+      typs[kf] = P.side_type[e * 6 + s];
+      if (ROT) rots[kf] = P.side_rot[e * 6 + s];
+      const double* tr = P.trace + (static_cast<size_t>(e) * 6 * N2 + it) * 5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) own[kf][v] = __ldg(tr + v);
+      if (VISC) {
+        const double2* fp = reinterpret_cast<const double2*>(P.fvn + (static_cast<size_t>(e) * 6 * N2 + it) * 4);
+        const double2 a0 = __ldg(fp), a1 = __ldg(fp + 1);
+        ofv[kf][0] = a0.x;
+        ofv[kf][1] = a0.y;
+        ofv[kf][2] = a1.x;
+        ofv[kf][3] = a1.y;
+      }
+      const double* fm = P.fmet + static_cast<size_t>(e) * D::FM + s * FW * N2 + f;  // [side][c][f]
+      nrm[kf][0] = __ldg(fm);
+      nrm[kf][1] = __ldg(fm + N2);
+      nrm[kf][2] = __ldg(fm + 2 * N2);
+      sjf[kf] = __ldg(fm + 3 * N2);
+      if (ROT) vgn[kf] = B.vg * __ldg(fm + 4 * N2);
+    }
+  }
+  load_tables<N1>(C, tab);
+  __syncthreads();  // barrier init visible, tables loaded
+  mbar_wait(bar, 0);
+
+  // Phase 1: numerical flux along each face node's normal -> sFlux, sJ -> sSJ.
+  if (active) {
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
+      const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
+      double* n = nrm[kf];
+      if (ROT) rotate_yz(rot, n[1], n[2]);
+      else vgn[kf] = B.vg * n[1];
+      const double* nb = sNb + s * D::NB;
+      const int typ = typs[kf];
+      double flux[5];
+      bool ok = true;
+      if (typ == kConforming) {
+        double other[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
+        double fvo[4];
+        if (VISC) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) fvo[c] = nb[D::TS + f * 4 + c];
+        }
+        if constexpr (ROT) {  // periodic annulus sector seam: the neighbour's vectors in this sector's frame
+          if (rots[kf] != 0) {
+            const double sn = rots[kf] * C.sec_s;
+            rot_yz(C.sec_c, sn, other[2], other[3]);
+            if (VISC) rot_yz(C.sec_c, sn, fvo[1], fvo[2]);
+          }
+        }
+        const double* um = (s & 1) ? own[kf] : other;
+        const double* up = (s & 1) ? other : own[kf];
+        ok = roe_flux_n(um, up, n, vgn[kf], C.gas, flux);
+        if (VISC) {
+          const double* fm = (s & 1) ? ofv[kf] : fvo;
+          const double* fp = (s & 1) ? fvo : ofv[kf];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
+        }
+      } else if (typ == kSliding) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) flux[v] = nb[f * 5 + v];
+      } else {
+        double x[3], ext[5];
+        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
+        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        const double* um = (s & 1) ? own[kf] : ext;
+        const double* up = (s & 1) ? ext : own[kf];
+        ok = roe_flux_n(um, up, n, vgn[kf], C.gas, flux);
+        if (VISC) {
+          const int idx = P.side_idx[e * 6 + s];
+          const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
+          double gg[12];
+#pragma unroll
+          for (int c = 0; c < 12; ++c) gg[c] = gd[c];
+          double fm[4], fp[4];
+          fv_n(um, gg, n, C.gas, fm);
+          fv_n(up, gg, n, C.gas, fp);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
+        }
+      }
+      if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own[kf]);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = flux[v];
+      sSJ[it] = sjf[kf];
+    }
+  }
+
+  // Phase 2: pointwise flux (ALE convective minus viscous) -> contravariant Ja^d . F, staged
+  // over this node's own metric / stress columns.
+  double ij = 0.0;
+  if (active) {
+    double u[5], F[3][5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
+    const double ir = rcp_nr(u[0]);
+    const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
+    const double p = pressure(u, ir, C.gas);
+    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, ROT ? 0.0 : B.vgz};  // annulus: grid velocity enters through V^d below
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      F[d][0] = u[0] * vv[d];
+      F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0);
+      F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0);
+      F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0);
+      F[d][4] = (u[4] + p) * vv[d];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) F[d][v] -= vgv[d] * u[v];
+    }
+    if (VISC) {
+      const double* vs = sV + t;
+      const double t00 = vs[0], t01 = vs[N3], t02 = vs[2 * N3], t11 = vs[3 * N3], t12 = vs[4 * N3], t22 = vs[5 * N3];
+      const double tau[3][3] = {{t00, t01, t02}, {t01, t11, t12}, {t02, t12, t22}};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        F[d][1] -= tau[d][0];
+        F[d][2] -= tau[d][1];
+        F[d][3] -= tau[d][2];
+        F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + vs[(6 + d) * N3];
+      }
+    }
+    if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
+    }
+    const double* ja = sM + t;  // [c][node]
+    ij = ja[9 * N3];
+    double Ft[3][5];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
+      const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
+    }
+    // Every read of this node's columns precedes these stores in program order.
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sF3[(d * 5 + v) * N3 + t] = Ft[d][v];
+    }
+  }
+  // RK register of this thread's flat positions (L2-prefetched), in flight across the barrier.
+  constexpr int KR = 5;
+  double rv[KR];
+  const size_t gbase = static_cast<size_t>(e0) * 5 * N3;
+  if (A.mode == 0) {
+#pragma unroll
+    for (int q = 0; q < KR; ++q) {
+      const int fI = threadIdx.x + q * THREADS;
+      rv[q] = (A.rk_a != 0.0 && fI < n_el * 5 * N3) ? P.reg[gbase + fI] : 0.0;
+    }
+  }
+  __syncthreads();
+
+  // Phase 3: weak divergence sum_m Dhat(i,m) Ft_d(m) over the three directions;
+  // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
+  if (active) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const double* dh = tab;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int ia = d == 0 ? i : (d == 1 ? j : k);
+      const int bse = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
+      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double c = dh[ia * N1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + bse + m * stride];
+      }
+    }
+    double du[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
+    const double* lw = tab + N1 * N1 + 2 * N1;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int dir = s >> 1;
+      const int ia = dir == 0 ? i : (dir == 1 ? j : k);
+      const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
+      const double l = lw[(s & 1) * N1 + ia];
+      if (l != 0.0) {
+        const double c = ((s & 1) ? -1.0 : 1.0) * l * sSJ[s * N2 + f] * ij;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) sD[t * 5 + v] = du[v];  // AoS, like the global state
+  }
+  __syncthreads();
+
+  // Phase 5: flat coalesced RK update (solver.cpp:912-917) or residual store.
+  if (A.mode == 1) {
+    for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += THREADS) {
+      const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+      P.out[gbase + fI] = base[l * PER + D::EL + D::MV + D::FX + D::SJ + r];
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < KR; ++q) {
+    const int fI = threadIdx.x + q * THREADS;
+    if (fI < n_el * 5 * N3) {
+      const int l = fI / (5 * N3), r = fI - l * 5 * N3;
+      double* us = base + l * PER + r;
+      const double dd = base[l * PER + D::EL + D::MV + D::FX + D::SJ + r];
+      const double rg = A.rk_a * rv[q] + A.dt * dd;
+      const double un = *us + A.rk_b * rg;
+      P.reg[gbase + fI] = rg;
+      P.U[gbase + fI] = un;
+      *us = un;
+    }
+  }
+  __syncthreads();
+  // Admissibility (check_admissible, solver.cpp:892-906), then the traces of the
+  // new state staged in the dead neighbour region [side][f][5] and bulk-stored.
+  double* sOut = sNb;
+  if (active) {
+    double w[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) w[v] = sU[t * 5 + v];
+    const double p = pressure(w, rcp_nr(w[0]), C.gas);
+    bool ok = w[0] > 0.0 && p > 0.0;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
+    if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf) {
+      const int it = t + kf * N3;
+      if (it >= 6 * N2) break;
+      const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
+      const double* ell = tab + N1 * N1 + (s & 1) * N1;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sOut[it * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+    }
+    fence_proxy_async();
+  }
+  __syncthreads();
+  if (active && t == 0) {
+    bulk_s2g(P.trace_out + static_cast<size_t>(e) * 6 * D::TS, sOut, 6 * D::TS * 8u);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+}
+
 template <int N1>
 bool update_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
   if constexpr (N1 % 2 != 0) {
@@ -1188,11 +1827,19 @@ bool update_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs&
 
 template <int N1, bool ROT>
 void gradient_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
+#ifdef SDG_GRAD_BULK  // the 3-CTA kernel that also stages the state and every metric row
   using D = CB<N1, ROT>;
   const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
   set_smem_checked(k_gradient_bulk<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
   k_gradient_bulk<N1, ROT><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
   check_launch("k_gradient_bulk");
+#else
+  using D = CG<N1, ROT>;
+  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+  set_smem_checked(k_gradient_cv<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
+  k_gradient_cv<N1, ROT><<<blocks, D::THREADS, D::SMEM, st>>>(c, p, a);
+  check_launch("k_gradient_cv");
+#endif
 }
 template <int N1>
 bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
@@ -1206,12 +1853,19 @@ bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArg
 }
 template <int N1, bool ROT>
 void update_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  using D = CB<N1, ROT>;
-  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-  auto kern = c.gas.viscous ? k_update_bulk<N1, true, ROT> : k_update_bulk<N1, false, ROT>;
-  set_smem_checked(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
-  kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
-  check_launch("k_update_bulk");
+  if (c.gas.viscous && p.visc == nullptr) throw ProtocolError("k_update_cv needs the stress buffer of k_gradient_bulk");
+  if (c.gas.viscous) {
+    using D = CV<N1, ROT, true>;
+    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    set_smem_checked(k_update_cv<N1, true, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
+    k_update_cv<N1, true, ROT><<<blocks, D::THREADS, D::SMEM, st>>>(c, p, a);
+  } else {
+    using D = CV<N1, ROT, false>;
+    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+    set_smem_checked(k_update_cv<N1, false, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
+    k_update_cv<N1, false, ROT><<<blocks, D::THREADS, D::SMEM, st>>>(c, p, a);
+  }
+  check_launch("k_update_cv");
 }
 template <int N1>
 bool update_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {

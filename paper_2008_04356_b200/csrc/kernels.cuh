@@ -69,6 +69,8 @@ struct FieldPtrs {
   const double* met;         // curved: E x N3 x 10 (Ja^d_c at 3d + c, 1/J)
   const double* fmet;        // curved: 6E x N2 x 4 (unit +xi normal, sJ) per local side
   const int8_t* side_rot;    // E x 6: neighbour vectors rotate by side_rot * sector angle (annulus sectors)
+  double* visc;              // curved, viscous, even N+1: E x 9 x N3 (tau_00 01 02 11 12 22, k dT/dx_d), written by
+                             // k_gradient_bulk and read by k_update_cv in place of a second gradient evaluation
   ErrRec* err;
   int E;        // element kernels process local elements [e_first, E)
   int e_first;  // (interior / boundary split for exchange overlap; 0 = all)
@@ -78,6 +80,9 @@ struct StageArgs {
   double t_stage, dt, rk_a, rk_b;
   int mode;  // 0: RK update (+ trace output), 1: residual into out
   int step, stage;
+  // Annulus: cos / sin of each band's rotation angle vg * t_stage, evaluated once on the host
+  // (every element of a band shares it; conforming faces never join two bands).
+  double rot_c[SDG_MAX_BANDS], rot_s[SDG_MAX_BANDS];
 };
 
 // ---- mortar side ----

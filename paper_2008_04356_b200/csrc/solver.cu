@@ -358,6 +358,7 @@ class GpuRankSolver {
                   const std::function<void()>& overlap_work = {});
   void join_comm();
   void element_kernel(bool update, const FieldPtrs& fp, const StageArgs& a, int e_first, int e_end, int n_sm);
+  StageArgs stage_args(double t_stage, double dt, double rk_a, double rk_b, int mode) const;
   void find_interior_run();
   FieldPtrs field_ptrs(double* U, double* out);
   MortarPtrs mortar_ptrs();
@@ -387,7 +388,7 @@ class GpuRankSolver {
   bool overlap_ = false;
   int sm_reserve_ = 0;  // SMs left free for the NCCL kernels while the interior run computes
 
-  DevBuf<double> U_, reg_, dudt_, trace_[2], fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_;
+  DevBuf<double> U_, reg_, dudt_, trace_[2], fvn_, slide_lift_, slide_flux_, slide_g_, dir_g_, grad_, visc_;
   // Curved elements (SDG_MAP_WARP): per-node metrics and per-side face metrics (host.cpp compute_metrics).
   bool curved_ = false;
   DevBuf<double> met_, fmet_;
@@ -623,6 +624,9 @@ void GpuRankSolver::upload_topology() {
     }
     met_.upload(cm.met, stream_);
     fmet_.upload(cm.fmet, stream_);
+    // Viscous stresses and heat flux per node, handed from the gradient kernel to the
+    // update kernel (bulk-loaded kernels, even N+1; curved.cuh k_update_cv).
+    if (cfg_.gas.mu > 0.0 && n_ % 2 == 0) visc_.alloc(static_cast<size_t>(E_) * n3_ * 9);
     cuda_check(cudaStreamSynchronize(stream_), "metric upload");
   }
   err_.alloc(1);
@@ -868,6 +872,7 @@ FieldPtrs GpuRankSolver::field_ptrs(double* U, double* out) {
   p.grad_out = nullptr;
   p.met = met_.p;
   p.fmet = fmet_.p;
+  p.visc = visc_.p;
   p.side_rot = side_rot_.p;
   p.err = err_.p;
   p.E = E_;
@@ -1330,6 +1335,26 @@ void GpuRankSolver::join_comm() {
   if (comm_stream_) cuda_check(cudaStreamWaitEvent(stream_, ev_comm_, 0), "wait event");
 }
 
+// Per-launch arguments of the element kernels; on an annulus, every band's rotation
+// (cos, sin)(vg * t_stage) is evaluated here once instead of by every thread.
+StageArgs GpuRankSolver::stage_args(double t_stage, double dt, double rk_a, double rk_b, int mode) const {
+  StageArgs a{};
+  a.t_stage = t_stage;
+  a.dt = dt;
+  a.rk_a = rk_a;
+  a.rk_b = rk_b;
+  a.mode = mode;
+  a.step = step_index_;
+  a.stage = stage_index_;
+  const bool rot = mesh_.spec.mapping == SDG_MAP_ANNULUS;
+  for (int b = 0; b < SDG_MAX_BANDS; ++b) {
+    const double phi = rot && b < static_cast<int>(mesh_.bands.size()) ? consts_.bands[b].vg * t_stage : 0.0;
+    a.rot_c[b] = std::cos(phi);
+    a.rot_s[b] = std::sin(phi);
+  }
+  return a;
+}
+
 // k_gradient / k_update over local elements [e_first, e_end).
 void GpuRankSolver::element_kernel(bool update, const FieldPtrs& fp0, const StageArgs& a, int e_first, int e_end,
                                    int n_sm) {
@@ -1413,7 +1438,7 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     nc_prepare(t_stage);
     nc_fill(false);
   }
-  StageArgs a{t_stage, dt, rk_a, rk_b, mode, step_index_, stage_index_};
+  const StageArgs a = stage_args(t_stage, dt, rk_a, rk_b, mode);
   // Element kernel over all local elements; with an exchange in flight, the interior run
   // first (on all but sm_reserve_ SMs), then the join, then the two boundary ranges.
   // Halo round of `arr` + element kernel: with overlap, the interior run is enqueued while the
@@ -1619,7 +1644,7 @@ void GpuRankSolver::compute_gradients(double t_stage, const double* d_u, double*
   fp.grad_out = d_grad;
   ElemConsts c = consts_;
   c.gas.viscous = 1;
-  StageArgs a{t_stage, 0.0, 0.0, 0.0, 1, step_index_, stage_index_};
+  const StageArgs a = stage_args(t_stage, 0.0, 0.0, 0.0, 1);
   if (curved_) launch_gradient_curved(n_, c, fp, a, stream_);
   else launch_gradient(n_, c, fp, a, stream_);
   launches_ += 6;
