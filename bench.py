@@ -341,15 +341,16 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     ach = value_per_gpu * bf / 1e9
     # ncu DRAM bytes of the stage's element kernels, from a capture of this exact
     # workload (tools/summarize_ncu.py writes the workload key into the file).
-    traffic, traffic_src = None, None
+    traffic, traffic_src, flops_per_dof = None, None, None
     key = {"mesh": conf.get("mesh"), "degree": args.degree, "elements_per_gpu": E}
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_stage_traffic.json")), key=os.path.getmtime):
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_stage_traffic.json"))):
         try:
             d = json.load(open(p))
         except Exception:
             continue
         if d.get("workload") == key:
             traffic, traffic_src = d.get("dram_bytes_per_stage"), os.path.relpath(p, ROOT)
+            flops_per_dof = d.get("fp64_flops_per_dof")
     rl = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
           "kernel": "RK stage = k_gradient + k_update + mortar/pairing kernels (one right-hand side + update)",
           "algorithmic_bytes_per_launch": bf * dof, "bytes_per_dof": bf,
@@ -357,14 +358,36 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
                               else "SURVEY.md §8(d) B_flow = 240 + 2712/(N+1) B per DOF-update (affine)"),
           "mean_launch_ms": stage_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
           "traffic_source": traffic_src}
+    # The FP64 side of the roofline (north star: "fraction of the HBM/FP64 roofline"): FP64 flops per
+    # DOF-update counted by ncu on this workload (same capture as `traffic`), against the DFMA peak
+    # measured by tools/fp64_peak.cu on this pool's B200 (profiles/*_fp64_peak.json).
+    fp64_peak, fp64_src = None, None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_fp64_peak.json"))):
+        try:
+            fp64_peak, fp64_src = json.load(open(p))["fp64_dfma_tflops"], os.path.relpath(p, ROOT)
+        except Exception:
+            pass
+    if flops_per_dof and fp64_peak:
+        tf = value_per_gpu * flops_per_dof / 1e12
+        rl["fp64"] = {"achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": tf / fp64_peak,
+                      "flops_per_dof": flops_per_dof, "flops_source": traffic_src, "peak_source": fp64_src,
+                      "intensity_flop_per_byte": (flops_per_dof * dof / traffic) if traffic else None}
     extra = {}
-    # This implementation's fused dataflow.
+    # This implementation's fused dataflow, doubles per element.
+    #   affine: k_gradient_ws reads U, own + neighbour traces, writes Fv.n; k_update_bulk reads U, the RK
+    #   register, own + neighbour traces and Fv.n, writes U, register, traces.
+    #   curved (even N+1): k_gradient_cv also reads Ja, 1/J (10 rows) and 4 face-metric rows and writes the
+    #   node's stress / heat flux (9); k_update_cv reads those 9, all node-metric rows and the face-metric rows
+    #   it uses instead of evaluating the gradient again.
     per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 18), "gradient": 8 * E * (5 * n3 + 6 * n2 * 9)}
-    if curved:  # + per-node metrics (10 doubles, 13 on the annulus) and per-side face metrics (4 / 6 doubles per
-        # face node), read by both kernels
-        mw, fw = (13, 6) if args.mesh == "rotor" else (10, 4)
-        for k in per_kernel:
-            per_kernel[k] += 8 * E * (mw * n3 + 6 * n2 * fw)
+    if curved:
+        mw, fw_u = (13, 5) if args.mesh == "rotor" else (10, 4)
+        if n1 % 2 == 0:
+            per_kernel["gradient"] += 8 * E * (10 * n3 + 6 * n2 * 4 + 9 * n3)
+            per_kernel["update"] += 8 * E * (mw * n3 + 6 * n2 * fw_u + 9 * n3)
+        else:  # plain-load kernels: every metric row in both, gradient evaluated twice
+            for k in per_kernel:
+                per_kernel[k] += 8 * E * (mw * n3 + 6 * n2 * (6 if args.mesh == "rotor" else 4))
     for name, byts in per_kernel.items():
         ms, cnt = kt.get(name, (0.0, 0))
         if cnt:

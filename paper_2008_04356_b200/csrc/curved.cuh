@@ -173,23 +173,6 @@ __device__ __forceinline__ void fv_n(const double* u, const double* gr, const do
   o[3] = r0 * v0 + r1 * v1 + r2 * v2 + g.kcond * dT;
 }
 
-// Viscous stress tensor (tau_00, tau_01, tau_02, tau_11, tau_12, tau_22) and heat flux
-// k dT/dx_d of a node from its BR1 gradient g[3 q + d] = d q / d x_d, q = (v1, v2, v3, T)
-// (viscous_flux, flux.cpp:23-42).
-__device__ __forceinline__ void visc_terms(const double* g, const GasD& gas, double* o) {
-  const double div = g[0] + g[4] + g[8];
-  const double mu = gas.mu, lam = gas.lam;
-  o[0] = 2.0 * mu * g[0] + lam * div;
-  o[1] = mu * (g[1] + g[3]);
-  o[2] = mu * (g[2] + g[6]);
-  o[3] = 2.0 * mu * g[4] + lam * div;
-  o[4] = mu * (g[5] + g[7]);
-  o[5] = 2.0 * mu * g[8] + lam * div;
-  o[6] = gas.kcond * g[9];
-  o[7] = gas.kcond * g[10];
-  o[8] = gas.kcond * g[11];
-}
-
 // Curved BR1 gradient at one node, conservative weak form:
 //   g_c = (1/J) sum_d [ lw1 q*+ (n sJ)+_c - lw0 q*- (n sJ)-_c - sum_m Dhat(ia, m) Ja^d_c(m) q(m) ].
 // sq [4][N3], sJa [10][N3] (Ja^d_c at 3d + c), sLift [6][4][N2], sfm [6][N2][4].
@@ -619,611 +602,24 @@ void update_curved_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a
 }
 
 // ============================================================================
-// Bulk-loaded curved kernels (even N+1: every per-element and per-slot block is
-// a multiple of 16 bytes).  One thread issues cp.async.bulk copies of
-// everything the element tile reads — state, metrics, face metrics, its own
-// face traces (and Fv.n), and per side the neighbour's trace + Fv.n slot (or
-// the sliding face's back-projected flux + lift*) — completing on one
-// mbarrier, so the tile's global reads are in flight together instead of as
-// dependent load chains (ncu: 50% long-scoreboard stalls in the kernels above).
-// Own traces are staged from the trace buffer, so both elements of a face use
-// the same stored bits.  The RK register is prefetched into L2.
+// Bulk-loaded element kernels (even N+1: every per-element and per-slot block is
+// a multiple of 16 bytes).  One thread issues cp.async.bulk copies of what the
+// element tile stages in shared memory, completing on one mbarrier, so the
+// tile's global reads are in flight together instead of as dependent load chains
+// (ncu: 50% long-scoreboard stalls in the plain-load kernels above); what only
+// one thread reads is loaded by that thread meanwhile.  Own traces come from
+// the trace buffer, so both elements of a face use the same stored bits.
 // ============================================================================
-// AFF: the same structure for affine elements (no metric arrays; the
-// reference's constant sJ / J per band) — an alternative to the persistent
-// TMA kernels of kernels.cu (SDG_AFFINE_B=1).
-template <int N1, bool ROT, bool AFF = false>
-struct CB {
-  static constexpr int N2 = N1 * N1, N3 = N2 * N1;
-  static constexpr int MW = MWidth<ROT>::MW, FW = MWidth<ROT>::FW;
-  static constexpr int EPB = N1 == 2 ? 16 : CDim<N1, ROT>::EPB;  // shared memory: <= 227 KB per CTA
-  static constexpr int THREADS = EPB * N3;
-  static constexpr int TAB = Dim<N1>::TAB;
-  static constexpr int EL = 5 * N3, ML = AFF ? 0 : MW * N3, FM = AFF ? 0 : 6 * FW * N2, TS = 5 * N2, FS = 4 * N2,
-                       NB = TS + FS;
-  static constexpr int GX = AFF ? 12 * N3 : 0;  // affine: separate gradient buffer (no metrics to alias)
-  // update, per element: U | met | fmet | own traces | own Fv.n | neighbour slots | sF | lift* | flux
-  // (face flux and lift* are written over the element's own traces and Fv.n once phase 1 has read them)
-  // (the staging buffer sF lives in the neighbour region, dead after phase 1)
-  // affine: + the RK register, bulk-loaded with the tile (its L2-prefetched global read stalled 7 %)
-  static constexpr int RG = EL + ML + FM + 6 * TS + 6 * FS + 6 * NB;
-  static constexpr int U_PER = RG + (AFF ? EL : 0);
-  static_assert(5 * N3 <= 6 * NB, "staging buffer fits the neighbour region");
-  // gradient, per element: U | met | fmet | own traces | neighbour trace / lift* | q | gradient | lift*
-  // (the gradient is written over the state and metrics once every node's gradient is computed)
-  static constexpr int G_PER = EL + ML + FM + 6 * TS + 6 * TS + 4 * N3 + 24 * N2 + GX;
-  static constexpr int KF = (6 * N2 + N3 - 1) / N3;  // face nodes per thread
-#ifndef SDG_CURVED_MINB
-#define SDG_CURVED_MINB 3
-#endif
-#ifndef SDG_CURVED_MINB_U
-#define SDG_CURVED_MINB_U 3
-#endif
-#ifndef SDG_AFFINE_MINB_U
-#define SDG_AFFINE_MINB_U 4  // affine update: 40 KB per CTA; 4 CTAs at <= 72 registers (128 B spills) beat 3 and 5
-#endif
-  // Resident CTAs per SM at N = 5: shared memory fits 3 (the annulus update kernel's 13 + 6-wide metrics: 2).
-  static constexpr int MINB_G = N1 == 6 ? SDG_CURVED_MINB : 1;
-#ifndef SDG_AFF_MINB8
-#define SDG_AFF_MINB8 2  // affine update, N = 7: 110 registers x 512 threads left one CTA (16 warps) per SM
-#endif
-#ifndef SDG_AFF_MINB4
-#define SDG_AFF_MINB4 3  // affine update, N = 3: 4 elements per CTA, 136 registers x 256 threads left one CTA (8 warps) per SM
-#endif
-  static constexpr int MINB_U = N1 == 6   ? (AFF ? SDG_AFFINE_MINB_U : SDG_CURVED_MINB_U)
-                                : N1 == 8 ? (AFF ? SDG_AFF_MINB8 : 1)
-                                : N1 == 4 ? (AFF ? SDG_AFF_MINB4 : 1)
-                                          : 1;
-  static_assert(AFF || 12 * N3 <= EL + ML, "gradient aliases state + metrics");
-  static constexpr int U_SMEM = (TAB + EPB * U_PER) * 8 + 16;
-  static constexpr int G_SMEM = (TAB + EPB * G_PER) * 8 + 16;
-  static_assert(N1 % 2 == 0, "bulk path needs even N+1");
-  static_assert(U_SMEM <= 227 * 1024 && G_SMEM <= 227 * 1024, "shared memory per CTA");
+// Elements per CTA (shared memory: <= 227 KB per CTA).
+template <int N1>
+struct BulkEpb {
+  static constexpr int EPB = N1 == 2 ? 16 : (N1 <= 4 ? Dim<N1>::EPB : 1);
 };
 
-// Issue the bulk copies of one element tile (thread 0).  GRAD: neighbour
-// trace (conforming) or lift* (sliding) only; else trace + Fv.n or flux + lift*.
-template <int N1, bool ROT, bool GRAD, bool VISC, bool AFF = false>
-__device__ __forceinline__ void curved_issue_loads(const FieldPtrs& P, int e0, int n, double* base, int per,
-                                                   uint64_t* bar, bool load_reg = false) {
-  using D = CB<N1, ROT, AFF>;
-  constexpr int N2 = D::N2, N3 = D::N3;
-  // The gradient needs Ja and 1/J of the node metrics and the normal and sJ of the face
-  // metrics: the annulus's grid-velocity rows (V^d, (vg / omega) . n and the pad) stay in HBM.
-  constexpr int ML_USED = (GRAD && !AFF) ? 10 * N3 : D::ML;
-  constexpr int FW_USED = (GRAD && !AFF) ? 4 : D::FW;
-  constexpr int FM_USED = AFF ? 0 : 6 * FW_USED * N2;
-  // The element's own blocks go first -- they need no table lookup -- so most of the
-  // tile is in flight while the side codes (one 32-byte read per element) arrive; the
-  // transaction count is announced with the single arrival at the end (it may run
-  // ahead of the completions: the phase cannot complete before the arrival).
-  uint32_t bytes = n * (D::EL + ML_USED + FM_USED + 6 * D::TS) * 8u;
-  if (load_reg) bytes += n * D::EL * 8u;
-  if (!GRAD && VISC) bytes += n * 6u * D::FS * 8u;
-  for (int le = 0; le < n; ++le) {
-    const int e = e0 + le;
-    double* b = base + le * per;
-    bulk_g2s(b, P.U + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
-    if (!AFF) {
-      bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, ML_USED * 8u, bar);
-      if (FW_USED == D::FW) {
-        bulk_g2s(b + D::EL + D::ML, P.fmet + static_cast<size_t>(e) * D::FM, D::FM * 8u, bar);
-      } else {  // [side][c][f]: the first FW_USED rows of every side
-        for (int sd = 0; sd < 6; ++sd)
-          bulk_g2s(b + D::EL + D::ML + sd * D::FW * N2, P.fmet + static_cast<size_t>(e) * D::FM + sd * D::FW * N2,
-                   FW_USED * N2 * 8u, bar);
-      }
-    }
-    double* tr = b + D::EL + D::ML + D::FM;
-    bulk_g2s(tr, P.trace + static_cast<size_t>(e) * 6 * D::TS, 6 * D::TS * 8u, bar);
-    if (load_reg) bulk_g2s(b + D::RG, P.reg + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
-    if (!GRAD && VISC) bulk_g2s(tr + 6 * D::TS, P.fvn + static_cast<size_t>(e) * 6 * D::FS, 6 * D::FS * 8u, bar);
-  }
-  constexpr int MASK = (1 << kCodeShift) - 1;
-  for (int le = 0; le < n; ++le) {
-    const int e = e0 + le;
-    const int4 c0 = *reinterpret_cast<const int4*>(P.side_code + 8 * e);
-    const int2 c1 = *reinterpret_cast<const int2*>(P.side_code + 8 * e + 4);
-    const int code[6] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y};
-    double* nb = base + le * per + D::EL + D::ML + D::FM + 6 * D::TS + (GRAD ? 0 : 6 * D::FS);
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const int typ = code[s] >> kCodeShift, idx = code[s] & MASK;
-      double* d = nb + s * (GRAD ? D::TS : D::NB);
-      if (typ == kConforming) {
-        bulk_g2s(d, P.trace + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-        bytes += D::TS * 8u;
-        if (!GRAD && VISC) {
-          bulk_g2s(d + D::TS, P.fvn + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-          bytes += D::FS * 8u;
-        }
-      } else if (typ == kSliding) {
-        if (GRAD) {
-          bulk_g2s(d, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-          bytes += D::FS * 8u;
-        } else {
-          bulk_g2s(d, P.slide_flux + static_cast<size_t>(idx) * D::TS, D::TS * 8u, bar);
-          bytes += D::TS * 8u;
-          if (VISC) {
-            bulk_g2s(d + D::TS, P.slide_lift + static_cast<size_t>(idx) * D::FS, D::FS * 8u, bar);
-            bytes += D::FS * 8u;
-          }
-        }
-      }
-    }
-  }
-  mbar_arrive_expect_tx(bar, bytes);
-}
-
-template <int N1, bool ROT, bool AFF = false>
-__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_G) k_gradient_bulk(
-    const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
-  using D = CB<N1, ROT, AFF>;
-  constexpr int FW = D::FW;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::G_PER;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* base = smem + D::TAB;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + EPB * PER);
-  const int e0 = P.e_first + blockIdx.x * EPB;
-  const int n_el = min(EPB, P.E - e0);
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-    curved_issue_loads<N1, ROT, true, true, AFF>(P, e0, n_el, base, PER, bar);
-  }
-  load_tables<N1>(C, tab);
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
-  const bool active = le < n_el;
-  double* sU = base + le * PER;
-  double* sM = sU + D::EL;
-  double* sfm = sM + D::ML;
-  double* sTr = sfm + D::FM;
-  double* sNb = sTr + 6 * D::TS;
-  double* sq = sNb + 6 * D::TS;
-  double* sLift = sq + 4 * N3;
-  double* sG = AFF ? sLift + 24 * N2 : sU;  // curved: over the dead state + metrics after the gradient phase
-  const int band = active ? P.coords[4 * e] : 0;
-  const BandD& B = C.bands[band];
-  const Rot rot = band_rotation(ROT, A, band);
-  // Side types of this thread's face nodes, fetched while the tile's bulk loads are in flight.
-  int typs[D::KF];
-#pragma unroll
-  for (int kf = 0; kf < D::KF; ++kf) {
-    const int it = t + kf * N3;
-    typs[kf] = (active && it < 6 * N2) ? P.side_type[e * 6 + it / N2] : 0;
-  }
-  __syncthreads();  // barrier init visible, tables loaded
-  mbar_wait(bar, 0);
-  if (active) {
-    double q[4];
-    prim4(sU + t * 5, C.gas, q);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) sq[c * N3 + t] = q[c];
-    // BR1 surface values lift* (run_lifting, solver.cpp:606-723).
-#pragma unroll
-    for (int kf = 0; kf < D::KF; ++kf) {
-      const int it = t + kf * N3;
-      if (it >= 6 * N2) break;
-      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-      const int typ = typs[kf];
-      const double* own = sTr + s * D::TS + f * 5;
-      double lift[4];
-      if (typ == kConforming) {
-        double qa[4], qb[4];
-        prim4(own, C.gas, qa);
-        if constexpr (ROT) {  // periodic annulus sector seam: rotate the neighbour trace in place
-          if (C.sec_s != 0.0 && P.side_rot[e * 6 + s] != 0)
-            rot_yz(C.sec_c, P.side_rot[e * 6 + s] * C.sec_s, sNb[s * D::TS + f * 5 + 2], sNb[s * D::TS + f * 5 + 3]);
-        }
-        prim4(sNb + s * D::TS + f * 5, C.gas, qb);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-      } else if (typ == kSliding) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) lift[c] = sNb[s * D::TS + f * 4 + c];
-      } else {
-        double x[3], ext[5];
-        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-        prim4(ext, C.gas, lift);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = lift[c];
-    }
-  }
-  __syncthreads();
-  double g[12];
-  if (active) {
-    const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-    if constexpr (AFF) node_gradient<N1>(tab, sq, sLift, B, i, j, k, g);
-    else node_gradient_curved<N1, FW, ROT>(tab, sq, sM, sLift, sfm, i, j, k, rot, g);
-    if (P.grad_out != nullptr) {
-      double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
-#pragma unroll
-      for (int c = 0; c < 12; ++c) go[c] = g[c];
-    }
-    if constexpr (!AFF) {
-      // Viscous stress and heat flux of the node for k_update_cv (coalesced rows [c][node]).
-      if (P.visc != nullptr) {
-        double vs[9];
-        visc_terms(g, C.gas, vs);
-        double* vo = P.visc + static_cast<size_t>(e) * 9 * N3 + t;
-#pragma unroll
-        for (int c = 0; c < 9; ++c) vo[c * N3] = vs[c];
-      }
-    }
-  }
-  __syncthreads();  // every node's gradient is computed: state and metrics are dead
-  if (active) {
-#pragma unroll
-    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
-  }
-  __syncthreads();
-  // Fv.n of the 6 sides staged in the dead neighbour-trace region [side][f][4]
-  // (zero on sliding / Dirichlet sides) and bulk-stored as one contiguous block.
-  double* sOut = sNb;
-  if (active) {
-#pragma unroll
-    for (int kf = 0; kf < D::KF; ++kf) {
-      const int it = t + kf * N3;
-      if (it >= 6 * N2) break;
-      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-      const double* ell = tab + N1 * N1 + (s & 1) * N1;
-      double gt[12];
-#pragma unroll
-      for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
-      const int typ = typs[kf];
-      double fv[4] = {0.0, 0.0, 0.0, 0.0};
-      if (typ == kConforming) {
-        if constexpr (AFF) {
-          fv_dir(sTr + s * D::TS + f * 5, gt, s >> 1, C.gas, fv);
-        } else {
-          double nrm[3], vgn;
-          face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
-          fv_n(sTr + s * D::TS + f * 5, gt, nrm, C.gas, fv);
-        }
-      } else {
-        const int idx = P.side_idx[e * 6 + s];
-        double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
-#pragma unroll
-        for (int c = 0; c < 12; ++c) dst[c] = gt[c];
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sOut[s * D::FS + f * 4 + c] = fv[c];
-    }
-    fence_proxy_async();
-  }
-  __syncthreads();
-  if (active && t == 0) {
-    bulk_s2g(P.fvn + static_cast<size_t>(e) * 6 * D::FS, sOut, 6 * D::FS * 8u);
-    bulk_commit();
-    bulk_wait_read0();
-  }
-}
-
-template <int N1, bool VISC, bool ROT, bool AFF = false>
-__global__ void __launch_bounds__(CB<N1, ROT, AFF>::THREADS, CB<N1, ROT, AFF>::MINB_U) k_update_bulk(
-    const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
-  using D = CB<N1, ROT, AFF>;
-  constexpr int FW = D::FW;
-  constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::U_PER;
-  extern __shared__ __align__(128) double smem[];
-  double* tab = smem;
-  double* base = smem + D::TAB;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + EPB * PER);
-  const int e0 = P.e_first + blockIdx.x * EPB;
-  const int n_el = min(EPB, P.E - e0);
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-    const bool load_reg = AFF && A.mode == 0 && A.rk_a != 0.0;
-    curved_issue_loads<N1, ROT, false, VISC, AFF>(P, e0, n_el, base, PER, bar, load_reg);
-    if (!AFF && A.mode == 0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
-  }
-  load_tables<N1>(C, tab);
-  const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
-  const bool active = le < n_el;
-  double* sU = base + le * PER;
-  double* sM = sU + D::EL;
-  double* sfm = sM + D::ML;
-  double* sTr = sfm + D::FM;
-  double* sFv = sTr + 6 * D::TS;
-  double* sNb = sFv + 6 * D::FS;
-  double* sF = sNb;  // q, flux staging and dudt: written only after phase 1 has read the neighbour slots
-  double* sFlux = sTr;  // written after phase 1 has read the own traces / Fv.n
-  double* sLift = sFv;
-  const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  const int band = active ? P.coords[4 * e] : 0;
-  const BandD& B = C.bands[band];
-  const Rot rot = band_rotation(ROT, A, band);
-  __syncthreads();
-  mbar_wait(bar, 0);
-
-  // Phase 1: numerical flux along each face node's normal and lift*, kept in
-  // registers until every thread has read its own traces / Fv.n, then stored
-  // over them (sFlux, sLift).
-  double rflux[D::KF][5], rlift[D::KF][4];
-  if (active) {
-#pragma unroll
-    for (int kf = 0; kf < D::KF; ++kf) {
-      const int it = t + kf * N3;
-      if (it >= 6 * N2) break;
-      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-      const double* own = sTr + s * D::TS + f * 5;
-      double nrm[3], vgn;
-      const int dir = s >> 1;
-      if constexpr (AFF) {
-        vgn = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
-      } else {
-        face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
-      }
-      const double* nb = sNb + s * D::NB;
-      const int typ = P.side_type[e * 6 + s];
-      double flux[5], lift[4];
-      bool ok = true;
-      if (typ == kConforming) {
-        if constexpr (ROT) {  // periodic annulus sector seam: rotate the neighbour slot in place
-          if (C.sec_s != 0.0 && P.side_rot[e * 6 + s] != 0) {  // (only this thread reads it)
-            const double sn = P.side_rot[e * 6 + s] * C.sec_s;
-            double* o = sNb + s * D::NB + f * 5;
-            rot_yz(C.sec_c, sn, o[2], o[3]);
-            if (VISC) {
-              double* fv = sNb + s * D::NB + D::TS + f * 4;
-              rot_yz(C.sec_c, sn, fv[1], fv[2]);
-            }
-          }
-        }
-        const double* other = nb + f * 5;
-        const double* um = (s & 1) ? own : other;
-        const double* up = (s & 1) ? other : own;
-        if constexpr (AFF) ok = roe_flux(um, up, dir, vgn, C.gas, flux);
-        else ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
-        if (VISC) {
-          double qa[4], qb[4];
-          prim4(own, C.gas, qa);
-          prim4(other, C.gas, qb);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lift[c] = __dmul_rn(0.5, __dadd_rn(qa[c], qb[c]));
-          const double* pa = sFv + s * D::FS + f * 4;
-          const double* pb = nb + D::TS + f * 4;
-          const double* fm = (s & 1) ? pa : pb;
-          const double* fp = (s & 1) ? pb : pa;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
-        }
-      } else if (typ == kSliding) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) flux[v] = nb[f * 5 + v];
-        if (VISC) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) lift[c] = nb[D::TS + f * 4 + c];
-        }
-      } else {
-        double x[3], ext[5];
-        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
-        const double* um = (s & 1) ? own : ext;
-        const double* up = (s & 1) ? ext : own;
-        if constexpr (AFF) ok = roe_flux(um, up, dir, vgn, C.gas, flux);
-        else ok = roe_flux_n(um, up, nrm, vgn, C.gas, flux);
-        if (VISC) {
-          prim4(ext, C.gas, lift);
-          const int idx = P.side_idx[e * 6 + s];
-          const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
-          double gg[12];
-#pragma unroll
-          for (int c = 0; c < 12; ++c) gg[c] = gd[c];
-          double fm[4], fp[4];
-          if constexpr (AFF) {
-            fv_dir(um, gg, dir, C.gas, fm);
-            fv_dir(up, gg, dir, C.gas, fp);
-          } else {
-            fv_n(um, gg, nrm, C.gas, fm);
-            fv_n(up, gg, nrm, C.gas, fp);
-          }
-#pragma unroll
-          for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
-        }
-      }
-      if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) rflux[kf][v] = flux[v];
-      if (VISC) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) rlift[kf][c] = lift[c];
-      }
-    }
-  }
-  __syncthreads();
-  if (active) {
-    if (VISC) {
-      double q[4];
-      prim4(sU + t * 5, C.gas, q);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sF[c * N3 + t] = q[c];
-    }
-#pragma unroll
-    for (int kf = 0; kf < D::KF; ++kf) {
-      const int it = t + kf * N3;
-      if (it >= 6 * N2) break;
-      const int s = it / N2, f = it % N2;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = rflux[kf][v];
-      if (VISC) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sLift[(s * 4 + c) * N2 + f] = rlift[kf][c];
-      }
-    }
-  }
-  __syncthreads();
-
-  // Phase 2: pointwise flux -> contravariant Ja^d . F.
-  double Ft[3][5];
-  if (active) {
-    double u[5], F[3][5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
-    const double ir = rcp_nr(u[0]);
-    const double vv[3] = {u[1] * ir, u[2] * ir, u[3] * ir};
-    const double p = pressure(u, ir, C.gas);
-    const double vgv[3] = {0.0, ROT ? 0.0 : B.vg, ROT ? 0.0 : B.vgz};  // annulus: grid velocity enters through V^d below
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      F[d][0] = u[0] * vv[d];
-      F[d][1] = u[1] * vv[d] + (d == 0 ? p : 0.0);
-      F[d][2] = u[2] * vv[d] + (d == 1 ? p : 0.0);
-      F[d][3] = u[3] * vv[d] + (d == 2 ? p : 0.0);
-      F[d][4] = (u[4] + p) * vv[d];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) F[d][v] -= vgv[d] * u[v];
-    }
-    if (VISC) {
-      double g[12];
-      if constexpr (AFF) node_gradient<N1>(tab, sF, sLift, B, i, j, k, g);
-      else node_gradient_curved<N1, FW, ROT>(tab, sF, sM, sLift, sfm, i, j, k, rot, g);
-      const double div = g[0] + g[4] + g[8];
-      const double mu = C.gas.mu, lam = C.gas.lam;
-      const double tau[3][3] = {{2.0 * mu * g[0] + lam * div, mu * (g[1] + g[3]), mu * (g[2] + g[6])},
-                                {mu * (g[1] + g[3]), 2.0 * mu * g[4] + lam * div, mu * (g[5] + g[7])},
-                                {mu * (g[2] + g[6]), mu * (g[5] + g[7]), 2.0 * mu * g[8] + lam * div}};
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        F[d][1] -= tau[d][0];
-        F[d][2] -= tau[d][1];
-        F[d][3] -= tau[d][2];
-        F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + C.gas.kcond * g[9 + d];
-      }
-    }
-    if constexpr (AFF) {  // contravariant flux sJ_d F_d (volume_kernel, solver.cpp:357-370)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) Ft[d][v] = F[d][v] * B.sj[d];
-      }
-    } else {
-      const double* ja = sM + t;  // [c][node]
-      if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
-      }
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
-        const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
-      }
-    }
-  }
-
-  // Phase 3: weak divergence per direction through the SoA staging buffer.
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  const double* dh = tab;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) sF[v * N3 + t] = Ft[d][v];
-    }
-    __syncthreads();
-    if (active) {
-      const int ia = d == 0 ? i : (d == 1 ? j : k);
-      const int bse = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
-      const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
-#pragma unroll
-      for (int m = 0; m < N1; ++m) {
-        const double c = dh[ia * N1 + m];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[v] += c * sF[v * N3 + bse + m * stride];
-      }
-    }
-  }
-
-  // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
-  double du[5];
-  if (active) {
-    const double ij = AFF ? B.inv_jac : sM[9 * N3 + t];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;
-    const double* lw = tab + N1 * N1 + 2 * N1;
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const int dir = s >> 1;
-      const int ia = dir == 0 ? i : (dir == 1 ? j : k);
-      const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
-      const double l = lw[(s & 1) * N1 + ia];
-      if (l != 0.0) {
-        const double c = AFF ? ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * l
-                             : ((s & 1) ? -1.0 : 1.0) * l * face_sj(sfm, s, f, N2, FW) * ij;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
-      }
-    }
-  }
-  __syncthreads();
-  if (active) {
-#pragma unroll
-    for (int v = 0; v < 5; ++v) sF[t * 5 + v] = du[v];  // AoS, like the global state
-  }
-  __syncthreads();
-
-  // Phase 5: flat coalesced RK update (solver.cpp:912-917) or residual store.
-  if (A.mode == 1) {
-    for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
-      const int l = fI / (5 * N3), r = fI - l * 5 * N3;
-      P.out[static_cast<size_t>(e0) * 5 * N3 + fI] = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + r];
-    }
-    return;
-  }
-  for (int fI = threadIdx.x; fI < n_el * 5 * N3; fI += blockDim.x) {
-    const int l = fI / (5 * N3), r = fI - l * 5 * N3;
-    double* us = base + l * PER + r;
-    const double dd = base[l * PER + D::EL + D::ML + D::FM + 6 * D::TS + 6 * D::FS + r];
-    const size_t g = static_cast<size_t>(e0) * 5 * N3 + fI;
-    double rv;
-    if constexpr (AFF) rv = A.rk_a != 0.0 ? base[l * PER + D::RG + r] : 0.0;
-    else rv = P.reg[g];
-    const double rg = A.rk_a * rv + A.dt * dd;
-    const double un = *us + A.rk_b * rg;
-    P.reg[g] = rg;
-    P.U[g] = un;
-    *us = un;
-  }
-  __syncthreads();
-  // Admissibility (check_admissible, solver.cpp:892-906), then the traces of the
-  // new state staged in the dead neighbour region [side][f][5] and bulk-stored.
-  double* sOut = sNb;
-  if (active) {
-    double w[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) w[v] = sU[t * 5 + v];
-    const double p = pressure(w, rcp_nr(w[0]), C.gas);
-    bool ok = w[0] > 0.0 && p > 0.0;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) ok = ok && isfinite(w[v]);
-    if (!ok) record_error(P.err, 2, A.step, A.stage, e, t, w);
-    for (int it = t; it < 6 * N2; it += N3) {
-      const int s = it / N2, f = it % N2, a = f / N1, b = f % N1;
-      const double* ell = tab + N1 * N1 + (s & 1) * N1;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) sOut[s * D::TS + f * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
-    }
-    fence_proxy_async();
-  }
-  __syncthreads();
-  if (active && t == 0) {
-    bulk_s2g(P.trace_out + static_cast<size_t>(e) * 6 * D::TS, sOut, 6 * D::TS * 8u);
-    bulk_commit();
-    bulk_wait_read0();
-  }
-}
-
-
 // ============================================================================
-// k_gradient_cv: k_gradient_bulk for curved elements at a smaller footprint
-// (N = 5: 55 KB of shared memory and <= 72 registers, 4 CTAs per SM instead of 3).
+// k_gradient_cv: lift* -> curved gradient -> Fv.n (conforming sides) / gradient
+// traces (sliding and Dirichlet sides), the node's viscous stress for k_update_cv
+// (N = 5: 55 KB of shared memory and <= 72 registers, 4 CTAs per SM).
 //   * the node's state is read by its own thread (it is only needed for the
 //     primitive variables), not staged;
 //   * only the metric rows the gradient uses are staged: Ja and 1/J of the node
@@ -1236,7 +632,7 @@ template <int N1, bool ROT>
 struct CG {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int MWG = MWidth<ROT>::MW, FWG = MWidth<ROT>::FW;  // row counts in global memory
-  static constexpr int EPB = CB<N1, ROT>::EPB;
+  static constexpr int EPB = BulkEpb<N1>::EPB;
   static constexpr int THREADS = EPB * N3;
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3, ML = 10 * N3, SQ = 4 * N3, FMC = 6 * 4 * N2, TS = 5 * N2, FS = 4 * N2;
@@ -1330,6 +726,18 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
     typs[kf] = on ? P.side_type[e * 6 + it / N2] : 0;
     rots[kf] = (ROT && on) ? P.side_rot[e * 6 + it / N2] : 0;
   }
+  // Elements whose six sides are all conforming need only Fv.n on their faces: the stress and
+  // heat flux are linear in the gradient, so their 9 components are prolonged instead of
+  // the gradient's 12.  Sliding / Dirichlet sides need the gradient trace itself.
+  bool allconf = false;
+  if (active) {
+    constexpr int MASK = (1 << kCodeShift) - 1;
+    const int4 c0 = __ldg(reinterpret_cast<const int4*>(P.side_code + 8 * e));
+    const int2 c1 = __ldg(reinterpret_cast<const int2*>(P.side_code + 8 * e + 4));
+    const int any = (c0.x | c0.y | c0.z | c0.w | c1.x | c1.y) & ~MASK;
+    const int all = (c0.x & c0.y & c0.z & c0.w & c1.x & c1.y) & ~MASK;
+    allconf = any == (kConforming << kCodeShift) && all == (kConforming << kCodeShift);
+  }
   load_tables<N1>(C, tab);
   __syncthreads();  // barrier init visible, tables loaded
   mbar_wait(bar, 0);
@@ -1380,18 +788,27 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
 #pragma unroll
       for (int c = 0; c < 12; ++c) go[c] = g[c];
     }
+    double vs[9];
+    visc_terms(g, C.gas, vs);
     if (P.visc != nullptr) {  // stress and heat flux of the node for k_update_cv (coalesced rows [c][node])
-      double vs[9];
-      visc_terms(g, C.gas, vs);
       double* vo = P.visc + static_cast<size_t>(e) * 9 * N3 + t;
 #pragma unroll
       for (int c = 0; c < 9; ++c) vo[c * N3] = vs[c];
     }
+    if (allconf) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) g[c] = vs[c];
+    }
   }
   __syncthreads();  // every node's gradient is computed: metrics and q are dead
   if (active) {
+    if (allconf) {
 #pragma unroll
-    for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
+      for (int c = 0; c < 9; ++c) sG[c * N3 + t] = g[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 12; ++c) sG[c * N3 + t] = g[c];
+    }
   }
   __syncthreads();
   // Fv.n of the 6 sides staged in the dead neighbour-trace region [side][f][4]
@@ -1404,15 +821,29 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
       if (it >= 6 * N2) break;
       const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
       const double* ell = tab + N1 * N1 + (s & 1) * N1;
+      const double* fm = sfm + s * 4 * N2 + f;
+      double nrm[3] = {fm[0], fm[N2], fm[2 * N2]};
+      if (ROT) rotate_yz(rot, nrm[1], nrm[2]);
+      double fv[4] = {0.0, 0.0, 0.0, 0.0};
+      if (allconf) {  // Fv.n from the prolonged stress and heat flux (flux.cpp:23-42 contracted with n)
+        double vt[9];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) vt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+        const double* uo = sTr + it * 5;
+        const double ir = rcp_nr(uo[0]);
+        fv[0] = vt[0] * nrm[0] + vt[1] * nrm[1] + vt[2] * nrm[2];
+        fv[1] = vt[1] * nrm[0] + vt[3] * nrm[1] + vt[4] * nrm[2];
+        fv[2] = vt[2] * nrm[0] + vt[4] * nrm[1] + vt[5] * nrm[2];
+        fv[3] = (fv[0] * uo[1] + fv[1] * uo[2] + fv[2] * uo[3]) * ir + vt[6] * nrm[0] + vt[7] * nrm[1] + vt[8] * nrm[2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sOut[it * 4 + c] = fv[c];
+        continue;
+      }
       double gt[12];
 #pragma unroll
       for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
       const int typ = typs[kf];
-      double fv[4] = {0.0, 0.0, 0.0, 0.0};
       if (typ == kConforming) {
-        const double* fm = sfm + s * 4 * N2 + f;
-        double nrm[3] = {fm[0], fm[N2], fm[2 * N2]};
-        if (ROT) rotate_yz(rot, nrm[1], nrm[2]);
         fv_n(sTr + it * 5, gt, nrm, C.gas, fv);
       } else {
         const int idx = P.side_idx[e * 6 + s];
@@ -1434,8 +865,8 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
 }
 
 // ============================================================================
-// k_update_cv: the update kernel of curved elements (even N+1).
-//   * The node's viscous stress and heat flux come from k_gradient_bulk (P.visc),
+// k_update_cv: the update kernel of curved and (AFF) affine elements (even N+1).
+//   * The node's viscous stress and heat flux come from the gradient kernel (P.visc),
 //     so the BR1 gradient is evaluated once per stage, not again here.
 //   * What only one thread reads is loaded by that thread while the tile's bulk
 //     copies are in flight: a face node's own trace, Fv.n and face metrics.
@@ -1450,17 +881,17 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
 // Shared memory per element: U | met, visc (later 3 x 5 staged fluxes) | face flux
 // | face sJ | neighbour slots (later dudt, then the new traces).
 // ============================================================================
-template <int N1, bool ROT, bool VISC>
+template <int N1, bool ROT, bool VISC, bool AFF = false>
 struct CV {
   static constexpr int N2 = N1 * N1, N3 = N2 * N1;
   static constexpr int MW = MWidth<ROT>::MW, FW = MWidth<ROT>::FW;
-  static constexpr int EPB = CB<N1, ROT>::EPB;
+  static constexpr int EPB = BulkEpb<N1>::EPB;
   static constexpr int THREADS = EPB * N3;
   static constexpr int TAB = Dim<N1>::TAB;
-  static constexpr int EL = 5 * N3, ML = MW * N3, VL = VISC ? 9 * N3 : 0;
+  static constexpr int EL = 5 * N3, ML = AFF ? 0 : MW * N3, VL = VISC ? 9 * N3 : 0;
   static constexpr int MV = (ML + VL > 15 * N3 ? ML + VL : 15 * N3);
   static constexpr int TS = 5 * N2, FS = 4 * N2, NB = TS + (VISC ? FS : 0);
-  static constexpr int FX = 6 * TS, SJ = 6 * N2;
+  static constexpr int FX = 6 * TS, SJ = AFF ? 0 : 6 * N2;
   static constexpr int NBR = 6 * NB > EL ? 6 * NB : EL;
   static constexpr int PER = EL + MV + FX + SJ + NBR;
   static constexpr int KF = (6 * N2 + N3 - 1) / N3;  // face nodes per thread
@@ -1468,22 +899,37 @@ struct CV {
 #ifndef SDG_CV_MINB
 #define SDG_CV_MINB 3
 #endif
-  static constexpr int MINB = N1 == 6 ? SDG_CV_MINB : 1;
+#ifndef SDG_CVA_MINB
+#define SDG_CVA_MINB 3  // affine: 58 KB per CTA
+#endif
+#ifndef SDG_CVA_MINB8
+#define SDG_CVA_MINB8 1
+#endif
+#ifndef SDG_CVA_MINB4
+#define SDG_CVA_MINB4 2
+#endif
+  static constexpr int MINB = N1 == 6   ? (AFF ? SDG_CVA_MINB : SDG_CV_MINB)
+                              : N1 == 8 ? (AFF ? SDG_CVA_MINB8 : 1)
+                              : N1 == 4 ? (AFF ? SDG_CVA_MINB4 : 1)
+                                        : 1;
+  // (Registers: the file is split over the SM's four schedulers, 16K each.  3 CTAs of 7 warps put 6
+  // warps on one scheduler -> at most 85 registers per thread; __launch_bounds__ makes ptxas stop at 80.
+  // A 96-register build -- 21 warps x 96 x 32 fits the SM's 64K as a whole -- ran 2 CTAs per SM.)
   static constexpr int SMEM = (TAB + EPB * PER) * 8 + 16;
   static_assert(N1 % 2 == 0, "bulk path needs even N+1");
   static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
   static_assert(6 * TS <= NBR, "new traces fit the neighbour region");
 };
 
-template <int N1, bool ROT, bool VISC>
+template <int N1, bool ROT, bool VISC, bool AFF>
 __device__ __forceinline__ void cv_issue_loads(const FieldPtrs& P, int e0, int n, double* base, uint64_t* bar) {
-  using D = CV<N1, ROT, VISC>;
+  using D = CV<N1, ROT, VISC, AFF>;
   uint32_t bytes = n * (D::EL + D::ML + D::VL) * 8u;
   for (int le = 0; le < n; ++le) {
     const int e = e0 + le;
     double* b = base + le * D::PER;
     bulk_g2s(b, P.U + static_cast<size_t>(e) * D::EL, D::EL * 8u, bar);
-    bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
+    if (!AFF) bulk_g2s(b + D::EL, P.met + static_cast<size_t>(e) * D::ML, D::ML * 8u, bar);
     if (VISC) bulk_g2s(b + D::EL + D::ML, P.visc + static_cast<size_t>(e) * D::VL, D::VL * 8u, bar);
   }
   constexpr int MASK = (1 << kCodeShift) - 1;
@@ -1513,10 +959,10 @@ __device__ __forceinline__ void cv_issue_loads(const FieldPtrs& P, int e0, int n
   mbar_arrive_expect_tx(bar, bytes);
 }
 
-template <int N1, bool VISC, bool ROT>
-__global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>::MINB) k_update_cv(
+template <int N1, bool VISC, bool ROT, bool AFF = false>
+__global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, VISC, AFF>::MINB) k_update_cv(
     const __grid_constant__ ElemConsts C, FieldPtrs P, const __grid_constant__ StageArgs A) {
-  using D = CV<N1, ROT, VISC>;
+  using D = CV<N1, ROT, VISC, AFF>;
   constexpr int FW = D::FW, KF = D::KF;
   constexpr int N2 = D::N2, N3 = D::N3, EPB = D::EPB, PER = D::PER, THREADS = D::THREADS;
   extern __shared__ __align__(128) double smem[];
@@ -1528,7 +974,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
-    cv_issue_loads<N1, ROT, VISC>(P, e0, n_el, base, bar);
+    cv_issue_loads<N1, ROT, VISC, AFF>(P, e0, n_el, base, bar);
     if (A.mode == 0 && A.rk_a != 0.0) bulk_prefetch_l2(P.reg + static_cast<size_t>(e0) * D::EL, n_el * D::EL * 8u);
   }
   const int le = threadIdx.x / N3, t = threadIdx.x % N3, e = e0 + le;
@@ -1548,7 +994,9 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
 
   // This thread's face nodes: own trace, own Fv.n, unit normal, sJ and vg.n straight from
   // global memory (nobody else reads them), in flight together with the bulk copies.
-  double own[KF][5], ofv[KF][4], nrm[KF][3], vgn[KF], sjf[KF];
+  // (sFlux and sSJ are no bulk-copy destinations: the own Fv.n waits in the flux slots this
+  // thread overwrites later, sJ goes straight to its place.)
+  double own[KF][5], nrm[KF][3], vgn[KF];
   int typs[KF], rots[KF];
 #pragma unroll
   for (int kf = 0; kf < KF; ++kf) {
@@ -1565,17 +1013,19 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
       if (VISC) {
         const double2* fp = reinterpret_cast<const double2*>(P.fvn + (static_cast<size_t>(e) * 6 * N2 + it) * 4);
         const double2 a0 = __ldg(fp), a1 = __ldg(fp + 1);
-        ofv[kf][0] = a0.x;
-        ofv[kf][1] = a0.y;
-        ofv[kf][2] = a1.x;
-        ofv[kf][3] = a1.y;
+        sFlux[(s * 5 + 1) * N2 + f] = a0.x;
+        sFlux[(s * 5 + 2) * N2 + f] = a0.y;
+        sFlux[(s * 5 + 3) * N2 + f] = a1.x;
+        sFlux[(s * 5 + 4) * N2 + f] = a1.y;
       }
-      const double* fm = P.fmet + static_cast<size_t>(e) * D::FM + s * FW * N2 + f;  // [side][c][f]
-      nrm[kf][0] = __ldg(fm);
-      nrm[kf][1] = __ldg(fm + N2);
-      nrm[kf][2] = __ldg(fm + 2 * N2);
-      sjf[kf] = __ldg(fm + 3 * N2);
-      if (ROT) vgn[kf] = B.vg * __ldg(fm + 4 * N2);
+      if constexpr (!AFF) {
+        const double* fm = P.fmet + static_cast<size_t>(e) * D::FM + s * FW * N2 + f;  // [side][c][f]
+        nrm[kf][0] = __ldg(fm);
+        nrm[kf][1] = __ldg(fm + N2);
+        nrm[kf][2] = __ldg(fm + 2 * N2);
+        sSJ[it] = __ldg(fm + 3 * N2);
+        if (ROT) vgn[kf] = B.vg * __ldg(fm + 4 * N2);
+      }
     }
   }
   load_tables<N1>(C, tab);
@@ -1590,7 +1040,9 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
       if (it >= 6 * N2) break;
       const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
       double* n = nrm[kf];
-      if (ROT) rotate_yz(rot, n[1], n[2]);
+      const int dir = s >> 1;
+      if constexpr (AFF) vgn[kf] = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
+      else if (ROT) rotate_yz(rot, n[1], n[2]);
       else vgn[kf] = B.vg * n[1];
       const double* nb = sNb + s * D::NB;
       const int typ = typs[kf];
@@ -1614,10 +1066,14 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
         }
         const double* um = (s & 1) ? own[kf] : other;
         const double* up = (s & 1) ? other : own[kf];
-        ok = roe_flux_n(um, up, n, vgn[kf], C.gas, flux);
+        if constexpr (AFF) ok = roe_flux(um, up, dir, vgn[kf], C.gas, flux);
+        else ok = roe_flux_n(um, up, n, vgn[kf], C.gas, flux);
         if (VISC) {
-          const double* fm = (s & 1) ? ofv[kf] : fvo;
-          const double* fp = (s & 1) ? fvo : ofv[kf];
+          double ofv[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ofv[c] = sFlux[(s * 5 + 1 + c) * N2 + f];
+          const double* fm = (s & 1) ? ofv : fvo;
+          const double* fp = (s & 1) ? fvo : ofv;
 #pragma unroll
           for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
         }
@@ -1630,7 +1086,8 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
         eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
         const double* um = (s & 1) ? own[kf] : ext;
         const double* up = (s & 1) ? ext : own[kf];
-        ok = roe_flux_n(um, up, n, vgn[kf], C.gas, flux);
+        if constexpr (AFF) ok = roe_flux(um, up, dir, vgn[kf], C.gas, flux);
+        else ok = roe_flux_n(um, up, n, vgn[kf], C.gas, flux);
         if (VISC) {
           const int idx = P.side_idx[e * 6 + s];
           const double* gd = P.dir_g + (static_cast<size_t>(idx) * N2 + f) * 12;
@@ -1638,8 +1095,13 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
 #pragma unroll
           for (int c = 0; c < 12; ++c) gg[c] = gd[c];
           double fm[4], fp[4];
-          fv_n(um, gg, n, C.gas, fm);
-          fv_n(up, gg, n, C.gas, fp);
+          if constexpr (AFF) {
+            fv_dir(um, gg, dir, C.gas, fm);
+            fv_dir(up, gg, dir, C.gas, fp);
+          } else {
+            fv_n(um, gg, n, C.gas, fm);
+            fv_n(up, gg, n, C.gas, fp);
+          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) flux[1 + c] -= 0.5 * (fm[c] + fp[c]);
         }
@@ -1647,7 +1109,6 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
       if (!ok) record_error(P.err, 2, A.step, A.stage, e, -1 - it, own[kf]);
 #pragma unroll
       for (int v = 0; v < 5; ++v) sFlux[(s * 5 + v) * N2 + f] = flux[v];
-      sSJ[it] = sjf[kf];
     }
   }
 
@@ -1684,19 +1145,28 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
         F[d][4] -= tau[d][0] * vv[0] + tau[d][1] * vv[1] + tau[d][2] * vv[2] + vs[(6 + d) * N3];
       }
     }
-    if (ROT) {  // Ja(t) . F = Ja(0) . (R^T F)
+    if (ROT && !AFF) {  // Ja(t) . F = Ja(0) . (R^T F)
 #pragma unroll
       for (int v = 0; v < 5; ++v) rotate_yz(Rot{rot.c, -rot.s}, F[1][v], F[2][v]);
     }
-    const double* ja = sM + t;  // [c][node]
-    ij = ja[9 * N3];
     double Ft[3][5];
+    if constexpr (AFF) {  // contravariant flux sJ_d F_d (volume_kernel, solver.cpp:357-370)
+      ij = B.inv_jac;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
-      const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
+      for (int d = 0; d < 3; ++d) {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
+        for (int v = 0; v < 5; ++v) Ft[d][v] = F[d][v] * B.sj[d];
+      }
+    } else {
+      const double* ja = sM + t;  // [c][node]
+      ij = ja[9 * N3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double wv = ROT ? B.vg * ja[(10 + d) * N3] : 0.0;  // contravariant grid velocity
+        const double j0 = ja[(3 * d) * N3], j1 = ja[(3 * d + 1) * N3], j2 = ja[(3 * d + 2) * N3];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) Ft[d][v] = j0 * F[0][v] + j1 * F[1][v] + j2 * F[2][v] - wv * u[v];
+      }
     }
     // Every read of this node's columns precedes these stores in program order.
 #pragma unroll
@@ -1746,7 +1216,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC>::THREADS, CV<N1, ROT, VISC>:
       const int f = dir == 0 ? j * N1 + k : (dir == 1 ? i * N1 + k : i * N1 + j);
       const double l = lw[(s & 1) * N1 + ia];
       if (l != 0.0) {
-        const double c = ((s & 1) ? -1.0 : 1.0) * l * sSJ[s * N2 + f] * ij;
+        const double c = AFF ? ((s & 1) ? -1.0 : 1.0) * B.cdir[dir] * l : ((s & 1) ? -1.0 : 1.0) * l * sSJ[s * N2 + f] * ij;
 #pragma unroll
         for (int v = 0; v < 5; ++v) du[v] += c * sFlux[(s * 5 + v) * N2 + f];
       }
@@ -1815,31 +1285,30 @@ bool update_affine_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs&
   if constexpr (N1 % 2 != 0) {
     return false;
   } else {
-    using D = CB<N1, false, true>;
-    const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-    auto kern = c.gas.viscous ? k_update_bulk<N1, true, false, true> : k_update_bulk<N1, false, false, true>;
-    set_smem_checked(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::U_SMEM);
-    kern<<<blocks, D::THREADS, D::U_SMEM, st>>>(c, p, a);
-    check_launch("k_update_bulk (affine)");
+    if (c.gas.viscous && p.visc == nullptr) throw ProtocolError("k_update_cv needs the stress buffer of the gradient kernel");
+    if (c.gas.viscous) {
+      using D = CV<N1, false, true, true>;
+      const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+      set_smem_checked(k_update_cv<N1, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
+      k_update_cv<N1, true, false, true><<<blocks, D::THREADS, D::SMEM, st>>>(c, p, a);
+    } else {
+      using D = CV<N1, false, false, true>;
+      const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
+      set_smem_checked(k_update_cv<N1, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
+      k_update_cv<N1, false, false, true><<<blocks, D::THREADS, D::SMEM, st>>>(c, p, a);
+    }
+    check_launch("k_update_cv (affine)");
     return true;
   }
 }
 
 template <int N1, bool ROT>
 void gradient_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-#ifdef SDG_GRAD_BULK  // the 3-CTA kernel that also stages the state and every metric row
-  using D = CB<N1, ROT>;
-  const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
-  set_smem_checked(k_gradient_bulk<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::G_SMEM);
-  k_gradient_bulk<N1, ROT><<<blocks, D::THREADS, D::G_SMEM, st>>>(c, p, a);
-  check_launch("k_gradient_bulk");
-#else
   using D = CG<N1, ROT>;
   const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;
   set_smem_checked(k_gradient_cv<N1, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
   k_gradient_cv<N1, ROT><<<blocks, D::THREADS, D::SMEM, st>>>(c, p, a);
   check_launch("k_gradient_cv");
-#endif
 }
 template <int N1>
 bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
@@ -1853,7 +1322,7 @@ bool gradient_curved_b_t(const ElemConsts& c, const FieldPtrs& p, const StageArg
 }
 template <int N1, bool ROT>
 void update_curved_b_r(const ElemConsts& c, const FieldPtrs& p, const StageArgs& a, cudaStream_t st) {
-  if (c.gas.viscous && p.visc == nullptr) throw ProtocolError("k_update_cv needs the stress buffer of k_gradient_bulk");
+  if (c.gas.viscous && p.visc == nullptr) throw ProtocolError("k_update_cv needs the stress buffer of the gradient kernel");
   if (c.gas.viscous) {
     using D = CV<N1, ROT, true>;
     const int blocks = (p.E - p.e_first + D::EPB - 1) / D::EPB;

@@ -328,6 +328,23 @@ __device__ __forceinline__ void face_position(const ElemConsts& C, const int* cr
   map_position(C, crd, xi, eta, zeta, t, x);
 }
 
+// Viscous stress tensor (tau_00, tau_01, tau_02, tau_11, tau_12, tau_22) and heat flux
+// k dT/dx_d of a node from its BR1 gradient g[3 q + d] = d q / d x_d, q = (v1, v2, v3, T)
+// (viscous_flux, flux.cpp:23-42).
+__device__ __forceinline__ void visc_terms(const double* g, const GasD& gas, double* o) {
+  const double div = g[0] + g[4] + g[8];
+  const double mu = gas.mu, lam = gas.lam;
+  o[0] = 2.0 * mu * g[0] + lam * div;
+  o[1] = mu * (g[1] + g[3]);
+  o[2] = mu * (g[2] + g[6]);
+  o[3] = 2.0 * mu * g[4] + lam * div;
+  o[4] = mu * (g[5] + g[7]);
+  o[5] = 2.0 * mu * g[8] + lam * div;
+  o[6] = gas.kcond * g[9];
+  o[7] = gas.kcond * g[10];
+  o[8] = gas.kcond * g[11];
+}
+
 template <int N1>
 __device__ __forceinline__ void load_tables(const ElemConsts& C, double* tab) {
   // tab: dhat[N1*N1] | fl | fr | liftw0 | liftw1 | inv_w | (unused)
@@ -1522,7 +1539,7 @@ __device__ __forceinline__ void issue_gradient_loads5(const FieldPtrs& P, int ti
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised k_gradient (SDG_GRAD_V=6): the same phases as k_gradient5 on
+// Warp-specialised k_gradient: the same phases as k_gradient5 on
 // the consumer warps (EPB*N3 threads rounded up to whole warps, synchronised by
 // named barrier 1), plus one producer warp that owns every asynchronous copy:
 // side-code prefetch, the TMA stage loads (full[s] barriers), and the bulk
@@ -1660,6 +1677,15 @@ __global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(
       double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
 #pragma unroll
       for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
+    }
+    if (active && P.visc != nullptr) {  // stress and heat flux of the node for k_update_cv (coalesced rows [c][node])
+      double g[12], vs[9];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) g[c] = gS[c * N3 + t];
+      visc_terms(g, C.gas, vs);
+      double* vo = P.visc + static_cast<size_t>(e) * 9 * N3 + t;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) vo[c * N3] = vs[c];
     }
     // Phase 3: Fv.n on conforming sides; full gradient traces on sliding / Dirichlet sides.
     if (active) {

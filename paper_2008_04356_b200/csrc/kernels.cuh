@@ -70,7 +70,7 @@ struct FieldPtrs {
   const double* fmet;        // curved: 6E x N2 x 4 (unit +xi normal, sJ) per local side
   const int8_t* side_rot;    // E x 6: neighbour vectors rotate by side_rot * sector angle (annulus sectors)
   double* visc;              // curved, viscous, even N+1: E x 9 x N3 (tau_00 01 02 11 12 22, k dT/dx_d), written by
-                             // k_gradient_bulk and read by k_update_cv in place of a second gradient evaluation
+                             // the gradient kernel and read by k_update_cv in place of a second gradient evaluation
   ErrRec* err;
   int E;        // element kernels process local elements [e_first, E)
   int e_first;  // (interior / boundary split for exchange overlap; 0 = all)

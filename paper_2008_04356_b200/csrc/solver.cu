@@ -624,11 +624,11 @@ void GpuRankSolver::upload_topology() {
     }
     met_.upload(cm.met, stream_);
     fmet_.upload(cm.fmet, stream_);
-    // Viscous stresses and heat flux per node, handed from the gradient kernel to the
-    // update kernel (bulk-loaded kernels, even N+1; curved.cuh k_update_cv).
-    if (cfg_.gas.mu > 0.0 && n_ % 2 == 0) visc_.alloc(static_cast<size_t>(E_) * n3_ * 9);
     cuda_check(cudaStreamSynchronize(stream_), "metric upload");
   }
+  // Viscous stresses and heat flux per node, handed from the gradient kernel to the
+  // update kernel (bulk-loaded kernels, even N+1; curved.cuh k_update_cv).
+  if (cfg_.gas.mu > 0.0 && n_ % 2 == 0) visc_.alloc(static_cast<size_t>(E_) * n3_ * 9);
   err_.alloc(1);
   err_.zero(stream_);
   dt_min_.alloc(1);

@@ -38,6 +38,9 @@ KEYS = [
     "launch__occupancy_limit_registers",
     "launch__occupancy_limit_shared_mem",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum.pct_of_peak_sustained_elapsed",
 ]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
@@ -52,8 +55,21 @@ def raw(rep):
     return [{h: (u, v) for h, u, v in zip(hdr, units, r)} for r in vals]
 
 
+def fp64_flops(rec):
+    """FP64 flops of one launch from the SASS thread-instruction rates (FMA = 2)."""
+    try:
+        cyc = float(rec["smsp__cycles_elapsed.avg"][1].replace(",", ""))
+        tot = 0.0
+        for op, w in (("dfma", 2), ("dadd", 1), ("dmul", 1)):
+            tot += w * cyc * float(rec[f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"][1]
+                                   .replace(",", ""))
+        return tot
+    except (KeyError, ValueError):
+        return None
+
+
 def summarize(tag, dof):
-    lines, kernels, bytes_k = [], [], []
+    lines, kernels, bytes_k, flops_k = [], [], [], []
     # Exactly this pass's element-kernel captures (measure.sh names them <tag>_<kernel>_raw.csv);
     # a bare prefix match would also take another pass's files whose tag extends this one.
     pat = re.compile(re.escape(tag) + r"_k_[a-z0-9_]+?(_raw\.csv|\.ncu-rep)$")
@@ -80,6 +96,9 @@ def summarize(tag, dof):
             wr = float(rec["dram__bytes_write.sum"][1].replace(",", "")) * SCALE[rec["dram__bytes_write.sum"][0]]
             kernels.append(name)
             bytes_k.append(rd + wr)
+            flops_k.append(fp64_flops(rec))
+            if flops_k[-1] is not None:
+                lines.append(f"  fp64 flops (2 dfma + dadd + dmul thread instructions)           {flops_k[-1]:.6g}")
     with open(os.path.join(PROF, f"{tag}_ncu_summary.txt"), "w") as f:
         f.write(f"# {tag}: ncu --set full --clock-control none --import-source on, one launch per kernel\n")
         f.write("# command: tools/measure.sh (python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e)\n")
@@ -101,6 +120,8 @@ def summarize(tag, dof):
             "dram_bytes_per_stage": sum(bytes_k),
             "dof": dof,
             "dram_bytes_per_dof": sum(bytes_k) / dof,
+            "fp64_flops_per_kernel": flops_k,
+            "fp64_flops_per_dof": (sum(flops_k) / dof) if all(f is not None for f in flops_k) else None,
             "note": f"ncu --set full (profiles/{tag}_ncu_summary.txt); one launch of each element kernel; "
                     "mortar/pairing kernels add <1%",
         }
