@@ -379,12 +379,18 @@ def roofline(kt, conf, args, peaks, value_per_gpu, ms_per_step):
     #   curved (even N+1): k_gradient_cv also reads Ja, 1/J (10 rows) and 4 face-metric rows and writes the
     #   node's stress / heat flux (9); k_update_cv reads those 9, all node-metric rows and the face-metric rows
     #   it uses instead of evaluating the gradient again.
-    per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 18), "gradient": 8 * E * (5 * n3 + 6 * n2 * 9)}
+    #   per face node: own trace 5 + own Fv.n 4 + neighbour trace 5 + Fv.n 4 read, new trace 5 written (update);
+    #   own + neighbour trace read, Fv.n written (gradient).
+    per_kernel = {"update": 8 * E * (20 * n3 + 6 * n2 * 23), "gradient": 8 * E * (5 * n3 + 6 * n2 * 14)}
+    even = n1 % 2 == 0
+    if even:  # the node's stress / heat flux (9 doubles) handed from the gradient to the update kernel
+        per_kernel["gradient"] += 8 * E * 9 * n3
+        per_kernel["update"] += 8 * E * 9 * n3
     if curved:
         mw, fw_u = (13, 5) if args.mesh == "rotor" else (10, 4)
-        if n1 % 2 == 0:
-            per_kernel["gradient"] += 8 * E * (10 * n3 + 6 * n2 * 4 + 9 * n3)
-            per_kernel["update"] += 8 * E * (mw * n3 + 6 * n2 * fw_u + 9 * n3)
+        if even:
+            per_kernel["gradient"] += 8 * E * (10 * n3 + 6 * n2 * 4)
+            per_kernel["update"] += 8 * E * (mw * n3 + 6 * n2 * fw_u)
         else:  # plain-load kernels: every metric row in both, gradient evaluated twice
             for k in per_kernel:
                 per_kernel[k] += 8 * E * (mw * n3 + 6 * n2 * (6 if args.mesh == "rotor" else 4))

@@ -616,6 +616,17 @@ struct BulkEpb {
   static constexpr int EPB = N1 == 2 ? 16 : (N1 <= 4 ? Dim<N1>::EPB : 1);
 };
 
+// Exterior state of a Dirichlet face node (the exact case at the node's position).  Kept out
+// of line: its position mapping and transcendental code would otherwise set the register
+// budget of the whole kernel, though only boundary elements run it.
+template <int N1>
+__device__ __noinline__ void dirichlet_state(const ElemConsts& C, const int* crd, int side, int a, int b, double t,
+                                             double* ext) {
+  double x[3];
+  face_position<N1>(C, crd, side, a, b, t, x);
+  eval_case(C.flow_case, x, t, C.gas, ext);
+}
+
 // ============================================================================
 // k_gradient_cv: lift* -> curved gradient -> Fv.n (conforming sides) / gradient
 // traces (sliding and Dirichlet sides), the node's viscous stress for k_update_cv
@@ -769,9 +780,8 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
 #pragma unroll
         for (int c = 0; c < 4; ++c) lift[c] = sNb[s * D::TS + f * 4 + c];
       } else {
-        double x[3], ext[5];
-        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        double ext[5];
+        dirichlet_state<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, ext);
         prim4(ext, C.gas, lift);
       }
 #pragma unroll
@@ -1081,9 +1091,8 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
 #pragma unroll
         for (int v = 0; v < 5; ++v) flux[v] = nb[f * 5 + v];
       } else {
-        double x[3], ext[5];
-        face_position<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, x);
-        eval_case(C.flow_case, x, A.t_stage, C.gas, ext);
+        double ext[5];
+        dirichlet_state<N1>(C, P.coords + 4 * e, s, a, b, A.t_stage, ext);
         const double* um = (s & 1) ? own[kf] : ext;
         const double* up = (s & 1) ? ext : own[kf];
         if constexpr (AFF) ok = roe_flux(um, up, dir, vgn[kf], C.gas, flux);

@@ -1949,9 +1949,9 @@ static void device_interface_project(int degree, int kind, const long* nfy, cons
   d_ivy.alloc(2 * (nfy[0] + nfy[1]));
   d_ivz.alloc(2 * (nfz[0] + nfz[1]));
   d_rng.alloc(4 * std::max(nfy[0] + nfy[1], nfz[0] + nfz[1]));
-  d_n.alloc(1);
+  d_n.alloc(2);
   launch_mortar_intervals(nfy[0], nfy[1], l_y, d_y, d_ivy.p, d_rng.p, d_n.p, st);
-  launch_mortar_intervals(nfz[0], nfz[1], l_z, d_z, d_ivz.p, d_rng.p, d_n.p, st);
+  launch_mortar_intervals(nfz[0], nfz[1], l_z, d_z, d_ivz.p, d_rng.p, d_n.p + 1, st);
   d_Fy.upload(Fy, st);
   d_By.upload(By, st);
   d_Fz.upload(Fz, st);
@@ -1972,7 +1972,12 @@ static void device_interface_project(int degree, int kind, const long* nfy, cons
   if (dst)
     cuda_check(cudaMemcpyAsync(dst, d_dst.p, nfy[to] * nfz[to] * per * sizeof(double), cudaMemcpyDeviceToHost, st),
                "copy");
+  long long dn[2] = {0, 0};
+  cuda_check(cudaMemcpyAsync(dn, d_n.p, sizeof(dn), cudaMemcpyDeviceToHost, st), "copy");
   cuda_check(cudaStreamSynchronize(st), "sync");
+  if (dn[0] != my || dn[1] != mz)  // the kernels indexed with the device's rows; the operators came from the host's
+    throw ProtocolError("interface transfer: device rows (" + std::to_string(dn[0]) + " x " + std::to_string(dn[1]) +
+                        ") differ from the host's (" + std::to_string(my) + " x " + std::to_string(mz) + ")");
 }
 
 // The operators of one side s of a mortar row: face -> mortar (F) and mortar ->
@@ -2088,8 +2093,14 @@ static void device_interface_flux(const sdg_gas& gas, int degree, int kind, cons
   if (flux_mortar)
     cuda_check(cudaMemcpyAsync(flux_mortar, d_flux.p, d_flux.n * sizeof(double), cudaMemcpyDeviceToHost, st), "copy");
   int bad = 0;
+  long long dn[2] = {0, 0};
   cuda_check(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+  cuda_check(cudaMemcpyAsync(dn, d_n.p, sizeof(dn), cudaMemcpyDeviceToHost, st), "copy");
   cuda_check(cudaStreamSynchronize(st), "sync");
+  // The kernels indexed with the device's rows; the operators came from the host's.
+  if (dn[0] != my || dn[1] != mz)
+    throw ProtocolError("interface flux: device rows (" + std::to_string(dn[0]) + " x " + std::to_string(dn[1]) +
+                        ") differ from the host's (" + std::to_string(my) + " x " + std::to_string(mz) + ")");
   if (bad) throw InvalidStateError("interface flux: non-positive Roe-averaged c^2 at " + std::to_string(bad) + " mortar nodes");
 }
 

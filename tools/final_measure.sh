@@ -1,7 +1,9 @@
-# End-of-round measurement: tests, smoke, default bench + reference arm + ncu (affine), then the curved
-# and configs[3] bench lines with their own ncu captures.
-bash tools/measure.sh ${1:-r1d}
-SKIP_TESTS=1 BENCH_ARGS="--mesh warped" bash tools/measure.sh ${1:-r1d}_curved_warped
-timeout 1500 python bench.py --mesh rotor --steps 3 --warmup 3 > gpurun_out/${1:-r1d}_bench_rotor.log 2>&1
-tail -1 gpurun_out/${1:-r1d}_bench_rotor.log > gpurun_out/${1:-r1d}_bench_rotor.json
+# End-of-round measurement: tests, smoke, the default (configs[3]) bench line + reference arm + ncu captures,
+# then the configs[4] TGV line with its own ncu captures, the curved TGV line and the configs[4] sweep.
+T=${1:-r2z}
+bash tools/measure.sh $T
+SKIP_TESTS=1 BENCH_ARGS="--mesh tgv" bash tools/measure.sh ${T}_tgv
+timeout 900 python bench.py --mesh warped --no-cpu-baseline --no-e2e > gpurun_out/${T}_bench_warped.log 2>&1
+tail -1 gpurun_out/${T}_bench_warped.log > gpurun_out/${T}_bench_warped.json
+bash tools/sweep.sh $T
 echo final-done

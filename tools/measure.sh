@@ -19,5 +19,6 @@ for k in k_update k_gradient; do
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e $BENCH_ARGS > $O/${TAG}_ncu_$k.log 2>&1
   $NCU -i /tmp/${TAG}_$k.ncu-rep --page raw --csv > $O/${TAG}_${k}_raw.csv 2>/dev/null
   $NCU -i /tmp/${TAG}_$k.ncu-rep --page details > $O/${TAG}_${k}_details.txt 2>/dev/null
+  $NCU -i /tmp/${TAG}_$k.ncu-rep --page source --csv > $O/${TAG}_${k}_src.csv 2>/dev/null
 done
 echo done
