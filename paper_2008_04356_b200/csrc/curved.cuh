@@ -720,9 +720,10 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
   double* sNb = sTr + 6 * D::TS;  // [side]: trace [f][5] or lift* [f][4]
   double* sLift = sNb + 6 * D::TS;
   double* sG = sM;                // [c][node], c < 12, once every node's gradient is computed
-  const int band = active ? P.coords[4 * e] : 0;
-  const Rot rot = band_rotation(ROT, A, band);
-  // While the bulk copies are in flight: this node's state and this thread's side types.
+  // While the bulk copies are in flight: this node's state and this thread's side types.  Nothing
+  // before the wait depends on another load's result (the band is used after it), so every
+  // thread's loads leave at once.
+  const int band_ld = active ? P.side_code[8 * e + 6] : 0;
   double u[5];
   int typs[KF], rots[KF];
   if (active) {
@@ -741,17 +742,26 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
   // heat flux are linear in the gradient, so their 9 components are prolonged instead of
   // the gradient's 12.  Sliding / Dirichlet sides need the gradient trace itself.
   bool allconf = false;
-  if (active) {
-    constexpr int MASK = (1 << kCodeShift) - 1;
-    const int4 c0 = __ldg(reinterpret_cast<const int4*>(P.side_code + 8 * e));
-    const int2 c1 = __ldg(reinterpret_cast<const int2*>(P.side_code + 8 * e + 4));
-    const int any = (c0.x | c0.y | c0.z | c0.w | c1.x | c1.y) & ~MASK;
-    const int all = (c0.x & c0.y & c0.z & c0.w & c1.x & c1.y) & ~MASK;
-    allconf = any == (kConforming << kCodeShift) && all == (kConforming << kCodeShift);
-  }
   load_tables<N1>(C, tab);
-  __syncthreads();  // barrier init visible, tables loaded
+  if constexpr (EPB == 1) {
+    // One element per CTA: the barrier before the wait doubles as the vote over the side types.
+    bool mine = true;
+#pragma unroll
+    for (int kf = 0; kf < KF; ++kf) mine = mine && (t + kf * N3 >= 6 * N2 || typs[kf] == kConforming);
+    allconf = __syncthreads_and(mine) != 0;  // barrier init visible, tables loaded
+  } else {
+    if (active) {
+      constexpr int MASK = (1 << kCodeShift) - 1;
+      const int4 c0 = __ldg(reinterpret_cast<const int4*>(P.side_code + 8 * e));
+      const int2 c1 = __ldg(reinterpret_cast<const int2*>(P.side_code + 8 * e + 4));
+      const int any = (c0.x | c0.y | c0.z | c0.w | c1.x | c1.y) & ~MASK;
+      const int all = (c0.x & c0.y & c0.z & c0.w & c1.x & c1.y) & ~MASK;
+      allconf = any == (kConforming << kCodeShift) && all == (kConforming << kCodeShift);
+    }
+    __syncthreads();  // barrier init visible, tables loaded
+  }
   mbar_wait(bar, 0);
+  const Rot rot = band_rotation(ROT, A, band_ld);
   if (active) {
     double q[4];
     prim4(u, C.gas, q);
@@ -998,9 +1008,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
   double* sNb = sSJ + D::SJ;         // [side]: trace [f][5] | Fv.n [f][4]  (sliding: flux [f][5])
   double* sD = sNb;                  // dudt [node][5], after the face phase
   const int i = t / N2, j = (t / N1) % N1, k = t % N1;
-  const int band = active ? P.coords[4 * e] : 0;
-  const BandD& B = C.bands[band];
-  const Rot rot = band_rotation(ROT, A, band);
+  const int band_ld = active ? P.side_code[8 * e + 6] : 0;  // used after the wait: no load below depends on it
 
   // This thread's face nodes: own trace, own Fv.n, unit normal, sJ and vg.n straight from
   // global memory (nobody else reads them), in flight together with the bulk copies.
@@ -1034,13 +1042,15 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
         nrm[kf][1] = __ldg(fm + N2);
         nrm[kf][2] = __ldg(fm + 2 * N2);
         sSJ[it] = __ldg(fm + 3 * N2);
-        if (ROT) vgn[kf] = B.vg * __ldg(fm + 4 * N2);
+        if (ROT) vgn[kf] = __ldg(fm + 4 * N2);  // (vg / omega) . n; times the band's omega after the wait
       }
     }
   }
   load_tables<N1>(C, tab);
   __syncthreads();  // barrier init visible, tables loaded
   mbar_wait(bar, 0);
+  const BandD& B = C.bands[band_ld];
+  const Rot rot = band_rotation(ROT, A, band_ld);
 
   // Phase 1: numerical flux along each face node's normal -> sFlux, sJ -> sSJ.
   if (active) {
@@ -1051,9 +1061,14 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
       const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
       double* n = nrm[kf];
       const int dir = s >> 1;
-      if constexpr (AFF) vgn[kf] = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
-      else if (ROT) rotate_yz(rot, n[1], n[2]);
-      else vgn[kf] = B.vg * n[1];
+      if constexpr (AFF) {
+        vgn[kf] = dir == 1 ? B.vg : (dir == 2 ? B.vgz : 0.0);
+      } else if (ROT) {
+        rotate_yz(rot, n[1], n[2]);
+        vgn[kf] *= B.vg;
+      } else {
+        vgn[kf] = B.vg * n[1];
+      }
       const double* nb = sNb + s * D::NB;
       const int typ = typs[kf];
       double flux[5];

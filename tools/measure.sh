@@ -9,7 +9,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O
 [ -n "$SKIP_TESTS" ] || timeout 1200 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/${TAG}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke exit $?" >> $O/${TAG}_smoke.log
 timeout 900 python bench.py $BENCH_ARGS > $O/${TAG}_bench.log 2>&1 && tail -1 $O/${TAG}_bench.log > $O/${TAG}_bench.json
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/${TAG}_bench_ref.log 2>&1 && tail -1 $O/${TAG}_bench_ref.log > $O/${TAG}_bench_ref.json
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 $BENCH_ARGS > $O/${TAG}_bench_ref.log 2>&1 && tail -1 $O/${TAG}_bench_ref.log > $O/${TAG}_bench_ref.json
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e $BENCH_ARGS > $O/${TAG}_ncu_launches.log 2>&1
