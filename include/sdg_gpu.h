@@ -77,6 +77,11 @@ SDG_API const char* sdg_last_error(const sdg_ctx* ctx);
 SDG_API const char* sdg_global_error(void);
 /* Fills SDG_NCCL_ID_BYTES bytes (rank 0 calls it and broadcasts). */
 SDG_API int sdg_nccl_unique_id(void* out);
+/* A one-rank NCCL communicator on `device` driven through every call of the transport
+ * (transport.hpp:39-81's role): init, the all-gathers of init_rank_maps, min / sum
+ * all-reduces, one grouped send + receive round of n_doubles to the rank itself.
+ * SDG_OK when every result is exact. */
+SDG_API int sdg_nccl_selfcheck(int device, long n_doubles);
 
 SDG_API int sdg_init_rank_maps(sdg_ctx* ctx);
 SDG_API int sdg_set_initial_condition(sdg_ctx* ctx, double t0);

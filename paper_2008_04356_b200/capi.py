@@ -47,6 +47,7 @@ def lib():
         L.sdg_last_error.restype = C.c_char_p
         L.sdg_global_error.restype = C.c_char_p
         L.sdg_nccl_unique_id.argtypes = [C.c_void_p]
+        L.sdg_nccl_selfcheck.argtypes = [C.c_int, C.c_long]
         L.sdg_init_rank_maps.argtypes = [_vp]
         L.sdg_set_initial_condition.argtypes = [_vp, C.c_double]
         L.sdg_n1.argtypes = [_vp]
@@ -108,7 +109,7 @@ def lib():
 
 
 EXPORTED = [
-    "sdg_create", "sdg_create_inproc", "sdg_destroy", "sdg_last_error", "sdg_global_error", "sdg_nccl_unique_id", "sdg_init_rank_maps",
+    "sdg_create", "sdg_create_inproc", "sdg_destroy", "sdg_last_error", "sdg_global_error", "sdg_nccl_unique_id", "sdg_nccl_selfcheck", "sdg_init_rank_maps",
     "sdg_set_initial_condition", "sdg_n1", "sdg_n_local_elements", "sdg_n_global_elements",
     "sdg_local_element_ids", "sdg_set_state", "sdg_get_state", "sdg_get_register", "sdg_state_device_ptr",
     "sdg_step", "sdg_steps", "sdg_steps_async", "sdg_synchronize", "sdg_rk_stage", "sdg_rk_coefficients",
@@ -139,6 +140,11 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     T.raise_for(lib().sdg_nccl_unique_id(buf), lib().sdg_global_error().decode())
     return buf.raw
+
+
+def nccl_selfcheck(device: int = 0, n_doubles: int = 1 << 20) -> None:
+    """Every NCCL call of the transport on a one-rank communicator (sdg_nccl_selfcheck)."""
+    T.raise_for(lib().sdg_nccl_selfcheck(device, n_doubles), lib().sdg_global_error().decode())
 
 
 class RankSolver:

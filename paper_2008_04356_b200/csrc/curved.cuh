@@ -909,7 +909,13 @@ struct CV {
   static constexpr int THREADS = EPB * N3;
   static constexpr int TAB = Dim<N1>::TAB;
   static constexpr int EL = 5 * N3, ML = AFF ? 0 : MW * N3, VL = VISC ? 9 * N3 : 0;
-  static constexpr int MV = (ML + VL > 15 * N3 ? ML + VL : 15 * N3);
+  // Directions staged at once for the weak divergence: all three (15 rows), or two and then
+  // the third (10 rows, two more barriers) where that buys another resident CTA: affine N = 7,
+  // 104 instead of 125 KB -> 2 CTAs/SM at 64 registers, 18.1 -> 16.7 ms at 64^3 elements
+  // (affine N = 5 at 4 CTAs x 72 registers lost: 5.47 -> 5.68 ms; profiles/r2l_ab.txt).
+  static constexpr int PASSES = (AFF && N1 == 8) ? 2 : 1;
+  static constexpr int FROWS = PASSES == 1 ? 15 : 10;
+  static constexpr int MV = (ML + VL > FROWS * N3 ? ML + VL : FROWS * N3);
   static constexpr int TS = 5 * N2, FS = 4 * N2, NB = TS + (VISC ? FS : 0);
   static constexpr int FX = 6 * TS, SJ = AFF ? 0 : 6 * N2;
   static constexpr int NBR = 6 * NB > EL ? 6 * NB : EL;
@@ -923,7 +929,7 @@ struct CV {
 #define SDG_CVA_MINB 3  // affine: 58 KB per CTA
 #endif
 #ifndef SDG_CVA_MINB8
-#define SDG_CVA_MINB8 1
+#define SDG_CVA_MINB8 2
 #endif
 #ifndef SDG_CVA_MINB4
 #define SDG_CVA_MINB4 2
@@ -1139,6 +1145,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
   // Phase 2: pointwise flux (ALE convective minus viscous) -> contravariant Ja^d . F, staged
   // over this node's own metric / stress columns.
   double ij = 0.0;
+  double ft2[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // third direction, staged in a second pass (PASSES == 2)
   if (active) {
     double u[5], F[3][5];
 #pragma unroll
@@ -1194,9 +1201,13 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
     }
     // Every read of this node's columns precedes these stores in program order.
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
+    for (int d = 0; d < (D::PASSES == 1 ? 3 : 2); ++d) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) sF3[(d * 5 + v) * N3 + t] = Ft[d][v];
+    }
+    if constexpr (D::PASSES == 2) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) ft2[v] = Ft[2][v];
     }
   }
   // RK register of this thread's flat positions (L2-prefetched), in flight across the barrier.
@@ -1214,11 +1225,11 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
 
   // Phase 3: weak divergence sum_m Dhat(i,m) Ft_d(m) over the three directions;
   // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double* dh = tab;
   if (active) {
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    const double* dh = tab;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
+    for (int d = 0; d < (D::PASSES == 1 ? 3 : 2); ++d) {
       const int ia = d == 0 ? i : (d == 1 ? j : k);
       const int bse = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
       const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
@@ -1229,6 +1240,25 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
         for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + bse + m * stride];
       }
     }
+  }
+  if constexpr (D::PASSES == 2) {
+    __syncthreads();  // the first two directions are consumed
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) sF3[v * N3 + t] = ft2[v];
+    }
+    __syncthreads();
+    if (active) {
+      const int bse = (i * N1 + j) * N1;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double c = dh[k * N1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF3[v * N3 + bse + m];
+      }
+    }
+  }
+  if (active) {
     double du[5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) du[v] = acc[v] * ij;

@@ -2416,6 +2416,47 @@ int sdg_nccl_unique_id(void* out) {
     std::memcpy(out, &id, sizeof(id));
   });
 }
+// One-rank communicator through every NcclComm method the solver uses: init, the two
+// all-gathers of init_rank_maps, the min / sum all-reduces of suggest_dt and the
+// diagnostics, and one grouped send + receive round (to the rank itself, the only
+// partner a single GPU offers).  The multi-rank data path is checked bitwise on the
+// in-process transport; this checks that the NCCL calls themselves run on the device.
+int sdg_nccl_selfcheck(int device, long n_doubles) {
+  return guarded(nullptr, [&] {
+    if (n_doubles < 1) throw sdg::ConfigError("sdg_nccl_selfcheck: n_doubles < 1");
+    int prev = -1;
+    sdg::cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    sdg::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    {
+      ncclUniqueId id;
+      sdg::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+      sdg::NcclComm comm(&id, 1, 0);
+      cudaStream_t st = nullptr;
+      sdg::cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+      std::vector<std::vector<int>> all;
+      const std::vector<int> mine = {7, 11, 13};
+      comm.allgather_ints(mine, all, st);
+      if (all.size() != 1 || all[0] != mine) throw sdg::ProtocolError("sdg_nccl_selfcheck: all-gather");
+      double v[3] = {3.5, -2.0, 8.25};
+      comm.allreduce(v, 3, 2, st);
+      comm.allreduce(v, 3, 0, st);
+      if (v[0] != 3.5 || v[1] != -2.0 || v[2] != 8.25) throw sdg::ProtocolError("sdg_nccl_selfcheck: all-reduce");
+      std::vector<double> h(static_cast<size_t>(n_doubles));
+      for (long i = 0; i < n_doubles; ++i) h[i] = 0.25 * static_cast<double>(i) - 3.0;
+      sdg::DevBuf<double> src, dst;
+      src.upload(h, st);
+      dst.alloc(h.size());
+      dst.zero(st);
+      comm.exchange({{0, src.p, h.size()}}, {{0, dst.p, h.size()}}, st);
+      std::vector<double> back(h.size());
+      sdg::cuda_check(cudaMemcpyAsync(back.data(), dst.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+      sdg::cuda_check(cudaStreamSynchronize(st), "sync");
+      cudaStreamDestroy(st);
+      if (back != h) throw sdg::ProtocolError("sdg_nccl_selfcheck: send / receive round");
+    }
+    if (prev >= 0) cudaSetDevice(prev);
+  });
+}
 int sdg_init_rank_maps(sdg_ctx* c) {
   return guarded(c, [&] { c->s->init_rank_maps(); });
 }

@@ -494,3 +494,13 @@ def test_update_interfaces_matches_oracle_and_reference(t):
                 rf, rb = P.ref_mortar_ops(3, T.NODES_GAUSS, gi["sigma_side"])
                 assert np.array_equal(ops[c, :2], rf) and np.array_equal(ops[c, 2:], rb)
         assert np.array_equal(g.mapping(c), o.mapping(c))
+
+
+def test_nccl_transport_calls_run_on_the_device():
+    """NCCL itself on the device (the N > 1 data path is checked bitwise on the in-process
+    transport; one GPU offers NCCL only the rank itself as a partner): a one-rank communicator
+    through every NcclComm method -- init, the all-gathers of init_rank_maps, min and sum
+    all-reduces, one grouped send + receive round of 8 MB -- with exact results."""
+    from paper_2008_04356_b200 import capi
+    capi.nccl_selfcheck(0, 1 << 20)
+    capi.nccl_selfcheck(0, 1)
