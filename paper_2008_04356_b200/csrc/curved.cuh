@@ -186,6 +186,7 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
   double acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+  const int rv = node_rot<N1>((i * N1 + j) * N1 + k);
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int ia = d == 0 ? i : (d == 1 ? j : k);
@@ -193,8 +194,9 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
     const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
-      const double c = dh[ia * N1 + m];
-      const int nd = base + m * stride;
+      const int mr = d == 2 ? m : rot_index<N1>(m, rv);  // bank rotation (node_rot)
+      const double c = dh[ia * N1 + mr];
+      const int nd = base + mr * stride;
       const double ja0 = sJa[(3 * d + 0) * N3 + nd], ja1 = sJa[(3 * d + 1) * N3 + nd],
                    ja2 = sJa[(3 * d + 2) * N3 + nd];
 #pragma unroll
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_gradient_curved(cons
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
     double gt[12];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
     const int slot = e * 6 + s;
     const int typ = P.side_type[slot], idx = P.side_idx[slot];
     if (typ == kConforming) {
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
       const double* ell = tab + N1 * N1 + (s & 1) * N1;
       double own[5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b);
+      for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b, face_rot<N1>(s, a, b));
       double nrm[3], vgn;
       face_normal<N2, FW, ROT>(sfm, s, f, rot, B, nrm, vgn);
       const int slot = e * 6 + s;
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(CDim<N1, ROT>::THREADS) k_update_curved(const 
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
     double* dst = P.trace_out + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
   }
 }
 
@@ -848,20 +850,21 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
       if (allconf) {  // Fv.n from the prolonged stress and heat flux (flux.cpp:23-42 contracted with n)
         double vt[9];
 #pragma unroll
-        for (int c = 0; c < 9; ++c) vt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+        for (int c = 0; c < 9; ++c) vt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
         const double* uo = sTr + it * 5;
         const double ir = rcp_nr(uo[0]);
         fv[0] = vt[0] * nrm[0] + vt[1] * nrm[1] + vt[2] * nrm[2];
         fv[1] = vt[1] * nrm[0] + vt[3] * nrm[1] + vt[4] * nrm[2];
         fv[2] = vt[2] * nrm[0] + vt[4] * nrm[1] + vt[5] * nrm[2];
         fv[3] = (fv[0] * uo[1] + fv[1] * uo[2] + fv[2] * uo[3]) * ir + vt[6] * nrm[0] + vt[7] * nrm[1] + vt[8] * nrm[2];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sOut[it * 4 + c] = fv[c];
+        double2* so = reinterpret_cast<double2*>(sOut + it * 4);  // [f][4]: 128-bit stores, no 4-way conflict
+        so[0] = make_double2(fv[0], fv[1]);
+        so[1] = make_double2(fv[2], fv[3]);
         continue;
       }
       double gt[12];
 #pragma unroll
-      for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+      for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
       const int typ = typs[kf];
       if (typ == kConforming) {
         fv_n(sTr + it * 5, gt, nrm, C.gas, fv);
@@ -1084,9 +1087,13 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
 #pragma unroll
         for (int v = 0; v < 5; ++v) other[v] = nb[f * 5 + v];
         double fvo[4];
-        if (VISC) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) fvo[c] = nb[D::TS + f * 4 + c];
+        if (VISC) {  // [f][4]: two 128-bit loads (stride-4 64-bit loads collide 4-way)
+          const double2* fq = reinterpret_cast<const double2*>(nb + D::TS + f * 4);
+          const double2 f0 = fq[0], f1 = fq[1];
+          fvo[0] = f0.x;
+          fvo[1] = f0.y;
+          fvo[2] = f1.x;
+          fvo[3] = f1.y;
         }
         if constexpr (ROT) {  // periodic annulus sector seam: the neighbour's vectors in this sector's frame
           if (rots[kf] != 0) {
@@ -1227,6 +1234,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
   // Phase 4: surface lift with (sJ of the face node) / (J of the volume node).
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const double* dh = tab;
+  const int nrot = node_rot<N1>(t);
   if (active) {
 #pragma unroll
     for (int d = 0; d < (D::PASSES == 1 ? 3 : 2); ++d) {
@@ -1235,9 +1243,10 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
       const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
 #pragma unroll
       for (int m = 0; m < N1; ++m) {
-        const double c = dh[ia * N1 + m];
+        const int mr = d == 2 ? m : rot_index<N1>(m, nrot);  // bank rotation (node_rot)
+        const double c = dh[ia * N1 + mr];
 #pragma unroll
-        for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + bse + m * stride];
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + bse + mr * stride];
       }
     }
   }
@@ -1322,7 +1331,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
       const int s = it / N2, f = it - s * N2, a = f / N1, b = f % N1;
       const double* ell = tab + N1 * N1 + (s & 1) * N1;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) sOut[it * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b);
+      for (int v = 0; v < 5; ++v) sOut[it * 5 + v] = prolong_aos<N1>(sU, v, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
     }
     fence_proxy_async();
   }

@@ -48,16 +48,72 @@ __device__ __forceinline__ void rot_yz(double c, double s, double& y, double& z)
 // written with explicit rounding intrinsics (no contraction freedom).
 // ----------------------------------------------------------------------------
 
+// Shared-memory bank rotation of the face contractions.  A face node's line of N1
+// values is read in the rotated order m -> (m + rot) mod N1, with rot a fixed function
+// of the face node (side, a, b), so that the 16 threads of a half-warp (consecutive
+// face nodes it = side * N2 + a * N1 + b) hit 16 different 8-byte banks of a
+// [row][node] element block.  Unrotated, the lines along j and k collide 2-way at
+// N+1 = 6, 4-way at 4 and up to 8-way at 8 (line starts are multiples of N+1).
+// The rotation is part of the canonical trace: every kernel that prolongs a
+// state uses the same order, so all of them produce the same bits.
+// N+1 = 6 has no closed form (36 face nodes per side do not tile half-warps);
+// its table comes from a per-half-warp search (tools/bank_rotation.py).
+__device__ const unsigned char kFaceRot6[216] = {
+    0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0,  // side 0
+    1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0,  // side 1
+    3, 3, 3, 3, 2, 2, 3, 3, 0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1,  // side 2
+    1, 1, 1, 1, 0, 0, 1, 1, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0, 1, 1, 0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0,  // side 3
+    0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0,  // side 4
+    1, 1, 1, 1, 1, 0, 1, 0, 5, 2, 5, 2, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0,  // side 5
+};
+
+template <int N1>
+__device__ __forceinline__ int face_rot(int side, int a, int b) {
+  const int dir = side >> 1;
+  if constexpr (N1 == 4) {
+    return dir == 0 ? 0 : a;
+  } else if constexpr (N1 == 8) {
+    return dir == 0 ? 0 : (dir == 1 ? (a & 1) : (b >> 1) + 4 * (a & 1));
+  } else if constexpr (N1 == 6) {
+    return kFaceRot6[side * 36 + a * 6 + b];
+  } else {
+    return 0;
+  }
+}
+
+// Rotated line index (m + rot) mod N1 for 0 <= m, rot < N1.
+template <int N1>
+__device__ __forceinline__ int rot_index(int m, int rot) {
+  const int r = m + rot;
+  return r >= N1 ? r - N1 : r;
+}
+
+// The same rotation for the volume contractions of node threads (thread t = node
+// (i, j, k) reads its lines along i and j): only N+1 = 6 needs it, where a half-warp
+// that straddles two i-planes (36 nodes each) hits the banks of the previous plane's
+// tail.  Those threads start their lines one node later.
+template <int N1>
+__device__ __forceinline__ int node_rot(int t) {
+  if constexpr (N1 == 6) {
+    return (t & ~15) < 36 * (t / 36) ? 1 : 0;
+  } else {
+    return 0;
+  }
+}
+
 // Face trace of one variable along the face normal (solver.cpp:208-232).
 template <int N1>
 __device__ __forceinline__ double prolong1(const double* __restrict__ s, const double* __restrict__ ell, int dir,
-                                           int a, int b) {
+                                           int a, int b, int rot) {
   constexpr int N2 = N1 * N1;
   const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
   const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
   double acc = 0.0;
 #pragma unroll
-  for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[base + m * stride], acc);
+  for (int m = 0; m < N1; ++m) {
+    const int mr = rot_index<N1>(m, rot);
+    acc = __fma_rn(ell[mr], s[base + mr * stride], acc);
+  }
   return acc;
 }
 
@@ -394,7 +450,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_prolong(const __grid_const
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
     double* dst = P.trace + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
   }
 }
 
@@ -413,7 +469,7 @@ __device__ __forceinline__ void face_lift_phase(const ElemConsts& C, const Field
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
     double own[5];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+    for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
     if (sTr != nullptr) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) sTr[(s * N2 + f) * 5 + v] = own[v];
@@ -595,7 +651,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_gradient(const __grid_cons
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
     double gt[12];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b);
+    for (int c = 0; c < 12; ++c) gt[c] = prolong1<N1>(sG + c * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
     const int slot = e * 6 + s;
     const int typ = P.side_type[slot], idx = P.side_idx[slot];
     if (typ == kConforming) {
@@ -661,7 +717,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
       const double* ell = tab + N1 * N1 + (s & 1) * N1;
       double own[5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b);
+      for (int v = 0; v < 5; ++v) own[v] = prolong1<N1>(su + v * N3, ell, dir, a, b, face_rot<N1>(s, a, b));
       const int slot = e * 6 + s;
       const int typ = P.side_type[slot], idx = P.side_idx[slot];
       double flux[5], lift[4];
@@ -861,7 +917,7 @@ __global__ void __launch_bounds__(Dim<N1>::THREADS) k_update(const __grid_consta
     const double* ell = tab + N1 * N1 + (s & 1) * N1;
     double* dst = P.trace_out + (static_cast<size_t>(e) * 6 + s) * N2 * 5 + f * 5;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b);
+    for (int v = 0; v < 5; ++v) dst[v] = prolong1<N1>(su + v * N3, ell, s >> 1, a, b, face_rot<N1>(s, a, b));
   }
 }
 
@@ -1398,17 +1454,38 @@ __device__ __forceinline__ void prefetch_codes(const FieldPtrs& P, int tile, int
   cp_async_commit();
 }
 
-// Prolongation of one variable from an AoS [node][5] element block.
+// Prolongation of one variable from an AoS [node][5] element block (same rotated order as prolong1).
 template <int N1>
 __device__ __forceinline__ double prolong_aos(const double* __restrict__ s, int v, const double* __restrict__ ell,
-                                              int dir, int a, int b) {
+                                              int dir, int a, int b, int rot) {
   constexpr int N2 = N1 * N1;
   const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
   const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
   double acc = 0.0;
 #pragma unroll
-  for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[(base + m * stride) * 5 + v], acc);
+  for (int m = 0; m < N1; ++m) {
+    const int mr = rot_index<N1>(m, rot);
+    acc = __fma_rn(ell[mr], s[(base + mr * stride) * 5 + v], acc);
+  }
   return acc;
+}
+
+// XOR swizzle of the node index inside the [row][node] blocks q and g of k_gradient_ws
+// (N+1 = 4 and 8, where a node row is a whole number of half-warps): lines along
+// j and k start at multiples of N+1, so unswizzled all 16 lines of a half-warp of line
+// tasks fall on 4 (N+1 = 4) or 2 (N+1 = 8) banks.  With the swizzle node rows, lines in
+// all three directions and face-node prolongations are conflict-free.
+template <int N1>
+__device__ __forceinline__ int swz(int n) {
+  if constexpr (N1 == 8) {
+    const int i = n >> 6, j = (n >> 3) & 7;
+    return n ^ ((i & 1) << 3) ^ j;
+  } else if constexpr (N1 == 4) {
+    const int i = n >> 4;
+    return n ^ (i << 2) ^ i;
+  } else {
+    return n;
+  }
 }
 
 // BR1 gradient by line tasks: task (d, c, line) loads q along the line once and
@@ -1427,18 +1504,18 @@ __device__ __forceinline__ void gradient_lines(const ElemConsts& C, const BandD&
     const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
     double x[N1];
 #pragma unroll
-    for (int m = 0; m < N1; ++m) x[m] = q[c * N3 + base + m * stride];
+    for (int m = 0; m < N1; ++m) x[m] = q[c * N3 + swz<N1>(base + m * stride)];
     const double lm = lift[(2 * d) * ls + f * lfs[2 * d] + c * lc];
     const double lp = lift[(2 * d + 1) * ls + f * lfs[2 * d + 1] + c * lc];
     const double cd = B.cdir[d];
-    double* out = g + (3 * c + d) * N3 + base;
+    double* out = g + (3 * c + d) * N3;
 #pragma unroll
     for (int o = 0; o < N1; ++o) {
       double vol = 0.0;
 #pragma unroll
       for (int m = 0; m < N1; ++m) vol += C.dhat[o * kMaxN1 + m] * x[m];
       const double surf = (lp * C.fr[o] - lm * C.fl[o]) * C.inv_w[o];
-      out[o * stride] = cd * (surf - vol);
+      out[swz<N1>(base + o * stride)] = cd * (surf - vol);
     }
   }
 }
@@ -1454,7 +1531,7 @@ __host__ __device__ constexpr int fv_comp(int dir, int q) {
 
 template <int N1, int DIR>
 __device__ __forceinline__ void fvn_item(const ElemConsts& C, const double* gS, const double* ell, int a, int b,
-                                         const double* own, double* out) {
+                                         int rot, const double* own, double* out) {
   constexpr int N2 = N1 * N1, N3 = N2 * N1;
   const int base = DIR == 0 ? a * N1 + b : (DIR == 1 ? a * N2 + b : (a * N1 + b) * N1);
   constexpr int stride = DIR == 0 ? N2 : (DIR == 1 ? N1 : 1);
@@ -1466,7 +1543,10 @@ __device__ __forceinline__ void fvn_item(const ElemConsts& C, const double* gS, 
     const int c = fv_comp(DIR, q);
     double acc = 0.0;
 #pragma unroll
-    for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], gS[c * N3 + base + m * stride], acc);
+    for (int m = 0; m < N1; ++m) {
+      const int mr = rot_index<N1>(m, rot);
+      acc = __fma_rn(ell[mr], gS[c * N3 + swz<N1>(base + mr * stride)], acc);
+    }
     gt[c] = acc;
   }
   fv_dir(own, gt, DIR, C.gas, out);
@@ -1498,18 +1578,6 @@ struct T5 {
   static constexpr int G_STAGE = EPB * (EL + 12 * TS);
   static constexpr int G_SMEM = (TAB + 2 * G_STAGE + EPB * 4 * N3 + EPB * 12 * N3 + EPB * 6 * FS) * 8 + 64;
 };
-
-template <int N1, int DIR>
-__device__ __forceinline__ double prolong_aos_d(const double* __restrict__ s, int v, const double* __restrict__ ell,
-                                                int a, int b) {
-  constexpr int N2 = N1 * N1;
-  const int base = DIR == 0 ? a * N1 + b : (DIR == 1 ? a * N2 + b : (a * N1 + b) * N1);
-  constexpr int stride = DIR == 0 ? N2 : (DIR == 1 ? N1 : 1);
-  double acc = 0.0;
-#pragma unroll
-  for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], s[(base + m * stride) * 5 + v], acc);
-  return acc;
-}
 
 template <int N1>
 __device__ __forceinline__ void issue_gradient_loads5(const FieldPtrs& P, int tile, const int* codes, double* st,
@@ -1635,7 +1703,7 @@ __global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(
       for (int v = 0; v < 5; ++v) u[v] = sU[t * 5 + v];
       prim4(u, C.gas, qq);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) q[c * N3 + t] = qq[c];
+      for (int c = 0; c < 4; ++c) q[c * N3 + swz<N1>(t)] = qq[c];
       for (int itm = t; itm < 6 * N2; itm += N3) {
         const int s = itm / N2, f = itm - s * N2;
         const int typ = myc[s] >> kCodeShift;
@@ -1676,12 +1744,12 @@ __global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(
     if (active && P.grad_out != nullptr) {
       double* go = P.grad_out + (static_cast<size_t>(e) * N3 + t) * 12;
 #pragma unroll
-      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + t];
+      for (int c = 0; c < 12; ++c) go[c] = gS[c * N3 + swz<N1>(t)];
     }
     if (active && P.visc != nullptr) {  // stress and heat flux of the node for k_update_cv (coalesced rows [c][node])
       double g[12], vs[9];
 #pragma unroll
-      for (int c = 0; c < 12; ++c) g[c] = gS[c * N3 + t];
+      for (int c = 0; c < 12; ++c) g[c] = gS[c * N3 + swz<N1>(t)];
       visc_terms(g, C.gas, vs);
       double* vo = P.visc + static_cast<size_t>(e) * 9 * N3 + t;
 #pragma unroll
@@ -1697,15 +1765,23 @@ __global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(
         if (typ == kConforming) {
           double fv[4];
           const double* own = sTr + s * D::TS + f * 5;
-          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, own, fv);
-          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, own, fv);
-          else fvn_item<N1, 2>(C, gS, ell, a, b, own, fv);
+          const int rot = (N1 == 4 || N1 == 8) ? 0 : face_rot<N1>(s, a, b);  // swizzled blocks need no rotation
+          if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, rot, own, fv);
+          else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, rot, own, fv);
+          else fvn_item<N1, 2>(C, gS, ell, a, b, rot, own, fv);
 #pragma unroll
           for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
         } else {
           double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
 #pragma unroll
-          for (int c = 0; c < 12; ++c) dst[c] = prolong1<N1>(gS + c * N3, ell, dir, a, b);
+          for (int c = 0; c < 12; ++c) {
+            const int base = dir == 0 ? a * N1 + b : (dir == 1 ? a * N2 + b : (a * N1 + b) * N1);
+            const int stride = dir == 0 ? N2 : (dir == 1 ? N1 : 1);
+            double acc = 0.0;
+#pragma unroll
+            for (int m = 0; m < N1; ++m) acc = __fma_rn(ell[m], gS[c * N3 + swz<N1>(base + m * stride)], acc);
+            dst[c] = acc;
+          }
         }
       }
     }
