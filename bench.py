@@ -47,7 +47,11 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--degree", type=int, default=5)
-    p.add_argument("--elems", type=int, default=64, help="elements per direction per GPU (weak scaling)")
+    p.add_argument("--elems", type=int, default=None,
+                   help="elements per direction per GPU (weak scaling, default 64); with --strong the whole mesh (default 128)")
+    p.add_argument("--strong", action="store_true",
+                   help="tgv / warped: configs[4] strong scaling -- --elems is the edge of the WHOLE mesh "
+                        "(128 unless given), split in y slabs over the GPUs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dry-run", action="store_true", help="stop before the first CUDA call (launcher test)")
@@ -55,10 +59,13 @@ def parse():
                    help="tgv: affine hexahedra (configs[4]); warped: the same case on curved hexahedra "
                         "(SDG_MAP_WARP, amplitude 5%% of the element size as in configs[3]); rotor: configs[3], "
                         "1.1M-element stator/rotor/stator 20-degree annulus sector (SDG_MAP_ANNULUS), strong scaling")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.elems is None:
+        a.elems = 128 if a.strong else 64
+    return a
 
 
-def tgv_mesh(T, elems_x, elems_yz, warp=None, copies=1):
+def tgv_mesh(T, elems_x, elems_yz, warp=None, copies=1, yslab=None):
     """Three blocks along x (= BASELINE z); interfaces at 2pi/3, 4pi/3.  Weak scaling over
     `copies` GPUs stacks that many periods of the (2 pi periodic) TGV along the sliding
     direction y and splits it in y slabs through all three blocks (partition 2): every GPU
@@ -68,7 +75,7 @@ def tgv_mesh(T, elems_x, elems_yz, warp=None, copies=1):
     n = [base + (rem == 2), base + (rem == 1), base + (rem == 2)]
     bands = [(n[0], 1.0, 0.0), (n[1], 1.0, 0.2), (n[2], 1.0, 0.0)]
     return T.mesh_spec(bands, ny=elems_yz * copies, nz=elems_yz, width=L, height=L * copies, depth=L, warp=warp,
-                       partition=T.PARTITION_YSLAB if copies > 1 else T.PARTITION_LEX), bands
+                       partition=T.PARTITION_YSLAB if (copies > 1 if yslab is None else yslab) else T.PARTITION_LEX), bands
 
 
 WARP = 0.05  # BASELINE configs[3]: "sinusoidal mesh warping of amplitude 5% of element size"
@@ -135,15 +142,20 @@ def workload(args, world):
     if args.mesh == "rotor":
         return rotor_workload(args, world)
     curved = args.mesh == "warped"
-    mesh, bands = tgv_mesh(T, args.elems, args.elems, warp=WARP if curved else None, copies=world)
+    strong = bool(getattr(args, "strong", False))
+    if strong:  # one mesh of elems^3, y slabs through all three blocks over the GPUs
+        mesh, bands = tgv_mesh(T, args.elems, args.elems, warp=WARP if curved else None, copies=1, yslab=world > 1)
+    else:
+        mesh, bands = tgv_mesh(T, args.elems, args.elems, warp=WARP if curved else None, copies=world)
     cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
     n1 = args.degree + 1
-    E = sum(b[0] for b in bands) * args.elems * args.elems * world
+    E = sum(b[0] for b in bands) * args.elems * args.elems * (1 if strong else world)
     geom = (f"curved hexahedra (SDG_MAP_WARP, warp {WARP} of the element size, as BASELINE configs[3]; "
             f"per-node metrics)" if curved else "affine hexahedra")
     conf = {
         "workload": f"BASELINE configs[4]: TGV M=0.1 Re=1600, 3 blocks, 2 planar sliding interfaces (middle +0.2), "
-                    f"{args.elems}^3 elements/GPU, N={args.degree} Gauss, viscous, {geom}",
+                    + (f"{args.elems}^3 elements over {world} GPU(s) (strong scaling), " if strong
+                       else f"{args.elems}^3 elements/GPU, ") + f"N={args.degree} Gauss, viscous, {geom}",
         "mesh": args.mesh,
         "geometry": "curved" if curved else "affine",
         "elements": E,
@@ -155,6 +167,7 @@ def workload(args, world):
         "l2_policy": "inputs larger than L2 (state %.0f MB, face traces %.0f MB per GPU)" % (
             E // world * n1 ** 3 * 40 / 1e6, E // world * 6 * n1 ** 2 * 72 / 1e6),
         "parallelism": (f"dp{world} (y slabs through all three blocks, NCCL halo + mortar exchange)" if world > 1 else "dp1"),
+        "scaling": "strong" if strong else "weak",
     }
     return mesh, cfg, conf, E * n1 ** 3
 
@@ -236,9 +249,11 @@ def cpu_sample(args, conf):
         desc = f"configs[3] periodic 1/8 theta slice (192x12x60 = {sconf['elements']} elements of the full mesh's geometry)"
     else:
         curved = args.mesh == "warped"
-        mesh, _ = tgv_mesh(T, args.elems, args.elems, warp=WARP if curved else None)
+        ne = min(args.elems, 64)  # the 128^3 strong-scaling mesh: a 64^3 TGV box of the same case and degree
+        mesh, _ = tgv_mesh(T, ne, ne, warp=WARP if curved else None)
         cfg = T.solver_config(args.degree, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
-        desc = f"the full printed mesh ({conf['elements_per_gpu']} elements)"
+        desc = (f"the full printed mesh ({conf['elements_per_gpu']} elements)" if ne == args.elems
+                else f"a {ne}^3-element TGV box of the printed case (the printed mesh has {conf['elements']} elements)")
     o = P.Oracle3D(mesh, cfg)
     o.set_initial_condition(0.0)
     return o, desc

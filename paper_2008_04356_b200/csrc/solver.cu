@@ -1427,13 +1427,23 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     mark(KC_PROLONG, false);
     launches_++;
   }
-  const MortarPtrs mp = mortar_ptrs();
+  // One rank: both roles' mortar blocks are this rank's, whole and at offset 0 (self_), so the
+  // four loopback copies of mortar_exchange are replaced by pointing each consumer at the
+  // producer's array (the 8^3-per-GPU end of configs[4] spent 20 % of its stage in them).
+  const bool loopback = n_ranks_ == 1;
+  MortarPtrs mp = mortar_ptrs();
+  if (loopback) {
+    mp.u_theirs = u_mine_[1].p;
+    mp.g_theirs = g_mine_[1].p;
+    mp.lift[1] = mlift_[0].p;
+    mp.flux[1] = mflux_[0].p;
+  }
   double* const u_src[2] = {u_mine_[0].p, u_mine_[1].p};
   mark(KC_MORTAR, true);
   if (!sides_.empty()) launch_mortar_fill(n_, 5, trace_[cur_trace_].p, u_src, fwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);
   launches_ += !sides_.empty();
-  mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
+  if (!loopback) mortar_exchange(u_src, u_theirs_.p, 5, true, MK_SOL_MORTAR);
   if (!nc_.empty()) {
     nc_prepare(t_stage);
     nc_fill(false);
@@ -1459,8 +1469,8 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     launch_mortar_lift(n_, consts_.gas, mp, max_mortars_[0], stream_);
     mark(KC_MORTAR, false);
     launches_ += max_mortars_[0] > 0;
-    double* const l_src[2] = {mlift_[0].p, mlift_[1].p};
-    mortar_exchange(l_src, mlift_[1].p, 4, false, MK_LIFT_MORTAR);
+    double* const l_src[2] = {mlift_[0].p, loopback ? mlift_[0].p : mlift_[1].p};
+    if (!loopback) mortar_exchange(l_src, mlift_[1].p, 4, false, MK_LIFT_MORTAR);
     mark(KC_MORTAR, true);
     if (!sides_.empty()) launch_mortar_backproject(n_, 4, l_src, slide_lift_.p, bwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
@@ -1473,14 +1483,14 @@ void GpuRankSolver::stage(double t_stage, int mode, double rk_a, double rk_b, do
     if (!sides_.empty()) launch_mortar_fill(n_, 12, slide_g_.p, g_src, fwd_ops_, mp, stream_);
     mark(KC_MORTAR, false);
     launches_ += !sides_.empty();
-    mortar_exchange(g_src, g_theirs_.p, 12, true, MK_GRAD_MORTAR);
+    if (!loopback) mortar_exchange(g_src, g_theirs_.p, 12, true, MK_GRAD_MORTAR);
   }
   mark(KC_MORTAR, true);
   launch_mortar_flux(n_, consts_.gas, lifting_ ? 1 : 0, mp, max_mortars_[0], err_.p, stream_);
   mark(KC_MORTAR, false);
   launches_ += max_mortars_[0] > 0;
-  double* const f_src[2] = {mflux_[0].p, mflux_[1].p};
-  mortar_exchange(f_src, mflux_[1].p, 5, false, MK_FLUX_MORTAR);
+  double* const f_src[2] = {mflux_[0].p, loopback ? mflux_[0].p : mflux_[1].p};
+  if (!loopback) mortar_exchange(f_src, mflux_[1].p, 5, false, MK_FLUX_MORTAR);
   mark(KC_MORTAR, true);
   if (!sides_.empty()) launch_mortar_backproject(n_, 5, f_src, slide_flux_.p, bwd_ops_, mp, stream_);
   mark(KC_MORTAR, false);

@@ -21,7 +21,7 @@ def run(*args):
     return [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
 
 
-@pytest.mark.parametrize("mesh,extra", [("tgv", ["--elems", "6"]), ("rotor", [])])
+@pytest.mark.parametrize("mesh,extra", [("tgv", ["--elems", "6"]), ("tgv", ["--strong", "--elems", "12"]), ("rotor", [])])
 def test_two_rank_launch_up_to_the_first_cuda_call(mesh, extra):
     lines = sorted(run("--gpus", "2", "--dry-run", "--mesh", mesh, *extra), key=lambda d: d["rank"])
     assert [d["rank"] for d in lines] == [0, 1] and all(d["world"] == 2 for d in lines)
@@ -31,8 +31,11 @@ def test_two_rank_launch_up_to_the_first_cuda_call(mesh, extra):
     assert sum(d["elements"] for d in lines) == conf["elements"]
     assert all(d["halo_peers"] == [1 - d["rank"]] for d in lines)
     assert all(d["interior_run"][0] == 0 and d["interior_run"][1] > d["elements"] // 2 for d in lines)
-    if mesh == "rotor":  # theta slabs: equal shares
+    if mesh == "rotor" or "--strong" in extra:  # theta / y slabs of one mesh: equal shares, strong scaling
         assert lines[0]["elements"] == lines[1]["elements"]
+        assert conf["scaling"] == "strong"
+    if "--strong" in extra:  # the whole mesh is --elems^3, not --elems^3 per GPU
+        assert conf["elements"] == 12 ** 3
 
 
 def test_world_size_must_match_gpus():
