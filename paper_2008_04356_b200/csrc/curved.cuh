@@ -192,11 +192,15 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
     const int ia = d == 0 ? i : (d == 1 ? j : k);
     const int base = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
     const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+    // Bank rotation (node_rot, 0 or 1) of the lines along i and j: nodes rv, .., N1-1, then node 0 if rv.
+    const int r = d == 2 ? 0 : rv;
+    const int b0 = base + r * stride, bl = base + (r ? 0 : (N1 - 1) * stride);
+    const double* dq = dh + ia * N1 + r;
+    const double dl = dh[ia * N1 + (r ? 0 : N1 - 1)];
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
-      const int mr = d == 2 ? m : rot_index<N1>(m, rv);  // bank rotation (node_rot)
-      const double c = dh[ia * N1 + mr];
-      const int nd = base + mr * stride;
+      const double c = m < N1 - 1 ? dq[m] : dl;
+      const int nd = m < N1 - 1 ? b0 + m * stride : bl;
       const double ja0 = sJa[(3 * d + 0) * N3 + nd], ja1 = sJa[(3 * d + 1) * N3 + nd],
                    ja2 = sJa[(3 * d + 2) * N3 + nd];
 #pragma unroll
@@ -1241,12 +1245,17 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
       const int ia = d == 0 ? i : (d == 1 ? j : k);
       const int bse = d == 0 ? j * N1 + k : (d == 1 ? i * N2 + k : (i * N1 + j) * N1);
       const int stride = d == 0 ? N2 : (d == 1 ? N1 : 1);
+      // Bank rotation (node_rot, 0 or 1) of the lines along i and j: nodes r, .., N1-1, then node 0 if r.
+      const int r = d == 2 ? 0 : nrot;
+      const int b0 = bse + r * stride, bl = bse + (r ? 0 : (N1 - 1) * stride);
+      const double* dq = dh + ia * N1 + r;
+      const double dl = dh[ia * N1 + (r ? 0 : N1 - 1)];
 #pragma unroll
       for (int m = 0; m < N1; ++m) {
-        const int mr = d == 2 ? m : rot_index<N1>(m, nrot);  // bank rotation (node_rot)
-        const double c = dh[ia * N1 + mr];
+        const double c = m < N1 - 1 ? dq[m] : dl;
+        const int nd = m < N1 - 1 ? b0 + m * stride : bl;
 #pragma unroll
-        for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + bse + mr * stride];
+        for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + nd];
       }
     }
   }
