@@ -5,7 +5,8 @@ north star's targets are quoted on -- a 20-degree rotationally periodic annulus
 sector, stator / rotor / stator, two sliding interfaces, 1.1M curved hexahedra
 (5% warp), N=5 Gauss, fp64, viscous, seeded broadband 1e-2 initial perturbation
 (SURVEY §8(d)), strong scaling over the GPUs.  --mesh tgv runs configs[4] (TGV,
-affine hexahedra, 64^3 elements per GPU, weak scaling); --mesh warped the same
+affine hexahedra, 64^3 elements per GPU, weak scaling; with --strong its 128^3
+strong-scaling mesh, split in y slabs over the GPUs); --mesh warped the same
 TGV on curved hexahedra.  configs[0]-[2] are parity cases (tests/).  One "step"
 = one 5-stage low-storage RK step (5 right-hand sides + mortars + updates).
 
