@@ -136,3 +136,25 @@ def test_baseline_config2_converges_on_device():
         errs.append(np.abs(g.field() - o.sample_case(t_end)).max())
     rate = math.log2(errs[0] / errs[1])
     assert rate > 3.0, (errs, rate)
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_bench_strong_scaling_mesh_rank_split_keeps_the_bits(ranks):
+    """`bench.py --mesh tgv --strong` (configs[4]'s strong-scaling mesh, scaled to 12^3): one mesh
+    split in y slabs through all three blocks.  2 and 4 ranks (in-process transport, one device)
+    against one rank, bitwise, at the bench degree; the one-rank run takes the loopback path
+    (mortar consumers read the producers' arrays), the others the per-partner block copies."""
+    from paper_2008_04356_b200 import capi
+    cfg = T.solver_config(5, T.NODES_GAUSS, gamma=1.4, R=1.0, mu=1.0 / 1600.0, Pr=0.72, case=T.tgv())
+    n_el = 12 ** 3
+
+    def body(s):
+        s.set_initial_condition(0.0)
+        s.step(s.suggest_dt(0.5), 2)
+        return s.local_element_ids(), s.field()
+
+    mesh, _ = bench.tgv_mesh(T, 12, 12, yslab=True)
+    ref = capi.gather_global(capi.run_inproc(mesh, cfg, 1, body, hub="strong1"), n_el, 6)
+    got = capi.gather_global(capi.run_inproc(mesh, cfg, ranks, body, hub=f"strong{ranks}"), n_el, 6)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref)
