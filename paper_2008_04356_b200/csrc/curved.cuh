@@ -199,7 +199,7 @@ __device__ __forceinline__ void node_gradient_curved(const double* tab, const do
     const double dl = dh[ia * N1 + (r ? 0 : N1 - 1)];
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
-      const double c = m < N1 - 1 ? dq[m] : dl;
+      const double c = d == 2 ? dhat_k<N1>(tab, ia, m) : (m < N1 - 1 ? dq[m] : dl);
       const int nd = m < N1 - 1 ? b0 + m * stride : bl;
       const double ja0 = sJa[(3 * d + 0) * N3 + nd], ja1 = sJa[(3 * d + 1) * N3 + nd],
                    ja2 = sJa[(3 * d + 2) * N3 + nd];
@@ -878,8 +878,9 @@ __global__ void __launch_bounds__(CG<N1, ROT>::THREADS, CG<N1, ROT>::MINB) k_gra
 #pragma unroll
         for (int c = 0; c < 12; ++c) dst[c] = gt[c];
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sOut[it * 4 + c] = fv[c];
+      double2* so = reinterpret_cast<double2*>(sOut + it * 4);
+      so[0] = make_double2(fv[0], fv[1]);
+      so[1] = make_double2(fv[2], fv[3]);
     }
     fence_proxy_async();
   }
@@ -1252,7 +1253,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
       const double dl = dh[ia * N1 + (r ? 0 : N1 - 1)];
 #pragma unroll
       for (int m = 0; m < N1; ++m) {
-        const double c = m < N1 - 1 ? dq[m] : dl;
+        const double c = d == 2 ? dhat_k<N1>(tab, ia, m) : (m < N1 - 1 ? dq[m] : dl);
         const int nd = m < N1 - 1 ? b0 + m * stride : bl;
 #pragma unroll
         for (int v = 0; v < 5; ++v) acc[v] += c * sF3[(d * 5 + v) * N3 + nd];
@@ -1270,7 +1271,7 @@ __global__ void __launch_bounds__(CV<N1, ROT, VISC, AFF>::THREADS, CV<N1, ROT, V
       const int bse = (i * N1 + j) * N1;
 #pragma unroll
       for (int m = 0; m < N1; ++m) {
-        const double c = dh[k * N1 + m];
+        const double c = dhat_k<N1>(tab, k, m);
 #pragma unroll
         for (int v = 0; v < 5; ++v) acc[v] += c * sF3[v * N3 + bse + m];
       }

@@ -30,7 +30,8 @@ struct Dim {
   // elements per CTA: keep CTAs at 200-512 threads
   static constexpr int EPB = N1 == 2 ? 32 : N1 == 3 ? 8 : N1 == 4 ? 4 : N1 <= 6 ? 2 : 1;
   static constexpr int THREADS = EPB * N3;
-  static constexpr int TAB = ((N1 * N1 + 6 * N1) + 1) & ~1;  // shared operator table (doubles)
+  // shared operator table (doubles); N1 = 8 appends D-hat transposed (load_tables, dhat_k)
+  static constexpr int TAB = ((N1 * N1 + 6 * N1 + (N1 == 8 ? N1 * N1 : 0)) + 1) & ~1;
 };
 
 __device__ __forceinline__ double sel3(int d, double a, double b, double c) { return d == 0 ? a : (d == 1 ? b : c); }
@@ -412,6 +413,18 @@ __device__ __forceinline__ void load_tables(const ElemConsts& C, double* tab) {
     tab[N1 * N1 + 3 * N1 + q] = C.liftw[1][q];
     tab[N1 * N1 + 4 * N1 + q] = C.inv_w[q];
   }
+  if constexpr (N1 == 8) {  // D-hat transposed for the lines along k (dhat_k)
+    for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) tab[N1 * N1 + 6 * N1 + q] = C.dhat[(q % N1) * kMaxN1 + q / N1];
+  }
+}
+
+// D-hat(k, m) for a node thread's line along k.  Rows of 8 doubles put the 8 values of k in a
+// half-warp on 2 banks (8 k + m mod 16), a 4-way conflict; N1 = 8 reads the transposed copy
+// (m * 8 + k: consecutive).  Rows of 4 and 6 doubles spread over distinct banks.
+template <int N1>
+__device__ __forceinline__ double dhat_k(const double* tab, int k, int m) {
+  if constexpr (N1 == 8) return tab[N1 * N1 + 6 * N1 + m * N1 + k];
+  else return tab[k * N1 + m];
 }
 
 
@@ -1769,8 +1782,9 @@ __global__ void __launch_bounds__(GWs<N1>::THREADS, T5<N1>::MINB) k_gradient_ws(
           if (dir == 0) fvn_item<N1, 0>(C, gS, ell, a, b, rot, own, fv);
           else if (dir == 1) fvn_item<N1, 1>(C, gS, ell, a, b, rot, own, fv);
           else fvn_item<N1, 2>(C, gS, ell, a, b, rot, own, fv);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) fvo[s * D::FS + f * 4 + c] = fv[c];
+          double2* fq = reinterpret_cast<double2*>(fvo + s * D::FS + f * 4);  // [f][4]: 128-bit stores, no 4-way conflict
+          fq[0] = make_double2(fv[0], fv[1]);
+          fq[1] = make_double2(fv[2], fv[3]);
         } else {
           double* dst = (typ == kSliding ? P.slide_g : P.dir_g) + (static_cast<size_t>(idx) * N2 + f) * 12;
 #pragma unroll
